@@ -11,7 +11,10 @@ class Tokenizer:
     def __init__(self, vocab, n_special=3):
         self.vocab = list(vocab)
         self.n_special = n_special
-        self.lookup = {s: i for i, s in enumerate(self.vocab) if i >= n_special}
+        self.lookup = {}
+        for i, s in enumerate(self.vocab):
+            if i >= n_special and s not in self.lookup:   # first id wins
+                self.lookup[s] = i
         self.max_len = max(len(s) for s in self.vocab[n_special:])
 
     def encode(self, data: bytes):

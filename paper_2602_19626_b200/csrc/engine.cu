@@ -1,0 +1,609 @@
+// Engine: model upload, the slabbed prefill + walk driver (compress), the
+// one-row-per-chunk decode-step driver (decompress), host WNC + NC05 assembly.
+#include <algorithm>
+#include <cmath>
+#include <thread>
+
+#include "engine.hpp"
+
+namespace nc {
+
+void check_cuda(cudaError_t e, const char *what) {
+  if (e != cudaSuccess) fail(NC_ERR_BACKEND, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ------------------------------------------------------------- allocator ---
+static void *(*g_alloc)(size_t, void *) = nullptr;
+static void (*g_free)(void *, void *) = nullptr;
+static void *g_ctx = nullptr;
+void set_allocator(void *(*a)(size_t, void *), void (*f)(void *, void *), void *ctx) {
+  g_alloc = a; g_free = f; g_ctx = ctx;
+}
+void *dev_alloc(size_t bytes, cudaStream_t s) {
+  if (bytes == 0) bytes = 16;
+  void *p = nullptr;
+  if (g_alloc) {
+    p = g_alloc(bytes, g_ctx);
+    if (!p) fail(NC_ERR_NOMEM, "device allocation failed (hook)");
+  } else {
+    cudaError_t e = cudaMallocAsync(&p, bytes, s);
+    if (e != cudaSuccess) fail(NC_ERR_NOMEM, std::string("cudaMallocAsync: ") + cudaGetErrorString(e));
+  }
+  return p;
+}
+void dev_free(void *p, cudaStream_t s) {
+  if (!p) return;
+  if (g_free) g_free(p, g_ctx);
+  else cudaFreeAsync(p, s);
+}
+
+Stats &stats() {
+  static thread_local Stats st;
+  return st;
+}
+
+// RAII bag of device buffers for one call
+struct Bag {
+  cudaStream_t s;
+  std::vector<void *> ptrs;
+  explicit Bag(cudaStream_t st) : s(st) {}
+  template <class T>
+  T *get(size_t n) {
+    T *p = static_cast<T *>(dev_alloc(n * sizeof(T), s));
+    ptrs.push_back(p);
+    return p;
+  }
+  template <class T>
+  T *upload(const std::vector<T> &v) {
+    T *p = get<T>(v.size());
+    if (!v.empty()) NC_CUDA(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+    return p;
+  }
+  ~Bag() {
+    cudaStreamSynchronize(s);
+    for (void *p : ptrs) dev_free(p, s);
+    cudaStreamSynchronize(s);
+  }
+};
+
+// ------------------------------------------------------------------ model ---
+void model_load(nc_model *m, const std::string &path, int device) {
+  NcwFile f = read_ncw(path);
+  const Shape &s = f.s;
+  if (s.dh != (uint32_t)kHeadDim) fail(NC_ERR_INVALID, "kernels are specialised to head_dim 64");
+  if (s.H % s.KV || s.H / s.KV > 3) fail(NC_ERR_INVALID, "GQA group must be <= 3");
+  if (s.d % 128 || s.d_ff % 64) fail(NC_ERR_INVALID, "d_model must be a multiple of 128, d_ff of 64");
+  if (s.V % 128) fail(NC_ERR_INVALID, "vocab must be a multiple of 128");
+  NC_CUDA(cudaSetDevice(device));
+  m->device = device;
+  m->s = s;
+  m->vocab = f.vocab;
+  m->tok.build(f.vocab, s.n_special);
+  const size_t d = s.d, V = s.V, qd = (size_t)s.H * s.dh, kvd = (size_t)s.KV * s.dh, ff = s.d_ff;
+  auto up = [&](const std::vector<float> &h) {
+    void *p = nullptr;
+    NC_CUDA(cudaMalloc(&p, h.size() * sizeof(float)));
+    NC_CUDA(cudaMemcpy(p, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice));
+    m->owned.push_back(p);
+    return static_cast<float *>(p);
+  };
+  size_t off = 0;
+  const float *E = f.tensor(0);
+  off += V * d;
+  std::vector<float> buf(E, E + V * d);
+  m->E = up(buf);
+  for (uint32_t l = 0; l < s.n_layers; ++l) {
+    const float *g1 = f.tensor(off); off += d;
+    const float *wq = f.tensor(off); off += qd * d;
+    const float *wk = f.tensor(off); off += kvd * d;
+    const float *wv = f.tensor(off); off += kvd * d;
+    const float *wo = f.tensor(off); off += d * qd;
+    const float *g2 = f.tensor(off); off += d;
+    const float *wg = f.tensor(off); off += ff * d;
+    const float *wu = f.tensor(off); off += ff * d;
+    const float *wd = f.tensor(off); off += d * ff;
+    // [Wq; Wk; Wv] with the attention RMSNorm gain folded into the columns
+    buf.assign((qd + 2 * kvd) * d, 0.f);
+    for (size_t r = 0; r < qd + 2 * kvd; ++r) {
+      const float *src = r < qd ? wq + r * d : (r < qd + kvd ? wk + (r - qd) * d : wv + (r - qd - kvd) * d);
+      for (size_t k = 0; k < d; ++k) buf[r * d + k] = src[k] * g1[k];
+    }
+    m->wqkv.push_back(up(buf));
+    buf.assign(wo, wo + d * qd);
+    m->wo.push_back(up(buf));
+    // gate/up interleaved in groups of 32 rows, MLP RMSNorm gain folded in
+    buf.assign(2 * ff * d, 0.f);
+    for (size_t gi = 0; gi < ff / 32; ++gi)
+      for (size_t j = 0; j < 32; ++j)
+        for (size_t k = 0; k < d; ++k) {
+          buf[(64 * gi + j) * d + k] = wg[(32 * gi + j) * d + k] * g2[k];
+          buf[(64 * gi + 32 + j) * d + k] = wu[(32 * gi + j) * d + k] * g2[k];
+        }
+    m->wgu.push_back(up(buf));
+    buf.assign(wd, wd + d * ff);
+    m->wd.push_back(up(buf));
+  }
+  const float *gf = f.tensor(off);
+  buf.assign(V * d, 0.f);
+  for (size_t v = 0; v < V; ++v)
+    for (size_t k = 0; k < d; ++k) buf[v * d + k] = E[v * d + k] * gf[k];
+  m->E_head = up(buf);
+  ensure_rope(m, 4096);
+}
+
+void model_free(nc_model *m) {
+  cudaSetDevice(m->device);
+  for (void *p : m->owned) cudaFree(p);
+  if (m->rope_cos) cudaFree(m->rope_cos);
+  if (m->rope_sin) cudaFree(m->rope_sin);
+  m->owned.clear();
+}
+
+// cos/sin of pos * theta^(-2i/64) computed in fp64, stored fp32 (D12)
+void ensure_rope(nc_model *m, int max_pos) {
+  if (max_pos <= m->rope_len) return;
+  int len = ((max_pos + 4095) / 4096) * 4096;
+  std::vector<float> c((size_t)len * 32), sn((size_t)len * 32);
+  for (int p = 0; p < len; ++p)
+    for (int i = 0; i < 32; ++i) {
+      double inv = std::pow(m->s.rope_theta, -(2.0 * i) / 64.0);
+      double ang = (double)p * inv;
+      c[(size_t)p * 32 + i] = (float)std::cos(ang);
+      sn[(size_t)p * 32 + i] = (float)std::sin(ang);
+    }
+  NC_CUDA(cudaDeviceSynchronize());
+  if (m->rope_cos) cudaFree(m->rope_cos);
+  if (m->rope_sin) cudaFree(m->rope_sin);
+  NC_CUDA(cudaMalloc(&m->rope_cos, c.size() * 4));
+  NC_CUDA(cudaMalloc(&m->rope_sin, sn.size() * 4));
+  NC_CUDA(cudaMemcpy(m->rope_cos, c.data(), c.size() * 4, cudaMemcpyHostToDevice));
+  NC_CUDA(cudaMemcpy(m->rope_sin, sn.data(), sn.size() * 4, cudaMemcpyHostToDevice));
+  m->rope_len = len;
+}
+
+// ---------------------------------------------------------------- forward ---
+struct Forward {
+  nc_model *m;
+  cudaStream_t s;
+  int Mmax = 0;
+  float *h, *rinv, *q, *o, *act, *logits;
+  KvRing ring{};
+  void alloc(Bag &bag, int Mmax_, int n_chunks, int ring_len) {
+    Mmax = Mmax_;
+    const Shape &S = m->s;
+    h = bag.get<float>((size_t)Mmax * S.d);
+    rinv = bag.get<float>((size_t)Mmax);
+    q = bag.get<float>((size_t)Mmax * S.H * S.dh);
+    o = bag.get<float>((size_t)Mmax * S.H * S.dh);
+    act = bag.get<float>((size_t)Mmax * S.d_ff);
+    logits = bag.get<float>((size_t)Mmax * S.V);
+    ring.n_layers = S.n_layers;
+    ring.ring = ring_len;
+    ring.kv = S.KV;
+    size_t rn = (size_t)n_chunks * S.n_layers * ring_len * S.KV * S.dh;
+    ring.k = bag.get<float>(rn);
+    ring.v = bag.get<float>(rn);
+  }
+  // embed -> n_layers x {QKV, attention, O, gate-up, down} -> head into `logits`
+  void run(int M, const RowMeta &rows, const AttnTile *tiles, int n_tiles, const Params &p, cudaEvent_t ev_head) {
+    const Shape &S = m->s;
+    Stats &st = stats();
+    const int qd = S.H * S.dh, kvd = S.KV * S.dh;
+    launch_embed(rows.x, M, m->E, S.d, h, s);
+    st.launches++;
+    for (uint32_t l = 0; l < S.n_layers; ++l) {
+      launch_rms(h, M, S.d, (float)S.eps, rinv, s);
+      GemmArgs g{};
+      g.A = h; g.lda = S.d; g.B = m->wqkv[l]; g.ldb = S.d; g.M = M; g.N = qd + 2 * kvd; g.K = S.d;
+      g.rinv = rinv; g.C = q; g.ldc = qd; g.layer = (int)l; g.n_q_cols = qd; g.n_kv_cols = kvd;
+      g.rows = rows; g.ring = ring; g.rope_cos = m->rope_cos; g.rope_sin = m->rope_sin;
+      launch_gemm(EPI_QKV, g, s);
+      AttnArgs at{};
+      at.tiles = tiles; at.n_tiles = n_tiles; at.q = q; at.o = o; at.ldq = qd; at.ring = ring; at.layer = (int)l;
+      at.H = S.H; at.KV = S.KV; at.window = (int)p.window; at.slide = (int)p.slide;
+      launch_attention(at, s);
+      GemmArgs go{};
+      go.A = o; go.lda = qd; go.B = m->wo[l]; go.ldb = qd; go.M = M; go.N = S.d; go.K = qd; go.C = h; go.ldc = S.d;
+      launch_gemm(EPI_RESID, go, s);
+      launch_rms(h, M, S.d, (float)S.eps, rinv, s);
+      GemmArgs gu{};
+      gu.A = h; gu.lda = S.d; gu.B = m->wgu[l]; gu.ldb = S.d; gu.M = M; gu.N = 2 * S.d_ff; gu.K = S.d;
+      gu.rinv = rinv; gu.C = act; gu.ldc = S.d_ff;
+      launch_gemm(EPI_SWIGLU, gu, s);
+      GemmArgs gd{};
+      gd.A = act; gd.lda = S.d_ff; gd.B = m->wd[l]; gd.ldb = S.d_ff; gd.M = M; gd.N = S.d; gd.K = S.d_ff;
+      gd.C = h; gd.ldc = S.d;
+      launch_gemm(EPI_RESID, gd, s);
+      st.launches += 6;
+    }
+    if (ev_head) NC_CUDA(cudaEventRecord(ev_head, s));
+    launch_rms(h, M, S.d, (float)S.eps, rinv, s);
+    GemmArgs gh{};
+    gh.A = h; gh.lda = S.d; gh.B = m->E_head; gh.ldb = S.d; gh.M = M; gh.N = S.V; gh.K = S.d;
+    gh.rinv = rinv; gh.C = logits; gh.ldc = S.V;
+    launch_gemm(EPI_HEAD, gh, s);
+    st.launches += 2;
+    NC_CUDA(cudaGetLastError());
+  }
+};
+
+__global__ void slab_rows_kernel(const uint32_t *tokens, const int64_t *tok_off, const uint32_t *ntok, int R, int s,
+                                 int M, uint32_t bos, uint32_t *x, int32_t *chunk, int32_t *pos) {
+  int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= M) return;
+  int c = m / R, r = m % R, p = s * R + r;
+  bool valid = p < (int)ntok[c];
+  x[m] = (!valid || p == 0) ? bos : tokens[tok_off[c] + p - 1];
+  chunk[m] = c;
+  pos[m] = valid ? p : -1;
+}
+
+__global__ void step_rows_kernel(const uint32_t *ntok, int n_chunks, int j, int32_t *chunk, int32_t *pos,
+                                 AttnTile *tiles, int32_t *chunk_of, int32_t *row0, int32_t *count) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n_chunks) return;
+  bool act = j < (int)ntok[c];
+  chunk[c] = c;
+  pos[c] = act ? j : -1;
+  tiles[c] = AttnTile{c, j, act ? 1 : 0, c};
+  chunk_of[c] = c;
+  row0[c] = c;
+  count[c] = act ? 1 : 0;
+}
+
+static uint32_t pow2_at_least(uint64_t x) {
+  uint32_t p = 32;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+struct WalkBufs {
+  WalkState *st;
+  double *b;
+  uint32_t *cu;
+  float *spadd;
+  unsigned long long *keys;
+  uint32_t *vals;
+  NgRecord *recs;
+  uint32_t hcap, rcap;
+  void alloc(Bag &bag, int n_chunks, uint32_t V, uint32_t max_n, const Params &p, cudaStream_t s) {
+    rcap = std::max<uint32_t>(1, std::min<uint32_t>(p.cap, max_n));
+    hcap = pow2_at_least(2ull * rcap);
+    st = bag.get<WalkState>(n_chunks);
+    b = bag.get<double>((size_t)n_chunks * V);
+    cu = bag.get<uint32_t>((size_t)n_chunks * V);
+    spadd = bag.get<float>((size_t)n_chunks * V);
+    keys = bag.get<unsigned long long>((size_t)n_chunks * kMaxOrders * hcap);
+    vals = bag.get<uint32_t>((size_t)n_chunks * kMaxOrders * hcap);
+    recs = bag.get<NgRecord>((size_t)n_chunks * kMaxOrders * rcap);
+    NC_CUDA(cudaMemsetAsync(b, 0, (size_t)n_chunks * V * sizeof(double), s));
+    NC_CUDA(cudaMemsetAsync(cu, 0, (size_t)n_chunks * V * sizeof(uint32_t), s));
+    NC_CUDA(cudaMemsetAsync(spadd, 0, (size_t)n_chunks * V * sizeof(float), s));
+    NC_CUDA(cudaMemsetAsync(keys, 0, (size_t)n_chunks * kMaxOrders * hcap * 8, s));
+    launch_walk_init(st, n_chunks, s);
+  }
+  void fill(WalkArgs &a, const Params &p, uint32_t V) const {
+    a.st = st; a.b = b; a.cu = cu; a.spadd = spadd; a.ng_keys = keys; a.ng_vals = vals; a.ng_recs = recs;
+    a.hcap = hcap; a.rcap = rcap;
+    a.V = V; a.cdf_bits = p.cdf_bits; a.warmup = p.warmup; a.flags = p.flags; a.orders = p.orders; a.cap = p.cap;
+    a.inv_tau = (float)p.inv_tau; a.alpha = p.alpha; a.eta = p.eta;
+  }
+};
+
+// --------------------------------------------------------------- compress ---
+void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<uint32_t> &ntok,
+                     const Params &p, cudaStream_t s, CompressOut &out) {
+  NC_CUDA(cudaSetDevice(m->device));
+  const Shape &S = m->s;
+  const int n_chunks = (int)ntok.size();
+  uint32_t max_n = 0;
+  uint64_t total = 0;
+  std::vector<int64_t> tok_off(n_chunks);
+  for (int c = 0; c < n_chunks; ++c) {
+    tok_off[c] = (int64_t)total;
+    total += ntok[c];
+    max_n = std::max(max_n, ntok[c]);
+  }
+  out.cum.assign(total, 0);
+  out.freq.assign(total, 0);
+  out.err.assign(n_chunks, 0);
+  if (p.debug_dump) out.p_true.assign(total, 0.f);
+  Stats &st = stats();
+  if (n_chunks == 0 || max_n == 0) return;
+  if (S.V >= (1u << p.cdf_bits)) fail(NC_ERR_INVALID, "T = 2^cdf_bits must exceed V");
+
+  int per_chunk = std::max(128, (int)(p.max_slab_rows / n_chunks) / 128 * 128);
+  const int R = std::min<int>(((max_n + 127) / 128) * 128, per_chunk);
+  const int n_slabs = (int)((max_n + R - 1) / R);
+  const int ring_len = (int)p.window + R;
+  const int M = n_chunks * R;
+  ensure_rope(m, (int)max_n + 1);
+
+  Bag bag(s);
+  Forward fw{m, s};
+  fw.alloc(bag, M, n_chunks, ring_len);
+  std::vector<uint32_t> ntok_v(ntok);
+  uint32_t *ntok_d = bag.upload(ntok_v);
+  int64_t *tok_off_d = bag.upload(tok_off);
+  uint32_t *xs = bag.get<uint32_t>(M);
+  int32_t *rchunk = bag.get<int32_t>(M), *rpos = bag.get<int32_t>(M);
+  // attention tiles and walk entries for every slab
+  std::vector<AttnTile> tiles;
+  std::vector<int> tile_off(n_slabs + 1, 0);
+  std::vector<int32_t> w_chunk, w_row0, w_count;
+  std::vector<int> w_off(n_slabs + 1, 0);
+  for (int sl = 0; sl < n_slabs; ++sl) {
+    tile_off[sl] = (int)tiles.size();
+    w_off[sl] = (int)w_chunk.size();
+    for (int c = 0; c < n_chunks; ++c) {
+      for (int b0 = 0; b0 < R; b0 += 64) {
+        int p0 = sl * R + b0;
+        int nr = std::min<int>(64, (int)ntok[c] - p0);
+        if (nr > 0) tiles.push_back(AttnTile{c, p0, nr, c * R + b0});
+      }
+      int cnt = std::min<int>(R, (int)ntok[c] - sl * R);
+      if (cnt > 0) { w_chunk.push_back(c); w_row0.push_back(c * R); w_count.push_back(cnt); }
+    }
+  }
+  tile_off[n_slabs] = (int)tiles.size();
+  w_off[n_slabs] = (int)w_chunk.size();
+  AttnTile *tiles_d = bag.upload(tiles);
+  int32_t *wc_d = bag.upload(w_chunk), *wr_d = bag.upload(w_row0), *wn_d = bag.upload(w_count);
+  WalkBufs wb;
+  wb.alloc(bag, n_chunks, S.V, max_n, p, s);
+  uint32_t *cum_d = bag.get<uint32_t>(total), *freq_d = bag.get<uint32_t>(total);
+  float *p_d = p.debug_dump ? bag.get<float>(total) : nullptr;
+
+  std::vector<cudaEvent_t> ev(3 * n_slabs + 1);
+  for (auto &e : ev) NC_CUDA(cudaEventCreate(&e));
+  for (int sl = 0; sl < n_slabs; ++sl) {
+    NC_CUDA(cudaEventRecord(ev[3 * sl], s));
+    slab_rows_kernel<<<(M + 255) / 256, 256, 0, s>>>(tokens_dev, tok_off_d, ntok_d, R, sl, M, S.bos, xs, rchunk, rpos);
+    st.launches++;
+    RowMeta rows{xs, rchunk, rpos};
+    fw.run(M, rows, tiles_d + tile_off[sl], tile_off[sl + 1] - tile_off[sl], p, ev[3 * sl + 1]);
+    NC_CUDA(cudaEventRecord(ev[3 * sl + 2], s));
+    WalkArgs wa{};
+    wa.chunk_of = wc_d + w_off[sl]; wa.row0 = wr_d + w_off[sl]; wa.count = wn_d + w_off[sl];
+    wa.n_entries = w_off[sl + 1] - w_off[sl];
+    wa.logits = fw.logits; wa.ldl = S.V;
+    wa.tokens = tokens_dev; wa.tok_off = tok_off_d;
+    wa.out_cum = cum_d; wa.out_freq = freq_d; wa.out_p = p_d;
+    wa.mode = 0;
+    wb.fill(wa, p, S.V);
+    launch_walk(wa, s);
+    st.launches++;
+    NC_CUDA(cudaGetLastError());
+  }
+  NC_CUDA(cudaEventRecord(ev[3 * n_slabs], s));
+  NC_CUDA(cudaMemcpyAsync(out.cum.data(), cum_d, total * 4, cudaMemcpyDeviceToHost, s));
+  NC_CUDA(cudaMemcpyAsync(out.freq.data(), freq_d, total * 4, cudaMemcpyDeviceToHost, s));
+  if (p_d) NC_CUDA(cudaMemcpyAsync(out.p_true.data(), p_d, total * 4, cudaMemcpyDeviceToHost, s));
+  std::vector<WalkState> hs(n_chunks);
+  NC_CUDA(cudaMemcpyAsync(hs.data(), wb.st, n_chunks * sizeof(WalkState), cudaMemcpyDeviceToHost, s));
+  NC_CUDA(cudaStreamSynchronize(s));
+  for (int c = 0; c < n_chunks; ++c) out.err[c] = hs[c].err;
+  for (int sl = 0; sl < n_slabs; ++sl) {
+    float a, b, c;
+    cudaEventElapsedTime(&a, ev[3 * sl], ev[3 * sl + 1]);
+    cudaEventElapsedTime(&b, ev[3 * sl + 1], ev[3 * sl + 2]);
+    cudaEventElapsedTime(&c, ev[3 * sl + 2], ev[3 * sl + 3]);
+    st.forward_ms += a + b;
+    st.head_ms += b;
+    st.walk_ms += c;
+  }
+  for (auto &e : ev) cudaEventDestroy(e);
+}
+
+// --------------------------------------------------------------- container ---
+void encode_container(const Params &p, const std::vector<uint32_t> &ntok, const CompressOut &co,
+                      std::vector<uint8_t> &out) {
+  const size_t n = ntok.size();
+  std::vector<Nc05Chunk> chunks(n);
+  std::vector<size_t> off(n + 1, 0);
+  for (size_t c = 0; c < n; ++c) off[c + 1] = off[c] + ntok[c];
+  for (size_t c = 0; c < n; ++c)
+    if (co.err[c]) fail(NC_ERR_INTEGRITY, "quantizer residual would drop a count below 1 (D6)");
+  auto work = [&](size_t c) {
+    WncEncoder enc;
+    for (size_t i = off[c]; i < off[c + 1]; ++i) enc.encode(co.cum[i], co.freq[i], p.cdf_bits);
+    uint64_t bits;
+    enc.finish(chunks[c].stream, bits);
+    if (bits > 0xFFFFFFFFull) fail(NC_ERR_INVALID, "chunk bitstream exceeds the u32 bit_count field");
+    chunks[c].bits = (uint32_t)bits;
+    chunks[c].tokens = ntok[c];
+  };
+  unsigned nt = std::max(1u, std::min<unsigned>((unsigned)n, std::thread::hardware_concurrency()));
+  if (nt <= 1 || n <= 1) {
+    for (size_t c = 0; c < n; ++c) work(c);
+  } else {
+    std::vector<std::thread> th;
+    std::vector<std::string> errs(nt);
+    for (unsigned t = 0; t < nt; ++t)
+      th.emplace_back([&, t] {
+        try {
+          for (size_t c = t; c < n; c += nt) work(c);
+        } catch (std::exception &e) { errs[t] = e.what(); }
+      });
+    for (auto &x : th) x.join();
+    for (auto &e : errs)
+      if (!e.empty()) fail(NC_ERR_INTEGRITY, e);
+  }
+  write_nc05((uint8_t)p.flags, (uint16_t)p.tau_milli, chunks, out);
+}
+
+// ------------------------------------------------------------- decompress ---
+void decompress_device(nc_model *m, const uint8_t *blob, const Nc05View &view, const Params &p,
+                       cudaStream_t s, std::vector<std::vector<uint32_t>> &toks) {
+  NC_CUDA(cudaSetDevice(m->device));
+  const Shape &S = m->s;
+  const int n_chunks = (int)view.ents.size();
+  toks.assign(n_chunks, {});
+  uint32_t max_n = 0;
+  uint64_t total = 0;
+  std::vector<int64_t> tok_off(n_chunks), s_off(n_chunks);
+  std::vector<uint64_t> s_bits(n_chunks);
+  std::vector<uint32_t> ntok(n_chunks);
+  uint64_t blob_len = 0;
+  for (int c = 0; c < n_chunks; ++c) {
+    ntok[c] = view.ents[c].tokens;
+    tok_off[c] = (int64_t)total;
+    total += ntok[c];
+    max_n = std::max(max_n, ntok[c]);
+    s_off[c] = (int64_t)view.ents[c].off;
+    s_bits[c] = view.ents[c].bits;
+    blob_len = std::max<uint64_t>(blob_len, view.ents[c].off + view.ents[c].len);
+  }
+  if (n_chunks == 0 || max_n == 0) return;
+  if (S.V >= (1u << p.cdf_bits)) fail(NC_ERR_INVALID, "T = 2^cdf_bits must exceed V");
+  Stats &st = stats();
+  ensure_rope(m, (int)max_n + 1);
+  Bag bag(s);
+  Forward fw{m, s};
+  const int ring_len = (int)p.window + 64;
+  fw.alloc(bag, n_chunks, n_chunks, ring_len);
+  std::vector<uint8_t> bl(blob, blob + blob_len);
+  uint8_t *blob_d = bag.upload(bl);
+  int64_t *s_off_d = bag.upload(s_off), *tok_off_d = bag.upload(tok_off);
+  uint64_t *s_bits_d = bag.upload(s_bits);
+  uint32_t *ntok_d = bag.upload(ntok);
+  std::vector<uint32_t> bos(n_chunks, S.bos);
+  uint32_t *x_cur = bag.upload(bos);
+  int32_t *rchunk = bag.get<int32_t>(n_chunks), *rpos = bag.get<int32_t>(n_chunks);
+  AttnTile *tiles = bag.get<AttnTile>(n_chunks);
+  int32_t *wc = bag.get<int32_t>(n_chunks), *wr = bag.get<int32_t>(n_chunks), *wn = bag.get<int32_t>(n_chunks);
+  WalkBufs wb;
+  wb.alloc(bag, n_chunks, S.V, max_n, p, s);
+  uint32_t *out_tok = bag.get<uint32_t>(total);
+  WalkArgs wa{};
+  wa.chunk_of = wc; wa.row0 = wr; wa.count = wn; wa.n_entries = n_chunks;
+  wa.logits = fw.logits; wa.ldl = S.V;
+  wa.tok_off = tok_off_d; wa.streams = blob_d; wa.stream_off = s_off_d; wa.stream_bits = s_bits_d;
+  wa.out_tok = out_tok; wa.next_x = x_cur; wa.mode = 1;
+  wb.fill(wa, p, S.V);
+  cudaEvent_t e0, e1;
+  NC_CUDA(cudaEventCreate(&e0));
+  NC_CUDA(cudaEventCreate(&e1));
+  NC_CUDA(cudaEventRecord(e0, s));
+  for (uint32_t j = 0; j < max_n; ++j) {
+    step_rows_kernel<<<(n_chunks + 127) / 128, 128, 0, s>>>(ntok_d, n_chunks, (int)j, rchunk, rpos, tiles, wc, wr, wn);
+    RowMeta rows{x_cur, rchunk, rpos};
+    fw.run(n_chunks, rows, tiles, n_chunks, p, nullptr);
+    launch_walk(wa, s);
+    st.launches += 2;
+    if ((j & 255) == 255) NC_CUDA(cudaGetLastError());
+  }
+  NC_CUDA(cudaEventRecord(e1, s));
+  std::vector<uint32_t> all(total);
+  NC_CUDA(cudaMemcpyAsync(all.data(), out_tok, total * 4, cudaMemcpyDeviceToHost, s));
+  std::vector<WalkState> hs(n_chunks);
+  NC_CUDA(cudaMemcpyAsync(hs.data(), wb.st, n_chunks * sizeof(WalkState), cudaMemcpyDeviceToHost, s));
+  NC_CUDA(cudaStreamSynchronize(s));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  st.forward_ms += ms;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  for (int c = 0; c < n_chunks; ++c) {
+    if (hs[c].err) fail(NC_ERR_INTEGRITY, "decoder integrity failure in chunk " + std::to_string(c));
+    // every renormalisation shift of the decoder matches one encoder step;
+    // bit_count = steps + 2 (finish emits 1 + (pending+1) bits)  (D8)
+    if (ntok[c] && hs[c].bitpos - 32 + 2 != s_bits[c])
+      fail(NC_ERR_INTEGRITY, "bit_count mismatch in chunk " + std::to_string(c) + " (wrong params or corrupt stream)");
+    toks[c].assign(all.begin() + tok_off[c], all.begin() + tok_off[c] + ntok[c]);
+  }
+}
+
+// ------------------------------------------------------------------ debug ---
+void debug_forward(nc_model *m, const uint32_t *x, uint32_t rows, const Params &p, int mode, float *out) {
+  NC_CUDA(cudaSetDevice(m->device));
+  const Shape &S = m->s;
+  cudaStream_t s = nullptr;
+  if (rows == 0) return;
+  ensure_rope(m, (int)rows + 1);
+  Bag bag(s);
+  std::vector<uint32_t> xv(x, x + rows);
+  uint32_t *x_d = bag.upload(xv);
+  Forward fw{m, s};
+  if (mode == 0) {
+    const int R = std::max(128, (int)p.max_slab_rows / 128 * 128);
+    const int Rr = std::min<int>(((rows + 127) / 128) * 128, R);
+    const int n_slabs = (int)((rows + Rr - 1) / Rr);
+    fw.alloc(bag, Rr, 1, (int)p.window + Rr);
+    // the slab kernel maps x through "tokens[p-1]"; feed x shifted so that x_j = x[j]
+    std::vector<uint32_t> shifted(rows);
+    for (uint32_t j = 0; j + 1 < rows; ++j) shifted[j] = x[j + 1];
+    uint32_t *t_d = bag.upload(shifted);
+    std::vector<int64_t> off{0};
+    int64_t *off_d = bag.upload(off);
+    std::vector<uint32_t> nt{rows};
+    uint32_t *nt_d = bag.upload(nt);
+    uint32_t *xs = bag.get<uint32_t>(Rr);
+    int32_t *rc = bag.get<int32_t>(Rr), *rp = bag.get<int32_t>(Rr);
+    for (int sl = 0; sl < n_slabs; ++sl) {
+      std::vector<AttnTile> tiles;
+      for (int b0 = 0; b0 < Rr; b0 += 64) {
+        int p0 = sl * Rr + b0;
+        int nr = std::min<int>(64, (int)rows - p0);
+        if (nr > 0) tiles.push_back(AttnTile{0, p0, nr, b0});
+      }
+      AttnTile *td = bag.upload(tiles);
+      slab_rows_kernel<<<(Rr + 255) / 256, 256, 0, s>>>(t_d, off_d, nt_d, Rr, sl, Rr, x[0], xs, rc, rp);
+      RowMeta rm{xs, rc, rp};
+      fw.run(Rr, rm, td, (int)tiles.size(), p, nullptr);
+      int cnt = std::min<int>(Rr, (int)rows - sl * Rr);
+      NC_CUDA(cudaMemcpyAsync(out + (size_t)sl * Rr * S.V, fw.logits, (size_t)cnt * S.V * 4, cudaMemcpyDeviceToHost, s));
+    }
+  } else {
+    fw.alloc(bag, 1, 1, (int)p.window + 64);
+    int32_t *rc = bag.get<int32_t>(1), *rp = bag.get<int32_t>(1);
+    AttnTile *tiles = bag.get<AttnTile>(1);
+    int32_t *wc = bag.get<int32_t>(1), *wr = bag.get<int32_t>(1), *wn = bag.get<int32_t>(1);
+    std::vector<uint32_t> nt{rows};
+    uint32_t *nt_d = bag.upload(nt);
+    for (uint32_t j = 0; j < rows; ++j) {
+      step_rows_kernel<<<1, 32, 0, s>>>(nt_d, 1, (int)j, rc, rp, tiles, wc, wr, wn);
+      RowMeta rm{x_d + j, rc, rp};
+      fw.run(1, rm, tiles, 1, p, nullptr);
+      NC_CUDA(cudaMemcpyAsync(out + (size_t)j * S.V, fw.logits, (size_t)S.V * 4, cudaMemcpyDeviceToHost, s));
+    }
+  }
+  NC_CUDA(cudaStreamSynchronize(s));
+}
+
+void debug_walk(int device, const float *logits, const uint32_t *tok, uint32_t n, uint32_t V, const Params &p,
+                uint32_t *cum, uint32_t *freq, float *p_true) {
+  NC_CUDA(cudaSetDevice(device));
+  if (n == 0) return;
+  if (V >= (1u << p.cdf_bits)) fail(NC_ERR_INVALID, "T = 2^cdf_bits must exceed V");
+  cudaStream_t s = nullptr;
+  Bag bag(s);
+  std::vector<float> lg(logits, logits + (size_t)n * V);
+  float *lg_d = bag.upload(lg);
+  std::vector<uint32_t> tk(tok, tok + n);
+  uint32_t *tk_d = bag.upload(tk);
+  std::vector<int64_t> off{0};
+  int64_t *off_d = bag.upload(off);
+  std::vector<int32_t> zero{0}, cnt{(int32_t)n};
+  int32_t *c_d = bag.upload(zero), *r_d = bag.upload(zero), *n_d = bag.upload(cnt);
+  WalkBufs wb;
+  wb.alloc(bag, 1, V, n, p, s);
+  uint32_t *cum_d = bag.get<uint32_t>(n), *freq_d = bag.get<uint32_t>(n);
+  float *p_d = bag.get<float>(n);
+  WalkArgs wa{};
+  wa.chunk_of = c_d; wa.row0 = r_d; wa.count = n_d; wa.n_entries = 1;
+  wa.logits = lg_d; wa.ldl = V; wa.tokens = tk_d; wa.tok_off = off_d;
+  wa.out_cum = cum_d; wa.out_freq = freq_d; wa.out_p = p_d; wa.mode = 0;
+  wb.fill(wa, p, V);
+  launch_walk(wa, s);
+  NC_CUDA(cudaGetLastError());
+  NC_CUDA(cudaMemcpyAsync(cum, cum_d, n * 4, cudaMemcpyDeviceToHost, s));
+  NC_CUDA(cudaMemcpyAsync(freq, freq_d, n * 4, cudaMemcpyDeviceToHost, s));
+  NC_CUDA(cudaMemcpyAsync(p_true, p_d, n * 4, cudaMemcpyDeviceToHost, s));
+  WalkState hs;
+  NC_CUDA(cudaMemcpyAsync(&hs, wb.st, sizeof(hs), cudaMemcpyDeviceToHost, s));
+  NC_CUDA(cudaStreamSynchronize(s));
+  if (hs.err) fail(NC_ERR_INTEGRITY, "walk integrity failure (D6)");
+}
+
+}  // namespace nc

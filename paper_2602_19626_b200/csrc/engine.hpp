@@ -1,0 +1,63 @@
+// Engine: device model, forward orchestration, compress / decompress drivers.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "nc_internal.hpp"
+#include "walk.cuh"
+
+struct nc_model {
+  int device = 0;
+  nc::Shape s{};
+  nc::Tokenizer tok;
+  std::vector<std::string> vocab;
+  float *E = nullptr, *E_head = nullptr;                 // [V, d]
+  std::vector<float *> wqkv, wo, wgu, wd;                // per layer
+  float *rope_cos = nullptr, *rope_sin = nullptr;        // [rope_len, 32]
+  int rope_len = 0;
+  std::vector<void *> owned;                             // cudaFree on destruction
+};
+
+namespace nc {
+
+void check_cuda(cudaError_t e, const char *what);
+#define NC_CUDA(x) ::nc::check_cuda((x), #x)
+
+// device allocation through the hook
+void *dev_alloc(size_t bytes, cudaStream_t s);
+void dev_free(void *p, cudaStream_t s);
+void set_allocator(void *(*a)(size_t, void *), void (*f)(void *, void *), void *ctx);
+
+struct Stats {
+  uint64_t launches = 0;
+  double walk_ms = 0, forward_ms = 0, head_ms = 0;
+};
+Stats &stats();  // thread-local
+
+void model_load(nc_model *m, const std::string &path, int device);
+void model_free(nc_model *m);
+void ensure_rope(nc_model *m, int max_pos);
+
+// Compress pre-tokenized chunks whose tokens live in device memory.
+struct CompressOut {
+  std::vector<uint32_t> cum, freq;   // per token, all chunks concatenated
+  std::vector<float> p_true;         // debug_dump only
+  std::vector<uint32_t> err;         // per chunk
+};
+void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<uint32_t> &ntok,
+                     const Params &p, cudaStream_t s, CompressOut &out);
+// Decode all chunks of a parsed container; returns token ids per chunk.
+void decompress_device(nc_model *m, const uint8_t *blob, const Nc05View &view, const Params &p,
+                       cudaStream_t s, std::vector<std::vector<uint32_t>> &toks);
+// host encode + container
+void encode_container(const Params &p, const std::vector<uint32_t> &ntok, const CompressOut &co,
+                      std::vector<uint8_t> &out);
+// debug
+void debug_forward(nc_model *m, const uint32_t *x, uint32_t rows, const Params &p, int mode, float *out);
+void debug_walk(int device, const float *logits, const uint32_t *tok, uint32_t n, uint32_t V,
+                const Params &p, uint32_t *cum, uint32_t *freq, float *p_true);
+
+}  // namespace nc

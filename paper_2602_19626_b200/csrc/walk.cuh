@@ -1,0 +1,56 @@
+// Per-chunk walk state and launcher for the vocab-row CDF kernel.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace nc {
+
+constexpr int kSlots = 64;            // N-gram continuation cap
+constexpr int kMaxOrders = 4;         // context tables k = 1..4 (D18)
+
+struct NgRecord {                     // one context's continuation table
+  uint32_t n;                         // context occurrences (never decremented, D19)
+  uint32_t nslot;                     // used slots (<= 64)
+  uint32_t tok[kSlots];
+  uint32_t cnt[kSlots];
+};
+
+struct WalkState {                    // per chunk, device resident
+  double lw[2];                       // mixer log-weights
+  uint32_t i;                         // tokens walked so far
+  uint32_t N;                         // unigram total
+  uint32_t hist[4];                   // last 4 tokens (oldest first)
+  uint32_t nrec[kMaxOrders];          // records in use per order
+  uint32_t err;                       // nonzero = integrity failure
+  uint32_t pad;
+  // device WNC decoder (D27)
+  unsigned long long low, high, value, bitpos;
+};
+
+struct WalkArgs {
+  // per launch: entry e handles chunk chunk_of[e], rows [row0[e], row0[e]+count[e]) of logits,
+  // tokens [tok0[e], ...) of the chunk (absolute token index in the chunk = st.i)
+  const int32_t *chunk_of, *row0, *count;
+  int n_entries;
+  const float *logits; int64_t ldl;
+  // encode inputs / outputs, indexed by tok_off[c] + i
+  const uint32_t *tokens; const int64_t *tok_off;
+  uint32_t *out_cum, *out_freq; float *out_p;
+  // decode
+  const uint8_t *streams; const int64_t *stream_off; const uint64_t *stream_bits;
+  uint32_t *out_tok; uint32_t *next_x;
+  // state
+  WalkState *st; double *b; uint32_t *cu; float *spadd;
+  unsigned long long *ng_keys; uint32_t *ng_vals; NgRecord *ng_recs;
+  uint32_t hcap, rcap;                // per (chunk, order) hash slots (pow2) / record pool
+  // params
+  uint32_t V, cdf_bits, warmup, flags, orders, cap;
+  float inv_tau; double alpha, eta;
+  int mode;                           // 0 encode, 1 decode
+};
+
+void launch_walk(const WalkArgs &a, cudaStream_t s);
+void launch_walk_init(WalkState *st, int n_chunks, cudaStream_t s);
+void launch_quantize_debug(const float *p, uint32_t V, uint32_t cdf_bits, uint32_t *counts, cudaStream_t s);
+
+}  // namespace nc

@@ -1,0 +1,226 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bars (BASELINE.json north_star): integer CDFs bit-exact given identical float
+inputs; per-token probabilities within 1e-4 relative of the oracle; compressed
+size within 0.5 %; GPU decompress(GPU compress(x)) == x; prefill and decode
+logits bit-identical (D15).  Logits: 1e-5 of max |z| (fp32-accurate forward,
+SURVEY T-K)."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+P_TOL = 1e-4
+Z_TOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def nc():
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_2602_19626_b200 as m
+    assert torch.cuda.is_available()
+    return m
+
+
+@pytest.fixture(scope="module")
+def m2(nc):
+    from synth import ensure_model
+    return nc.Model(ensure_model("smollm2-2l"), 0)
+
+
+@pytest.fixture(scope="module")
+def w2():
+    from synth import ensure_model
+    from oracle.ncw import Weights
+    return Weights(ensure_model("smollm2-2l"))
+
+
+def _softmax32(z):
+    e = np.exp(z - z.max())
+    return (e / e.sum()).astype(np.float32)
+
+
+# ------------------------------------------------------------ quantizer ----
+@pytest.mark.parametrize("bits", [16, 24])
+def test_quantize_bitexact(nc, bits):
+    from oracle.cdf import quantize
+    rng = np.random.default_rng(bits)
+    V = 49152
+    for scale in (0.3, 1.0, 4.0, 12.0):
+        p = _softmax32(rng.standard_normal(V) * scale)
+        assert np.array_equal(nc.nc_debug_quantize(p, bits), quantize(p, 1 << bits))
+    p = np.zeros(V, np.float32)
+    p[77] = 1.0
+    assert np.array_equal(nc.nc_debug_quantize(p, bits), quantize(p, 1 << bits))
+    p = np.full(V, 1.0 / V, np.float32)          # ties -> lowest index
+    assert np.array_equal(nc.nc_debug_quantize(p, bits), quantize(p, 1 << bits))
+
+
+def test_quantize_negative_residual(nc):
+    from oracle.cdf import quantize
+    p = np.zeros(256, np.float32)
+    p[3] = 1.05                                   # sum p > 1, floors saturated (D6)
+    assert np.array_equal(nc.nc_debug_quantize(p, 16), quantize(p, 1 << 16))
+
+
+# ---------------------------------------------------------------- walker ---
+def _markov_tokens(V, n, seed, k=8):
+    rng = np.random.default_rng(seed)
+    succ = rng.integers(0, V, (V, k))
+    t = [int(rng.integers(V))]
+    for _ in range(n - 1):
+        t.append(int(succ[t[-1], rng.integers(k)]) if rng.random() < 0.7 else int(rng.integers(V)))
+    return t
+
+
+@pytest.mark.parametrize("V,n,flags,bits", [(49152, 400, 3, 24), (49152, 300, 1, 16), (256, 1500, 3, 24),
+                                            (256, 800, 2, 24), (16, 600, 3, 24), (4, 300, 3, 16)])
+def test_walk_parity_synthetic(nc, V, n, flags, bits):
+    from oracle.ensemble import Params, encode_tokens
+    rng = np.random.default_rng(V + n)
+    Z = (rng.standard_normal((n, V)) * (1.0 + rng.random((n, 1)) * 2)).astype(np.float32)
+    toks = _markov_tokens(V, n, V)
+    warm = 50
+    prm = nc.nc_params_default(flags=flags, cdf_bits=bits, warmup=warm)
+    cum, freq, p_gpu = nc.nc_debug_walk(Z, toks, prm)
+    ref = encode_tokens(Z.astype(np.float64), toks, V, Params(flags=flags, cdf_bits=bits, warmup=warm))
+    p_ref = np.array(ref["p_true"])
+    rel = np.abs(p_gpu - p_ref) / p_ref
+    assert rel.max() < P_TOL, rel.max()
+    T = 1 << bits
+    assert (freq >= 1).all() and (cum.astype(np.int64) + freq <= T).all()
+    # integer outputs agree except where fp32 rounding moves a floor boundary
+    assert np.mean(freq == np.array(ref["freq"])) > 0.97
+    ideal_gpu = -np.log2(freq / T).sum()
+    ideal_ref = -np.log2(np.array(ref["freq"]) / T).sum()
+    assert abs(ideal_gpu - ideal_ref) <= 0.005 * ideal_ref + 1
+
+
+def test_walk_gpu_stream_decodes_with_oracle_decoder_when_counts_match(nc):
+    """host encoder on GPU (cum, freq) == oracle encoder on the same pairs."""
+    from oracle.coder import Encoder
+    V, n = 49152, 200
+    rng = np.random.default_rng(5)
+    Z = rng.standard_normal((n, V)).astype(np.float32)
+    toks = list(rng.integers(0, V, n))
+    cum, freq, _ = nc.nc_debug_walk(Z, toks, nc.nc_params_default())
+    enc = Encoder()
+    for c, f in zip(cum, freq):
+        enc.encode(int(c), int(f), 1 << 24)
+    assert nc.nc_host_wnc_encode(cum, freq, 24) == enc.finish()
+
+
+# --------------------------------------------------------------- forward ---
+def test_forward_parity_and_window(nc, m2, w2):
+    from oracle.lm import LM
+    rng = np.random.default_rng(7)
+    n = 700
+    x = [0] + list(rng.integers(3, w2.V, n - 1))
+    prm = nc.nc_params_default(window=256, slide=128, max_slab_rows=256)
+    z_gpu = nc.nc_debug_forward(m2, x, prm, 0)
+    z_ref = LM(w2).forward_blocked(x, 256, 128)
+    err = np.abs(z_gpu - z_ref).max() / np.abs(z_ref).max()
+    assert err < Z_TOL, err
+
+
+def test_prefill_decode_bit_identity(nc, m2, w2):
+    rng = np.random.default_rng(8)
+    n = 420
+    x = [0] + list(rng.integers(3, w2.V, n - 1))
+    prm = nc.nc_params_default(window=256, slide=128, max_slab_rows=256)
+    a = nc.nc_debug_forward(m2, x, prm, 0)
+    b = nc.nc_debug_forward(m2, x, prm, 1)
+    assert np.array_equal(a, b)
+    prm2 = nc.nc_params_default(window=256, slide=128, max_slab_rows=128)
+    assert np.array_equal(a, nc.nc_debug_forward(m2, x, prm2, 0))     # slab size invariance
+
+
+# ------------------------------------------------------------ end to end ---
+def _oracle_size_and_p(w, data, prm_o):
+    from oracle.chunking import split_chunks
+    from oracle.ensemble import encode_tokens
+    from oracle.lm import LM
+    from oracle.tokenizer import Tokenizer
+    tk, lm = Tokenizer(w.vocab), LM(w)
+    size, ps, xs, ts = 9, [], [], []
+    for ch in split_chunks(data, prm_o.n_chunks):
+        t = tk.encode(ch)
+        x = [w.bos] + t[:-1] if t else []
+        Z = lm.forward_blocked(x, prm_o.window, prm_o.slide)
+        r = encode_tokens(Z, t, w.V, prm_o)
+        size += 12 + (r["bits"] + 7) // 8
+        ps.append(np.array(r["p_true"]))
+        xs.append(x)
+        ts.append(t)
+    return size, ps, xs, ts
+
+
+@pytest.mark.parametrize("n_chunks,flags,bits", [(1, 3, 24), (3, 3, 24), (2, 1, 16), (1, 0, 24)])
+def test_config1_roundtrip_size_and_p(nc, m2, w2, n_chunks, flags, bits):
+    from oracle.ensemble import Params
+    from synth import make_text
+    data = make_text("alice", 4096, 1001)
+    prm = nc.nc_params_default(window=512, slide=128, n_chunks=n_chunks, flags=flags, cdf_bits=bits)
+    blob = nc.nc_compress(m2, data, prm)
+    assert nc.nc_decompress(m2, blob, prm) == data
+    size, ps, xs, ts = _oracle_size_and_p(w2, data, Params(window=512, slide=128, n_chunks=n_chunks,
+                                                            flags=flags, cdf_bits=bits))
+    assert abs(len(blob) - size) <= 0.005 * size, (len(blob), size)
+    for x, t, p_ref in zip(xs, ts, ps):
+        z = nc.nc_debug_forward(m2, x, prm, 0)
+        _, _, p_gpu = nc.nc_debug_walk(z, t, prm)
+        assert (np.abs(p_gpu - p_ref) / p_ref).max() < P_TOL
+
+
+def test_edge_inputs_roundtrip(nc, m2):
+    prm = nc.nc_params_default(window=256, slide=128, n_chunks=4)
+    for data in (b"", b"a", b"\x00\x00\xff\n", b"\n" * 9, bytes(range(256)) * 3):
+        assert nc.nc_decompress(m2, nc.nc_compress(m2, data, prm), prm) == data
+
+
+def test_decompress_detects_wrong_params_and_corruption(nc, m2):
+    from synth import make_text
+    data = make_text("alice", 1500, 5)
+    prm = nc.nc_params_default(window=256, slide=128, n_chunks=1)
+    blob = nc.nc_compress(m2, data, prm)
+    bad = nc.nc_params_default(window=256, slide=128, n_chunks=1, warmup=7)
+    try:
+        out = nc.nc_decompress(m2, blob, bad)
+        assert out != data
+    except nc.NcError as e:
+        assert e.status in (nc._lib.NC_ERR_INTEGRITY,)
+    corrupt = bytearray(blob)
+    corrupt[len(blob) // 2] ^= 0x40
+    try:
+        assert nc.nc_decompress(m2, bytes(corrupt), prm) != data
+    except nc.NcError:
+        pass
+    with pytest.raises(nc.NcError):
+        nc.nc_decompress(m2, b"NC99" + blob[4:], prm)
+    with pytest.raises(nc.NcError):
+        nc.nc_decompress(m2, blob[:-3], prm)
+
+
+# --------------------------------------------------- full-size sampled rows ---
+@pytest.mark.slow
+def test_full_model_sampled_rows(nc):
+    """30-layer model, L=2048/C=512 as bench.py runs it: the first 2,600 rows of
+    one chunk (two slides) against the oracle, plus decode bit-identity on a
+    sample of rows."""
+    from oracle.lm import LM
+    from oracle.ncw import Weights
+    from synth import ensure_model
+    path = ensure_model("smollm2-135m")
+    m = nc.Model(path, 0)
+    w = Weights(path)
+    rng = np.random.default_rng(11)
+    n = 2600
+    x = [0] + list(rng.integers(3, w.V, n - 1))
+    prm = nc.nc_params_default()
+    z = nc.nc_debug_forward(m, x, prm, 0)
+    ref = LM(w).forward_blocked(x, 2048, 512)
+    err = np.abs(z - ref).max() / np.abs(ref).max()
+    assert err < Z_TOL, err
+    m.close()
