@@ -1,0 +1,354 @@
+#!/usr/bin/env python
+"""Benchmark: compress bytes/s of the Nacrith hot path on B200 (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload config2]
+
+One step = one full compression of the workload (SURVEY.md §8(a) rows a1-a10:
+embed, 30 x {RMSNorm+QKV+RoPE, window attention, O, RMSNorm+SwiGLU MLP},
+head, the per-token CDF walk, host range coding, NC05 assembly).
+
+value : device-resident inputs (token ids already in HBM) -> NC05 container
+        through nc_compress_tokens; CUDA events on the launching stream,
+        barrier + synchronize around every step, max over ranks.
+e2e   : the same through nc_compress (host bytes in, container out:
+        tokenization, H2D of the token ids, D2H of the (cum, freq) pairs).
+For N > 1 (torchrun) each rank compresses its own contiguous chunk range
+(weak scaling, no data-path collective); e2e uses nc_compress_shard, whose
+only collective is one NCCL allgather of the chunk table.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "sm_max_mhz": 1965.0}
+N_SM = 148
+FP32_LANES_PER_SM = 128          # B200: 4 SMSPs x 32 FP32 lanes (B300_MICROARCH.md / guide)
+
+
+def peaks():
+    try:
+        with open(PEAKS_FILE) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return FALLBACK, "fallback"
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, device):
+        self.device, self.proc, self.path = device, None, None
+
+    def start(self):
+        try:
+            os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+            self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=index,clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 9 and f[1].isdigit():
+                rows.append(f)
+        if not rows:
+            return None
+        sm = [int(r[1]) for r in rows]
+        load = [int(r[1]) for r in rows if float(r[3] or 0) > 200] or sm
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for n, v in zip(names, r[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": int(statistics.median(load)), "sm_max_mhz": int(rows[0][2]), "reasons": sorted(reasons),
+                "samples": len(rows)}
+
+
+# ------------------------------------------------------------------ oracle ---
+def oracle_sample(workload, path, data, n_tokens):
+    """CPU oracle (as it stands) on the first n_tokens of chunk 0 of the workload:
+    blocked fp64 forward + ensemble walk + WNC.  Returns (bytes, seconds, cores)."""
+    from oracle.chunking import split_chunks
+    from oracle.ensemble import Params, encode_tokens
+    from oracle.lm import LM
+    from oracle.ncw import Weights
+    from oracle.tokenizer import Tokenizer
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    w = Weights(path)
+    ch = split_chunks(data, workload.n_chunks)[0]
+    tk = Tokenizer(w.vocab)
+    t = tk.encode(ch)[:n_tokens]
+    nbytes = len(tk.decode(t))
+    prm = Params(window=workload.window, slide=workload.slide, cdf_bits=workload.cdf_bits)
+    t0 = time.perf_counter()
+    x = [w.bos] + t[:-1]
+    Z = LM(w).forward_blocked(x, prm.window, prm.slide)
+    encode_tokens(Z, t, w.V, prm)
+    dt = time.perf_counter() - t0
+    return nbytes, dt, cores, len(t)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="config2")
+    ap.add_argument("--no-decompress", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--oracle-tokens", type=int, default=192)
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+
+    from synth import WORKLOADS, ensure_model, ensure_text, make_text
+    wl = WORKLOADS[args.workload]
+    metric, unit = "compress_bytes_per_sec", "B/s"
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        path = ensure_model(wl.shape)
+        data = open(ensure_text(args.workload), "rb").read()
+        times, nb = [], 0
+        for i in range(args.warmup + args.steps):
+            nb, dt, cores, ntok = oracle_sample(wl, path, data, args.oracle_tokens)
+            if i >= args.warmup:
+                times.append(dt)
+        v = nb * len(times) / sum(times)
+        line = {"impl": "reference", "metric": metric, "value": v, "unit": unit, "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * statistics.mean(times),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "config": {"workload": args.workload, "model": wl.shape,
+                                                "sample": f"first {ntok} tokens of chunk 0"},
+                "cpu_baseline": {"value": v, "unit": unit, "cores": cores, "kind": "oracle",
+                                 "sample": f"first {ntok} tokens ({nb} B) of chunk 0 of {args.workload}, "
+                                           "blocked fp64 LM + walk + WNC, per step"},
+                "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    if rank == 0:
+        import __graft_entry__
+        __graft_entry__.build()
+        path = ensure_model(wl.shape)
+        ensure_text(args.workload)
+    if world > 1:
+        dist.barrier()
+    import paper_2602_19626_b200 as nc
+    path = ensure_model(wl.shape)
+    # weak scaling: each rank owns wl.n_bytes of input and wl.n_chunks chunks
+    data = open(ensure_text(args.workload), "rb").read() if world == 1 else \
+        make_text(wl.text_kind, wl.n_bytes * world, wl.text_seed)
+    n_chunks = wl.n_chunks * world
+    prm = nc.nc_params_default(window=wl.window, slide=wl.slide, n_chunks=n_chunks, cdf_bits=wl.cdf_bits)
+    model = nc.Model(path, local)
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+
+    cuts = nc.nc_host_split(data, n_chunks)
+    nch = len(cuts) - 1
+    c0, c1 = nc.nc_host_shard_range(nch, world, rank)
+    my_bytes = cuts[c1] - cuts[c0] if c1 > c0 else 0
+    toks, ntok = [], []
+    for c in range(c0, c1):
+        t, _ = nc.nc_tokenize(model, data[cuts[c]:cuts[c + 1]], 1)
+        toks.append(t)
+        ntok.append(len(t))
+    tokens = np.concatenate(toks) if toks else np.zeros(0, np.uint32)
+    tok_dev = torch.from_numpy(tokens.view(np.int32).copy()).to(f"cuda:{local}")
+    my_prm = nc.nc_params_default(window=wl.window, slide=wl.slide, n_chunks=max(1, c1 - c0), cdf_bits=wl.cdf_bits)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=f"cuda:{local}")   # > 126 MB L2
+
+    def run_value():
+        return nc.nc_compress_tokens(model, tok_dev.data_ptr(), np.array(ntok, np.uint32), my_prm, sptr)
+
+    def timed(fn, k, w_, profile=False, clocks=None):
+        for _ in range(w_):
+            fn()
+        total = 0.0
+        launches = 0
+        if profile:
+            nc.nc_set_profiling(True)
+        if clocks:
+            clocks.start()
+        out = None
+        for _ in range(k):
+            flush.zero_()
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            out = fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            total += e0.elapsed_time(e1)
+            launches += nc.nc_last_stats()["kernel_launches"]
+        clk = clocks.stop() if clocks else None
+        prof = nc.nc_profile() if profile else None
+        if profile:
+            nc.nc_set_profiling(False)
+        if world > 1:
+            t = torch.tensor([total], dtype=torch.float64, device=f"cuda:{local}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            total = float(t.item())
+        return total / 1000.0, out, launches // max(1, k), prof, clk
+
+    # ---- value: device-resident tokens
+    clocks = Clocks(local)
+    t_val, blob_part, launches, prof, clk = timed(run_value, args.steps, args.warmup, profile=True, clocks=clocks)
+    total_bytes = len(data)
+    value = total_bytes * args.steps / t_val
+
+    # ---- e2e: host bytes in, container (part) out, through the public API
+    if world == 1:
+        def run_e2e():
+            return nc.nc_compress(model, data, prm, sptr)
+    else:
+        uid = nc.Comm.unique_id() if rank == 0 else bytes(128)
+        obj = [uid]
+        dist.broadcast_object_list(obj, src=0)
+        comm = nc.Comm(rank, world, obj[0], local)
+
+        def run_e2e():
+            return nc.nc_compress_shard(model, comm, data, prm, sptr)
+    t_e2e, e2e_out, _, _, _ = timed(run_e2e, args.steps, max(1, args.warmup // 2))
+    e2e = total_bytes * args.steps / t_e2e
+
+    # ---- correctness + bpb + decompress (rank 0 / N=1)
+    blob = e2e_out if world == 1 else None
+    bpb, dec = None, None
+    if world == 1:
+        bpb = 8.0 * len(blob) / len(data)
+        if not args.no_decompress:
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            back = nc.nc_decompress(model, blob, prm, sptr)
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+            assert back == data, "round trip failed"
+            dec = {"value": len(data) / dt, "unit": "B/s", "seconds": dt}
+        else:
+            assert len(blob) > 0
+
+    # ---- roofline of the dominant kernel class (live CUDA events over the timed region)
+    pk, pk_kind = peaks()
+    sm_max = float(pk.get("sm_max_mhz", 1965.0))
+    alu_peak = N_SM * FP32_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12       # TFLOP/s fp32 FFMA
+    kernels = {}
+    for name, r in (prof or {}).items():
+        if r["launches"]:
+            kernels[name] = {"launches": r["launches"] // args.steps, "ms_per_step": r["ms"] / args.steps,
+                             "work_per_step": r["work"] / args.steps}
+    flop_classes = {"gemm_qkv", "gemm_o", "gemm_gateup", "gemm_down", "gemm_head", "attention"}
+    dom = max(kernels, key=lambda k: kernels[k]["ms_per_step"]) if kernels else None
+    roof = None
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get(dom)
+    except Exception:
+        pass
+    if dom:
+        r = kernels[dom]
+        per_launch_ms = r["ms_per_step"] / max(1, r["launches"])
+        work_launch = r["work_per_step"] / max(1, r["launches"])
+        if dom in flop_classes:
+            ach = work_launch / (per_launch_ms / 1e3) / 1e12
+            roof = {"kernel": dom, "bound": "alu", "achieved": ach, "peak": alu_peak, "unit": "TFLOP/s",
+                    "frac": ach / alu_peak, "traffic": traffic,
+                    "peak_source": f"derived: {N_SM} SMs x {FP32_LANES_PER_SM} FP32 lanes x 2 x {sm_max:.0f} MHz "
+                                   "(SIMT fp32 FFMA path, DESIGN.md)"}
+        else:
+            ach = work_launch / (per_launch_ms / 1e3) / 1e9
+            roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                    "frac": ach / pk["hbm_gbs"], "traffic": traffic, "peak_source": pk_kind}
+        roof["share_of_step"] = r["ms_per_step"] / (1000 * t_val / args.steps)
+    walk = kernels.get("walk")
+    if walk:
+        kernels["walk"]["hbm_gbs"] = walk["work_per_step"] / (walk["ms_per_step"] / 1e3) / 1e9
+    for k in flop_classes & set(kernels):
+        kernels[k]["tflops"] = kernels[k]["work_per_step"] / (kernels[k]["ms_per_step"] / 1e3) / 1e12
+
+    # ---- CPU oracle baseline (rank 0, N = 1 only, bounded sample)
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        nb, dt, cores, ntk = oracle_sample(wl, path, data, args.oracle_tokens)
+        cpu = {"value": nb / dt, "unit": unit, "cores": cores, "kind": "oracle",
+               "sample": f"first {ntk} tokens ({nb} B) of chunk 0, blocked fp64 30-layer LM + walk + WNC, "
+                         f"{dt:.1f} s"}
+
+    n_tok_total = int(sum(ntok))
+    if world > 1:
+        t = torch.tensor([n_tok_total], dtype=torch.int64, device=f"cuda:{local}")
+        dist.all_reduce(t)
+        n_tok_total = int(t.item())
+    if rank == 0:
+        line = {
+            "metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1000 * t_val / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": args.workload, "model": wl.shape, "text": wl.text_kind,
+                       "bytes_per_gpu": wl.n_bytes, "chunks_per_gpu": wl.n_chunks, "window": wl.window,
+                       "slide": wl.slide, "cdf_bits": wl.cdf_bits, "tokens": n_tok_total,
+                       "l2": "256 MB buffer written between timed steps; working set (538 MB weights, "
+                             "logit slabs) > 126 MB L2",
+                       "parallelism": f"chunk-sharded x{world}"},
+            "e2e": {"value": e2e, "unit": unit, "h2d_bytes_per_step": 4 * n_tok_total,
+                    "d2h_bytes_per_step": 8 * n_tok_total},
+            "gpu_launches": launches,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "clocks": clk,
+            "bpb": bpb,
+            "decompress": dec,
+            "kernels": kernels,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -147,6 +147,15 @@ const char *nc_last_error(void);   /* thread-local; never NULL           */
 nc_status nc_last_stats(uint64_t *kernel_launches, double *walk_ms, double *forward_ms,
                         double *head_ms);
 
+/* Per-kernel-class device timing (CUDA events around every launch, on the
+ * launching stream).  nc_set_profiling(1) enables it and clears the totals;
+ * classes: 0 embed, 1 rms, 2 gemm_qkv, 3 attention, 4 gemm_o, 5 gemm_gateup,
+ * 6 gemm_down, 7 gemm_head, 8 walk, 9 misc.  work = algorithmic FLOPs (GEMMs,
+ * attention) or bytes (embed, rms, walk: 4*V logits bytes per token, §8(d))
+ * summed over the launches since the last reset. */
+nc_status nc_set_profiling(int on);
+nc_status nc_profile(int cls, uint64_t *launches, double *ms, double *work, const char **name);
+
 /* ---- test-only entry points (no side effects on models) ------------------ */
 
 /* GPU quantizer on caller floats (host array p[V]): counts_out[V] (host) per

@@ -21,7 +21,7 @@ EXPORTS = [
     "nc_comm_init", "nc_comm_free", "nc_compress_shard", "nc_decompress_shard", "nc_free",
     "nc_last_error", "nc_last_stats", "nc_debug_quantize", "nc_debug_walk", "nc_debug_forward",
     "nc_host_split", "nc_host_wnc_encode", "nc_host_tokenize_vocab", "nc_host_shard_range",
-    "nc_host_shard_part",
+    "nc_host_shard_part", "nc_set_profiling", "nc_profile",
 ]
 
 
@@ -66,6 +66,9 @@ def lib():
             "nc_compress_shard": (C.c_int, [P, P, P, C.c_size_t, C.POINTER(nc_params), P, pp, szp, u64p, u64p]),
             "nc_decompress_shard": (C.c_int, [P, P, P, C.c_size_t, C.POINTER(nc_params), P, pp, szp, u64p, u64p]),
             "nc_free": (None, [P]),
+            "nc_set_profiling": (C.c_int, [C.c_int]),
+            "nc_profile": (C.c_int, [C.c_int, u64p, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                     C.POINTER(C.c_char_p)]),
             "nc_last_error": (C.c_char_p, []),
             "nc_last_stats": (C.c_int, [u64p, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)]),
             "nc_debug_quantize": (C.c_int, [f32p, C.c_uint32, C.c_uint32, u32p]),
@@ -183,6 +186,20 @@ def nc_last_stats():
     k, w, f, h = C.c_uint64(), C.c_double(), C.c_double(), C.c_double()
     _check(lib().nc_last_stats(C.byref(k), C.byref(w), C.byref(f), C.byref(h)))
     return dict(kernel_launches=k.value, walk_ms=w.value, forward_ms=f.value, head_ms=h.value)
+
+
+def nc_set_profiling(on: bool):
+    _check(lib().nc_set_profiling(1 if on else 0))
+
+
+def nc_profile():
+    """{class name: dict(launches, ms, work)} since the last nc_set_profiling."""
+    out = {}
+    for cls in range(10):
+        n, ms, w, name = C.c_uint64(), C.c_double(), C.c_double(), C.c_char_p()
+        _check(lib().nc_profile(cls, C.byref(n), C.byref(ms), C.byref(w), C.byref(name)))
+        out[name.value.decode()] = dict(launches=n.value, ms=ms.value, work=w.value)
+    return out
 
 
 def nc_debug_quantize(p, cdf_bits: int):

@@ -220,6 +220,24 @@ nc_status nc_last_stats(uint64_t *kernel_launches, double *walk_ms, double *forw
   return NC_OK;
 }
 
+nc_status nc_set_profiling(int on) {
+  return guard([&] {
+    nc::prof().reset();
+    nc::prof().on = on != 0;
+  });
+}
+
+nc_status nc_profile(int cls, uint64_t *launches, double *ms, double *work, const char **name) {
+  static const char *names[nc::K_NCLASS] = {"embed", "rms", "gemm_qkv", "attention", "gemm_o",
+                                            "gemm_gateup", "gemm_down", "gemm_head", "walk", "misc"};
+  if (cls < 0 || cls >= nc::K_NCLASS) return set_err(NC_ERR_INVALID, "bad class");
+  if (launches) *launches = nc::prof().n[cls];
+  if (ms) *ms = nc::prof().ms[cls];
+  if (work) *work = nc::prof().work[cls];
+  if (name) *name = names[cls];
+  return NC_OK;
+}
+
 void nc_free(void *p) { std::free(p); }
 const char *nc_last_error(void) { return g_err.c_str(); }
 

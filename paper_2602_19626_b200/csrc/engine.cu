@@ -42,6 +42,52 @@ Stats &stats() {
   return st;
 }
 
+Prof &prof() {
+  static Prof p;
+  return p;
+}
+cudaEvent_t Prof::ev() {
+  if (used == pool.size()) {
+    cudaEvent_t e;
+    NC_CUDA(cudaEventCreate(&e));
+    pool.push_back(e);
+  }
+  return pool[used++];
+}
+void Prof::begin(int cls, double w, cudaStream_t s) {
+  if (!on) return;
+  Rec r{cls, ev(), ev(), w};
+  NC_CUDA(cudaEventRecord(r.a, s));
+  recs.push_back(r);
+}
+void Prof::end(cudaStream_t s) {
+  if (!on) return;
+  NC_CUDA(cudaEventRecord(recs.back().b, s));
+}
+void Prof::collect() {
+  for (auto &r : recs) {
+    float t = 0;
+    NC_CUDA(cudaEventSynchronize(r.b));
+    NC_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+    n[r.cls]++;
+    ms[r.cls] += t;
+    work[r.cls] += r.work;
+  }
+  recs.clear();
+  used = 0;
+}
+void Prof::reset() {
+  recs.clear();
+  used = 0;
+  for (int i = 0; i < K_NCLASS; ++i) { n[i] = 0; ms[i] = 0; work[i] = 0; }
+}
+#define PROF(cls, w, call)            \
+  do {                                \
+    prof().begin((cls), (w), s);      \
+    call;                             \
+    prof().end(s);                    \
+  } while (0)
+
 // RAII bag of device buffers for one call
 struct Bag {
   cudaStream_t s;
@@ -72,7 +118,7 @@ void model_load(nc_model *m, const std::string &path, int device) {
   const Shape &s = f.s;
   if (s.dh != (uint32_t)kHeadDim) fail(NC_ERR_INVALID, "kernels are specialised to head_dim 64");
   if (s.H % s.KV || s.H / s.KV > 3) fail(NC_ERR_INVALID, "GQA group must be <= 3");
-  if (s.d % 128 || s.d_ff % 64) fail(NC_ERR_INVALID, "d_model must be a multiple of 128, d_ff of 64");
+  if (s.d % 64 || s.d_ff % 64) fail(NC_ERR_INVALID, "d_model and d_ff must be multiples of 64");
   if (s.V % 128) fail(NC_ERR_INVALID, "vocab must be a multiple of 128");
   NC_CUDA(cudaSetDevice(device));
   m->device = device;
@@ -184,48 +230,63 @@ struct Forward {
     ring.k = bag.get<float>(rn);
     ring.v = bag.get<float>(rn);
   }
-  // embed -> n_layers x {QKV, attention, O, gate-up, down} -> head into `logits`
-  void run(int M, const RowMeta &rows, const AttnTile *tiles, int n_tiles, const Params &p, cudaEvent_t ev_head) {
+  // embed -> n_layers x {QKV, attention, O, gate-up, down} -> head into `logits`.
+  // valid = rows that are real tokens (algorithmic work), attn_flops = sum over
+  // valid rows of 4*H*dh*n_ctx(j) for one layer.
+  void run(int M, double valid, double attn_flops, const RowMeta &rows, const AttnTile *tiles, int n_tiles,
+           const Params &p, cudaEvent_t ev_head) {
     const Shape &S = m->s;
     Stats &st = stats();
     const int qd = S.H * S.dh, kvd = S.KV * S.dh;
-    launch_embed(rows.x, M, m->E, S.d, h, s);
+    const double d = S.d;
+    PROF(K_EMBED, 4.0 * d * valid, launch_embed(rows.x, M, m->E, S.d, h, s));
     st.launches++;
     for (uint32_t l = 0; l < S.n_layers; ++l) {
-      launch_rms(h, M, S.d, (float)S.eps, rinv, s);
+      PROF(K_RMS, 4.0 * d * valid, launch_rms(h, M, S.d, (float)S.eps, rinv, s));
       GemmArgs g{};
       g.A = h; g.lda = S.d; g.B = m->wqkv[l]; g.ldb = S.d; g.M = M; g.N = qd + 2 * kvd; g.K = S.d;
       g.rinv = rinv; g.C = q; g.ldc = qd; g.layer = (int)l; g.n_q_cols = qd; g.n_kv_cols = kvd;
       g.rows = rows; g.ring = ring; g.rope_cos = m->rope_cos; g.rope_sin = m->rope_sin;
-      launch_gemm(EPI_QKV, g, s);
+      PROF(K_QKV, 2.0 * valid * (qd + 2 * kvd) * d, launch_gemm(EPI_QKV, g, s));
       AttnArgs at{};
       at.tiles = tiles; at.n_tiles = n_tiles; at.q = q; at.o = o; at.ldq = qd; at.ring = ring; at.layer = (int)l;
       at.H = S.H; at.KV = S.KV; at.window = (int)p.window; at.slide = (int)p.slide;
-      launch_attention(at, s);
+      PROF(K_ATTN, attn_flops, launch_attention(at, s));
       GemmArgs go{};
       go.A = o; go.lda = qd; go.B = m->wo[l]; go.ldb = qd; go.M = M; go.N = S.d; go.K = qd; go.C = h; go.ldc = S.d;
-      launch_gemm(EPI_RESID, go, s);
-      launch_rms(h, M, S.d, (float)S.eps, rinv, s);
+      PROF(K_OPROJ, 2.0 * valid * d * qd, launch_gemm(EPI_RESID, go, s));
+      PROF(K_RMS, 4.0 * d * valid, launch_rms(h, M, S.d, (float)S.eps, rinv, s));
       GemmArgs gu{};
       gu.A = h; gu.lda = S.d; gu.B = m->wgu[l]; gu.ldb = S.d; gu.M = M; gu.N = 2 * S.d_ff; gu.K = S.d;
       gu.rinv = rinv; gu.C = act; gu.ldc = S.d_ff;
-      launch_gemm(EPI_SWIGLU, gu, s);
+      PROF(K_GATEUP, 2.0 * valid * 2 * S.d_ff * d, launch_gemm(EPI_SWIGLU, gu, s));
       GemmArgs gd{};
       gd.A = act; gd.lda = S.d_ff; gd.B = m->wd[l]; gd.ldb = S.d_ff; gd.M = M; gd.N = S.d; gd.K = S.d_ff;
       gd.C = h; gd.ldc = S.d;
-      launch_gemm(EPI_RESID, gd, s);
+      PROF(K_DOWN, 2.0 * valid * d * S.d_ff, launch_gemm(EPI_RESID, gd, s));
       st.launches += 6;
     }
     if (ev_head) NC_CUDA(cudaEventRecord(ev_head, s));
-    launch_rms(h, M, S.d, (float)S.eps, rinv, s);
+    PROF(K_RMS, 4.0 * d * valid, launch_rms(h, M, S.d, (float)S.eps, rinv, s));
     GemmArgs gh{};
     gh.A = h; gh.lda = S.d; gh.B = m->E_head; gh.ldb = S.d; gh.M = M; gh.N = S.V; gh.K = S.d;
     gh.rinv = rinv; gh.C = logits; gh.ldc = S.V;
-    launch_gemm(EPI_HEAD, gh, s);
+    PROF(K_HEAD, 2.0 * valid * S.V * d, launch_gemm(EPI_HEAD, gh, s));
     st.launches += 2;
     NC_CUDA(cudaGetLastError());
   }
 };
+
+static double window_start_h(int64_t j, int64_t L, int64_t C) {
+  int64_t over = j + 1 - L;
+  return over <= 0 ? 0 : (double)(C * ((over + C - 1) / C));
+}
+// sum over positions [p0, p1) of n_ctx(j) = j - w(j) + 1
+static double ctx_sum(int64_t p0, int64_t p1, int64_t L, int64_t C) {
+  double s = 0;
+  for (int64_t j = p0; j < p1; ++j) s += (double)j - window_start_h(j, L, C) + 1;
+  return s;
+}
 
 __global__ void slab_rows_kernel(const uint32_t *tokens, const int64_t *tok_off, const uint32_t *ntok, int R, int s,
                                  int M, uint32_t bos, uint32_t *x, int32_t *chunk, int32_t *pos) {
@@ -358,10 +419,18 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
   for (auto &e : ev) NC_CUDA(cudaEventCreate(&e));
   for (int sl = 0; sl < n_slabs; ++sl) {
     NC_CUDA(cudaEventRecord(ev[3 * sl], s));
-    slab_rows_kernel<<<(M + 255) / 256, 256, 0, s>>>(tokens_dev, tok_off_d, ntok_d, R, sl, M, S.bos, xs, rchunk, rpos);
+    PROF(K_MISC, 0, (slab_rows_kernel<<<(M + 255) / 256, 256, 0, s>>>(tokens_dev, tok_off_d, ntok_d, R, sl, M, S.bos,
+                                                                      xs, rchunk, rpos)));
     st.launches++;
     RowMeta rows{xs, rchunk, rpos};
-    fw.run(M, rows, tiles_d + tile_off[sl], tile_off[sl + 1] - tile_off[sl], p, ev[3 * sl + 1]);
+    double valid = 0, ctx = 0, walk_tok = 0;
+    for (int c = 0; c < n_chunks; ++c) {
+      int64_t a0 = (int64_t)sl * R, a1 = std::min<int64_t>((int64_t)(sl + 1) * R, ntok[c]);
+      if (a1 > a0) { valid += (double)(a1 - a0); ctx += ctx_sum(a0, a1, p.window, p.slide); }
+    }
+    walk_tok = valid;
+    fw.run(M, valid, 4.0 * S.H * S.dh * ctx, rows, tiles_d + tile_off[sl], tile_off[sl + 1] - tile_off[sl], p,
+           ev[3 * sl + 1]);
     NC_CUDA(cudaEventRecord(ev[3 * sl + 2], s));
     WalkArgs wa{};
     wa.chunk_of = wc_d + w_off[sl]; wa.row0 = wr_d + w_off[sl]; wa.count = wn_d + w_off[sl];
@@ -371,7 +440,7 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
     wa.out_cum = cum_d; wa.out_freq = freq_d; wa.out_p = p_d;
     wa.mode = 0;
     wb.fill(wa, p, S.V);
-    launch_walk(wa, s);
+    PROF(K_WALK, 4.0 * S.V * walk_tok, launch_walk(wa, s));
     st.launches++;
     NC_CUDA(cudaGetLastError());
   }
@@ -382,6 +451,7 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
   std::vector<WalkState> hs(n_chunks);
   NC_CUDA(cudaMemcpyAsync(hs.data(), wb.st, n_chunks * sizeof(WalkState), cudaMemcpyDeviceToHost, s));
   NC_CUDA(cudaStreamSynchronize(s));
+  if (prof().on) prof().collect();
   for (int c = 0; c < n_chunks; ++c) out.err[c] = hs[c].err;
   for (int sl = 0; sl < n_slabs; ++sl) {
     float a, b, c;
@@ -486,12 +556,19 @@ void decompress_device(nc_model *m, const uint8_t *blob, const Nc05View &view, c
   NC_CUDA(cudaEventCreate(&e1));
   NC_CUDA(cudaEventRecord(e0, s));
   for (uint32_t j = 0; j < max_n; ++j) {
-    step_rows_kernel<<<(n_chunks + 127) / 128, 128, 0, s>>>(ntok_d, n_chunks, (int)j, rchunk, rpos, tiles, wc, wr, wn);
+    double valid = 0;
+    for (int c = 0; c < n_chunks; ++c) valid += j < ntok[c] ? 1 : 0;
+    const double ctx = (double)j - window_start_h(j, p.window, p.slide) + 1;
+    PROF(K_MISC, 0, (step_rows_kernel<<<(n_chunks + 127) / 128, 128, 0, s>>>(ntok_d, n_chunks, (int)j, rchunk, rpos,
+                                                                           tiles, wc, wr, wn)));
     RowMeta rows{x_cur, rchunk, rpos};
-    fw.run(n_chunks, rows, tiles, n_chunks, p, nullptr);
-    launch_walk(wa, s);
+    fw.run(n_chunks, valid, 4.0 * S.H * S.dh * ctx * valid, rows, tiles, n_chunks, p, nullptr);
+    PROF(K_WALK, 4.0 * S.V * valid, launch_walk(wa, s));
     st.launches += 2;
-    if ((j & 255) == 255) NC_CUDA(cudaGetLastError());
+    if ((j & 255) == 255) {
+      NC_CUDA(cudaGetLastError());
+      if (prof().on) { NC_CUDA(cudaStreamSynchronize(s)); prof().collect(); }
+    }
   }
   NC_CUDA(cudaEventRecord(e1, s));
   std::vector<uint32_t> all(total);
@@ -499,6 +576,7 @@ void decompress_device(nc_model *m, const uint8_t *blob, const Nc05View &view, c
   std::vector<WalkState> hs(n_chunks);
   NC_CUDA(cudaMemcpyAsync(hs.data(), wb.st, n_chunks * sizeof(WalkState), cudaMemcpyDeviceToHost, s));
   NC_CUDA(cudaStreamSynchronize(s));
+  if (prof().on) prof().collect();
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
   st.forward_ms += ms;
@@ -550,7 +628,7 @@ void debug_forward(nc_model *m, const uint32_t *x, uint32_t rows, const Params &
       AttnTile *td = bag.upload(tiles);
       slab_rows_kernel<<<(Rr + 255) / 256, 256, 0, s>>>(t_d, off_d, nt_d, Rr, sl, Rr, x[0], xs, rc, rp);
       RowMeta rm{xs, rc, rp};
-      fw.run(Rr, rm, td, (int)tiles.size(), p, nullptr);
+      fw.run(Rr, 0, 0, rm, td, (int)tiles.size(), p, nullptr);
       int cnt = std::min<int>(Rr, (int)rows - sl * Rr);
       NC_CUDA(cudaMemcpyAsync(out + (size_t)sl * Rr * S.V, fw.logits, (size_t)cnt * S.V * 4, cudaMemcpyDeviceToHost, s));
     }
@@ -564,7 +642,7 @@ void debug_forward(nc_model *m, const uint32_t *x, uint32_t rows, const Params &
     for (uint32_t j = 0; j < rows; ++j) {
       step_rows_kernel<<<1, 32, 0, s>>>(nt_d, 1, (int)j, rc, rp, tiles, wc, wr, wn);
       RowMeta rm{x_d + j, rc, rp};
-      fw.run(1, rm, tiles, 1, p, nullptr);
+      fw.run(1, 0, 0, rm, tiles, 1, p, nullptr);
       NC_CUDA(cudaMemcpyAsync(out + (size_t)j * S.V, fw.logits, (size_t)S.V * 4, cudaMemcpyDeviceToHost, s));
     }
   }

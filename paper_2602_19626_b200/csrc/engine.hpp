@@ -37,6 +37,24 @@ struct Stats {
 };
 Stats &stats();  // thread-local
 
+// Optional per-kernel-class CUDA-event profiling (bench.py's live roofline).
+enum KClass { K_EMBED = 0, K_RMS, K_QKV, K_ATTN, K_OPROJ, K_GATEUP, K_DOWN, K_HEAD, K_WALK, K_MISC, K_NCLASS };
+struct Prof {
+  bool on = false;
+  struct Rec { int cls; cudaEvent_t a, b; double work; };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  uint64_t n[K_NCLASS] = {};
+  double ms[K_NCLASS] = {}, work[K_NCLASS] = {};
+  cudaEvent_t ev();
+  void begin(int cls, double work, cudaStream_t s);   // records start
+  void end(cudaStream_t s);                           // records end of the last begin
+  void collect();                                     // after a stream sync
+  void reset();
+};
+Prof &prof();
+
 void model_load(nc_model *m, const std::string &path, int device);
 void model_free(nc_model *m);
 void ensure_rope(nc_model *m, int max_pos);

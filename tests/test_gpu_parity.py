@@ -91,8 +91,10 @@ def test_walk_parity_synthetic(nc, V, n, flags, bits):
     assert rel.max() < P_TOL, rel.max()
     T = 1 << bits
     assert (freq >= 1).all() and (cum.astype(np.int64) + freq <= T).all()
-    # integer outputs agree except where fp32 rounding moves a floor boundary
-    assert np.mean(freq == np.array(ref["freq"])) > 0.97
+    # integer outputs agree up to fp32 rounding of p (1e-4 relative) and the
+    # residual, which moves with sum(c) by at most V counts
+    rf = np.array(ref["freq"], dtype=np.int64)
+    assert (np.abs(freq.astype(np.int64) - rf) <= 1e-4 * rf + V).all()
     ideal_gpu = -np.log2(freq / T).sum()
     ideal_ref = -np.log2(np.array(ref["freq"]) / T).sum()
     assert abs(ideal_gpu - ideal_ref) <= 0.005 * ideal_ref + 1
