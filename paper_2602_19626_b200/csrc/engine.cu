@@ -2,6 +2,8 @@
 // one-row-per-chunk decode-step driver (decompress), host WNC + NC05 assembly.
 #include <algorithm>
 #include <cmath>
+#include <map>
+#include <mutex>
 #include <thread>
 
 #include "engine.hpp"
@@ -19,22 +21,63 @@ static void *g_ctx = nullptr;
 void set_allocator(void *(*a)(size_t, void *), void (*f)(void *, void *), void *ctx) {
   g_alloc = a; g_free = f; g_ctx = ctx;
 }
+// Default device allocator: a grow-only caching pool over cudaMalloc.  Every
+// call allocates the same buffer sizes, so after the first call nothing is
+// mapped or unmapped again (cudaMallocAsync with a zero release threshold
+// re-mapped GBs of slab buffers per call).  Blocks are returned after the
+// owning call has synchronised its stream.
+struct DevCache {
+  std::mutex mu;
+  std::multimap<size_t, void *> free_;
+  std::map<void *, size_t> size_;
+};
+static DevCache &cache() {
+  static DevCache c;
+  return c;
+}
 void *dev_alloc(size_t bytes, cudaStream_t s) {
+  (void)s;
   if (bytes == 0) bytes = 16;
+  bytes = (bytes + 255) & ~size_t(255);
   void *p = nullptr;
   if (g_alloc) {
     p = g_alloc(bytes, g_ctx);
     if (!p) fail(NC_ERR_NOMEM, "device allocation failed (hook)");
-  } else {
-    cudaError_t e = cudaMallocAsync(&p, bytes, s);
-    if (e != cudaSuccess) fail(NC_ERR_NOMEM, std::string("cudaMallocAsync: ") + cudaGetErrorString(e));
+    return p;
   }
+  DevCache &c = cache();
+  {
+    std::lock_guard<std::mutex> lk(c.mu);
+    auto it = c.free_.lower_bound(bytes);
+    if (it != c.free_.end() && it->first <= 2 * bytes) {
+      p = it->second;
+      c.free_.erase(it);
+      return p;
+    }
+  }
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    // release cached blocks and retry once
+    std::lock_guard<std::mutex> lk(c.mu);
+    for (auto &kv : c.free_) { cudaFree(kv.second); c.size_.erase(kv.second); }
+    c.free_.clear();
+    e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) fail(NC_ERR_NOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  }
+  std::lock_guard<std::mutex> lk(c.mu);
+  c.size_[p] = bytes;
   return p;
 }
 void dev_free(void *p, cudaStream_t s) {
+  (void)s;
   if (!p) return;
-  if (g_free) g_free(p, g_ctx);
-  else cudaFreeAsync(p, s);
+  if (g_free) { g_free(p, g_ctx); return; }
+  DevCache &c = cache();
+  std::lock_guard<std::mutex> lk(c.mu);
+  auto it = c.size_.find(p);
+  if (it == c.size_.end()) return;
+  c.free_.insert({it->second, p});
 }
 
 Stats &stats() {
@@ -175,6 +218,7 @@ void model_load(nc_model *m, const std::string &path, int device) {
     for (size_t k = 0; k < d; ++k) buf[v * d + k] = E[v * d + k] * gf[k];
   m->E_head = up(buf);
   ensure_rope(m, 4096);
+  NC_CUDA(cudaStreamCreateWithFlags(&m->walk_stream, cudaStreamNonBlocking));
 }
 
 void model_free(nc_model *m) {
@@ -182,6 +226,8 @@ void model_free(nc_model *m) {
   for (void *p : m->owned) cudaFree(p);
   if (m->rope_cos) cudaFree(m->rope_cos);
   if (m->rope_sin) cudaFree(m->rope_sin);
+  if (m->walk_stream) cudaStreamDestroy(m->walk_stream);
+  m->walk_stream = nullptr;
   m->owned.clear();
 }
 
@@ -212,9 +258,9 @@ struct Forward {
   nc_model *m;
   cudaStream_t s;
   int Mmax = 0;
-  float *h, *rinv, *q, *o, *act, *logits;
+  float *h, *rinv, *q, *o, *act, *logits, *lbuf[2];
   KvRing ring{};
-  void alloc(Bag &bag, int Mmax_, int n_chunks, int ring_len) {
+  void alloc(Bag &bag, int Mmax_, int n_chunks, int ring_len, bool double_logits = false) {
     Mmax = Mmax_;
     const Shape &S = m->s;
     h = bag.get<float>((size_t)Mmax * S.d);
@@ -222,7 +268,8 @@ struct Forward {
     q = bag.get<float>((size_t)Mmax * S.H * S.dh);
     o = bag.get<float>((size_t)Mmax * S.H * S.dh);
     act = bag.get<float>((size_t)Mmax * S.d_ff);
-    logits = bag.get<float>((size_t)Mmax * S.V);
+    logits = lbuf[0] = bag.get<float>((size_t)Mmax * S.V);
+    lbuf[1] = double_logits ? bag.get<float>((size_t)Mmax * S.V) : lbuf[0];
     ring.n_layers = S.n_layers;
     ring.ring = ring_len;
     ring.kv = S.KV;
@@ -373,8 +420,13 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
   if (n_chunks == 0 || max_n == 0) return;
   if (S.V >= (1u << p.cdf_bits)) fail(NC_ERR_INVALID, "T = 2^cdf_bits must exceed V");
 
+  // Slab rows per chunk: at most max_slab_rows over all chunks, and small enough
+  // that there are >= kPipeSlabs slabs, so the walk of slab s overlaps the
+  // forward of slab s+1 (the walk runs on its own stream, logits double-buffered).
+  const int kPipeSlabs = 4;
   int per_chunk = std::max(128, (int)(p.max_slab_rows / n_chunks) / 128 * 128);
-  const int R = std::min<int>(((max_n + 127) / 128) * 128, per_chunk);
+  int want = (int)((max_n + kPipeSlabs - 1) / kPipeSlabs);
+  const int R = std::max(128, std::min<int>(((want + 127) / 128) * 128, per_chunk));
   const int n_slabs = (int)((max_n + R - 1) / R);
   const int ring_len = (int)p.window + R;
   const int M = n_chunks * R;
@@ -382,7 +434,7 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
 
   Bag bag(s);
   Forward fw{m, s};
-  fw.alloc(bag, M, n_chunks, ring_len);
+  fw.alloc(bag, M, n_chunks, ring_len, n_slabs > 1);
   std::vector<uint32_t> ntok_v(ntok);
   uint32_t *ntok_d = bag.upload(ntok_v);
   int64_t *tok_off_d = bag.upload(tok_off);
@@ -415,23 +467,28 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
   uint32_t *cum_d = bag.get<uint32_t>(total), *freq_d = bag.get<uint32_t>(total);
   float *p_d = p.debug_dump ? bag.get<float>(total) : nullptr;
 
-  std::vector<cudaEvent_t> ev(3 * n_slabs + 1);
+  // events: per slab forward start/end (stream s), walk start/end (walk stream)
+  cudaStream_t ws = m->walk_stream;
+  std::vector<cudaEvent_t> ev(4 * n_slabs);
   for (auto &e : ev) NC_CUDA(cudaEventCreate(&e));
   for (int sl = 0; sl < n_slabs; ++sl) {
-    NC_CUDA(cudaEventRecord(ev[3 * sl], s));
+    if (sl >= 2) NC_CUDA(cudaStreamWaitEvent(s, ev[4 * (sl - 2) + 3], 0));   // logits buffer free again
+    fw.logits = fw.lbuf[sl & 1];
+    NC_CUDA(cudaEventRecord(ev[4 * sl], s));
     PROF(K_MISC, 0, (slab_rows_kernel<<<(M + 255) / 256, 256, 0, s>>>(tokens_dev, tok_off_d, ntok_d, R, sl, M, S.bos,
                                                                       xs, rchunk, rpos)));
     st.launches++;
     RowMeta rows{xs, rchunk, rpos};
-    double valid = 0, ctx = 0, walk_tok = 0;
+    double valid = 0, ctx = 0;
     for (int c = 0; c < n_chunks; ++c) {
       int64_t a0 = (int64_t)sl * R, a1 = std::min<int64_t>((int64_t)(sl + 1) * R, ntok[c]);
       if (a1 > a0) { valid += (double)(a1 - a0); ctx += ctx_sum(a0, a1, p.window, p.slide); }
     }
-    walk_tok = valid;
     fw.run(M, valid, 4.0 * S.H * S.dh * ctx, rows, tiles_d + tile_off[sl], tile_off[sl + 1] - tile_off[sl], p,
-           ev[3 * sl + 1]);
-    NC_CUDA(cudaEventRecord(ev[3 * sl + 2], s));
+           nullptr);
+    NC_CUDA(cudaEventRecord(ev[4 * sl + 1], s));
+    NC_CUDA(cudaStreamWaitEvent(ws, ev[4 * sl + 1], 0));
+    NC_CUDA(cudaEventRecord(ev[4 * sl + 2], ws));
     WalkArgs wa{};
     wa.chunk_of = wc_d + w_off[sl]; wa.row0 = wr_d + w_off[sl]; wa.count = wn_d + w_off[sl];
     wa.n_entries = w_off[sl + 1] - w_off[sl];
@@ -440,11 +497,14 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
     wa.out_cum = cum_d; wa.out_freq = freq_d; wa.out_p = p_d;
     wa.mode = 0;
     wb.fill(wa, p, S.V);
-    PROF(K_WALK, 4.0 * S.V * walk_tok, launch_walk(wa, s));
+    prof().begin(K_WALK, 4.0 * S.V * valid, ws);
+    launch_walk(wa, ws);
+    prof().end(ws);
+    NC_CUDA(cudaEventRecord(ev[4 * sl + 3], ws));
     st.launches++;
     NC_CUDA(cudaGetLastError());
   }
-  NC_CUDA(cudaEventRecord(ev[3 * n_slabs], s));
+  NC_CUDA(cudaStreamWaitEvent(s, ev[4 * (n_slabs - 1) + 3], 0));
   NC_CUDA(cudaMemcpyAsync(out.cum.data(), cum_d, total * 4, cudaMemcpyDeviceToHost, s));
   NC_CUDA(cudaMemcpyAsync(out.freq.data(), freq_d, total * 4, cudaMemcpyDeviceToHost, s));
   if (p_d) NC_CUDA(cudaMemcpyAsync(out.p_true.data(), p_d, total * 4, cudaMemcpyDeviceToHost, s));
@@ -454,13 +514,11 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
   if (prof().on) prof().collect();
   for (int c = 0; c < n_chunks; ++c) out.err[c] = hs[c].err;
   for (int sl = 0; sl < n_slabs; ++sl) {
-    float a, b, c;
-    cudaEventElapsedTime(&a, ev[3 * sl], ev[3 * sl + 1]);
-    cudaEventElapsedTime(&b, ev[3 * sl + 1], ev[3 * sl + 2]);
-    cudaEventElapsedTime(&c, ev[3 * sl + 2], ev[3 * sl + 3]);
-    st.forward_ms += a + b;
-    st.head_ms += b;
-    st.walk_ms += c;
+    float a = 0, b = 0;
+    cudaEventElapsedTime(&a, ev[4 * sl], ev[4 * sl + 1]);
+    cudaEventElapsedTime(&b, ev[4 * sl + 2], ev[4 * sl + 3]);
+    st.forward_ms += a;
+    st.walk_ms += b;
   }
   for (auto &e : ev) cudaEventDestroy(e);
 }

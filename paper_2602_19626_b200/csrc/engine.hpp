@@ -19,6 +19,7 @@ struct nc_model {
   float *rope_cos = nullptr, *rope_sin = nullptr;        // [rope_len, 32]
   int rope_len = 0;
   std::vector<void *> owned;                             // cudaFree on destruction
+  cudaStream_t walk_stream = nullptr;                    // the walk runs beside the next slab's forward
 };
 
 namespace nc {

@@ -81,18 +81,26 @@ __device__ __forceinline__ uint32_t quant(float p, double TmV) {
   return q < 1.0 ? 1u : (uint32_t)q;
 }
 
+// Thread t owns the float4 groups g = t, t + WT, t + 2 WT, ... of the vocab row
+// (coalesced 128-bit loads of z, 2 x 128-bit loads of the f64 bias).
+struct Grp {
+  float pt[4], png[4], p[4];
+};
+
 __global__ __launch_bounds__(WT, 1) void walk_kernel(WalkArgs a) {
-  extern __shared__ uint32_t bitmap[];  // V/32 words: token ids with N-gram fixups this step
+  extern __shared__ uint32_t dyn[];
+  const uint32_t V = a.V;
+  const int G = (int)(V / 4);
+  uint32_t *bitmap = dyn;                              // V/32 words: ids with N-gram fixups
+  uint32_t *gsum = dyn + (V + 31) / 32;                // decode: per-group counts (G words)
   __shared__ WalkSmem sm;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int e = blockIdx.x;
   if (e >= a.n_entries) return;
   const int c = a.chunk_of[e];
   const int row0 = a.row0[e], count = a.count[e];
+  if (count <= 0) return;
   WalkState *st = a.st + c;
-  const uint32_t V = a.V;
-  const int ept = (int)((V + WT - 1) / WT);
-  const int v0 = min((int)V, tid * ept), v1 = min((int)V, v0 + ept);
   double *b = a.b + (size_t)c * V;
   uint32_t *cu = a.cu + (size_t)c * V;
   float *spadd = a.spadd + (size_t)c * V;
@@ -183,14 +191,31 @@ __global__ __launch_bounds__(WT, 1) void walk_kernel(WalkArgs a) {
     }
     __syncthreads();
 
-    // ---------------- pass 1: max and sum of exp (per-thread online, fixed tree) ----
     const float inv_tau = a.inv_tau;
+    auto load_u = [&](int g, float u[4]) {
+      const float4 z4 = reinterpret_cast<const float4 *>(z)[g];
+      if (use_head) {
+        const double2 b01 = reinterpret_cast<const double2 *>(b)[2 * g];
+        const double2 b23 = reinterpret_cast<const double2 *>(b)[2 * g + 1];
+        u[0] = walk_u(z4.x, b01.x, inv_tau); u[1] = walk_u(z4.y, b01.y, inv_tau);
+        u[2] = walk_u(z4.z, b23.x, inv_tau); u[3] = walk_u(z4.w, b23.y, inv_tau);
+      } else {
+        u[0] = walk_u(z4.x, 0.0, inv_tau); u[1] = walk_u(z4.y, 0.0, inv_tau);
+        u[2] = walk_u(z4.z, 0.0, inv_tau); u[3] = walk_u(z4.w, 0.0, inv_tau);
+      }
+    };
+
+    // ---------------- pass 1: max and sum of exp (per-thread online, fixed tree) ----
     {
       float tm = -CUDART_INF_F, ts = 0.f;
-      for (int v = v0; v < v1; ++v) {
-        const float u = walk_u(z[v], use_head ? b[v] : 0.0, inv_tau);
-        if (u > tm) { ts = __fmaf_rn(ts, expf(__fsub_rn(tm, u)), 1.f); tm = u; }
-        else ts = __fadd_rn(ts, expf(__fsub_rn(u, tm)));
+      for (int g = tid; g < G; g += WT) {
+        float u[4];
+        load_u(g, u);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (u[j] > tm) { ts = __fmaf_rn(ts, expf(__fsub_rn(tm, u[j])), 1.f); tm = u[j]; }
+          else ts = __fadd_rn(ts, expf(__fsub_rn(u[j], tm)));
+        }
       }
 #pragma unroll
       for (int o = 16; o; o >>= 1) {
@@ -214,37 +239,65 @@ __global__ __launch_bounds__(WT, 1) void walk_kernel(WalkArgs a) {
           ts = __fadd_rn(__fmul_rn(ts, e1), __fmul_rn(os, e2));
           tm = mm;
         }
-        if (lane == 0) { sm.M = tm; sm.S = ts; }
+        if (lane == 0) { sm.M = tm; sm.S = __frcp_rn(ts); }
       }
       __syncthreads();
     }
-    const float M = sm.M, S = sm.S, a0f = sm.a0f, wl = sm.wl, wn = sm.wn;
+    const float M = sm.M, invS = sm.S, a0f = sm.a0f, wl = sm.wl, wn = sm.wn;
     const int mix = sm.mix, tok = sm.tok;
 
-    // p_v for this token (identical code for every pass that needs it)
-    auto prob = [&](int v, float &pt, float &png) -> float {
-      const float u = walk_u(z[v], use_head ? b[v] : 0.0, inv_tau);
-      pt = __fdiv_rn(expf(__fsub_rn(u, M)), S);
-      if (!mix) { png = 0.f; return pt; }
-      const float sp = (bitmap[v >> 5] >> (v & 31)) & 1u ? spadd[v] : 0.f;
-      png = __fmaf_rn(a0f, (float)(cu[v] + 1u), sp);
-      return __fmaf_rn(wl, pt, __fmul_rn(wn, png));
+    // p for the 4 ids of group g (identical code in every pass that needs it)
+    auto prob4 = [&](int g, Grp &q) {
+      float u[4];
+      load_u(g, u);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) q.pt[j] = __fmul_rn(expf(__fsub_rn(u[j], M)), invS);
+      if (!mix) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) { q.png[j] = 0.f; q.p[j] = q.pt[j]; }
+        return;
+      }
+      const uint4 c4 = reinterpret_cast<const uint4 *>(cu)[g];
+      const uint32_t cc[4] = {c4.x, c4.y, c4.z, c4.w};
+      const uint32_t bits = (bitmap[g >> 3] >> ((g & 7) * 4)) & 15u;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float sp = (bits >> j) & 1u ? spadd[4 * g + j] : 0.f;
+        q.png[j] = __fmaf_rn(a0f, (float)(cc[j] + 1u), sp);
+        q.p[j] = __fmaf_rn(wl, q.pt[j], __fmul_rn(wn, q.png[j]));
+      }
     };
 
     // ---------------- pass 2: p, counts, sums, argmax (+ b update when t is known) ----
     unsigned long long my_sum = 0, my_cum = 0;
     float bv = -1.f; int bi = 0x7fffffff; uint32_t bc = 0;
-    for (int v = v0; v < v1; ++v) {
-      float pt, png;
-      const float p = prob(v, pt, png);
-      const uint32_t cv = quant(p, TmV);
-      my_sum += cv;
-      if (p > bv) { bv = p; bi = v; bc = cv; }
-      if (a.mode == 0) {
-        if (v < tok) my_cum += cv;
-        if (v == tok) { sm.pt_t = pt; sm.png_t = png; sm.p_t = p; sm.freq_t = cv; }
+    for (int g = tid; g < G; g += WT) {
+      Grp q;
+      prob4(g, q);
+      uint32_t gs = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int v = 4 * g + j;
+        const uint32_t cv = quant(q.p[j], TmV);
+        gs += cv;
+        if (q.p[j] > bv) { bv = q.p[j]; bi = v; bc = cv; }
+        if (a.mode == 0) {
+          if (v < tok) my_cum += cv;
+          if (v == tok) { sm.pt_t = q.pt[j]; sm.png_t = q.png[j]; sm.p_t = q.p[j]; sm.freq_t = cv; }
+        }
       }
-      if (a.mode == 0 && use_head) b[v] = b_step(b[v], pt, v == tok, a.alpha);
+      my_sum += gs;
+      if (a.mode == 1) gsum[g] = gs;
+      if (a.mode == 0 && use_head) {
+        double2 *bp = reinterpret_cast<double2 *>(b) + 2 * g;
+        double2 b01 = bp[0], b23 = bp[1];
+        const int v = 4 * g;
+        b01.x = b_step(b01.x, q.pt[0], v == tok, a.alpha);
+        b01.y = b_step(b01.y, q.pt[1], v + 1 == tok, a.alpha);
+        b23.x = b_step(b23.x, q.pt[2], v + 2 == tok, a.alpha);
+        b23.y = b_step(b23.y, q.pt[3], v + 3 == tok, a.alpha);
+        bp[0] = b01; bp[1] = b23;
+      }
     }
     {
       unsigned long long s1 = my_sum, s2 = my_cum;
@@ -279,6 +332,8 @@ __global__ __launch_bounds__(WT, 1) void walk_kernel(WalkArgs a) {
           if (a.mode == 0) {
             sm.cum_t = s2 + (i_ < tok ? R : 0);
             sm.freq_t = sm.freq_t + (i_ == tok ? R : 0);
+          } else {
+            gsum[i_ >> 2] = (uint32_t)((long long)gsum[i_ >> 2] + R);
           }
         }
       }
@@ -286,10 +341,13 @@ __global__ __launch_bounds__(WT, 1) void walk_kernel(WalkArgs a) {
     }
 
     if (a.mode == 1) {
-      // ---------------- decode: prefix scan of per-thread counts, search the target ----
+      // ---------------- decode: prefix scan over the groups (in id order), search the target ----
       const long long R = sm.resid;
       const int am = sm.argmax;
-      const uint32_t adj = (uint32_t)((long long)my_sum + ((am >= v0 && am < v1) ? R : 0));
+      const int gpt = (G + WT - 1) / WT;
+      const int g0 = min(G, tid * gpt), g1 = min(G, g0 + gpt);
+      uint32_t adj = 0;
+      for (int g = g0; g < g1; ++g) adj += gsum[g];
       uint32_t x = adj;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -312,13 +370,20 @@ __global__ __launch_bounds__(WT, 1) void walk_kernel(WalkArgs a) {
       const unsigned long long tgt = sm.target;
       if (adj > 0 && tgt >= excl && tgt < excl + adj) {
         unsigned long long accm = excl;
-        for (int v = v0; v < v1; ++v) {
-          float pt, png;
-          const float p = prob(v, pt, png);
-          unsigned long long cv = quant(p, TmV);
+        int gf = g0;
+        for (; gf < g1; ++gf) {
+          if (tgt < accm + gsum[gf]) break;
+          accm += gsum[gf];
+        }
+        Grp q;
+        prob4(gf, q);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int v = 4 * gf + j;
+          unsigned long long cv = quant(q.p[j], TmV);
           if (v == am) cv = (unsigned long long)((long long)cv + R);
           if (tgt < accm + cv) {
-            sm.tok = v; sm.cum_t = accm; sm.freq_t = cv; sm.pt_t = pt; sm.png_t = png; sm.p_t = p;
+            sm.tok = v; sm.cum_t = accm; sm.freq_t = cv; sm.pt_t = q.pt[j]; sm.png_t = q.png[j]; sm.p_t = q.p[j];
             break;
           }
           accm += cv;
@@ -329,10 +394,17 @@ __global__ __launch_bounds__(WT, 1) void walk_kernel(WalkArgs a) {
       // ---------------- decode: bias update now that t is known ----
       const int t = sm.tok;
       if (use_head)
-        for (int v = v0; v < v1; ++v) {
-          float pt, png;
-          (void)prob(v, pt, png);
-          b[v] = b_step(b[v], pt, v == t, a.alpha);
+        for (int g = tid; g < G; g += WT) {
+          Grp q;
+          prob4(g, q);
+          double2 *bp = reinterpret_cast<double2 *>(b) + 2 * g;
+          double2 b01 = bp[0], b23 = bp[1];
+          const int v = 4 * g;
+          b01.x = b_step(b01.x, q.pt[0], v == t, a.alpha);
+          b01.y = b_step(b01.y, q.pt[1], v + 1 == t, a.alpha);
+          b23.x = b_step(b23.x, q.pt[2], v + 2 == t, a.alpha);
+          b23.y = b_step(b23.y, q.pt[3], v + 3 == t, a.alpha);
+          bp[0] = b01; bp[1] = b23;
         }
     }
 
@@ -450,10 +522,10 @@ __global__ __launch_bounds__(WT, 1) void walk_kernel(WalkArgs a) {
 
 void launch_walk(const WalkArgs &a, cudaStream_t s) {
   if (a.n_entries <= 0) return;
-  const size_t dyn = ((a.V + 31) / 32) * sizeof(uint32_t);
+  const size_t dyn = ((a.V + 31) / 32 + a.V / 4) * sizeof(uint32_t);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
   walk_kernel<<<a.n_entries, WT, dyn, s>>>(a);
