@@ -177,6 +177,11 @@ nc_status nc_debug_walk(int device, const float *logits, const uint32_t *tok, ui
 nc_status nc_debug_forward(nc_model *m, const uint32_t *x, uint32_t rows, const nc_params *p,
                            int mode, float *logits_out);
 
+/* One GEMM out[M,N] = A[M,K] B[N,K]^T (host fp32 arrays) through the forward's
+ * GEMM kernel: mode 0 = tcgen05 3xTF32 (TMA + TMEM), 1 = SIMT fp32.  K % 32 == 0. */
+nc_status nc_debug_gemm(int device, const float *A, const float *B, uint32_t M, uint32_t N, uint32_t K, int mode,
+                        float *out);
+
 /* Host-side pieces exported for CPU tests of the host logic (no GPU needed). */
 nc_status nc_host_split(const uint8_t *in, size_t n, uint32_t n_chunks, uint64_t *cuts,
                         uint32_t *n_cuts); /* cuts: n_chunks+1 capacity, chunk i = [cuts[i], cuts[i+1]) */

@@ -21,7 +21,7 @@ EXPORTS = [
     "nc_comm_init", "nc_comm_free", "nc_compress_shard", "nc_decompress_shard", "nc_free",
     "nc_last_error", "nc_last_stats", "nc_debug_quantize", "nc_debug_walk", "nc_debug_forward",
     "nc_host_split", "nc_host_wnc_encode", "nc_host_tokenize_vocab", "nc_host_shard_range",
-    "nc_host_shard_part", "nc_set_profiling", "nc_profile",
+    "nc_host_shard_part", "nc_set_profiling", "nc_profile", "nc_debug_gemm",
 ]
 
 
@@ -75,6 +75,7 @@ def lib():
             "nc_debug_walk": (C.c_int, [C.c_int, f32p, u32p, C.c_uint32, C.c_uint32, C.POINTER(nc_params),
                                         u32p, u32p, f32p]),
             "nc_debug_forward": (C.c_int, [P, u32p, C.c_uint32, C.POINTER(nc_params), C.c_int, f32p]),
+            "nc_debug_gemm": (C.c_int, [C.c_int, f32p, f32p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int, f32p]),
             "nc_host_split": (C.c_int, [P, C.c_size_t, C.c_uint32, u64p, u32p]),
             "nc_host_wnc_encode": (C.c_int, [u32p, u32p, C.c_size_t, C.c_uint32, pp, szp, u64p]),
             "nc_host_tokenize_vocab": (C.c_int, [P, u32p, C.c_uint32, C.c_uint32, P, C.c_size_t, pp, szp]),
@@ -226,6 +227,17 @@ def nc_debug_forward(model: Model, x, params: nc_params, mode: int = 0):
     out = np.zeros((len(xv), model.vocab), np.float32)
     _check(lib().nc_debug_forward(model.h, xp, len(xv), C.byref(params), mode,
                                   out.ctypes.data_as(C.POINTER(C.c_float))))
+    return out
+
+
+def nc_debug_gemm(A, B, mode: int = 0, device: int = 0):
+    """out = A @ B.T through the forward's GEMM (mode 0 tcgen05 3xTF32, 1 SIMT fp32)."""
+    a, ap = _f32(A)
+    b, bp = _f32(B)
+    M, K = a.shape
+    N = b.shape[0]
+    out = np.zeros((M, N), np.float32)
+    _check(lib().nc_debug_gemm(device, ap, bp, M, N, K, mode, out.ctypes.data_as(C.POINTER(C.c_float))))
     return out
 
 

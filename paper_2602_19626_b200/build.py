@@ -14,7 +14,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
          "--expt-relaxed-constexpr", f"-I{PKG.parent / 'include'}"]
-SOURCES = ["host_runtime.cpp", "api.cpp", "comm.cpp", "engine.cu", "k_forward_simt.cu", "k_walk.cu"]
+SOURCES = ["host_runtime.cpp", "api.cpp", "comm.cpp", "engine.cu", "k_forward_simt.cu", "k_walk.cu",
+           "k_gemm_tc.cu"]
 
 
 def _stale(obj: Path, src: Path) -> bool:

@@ -282,6 +282,15 @@ nc_status nc_debug_forward(nc_model *m, const uint32_t *x, uint32_t rows, const 
   });
 }
 
+nc_status nc_debug_gemm(int device, const float *A, const float *B, uint32_t M, uint32_t N, uint32_t K, int mode,
+                        float *out) {
+  if (!A || !B || !out || !M || !N || !K) return set_err(NC_ERR_INVALID, "null argument");
+  return guard([&] {
+    require_device();
+    nc::debug_gemm(device, A, B, M, N, K, mode, out);
+  });
+}
+
 // ----------------------------------------------------------- host pieces ---
 nc_status nc_host_split(const uint8_t *in, size_t n, uint32_t n_chunks, uint64_t *cuts, uint32_t *n_cuts) {
   if ((!in && n) || !cuts || !n_cuts) return set_err(NC_ERR_INVALID, "null argument");

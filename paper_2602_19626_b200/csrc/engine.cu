@@ -2,11 +2,13 @@
 // one-row-per-chunk decode-step driver (decompress), host WNC + NC05 assembly.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <thread>
 
 #include "engine.hpp"
+#include "gemm_tc.cuh"
 
 namespace nc {
 
@@ -217,6 +219,27 @@ void model_load(nc_model *m, const std::string &path, int device) {
   for (size_t v = 0; v < V; ++v)
     for (size_t k = 0; k < d; ++k) buf[v * d + k] = E[v * d + k] * gf[k];
   m->E_head = up(buf);
+  // tf32 planes for the tensor-core path (split on device: same code as the activations)
+  auto planes = [&](const float *src, size_t n, float *&hi, float *&lo) {
+    NC_CUDA(cudaMalloc(&hi, n * 4));
+    NC_CUDA(cudaMalloc(&lo, n * 4));
+    m->owned.push_back(hi);
+    m->owned.push_back(lo);
+    launch_split_planes(src, hi, lo, n, nullptr);
+  };
+  planes(m->E_head, V * d, m->E_head_hi, m->E_head_lo);
+  m->wqkv_hi.resize(s.n_layers); m->wqkv_lo.resize(s.n_layers); m->wo_hi.resize(s.n_layers);
+  m->wo_lo.resize(s.n_layers); m->wgu_hi.resize(s.n_layers); m->wgu_lo.resize(s.n_layers);
+  m->wd_hi.resize(s.n_layers); m->wd_lo.resize(s.n_layers);
+  for (uint32_t l = 0; l < s.n_layers; ++l) {
+    planes(m->wqkv[l], (qd + 2 * kvd) * d, m->wqkv_hi[l], m->wqkv_lo[l]);
+    planes(m->wo[l], d * qd, m->wo_hi[l], m->wo_lo[l]);
+    planes(m->wgu[l], 2 * ff * d, m->wgu_hi[l], m->wgu_lo[l]);
+    planes(m->wd[l], d * ff, m->wd_hi[l], m->wd_lo[l]);
+  }
+  NC_CUDA(cudaDeviceSynchronize());
+  const char *g = std::getenv("NC_GEMM");
+  m->use_tc = !(g && std::string(g) == "simt");
   ensure_rope(m, 4096);
   NC_CUDA(cudaStreamCreateWithFlags(&m->walk_stream, cudaStreamNonBlocking));
 }
@@ -259,6 +282,7 @@ struct Forward {
   cudaStream_t s;
   int Mmax = 0;
   float *h, *rinv, *q, *o, *act, *logits, *lbuf[2];
+  float *h_hi, *h_lo, *o_hi, *o_lo, *act_hi, *act_lo;   // tf32 planes (tensor-core GEMM operands)
   KvRing ring{};
   void alloc(Bag &bag, int Mmax_, int n_chunks, int ring_len, bool double_logits = false) {
     Mmax = Mmax_;
@@ -268,6 +292,12 @@ struct Forward {
     q = bag.get<float>((size_t)Mmax * S.H * S.dh);
     o = bag.get<float>((size_t)Mmax * S.H * S.dh);
     act = bag.get<float>((size_t)Mmax * S.d_ff);
+    h_hi = bag.get<float>((size_t)Mmax * S.d);
+    h_lo = bag.get<float>((size_t)Mmax * S.d);
+    o_hi = bag.get<float>((size_t)Mmax * S.H * S.dh);
+    o_lo = bag.get<float>((size_t)Mmax * S.H * S.dh);
+    act_hi = bag.get<float>((size_t)Mmax * S.d_ff);
+    act_lo = bag.get<float>((size_t)Mmax * S.d_ff);
     logits = lbuf[0] = bag.get<float>((size_t)Mmax * S.V);
     lbuf[1] = double_logits ? bag.get<float>((size_t)Mmax * S.V) : lbuf[0];
     ring.n_layers = S.n_layers;
@@ -286,39 +316,76 @@ struct Forward {
     Stats &st = stats();
     const int qd = S.H * S.dh, kvd = S.KV * S.dh;
     const double d = S.d;
-    PROF(K_EMBED, 4.0 * d * valid, launch_embed(rows.x, M, m->E, S.d, h, s));
+    const bool tcm = m->use_tc;
+    PROF(K_EMBED, 4.0 * d * valid, launch_embed(rows.x, M, m->E, S.d, h, tcm ? h_hi : nullptr, tcm ? h_lo : nullptr, s));
     st.launches++;
     for (uint32_t l = 0; l < S.n_layers; ++l) {
       PROF(K_RMS, 4.0 * d * valid, launch_rms(h, M, S.d, (float)S.eps, rinv, s));
-      GemmArgs g{};
-      g.A = h; g.lda = S.d; g.B = m->wqkv[l]; g.ldb = S.d; g.M = M; g.N = qd + 2 * kvd; g.K = S.d;
-      g.rinv = rinv; g.C = q; g.ldc = qd; g.layer = (int)l; g.n_q_cols = qd; g.n_kv_cols = kvd;
-      g.rows = rows; g.ring = ring; g.rope_cos = m->rope_cos; g.rope_sin = m->rope_sin;
-      PROF(K_QKV, 2.0 * valid * (qd + 2 * kvd) * d, launch_gemm(EPI_QKV, g, s));
+      // RMSNorm + QKV + RoPE + KV-ring scatter
+      if (tcm) {
+        TcGemmArgs g{};
+        g.M = M; g.N = qd + 2 * kvd; g.K = S.d; g.rinv = rinv; g.C = q; g.ldc = qd;
+        g.layer = (int)l; g.n_q_cols = qd; g.n_kv_cols = kvd; g.rows = rows; g.ring = ring;
+        g.rope_cos = m->rope_cos; g.rope_sin = m->rope_sin;
+        TcOperands op{h_hi, h_lo, (uint64_t)Mmax, m->wqkv_hi[l], m->wqkv_lo[l]};
+        PROF(K_QKV, 2.0 * valid * (qd + 2 * kvd) * d, launch_gemm_tc(EPI_QKV, g, op, s));
+      } else {
+        GemmArgs g{};
+        g.A = h; g.lda = S.d; g.B = m->wqkv[l]; g.ldb = S.d; g.M = M; g.N = qd + 2 * kvd; g.K = S.d;
+        g.rinv = rinv; g.C = q; g.ldc = qd; g.layer = (int)l; g.n_q_cols = qd; g.n_kv_cols = kvd;
+        g.rows = rows; g.ring = ring; g.rope_cos = m->rope_cos; g.rope_sin = m->rope_sin;
+        PROF(K_QKV, 2.0 * valid * (qd + 2 * kvd) * d, launch_gemm(EPI_QKV, g, s));
+      }
       AttnArgs at{};
       at.tiles = tiles; at.n_tiles = n_tiles; at.q = q; at.o = o; at.ldq = qd; at.ring = ring; at.layer = (int)l;
       at.H = S.H; at.KV = S.KV; at.window = (int)p.window; at.slide = (int)p.slide;
+      at.o_hi = tcm ? o_hi : nullptr; at.o_lo = tcm ? o_lo : nullptr;
       PROF(K_ATTN, attn_flops, launch_attention(at, s));
-      GemmArgs go{};
-      go.A = o; go.lda = qd; go.B = m->wo[l]; go.ldb = qd; go.M = M; go.N = S.d; go.K = qd; go.C = h; go.ldc = S.d;
-      PROF(K_OPROJ, 2.0 * valid * d * qd, launch_gemm(EPI_RESID, go, s));
+      if (tcm) {
+        TcGemmArgs g{};
+        g.M = M; g.N = S.d; g.K = qd; g.C = h; g.ldc = S.d; g.C_hi = h_hi; g.C_lo = h_lo;
+        TcOperands op{o_hi, o_lo, (uint64_t)Mmax, m->wo_hi[l], m->wo_lo[l]};
+        PROF(K_OPROJ, 2.0 * valid * d * qd, launch_gemm_tc(EPI_RESID, g, op, s));
+      } else {
+        GemmArgs go{};
+        go.A = o; go.lda = qd; go.B = m->wo[l]; go.ldb = qd; go.M = M; go.N = S.d; go.K = qd; go.C = h; go.ldc = S.d;
+        PROF(K_OPROJ, 2.0 * valid * d * qd, launch_gemm(EPI_RESID, go, s));
+      }
       PROF(K_RMS, 4.0 * d * valid, launch_rms(h, M, S.d, (float)S.eps, rinv, s));
-      GemmArgs gu{};
-      gu.A = h; gu.lda = S.d; gu.B = m->wgu[l]; gu.ldb = S.d; gu.M = M; gu.N = 2 * S.d_ff; gu.K = S.d;
-      gu.rinv = rinv; gu.C = act; gu.ldc = S.d_ff;
-      PROF(K_GATEUP, 2.0 * valid * 2 * S.d_ff * d, launch_gemm(EPI_SWIGLU, gu, s));
-      GemmArgs gd{};
-      gd.A = act; gd.lda = S.d_ff; gd.B = m->wd[l]; gd.ldb = S.d_ff; gd.M = M; gd.N = S.d; gd.K = S.d_ff;
-      gd.C = h; gd.ldc = S.d;
-      PROF(K_DOWN, 2.0 * valid * d * S.d_ff, launch_gemm(EPI_RESID, gd, s));
+      if (tcm) {
+        TcGemmArgs g{};
+        g.M = M; g.N = 2 * S.d_ff; g.K = S.d; g.rinv = rinv; g.C_hi = act_hi; g.C_lo = act_lo; g.ldc = S.d_ff;
+        TcOperands op{h_hi, h_lo, (uint64_t)Mmax, m->wgu_hi[l], m->wgu_lo[l]};
+        PROF(K_GATEUP, 2.0 * valid * 2 * S.d_ff * d, launch_gemm_tc(EPI_SWIGLU, g, op, s));
+        TcGemmArgs g2{};
+        g2.M = M; g2.N = S.d; g2.K = S.d_ff; g2.C = h; g2.ldc = S.d; g2.C_hi = h_hi; g2.C_lo = h_lo;
+        TcOperands op2{act_hi, act_lo, (uint64_t)Mmax, m->wd_hi[l], m->wd_lo[l]};
+        PROF(K_DOWN, 2.0 * valid * d * S.d_ff, launch_gemm_tc(EPI_RESID, g2, op2, s));
+      } else {
+        GemmArgs gu{};
+        gu.A = h; gu.lda = S.d; gu.B = m->wgu[l]; gu.ldb = S.d; gu.M = M; gu.N = 2 * S.d_ff; gu.K = S.d;
+        gu.rinv = rinv; gu.C = act; gu.ldc = S.d_ff;
+        PROF(K_GATEUP, 2.0 * valid * 2 * S.d_ff * d, launch_gemm(EPI_SWIGLU, gu, s));
+        GemmArgs gd{};
+        gd.A = act; gd.lda = S.d_ff; gd.B = m->wd[l]; gd.ldb = S.d_ff; gd.M = M; gd.N = S.d; gd.K = S.d_ff;
+        gd.C = h; gd.ldc = S.d;
+        PROF(K_DOWN, 2.0 * valid * d * S.d_ff, launch_gemm(EPI_RESID, gd, s));
+      }
       st.launches += 6;
     }
     if (ev_head) NC_CUDA(cudaEventRecord(ev_head, s));
     PROF(K_RMS, 4.0 * d * valid, launch_rms(h, M, S.d, (float)S.eps, rinv, s));
-    GemmArgs gh{};
-    gh.A = h; gh.lda = S.d; gh.B = m->E_head; gh.ldb = S.d; gh.M = M; gh.N = S.V; gh.K = S.d;
-    gh.rinv = rinv; gh.C = logits; gh.ldc = S.V;
-    PROF(K_HEAD, 2.0 * valid * S.V * d, launch_gemm(EPI_HEAD, gh, s));
+    if (tcm) {
+      TcGemmArgs g{};
+      g.M = M; g.N = S.V; g.K = S.d; g.rinv = rinv; g.C = logits; g.ldc = S.V;
+      TcOperands op{h_hi, h_lo, (uint64_t)Mmax, m->E_head_hi, m->E_head_lo};
+      PROF(K_HEAD, 2.0 * valid * S.V * d, launch_gemm_tc(EPI_HEAD, g, op, s));
+    } else {
+      GemmArgs gh{};
+      gh.A = h; gh.lda = S.d; gh.B = m->E_head; gh.ldb = S.d; gh.M = M; gh.N = S.V; gh.K = S.d;
+      gh.rinv = rinv; gh.C = logits; gh.ldc = S.V;
+      PROF(K_HEAD, 2.0 * valid * S.V * d, launch_gemm(EPI_HEAD, gh, s));
+    }
     st.launches += 2;
     NC_CUDA(cudaGetLastError());
   }
@@ -704,6 +771,35 @@ void debug_forward(nc_model *m, const uint32_t *x, uint32_t rows, const Params &
       NC_CUDA(cudaMemcpyAsync(out + (size_t)j * S.V, fw.logits, (size_t)S.V * 4, cudaMemcpyDeviceToHost, s));
     }
   }
+  NC_CUDA(cudaStreamSynchronize(s));
+}
+
+void debug_gemm(int device, const float *A, const float *B, uint32_t M, uint32_t N, uint32_t K, int mode,
+                float *out) {
+  NC_CUDA(cudaSetDevice(device));
+  if (K % 32 || N % 64) fail(NC_ERR_INVALID, "debug_gemm needs K % 32 == 0 and N % 64 == 0");
+  cudaStream_t s = nullptr;
+  Bag bag(s);
+  std::vector<float> a(A, A + (size_t)M * K), b(B, B + (size_t)N * K), ones(M, 1.f);
+  float *a_d = bag.upload(a), *b_d = bag.upload(b), *r_d = bag.upload(ones);
+  float *c_d = bag.get<float>((size_t)M * N);
+  if (mode == 0) {
+    float *ah = bag.get<float>((size_t)M * K), *al = bag.get<float>((size_t)M * K);
+    float *bh = bag.get<float>((size_t)N * K), *bl = bag.get<float>((size_t)N * K);
+    launch_split_planes(a_d, ah, al, (size_t)M * K, s);
+    launch_split_planes(b_d, bh, bl, (size_t)N * K, s);
+    TcGemmArgs g{};
+    g.M = (int)M; g.N = (int)N; g.K = (int)K; g.rinv = r_d; g.C = c_d; g.ldc = (int)N;
+    TcOperands op{ah, al, (uint64_t)M, bh, bl};
+    launch_gemm_tc(EPI_HEAD, g, op, s);
+  } else {
+    GemmArgs g{};
+    g.A = a_d; g.lda = (int)K; g.B = b_d; g.ldb = (int)K; g.M = (int)M; g.N = (int)N; g.K = (int)K;
+    g.rinv = r_d; g.C = c_d; g.ldc = (int)N;
+    launch_gemm(EPI_HEAD, g, s);
+  }
+  NC_CUDA(cudaGetLastError());
+  NC_CUDA(cudaMemcpyAsync(out, c_d, (size_t)M * N * 4, cudaMemcpyDeviceToHost, s));
   NC_CUDA(cudaStreamSynchronize(s));
 }
 

@@ -15,7 +15,11 @@ struct nc_model {
   nc::Tokenizer tok;
   std::vector<std::string> vocab;
   float *E = nullptr, *E_head = nullptr;                 // [V, d]
-  std::vector<float *> wqkv, wo, wgu, wd;                // per layer
+  std::vector<float *> wqkv, wo, wgu, wd;                // per layer, fp32 (SIMT path)
+  // tf32 hi/lo planes of every projection for the tcgen05 3xTF32 GEMM (D14)
+  float *E_head_hi = nullptr, *E_head_lo = nullptr;
+  std::vector<float *> wqkv_hi, wqkv_lo, wo_hi, wo_lo, wgu_hi, wgu_lo, wd_hi, wd_lo;
+  bool use_tc = true;                                    // NC_GEMM=simt selects the SIMT GEMMs
   float *rope_cos = nullptr, *rope_sin = nullptr;        // [rope_len, 32]
   int rope_len = 0;
   std::vector<void *> owned;                             // cudaFree on destruction
@@ -75,6 +79,8 @@ void decompress_device(nc_model *m, const uint8_t *blob, const Nc05View &view, c
 void encode_container(const Params &p, const std::vector<uint32_t> &ntok, const CompressOut &co,
                       std::vector<uint8_t> &out);
 // debug
+void debug_gemm(int device, const float *A, const float *B, uint32_t M, uint32_t N, uint32_t K, int mode,
+                float *out);
 void debug_forward(nc_model *m, const uint32_t *x, uint32_t rows, const Params &p, int mode, float *out);
 void debug_walk(int device, const float *logits, const uint32_t *tok, uint32_t n, uint32_t V,
                 const Params &p, uint32_t *cum, uint32_t *freq, float *p_true);

@@ -1,0 +1,30 @@
+// Host interface of the tcgen05 3xTF32 GEMM.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.cuh"
+
+namespace nc {
+
+struct TcGemmArgs {
+  int M, N, K;
+  const float *rinv;          // per-row RMSNorm scale (QKV, SWIGLU, HEAD)
+  float *C; int ldc;          // fp32 output: logits (HEAD), residual h in/out (RESID), q (QKV)
+  float *C_hi, *C_lo;         // tf32 planes written for the next GEMM (RESID: h, SWIGLU: act)
+  int layer, n_q_cols, n_kv_cols;
+  RowMeta rows; KvRing ring;
+  const float *rope_cos, *rope_sin;
+};
+
+struct TcOperands {
+  const float *A_hi, *A_lo;   // [a_rows >= M, K]
+  uint64_t a_rows;
+  const float *B_hi, *B_lo;   // [N, K]
+};
+
+void launch_gemm_tc(GemmEpi epi, const TcGemmArgs &a, const TcOperands &op, cudaStream_t s);
+void launch_split_planes(const float *x, float *hi, float *lo, size_t n, cudaStream_t s);
+
+}  // namespace nc

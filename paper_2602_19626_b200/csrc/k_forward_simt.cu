@@ -16,20 +16,32 @@
 #include <math_constants.h>
 
 #include "kernels.cuh"
+#include "tc_common.cuh"
 
 namespace nc {
 
 // ------------------------------------------------------------------ embed ---
 __global__ void embed_kernel(const uint32_t *__restrict__ x, int M, const float *__restrict__ E, int d,
-                             float *__restrict__ h) {
+                             float *__restrict__ h, float *__restrict__ h_hi, float *__restrict__ h_lo) {
   int m = blockIdx.x;
   if (m >= M) return;
   const float4 *src = reinterpret_cast<const float4 *>(E + (size_t)x[m] * d);
   float4 *dst = reinterpret_cast<float4 *>(h + (size_t)m * d);
-  for (int i = threadIdx.x; i < d / 4; i += blockDim.x) dst[i] = src[i];
+  for (int i = threadIdx.x; i < d / 4; i += blockDim.x) {
+    const float4 v = src[i];
+    dst[i] = v;
+    if (h_hi) {
+      float4 hi, lo;
+      tc::split_tf32(v.x, hi.x, lo.x); tc::split_tf32(v.y, hi.y, lo.y);
+      tc::split_tf32(v.z, hi.z, lo.z); tc::split_tf32(v.w, hi.w, lo.w);
+      reinterpret_cast<float4 *>(h_hi + (size_t)m * d)[i] = hi;
+      reinterpret_cast<float4 *>(h_lo + (size_t)m * d)[i] = lo;
+    }
+  }
 }
-void launch_embed(const uint32_t *x, int M, const float *E, int d, float *h, cudaStream_t s) {
-  if (M > 0) embed_kernel<<<M, 128, 0, s>>>(x, M, E, d, h);
+void launch_embed(const uint32_t *x, int M, const float *E, int d, float *h, float *h_hi, float *h_lo,
+                  cudaStream_t s) {
+  if (M > 0) embed_kernel<<<M, 128, 0, s>>>(x, M, E, d, h, h_hi, h_lo);
 }
 
 // -------------------------------------------------------------------- rms ---
@@ -266,11 +278,21 @@ __global__ __launch_bounds__(192) void attention_kernel(AttnArgs a) {
     }
   }
   if (valid) {
-    float4 *op = reinterpret_cast<float4 *>(a.o + (size_t)(t.qrow0 + r) * a.ldq + hq * 64);
+    const size_t ob = (size_t)(t.qrow0 + r) * a.ldq + hq * 64;
+    float4 *op = reinterpret_cast<float4 *>(a.o + ob);
 #pragma unroll
-    for (int i = 0; i < 16; ++i)
-      op[i] = make_float4(__fdiv_rn(acc[4 * i], l), __fdiv_rn(acc[4 * i + 1], l),
-                          __fdiv_rn(acc[4 * i + 2], l), __fdiv_rn(acc[4 * i + 3], l));
+    for (int i = 0; i < 16; ++i) {
+      const float4 v = make_float4(__fdiv_rn(acc[4 * i], l), __fdiv_rn(acc[4 * i + 1], l),
+                                   __fdiv_rn(acc[4 * i + 2], l), __fdiv_rn(acc[4 * i + 3], l));
+      op[i] = v;
+      if (a.o_hi) {
+        float4 hi, lo;
+        tc::split_tf32(v.x, hi.x, lo.x); tc::split_tf32(v.y, hi.y, lo.y);
+        tc::split_tf32(v.z, hi.z, lo.z); tc::split_tf32(v.w, hi.w, lo.w);
+        reinterpret_cast<float4 *>(a.o_hi + ob)[i] = hi;
+        reinterpret_cast<float4 *>(a.o_lo + ob)[i] = lo;
+      }
+    }
   }
 }
 

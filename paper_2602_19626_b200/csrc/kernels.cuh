@@ -24,7 +24,7 @@ struct KvRing {
 };
 
 // ---------------------------------------------------------------- launchers
-void launch_embed(const uint32_t *x, int M, const float *E, int d, float *h, cudaStream_t s);
+void launch_embed(const uint32_t *x, int M, const float *E, int d, float *h, float *h_hi, float *h_lo, cudaStream_t s);
 void launch_rms(const float *h, int M, int d, float eps, float *rinv, cudaStream_t s);
 
 enum GemmEpi { EPI_QKV = 0, EPI_RESID = 1, EPI_SWIGLU = 2, EPI_HEAD = 3 };
@@ -45,6 +45,7 @@ struct AttnTile { int chunk, p0, nrows, qrow0; };
 struct AttnArgs {
   const AttnTile *tiles; int n_tiles;
   const float *q; float *o; int ldq;   // [rows, H*64]
+  float *o_hi, *o_lo;                  // optional tf32 planes of o for the tensor-core O projection
   KvRing ring; int layer;
   int H, KV, window, slide;
 };
