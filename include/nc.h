@@ -182,6 +182,12 @@ nc_status nc_debug_forward(nc_model *m, const uint32_t *x, uint32_t rows, const 
 nc_status nc_debug_gemm(int device, const float *A, const float *B, uint32_t M, uint32_t N, uint32_t K, int mode,
                         float *out);
 
+/* One attention layer for ONE chunk: o[n, H*64] from q[n, H*64] (RoPE already
+ * applied), k, v [n, KV*64] (host fp32, positions 0..n-1), block-window mask
+ * (window, slide).  mode 0 = tensor-core kernel (3xTF32), 1 = SIMT fp32. */
+nc_status nc_debug_attention(int device, const float *q, const float *k, const float *v, uint32_t n, uint32_t H,
+                             uint32_t KV, uint32_t window, uint32_t slide, int mode, float *o);
+
 /* Host-side pieces exported for CPU tests of the host logic (no GPU needed). */
 nc_status nc_host_split(const uint8_t *in, size_t n, uint32_t n_chunks, uint64_t *cuts,
                         uint32_t *n_cuts); /* cuts: n_chunks+1 capacity, chunk i = [cuts[i], cuts[i+1]) */

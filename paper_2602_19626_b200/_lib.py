@@ -21,7 +21,7 @@ EXPORTS = [
     "nc_comm_init", "nc_comm_free", "nc_compress_shard", "nc_decompress_shard", "nc_free",
     "nc_last_error", "nc_last_stats", "nc_debug_quantize", "nc_debug_walk", "nc_debug_forward",
     "nc_host_split", "nc_host_wnc_encode", "nc_host_tokenize_vocab", "nc_host_shard_range",
-    "nc_host_shard_part", "nc_set_profiling", "nc_profile", "nc_debug_gemm",
+    "nc_host_shard_part", "nc_set_profiling", "nc_profile", "nc_debug_gemm", "nc_debug_attention",
 ]
 
 
@@ -75,6 +75,8 @@ def lib():
             "nc_debug_walk": (C.c_int, [C.c_int, f32p, u32p, C.c_uint32, C.c_uint32, C.POINTER(nc_params),
                                         u32p, u32p, f32p]),
             "nc_debug_forward": (C.c_int, [P, u32p, C.c_uint32, C.POINTER(nc_params), C.c_int, f32p]),
+            "nc_debug_attention": (C.c_int, [C.c_int, f32p, f32p, f32p, C.c_uint32, C.c_uint32, C.c_uint32,
+                                             C.c_uint32, C.c_uint32, C.c_int, f32p]),
             "nc_debug_gemm": (C.c_int, [C.c_int, f32p, f32p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int, f32p]),
             "nc_host_split": (C.c_int, [P, C.c_size_t, C.c_uint32, u64p, u32p]),
             "nc_host_wnc_encode": (C.c_int, [u32p, u32p, C.c_size_t, C.c_uint32, pp, szp, u64p]),
@@ -238,6 +240,18 @@ def nc_debug_gemm(A, B, mode: int = 0, device: int = 0):
     N = b.shape[0]
     out = np.zeros((M, N), np.float32)
     _check(lib().nc_debug_gemm(device, ap, bp, M, N, K, mode, out.ctypes.data_as(C.POINTER(C.c_float))))
+    return out
+
+
+def nc_debug_attention(q, k, v, H, KV, window, slide, mode=0, device=0):
+    """one attention layer of one chunk (q rotated): mode 0 tensor cores, 1 SIMT."""
+    qa, qp = _f32(q)
+    ka, kp = _f32(k)
+    va, vp = _f32(v)
+    n = qa.shape[0]
+    out = np.zeros((n, H * 64), np.float32)
+    _check(lib().nc_debug_attention(device, qp, kp, vp, n, H, KV, window, slide, mode,
+                                    out.ctypes.data_as(C.POINTER(C.c_float))))
     return out
 
 

@@ -15,7 +15,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
          "--expt-relaxed-constexpr", f"-I{PKG.parent / 'include'}"]
 SOURCES = ["host_runtime.cpp", "api.cpp", "comm.cpp", "engine.cu", "k_forward_simt.cu", "k_walk.cu",
-           "k_gemm_tc.cu"]
+           "k_gemm_tc.cu", "k_attn_tc.cu"]
 
 
 def _stale(obj: Path, src: Path) -> bool:

@@ -291,6 +291,16 @@ nc_status nc_debug_gemm(int device, const float *A, const float *B, uint32_t M, 
   });
 }
 
+nc_status nc_debug_attention(int device, const float *q, const float *k, const float *v, uint32_t n, uint32_t H,
+                             uint32_t KV, uint32_t window, uint32_t slide, int mode, float *o) {
+  if (!q || !k || !v || !o || !H || !KV || H % KV) return set_err(NC_ERR_INVALID, "bad argument");
+  return guard([&] {
+    require_device();
+    if (window % 128 || slide % 128 || slide >= window) nc::fail(NC_ERR_INVALID, "window/slide");
+    nc::debug_attention(device, q, k, v, n, H, KV, window, slide, mode, o);
+  });
+}
+
 // ----------------------------------------------------------- host pieces ---
 nc_status nc_host_split(const uint8_t *in, size_t n, uint32_t n_chunks, uint64_t *cuts, uint32_t *n_cuts) {
   if ((!in && n) || !cuts || !n_cuts) return set_err(NC_ERR_INVALID, "null argument");

@@ -1,0 +1,21 @@
+// Host interface of the tensor-core window attention.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "kernels.cuh"
+
+namespace nc {
+
+struct AttnTcArgs {
+  const AttnTile *tiles; int n_tiles;        // tiles of <= 128 consecutive rows of one chunk
+  const float *q_hi, *q_lo; int ldq; int q_rows;
+  const float *k_hi, *k_lo, *v_hi, *v_lo;    // ring planes [chunk][layer][ring][KV][64]
+  int ring, n_chunks, n_layers, layer;
+  float *o_hi, *o_lo; int ldo;               // output tf32 planes [rows, H*64]
+  int H, KV, window, slide;
+  int debug;                                 // test only: dump S/l/m/O-partial of block 0
+};
+
+void launch_attention_tc(const AttnTcArgs &a, cudaStream_t s);
+
+}  // namespace nc

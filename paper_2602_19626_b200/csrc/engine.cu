@@ -8,6 +8,7 @@
 #include <thread>
 
 #include "engine.hpp"
+#include "attn_tc.cuh"
 #include "gemm_tc.cuh"
 
 namespace nc {
@@ -240,6 +241,8 @@ void model_load(nc_model *m, const std::string &path, int device) {
   NC_CUDA(cudaDeviceSynchronize());
   const char *g = std::getenv("NC_GEMM");
   m->use_tc = !(g && std::string(g) == "simt");
+  const char *ga = std::getenv("NC_ATTN");
+  m->use_tc_attn = m->use_tc && !(ga && std::string(ga) == "simt");
   ensure_rope(m, 4096);
   NC_CUDA(cudaStreamCreateWithFlags(&m->walk_stream, cudaStreamNonBlocking));
 }
@@ -283,6 +286,8 @@ struct Forward {
   int Mmax = 0;
   float *h, *rinv, *q, *o, *act, *logits, *lbuf[2];
   float *h_hi, *h_lo, *o_hi, *o_lo, *act_hi, *act_lo;   // tf32 planes (tensor-core GEMM operands)
+  float *q_hi = nullptr, *q_lo = nullptr;               // tf32 planes of q (tensor-core attention)
+  int n_chunks_ = 0;
   KvRing ring{};
   void alloc(Bag &bag, int Mmax_, int n_chunks, int ring_len, bool double_logits = false) {
     Mmax = Mmax_;
@@ -304,8 +309,23 @@ struct Forward {
     ring.ring = ring_len;
     ring.kv = S.KV;
     size_t rn = (size_t)n_chunks * S.n_layers * ring_len * S.KV * S.dh;
-    ring.k = bag.get<float>(rn);
-    ring.v = bag.get<float>(rn);
+    n_chunks_ = n_chunks;
+    if (m->use_tc_attn) {
+      q_hi = bag.get<float>((size_t)Mmax * S.H * S.dh);
+      q_lo = bag.get<float>((size_t)Mmax * S.H * S.dh);
+      ring.k = ring.v = nullptr;
+      ring.k_hi = bag.get<float>(rn); ring.k_lo = bag.get<float>(rn);
+      ring.v_hi = bag.get<float>(rn); ring.v_lo = bag.get<float>(rn);
+      // The PV MMA multiplies masked keys by P = 0; a ring slot not written yet
+      // (past the chunk end, or ahead of the decode position) must hold a finite
+      // value or 0 * NaN poisons the row.  Masked K slots never reach P.
+      NC_CUDA(cudaMemsetAsync(ring.v_hi, 0, rn * sizeof(float), s));
+      NC_CUDA(cudaMemsetAsync(ring.v_lo, 0, rn * sizeof(float), s));
+    } else {
+      ring.k = bag.get<float>(rn);
+      ring.v = bag.get<float>(rn);
+      ring.k_hi = ring.k_lo = ring.v_hi = ring.v_lo = nullptr;
+    }
   }
   // embed -> n_layers x {QKV, attention, O, gate-up, down} -> head into `logits`.
   // valid = rows that are real tokens (algorithmic work), attn_flops = sum over
@@ -327,6 +347,7 @@ struct Forward {
         g.M = M; g.N = qd + 2 * kvd; g.K = S.d; g.rinv = rinv; g.C = q; g.ldc = qd;
         g.layer = (int)l; g.n_q_cols = qd; g.n_kv_cols = kvd; g.rows = rows; g.ring = ring;
         g.rope_cos = m->rope_cos; g.rope_sin = m->rope_sin;
+        g.planes = m->use_tc_attn ? 1 : 0; g.C_hi = q_hi; g.C_lo = q_lo;
         TcOperands op{h_hi, h_lo, (uint64_t)Mmax, m->wqkv_hi[l], m->wqkv_lo[l]};
         PROF(K_QKV, 2.0 * valid * (qd + 2 * kvd) * d, launch_gemm_tc(EPI_QKV, g, op, s));
       } else {
@@ -336,11 +357,21 @@ struct Forward {
         g.rows = rows; g.ring = ring; g.rope_cos = m->rope_cos; g.rope_sin = m->rope_sin;
         PROF(K_QKV, 2.0 * valid * (qd + 2 * kvd) * d, launch_gemm(EPI_QKV, g, s));
       }
-      AttnArgs at{};
-      at.tiles = tiles; at.n_tiles = n_tiles; at.q = q; at.o = o; at.ldq = qd; at.ring = ring; at.layer = (int)l;
-      at.H = S.H; at.KV = S.KV; at.window = (int)p.window; at.slide = (int)p.slide;
-      at.o_hi = tcm ? o_hi : nullptr; at.o_lo = tcm ? o_lo : nullptr;
-      PROF(K_ATTN, attn_flops, launch_attention(at, s));
+      if (m->use_tc_attn) {
+        AttnTcArgs at{};
+        at.tiles = tiles; at.n_tiles = n_tiles; at.q_hi = q_hi; at.q_lo = q_lo; at.ldq = qd; at.q_rows = Mmax;
+        at.k_hi = ring.k_hi; at.k_lo = ring.k_lo; at.v_hi = ring.v_hi; at.v_lo = ring.v_lo;
+        at.ring = ring.ring; at.n_chunks = n_chunks_; at.n_layers = (int)S.n_layers; at.layer = (int)l;
+        at.o_hi = o_hi; at.o_lo = o_lo; at.ldo = qd;
+        at.H = S.H; at.KV = S.KV; at.window = (int)p.window; at.slide = (int)p.slide;
+        PROF(K_ATTN, attn_flops, launch_attention_tc(at, s));
+      } else {
+        AttnArgs at{};
+        at.tiles = tiles; at.n_tiles = n_tiles; at.q = q; at.o = o; at.ldq = qd; at.ring = ring; at.layer = (int)l;
+        at.H = S.H; at.KV = S.KV; at.window = (int)p.window; at.slide = (int)p.slide;
+        at.o_hi = tcm ? o_hi : nullptr; at.o_lo = tcm ? o_lo : nullptr;
+        PROF(K_ATTN, attn_flops, launch_attention(at, s));
+      }
       if (tcm) {
         TcGemmArgs g{};
         g.M = M; g.N = S.d; g.K = qd; g.C = h; g.ldc = S.d; g.C_hi = h_hi; g.C_lo = h_lo;
@@ -515,10 +546,11 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
   for (int sl = 0; sl < n_slabs; ++sl) {
     tile_off[sl] = (int)tiles.size();
     w_off[sl] = (int)w_chunk.size();
+    const int TR = m->attn_tile_rows();
     for (int c = 0; c < n_chunks; ++c) {
-      for (int b0 = 0; b0 < R; b0 += 64) {
+      for (int b0 = 0; b0 < R; b0 += TR) {
         int p0 = sl * R + b0;
-        int nr = std::min<int>(64, (int)ntok[c] - p0);
+        int nr = std::min<int>(TR, (int)ntok[c] - p0);
         if (nr > 0) tiles.push_back(AttnTile{c, p0, nr, c * R + b0});
       }
       int cnt = std::min<int>(R, (int)ntok[c] - sl * R);
@@ -745,9 +777,10 @@ void debug_forward(nc_model *m, const uint32_t *x, uint32_t rows, const Params &
     int32_t *rc = bag.get<int32_t>(Rr), *rp = bag.get<int32_t>(Rr);
     for (int sl = 0; sl < n_slabs; ++sl) {
       std::vector<AttnTile> tiles;
-      for (int b0 = 0; b0 < Rr; b0 += 64) {
+      const int TR = m->attn_tile_rows();
+      for (int b0 = 0; b0 < Rr; b0 += TR) {
         int p0 = sl * Rr + b0;
-        int nr = std::min<int>(64, (int)rows - p0);
+        int nr = std::min<int>(TR, (int)rows - p0);
         if (nr > 0) tiles.push_back(AttnTile{0, p0, nr, b0});
       }
       AttnTile *td = bag.upload(tiles);
@@ -801,6 +834,64 @@ void debug_gemm(int device, const float *A, const float *B, uint32_t M, uint32_t
   NC_CUDA(cudaGetLastError());
   NC_CUDA(cudaMemcpyAsync(out, c_d, (size_t)M * N * 4, cudaMemcpyDeviceToHost, s));
   NC_CUDA(cudaStreamSynchronize(s));
+}
+
+void debug_attention(int device, const float *q, const float *k, const float *v, uint32_t n, uint32_t H, uint32_t KV,
+                     uint32_t window, uint32_t slide, int mode, float *o) {
+  NC_CUDA(cudaSetDevice(device));
+  if (!n) return;
+  cudaStream_t s = nullptr;
+  Bag bag(s);
+  const int ring = (int)(((n + 127) / 128) * 128);   // every position in its own slot
+  const size_t qd = (size_t)H * 64, kvd = (size_t)KV * 64;
+  std::vector<float> qv(q, q + n * qd), kv(k, k + n * kvd), vv(v, v + n * kvd);
+  const int rows = ring;
+  std::vector<float> qpad(rows * qd, 0.f), kpad((size_t)ring * kvd, 0.f), vpad((size_t)ring * kvd, 0.f);
+  std::copy(qv.begin(), qv.end(), qpad.begin());
+  std::copy(kv.begin(), kv.end(), kpad.begin());
+  std::copy(vv.begin(), vv.end(), vpad.begin());
+  float *q_d = bag.upload(qpad), *k_d = bag.upload(kpad), *v_d = bag.upload(vpad);
+  float *o_d = bag.get<float>((size_t)rows * qd);
+  float *oh = bag.get<float>((size_t)rows * qd), *ol = bag.get<float>((size_t)rows * qd);
+  const int TR = mode == 0 ? 128 : 64;
+  std::vector<AttnTile> tiles;
+  for (uint32_t p0 = 0; p0 < n; p0 += TR) tiles.push_back(AttnTile{0, (int)p0, (int)std::min<uint32_t>(TR, n - p0), (int)p0});
+  AttnTile *t_d = bag.upload(tiles);
+  if (mode == 0) {
+    float *qh = bag.get<float>(rows * qd), *ql = bag.get<float>(rows * qd);
+    float *kh = bag.get<float>(ring * kvd), *kl = bag.get<float>(ring * kvd);
+    float *vh = bag.get<float>(ring * kvd), *vl = bag.get<float>(ring * kvd);
+    launch_split_planes(q_d, qh, ql, rows * qd, s);
+    launch_split_planes(k_d, kh, kl, ring * kvd, s);
+    launch_split_planes(v_d, vh, vl, ring * kvd, s);
+    AttnTcArgs at{};
+    at.tiles = t_d; at.n_tiles = (int)tiles.size(); at.q_hi = qh; at.q_lo = ql; at.ldq = (int)qd; at.q_rows = rows;
+    at.k_hi = kh; at.k_lo = kl; at.v_hi = vh; at.v_lo = vl; at.ring = ring; at.n_chunks = 1; at.n_layers = 1;
+    at.layer = 0; at.o_hi = oh; at.o_lo = ol; at.ldo = (int)qd; at.H = (int)H; at.KV = (int)KV;
+    at.window = (int)window; at.slide = (int)slide;
+    const char *dbg = std::getenv("NC_ATTN_DEBUG");
+    at.debug = dbg ? std::atoi(dbg) : 0;
+    if (at.debug) {
+      NC_CUDA(cudaMemsetAsync(oh, 0, rows * qd * 4, s));
+      NC_CUDA(cudaMemsetAsync(ol, 0, rows * qd * 4, s));
+    }
+    launch_attention_tc(at, s);
+    std::vector<float> a(rows * qd), b(rows * qd);
+    NC_CUDA(cudaMemcpyAsync(a.data(), oh, a.size() * 4, cudaMemcpyDeviceToHost, s));
+    NC_CUDA(cudaMemcpyAsync(b.data(), ol, b.size() * 4, cudaMemcpyDeviceToHost, s));
+    NC_CUDA(cudaStreamSynchronize(s));
+    for (size_t i = 0; i < n * qd; ++i) o[i] = a[i] + b[i];
+  } else {
+    AttnArgs at{};
+    KvRing rg{};
+    rg.k = k_d; rg.v = v_d; rg.n_layers = 1; rg.ring = ring; rg.kv = (int)KV;
+    at.tiles = t_d; at.n_tiles = (int)tiles.size(); at.q = q_d; at.o = o_d; at.ldq = (int)qd; at.ring = rg;
+    at.layer = 0; at.H = (int)H; at.KV = (int)KV; at.window = (int)window; at.slide = (int)slide;
+    launch_attention(at, s);
+    NC_CUDA(cudaMemcpyAsync(o, o_d, n * qd * 4, cudaMemcpyDeviceToHost, s));
+    NC_CUDA(cudaStreamSynchronize(s));
+  }
+  NC_CUDA(cudaGetLastError());
 }
 
 void debug_walk(int device, const float *logits, const uint32_t *tok, uint32_t n, uint32_t V, const Params &p,

@@ -20,6 +20,8 @@ struct nc_model {
   float *E_head_hi = nullptr, *E_head_lo = nullptr;
   std::vector<float *> wqkv_hi, wqkv_lo, wo_hi, wo_lo, wgu_hi, wgu_lo, wd_hi, wd_lo;
   bool use_tc = true;                                    // NC_GEMM=simt selects the SIMT GEMMs
+  bool use_tc_attn = true;                               // NC_ATTN=simt selects the SIMT attention
+  int attn_tile_rows() const { return use_tc_attn ? 128 : 64; }
   float *rope_cos = nullptr, *rope_sin = nullptr;        // [rope_len, 32]
   int rope_len = 0;
   std::vector<void *> owned;                             // cudaFree on destruction
@@ -81,6 +83,8 @@ void encode_container(const Params &p, const std::vector<uint32_t> &ntok, const 
 // debug
 void debug_gemm(int device, const float *A, const float *B, uint32_t M, uint32_t N, uint32_t K, int mode,
                 float *out);
+void debug_attention(int device, const float *q, const float *k, const float *v, uint32_t n, uint32_t H, uint32_t KV,
+                     uint32_t window, uint32_t slide, int mode, float *o);
 void debug_forward(nc_model *m, const uint32_t *x, uint32_t rows, const Params &p, int mode, float *out);
 void debug_walk(int device, const float *logits, const uint32_t *tok, uint32_t n, uint32_t V,
                 const Params &p, uint32_t *cum, uint32_t *freq, float *p_true);

@@ -1,0 +1,381 @@
+// Block-window causal GQA attention on the tensor cores (
+// P:482-502 retained-KV window, D9-D12), fp32-accurate via 3xTF32:
+//
+//   for each 32-key block b of keys [w(j), j] (blocks aligned to absolute positions):
+//     S_b  = Q K_b^T              tcgen05 kind::tf32, 3 products x 8 k-steps  -> TMEM
+//     m_b  = max(m_{b-1}, rowmax(S_b / 8)), P_b = exp(S_b/8 - m_b) (masked), l updated
+//     O_b  = P_b V_b              tcgen05 kind::tf32 (V as an MN-major B operand) -> fresh TMEM partial
+//     O   <- O * exp(m_{b-1} - m_b) + O_b     in fp32 RN registers (promotion, see k_gemm_tc.cu)
+//   o = O / l
+//
+// One CTA per (128-row query tile of one chunk, q head); 256 threads:
+//   warp 0 TMA (Q once; K_hi/K_lo/V_hi/V_lo per block, 3 stages) from the tf32 planes
+//   warp 1 tcgen05.mma issuer; warp 2 TMEM allocator;
+//   warps 4-7 softmax + promotion, thread = query row (TMEM lane), writes P (hi/lo) into
+//   shared memory in the SWIZZLE_128B K-major layout the PV MMA reads.
+// A row's arithmetic depends only on its own q row and the key blocks up to its
+// position (later, fully masked blocks are exact no-ops: alpha = 1, P = 0), so the
+// decode step (tiles of one row) reproduces the prefill bit for bit (D15).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <math_constants.h>
+
+#include <algorithm>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+
+#include "attn_tc.cuh"
+#include "tc_common.cuh"
+
+namespace nc {
+
+constexpr int AQ = 128;          // query rows per tile
+constexpr int AK = 32;           // keys per block
+constexpr int AST = 3;           // K/V stages
+constexpr int Q_SUB = AQ * 128;  // one [128 rows x 32 fp32] swizzled sub-tile: 16 KB
+constexpr int KV_SUB = AK * 128; // one [32 keys x 32 fp32] sub-tile: 4 KB
+constexpr int Q_BYTES = 4 * Q_SUB;               // hi/lo x two 32-dim halves: 64 KB
+constexpr int KV_STAGE = 8 * KV_SUB;             // K hi/lo, V hi/lo, x two 32-dim halves: 32 KB
+constexpr int P_BYTES = 2 * Q_SUB;               // P hi, P lo: [128 x 32 keys]: 32 KB
+constexpr int ATT_SMEM = Q_BYTES + AST * KV_STAGE + P_BYTES + 1024 + 256;
+constexpr int ATT_THREADS = 256;
+
+__device__ __forceinline__ int wstart(int j, int L, int C) {
+  const int over = j + 1 - L;
+  return over <= 0 ? 0 : C * ((over + C - 1) / C);
+}
+
+// MN-major tf32 operand descriptor.  For 32-bit MN-major operands the only
+// smem layout UMMA accepts is SWIZZLE_128B_BASE32B (layout type 1: 128 B rows,
+// 32 B swizzle atoms, 4-row K atoms; CUTLASS sm100_common.inl), written by TMA
+// with CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B.  N blocks of 32 fp32 are LBO bytes
+// apart; 4-row K groups are 512 B apart (SBO).
+__device__ __forceinline__ uint64_t desc_mn_sw128_32b(uint32_t saddr, uint32_t lbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)(512u >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)1 << 61;
+  return d;
+}
+
+__device__ __forceinline__ void tma_load_4d(void *smem_dst, const CUtensorMap *m, int c0, int c1, int c2, int c3,
+                                            uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];" ::"r"(tc::smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(tc::smem_u32(bar))
+      : "memory");
+}
+
+__global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_constant__ CUtensorMap tmQh,
+                                                                const __grid_constant__ CUtensorMap tmQl,
+                                                                const __grid_constant__ CUtensorMap tmKh,
+                                                                const __grid_constant__ CUtensorMap tmKl,
+                                                                const __grid_constant__ CUtensorMap tmVh,
+                                                                const __grid_constant__ CUtensorMap tmVl,
+                                                                AttnTcArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *sQ = smem;                                  // [hi d0-31][hi d32-63][lo d0-31][lo d32-63]
+  uint8_t *sKV = smem + Q_BYTES;                       // per stage: Kh0 Kh1 Kl0 Kl1 Vh0 Vh1 Vl0 Vl1
+  uint8_t *sP = sKV + AST * KV_STAGE;                  // P hi, P lo
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sP + P_BYTES);
+  uint64_t *q_full = bars, *kv_full = bars + 1, *kv_empty = bars + 1 + AST;
+  uint64_t *s_full = bars + 1 + 2 * AST, *s_empty = s_full + 2, *p_full = s_empty + 2, *p_empty = p_full + 1;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(p_empty + 1);
+
+  const AttnTile t = a.tiles[blockIdx.x];
+  if (t.nrows <= 0) return;                        // inactive chunk in a decode step
+  const int h = blockIdx.y, g = h / (a.H / a.KV);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int w = wstart(t.p0, a.window, a.slide);
+  const int kb0 = w / AK, kb1 = (t.p0 + t.nrows - 1) / AK;
+  const int nkb = kb1 - kb0 + 1;
+  const int zc = t.chunk * a.n_layers + a.layer;   // (chunk, layer) coordinate of the ring maps
+
+  if (threadIdx.x == 0) {
+    tc::tma_prefetch(&tmQh); tc::tma_prefetch(&tmKh); tc::tma_prefetch(&tmVh);
+    tc::mbar_init(q_full, 1);
+    for (int s = 0; s < AST; ++s) { tc::mbar_init(&kv_full[s], 1); tc::mbar_init(&kv_empty[s], 1); }
+    for (int s = 0; s < 2; ++s) { tc::mbar_init(&s_full[s], 1); tc::mbar_init(&s_empty[s], 4); }
+    tc::mbar_init(p_full, 4);
+    tc::mbar_init(p_empty, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 2) tc::tmem_alloc(tmem_slot, 128);     // S[2] x 32 cols, O partial 64 cols
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS0 = tmem, tO = tmem + 64;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tc::mbar_expect_tx(q_full, Q_BYTES);
+      tc::tma_load_2d(sQ, &tmQh, h * 64, t.qrow0, q_full);
+      tc::tma_load_2d(sQ + Q_SUB, &tmQh, h * 64 + 32, t.qrow0, q_full);
+      tc::tma_load_2d(sQ + 2 * Q_SUB, &tmQl, h * 64, t.qrow0, q_full);
+      tc::tma_load_2d(sQ + 3 * Q_SUB, &tmQl, h * 64 + 32, t.qrow0, q_full);
+      int st = 0;
+      uint32_t ph = 0;
+      for (int i = 0; i < nkb; ++i) {
+        tc::mbar_wait(&kv_empty[st], ph ^ 1);
+        uint8_t *b = sKV + st * KV_STAGE;
+        const int slot = ((kb0 + i) * AK) % a.ring;
+        tc::mbar_expect_tx(&kv_full[st], KV_STAGE);
+        tma_load_4d(b + 0 * KV_SUB, &tmKh, 0, g, slot, zc, &kv_full[st]);
+        tma_load_4d(b + 1 * KV_SUB, &tmKh, 32, g, slot, zc, &kv_full[st]);
+        tma_load_4d(b + 2 * KV_SUB, &tmKl, 0, g, slot, zc, &kv_full[st]);
+        tma_load_4d(b + 3 * KV_SUB, &tmKl, 32, g, slot, zc, &kv_full[st]);
+        tma_load_4d(b + 4 * KV_SUB, &tmVh, 0, g, slot, zc, &kv_full[st]);
+        tma_load_4d(b + 5 * KV_SUB, &tmVh, 32, g, slot, zc, &kv_full[st]);
+        tma_load_4d(b + 6 * KV_SUB, &tmVl, 0, g, slot, zc, &kv_full[st]);
+        tma_load_4d(b + 7 * KV_SUB, &tmVl, 32, g, slot, zc, &kv_full[st]);
+        if (++st == AST) { st = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idS = tc::idesc_tf32(AQ, AK);                  // S: K-major A and B
+      constexpr uint32_t idO = tc::idesc_tf32(AQ, 64) | (1u << 16);     // O: B (V) MN-major
+      tc::mbar_wait(q_full, 0);
+      tc::fence_after();
+      const uint32_t q0 = tc::smem_u32(sQ);
+      const uint32_t p0 = tc::smem_u32(sP);
+      int st = 0;
+      uint32_t ph = 0;
+      uint32_t sph[2] = {0, 0};
+      uint32_t pph = 0;
+      auto issue_pv = [&](int stage) {
+        tc::mbar_wait(p_full, pph);
+        pph ^= 1;
+        tc::fence_after();
+        const uint32_t v0 = tc::smem_u32(sKV + stage * KV_STAGE + 4 * KV_SUB);
+#pragma unroll
+        for (int j = 0; j < AK / 8; ++j) {
+          const uint32_t abase = a.debug == 2 ? q0 : p0;   // debug 2: A = Q instead of P
+          const uint64_t pa = tc::desc_k_sw128(abase + j * 32), pl = tc::desc_k_sw128(abase + Q_SUB + j * 32);
+          const uint64_t vh = desc_mn_sw128_32b(v0 + j * 1024, KV_SUB);
+          const uint64_t vl = desc_mn_sw128_32b(v0 + 2 * KV_SUB + j * 1024, KV_SUB);
+          if (a.debug == 3) {   // readback check: tO = Q[:, 0:32] K^T with the proven K-major path
+            const uint32_t kk0 = tc::smem_u32(sKV + stage * KV_STAGE);
+            tc::mma_tf32(tO, tc::desc_k_sw128(q0 + j * 32), tc::desc_k_sw128(kk0 + j * 32), idS, j != 0);
+            continue;
+          }
+          tc::mma_tf32(tO, pa, vh, idO, j != 0);
+          tc::mma_tf32(tO, pa, vl, idO, 1);
+          tc::mma_tf32(tO, pl, vh, idO, 1);
+        }
+        tc::mma_commit(p_empty);
+        tc::mma_commit(&kv_empty[stage]);
+      };
+      int prev_stage = -1;
+      for (int i = 0; i < nkb; ++i) {
+        tc::mbar_wait(&kv_full[st], ph);
+        const int sb = i & 1;
+        tc::mbar_wait(&s_empty[sb], sph[sb] ^ 1);
+        sph[sb] ^= 1;
+        tc::fence_after();
+        const uint32_t k0 = tc::smem_u32(sKV + st * KV_STAGE);
+        const uint32_t dS = tS0 + sb * 32;
+#pragma unroll
+        for (int dsub = 0; dsub < 2; ++dsub)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t adv = j * 32;
+            const uint64_t qh = tc::desc_k_sw128(q0 + dsub * Q_SUB + adv);
+            const uint64_t ql = tc::desc_k_sw128(q0 + (2 + dsub) * Q_SUB + adv);
+            const uint64_t kh = tc::desc_k_sw128(k0 + dsub * KV_SUB + adv);
+            const uint64_t kl = tc::desc_k_sw128(k0 + (2 + dsub) * KV_SUB + adv);
+            tc::mma_tf32(dS, qh, kh, idS, (dsub | j) != 0);
+            tc::mma_tf32(dS, qh, kl, idS, 1);
+            tc::mma_tf32(dS, ql, kh, idS, 1);
+          }
+        tc::mma_commit(&s_full[sb]);
+        if (prev_stage >= 0) issue_pv(prev_stage);
+        prev_stage = st;
+        if (++st == AST) { st = 0; ph ^= 1; }
+      }
+      issue_pv(prev_stage);
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3, r = q * 32 + lane;     // query row of this thread (TMEM lane)
+    const bool valid = r < t.nrows;
+    const int j = t.p0 + r;
+    float O[64];
+#pragma unroll
+    for (int d = 0; d < 64; ++d) O[d] = 0.f;
+    float m = -CUDART_INF_F, l = 0.f, alpha_pend = 1.f;
+    uint32_t sph[2] = {0, 0}, pph = 0;
+    uint8_t *ph_hi = sP, *ph_lo = sP + Q_SUB;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    int nfold = 0;
+    auto fold = [&]() {                       // O <- O * alpha_pend + O_partial
+      tc::mbar_wait(p_empty, pph);
+      pph ^= 1;
+      tc::fence_after();
+      uint32_t x0[32], x1[32];
+      tc::tmem_ld32(tO + lane_off, x0);
+      tc::tmem_ld32(tO + lane_off + 32, x1);
+      tc::tmem_wait_ld();
+      if (a.debug && nfold == 0 && valid)
+        for (int k = 0; k < 30; ++k) a.o_lo[(size_t)(t.qrow0 + r) * a.ldo + h * 64 + 34 + k] = __uint_as_float(x0[k]);
+      ++nfold;
+#pragma unroll
+      for (int d = 0; d < 32; ++d) {
+        O[d] = __fmaf_rn(O[d], alpha_pend, __uint_as_float(x0[d]));
+        O[32 + d] = __fmaf_rn(O[32 + d], alpha_pend, __uint_as_float(x1[d]));
+      }
+    };
+    for (int i = 0; i < nkb; ++i) {
+      const int sb = i & 1;
+      tc::mbar_wait(&s_full[sb], sph[sb]);
+      sph[sb] ^= 1;
+      tc::fence_after();
+      uint32_t sr[32];
+      tc::tmem_ld32(tS0 + sb * 32 + lane_off, sr);
+      tc::tmem_wait_ld();
+      if (a.debug && i == 0 && valid)
+        for (int k = 0; k < 32; ++k) a.o_hi[(size_t)(t.qrow0 + r) * a.ldo + h * 64 + k] = __uint_as_float(sr[k]);
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&s_empty[sb]);
+      const int key0 = (kb0 + i) * AK;
+      float s[32];
+      float mb = -CUDART_INF_F;
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        const bool ok = key0 + k <= j;       // keys >= w(j) by construction of the block range
+        s[k] = ok ? __fmul_rn(__uint_as_float(sr[k]), 0.125f) : -CUDART_INF_F;
+        mb = fmaxf(mb, s[k]);
+      }
+      const float mn = fmaxf(m, mb);
+      const float alpha = (mn == -CUDART_INF_F) ? 1.f : expf(__fsub_rn(m, mn));
+      float ps = 0.f;
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        s[k] = (s[k] == -CUDART_INF_F) ? 0.f : expf(__fsub_rn(s[k], mn));
+        ps = __fadd_rn(ps, s[k]);
+      }
+      l = __fmaf_rn(l, alpha, ps);
+      m = mn;
+      if (i > 0) fold();                      // O partial of block i-1 (uses alpha of block i-1)
+      alpha_pend = alpha;
+      // P_i (hi/lo) -> shared memory, 128B-swizzled K-major rows of 32 keys
+#pragma unroll
+      for (int c4 = 0; c4 < 8; ++c4) {
+        float4 hi, lo;
+        tc::split_tf32(s[4 * c4 + 0], hi.x, lo.x); tc::split_tf32(s[4 * c4 + 1], hi.y, lo.y);
+        tc::split_tf32(s[4 * c4 + 2], hi.z, lo.z); tc::split_tf32(s[4 * c4 + 3], hi.w, lo.w);
+        const int off = r * 128 + ((c4 ^ (r & 7)) << 4);
+        *reinterpret_cast<float4 *>(ph_hi + off) = hi;
+        *reinterpret_cast<float4 *>(ph_lo + off) = lo;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(p_full);
+    }
+    fold();
+    if (a.debug) {
+      if (valid) {
+        a.o_lo[(size_t)(t.qrow0 + r) * a.ldo + h * 64 + 32] = l;
+        a.o_lo[(size_t)(t.qrow0 + r) * a.ldo + h * 64 + 33] = m;
+      }
+    } else if (valid) {
+      const size_t ob = (size_t)(t.qrow0 + r) * a.ldo + h * 64;
+#pragma unroll
+      for (int d = 0; d < 64; d += 4) {
+        float4 hi, lo, v;
+        v.x = __fdiv_rn(O[d], l); v.y = __fdiv_rn(O[d + 1], l);
+        v.z = __fdiv_rn(O[d + 2], l); v.w = __fdiv_rn(O[d + 3], l);
+        tc::split_tf32(v.x, hi.x, lo.x); tc::split_tf32(v.y, hi.y, lo.y);
+        tc::split_tf32(v.z, hi.z, lo.z); tc::split_tf32(v.w, hi.w, lo.w);
+        *reinterpret_cast<float4 *>(a.o_hi + ob + d) = hi;
+        *reinterpret_cast<float4 *>(a.o_lo + ob + d) = lo;
+      }
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  if (warp == 2) tc::tmem_dealloc(tmem, 128);
+}
+
+// ------------------------------------------------------------- host side ---
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn2() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult qr;
+    void *p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) != cudaSuccess ||
+        qr != cudaDriverEntryPointSuccess || !p)
+      throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+static const CUtensorMap *tmap_nd(const float *ptr, int rank, const uint64_t *dims, const uint32_t *box,
+                                 CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+  struct Key {
+    const void *p; int r; uint64_t d[4]; uint32_t b[4]; int sw;
+    bool operator==(const Key &o) const {
+      return p == o.p && r == o.r && sw == o.sw && !memcmp(d, o.d, sizeof(d)) && !memcmp(b, o.b, sizeof(b));
+    }
+  };
+  struct H {
+    size_t operator()(const Key &k) const {
+      size_t x = std::hash<const void *>()(k.p);
+      for (int i = 0; i < 4; ++i) x = x * 1315423911u ^ k.d[i] ^ ((size_t)k.b[i] << 32);
+      return x;
+    }
+  };
+  static std::mutex mu;
+  static std::unordered_map<Key, CUtensorMap, H> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  Key k{ptr, rank, {0, 0, 0, 0}, {0, 0, 0, 0}, (int)swz};
+  for (int i = 0; i < rank; ++i) { k.d[i] = dims[i]; k.b[i] = box[i]; }
+  auto it = cache.find(k);
+  if (it != cache.end()) return &it->second;
+  CUtensorMap m;
+  cuuint64_t gd[4], gs[3];
+  cuuint32_t bx[4], es[4] = {1, 1, 1, 1};
+  uint64_t stride = 4;
+  for (int i = 0; i < rank; ++i) {
+    gd[i] = dims[i];
+    bx[i] = box[i];
+    if (i > 0) gs[i - 1] = stride;
+    stride *= dims[i];
+  }
+  CUresult r = encode_fn2()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<float *>(ptr), gd, gs, bx, es,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled (attention) failed: " + std::to_string((int)r));
+  return &cache.emplace(k, m).first->second;
+}
+
+void launch_attention_tc(const AttnTcArgs &a, cudaStream_t s) {
+  if (a.n_tiles <= 0) return;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ATT_SMEM);
+    attr = true;
+  }
+  const uint64_t qd[2] = {(uint64_t)a.ldq, (uint64_t)a.q_rows};
+  const uint32_t qb[2] = {32, AQ};
+  const uint64_t kd[4] = {64, (uint64_t)a.KV, (uint64_t)a.ring, (uint64_t)a.n_chunks * a.n_layers};
+  const uint32_t kbx[4] = {32, 1, AK, 1};
+  const CUtensorMap *qh = tmap_nd(a.q_hi, 2, qd, qb), *ql = tmap_nd(a.q_lo, 2, qd, qb);
+  const CUtensorMap *kh = tmap_nd(a.k_hi, 4, kd, kbx), *kl = tmap_nd(a.k_lo, 4, kd, kbx);
+  const CUtensorMap *vh = tmap_nd(a.v_hi, 4, kd, kbx, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  const CUtensorMap *vl = tmap_nd(a.v_lo, 4, kd, kbx, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  dim3 grid(a.n_tiles, a.H);
+  attn_tc_kernel<<<grid, ATT_THREADS, ATT_SMEM, s>>>(*qh, *ql, *kh, *kl, *vh, *vl, a);
+}
+
+}  // namespace nc

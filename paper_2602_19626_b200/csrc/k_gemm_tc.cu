@@ -221,18 +221,41 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
                   x[j + 32] = __fmaf_rn(x2, c, __fmul_rn(x1, s));
                 }
               }
-              float *dst;
-              if (cb < nq) {
-                dst = a.C + (size_t)m * a.ldc + cb;
-              } else {
-                const int ch = a.rows.chunk[m];
-                const bool isk = cb < nq + nkv;
-                const int kvh = (cb - nq - (isk ? 0 : nkv)) / 64;
-                dst = (isk ? a.ring.k : a.ring.v) + a.ring.off(ch, a.layer, pos) + kvh * 64;
-              }
+              if (a.planes) {
+                float *dh, *dl;
+                if (cb < nq) {
+                  dh = a.C_hi + (size_t)m * a.ldc + cb;
+                  dl = a.C_lo + (size_t)m * a.ldc + cb;
+                } else {
+                  const int ch = a.rows.chunk[m];
+                  const bool isk = cb < nq + nkv;
+                  const int kvh = (cb - nq - (isk ? 0 : nkv)) / 64;
+                  const size_t o = a.ring.off(ch, a.layer, pos) + kvh * 64;
+                  dh = (isk ? a.ring.k_hi : a.ring.v_hi) + o;
+                  dl = (isk ? a.ring.k_lo : a.ring.v_lo) + o;
+                }
 #pragma unroll
-              for (int j = 0; j < 64; j += 4)
-                *reinterpret_cast<float4 *>(dst + j) = make_float4(x[j], x[j + 1], x[j + 2], x[j + 3]);
+                for (int j = 0; j < 64; j += 4) {
+                  float4 h4, l4;
+                  tc::split_tf32(x[j], h4.x, l4.x); tc::split_tf32(x[j + 1], h4.y, l4.y);
+                  tc::split_tf32(x[j + 2], h4.z, l4.z); tc::split_tf32(x[j + 3], h4.w, l4.w);
+                  *reinterpret_cast<float4 *>(dh + j) = h4;
+                  *reinterpret_cast<float4 *>(dl + j) = l4;
+                }
+              } else {
+                float *dst;
+                if (cb < nq) {
+                  dst = a.C + (size_t)m * a.ldc + cb;
+                } else {
+                  const int ch = a.rows.chunk[m];
+                  const bool isk = cb < nq + nkv;
+                  const int kvh = (cb - nq - (isk ? 0 : nkv)) / 64;
+                  dst = (isk ? a.ring.k : a.ring.v) + a.ring.off(ch, a.layer, pos) + kvh * 64;
+                }
+#pragma unroll
+                for (int j = 0; j < 64; j += 4)
+                  *reinterpret_cast<float4 *>(dst + j) = make_float4(x[j], x[j + 1], x[j + 2], x[j + 3]);
+              }
             }
           }
         }

@@ -16,7 +16,8 @@ struct RowMeta {
 
 // K/V ring of one layer set: [chunk][layer][ring][KV][64] fp32.
 struct KvRing {
-  float *k, *v;
+  float *k, *v;                 // fp32 (SIMT attention)
+  float *k_hi, *k_lo, *v_hi, *v_lo;  // tf32 planes (tensor-core attention); null when unused
   int n_layers, ring, kv;
   __host__ __device__ size_t off(int c, int layer, int pos) const {
     return (((size_t)c * n_layers + layer) * ring + (size_t)(pos % ring)) * kv * kHeadDim;

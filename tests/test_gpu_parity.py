@@ -226,3 +226,41 @@ def test_full_model_sampled_rows(nc):
     err = np.abs(z - ref).max() / np.abs(ref).max()
     assert err < Z_TOL, err
     m.close()
+
+
+# ------------------------------------------------------- op-level kernels ---
+@pytest.mark.parametrize("mode", [0, 1])
+def test_attention_op_vs_numpy(nc, mode):
+    """one attention layer (block-window causal GQA, D9-D10) against fp64 numpy,
+    tensor-core (mode 0) and SIMT (mode 1) kernels, with slides (n > L)."""
+    from oracle.lm import window_start
+    rng = np.random.default_rng(21)
+    n, H, KV, L, C = 390, 9, 3, 256, 128
+    q = rng.standard_normal((n, H * 64)).astype(np.float32)
+    k = rng.standard_normal((n, KV * 64)).astype(np.float32)
+    v = rng.standard_normal((n, KV * 64)).astype(np.float32)
+    ref = np.zeros((n, H * 64))
+    for j in range(n):
+        w0 = window_start(j, L, C)
+        for h in range(H):
+            g = h // (H // KV)
+            s = k[w0:j + 1, g * 64:(g + 1) * 64].astype(np.float64) @ q[j, h * 64:(h + 1) * 64] / 8
+            p = np.exp(s - s.max())
+            ref[j, h * 64:(h + 1) * 64] = (p / p.sum()) @ v[w0:j + 1, g * 64:(g + 1) * 64]
+    o = nc.nc_debug_attention(q, k, v, H, KV, L, C, mode)
+    assert np.abs(o - ref).max() < 1e-5
+
+
+@pytest.mark.parametrize("K", [576, 1536])
+def test_tc_gemm_op_vs_numpy(nc, K):
+    """tcgen05 3xTF32 GEMM with fp32-RN promotion: at least SIMT-fp32 accuracy."""
+    rng = np.random.default_rng(K)
+    A = rng.standard_normal((300, K)).astype(np.float32)
+    B = (rng.standard_normal((448, K)) / 24).astype(np.float32)
+    ref = A.astype(np.float64) @ B.astype(np.float64).T
+    out = nc.nc_debug_gemm(A, B, 0)
+    assert np.abs(out - ref).max() / np.abs(ref).max() < 2e-6
+    P = rng.random((256, K)).astype(np.float32)              # positive data: no cancellation of bias
+    Q = rng.random((128, K)).astype(np.float32)
+    r2 = P.astype(np.float64) @ Q.astype(np.float64).T
+    assert abs(((nc.nc_debug_gemm(P, Q, 0) - r2) / r2).mean()) < 1e-6
