@@ -245,6 +245,7 @@ void model_load(nc_model *m, const std::string &path, int device) {
   m->use_tc_attn = m->use_tc && !(ga && std::string(ga) == "simt");
   ensure_rope(m, 4096);
   NC_CUDA(cudaStreamCreateWithFlags(&m->walk_stream, cudaStreamNonBlocking));
+  NC_CUDA(cudaStreamCreateWithFlags(&m->ng_stream, cudaStreamNonBlocking));
 }
 
 void model_free(nc_model *m) {
@@ -253,7 +254,8 @@ void model_free(nc_model *m) {
   if (m->rope_cos) cudaFree(m->rope_cos);
   if (m->rope_sin) cudaFree(m->rope_sin);
   if (m->walk_stream) cudaStreamDestroy(m->walk_stream);
-  m->walk_stream = nullptr;
+  if (m->ng_stream) cudaStreamDestroy(m->ng_stream);
+  m->walk_stream = m->ng_stream = nullptr;
   m->owned.clear();
 }
 
@@ -471,8 +473,12 @@ struct WalkBufs {
   unsigned long long *keys;
   uint32_t *vals;
   NgRecord *recs;
-  uint32_t hcap, rcap;
-  void alloc(Bag &bag, int n_chunks, uint32_t V, uint32_t max_n, const Params &p, cudaStream_t s) {
+  NgTok *ng_pre = nullptr;
+  float *ng_spadd = nullptr;
+  uint32_t hcap, rcap, ng_ring = 1;
+  // ng_ring > 0: tokens per chunk kept in the precomputed N-gram ring (encode)
+  void alloc(Bag &bag, int n_chunks, uint32_t V, uint32_t max_n, const Params &p, cudaStream_t s,
+             uint32_t ring = 0) {
     rcap = std::max<uint32_t>(1, std::min<uint32_t>(p.cap, max_n));
     hcap = pow2_at_least(2ull * rcap);
     st = bag.get<WalkState>(n_chunks);
@@ -486,11 +492,17 @@ struct WalkBufs {
     NC_CUDA(cudaMemsetAsync(cu, 0, (size_t)n_chunks * V * sizeof(uint32_t), s));
     NC_CUDA(cudaMemsetAsync(spadd, 0, (size_t)n_chunks * V * sizeof(float), s));
     NC_CUDA(cudaMemsetAsync(keys, 0, (size_t)n_chunks * kMaxOrders * hcap * 8, s));
+    if (ring) {
+      ng_ring = ring;
+      ng_pre = bag.get<NgTok>((size_t)n_chunks * ring);
+      ng_spadd = bag.get<float>((size_t)n_chunks * V);
+      NC_CUDA(cudaMemsetAsync(ng_spadd, 0, (size_t)n_chunks * V * sizeof(float), s));
+    }
     launch_walk_init(st, n_chunks, s);
   }
   void fill(WalkArgs &a, const Params &p, uint32_t V) const {
     a.st = st; a.b = b; a.cu = cu; a.spadd = spadd; a.ng_keys = keys; a.ng_vals = vals; a.ng_recs = recs;
-    a.hcap = hcap; a.rcap = rcap;
+    a.hcap = hcap; a.rcap = rcap; a.ng_pre = ng_pre; a.ng_ring = ng_ring; a.ng_spadd = ng_spadd;
     a.V = V; a.cdf_bits = p.cdf_bits; a.warmup = p.warmup; a.flags = p.flags; a.orders = p.orders; a.cap = p.cap;
     a.inv_tau = (float)p.inv_tau; a.alpha = p.alpha; a.eta = p.eta;
   }
@@ -562,15 +574,39 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
   AttnTile *tiles_d = bag.upload(tiles);
   int32_t *wc_d = bag.upload(w_chunk), *wr_d = bag.upload(w_row0), *wn_d = bag.upload(w_count);
   WalkBufs wb;
-  wb.alloc(bag, n_chunks, S.V, max_n, p, s);
+  const bool use_ng = p.flags & 1u;
+  wb.alloc(bag, n_chunks, S.V, max_n, p, s, use_ng ? (uint32_t)(2 * R) : 0u);
   uint32_t *cum_d = bag.get<uint32_t>(total), *freq_d = bag.get<uint32_t>(total);
   float *p_d = p.debug_dump ? bag.get<float>(total) : nullptr;
 
-  // events: per slab forward start/end (stream s), walk start/end (walk stream)
-  cudaStream_t ws = m->walk_stream;
-  std::vector<cudaEvent_t> ev(4 * n_slabs);
-  for (auto &e : ev) NC_CUDA(cudaEventCreate(&e));
+  // streams: forward (s), N-gram precompute (ns, runs ahead; ring of 2 slabs), walk (ws)
+  // events: per slab forward start/end, walk start/end, N-gram done
+  cudaStream_t ws = m->walk_stream, ns = m->ng_stream;
+  std::vector<cudaEvent_t> ev(5 * n_slabs + 1);
+  for (auto &e : ev) NC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDefault));
+  cudaEvent_t ev_init = ev[5 * n_slabs];
+  NC_CUDA(cudaEventRecord(ev_init, s));
+  NC_CUDA(cudaStreamWaitEvent(ns, ev_init, 0));
+  NC_CUDA(cudaStreamWaitEvent(ws, ev_init, 0));
+  // the walk keeps one SM per chunk busy for a whole slab: leave those SMs out of
+  // the persistent GEMM grids so every GEMM CTA is resident at once
+  set_reserved_sms(n_slabs > 1 ? n_chunks : 0);
+  WalkArgs wbase{};
+  wbase.logits = nullptr; wbase.ldl = S.V;
+  wbase.tokens = tokens_dev; wbase.tok_off = tok_off_d;
+  wbase.out_cum = cum_d; wbase.out_freq = freq_d; wbase.out_p = p_d;
+  wbase.mode = 0;
+  wb.fill(wbase, p, S.V);
   for (int sl = 0; sl < n_slabs; ++sl) {
+    if (use_ng) {
+      if (sl >= 2) NC_CUDA(cudaStreamWaitEvent(ns, ev[4 * (sl - 2) + 3], 0));   // ring slots free again
+      WalkArgs na = wbase;
+      na.chunk_of = wc_d + w_off[sl]; na.row0 = wr_d + w_off[sl]; na.count = wn_d + w_off[sl];
+      na.n_entries = w_off[sl + 1] - w_off[sl];
+      launch_ngram_precompute(na, ns);
+      NC_CUDA(cudaEventRecord(ev[4 * n_slabs + sl], ns));
+      st.launches++;
+    }
     if (sl >= 2) NC_CUDA(cudaStreamWaitEvent(s, ev[4 * (sl - 2) + 3], 0));   // logits buffer free again
     fw.logits = fw.lbuf[sl & 1];
     NC_CUDA(cudaEventRecord(ev[4 * sl], s));
@@ -587,15 +623,12 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
            nullptr);
     NC_CUDA(cudaEventRecord(ev[4 * sl + 1], s));
     NC_CUDA(cudaStreamWaitEvent(ws, ev[4 * sl + 1], 0));
+    if (use_ng) NC_CUDA(cudaStreamWaitEvent(ws, ev[4 * n_slabs + sl], 0));
     NC_CUDA(cudaEventRecord(ev[4 * sl + 2], ws));
-    WalkArgs wa{};
+    WalkArgs wa = wbase;
     wa.chunk_of = wc_d + w_off[sl]; wa.row0 = wr_d + w_off[sl]; wa.count = wn_d + w_off[sl];
     wa.n_entries = w_off[sl + 1] - w_off[sl];
-    wa.logits = fw.logits; wa.ldl = S.V;
-    wa.tokens = tokens_dev; wa.tok_off = tok_off_d;
-    wa.out_cum = cum_d; wa.out_freq = freq_d; wa.out_p = p_d;
-    wa.mode = 0;
-    wb.fill(wa, p, S.V);
+    wa.logits = fw.logits;
     prof().begin(K_WALK, 4.0 * S.V * valid, ws);
     launch_walk(wa, ws);
     prof().end(ws);
@@ -604,6 +637,7 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
     NC_CUDA(cudaGetLastError());
   }
   NC_CUDA(cudaStreamWaitEvent(s, ev[4 * (n_slabs - 1) + 3], 0));
+  set_reserved_sms(0);
   NC_CUDA(cudaMemcpyAsync(out.cum.data(), cum_d, total * 4, cudaMemcpyDeviceToHost, s));
   NC_CUDA(cudaMemcpyAsync(out.freq.data(), freq_d, total * 4, cudaMemcpyDeviceToHost, s));
   if (p_d) NC_CUDA(cudaMemcpyAsync(out.p_true.data(), p_d, total * 4, cudaMemcpyDeviceToHost, s));
@@ -910,7 +944,7 @@ void debug_walk(int device, const float *logits, const uint32_t *tok, uint32_t n
   std::vector<int32_t> zero{0}, cnt{(int32_t)n};
   int32_t *c_d = bag.upload(zero), *r_d = bag.upload(zero), *n_d = bag.upload(cnt);
   WalkBufs wb;
-  wb.alloc(bag, 1, V, n, p, s);
+  wb.alloc(bag, 1, V, n, p, s, n);
   uint32_t *cum_d = bag.get<uint32_t>(n), *freq_d = bag.get<uint32_t>(n);
   float *p_d = bag.get<float>(n);
   WalkArgs wa{};
@@ -918,6 +952,7 @@ void debug_walk(int device, const float *logits, const uint32_t *tok, uint32_t n
   wa.logits = lg_d; wa.ldl = V; wa.tokens = tk_d; wa.tok_off = off_d;
   wa.out_cum = cum_d; wa.out_freq = freq_d; wa.out_p = p_d; wa.mode = 0;
   wb.fill(wa, p, V);
+  if (p.flags & 1u) launch_ngram_precompute(wa, s);
   launch_walk(wa, s);
   NC_CUDA(cudaGetLastError());
   NC_CUDA(cudaMemcpyAsync(cum, cum_d, n * 4, cudaMemcpyDeviceToHost, s));

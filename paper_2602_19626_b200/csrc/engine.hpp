@@ -26,6 +26,7 @@ struct nc_model {
   int rope_len = 0;
   std::vector<void *> owned;                             // cudaFree on destruction
   cudaStream_t walk_stream = nullptr;                    // the walk runs beside the next slab's forward
+  cudaStream_t ng_stream = nullptr;                      // the N-gram precompute runs ahead of the walk
 };
 
 namespace nc {

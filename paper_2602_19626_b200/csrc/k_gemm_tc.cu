@@ -311,6 +311,9 @@ const CUtensorMap *tmap_2d(const float *ptr, uint64_t rows, uint64_t cols, uint3
   return &cache.emplace(k, m).first->second;
 }
 
+static int g_reserved_sms = 0;
+void set_reserved_sms(int n) { g_reserved_sms = n; }
+
 static int num_sms() {
   static int n = 0;
   if (!n) {
@@ -331,7 +334,7 @@ static void launch_tc(const TcGemmArgs &a, const TcOperands &op, cudaStream_t s)
   const CUtensorMap *ah = tmap_2d(op.A_hi, op.a_rows, a.K, TBM), *al = tmap_2d(op.A_lo, op.a_rows, a.K, TBM);
   const CUtensorMap *bh = tmap_2d(op.B_hi, a.N, a.K, TBN), *bl = tmap_2d(op.B_lo, a.N, a.K, TBN);
   const int tiles = ((a.M + TBM - 1) / TBM) * ((a.N + TBN - 1) / TBN);
-  const int grid = std::min(tiles, num_sms());
+  const int grid = std::min(tiles, std::max(1, num_sms() - g_reserved_sms));
   gemm_tc_kernel<EPI><<<grid, TC_THREADS, TC_SMEM, s>>>(*ah, *al, *bh, *bl, a);
 }
 

@@ -1,22 +1,31 @@
-// The per-token vocab-row CDF kernel ("walk"), v1: one 1024-thread CTA per
-// chunk walks that chunk's tokens in order.
+// The per-token vocab-row CDF kernel ("walk") and
+// the N-gram precompute kernel.
 //
 // Per token i of a chunk (alg:compress P:246-267; SURVEY.md §8(c) canonical loop):
-//   u_v  = z_v / tau + (f32) b_v                           (D16a)
-//   pt_v = exp(u_v - max u) / sum exp(u - max u)            (softmax, fp32)
-//   p_v  = pt_v                                   (i < W or N-gram off)
-//        = w_l pt_v + w_n p_ng(v)                 (otherwise)
-//        p_ng(v) = a0 (c(v)+1)/(N+V) + sum_k a_k cnt_k(v)   (closed form of P:361-374)
-//   c_v  = max(1, floor((double) p_v (T - V)))    (exact product, D5)
+//   u_v  = z_v / tau + (f32) b_v                            (D16a)
+//   pt_v = exp(u_v - max u) / sum exp(u - max u)             (softmax, fp32)
+//   p_v  = pt_v                                    (i < W or N-gram off)
+//        = w_l pt_v + w_n p_ng(v)                  (otherwise)
+//        p_ng(v) = a0/(N+V) (c(v)+1) + sum_k a_k cnt_k(v)   (closed form of P:361-374)
+//   c_v  = max(1, floor((double) p_v (T - V)))     (exact product, D5)
 //   residual T - sum c added to c_argmax (lowest index on ties, D4; signed, D6)
-//   encode: emit (cum_t, freq_t);  decode: prefix scan + WNC target search (D27)
-//   b_v -= alpha (pt_v - [v = t])  in f64           (D17)
+//   encode: (cum_t, freq_t);  decode: group prefix scan + WNC target search (D27)
+//   b_v -= alpha (pt_v - [v = t])  in f64            (D17)
 //   mixer: lw += eta [ln pt_t, ln p_ng(t)], renormalise (D24-D26)
-//   N-gram update with t (D18-D23)
+//   unigram c(t)++ and the order-1..4 context tables    (D18-D23)
 //
-// Every float operation is an explicit round-to-nearest intrinsic, and encode
-// and decode run the same code, so the decoder reproduces the encoder's counts
-// bit for bit (D15).
+// One 1024-thread CTA per chunk walks the chunk's tokens in order; thread t owns
+// the float4 groups g = t, t + 1024, ... of the vocab row (coalesced loads).
+//
+// Compression knows every token, so the N-gram (which depends on tokens only)
+// runs ahead in `ngram_pre_kernel` (one warp per chunk) and hands the walk a
+// merged sparse list per token; the walk's main pass then also folds in the
+// NEXT token's softmax statistics (u_{i+1} = z_{i+1} + b after this token's
+// update), so a token costs one pass over the row and one block reduction.
+// Decompression runs the same N-gram functions inline and the same element
+// arithmetic; every float op is an explicit round-to-nearest intrinsic and
+// every reduction has a fixed tree, so the decoder reproduces the encoder's
+// counts bit for bit (D15).
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
@@ -24,7 +33,7 @@
 
 namespace nc {
 
-constexpr int WT = 1024;   // threads per CTA
+constexpr int WT = 1024;   // threads per walk CTA
 constexpr int NW = WT / 32;
 
 struct WalkSmem {
@@ -32,22 +41,67 @@ struct WalkSmem {
   unsigned long long red_sum[NW], red_cum[NW];
   float red_bv[NW]; int red_bi[NW]; uint32_t red_bc[NW];
   uint32_t scan[NW];
-  uint32_t sp_tok[kMaxOrders * kSlots];
-  int sp_n;
   // per-token broadcast scalars
-  float M, S, a0f, wl, wn;
-  int mix, tok, argmax;
+  float M, invS, a0f;
+  int mix, tok, argmax, nsp;
   long long resid;
   unsigned long long target, cum_t, freq_t;
   float pt_t, png_t, p_t;
+  __align__(16) NgTok lists[2];   // sparse N-gram fixups of the current / next token
 };
 
+// ------------------------------------------------------------ elementwise ---
+__device__ __forceinline__ float walk_u(float z, double b, float inv_tau) { return __fmaf_rn(z, inv_tau, (float)b); }
+__device__ __forceinline__ double b_step(double b, float pt, bool is_t, double alpha) {
+  return __fma_rn(-alpha, __dsub_rn((double)pt, is_t ? 1.0 : 0.0), b);
+}
+// c = max(1, floor(p * (T - V))) with the EXACT product (D5), in fp32 only:
+// T - V < 2^24 is exact in fp32; q = floor(rn(p * TmV)) is off by at most one,
+// and the sign of the exact residual p * TmV - q is that of fma(p, TmV, -q).
+__device__ __forceinline__ uint32_t quant(float p, float TmV) {
+  float q = floorf(__fmul_rn(p, TmV));
+  const float r = __fmaf_rn(p, TmV, -q);
+  q = r < 0.f ? __fsub_rn(q, 1.f) : (r >= 1.f ? __fadd_rn(q, 1.f) : q);
+  return q < 1.f ? 1u : (uint32_t)q;
+}
+// exp on the SFU (ex2.approx; relative error ~1e-6 for the |x| < 30 used here)
+__device__ __forceinline__ float fexp(float x) { return exp2f(__fmul_rn(x, 1.44269504088896341f)); }
+// online (max, sum exp) of one thread
+__device__ __forceinline__ void ms_push(float &tm, float &ts, float u) {
+  if (u > tm) { ts = __fmaf_rn(ts, fexp(__fsub_rn(tm, u)), 1.f); tm = u; }
+  else ts = __fadd_rn(ts, fexp(__fsub_rn(u, tm)));
+}
+__device__ __forceinline__ void ms_merge(float &tm, float &ts, float om, float os) {
+  const float mm = fmaxf(tm, om);
+  const float e1 = (tm == -CUDART_INF_F) ? 0.f : fexp(__fsub_rn(tm, mm));
+  const float e2 = (om == -CUDART_INF_F) ? 0.f : fexp(__fsub_rn(om, mm));
+  ts = __fadd_rn(__fmul_rn(ts, e1), __fmul_rn(os, e2));
+  tm = mm;
+}
+__device__ __forceinline__ void ms_warp(float &tm, float &ts) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1)
+    ms_merge(tm, ts, __shfl_xor_sync(0xffffffffu, tm, o), __shfl_xor_sync(0xffffffffu, ts, o));
+}
+// p = w_l pt + w_n (a0f (c+1) + add)
+__device__ __forceinline__ float mix_p(float pt, float a0f, uint32_t cuv, float add, float wl, float wn, float &png) {
+  png = __fmaf_rn(a0f, (float)(cuv + 1u), add);
+  return __fmaf_rn(wl, pt, __fmul_rn(wn, png));
+}
+struct Best {
+  float v; int i; uint32_t c;
+};
+__device__ __forceinline__ void best_merge(Best &a, float v, int i, uint32_t c) {
+  if (v > a.v || (v == a.v && i < a.i)) { a.v = v; a.i = i; a.c = c; }
+}
+
+// ------------------------------------------------------------------ N-gram ---
 __device__ __forceinline__ unsigned long long fnv_ctx(int k, const uint32_t *hist) {
   unsigned long long h = 0xcbf29ce484222325ull;
   const unsigned long long P = 0x100000001b3ull;
   h ^= (unsigned long long)(k & 255); h *= P;
   for (int j = 4 - k; j < 4; ++j) {
-    uint32_t t = hist[j];
+    const uint32_t t = hist[j];
 #pragma unroll
     for (int by = 0; by < 4; ++by) { h ^= (t >> (8 * by)) & 255u; h *= P; }
   }
@@ -57,41 +111,187 @@ __device__ __forceinline__ unsigned long long fnv_ctx(int k, const uint32_t *his
 // warp-parallel linear probe; returns record index or -1 (and the first empty slot).
 __device__ __forceinline__ int ng_probe(const unsigned long long *keys, const uint32_t *vals, uint32_t hcap,
                                         unsigned long long key, int lane, uint32_t *empty_slot) {
-  uint32_t base = (uint32_t)(key ^ (key >> 32)) & (hcap - 1);
+  const uint32_t base = (uint32_t)(key ^ (key >> 32)) & (hcap - 1);
   for (uint32_t p = 0; p < hcap; p += 32) {
-    uint32_t idx = (base + p + lane) & (hcap - 1);
-    unsigned long long kk = keys[idx];
-    unsigned m = __ballot_sync(0xffffffffu, kk == key);
+    const uint32_t idx = (base + p + lane) & (hcap - 1);
+    const unsigned long long kk = keys[idx];
+    const unsigned m = __ballot_sync(0xffffffffu, kk == key);
     if (m) return (int)vals[__shfl_sync(0xffffffffu, idx, __ffs(m) - 1)];
-    unsigned e = __ballot_sync(0xffffffffu, kk == 0ull);
+    const unsigned e = __ballot_sync(0xffffffffu, kk == 0ull);
     if (e) { *empty_slot = __shfl_sync(0xffffffffu, idx, __ffs(e) - 1); return -1; }
   }
   *empty_slot = 0xffffffffu;
   return -1;
 }
 
-__device__ __forceinline__ float walk_u(float z, double b, float inv_tau) {
-  return __fmaf_rn(z, inv_tau, (float)b);
-}
-__device__ __forceinline__ double b_step(double b, float pt, bool is_t, double alpha) {
-  return __fma_rn(-alpha, __dsub_rn((double)pt, is_t ? 1.0 : 0.0), b);
-}
-__device__ __forceinline__ uint32_t quant(float p, double TmV) {
-  double q = floor(__dmul_rn((double)p, TmV));
-  return q < 1.0 ? 1u : (uint32_t)q;
+// Prediction for token i (one warp): a0f and the merged sparse list, ids in order
+// of first appearance over k = 1..4 then slots, adds accumulated in that order.
+// `spadd` (global, zero) and `bitmap` (zero) are scratch and are left zero.
+__device__ void ng_predict_warp(const WalkArgs &a, int c, uint32_t i, const uint32_t *hist, float *spadd,
+                                uint32_t *bitmap, NgTok *out, int lane) {
+  double mu[kMaxOrders + 1], beta[kMaxOrders + 1];
+  int rec[kMaxOrders + 1];
+  for (int k = 1; k <= kMaxOrders; ++k) { mu[k] = 1.0; beta[k] = 0.0; rec[k] = -1; }
+  for (int k = 1; k <= (int)a.orders; ++k) {
+    if (i < (uint32_t)k) continue;
+    const size_t tb = (size_t)c * kMaxOrders + (k - 1);
+    uint32_t es;
+    const int r = ng_probe(a.ng_keys + tb * a.hcap, a.ng_vals + tb * a.hcap, a.hcap, fnv_ctx(k, hist), lane, &es);
+    if (r < 0) continue;
+    const NgRecord *R = a.ng_recs + tb * a.rcap + r;
+    const uint32_t ns = R->nslot;
+    uint32_t s = 0;
+    if ((uint32_t)lane < ns) s += R->cnt[lane];
+    if ((uint32_t)lane + 32 < ns) s += R->cnt[lane + 32];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const double n = (double)R->n;
+    const double lam = __ddiv_rn(n, __dadd_rn(n, 5.0));
+    mu[k] = __dsub_rn(1.0, __ddiv_rn(__dmul_rn(lam, (double)s), n));
+    beta[k] = __ddiv_rn(lam, n);
+    rec[k] = r;
+  }
+  double a0 = 1.0;
+  for (int k = 1; k <= (int)a.orders; ++k) a0 = __dmul_rn(a0, mu[k]);
+  uint32_t nout = 0;
+  for (int k = 1; k <= (int)a.orders; ++k) {
+    if (rec[k] < 0) continue;
+    double ak = beta[k];
+    for (int j = k + 1; j <= (int)a.orders; ++j) ak = __dmul_rn(ak, mu[j]);
+    const size_t tb = (size_t)c * kMaxOrders + (k - 1);
+    const NgRecord *R = a.ng_recs + tb * a.rcap + rec[k];
+    const uint32_t ns = R->nslot;
+    for (uint32_t s0 = 0; s0 < ns; s0 += 32) {
+      const uint32_t s = s0 + lane;
+      const bool act = s < ns;
+      uint32_t tk = 0;
+      bool first = false;
+      if (act) {
+        tk = R->tok[s];
+        const float add = (float)__dmul_rn(ak, (double)R->cnt[s]);
+        const uint32_t bit = 1u << (tk & 31);
+        first = !(atomicOr(&bitmap[tk >> 5], bit) & bit);
+        spadd[tk] = first ? add : __fadd_rn(spadd[tk], add);     // ids are unique within one order
+      }
+      const unsigned fm = __ballot_sync(0xffffffffu, act && first);
+      if (act && first) out->tok[nout + __popc(fm & ((1u << lane) - 1))] = tk;
+      nout += __popc(fm);
+    }
+    __syncwarp();
+    __threadfence_block();
+  }
+  for (uint32_t j = lane; j < nout; j += 32) {
+    const uint32_t tk = out->tok[j];
+    out->add[j] = spadd[tk];
+    spadd[tk] = 0.f;
+    bitmap[tk >> 5] = 0u;
+  }
+  if (lane == 0) {
+    out->n = nout;
+    out->a0f = (float)__ddiv_rn(a0, (double)i + (double)a.V);
+  }
+  __syncwarp();
 }
 
-// Thread t owns the float4 groups g = t, t + WT, t + 2 WT, ... of the vocab row
-// (coalesced 128-bit loads of z, 2 x 128-bit loads of the f64 bias).
-struct Grp {
-  float pt[4], png[4], p[4];
-};
+// Count update with token t after token i (one warp): P:375-387, D19-D22.
+__device__ void ng_update_warp(const WalkArgs &a, int c, uint32_t i, const uint32_t *hist, uint32_t t,
+                               WalkState *st, int lane) {
+  for (int k = 1; k <= (int)a.orders; ++k) {
+    if (i < (uint32_t)k) continue;
+    const size_t tb = (size_t)c * kMaxOrders + (k - 1);
+    unsigned long long *keys = a.ng_keys + tb * a.hcap;
+    uint32_t *vals = a.ng_vals + tb * a.hcap;
+    const unsigned long long key = fnv_ctx(k, hist);
+    uint32_t es = 0xffffffffu;
+    int r = ng_probe(keys, vals, a.hcap, key, lane, &es);
+    if (r < 0) {
+      const uint32_t used = st->nrec[k - 1];
+      if (used >= a.cap || used >= a.rcap || es == 0xffffffffu) continue;   // capacity freeze (D22)
+      r = (int)used;
+      if (lane == 0) {
+        st->nrec[k - 1] = used + 1;
+        keys[es] = key; vals[es] = (uint32_t)r;
+        a.ng_recs[tb * a.rcap + r].n = 0;
+        a.ng_recs[tb * a.rcap + r].nslot = 0;
+      }
+      __syncwarp();
+      __threadfence_block();
+    }
+    NgRecord *R = a.ng_recs + tb * a.rcap + r;
+    const uint32_t ns = R->nslot;
+    const bool h0 = (uint32_t)lane < ns && R->tok[lane] == t;
+    const bool h1 = (uint32_t)lane + 32 < ns && R->tok[lane + 32] == t;
+    const unsigned m0 = __ballot_sync(0xffffffffu, h0), m1 = __ballot_sync(0xffffffffu, h1);
+    if (m0 | m1) {
+      if (h0) R->cnt[lane] += 1;
+      if (h1) R->cnt[lane + 32] += 1;
+    } else if (ns < kSlots) {
+      if (lane == 0) { R->tok[ns] = t; R->cnt[ns] = 1; R->nslot = ns + 1; }
+    } else {   // evict the lowest count, ties -> lowest slot (D21)
+      uint32_t bcnt = R->cnt[lane], bidx = lane;
+      if (R->cnt[lane + 32] < bcnt) { bcnt = R->cnt[lane + 32]; bidx = lane + 32; }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const uint32_t oc = __shfl_xor_sync(0xffffffffu, bcnt, o), oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+        if (oc < bcnt || (oc == bcnt && oi < bidx)) { bcnt = oc; bidx = oi; }
+      }
+      if (lane == 0) { R->tok[bidx] = t; R->cnt[bidx] = 1; }
+    }
+    if (lane == 0) R->n += 1;
+    __syncwarp();
+    __threadfence_block();
+  }
+}
 
+__device__ __forceinline__ void ng_hist_push(WalkState *st, uint32_t t) {
+  st->hist[0] = st->hist[1]; st->hist[1] = st->hist[2]; st->hist[2] = st->hist[3]; st->hist[3] = t;
+}
+
+// ---------------------------------------------------- N-gram precompute ---
+__global__ void ngram_pre_kernel(WalkArgs a) {
+  extern __shared__ uint32_t bitmap[];   // V/32 words
+  const int lane = threadIdx.x;
+  const int e = blockIdx.x;
+  if (e >= a.n_entries) return;
+  const int c = a.chunk_of[e], count = a.count[e];
+  WalkState *st = a.st + c;
+  for (int w = lane; w < (int)((a.V + 31) / 32); w += 32) bitmap[w] = 0u;
+  __syncwarp();
+  float *spadd = a.ng_spadd + (size_t)c * a.V;
+  for (int it = 0; it < count; ++it) {
+    const uint32_t i = st->ng_i;
+    const uint32_t t = a.tokens[a.tok_off[c] + i];
+    uint32_t hist[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) hist[j] = st->hist[j];
+    NgTok *out = a.ng_pre + (size_t)c * a.ng_ring + (i % a.ng_ring);
+    if (i >= a.warmup) {
+      ng_predict_warp(a, c, i, hist, spadd, bitmap, out, lane);
+    } else if (lane == 0) {
+      out->n = 0;
+      out->a0f = 0.f;
+    }
+    ng_update_warp(a, c, i, hist, t, st, lane);
+    if (lane == 0) {
+      ng_hist_push(st, t);
+      st->ng_i = i + 1;
+    }
+    __syncwarp();
+    __threadfence_block();
+  }
+}
+
+void launch_ngram_precompute(const WalkArgs &a, cudaStream_t s) {
+  if (a.n_entries <= 0) return;
+  ngram_pre_kernel<<<a.n_entries, 32, ((a.V + 31) / 32) * sizeof(uint32_t), s>>>(a);
+}
+
+// ---------------------------------------------------------------- walk ---
 __global__ __launch_bounds__(WT, 1) void walk_kernel(WalkArgs a) {
   extern __shared__ uint32_t dyn[];
   const uint32_t V = a.V;
   const int G = (int)(V / 4);
-  uint32_t *bitmap = dyn;                              // V/32 words: ids with N-gram fixups
+  uint32_t *bitmap = dyn;                              // V/32 words: ids with N-gram fixups this token
   uint32_t *gsum = dyn + (V + 31) / 32;                // decode: per-group counts (G words)
   __shared__ WalkSmem sm;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -105,243 +305,276 @@ __global__ __launch_bounds__(WT, 1) void walk_kernel(WalkArgs a) {
   uint32_t *cu = a.cu + (size_t)c * V;
   float *spadd = a.spadd + (size_t)c * V;
   const bool use_ng = a.flags & 1u, use_head = a.flags & 2u;
+  const bool enc = a.mode == 0;
   const uint64_t T = 1ull << a.cdf_bits;
-  const double TmV = (double)(T - V);
+  const float TmV = (float)(T - V);
+  const float inv_tau = a.inv_tau;
   const unsigned long long HALF = 1ull << 31, QTR = 1ull << 30;
 
   for (int w = tid; w < (int)((V + 31) / 32); w += WT) bitmap[w] = 0u;
-  if (a.mode == 1 && tid == 0 && st->i == 0) {   // prime the decoder with 32 bits
+  if (!enc && tid == 0 && st->i == 0) {   // prime the decoder with 32 bits
     const uint8_t *s = a.streams + a.stream_off[c];
-    unsigned long long v = 0, nb = a.stream_bits[c];
-    for (int k = 0; k < 32; ++k) v = 2 * v + (k < (long long)nb ? (s[k >> 3] >> (7 - (k & 7))) & 1u : 0u);
+    const unsigned long long nb = a.stream_bits[c];
+    unsigned long long v = 0;
+    for (int k = 0; k < 32; ++k) v = 2 * v + ((unsigned long long)k < nb ? (s[k >> 3] >> (7 - (k & 7))) & 1u : 0u);
     st->low = 0; st->high = 0xFFFFFFFFull; st->value = v; st->bitpos = 32;
   }
   __syncthreads();
 
+  auto load_u = [&](const float *z, int g, float u[4]) {
+    const float4 z4 = reinterpret_cast<const float4 *>(z)[g];
+    if (use_head) {
+      const double2 b01 = reinterpret_cast<const double2 *>(b)[2 * g];
+      const double2 b23 = reinterpret_cast<const double2 *>(b)[2 * g + 1];
+      u[0] = walk_u(z4.x, b01.x, inv_tau); u[1] = walk_u(z4.y, b01.y, inv_tau);
+      u[2] = walk_u(z4.z, b23.x, inv_tau); u[3] = walk_u(z4.w, b23.y, inv_tau);
+    } else {
+      u[0] = walk_u(z4.x, 0.0, inv_tau); u[1] = walk_u(z4.y, 0.0, inv_tau);
+      u[2] = walk_u(z4.z, 0.0, inv_tau); u[3] = walk_u(z4.w, 0.0, inv_tau);
+    }
+  };
+  // block-wide (max, sum exp) of u over the row z -> sm.M, sm.invS
+  auto softmax_stats = [&](const float *z) {
+    float tm = -CUDART_INF_F, ts = 0.f;
+    for (int g = tid; g < G; g += WT) {
+      float u[4];
+      load_u(z, g, u);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) ms_push(tm, ts, u[j]);
+    }
+    ms_warp(tm, ts);
+    if (lane == 0) { sm.red_m[wid] = tm; sm.red_s[wid] = ts; }
+    __syncthreads();
+    if (wid == 0) {
+      tm = sm.red_m[lane]; ts = sm.red_s[lane];
+      ms_warp(tm, ts);
+      if (lane == 0) { sm.M = tm; sm.invS = __frcp_rn(ts); }
+    }
+    __syncthreads();
+  };
+  // warp 0: make token i's sparse list live (spadd + bitmap) and its scalars
+  auto scatter_list = [&](uint32_t i) {
+    const NgTok &L = sm.lists[i & 1];
+    const int mix = (use_ng && i >= a.warmup) ? 1 : 0;
+    const int n = mix ? (int)L.n : 0;
+    for (int j = lane; j < n; j += 32) {
+      const uint32_t tk = L.tok[j];
+      spadd[tk] = L.add[j];
+      atomicOr(&bitmap[tk >> 5], 1u << (tk & 31));
+    }
+    if (lane == 0) { sm.mix = mix; sm.nsp = n; sm.a0f = mix ? L.a0f : 0.f; }
+  };
+  auto clear_list = [&](uint32_t i) {
+    const NgTok &L = sm.lists[i & 1];
+    for (int j = lane; j < sm.nsp; j += 32) {
+      const uint32_t tk = L.tok[j];
+      spadd[tk] = 0.f;
+      bitmap[tk >> 5] = 0u;
+    }
+  };
+  // one warp: asynchronous copy (cp.async) of token i's precomputed list into smem
+  auto prefetch_pre = [&](uint32_t i) {
+    const char *src = reinterpret_cast<const char *>(a.ng_pre + (size_t)c * a.ng_ring + (i % a.ng_ring));
+    char *dst = reinterpret_cast<char *>(&sm.lists[i & 1]);
+    for (int ofs = lane * 16; ofs < (int)sizeof(NgTok); ofs += 32 * 16)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst + ofs)),
+                   "l"(src + ofs)
+                   : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  auto prefetch_wait = [&]() { asm volatile("cp.async.wait_all;" ::: "memory"); };
+
+  // the 4 probabilities of group g for the current token (identical code in every pass)
+  auto prob4 = [&](const float *z, int g, float M, float invS, float wl, float wn, float a0f, int mix, float pt[4],
+                   float png[4], float p[4]) {
+    float u[4];
+    load_u(z, g, u);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) pt[j] = __fmul_rn(fexp(__fsub_rn(u[j], M)), invS);
+    if (!mix) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) { png[j] = 0.f; p[j] = pt[j]; }
+      return;
+    }
+    const uint4 c4 = reinterpret_cast<const uint4 *>(cu)[g];
+    const uint32_t cc[4] = {c4.x, c4.y, c4.z, c4.w};
+    const uint32_t bits = (bitmap[g >> 3] >> ((g & 7) * 4)) & 15u;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) p[j] = mix_p(pt[j], a0f, cc[j], (bits >> j) & 1u ? spadd[4 * g + j] : 0.f, wl, wn, png[j]);
+  };
+
+  // thread 0, after t is known: mixer update and the next weights
+  auto mixer_update = [&](float pt_t, float png_t) {
+    double l0 = __dadd_rn(st->lw[0], __dmul_rn(a.eta, log(fmax((double)pt_t, 1e-12))));
+    double l1 = __dadd_rn(st->lw[1], __dmul_rn(a.eta, log(fmax((double)png_t, 1e-12))));
+    double mx = fmax(l0, l1);
+    double lse = __dadd_rn(mx, log(__dadd_rn(exp(__dsub_rn(l0, mx)), exp(__dsub_rn(l1, mx)))));
+    l0 = __dsub_rn(l0, lse);
+    l1 = __dsub_rn(l1, lse);
+    st->lw[0] = l0;
+    st->lw[1] = l1;
+    st->wl = (float)exp(l0);     // lw is renormalised: softmax(lw) = exp(lw) (to ~1e-16)
+    st->wn = (float)exp(l1);
+  };
+
+  // block reduction of (sum c, cum, argmax) -> warp 0 lane 0 holds the totals
+  auto reduce_counts = [&](unsigned long long s1, unsigned long long s2, Best bb) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+      s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+      best_merge(bb, __shfl_xor_sync(0xffffffffu, bb.v, o), __shfl_xor_sync(0xffffffffu, bb.i, o),
+                 __shfl_xor_sync(0xffffffffu, bb.c, o));
+    }
+    if (lane == 0) { sm.red_sum[wid] = s1; sm.red_cum[wid] = s2; sm.red_bv[wid] = bb.v; sm.red_bi[wid] = bb.i; sm.red_bc[wid] = bb.c; }
+  };
+  auto finish_counts = [&](int tok) {   // warp 0, after a __syncthreads
+    unsigned long long s1 = sm.red_sum[lane], s2 = sm.red_cum[lane];
+    Best bb{sm.red_bv[lane], sm.red_bi[lane], sm.red_bc[lane]};
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+      s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+      best_merge(bb, __shfl_xor_sync(0xffffffffu, bb.v, o), __shfl_xor_sync(0xffffffffu, bb.i, o),
+                 __shfl_xor_sync(0xffffffffu, bb.c, o));
+    }
+    if (lane == 0) {
+      const long long R = (long long)T - (long long)s1;
+      sm.resid = R;
+      sm.argmax = bb.i;
+      if ((long long)bb.c + R < 1) st->err = 1;      // D6: residual would drop a count below 1
+      if (tok >= 0) {
+        sm.cum_t = s2 + (bb.i < tok ? R : 0);
+        sm.freq_t = sm.freq_t + (bb.i == tok ? R : 0);
+      }
+    }
+  };
+
+  if (enc) {
+    // ===================================================== compression ===
+    if (wid == 0) {
+      const uint32_t i0 = st->i;
+      if (use_ng && i0 >= a.warmup) { prefetch_pre(i0); prefetch_wait(); __syncwarp(); }
+      scatter_list(i0);
+    }
+    softmax_stats(a.logits + (size_t)row0 * a.ldl);
+    for (int it = 0; it < count; ++it) {
+      const float *z = a.logits + (size_t)(row0 + it) * a.ldl;
+      const bool has_next = it + 1 < count;
+      const float *zn = a.logits + (size_t)(row0 + it + 1) * a.ldl;
+      const uint32_t i = st->i;
+      const int tok = (int)a.tokens[a.tok_off[c] + i];
+      const float M = sm.M, invS = sm.invS, a0f = sm.a0f, wl = st->wl, wn = st->wn;
+      const int mix = sm.mix;
+      const bool pre_next = has_next && use_ng && i + 1 >= a.warmup;
+      if (wid == 1 && pre_next) prefetch_pre(i + 1);
+      unsigned long long my_sum = 0, my_cum = 0;
+      Best bb{-1.f, 0x7fffffff, 0};
+      float tm = -CUDART_INF_F, ts = 0.f;   // next token's softmax statistics
+      for (int g = tid; g < G; g += WT) {
+        float pt[4], png[4], p[4];
+        prob4(z, g, M, invS, wl, wn, a0f, mix, pt, png, p);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int v = 4 * g + j;
+          const uint32_t cv = quant(p[j], TmV);
+          my_sum += cv;
+          if (p[j] > bb.v) { bb.v = p[j]; bb.i = v; bb.c = cv; }
+          if (v < tok) my_cum += cv;
+          if (v == tok) { sm.pt_t = pt[j]; sm.png_t = png[j]; sm.p_t = p[j]; sm.freq_t = cv; }
+        }
+        if (use_head) {
+          double2 *bp = reinterpret_cast<double2 *>(b) + 2 * g;
+          double2 b01 = bp[0], b23 = bp[1];
+          const int v = 4 * g;
+          b01.x = b_step(b01.x, pt[0], v == tok, a.alpha);
+          b01.y = b_step(b01.y, pt[1], v + 1 == tok, a.alpha);
+          b23.x = b_step(b23.x, pt[2], v + 2 == tok, a.alpha);
+          b23.y = b_step(b23.y, pt[3], v + 3 == tok, a.alpha);
+          bp[0] = b01; bp[1] = b23;
+        }
+        if (has_next) {
+          float u[4];
+          load_u(zn, g, u);           // b already updated for this group
+#pragma unroll
+          for (int j = 0; j < 4; ++j) ms_push(tm, ts, u[j]);
+        }
+      }
+      reduce_counts(my_sum, my_cum, bb);
+      ms_warp(tm, ts);
+      if (lane == 0) { sm.red_m[wid] = tm; sm.red_s[wid] = ts; }
+      if (wid == 1 && pre_next) prefetch_wait();
+      __syncthreads();
+      if (wid == 0) {
+        finish_counts(tok);
+        tm = sm.red_m[lane]; ts = sm.red_s[lane];
+        ms_warp(tm, ts);
+        if (lane == 0) {
+          const size_t oi = (size_t)a.tok_off[c] + i;
+          a.out_cum[oi] = (uint32_t)sm.cum_t;
+          a.out_freq[oi] = (uint32_t)sm.freq_t;
+          if (a.out_p) a.out_p[oi] = sm.p_t;
+          if (mix) mixer_update(sm.pt_t, sm.png_t);
+          if (use_ng) cu[tok] += 1u;
+          st->i = i + 1;
+          if (has_next) { sm.M = tm; sm.invS = __frcp_rn(ts); }
+        }
+        __syncwarp();
+        clear_list(i);
+        __syncwarp();
+        if (has_next) scatter_list(i + 1);
+      }
+      __syncthreads();
+    }
+    return;
+  }
+
+  // ======================================================== decompression ===
   for (int it = 0; it < count; ++it) {
     const float *z = a.logits + (size_t)(row0 + it) * a.ldl;
     const uint32_t i = st->i;
-
-    // ---------------- phase A: N-gram prediction + mixer weights (warp 0) ----
     if (wid == 0) {
-      const int mix = (use_ng && i >= a.warmup) ? 1 : 0;
-      int nsp = 0;
-      if (mix) {
+      if (use_ng && i >= a.warmup) {
         uint32_t hist[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) hist[j] = st->hist[j];
-        double mu[kMaxOrders + 1], beta[kMaxOrders + 1];
-        int rec[kMaxOrders + 1];
-        for (int k = 1; k <= kMaxOrders; ++k) { mu[k] = 1.0; beta[k] = 0.0; rec[k] = -1; }
-        for (int k = 1; k <= (int)a.orders; ++k) {
-          if (i < (uint32_t)k) continue;
-          const size_t tb = ((size_t)c * kMaxOrders + (k - 1));
-          uint32_t es;
-          int r = ng_probe(a.ng_keys + tb * a.hcap, a.ng_vals + tb * a.hcap, a.hcap, fnv_ctx(k, hist), lane, &es);
-          if (r < 0) continue;
-          const NgRecord *R = a.ng_recs + tb * a.rcap + r;
-          uint32_t ns = R->nslot, s = 0;
-          if ((uint32_t)lane < ns) s += R->cnt[lane];
-          if ((uint32_t)lane + 32 < ns) s += R->cnt[lane + 32];
-#pragma unroll
-          for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-          const double n = (double)R->n;
-          const double lam = __ddiv_rn(n, __dadd_rn(n, 5.0));
-          mu[k] = __dsub_rn(1.0, __ddiv_rn(__dmul_rn(lam, (double)s), n));
-          beta[k] = __ddiv_rn(lam, n);
-          rec[k] = r;
-        }
-        double a0 = 1.0;
-        for (int k = 1; k <= (int)a.orders; ++k) a0 = __dmul_rn(a0, mu[k]);
-        for (int k = 1; k <= (int)a.orders; ++k) {
-          if (rec[k] < 0) continue;
-          double ak = beta[k];
-          for (int j = k + 1; j <= (int)a.orders; ++j) ak = __dmul_rn(ak, mu[j]);
-          const size_t tb = ((size_t)c * kMaxOrders + (k - 1));
-          const NgRecord *R = a.ng_recs + tb * a.rcap + rec[k];
-          const uint32_t ns = R->nslot;
-          for (uint32_t s = lane; s < ns; s += 32) {
-            const uint32_t tk = R->tok[s];
-            spadd[tk] = __fadd_rn(spadd[tk], (float)__dmul_rn(ak, (double)R->cnt[s]));
-            atomicOr(&bitmap[tk >> 5], 1u << (tk & 31));
-            sm.sp_tok[nsp + s] = tk;
-          }
-          nsp += (int)ns;
-          __syncwarp();
-          __threadfence_block();
-        }
-        if (lane == 0) {
-          const double l0 = st->lw[0], l1 = st->lw[1];
-          const double mx = fmax(l0, l1);
-          const double lse = __dadd_rn(mx, log(__dadd_rn(exp(__dsub_rn(l0, mx)), exp(__dsub_rn(l1, mx)))));
-          sm.wl = (float)exp(__dsub_rn(l0, lse));
-          sm.wn = (float)exp(__dsub_rn(l1, lse));
-          sm.a0f = (float)__ddiv_rn(a0, (double)st->N + (double)V);
-        }
+        ng_predict_warp(a, c, i, hist, spadd, bitmap, &sm.lists[i & 1], lane);
       }
-      if (lane == 0) {
-        sm.mix = mix;
-        sm.sp_n = nsp;
-        sm.tok = (a.mode == 0) ? (int)a.tokens[a.tok_off[c] + i] : -1;
-        if (a.mode == 1) {   // WNC decode target (D8)
-          const unsigned long long R = st->high - st->low + 1;
-          sm.target = ((st->value - st->low + 1) * T - 1) / R;
-        }
+      scatter_list(i);
+      if (lane == 0) {   // WNC decode target (D8)
+        const unsigned long long R = st->high - st->low + 1;
+        sm.target = ((st->value - st->low + 1) * T - 1) / R;
+        sm.tok = -1;
       }
     }
     __syncthreads();
-
-    const float inv_tau = a.inv_tau;
-    auto load_u = [&](int g, float u[4]) {
-      const float4 z4 = reinterpret_cast<const float4 *>(z)[g];
-      if (use_head) {
-        const double2 b01 = reinterpret_cast<const double2 *>(b)[2 * g];
-        const double2 b23 = reinterpret_cast<const double2 *>(b)[2 * g + 1];
-        u[0] = walk_u(z4.x, b01.x, inv_tau); u[1] = walk_u(z4.y, b01.y, inv_tau);
-        u[2] = walk_u(z4.z, b23.x, inv_tau); u[3] = walk_u(z4.w, b23.y, inv_tau);
-      } else {
-        u[0] = walk_u(z4.x, 0.0, inv_tau); u[1] = walk_u(z4.y, 0.0, inv_tau);
-        u[2] = walk_u(z4.z, 0.0, inv_tau); u[3] = walk_u(z4.w, 0.0, inv_tau);
-      }
-    };
-
-    // ---------------- pass 1: max and sum of exp (per-thread online, fixed tree) ----
-    {
-      float tm = -CUDART_INF_F, ts = 0.f;
-      for (int g = tid; g < G; g += WT) {
-        float u[4];
-        load_u(g, u);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          if (u[j] > tm) { ts = __fmaf_rn(ts, expf(__fsub_rn(tm, u[j])), 1.f); tm = u[j]; }
-          else ts = __fadd_rn(ts, expf(__fsub_rn(u[j], tm)));
-        }
-      }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        const float om = __shfl_xor_sync(0xffffffffu, tm, o), os = __shfl_xor_sync(0xffffffffu, ts, o);
-        const float mm = fmaxf(tm, om);
-        const float e1 = (tm == -CUDART_INF_F) ? 0.f : expf(__fsub_rn(tm, mm));
-        const float e2 = (om == -CUDART_INF_F) ? 0.f : expf(__fsub_rn(om, mm));
-        ts = __fadd_rn(__fmul_rn(ts, e1), __fmul_rn(os, e2));
-        tm = mm;
-      }
-      if (lane == 0) { sm.red_m[wid] = tm; sm.red_s[wid] = ts; }
-      __syncthreads();
-      if (wid == 0) {
-        tm = sm.red_m[lane]; ts = sm.red_s[lane];
-#pragma unroll
-        for (int o = 16; o; o >>= 1) {
-          const float om = __shfl_xor_sync(0xffffffffu, tm, o), os = __shfl_xor_sync(0xffffffffu, ts, o);
-          const float mm = fmaxf(tm, om);
-          const float e1 = (tm == -CUDART_INF_F) ? 0.f : expf(__fsub_rn(tm, mm));
-          const float e2 = (om == -CUDART_INF_F) ? 0.f : expf(__fsub_rn(om, mm));
-          ts = __fadd_rn(__fmul_rn(ts, e1), __fmul_rn(os, e2));
-          tm = mm;
-        }
-        if (lane == 0) { sm.M = tm; sm.S = __frcp_rn(ts); }
-      }
-      __syncthreads();
-    }
-    const float M = sm.M, invS = sm.S, a0f = sm.a0f, wl = sm.wl, wn = sm.wn;
-    const int mix = sm.mix, tok = sm.tok;
-
-    // p for the 4 ids of group g (identical code in every pass that needs it)
-    auto prob4 = [&](int g, Grp &q) {
-      float u[4];
-      load_u(g, u);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) q.pt[j] = __fmul_rn(expf(__fsub_rn(u[j], M)), invS);
-      if (!mix) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) { q.png[j] = 0.f; q.p[j] = q.pt[j]; }
-        return;
-      }
-      const uint4 c4 = reinterpret_cast<const uint4 *>(cu)[g];
-      const uint32_t cc[4] = {c4.x, c4.y, c4.z, c4.w};
-      const uint32_t bits = (bitmap[g >> 3] >> ((g & 7) * 4)) & 15u;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float sp = (bits >> j) & 1u ? spadd[4 * g + j] : 0.f;
-        q.png[j] = __fmaf_rn(a0f, (float)(cc[j] + 1u), sp);
-        q.p[j] = __fmaf_rn(wl, q.pt[j], __fmul_rn(wn, q.png[j]));
-      }
-    };
-
-    // ---------------- pass 2: p, counts, sums, argmax (+ b update when t is known) ----
-    unsigned long long my_sum = 0, my_cum = 0;
-    float bv = -1.f; int bi = 0x7fffffff; uint32_t bc = 0;
+    softmax_stats(z);
+    const float M = sm.M, invS = sm.invS, a0f = sm.a0f, wl = st->wl, wn = st->wn;
+    const int mix = sm.mix;
+    unsigned long long my_sum = 0;
+    Best bb{-1.f, 0x7fffffff, 0};
     for (int g = tid; g < G; g += WT) {
-      Grp q;
-      prob4(g, q);
+      float pt[4], png[4], p[4];
+      prob4(z, g, M, invS, wl, wn, a0f, mix, pt, png, p);
       uint32_t gs = 0;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const int v = 4 * g + j;
-        const uint32_t cv = quant(q.p[j], TmV);
+        const uint32_t cv = quant(p[j], TmV);
         gs += cv;
-        if (q.p[j] > bv) { bv = q.p[j]; bi = v; bc = cv; }
-        if (a.mode == 0) {
-          if (v < tok) my_cum += cv;
-          if (v == tok) { sm.pt_t = q.pt[j]; sm.png_t = q.png[j]; sm.p_t = q.p[j]; sm.freq_t = cv; }
-        }
+        if (p[j] > bb.v) { bb.v = p[j]; bb.i = 4 * g + j; bb.c = cv; }
       }
       my_sum += gs;
-      if (a.mode == 1) gsum[g] = gs;
-      if (a.mode == 0 && use_head) {
-        double2 *bp = reinterpret_cast<double2 *>(b) + 2 * g;
-        double2 b01 = bp[0], b23 = bp[1];
-        const int v = 4 * g;
-        b01.x = b_step(b01.x, q.pt[0], v == tok, a.alpha);
-        b01.y = b_step(b01.y, q.pt[1], v + 1 == tok, a.alpha);
-        b23.x = b_step(b23.x, q.pt[2], v + 2 == tok, a.alpha);
-        b23.y = b_step(b23.y, q.pt[3], v + 3 == tok, a.alpha);
-        bp[0] = b01; bp[1] = b23;
-      }
+      gsum[g] = gs;
     }
+    reduce_counts(my_sum, 0ull, bb);
+    __syncthreads();
+    if (wid == 0) {
+      finish_counts(-1);
+      if (lane == 0) gsum[sm.argmax >> 2] = (uint32_t)((long long)gsum[sm.argmax >> 2] + sm.resid);
+    }
+    __syncthreads();
+    // prefix scan over the groups in id order, search the target
     {
-      unsigned long long s1 = my_sum, s2 = my_cum;
-      float v_ = bv; int i_ = bi; uint32_t c_ = bc;
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-        const float ov = __shfl_xor_sync(0xffffffffu, v_, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, i_, o);
-        const uint32_t oc = __shfl_xor_sync(0xffffffffu, c_, o);
-        if (ov > v_ || (ov == v_ && oi < i_)) { v_ = ov; i_ = oi; c_ = oc; }
-      }
-      if (lane == 0) { sm.red_sum[wid] = s1; sm.red_cum[wid] = s2; sm.red_bv[wid] = v_; sm.red_bi[wid] = i_; sm.red_bc[wid] = c_; }
-      __syncthreads();
-      if (wid == 0) {
-        s1 = sm.red_sum[lane]; s2 = sm.red_cum[lane]; v_ = sm.red_bv[lane]; i_ = sm.red_bi[lane]; c_ = sm.red_bc[lane];
-#pragma unroll
-        for (int o = 16; o; o >>= 1) {
-          s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-          s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-          const float ov = __shfl_xor_sync(0xffffffffu, v_, o);
-          const int oi = __shfl_xor_sync(0xffffffffu, i_, o);
-          const uint32_t oc = __shfl_xor_sync(0xffffffffu, c_, o);
-          if (ov > v_ || (ov == v_ && oi < i_)) { v_ = ov; i_ = oi; c_ = oc; }
-        }
-        if (lane == 0) {
-          const long long R = (long long)T - (long long)s1;
-          sm.resid = R;
-          sm.argmax = i_;
-          if ((long long)c_ + R < 1) st->err = 1;      // D6: residual would drop a count below 1
-          if (a.mode == 0) {
-            sm.cum_t = s2 + (i_ < tok ? R : 0);
-            sm.freq_t = sm.freq_t + (i_ == tok ? R : 0);
-          } else {
-            gsum[i_ >> 2] = (uint32_t)((long long)gsum[i_ >> 2] + R);
-          }
-        }
-      }
-      __syncthreads();
-    }
-
-    if (a.mode == 1) {
-      // ---------------- decode: prefix scan over the groups (in id order), search the target ----
       const long long R = sm.resid;
       const int am = sm.argmax;
       const int gpt = (G + WT - 1) / WT;
@@ -363,7 +596,7 @@ __global__ __launch_bounds__(WT, 1) void walk_kernel(WalkArgs a) {
           const uint32_t z2 = __shfl_up_sync(0xffffffffu, y, o);
           if (lane >= o) y += z2;
         }
-        sm.scan[lane] = y;   // inclusive warp totals
+        sm.scan[lane] = y;
       }
       __syncthreads();
       const unsigned long long excl = (unsigned long long)(x - adj) + (wid ? sm.scan[wid - 1] : 0u);
@@ -375,52 +608,45 @@ __global__ __launch_bounds__(WT, 1) void walk_kernel(WalkArgs a) {
           if (tgt < accm + gsum[gf]) break;
           accm += gsum[gf];
         }
-        Grp q;
-        prob4(gf, q);
+        float pt[4], png[4], p[4];
+        prob4(z, gf, M, invS, wl, wn, a0f, mix, pt, png, p);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const int v = 4 * gf + j;
-          unsigned long long cv = quant(q.p[j], TmV);
+          unsigned long long cv = quant(p[j], TmV);
           if (v == am) cv = (unsigned long long)((long long)cv + R);
           if (tgt < accm + cv) {
-            sm.tok = v; sm.cum_t = accm; sm.freq_t = cv; sm.pt_t = q.pt[j]; sm.png_t = q.png[j]; sm.p_t = q.p[j];
+            sm.tok = v; sm.cum_t = accm; sm.freq_t = cv; sm.pt_t = pt[j]; sm.png_t = png[j]; sm.p_t = p[j];
             break;
           }
           accm += cv;
         }
       }
       if (tid == 0 && tgt >= T) st->err = 2;
-      __syncthreads();
-      // ---------------- decode: bias update now that t is known ----
-      const int t = sm.tok;
-      if (use_head)
-        for (int g = tid; g < G; g += WT) {
-          Grp q;
-          prob4(g, q);
-          double2 *bp = reinterpret_cast<double2 *>(b) + 2 * g;
-          double2 b01 = bp[0], b23 = bp[1];
-          const int v = 4 * g;
-          b01.x = b_step(b01.x, q.pt[0], v == t, a.alpha);
-          b01.y = b_step(b01.y, q.pt[1], v + 1 == t, a.alpha);
-          b23.x = b_step(b23.x, q.pt[2], v + 2 == t, a.alpha);
-          b23.y = b_step(b23.y, q.pt[3], v + 3 == t, a.alpha);
-          bp[0] = b01; bp[1] = b23;
-        }
     }
-
-    // ---------------- phase D: outputs, coder, mixer (thread 0), N-gram update (warp 0) ----
     __syncthreads();
     const int t = sm.tok;
-    if (tid == 0) {
-      const size_t oi = (size_t)a.tok_off[c] + i;
-      if (a.mode == 0) {
-        a.out_cum[oi] = (uint32_t)sm.cum_t;
-        a.out_freq[oi] = (uint32_t)sm.freq_t;
-        if (a.out_p) a.out_p[oi] = sm.p_t;
-      } else {
+    if (use_head)
+      for (int g = tid; g < G; g += WT) {
+        float pt[4], png[4], p[4];
+        prob4(z, g, M, invS, wl, wn, a0f, mix, pt, png, p);
+        double2 *bp = reinterpret_cast<double2 *>(b) + 2 * g;
+        double2 b01 = bp[0], b23 = bp[1];
+        const int v = 4 * g;
+        b01.x = b_step(b01.x, pt[0], v == t, a.alpha);
+        b01.y = b_step(b01.y, pt[1], v + 1 == t, a.alpha);
+        b23.x = b_step(b23.x, pt[2], v + 2 == t, a.alpha);
+        b23.y = b_step(b23.y, pt[3], v + 3 == t, a.alpha);
+        bp[0] = b01; bp[1] = b23;
+      }
+    __syncthreads();
+    if (wid == 0) {
+      if (lane == 0) {
+        const size_t oi = (size_t)a.tok_off[c] + i;
         if (t < 0) st->err = 3;
-        a.out_tok[oi] = (uint32_t)max(t, 0);
-        if (a.next_x) a.next_x[c] = (uint32_t)max(t, 0);
+        const uint32_t tt = (uint32_t)max(t, 0);
+        a.out_tok[oi] = tt;
+        if (a.next_x) a.next_x[c] = tt;
         if (a.out_p) a.out_p[oi] = sm.p_t;
         // consume the symbol (D8)
         const unsigned long long R = st->high - st->low + 1;
@@ -440,80 +666,22 @@ __global__ __launch_bounds__(WT, 1) void walk_kernel(WalkArgs a) {
           ++bp;
         }
         st->low = lo; st->high = hi; st->value = val; st->bitpos = bp;
+        if (mix) mixer_update(sm.pt_t, sm.png_t);
+        if (use_ng) cu[tt] += 1u;
+        st->i = i + 1;
       }
-      if (mix) {   // exponential-weights update, log clamp 1e-12
-        double l0 = __dadd_rn(st->lw[0], __dmul_rn(a.eta, log(fmax((double)sm.pt_t, 1e-12))));
-        double l1 = __dadd_rn(st->lw[1], __dmul_rn(a.eta, log(fmax((double)sm.png_t, 1e-12))));
-        const double mx = fmax(l0, l1);
-        const double lse = __dadd_rn(mx, log(__dadd_rn(exp(__dsub_rn(l0, mx)), exp(__dsub_rn(l1, mx)))));
-        st->lw[0] = __dsub_rn(l0, lse);
-        st->lw[1] = __dsub_rn(l1, lse);
-      }
-    }
-    if (wid == 0) {
-      // clear this step's fixups
-      const int nsp = sm.sp_n;
-      for (int k = lane; k < nsp; k += 32) {
-        const uint32_t tk = sm.sp_tok[k];
-        spadd[tk] = 0.f;
-        bitmap[tk >> 5] = 0u;
-      }
+      __syncwarp();
+      clear_list(i);
+      __syncwarp();
       if (use_ng && t >= 0) {
         uint32_t hist[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) hist[j] = st->hist[j];
-        for (int k = 1; k <= (int)a.orders; ++k) {
-          if (i < (uint32_t)k) continue;
-          const size_t tb = ((size_t)c * kMaxOrders + (k - 1));
-          unsigned long long *keys = a.ng_keys + tb * a.hcap;
-          uint32_t *vals = a.ng_vals + tb * a.hcap;
-          const unsigned long long key = fnv_ctx(k, hist);
-          uint32_t es = 0xffffffffu;
-          int r = ng_probe(keys, vals, a.hcap, key, lane, &es);
-          if (r < 0) {
-            const uint32_t used = st->nrec[k - 1];
-            if (used >= a.cap || used >= a.rcap || es == 0xffffffffu) continue;   // capacity freeze (D22)
-            r = (int)used;
-            if (lane == 0) {
-              st->nrec[k - 1] = used + 1;
-              keys[es] = key; vals[es] = (uint32_t)r;
-              a.ng_recs[tb * a.rcap + r].n = 0;
-              a.ng_recs[tb * a.rcap + r].nslot = 0;
-            }
-            __syncwarp();
-          }
-          NgRecord *R = a.ng_recs + tb * a.rcap + r;
-          const uint32_t ns = R->nslot;
-          const bool h0 = (uint32_t)lane < ns && R->tok[lane] == (uint32_t)t;
-          const bool h1 = (uint32_t)lane + 32 < ns && R->tok[lane + 32] == (uint32_t)t;
-          const unsigned m0 = __ballot_sync(0xffffffffu, h0), m1 = __ballot_sync(0xffffffffu, h1);
-          if (m0 | m1) {
-            if (h0) R->cnt[lane] += 1;
-            if (h1) R->cnt[lane + 32] += 1;
-          } else if (ns < kSlots) {
-            if (lane == 0) { R->tok[ns] = (uint32_t)t; R->cnt[ns] = 1; R->nslot = ns + 1; }
-          } else {   // evict the lowest count, ties -> lowest slot (D21)
-            uint32_t bcnt = R->cnt[lane], bidx = lane;
-            if (R->cnt[lane + 32] < bcnt) { bcnt = R->cnt[lane + 32]; bidx = lane + 32; }
-#pragma unroll
-            for (int o = 16; o; o >>= 1) {
-              const uint32_t oc = __shfl_xor_sync(0xffffffffu, bcnt, o), oi2 = __shfl_xor_sync(0xffffffffu, bidx, o);
-              if (oc < bcnt || (oc == bcnt && oi2 < bidx)) { bcnt = oc; bidx = oi2; }
-            }
-            if (lane == 0) { R->tok[bidx] = (uint32_t)t; R->cnt[bidx] = 1; }
-          }
-          if (lane == 0) R->n += 1;
-          __syncwarp();
-        }
+        ng_update_warp(a, c, i, hist, (uint32_t)t, st, lane);
         if (lane == 0) {
-          cu[t] += 1u;
-          st->N += 1;
+          ng_hist_push(st, (uint32_t)t);
+          st->ng_i = i + 1;
         }
-      }
-      if (lane == 0) {
-        st->hist[0] = st->hist[1]; st->hist[1] = st->hist[2]; st->hist[2] = st->hist[3];
-        st->hist[3] = (uint32_t)max(t, 0);
-        st->i = i + 1;
       }
     }
     __syncthreads();
@@ -522,7 +690,7 @@ __global__ __launch_bounds__(WT, 1) void walk_kernel(WalkArgs a) {
 
 void launch_walk(const WalkArgs &a, cudaStream_t s) {
   if (a.n_entries <= 0) return;
-  const size_t dyn = ((a.V + 31) / 32 + a.V / 4) * sizeof(uint32_t);
+  const size_t dyn = ((a.V + 31) / 32 + (a.mode == 1 ? a.V / 4 : 0)) * sizeof(uint32_t);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -532,11 +700,15 @@ void launch_walk(const WalkArgs &a, cudaStream_t s) {
 }
 
 __global__ void walk_init_kernel(WalkState *st, int n, double lw0, double lw1) {
-  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= n) return;
   WalkState w;
   memset(&w, 0, sizeof(w));
   w.lw[0] = lw0; w.lw[1] = lw1;
+  const double mx = fmax(lw0, lw1);
+  const double lse = __dadd_rn(mx, log(__dadd_rn(exp(__dsub_rn(lw0, mx)), exp(__dsub_rn(lw1, mx)))));
+  w.wl = (float)exp(__dsub_rn(lw0, lse));
+  w.wn = (float)exp(__dsub_rn(lw1, lse));
   w.high = 0xFFFFFFFFull;
   st[c] = w;
 }
@@ -550,7 +722,7 @@ __global__ void quantize_debug_kernel(const float *p, uint32_t V, uint32_t bits,
   __shared__ unsigned long long rs[NW];
   __shared__ float rv[NW]; __shared__ int ri[NW];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const double TmV = (double)((1ull << bits) - V);
+  const float TmV = (float)((1ull << bits) - V);
   unsigned long long s = 0; float bv = -1.f; int bi = 0x7fffffff;
   for (uint32_t v = tid; v < V; v += WT) {
     const uint32_t c = quant(p[v], TmV);

@@ -1,4 +1,5 @@
-// Per-chunk walk state and launcher for the vocab-row CDF kernel.
+// Per-chunk walk state and launchers for the vocab-row CDF kernel and the
+// N-gram precompute kernel.
 #pragma once
 #include <cuda_runtime.h>
 #include <cstdint>
@@ -7,6 +8,7 @@ namespace nc {
 
 constexpr int kSlots = 64;            // N-gram continuation cap
 constexpr int kMaxOrders = 4;         // context tables k = 1..4 (D18)
+constexpr int kMaxSparse = kMaxOrders * kSlots;
 
 struct NgRecord {                     // one context's continuation table
   uint32_t n;                         // context occurrences (never decremented, D19)
@@ -15,13 +17,24 @@ struct NgRecord {                     // one context's continuation table
   uint32_t cnt[kSlots];
 };
 
+// N-gram prediction of one token in closed form:
+//   p_ng(v) = a0f * (c(v) + 1) + add[v]  (add = sum_k a_k cnt_k(v), merged in order k = 1..4)
+struct __align__(16) NgTok {
+  uint32_t n;                         // number of distinct sparse ids
+  float a0f;                          // a0 / (N + V) as f32, N = tokens seen = i
+  uint32_t pad[2];
+  uint32_t tok[kMaxSparse];
+  float add[kMaxSparse];
+};
+
 struct WalkState {                    // per chunk, device resident
   double lw[2];                       // mixer log-weights
-  uint32_t i;                         // tokens walked so far
-  uint32_t N;                         // unigram total
-  uint32_t hist[4];                   // last 4 tokens (oldest first)
+  uint32_t i;                         // tokens walked so far (walk kernel)
+  uint32_t ng_i;                      // tokens seen by the N-gram (precompute / inline)
+  uint32_t hist[4];                   // last 4 tokens (oldest first), N-gram side
   uint32_t nrec[kMaxOrders];          // records in use per order
   uint32_t err;                       // nonzero = integrity failure
+  float wl, wn;                       // current mixer weights (softmax of lw) as f32
   uint32_t pad;
   // device WNC decoder (D27)
   unsigned long long low, high, value, bitpos;
@@ -29,13 +42,16 @@ struct WalkState {                    // per chunk, device resident
 
 struct WalkArgs {
   // per launch: entry e handles chunk chunk_of[e], rows [row0[e], row0[e]+count[e]) of logits,
-  // tokens [tok0[e], ...) of the chunk (absolute token index in the chunk = st.i)
+  // i.e. tokens st.i .. st.i + count - 1 of that chunk
   const int32_t *chunk_of, *row0, *count;
   int n_entries;
   const float *logits; int64_t ldl;
   // encode inputs / outputs, indexed by tok_off[c] + i
   const uint32_t *tokens; const int64_t *tok_off;
   uint32_t *out_cum, *out_freq; float *out_p;
+  NgTok *ng_pre;                      // encode: precomputed N-gram predictions, ring of ng_ring per chunk:
+  uint32_t ng_ring;                   //   token i of chunk c at ng_pre[c * ng_ring + i % ng_ring]
+  float *ng_spadd;                    // precompute scratch (separate from the walk's spadd)
   // decode
   const uint8_t *streams; const int64_t *stream_off; const uint64_t *stream_bits;
   uint32_t *out_tok; uint32_t *next_x;
@@ -50,6 +66,8 @@ struct WalkArgs {
 };
 
 void launch_walk(const WalkArgs &a, cudaStream_t s);
+// encode only: N-gram predictions for the entries' tokens (one warp per chunk)
+void launch_ngram_precompute(const WalkArgs &a, cudaStream_t s);
 void launch_walk_init(WalkState *st, int n_chunks, cudaStream_t s);
 void launch_quantize_debug(const float *p, uint32_t V, uint32_t cdf_bits, uint32_t *counts, cudaStream_t s);
 
