@@ -246,20 +246,26 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&s_empty[sb]);
       const int key0 = (kb0 + i) * AK;
+      // scores in the log2 domain: x = S * (1/8 * log2 e); p = 2^(x - m)
+      constexpr float kScale = 0.125f * 1.44269504088896341f;
       float s[32];
       float mb = -CUDART_INF_F;
+      if (key0 + 31 <= j) {                  // whole block inside the window: no masking
 #pragma unroll
-      for (int k = 0; k < 32; ++k) {
-        const bool ok = key0 + k <= j;       // keys >= w(j) by construction of the block range
-        s[k] = ok ? __fmul_rn(__uint_as_float(sr[k]), 0.125f) : -CUDART_INF_F;
-        mb = fmaxf(mb, s[k]);
+        for (int k = 0; k < 32; ++k) { s[k] = __fmul_rn(__uint_as_float(sr[k]), kScale); mb = fmaxf(mb, s[k]); }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          s[k] = key0 + k <= j ? __fmul_rn(__uint_as_float(sr[k]), kScale) : -CUDART_INF_F;
+          mb = fmaxf(mb, s[k]);
+        }
       }
       const float mn = fmaxf(m, mb);
-      const float alpha = (mn == -CUDART_INF_F) ? 1.f : expf(__fsub_rn(m, mn));
+      const float alpha = (mn == -CUDART_INF_F) ? 1.f : tc::ex2(__fsub_rn(m, mn));
       float ps = 0.f;
 #pragma unroll
       for (int k = 0; k < 32; ++k) {
-        s[k] = (s[k] == -CUDART_INF_F) ? 0.f : expf(__fsub_rn(s[k], mn));
+        s[k] = tc::ex2(__fsub_rn(s[k], mn));    // ex2(-inf) = 0 for masked keys
         ps = __fadd_rn(ps, s[k]);
       }
       l = __fmaf_rn(l, alpha, ps);

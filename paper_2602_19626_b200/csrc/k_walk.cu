@@ -29,6 +29,7 @@
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
+#include "tc_common.cuh"
 #include "walk.cuh"
 
 namespace nc {
@@ -65,7 +66,7 @@ __device__ __forceinline__ uint32_t quant(float p, float TmV) {
   return q < 1.f ? 1u : (uint32_t)q;
 }
 // exp on the SFU (ex2.approx; relative error ~1e-6 for the |x| < 30 used here)
-__device__ __forceinline__ float fexp(float x) { return exp2f(__fmul_rn(x, 1.44269504088896341f)); }
+__device__ __forceinline__ float fexp(float x) { return tc::ex2(__fmul_rn(x, 1.44269504088896341f)); }
 // online (max, sum exp) of one thread
 __device__ __forceinline__ void ms_push(float &tm, float &ts, float u) {
   if (u > tm) { ts = __fmaf_rn(ts, fexp(__fsub_rn(tm, u)), 1.f); tm = u; }
@@ -468,20 +469,29 @@ __global__ __launch_bounds__(WT, 1) void walk_kernel(WalkArgs a) {
       const int mix = sm.mix;
       const bool pre_next = has_next && use_ng && i + 1 >= a.warmup;
       if (wid == 1 && pre_next) prefetch_pre(i + 1);
-      unsigned long long my_sum = 0, my_cum = 0;
+      uint32_t my_sum = 0, my_cum = 0;     // per thread <= 4 G/WT counts of < 2^24: fits u32
       Best bb{-1.f, 0x7fffffff, 0};
       float tm = -CUDART_INF_F, ts = 0.f;   // next token's softmax statistics
+      const int tg = tok >> 2;
       for (int g = tid; g < G; g += WT) {
         float pt[4], png[4], p[4];
         prob4(z, g, M, invS, wl, wn, a0f, mix, pt, png, p);
+        uint32_t cv[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const int v = 4 * g + j;
-          const uint32_t cv = quant(p[j], TmV);
-          my_sum += cv;
-          if (p[j] > bb.v) { bb.v = p[j]; bb.i = v; bb.c = cv; }
-          if (v < tok) my_cum += cv;
-          if (v == tok) { sm.pt_t = pt[j]; sm.png_t = png[j]; sm.p_t = p[j]; sm.freq_t = cv; }
+          cv[j] = quant(p[j], TmV);
+          if (p[j] > bb.v) { bb.v = p[j]; bb.i = 4 * g + j; bb.c = cv[j]; }
+        }
+        const uint32_t gs = cv[0] + cv[1] + cv[2] + cv[3];
+        my_sum += gs;
+        if (g < tg) {
+          my_cum += gs;
+        } else if (g == tg) {
+          const int jt = tok & 3;
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (j < jt) my_cum += cv[j];
+            else if (j == jt) { sm.pt_t = pt[j]; sm.png_t = png[j]; sm.p_t = p[j]; sm.freq_t = cv[j]; }
         }
         if (use_head) {
           double2 *bp = reinterpret_cast<double2 *>(b) + 2 * g;
@@ -500,7 +510,7 @@ __global__ __launch_bounds__(WT, 1) void walk_kernel(WalkArgs a) {
           for (int j = 0; j < 4; ++j) ms_push(tm, ts, u[j]);
         }
       }
-      reduce_counts(my_sum, my_cum, bb);
+      reduce_counts((unsigned long long)my_sum, (unsigned long long)my_cum, bb);
       ms_warp(tm, ts);
       if (lane == 0) { sm.red_m[wid] = tm; sm.red_s[wid] = ts; }
       if (wid == 1 && pre_next) prefetch_wait();

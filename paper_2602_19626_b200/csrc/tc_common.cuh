@@ -119,5 +119,12 @@ __device__ __forceinline__ void split_tf32(float x, float &hi, float &lo) {
   lo = __fsub_rn(x, hi);
 }
 
+// 2^x on the SFU (ex2.approx.ftz: ~2 ulp; one MUFU op)
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 }  // namespace tc
 }  // namespace nc
