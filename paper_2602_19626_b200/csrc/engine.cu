@@ -533,7 +533,8 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
   // Slab rows per chunk: at most max_slab_rows over all chunks, and small enough
   // that there are >= kPipeSlabs slabs, so the walk of slab s overlaps the
   // forward of slab s+1 (the walk runs on its own stream, logits double-buffered).
-  const int kPipeSlabs = 4;
+  const char *es = std::getenv("NC_SLABS");
+  const int kPipeSlabs = es ? std::max(1, std::atoi(es)) : 4;
   int per_chunk = std::max(128, (int)(p.max_slab_rows / n_chunks) / 128 * 128);
   int want = (int)((max_n + kPipeSlabs - 1) / kPipeSlabs);
   const int R = std::max(128, std::min<int>(((want + 127) / 128) * 128, per_chunk));
@@ -590,7 +591,7 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
   NC_CUDA(cudaStreamWaitEvent(ws, ev_init, 0));
   // the walk keeps one SM per chunk busy for a whole slab: leave those SMs out of
   // the persistent GEMM grids so every GEMM CTA is resident at once
-  set_reserved_sms(n_slabs > 1 ? n_chunks : 0);
+  set_reserved_sms(n_slabs > 1 ? n_chunks * walk_ctas_per_chunk(S.V) : 0);
   WalkArgs wbase{};
   wbase.logits = nullptr; wbase.ldl = S.V;
   wbase.tokens = tokens_dev; wbase.tok_off = tok_off_d;

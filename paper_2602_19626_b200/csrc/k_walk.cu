@@ -288,23 +288,64 @@ void launch_ngram_precompute(const WalkArgs &a, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------- walk ---
-__global__ __launch_bounds__(WT, 1) void walk_kernel(WalkArgs a) {
-  extern __shared__ uint32_t dyn[];
-  const uint32_t V = a.V;
-  const int G = (int)(V / 4);
-  uint32_t *bitmap = dyn;                              // V/32 words: ids with N-gram fixups this token
-  uint32_t *gsum = dyn + (V + 31) / 32;                // decode: per-group counts (G words)
+// A chunk's vocab row is split over a thread-block cluster of CS CTAs: CTA r
+// owns ids [r V/CS, (r+1) V/CS) and keeps their f64 bias, unigram counts and
+// N-gram fixups in shared memory; thread t of a CTA owns the local float4
+// groups t, t + 1024, ...  Per token the CTAs exchange their partial
+// reductions through distributed shared memory (one cluster barrier per token
+// in compression) and every CTA combines them in rank order, so all CTAs hold
+// identical scalars and decode (same code, same order) is bit-identical.
+
+struct Xch {                  // one CTA's per-token partials, read by the whole cluster
+  unsigned long long sum, cum;
+  float bv; int bi; uint32_t bc;
+  float m, s;                 // softmax statistics partial
+  int has_tok; float pt_t, png_t, p_t; uint32_t freq_t;
+  int found, t; unsigned long long cum_t, fq_t; float fpt, fpng, fp;
+  uint32_t pad;
+};
+constexpr int XW = sizeof(Xch) / 4;
+static_assert(sizeof(Xch) % 4 == 0, "Xch words");
+
+__device__ __forceinline__ uint32_t cl_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cl_ld(const void *local_smem, uint32_t rank) {
+  uint32_t a = tc::smem_u32(local_smem), r, v;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(r) : "memory");
+  return v;
+}
+
+template <int CS>
+__global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
+  extern __shared__ __align__(16) uint8_t dsm[];
   __shared__ WalkSmem sm;
+  __shared__ Xch xs[2];            // own slots (token parity)
+  __shared__ Xch xin[CS];          // copies of the cluster's slots
+  __shared__ double s_lw[2];
+  __shared__ float s_w[2];
+  __shared__ uint32_t s_i;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int e = blockIdx.x;
-  if (e >= a.n_entries) return;
+  const uint32_t rank = CS > 1 ? cl_rank() : 0u;
+  const int e = blockIdx.x / CS;
   const int c = a.chunk_of[e];
   const int row0 = a.row0[e], count = a.count[e];
-  if (count <= 0) return;
+  const uint32_t V = a.V, Vc = V / CS, vb = rank * Vc;
+  const int Gc = (int)(Vc / 4);
+  double *b_s = reinterpret_cast<double *>(dsm);
+  uint32_t *cu_s = reinterpret_cast<uint32_t *>(b_s + Vc);
+  float *sp_s = reinterpret_cast<float *>(cu_s + Vc);
+  uint32_t *bitmap = reinterpret_cast<uint32_t *>(sp_s + Vc);
+  uint32_t *gsum = bitmap + (Vc + 31) / 32;
   WalkState *st = a.st + c;
-  double *b = a.b + (size_t)c * V;
-  uint32_t *cu = a.cu + (size_t)c * V;
-  float *spadd = a.spadd + (size_t)c * V;
+  double *b_g = a.b + (size_t)c * V + vb;
+  uint32_t *cu_g = a.cu + (size_t)c * V + vb;
   const bool use_ng = a.flags & 1u, use_head = a.flags & 2u;
   const bool enc = a.mode == 0;
   const uint64_t T = 1ull << a.cdf_bits;
@@ -312,80 +353,35 @@ __global__ __launch_bounds__(WT, 1) void walk_kernel(WalkArgs a) {
   const float inv_tau = a.inv_tau;
   const unsigned long long HALF = 1ull << 31, QTR = 1ull << 30;
 
-  for (int w = tid; w < (int)((V + 31) / 32); w += WT) bitmap[w] = 0u;
-  if (!enc && tid == 0 && st->i == 0) {   // prime the decoder with 32 bits
-    const uint8_t *s = a.streams + a.stream_off[c];
-    const unsigned long long nb = a.stream_bits[c];
-    unsigned long long v = 0;
-    for (int k = 0; k < 32; ++k) v = 2 * v + ((unsigned long long)k < nb ? (s[k >> 3] >> (7 - (k & 7))) & 1u : 0u);
-    st->low = 0; st->high = 0xFFFFFFFFull; st->value = v; st->bitpos = 32;
+  // ---- load this CTA's slice of the chunk state into shared memory
+  for (uint32_t v = tid; v < Vc; v += WT) {
+    b_s[v] = use_head ? b_g[v] : 0.0;
+    cu_s[v] = use_ng ? cu_g[v] : 0u;
+    sp_s[v] = 0.f;
+  }
+  for (uint32_t w = tid; w < (Vc + 31) / 32; w += WT) bitmap[w] = 0u;
+  if (tid == 0) {
+    s_lw[0] = st->lw[0]; s_lw[1] = st->lw[1];
+    s_w[0] = st->wl; s_w[1] = st->wn;
+    s_i = st->i;
+    if (!enc && st->i == 0 && rank == 0) {   // prime the decoder with 32 bits
+      const uint8_t *s = a.streams + a.stream_off[c];
+      const unsigned long long nb = a.stream_bits[c];
+      unsigned long long v = 0;
+      for (int k = 0; k < 32; ++k) v = 2 * v + ((unsigned long long)k < nb ? (s[k >> 3] >> (7 - (k & 7))) & 1u : 0u);
+      st->low = 0; st->high = 0xFFFFFFFFull; st->value = v; st->bitpos = 32;
+    }
   }
   __syncthreads();
+  if (CS > 1) cl_sync();
 
   auto load_u = [&](const float *z, int g, float u[4]) {
-    const float4 z4 = reinterpret_cast<const float4 *>(z)[g];
-    if (use_head) {
-      const double2 b01 = reinterpret_cast<const double2 *>(b)[2 * g];
-      const double2 b23 = reinterpret_cast<const double2 *>(b)[2 * g + 1];
-      u[0] = walk_u(z4.x, b01.x, inv_tau); u[1] = walk_u(z4.y, b01.y, inv_tau);
-      u[2] = walk_u(z4.z, b23.x, inv_tau); u[3] = walk_u(z4.w, b23.y, inv_tau);
-    } else {
-      u[0] = walk_u(z4.x, 0.0, inv_tau); u[1] = walk_u(z4.y, 0.0, inv_tau);
-      u[2] = walk_u(z4.z, 0.0, inv_tau); u[3] = walk_u(z4.w, 0.0, inv_tau);
-    }
+    const float4 z4 = reinterpret_cast<const float4 *>(z + vb)[g];
+    const double2 b01 = reinterpret_cast<const double2 *>(b_s)[2 * g];
+    const double2 b23 = reinterpret_cast<const double2 *>(b_s)[2 * g + 1];
+    u[0] = walk_u(z4.x, b01.x, inv_tau); u[1] = walk_u(z4.y, b01.y, inv_tau);
+    u[2] = walk_u(z4.z, b23.x, inv_tau); u[3] = walk_u(z4.w, b23.y, inv_tau);
   };
-  // block-wide (max, sum exp) of u over the row z -> sm.M, sm.invS
-  auto softmax_stats = [&](const float *z) {
-    float tm = -CUDART_INF_F, ts = 0.f;
-    for (int g = tid; g < G; g += WT) {
-      float u[4];
-      load_u(z, g, u);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) ms_push(tm, ts, u[j]);
-    }
-    ms_warp(tm, ts);
-    if (lane == 0) { sm.red_m[wid] = tm; sm.red_s[wid] = ts; }
-    __syncthreads();
-    if (wid == 0) {
-      tm = sm.red_m[lane]; ts = sm.red_s[lane];
-      ms_warp(tm, ts);
-      if (lane == 0) { sm.M = tm; sm.invS = __frcp_rn(ts); }
-    }
-    __syncthreads();
-  };
-  // warp 0: make token i's sparse list live (spadd + bitmap) and its scalars
-  auto scatter_list = [&](uint32_t i) {
-    const NgTok &L = sm.lists[i & 1];
-    const int mix = (use_ng && i >= a.warmup) ? 1 : 0;
-    const int n = mix ? (int)L.n : 0;
-    for (int j = lane; j < n; j += 32) {
-      const uint32_t tk = L.tok[j];
-      spadd[tk] = L.add[j];
-      atomicOr(&bitmap[tk >> 5], 1u << (tk & 31));
-    }
-    if (lane == 0) { sm.mix = mix; sm.nsp = n; sm.a0f = mix ? L.a0f : 0.f; }
-  };
-  auto clear_list = [&](uint32_t i) {
-    const NgTok &L = sm.lists[i & 1];
-    for (int j = lane; j < sm.nsp; j += 32) {
-      const uint32_t tk = L.tok[j];
-      spadd[tk] = 0.f;
-      bitmap[tk >> 5] = 0u;
-    }
-  };
-  // one warp: asynchronous copy (cp.async) of token i's precomputed list into smem
-  auto prefetch_pre = [&](uint32_t i) {
-    const char *src = reinterpret_cast<const char *>(a.ng_pre + (size_t)c * a.ng_ring + (i % a.ng_ring));
-    char *dst = reinterpret_cast<char *>(&sm.lists[i & 1]);
-    for (int ofs = lane * 16; ofs < (int)sizeof(NgTok); ofs += 32 * 16)
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst + ofs)),
-                   "l"(src + ofs)
-                   : "memory");
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-  auto prefetch_wait = [&]() { asm volatile("cp.async.wait_all;" ::: "memory"); };
-
-  // the 4 probabilities of group g for the current token (identical code in every pass)
   auto prob4 = [&](const float *z, int g, float M, float invS, float wl, float wn, float a0f, int mix, float pt[4],
                    float png[4], float p[4]) {
     float u[4];
@@ -397,29 +393,26 @@ __global__ __launch_bounds__(WT, 1) void walk_kernel(WalkArgs a) {
       for (int j = 0; j < 4; ++j) { png[j] = 0.f; p[j] = pt[j]; }
       return;
     }
-    const uint4 c4 = reinterpret_cast<const uint4 *>(cu)[g];
+    const uint4 c4 = reinterpret_cast<const uint4 *>(cu_s)[g];
     const uint32_t cc[4] = {c4.x, c4.y, c4.z, c4.w};
     const uint32_t bits = (bitmap[g >> 3] >> ((g & 7) * 4)) & 15u;
+    const float4 s4 = bits ? reinterpret_cast<const float4 *>(sp_s)[g] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float sa[4] = {s4.x, s4.y, s4.z, s4.w};
 #pragma unroll
-    for (int j = 0; j < 4; ++j) p[j] = mix_p(pt[j], a0f, cc[j], (bits >> j) & 1u ? spadd[4 * g + j] : 0.f, wl, wn, png[j]);
+    for (int j = 0; j < 4; ++j) p[j] = mix_p(pt[j], a0f, cc[j], sa[j], wl, wn, png[j]);
   };
-
-  // thread 0, after t is known: mixer update and the next weights
-  auto mixer_update = [&](float pt_t, float png_t) {
-    double l0 = __dadd_rn(st->lw[0], __dmul_rn(a.eta, log(fmax((double)pt_t, 1e-12))));
-    double l1 = __dadd_rn(st->lw[1], __dmul_rn(a.eta, log(fmax((double)png_t, 1e-12))));
-    double mx = fmax(l0, l1);
-    double lse = __dadd_rn(mx, log(__dadd_rn(exp(__dsub_rn(l0, mx)), exp(__dsub_rn(l1, mx)))));
-    l0 = __dsub_rn(l0, lse);
-    l1 = __dsub_rn(l1, lse);
-    st->lw[0] = l0;
-    st->lw[1] = l1;
-    st->wl = (float)exp(l0);     // lw is renormalised: softmax(lw) = exp(lw) (to ~1e-16)
-    st->wn = (float)exp(l1);
+  // CTA reduction of (m, s) into warp 0 (all lanes hold the CTA value)
+  auto cta_ms = [&](float &tm, float &ts) {
+    ms_warp(tm, ts);
+    if (lane == 0) { sm.red_m[wid] = tm; sm.red_s[wid] = ts; }
+    __syncthreads();
+    if (wid == 0) {
+      tm = sm.red_m[lane]; ts = sm.red_s[lane];
+      ms_warp(tm, ts);
+    }
   };
-
-  // block reduction of (sum c, cum, argmax) -> warp 0 lane 0 holds the totals
-  auto reduce_counts = [&](unsigned long long s1, unsigned long long s2, Best bb) {
+  auto cta_counts = [&](unsigned long long s1, unsigned long long s2, Best bb, unsigned long long &o1,
+                        unsigned long long &o2, Best &ob) {   // call after the caller's __syncthreads scheme
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       s1 += __shfl_xor_sync(0xffffffffu, s1, o);
@@ -428,106 +421,195 @@ __global__ __launch_bounds__(WT, 1) void walk_kernel(WalkArgs a) {
                  __shfl_xor_sync(0xffffffffu, bb.c, o));
     }
     if (lane == 0) { sm.red_sum[wid] = s1; sm.red_cum[wid] = s2; sm.red_bv[wid] = bb.v; sm.red_bi[wid] = bb.i; sm.red_bc[wid] = bb.c; }
-  };
-  auto finish_counts = [&](int tok) {   // warp 0, after a __syncthreads
-    unsigned long long s1 = sm.red_sum[lane], s2 = sm.red_cum[lane];
-    Best bb{sm.red_bv[lane], sm.red_bi[lane], sm.red_bc[lane]};
+    __syncthreads();
+    if (wid == 0) {
+      s1 = sm.red_sum[lane]; s2 = sm.red_cum[lane];
+      Best b2{sm.red_bv[lane], sm.red_bi[lane], sm.red_bc[lane]};
 #pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-      s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-      best_merge(bb, __shfl_xor_sync(0xffffffffu, bb.v, o), __shfl_xor_sync(0xffffffffu, bb.i, o),
-                 __shfl_xor_sync(0xffffffffu, bb.c, o));
+      for (int o = 16; o; o >>= 1) {
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+        best_merge(b2, __shfl_xor_sync(0xffffffffu, b2.v, o), __shfl_xor_sync(0xffffffffu, b2.i, o),
+                   __shfl_xor_sync(0xffffffffu, b2.c, o));
+      }
+      o1 = s1; o2 = s2; ob = b2;
     }
-    if (lane == 0) {
-      const long long R = (long long)T - (long long)s1;
-      sm.resid = R;
-      sm.argmax = bb.i;
-      if ((long long)bb.c + R < 1) st->err = 1;      // D6: residual would drop a count below 1
-      if (tok >= 0) {
-        sm.cum_t = s2 + (bb.i < tok ? R : 0);
-        sm.freq_t = sm.freq_t + (bb.i == tok ? R : 0);
+  };
+  // warp 0: copy every CTA's slot `par` into xin[] (DSMEM), then lane 0 combines
+  auto gather = [&](int par) {
+    for (int r = 0; r < CS; ++r) {
+      uint32_t *dst = reinterpret_cast<uint32_t *>(&xin[r]);
+      const uint32_t *src = reinterpret_cast<const uint32_t *>(&xs[par]);
+      for (int w = lane; w < XW; w += 32) dst[w] = CS > 1 ? cl_ld(src + w, (uint32_t)r) : src[w];
+    }
+    __syncwarp();
+  };
+  auto scatter_list = [&](uint32_t i) {   // warp 0: fixups of token i inside this CTA's range
+    const NgTok &L = sm.lists[i & 1];
+    const int mix = (use_ng && i >= a.warmup) ? 1 : 0;
+    const int n = mix ? (int)L.n : 0;
+    for (int j = lane; j < n; j += 32) {
+      const uint32_t tk = L.tok[j];
+      if (tk >= vb && tk < vb + Vc) {
+        sp_s[tk - vb] = L.add[j];
+        atomicOr(&bitmap[(tk - vb) >> 5], 1u << ((tk - vb) & 31));
       }
     }
+    if (lane == 0) { sm.mix = mix; sm.nsp = n; sm.a0f = mix ? L.a0f : 0.f; }
+  };
+  auto clear_list = [&](uint32_t i) {
+    const NgTok &L = sm.lists[i & 1];
+    for (int j = lane; j < sm.nsp; j += 32) {
+      const uint32_t tk = L.tok[j];
+      if (tk >= vb && tk < vb + Vc) { sp_s[tk - vb] = 0.f; bitmap[(tk - vb) >> 5] = 0u; }
+    }
+  };
+  auto prefetch_pre = [&](uint32_t i) {
+    const char *src = reinterpret_cast<const char *>(a.ng_pre + (size_t)c * a.ng_ring + (i % a.ng_ring));
+    char *dst = reinterpret_cast<char *>(&sm.lists[i & 1]);
+    for (int ofs = lane * 16; ofs < (int)sizeof(NgTok); ofs += 32 * 16)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst + ofs)),
+                   "l"(src + ofs)
+                   : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  auto prefetch_wait = [&]() { asm volatile("cp.async.wait_all;" ::: "memory"); };
+  auto mixer_update = [&](float pt_t, float png_t) {   // thread 0 of every CTA, identical arithmetic
+    double l0 = __dadd_rn(s_lw[0], __dmul_rn(a.eta, log(fmax((double)pt_t, 1e-12))));
+    double l1 = __dadd_rn(s_lw[1], __dmul_rn(a.eta, log(fmax((double)png_t, 1e-12))));
+    const double mx = fmax(l0, l1);
+    const double lse = __dadd_rn(mx, log(__dadd_rn(exp(__dsub_rn(l0, mx)), exp(__dsub_rn(l1, mx)))));
+    l0 = __dsub_rn(l0, lse);
+    l1 = __dsub_rn(l1, lse);
+    s_lw[0] = l0; s_lw[1] = l1;
+    s_w[0] = (float)exp(l0);     // lw is renormalised: softmax(lw) = exp(lw) (to ~1e-16)
+    s_w[1] = (float)exp(l1);
   };
 
   if (enc) {
     // ===================================================== compression ===
+    const uint32_t i0 = s_i;
     if (wid == 0) {
-      const uint32_t i0 = st->i;
       if (use_ng && i0 >= a.warmup) { prefetch_pre(i0); prefetch_wait(); __syncwarp(); }
       scatter_list(i0);
     }
-    softmax_stats(a.logits + (size_t)row0 * a.ldl);
+    // softmax statistics of the first token
+    {
+      const float *z0 = a.logits + (size_t)row0 * a.ldl;
+      float tm = -CUDART_INF_F, ts = 0.f;
+      for (int g = tid; g < Gc; g += WT) {
+        float u[4];
+        load_u(z0, g, u);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) ms_push(tm, ts, u[j]);
+      }
+      cta_ms(tm, ts);
+      if (tid == 0) { xs[1].m = tm; xs[1].s = ts; }
+      __syncthreads();
+      if (CS > 1) cl_sync();
+      if (wid == 0) {
+        gather(1);
+        if (lane == 0) {
+          float M = xin[0].m, S = xin[0].s;
+          for (int r = 1; r < CS; ++r) ms_merge(M, S, xin[r].m, xin[r].s);
+          sm.M = M; sm.invS = __frcp_rn(S);
+        }
+      }
+      __syncthreads();
+    }
     for (int it = 0; it < count; ++it) {
       const float *z = a.logits + (size_t)(row0 + it) * a.ldl;
       const bool has_next = it + 1 < count;
       const float *zn = a.logits + (size_t)(row0 + it + 1) * a.ldl;
-      const uint32_t i = st->i;
+      const uint32_t i = i0 + it;
+      const int par = it & 1;
       const int tok = (int)a.tokens[a.tok_off[c] + i];
-      const float M = sm.M, invS = sm.invS, a0f = sm.a0f, wl = st->wl, wn = st->wn;
+      const int ltok = tok - (int)vb;                  // local id (may be outside [0, Vc))
+      const float M = sm.M, invS = sm.invS, a0f = sm.a0f, wl = s_w[0], wn = s_w[1];
       const int mix = sm.mix;
       const bool pre_next = has_next && use_ng && i + 1 >= a.warmup;
       if (wid == 1 && pre_next) prefetch_pre(i + 1);
-      uint32_t my_sum = 0, my_cum = 0;     // per thread <= 4 G/WT counts of < 2^24: fits u32
+      uint32_t my_sum = 0, my_cum = 0;
       Best bb{-1.f, 0x7fffffff, 0};
-      float tm = -CUDART_INF_F, ts = 0.f;   // next token's softmax statistics
-      const int tg = tok >> 2;
-      for (int g = tid; g < G; g += WT) {
+      float tm = -CUDART_INF_F, ts = 0.f;
+      const int tg = ltok >= 0 ? (ltok >> 2) : -1;
+      const int gcut = ltok < 0 ? 0 : (ltok >= (int)Vc ? Gc : tg);   // local groups entirely below tok
+      for (int g = tid; g < Gc; g += WT) {
         float pt[4], png[4], p[4];
         prob4(z, g, M, invS, wl, wn, a0f, mix, pt, png, p);
         uint32_t cv[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           cv[j] = quant(p[j], TmV);
-          if (p[j] > bb.v) { bb.v = p[j]; bb.i = 4 * g + j; bb.c = cv[j]; }
+          if (p[j] > bb.v) { bb.v = p[j]; bb.i = (int)vb + 4 * g + j; bb.c = cv[j]; }
         }
         const uint32_t gs = cv[0] + cv[1] + cv[2] + cv[3];
         my_sum += gs;
-        if (g < tg) {
+        if (g < gcut) {
           my_cum += gs;
-        } else if (g == tg) {
-          const int jt = tok & 3;
+        } else if (g == tg && ltok < (int)Vc) {
+          const int jt = ltok & 3;
 #pragma unroll
           for (int j = 0; j < 4; ++j)
             if (j < jt) my_cum += cv[j];
-            else if (j == jt) { sm.pt_t = pt[j]; sm.png_t = png[j]; sm.p_t = p[j]; sm.freq_t = cv[j]; }
+            else if (j == jt) { xs[par].pt_t = pt[j]; xs[par].png_t = png[j]; xs[par].p_t = p[j]; xs[par].freq_t = cv[j]; }
         }
         if (use_head) {
-          double2 *bp = reinterpret_cast<double2 *>(b) + 2 * g;
+          double2 *bp = reinterpret_cast<double2 *>(b_s) + 2 * g;
           double2 b01 = bp[0], b23 = bp[1];
           const int v = 4 * g;
-          b01.x = b_step(b01.x, pt[0], v == tok, a.alpha);
-          b01.y = b_step(b01.y, pt[1], v + 1 == tok, a.alpha);
-          b23.x = b_step(b23.x, pt[2], v + 2 == tok, a.alpha);
-          b23.y = b_step(b23.y, pt[3], v + 3 == tok, a.alpha);
+          b01.x = b_step(b01.x, pt[0], v == ltok, a.alpha);
+          b01.y = b_step(b01.y, pt[1], v + 1 == ltok, a.alpha);
+          b23.x = b_step(b23.x, pt[2], v + 2 == ltok, a.alpha);
+          b23.y = b_step(b23.y, pt[3], v + 3 == ltok, a.alpha);
           bp[0] = b01; bp[1] = b23;
         }
         if (has_next) {
           float u[4];
-          load_u(zn, g, u);           // b already updated for this group
+          load_u(zn, g, u);           // bias already updated for this group
 #pragma unroll
           for (int j = 0; j < 4; ++j) ms_push(tm, ts, u[j]);
         }
       }
-      reduce_counts((unsigned long long)my_sum, (unsigned long long)my_cum, bb);
-      ms_warp(tm, ts);
-      if (lane == 0) { sm.red_m[wid] = tm; sm.red_s[wid] = ts; }
       if (wid == 1 && pre_next) prefetch_wait();
+      unsigned long long c1 = 0, c2 = 0;
+      Best cb{};
+      cta_ms(tm, ts);                                   // contains a __syncthreads
+      cta_counts((unsigned long long)my_sum, (unsigned long long)my_cum, bb, c1, c2, cb);
+      if (tid == 0) {
+        Xch &x = xs[par];
+        x.sum = c1; x.cum = c2; x.bv = cb.v; x.bi = cb.i; x.bc = cb.c; x.m = tm; x.s = ts;
+        x.has_tok = (ltok >= 0 && ltok < (int)Vc) ? 1 : 0;
+      }
       __syncthreads();
+      if (CS > 1) cl_sync();
       if (wid == 0) {
-        finish_counts(tok);
-        tm = sm.red_m[lane]; ts = sm.red_s[lane];
-        ms_warp(tm, ts);
+        gather(par);
         if (lane == 0) {
-          const size_t oi = (size_t)a.tok_off[c] + i;
-          a.out_cum[oi] = (uint32_t)sm.cum_t;
-          a.out_freq[oi] = (uint32_t)sm.freq_t;
-          if (a.out_p) a.out_p[oi] = sm.p_t;
-          if (mix) mixer_update(sm.pt_t, sm.png_t);
-          if (use_ng) cu[tok] += 1u;
-          st->i = i + 1;
-          if (has_next) { sm.M = tm; sm.invS = __frcp_rn(ts); }
+          unsigned long long s1 = 0, s2 = 0;
+          Best b2{-1.f, 0x7fffffff, 0};
+          float nm = xin[0].m, ns = xin[0].s;
+          float pt_t = 0.f, png_t = 0.f, p_t = 0.f;
+          uint32_t fq = 0;
+          for (int r = 0; r < CS; ++r) {
+            s1 += xin[r].sum; s2 += xin[r].cum;
+            best_merge(b2, xin[r].bv, xin[r].bi, xin[r].bc);
+            if (r) ms_merge(nm, ns, xin[r].m, xin[r].s);
+            if (xin[r].has_tok) { pt_t = xin[r].pt_t; png_t = xin[r].png_t; p_t = xin[r].p_t; fq = xin[r].freq_t; }
+          }
+          const long long R = (long long)T - (long long)s1;
+          if ((long long)b2.c + R < 1) st->err = 1;     // D6
+          const unsigned long long cum_t = s2 + (b2.i < tok ? R : 0);
+          const unsigned long long freq_t = (unsigned long long)((long long)fq + (b2.i == tok ? R : 0));
+          if (rank == 0) {
+            const size_t oi = (size_t)a.tok_off[c] + i;
+            a.out_cum[oi] = (uint32_t)cum_t;
+            a.out_freq[oi] = (uint32_t)freq_t;
+            if (a.out_p) a.out_p[oi] = p_t;
+          }
+          if (mix) mixer_update(pt_t, png_t);
+          if (use_ng && ltok >= 0 && ltok < (int)Vc) cu_s[ltok] += 1u;
+          if (has_next) { sm.M = nm; sm.invS = __frcp_rn(ns); }
         }
         __syncwarp();
         clear_list(i);
@@ -536,177 +618,286 @@ __global__ __launch_bounds__(WT, 1) void walk_kernel(WalkArgs a) {
       }
       __syncthreads();
     }
-    return;
-  }
-
-  // ======================================================== decompression ===
-  for (int it = 0; it < count; ++it) {
-    const float *z = a.logits + (size_t)(row0 + it) * a.ldl;
-    const uint32_t i = st->i;
-    if (wid == 0) {
-      if (use_ng && i >= a.warmup) {
+    if (tid == 0) s_i = i0 + count;
+  } else {
+    // ======================================================== decompression ===
+    for (int it = 0; it < count; ++it) {
+      const float *z = a.logits + (size_t)(row0 + it) * a.ldl;
+      const uint32_t i = s_i;
+      const int par = it & 1;
+      // (1) N-gram prediction by rank 0, shared through DSMEM; decoder target.
+      //     gsum (>= V/32 words, idle here) is the predictor's full-vocab bitmap scratch.
+      for (int w = tid; w < Gc; w += WT) gsum[w] = 0u;
+      __syncthreads();
+      if (rank == 0 && wid == 0 && use_ng && i >= a.warmup) {
         uint32_t hist[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) hist[j] = st->hist[j];
-        ng_predict_warp(a, c, i, hist, spadd, bitmap, &sm.lists[i & 1], lane);
+        ng_predict_warp(a, c, i, hist, a.spadd + (size_t)c * V, gsum, &sm.lists[i & 1], lane);
       }
-      scatter_list(i);
-      if (lane == 0) {   // WNC decode target (D8)
-        const unsigned long long R = st->high - st->low + 1;
-        sm.target = ((st->value - st->low + 1) * T - 1) / R;
-        sm.tok = -1;
-      }
-    }
-    __syncthreads();
-    softmax_stats(z);
-    const float M = sm.M, invS = sm.invS, a0f = sm.a0f, wl = st->wl, wn = st->wn;
-    const int mix = sm.mix;
-    unsigned long long my_sum = 0;
-    Best bb{-1.f, 0x7fffffff, 0};
-    for (int g = tid; g < G; g += WT) {
-      float pt[4], png[4], p[4];
-      prob4(z, g, M, invS, wl, wn, a0f, mix, pt, png, p);
-      uint32_t gs = 0;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint32_t cv = quant(p[j], TmV);
-        gs += cv;
-        if (p[j] > bb.v) { bb.v = p[j]; bb.i = 4 * g + j; bb.c = cv; }
-      }
-      my_sum += gs;
-      gsum[g] = gs;
-    }
-    reduce_counts(my_sum, 0ull, bb);
-    __syncthreads();
-    if (wid == 0) {
-      finish_counts(-1);
-      if (lane == 0) gsum[sm.argmax >> 2] = (uint32_t)((long long)gsum[sm.argmax >> 2] + sm.resid);
-    }
-    __syncthreads();
-    // prefix scan over the groups in id order, search the target
-    {
-      const long long R = sm.resid;
-      const int am = sm.argmax;
-      const int gpt = (G + WT - 1) / WT;
-      const int g0 = min(G, tid * gpt), g1 = min(G, g0 + gpt);
-      uint32_t adj = 0;
-      for (int g = g0; g < g1; ++g) adj += gsum[g];
-      uint32_t x = adj;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-      }
-      if (lane == 31) sm.scan[wid] = x;
       __syncthreads();
+      if (CS > 1) cl_sync();
       if (wid == 0) {
-        uint32_t y = sm.scan[lane];
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t z2 = __shfl_up_sync(0xffffffffu, y, o);
-          if (lane >= o) y += z2;
+        if (rank != 0 && use_ng && i >= a.warmup) {   // copy rank 0's list (header + used entries)
+          NgTok &L = sm.lists[i & 1];
+          uint32_t *hdr = reinterpret_cast<uint32_t *>(&L);
+          for (uint32_t w = lane; w < 4; w += 32) hdr[w] = cl_ld(hdr + w, 0u);
+          const uint32_t n = cl_ld(&L.n, 0u);
+          for (uint32_t j = lane; j < n; j += 32) {
+            L.tok[j] = cl_ld(&L.tok[j], 0u);
+            L.add[j] = __uint_as_float(cl_ld(&L.add[j], 0u));
+          }
+          __syncwarp();
         }
-        sm.scan[lane] = y;
+        scatter_list(i);
+        if (lane == 0) {
+          const unsigned long long R = st->high - st->low + 1;
+          sm.target = ((st->value - st->low + 1) * T - 1) / R;
+        }
       }
       __syncthreads();
-      const unsigned long long excl = (unsigned long long)(x - adj) + (wid ? sm.scan[wid - 1] : 0u);
-      const unsigned long long tgt = sm.target;
-      if (adj > 0 && tgt >= excl && tgt < excl + adj) {
-        unsigned long long accm = excl;
-        int gf = g0;
-        for (; gf < g1; ++gf) {
-          if (tgt < accm + gsum[gf]) break;
-          accm += gsum[gf];
-        }
-        float pt[4], png[4], p[4];
-        prob4(z, gf, M, invS, wl, wn, a0f, mix, pt, png, p);
+      // (2) softmax statistics
+      {
+        float tm = -CUDART_INF_F, ts = 0.f;
+        for (int g = tid; g < Gc; g += WT) {
+          float u[4];
+          load_u(z, g, u);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int v = 4 * gf + j;
-          unsigned long long cv = quant(p[j], TmV);
-          if (v == am) cv = (unsigned long long)((long long)cv + R);
-          if (tgt < accm + cv) {
-            sm.tok = v; sm.cum_t = accm; sm.freq_t = cv; sm.pt_t = pt[j]; sm.png_t = png[j]; sm.p_t = p[j];
-            break;
-          }
-          accm += cv;
+          for (int j = 0; j < 4; ++j) ms_push(tm, ts, u[j]);
         }
+        cta_ms(tm, ts);
+        if (tid == 0) { xs[par].m = tm; xs[par].s = ts; }
+        __syncthreads();
+        if (CS > 1) cl_sync();
+        if (wid == 0) {
+          gather(par);
+          if (lane == 0) {
+            float M = xin[0].m, S = xin[0].s;
+            for (int r = 1; r < CS; ++r) ms_merge(M, S, xin[r].m, xin[r].s);
+            sm.M = M; sm.invS = __frcp_rn(S);
+          }
+        }
+        __syncthreads();
       }
-      if (tid == 0 && tgt >= T) st->err = 2;
-    }
-    __syncthreads();
-    const int t = sm.tok;
-    if (use_head)
-      for (int g = tid; g < G; g += WT) {
+      const float M = sm.M, invS = sm.invS, a0f = sm.a0f, wl = s_w[0], wn = s_w[1];
+      const int mix = sm.mix;
+      // (3) counts
+      uint32_t my_sum = 0;
+      Best bb{-1.f, 0x7fffffff, 0};
+      for (int g = tid; g < Gc; g += WT) {
         float pt[4], png[4], p[4];
         prob4(z, g, M, invS, wl, wn, a0f, mix, pt, png, p);
-        double2 *bp = reinterpret_cast<double2 *>(b) + 2 * g;
-        double2 b01 = bp[0], b23 = bp[1];
-        const int v = 4 * g;
-        b01.x = b_step(b01.x, pt[0], v == t, a.alpha);
-        b01.y = b_step(b01.y, pt[1], v + 1 == t, a.alpha);
-        b23.x = b_step(b23.x, pt[2], v + 2 == t, a.alpha);
-        b23.y = b_step(b23.y, pt[3], v + 3 == t, a.alpha);
-        bp[0] = b01; bp[1] = b23;
-      }
-    __syncthreads();
-    if (wid == 0) {
-      if (lane == 0) {
-        const size_t oi = (size_t)a.tok_off[c] + i;
-        if (t < 0) st->err = 3;
-        const uint32_t tt = (uint32_t)max(t, 0);
-        a.out_tok[oi] = tt;
-        if (a.next_x) a.next_x[c] = tt;
-        if (a.out_p) a.out_p[oi] = sm.p_t;
-        // consume the symbol (D8)
-        const unsigned long long R = st->high - st->low + 1;
-        unsigned long long lo = st->low, hi = st->low + ((R * (sm.cum_t + sm.freq_t)) >> a.cdf_bits) - 1;
-        lo = lo + ((R * sm.cum_t) >> a.cdf_bits);
-        unsigned long long val = st->value, bp = st->bitpos;
-        const uint8_t *s = a.streams + a.stream_off[c];
-        const unsigned long long nb = a.stream_bits[c];
-        for (;;) {
-          if (hi < HALF) {
-          } else if (lo >= HALF) { lo -= HALF; hi -= HALF; val -= HALF; }
-          else if (lo >= QTR && hi < 3 * QTR) { lo -= QTR; hi -= QTR; val -= QTR; }
-          else break;
-          lo = 2 * lo; hi = 2 * hi + 1;
-          const unsigned long long bit = bp < nb ? (s[bp >> 3] >> (7 - (bp & 7))) & 1u : 0u;
-          val = 2 * val + bit;
-          ++bp;
-        }
-        st->low = lo; st->high = hi; st->value = val; st->bitpos = bp;
-        if (mix) mixer_update(sm.pt_t, sm.png_t);
-        if (use_ng) cu[tt] += 1u;
-        st->i = i + 1;
-      }
-      __syncwarp();
-      clear_list(i);
-      __syncwarp();
-      if (use_ng && t >= 0) {
-        uint32_t hist[4];
+        uint32_t gs = 0;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) hist[j] = st->hist[j];
-        ng_update_warp(a, c, i, hist, (uint32_t)t, st, lane);
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t cv = quant(p[j], TmV);
+          gs += cv;
+          if (p[j] > bb.v) { bb.v = p[j]; bb.i = (int)vb + 4 * g + j; bb.c = cv; }
+        }
+        my_sum += gs;
+        gsum[g] = gs;
+      }
+      {
+        unsigned long long c1 = 0, c2 = 0;
+        Best cb{};
+        cta_counts((unsigned long long)my_sum, 0ull, bb, c1, c2, cb);
+        if (tid == 0) { Xch &x = xs[par]; x.sum = c1; x.bv = cb.v; x.bi = cb.i; x.bc = cb.c; x.found = 0; }
+        __syncthreads();
+        if (CS > 1) cl_sync();
+        if (wid == 0) {
+          gather(par);
+          if (lane == 0) {
+            unsigned long long s1 = 0, before = 0;
+            Best b2{-1.f, 0x7fffffff, 0};
+            for (int r = 0; r < CS; ++r) { s1 += xin[r].sum; best_merge(b2, xin[r].bv, xin[r].bi, xin[r].bc); }
+            const long long R = (long long)T - (long long)s1;
+            if ((long long)b2.c + R < 1) st->err = 1;
+            for (int r = 0; r < (int)rank; ++r) before += xin[r].sum + ((uint32_t)b2.i / Vc == (uint32_t)r ? R : 0);
+            sm.resid = R;
+            sm.argmax = b2.i;
+            sm.cum_t = before;                           // this CTA's first cumulative count
+            if ((uint32_t)b2.i / Vc == rank) gsum[(b2.i - vb) >> 2] = (uint32_t)((long long)gsum[(b2.i - vb) >> 2] + R);
+          }
+        }
+        __syncthreads();
+      }
+      // (4) prefix scan over the local groups in id order, search the target
+      {
+        const long long R = sm.resid;
+        const int am = sm.argmax - (int)vb;
+        const int gpt = (Gc + WT - 1) / WT;
+        const int g0 = min(Gc, tid * gpt), g1 = min(Gc, g0 + gpt);
+        uint32_t adj = 0;
+        for (int g = g0; g < g1; ++g) adj += gsum[g];
+        uint32_t x = adj;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        if (lane == 31) sm.scan[wid] = x;
+        __syncthreads();
+        if (wid == 0) {
+          uint32_t y = sm.scan[lane];
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t z2 = __shfl_up_sync(0xffffffffu, y, o);
+            if (lane >= o) y += z2;
+          }
+          sm.scan[lane] = y;
+        }
+        __syncthreads();
+        const unsigned long long excl = sm.cum_t + (unsigned long long)(x - adj) + (wid ? sm.scan[wid - 1] : 0u);
+        const unsigned long long tgt = sm.target;
+        if (adj > 0 && tgt >= excl && tgt < excl + adj) {
+          unsigned long long accm = excl;
+          int gf = g0;
+          for (; gf < g1; ++gf) {
+            if (tgt < accm + gsum[gf]) break;
+            accm += gsum[gf];
+          }
+          float pt[4], png[4], p[4];
+          prob4(z, gf, M, invS, wl, wn, a0f, mix, pt, png, p);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int v = 4 * gf + j;
+            unsigned long long cv = quant(p[j], TmV);
+            if (v == am) cv = (unsigned long long)((long long)cv + R);
+            if (tgt < accm + cv) {
+              Xch &xx = xs[par];
+              xx.found = 1; xx.t = (int)vb + v; xx.cum_t = accm; xx.fq_t = cv;
+              xx.fpt = pt[j]; xx.fpng = png[j]; xx.fp = p[j];
+              break;
+            }
+            accm += cv;
+          }
+        }
+        __syncthreads();
+        if (CS > 1) cl_sync();
+        if (wid == 0) {
+          gather(par);
+          if (lane == 0) {
+            int t = -1;
+            for (int r = 0; r < CS; ++r)
+              if (xin[r].found) {
+                t = xin[r].t; sm.cum_t = xin[r].cum_t; sm.freq_t = xin[r].fq_t;
+                sm.pt_t = xin[r].fpt; sm.png_t = xin[r].fpng; sm.p_t = xin[r].fp;
+              }
+            sm.tok = t;
+            if (t < 0 || tgt >= T) st->err = 2;
+          }
+        }
+        __syncthreads();
+      }
+      // (5) bias update with the decoded token
+      const int t = sm.tok;
+      const int lt = t - (int)vb;
+      if (use_head)
+        for (int g = tid; g < Gc; g += WT) {
+          float pt[4], png[4], p[4];
+          prob4(z, g, M, invS, wl, wn, a0f, mix, pt, png, p);
+          double2 *bp = reinterpret_cast<double2 *>(b_s) + 2 * g;
+          double2 b01 = bp[0], b23 = bp[1];
+          const int v = 4 * g;
+          b01.x = b_step(b01.x, pt[0], v == lt, a.alpha);
+          b01.y = b_step(b01.y, pt[1], v + 1 == lt, a.alpha);
+          b23.x = b_step(b23.x, pt[2], v + 2 == lt, a.alpha);
+          b23.y = b_step(b23.y, pt[3], v + 3 == lt, a.alpha);
+          bp[0] = b01; bp[1] = b23;
+        }
+      __syncthreads();
+      // (6) scalars: outputs, coder, mixer, counts, N-gram update (rank 0)
+      if (wid == 0) {
         if (lane == 0) {
-          ng_hist_push(st, (uint32_t)t);
-          st->ng_i = i + 1;
+          const uint32_t tt = (uint32_t)max(t, 0);
+          if (rank == 0) {
+            const size_t oi = (size_t)a.tok_off[c] + i;
+            a.out_tok[oi] = tt;
+            if (a.next_x) a.next_x[c] = tt;
+            if (a.out_p) a.out_p[oi] = sm.p_t;
+            const unsigned long long Rg = st->high - st->low + 1;
+            unsigned long long lo = st->low, hi = st->low + ((Rg * (sm.cum_t + sm.freq_t)) >> a.cdf_bits) - 1;
+            lo = lo + ((Rg * sm.cum_t) >> a.cdf_bits);
+            unsigned long long val = st->value, bp = st->bitpos;
+            const uint8_t *s = a.streams + a.stream_off[c];
+            const unsigned long long nb = a.stream_bits[c];
+            for (;;) {
+              if (hi < HALF) {
+              } else if (lo >= HALF) { lo -= HALF; hi -= HALF; val -= HALF; }
+              else if (lo >= QTR && hi < 3 * QTR) { lo -= QTR; hi -= QTR; val -= QTR; }
+              else break;
+              lo = 2 * lo; hi = 2 * hi + 1;
+              const unsigned long long bit = bp < nb ? (s[bp >> 3] >> (7 - (bp & 7))) & 1u : 0u;
+              val = 2 * val + bit;
+              ++bp;
+            }
+            st->low = lo; st->high = hi; st->value = val; st->bitpos = bp;
+          }
+          if (mix) mixer_update(sm.pt_t, sm.png_t);
+          if (use_ng && lt >= 0 && lt < (int)Vc) cu_s[lt] += 1u;
+          s_i = i + 1;
+        }
+        __syncwarp();
+        clear_list(i);
+        __syncwarp();
+        if (rank == 0 && use_ng && t >= 0) {
+          uint32_t hist[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) hist[j] = st->hist[j];
+          ng_update_warp(a, c, i, hist, (uint32_t)t, st, lane);
+          if (lane == 0) { ng_hist_push(st, (uint32_t)t); st->ng_i = i + 1; }
         }
       }
+      __syncthreads();
     }
-    __syncthreads();
   }
+
+  // ---- write the state slice back
+  for (uint32_t v = tid; v < Vc; v += WT) {
+    if (use_head) b_g[v] = b_s[v];
+    if (use_ng) cu_g[v] = cu_s[v];
+  }
+  if (tid == 0 && rank == 0) {
+    st->lw[0] = s_lw[0]; st->lw[1] = s_lw[1];
+    st->wl = s_w[0]; st->wn = s_w[1];
+    st->i = s_i;
+  }
+  if (CS > 1) cl_sync();     // no CTA leaves while a peer may still read its shared memory
 }
+
+// Cluster size used for a vocabulary: fixed per V (never per batch), so that the
+// reduction trees of compression and decompression are the same.
+static int walk_cluster_size(uint32_t V) { return (V >= 4096 && V % 64 == 0) ? 4 : 1; }
+
+template <int CS>
+static void launch_walk_cs(const WalkArgs &a, cudaStream_t s) {
+  const uint32_t Vc = a.V / CS;
+  const size_t dyn = (size_t)Vc * 8 + Vc * 4 + Vc * 4 + ((Vc + 31) / 32) * 4 + (Vc / 4) * 4 + 64;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(walk_cl_kernel<CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+    if (CS > 1) cudaFuncSetAttribute(walk_cl_kernel<CS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(a.n_entries * CS);
+  cfg.blockDim = dim3(WT);
+  cfg.dynamicSmemBytes = dyn;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CS; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, walk_cl_kernel<CS>, a);
+}
+
+int walk_ctas_per_chunk(uint32_t V) { return walk_cluster_size(V); }
 
 void launch_walk(const WalkArgs &a, cudaStream_t s) {
   if (a.n_entries <= 0) return;
-  const size_t dyn = ((a.V + 31) / 32 + (a.mode == 1 ? a.V / 4 : 0)) * sizeof(uint32_t);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
-  walk_kernel<<<a.n_entries, WT, dyn, s>>>(a);
+  if (walk_cluster_size(a.V) == 4) launch_walk_cs<4>(a, s);
+  else launch_walk_cs<1>(a, s);
 }
 
 __global__ void walk_init_kernel(WalkState *st, int n, double lw0, double lw1) {
