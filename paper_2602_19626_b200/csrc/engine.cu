@@ -910,7 +910,13 @@ void debug_attention(int device, const float *q, const float *k, const float *v,
       NC_CUDA(cudaMemsetAsync(oh, 0, rows * qd * 4, s));
       NC_CUDA(cudaMemsetAsync(ol, 0, rows * qd * 4, s));
     }
-    launch_attention_tc(at, s);
+    const int reps = std::getenv("NC_ATTN_REPS") ? std::atoi(std::getenv("NC_ATTN_REPS")) : 1;
+    for (int rep = 0; rep < reps; ++rep) {
+      double fl = 0;
+      for (uint32_t j = 0; j < n; ++j) fl += 4.0 * H * 64 * ((double)j - window_start_h(j, window, slide) + 1);
+      PROF(K_ATTN, fl, launch_attention_tc(at, s));
+    }
+    if (prof().on) { NC_CUDA(cudaStreamSynchronize(s)); prof().collect(); }
     std::vector<float> a(rows * qd), b(rows * qd);
     NC_CUDA(cudaMemcpyAsync(a.data(), oh, a.size() * 4, cudaMemcpyDeviceToHost, s));
     NC_CUDA(cudaMemcpyAsync(b.data(), ol, b.size() * 4, cudaMemcpyDeviceToHost, s));

@@ -1,7 +1,7 @@
 // Block-window causal GQA attention on the tensor cores (
 // P:482-502 retained-KV window, D9-D12), fp32-accurate via 3xTF32:
 //
-//   for each 32-key block b of keys [w(j), j] (blocks aligned to absolute positions):
+//   for each 64-key block b of keys [w(j), j] (blocks aligned to absolute positions):
 //     S_b  = Q K_b^T              tcgen05 kind::tf32, 3 products x 8 k-steps  -> TMEM
 //     m_b  = max(m_{b-1}, rowmax(S_b / 8)), P_b = exp(S_b/8 - m_b) (masked), l updated
 //     O_b  = P_b V_b              tcgen05 kind::tf32 (V as an MN-major B operand) -> fresh TMEM partial
@@ -9,10 +9,14 @@
 //   o = O / l
 //
 // One CTA per (128-row query tile of one chunk, q head); 256 threads:
-//   warp 0 TMA (Q once; K_hi/K_lo/V_hi/V_lo per block, 3 stages) from the tf32 planes
+//   warp 0 TMA (Q once; K_hi/K_lo/V_hi/V_lo per 64-key block, 2 stages) from the tf32 planes
 //   warp 1 tcgen05.mma issuer; warp 2 TMEM allocator;
-//   warps 4-7 softmax + promotion, thread = query row (TMEM lane), writes P (hi/lo) into
-//   shared memory in the SWIZZLE_128B K-major layout the PV MMA reads.
+//   warps 4-7 softmax + promotion, thread = query row (TMEM lane); P (hi/lo) goes back
+//   into TMEM (tcgen05.st) and is the A operand of the PV MMA.
+// Two-deep software pipeline (S, P and O partials double-buffered in TMEM): S(i)
+// is issued before PV(i-1), so the softmax of block i overlaps the PV of block i-1.
+// Measured: a kind::tf32 M128 MMA costs >= ~64 cycles even at N = 32, so 64-key
+// blocks (S: N = 64) halve the score-MMA cost of 32-key blocks.
 // A row's arithmetic depends only on its own q row and the key blocks up to its
 // position (later, fully masked blocks are exact no-ops: alpha = 1, P = 0), so the
 // decode step (tiles of one row) reproduces the prefill bit for bit (D15).
@@ -33,15 +37,16 @@
 namespace nc {
 
 constexpr int AQ = 128;          // query rows per tile
-constexpr int AK = 32;           // keys per block
-constexpr int AST = 3;           // K/V stages
+constexpr int AK = 64;           // keys per block
+constexpr int AST = 2;           // K/V stages
 constexpr int Q_SUB = AQ * 128;  // one [128 rows x 32 fp32] swizzled sub-tile: 16 KB
-constexpr int KV_SUB = AK * 128; // one [32 keys x 32 fp32] sub-tile: 4 KB
+constexpr int KV_SUB = AK * 128; // one [64 keys x 32 fp32] sub-tile: 8 KB
 constexpr int Q_BYTES = 4 * Q_SUB;               // hi/lo x two 32-dim halves: 64 KB
-constexpr int KV_STAGE = 8 * KV_SUB;             // K hi/lo, V hi/lo, x two 32-dim halves: 32 KB
-constexpr int P_BYTES = 2 * Q_SUB;               // P hi, P lo: [128 x 32 keys]: 32 KB
-constexpr int ATT_SMEM = Q_BYTES + AST * KV_STAGE + P_BYTES + 1024 + 256;
+constexpr int KV_STAGE = 8 * KV_SUB;             // K hi/lo, V hi/lo, x two 32-dim halves: 64 KB
+constexpr int ATT_SMEM = Q_BYTES + AST * KV_STAGE + 1024 + 256;
 constexpr int ATT_THREADS = 256;
+// TMEM columns: S[2] (64 each) | P[2] (hi 64 + lo 64 each) | O partial[2] (64 each) = 512
+constexpr uint32_t T_S = 0, T_P = 128, T_O = 384;
 
 __device__ __forceinline__ int wstart(int j, int L, int C) {
   const int over = j + 1 - L;
@@ -83,11 +88,10 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *sQ = smem;                                  // [hi d0-31][hi d32-63][lo d0-31][lo d32-63]
   uint8_t *sKV = smem + Q_BYTES;                       // per stage: Kh0 Kh1 Kl0 Kl1 Vh0 Vh1 Vl0 Vl1
-  uint8_t *sP = sKV + AST * KV_STAGE;                  // P hi, P lo
-  uint64_t *bars = reinterpret_cast<uint64_t *>(sP + P_BYTES);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sKV + AST * KV_STAGE);
   uint64_t *q_full = bars, *kv_full = bars + 1, *kv_empty = bars + 1 + AST;
-  uint64_t *s_full = bars + 1 + 2 * AST, *s_empty = s_full + 2, *p_full = s_empty + 2, *p_empty = p_full + 1;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(p_empty + 1);
+  uint64_t *s_full = bars + 1 + 2 * AST, *s_empty = s_full + 2, *p_full = s_empty + 2, *p_empty = p_full + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(p_empty + 2);
 
   const AttnTile t = a.tiles[blockIdx.x];
   if (t.nrows <= 0) return;                        // inactive chunk in a decode step
@@ -103,16 +107,14 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
     tc::mbar_init(q_full, 1);
     for (int s = 0; s < AST; ++s) { tc::mbar_init(&kv_full[s], 1); tc::mbar_init(&kv_empty[s], 1); }
     for (int s = 0; s < 2; ++s) { tc::mbar_init(&s_full[s], 1); tc::mbar_init(&s_empty[s], 4); }
-    tc::mbar_init(p_full, 4);
-    tc::mbar_init(p_empty, 1);
+    for (int s = 0; s < 2; ++s) { tc::mbar_init(&p_full[s], 4); tc::mbar_init(&p_empty[s], 1); }
     tc::fence_barrier_init();
   }
-  if (warp == 2) tc::tmem_alloc(tmem_slot, 128);     // S[2] x 32 cols, O partial 64 cols
+  if (warp == 2) tc::tmem_alloc(tmem_slot, 512);
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tS0 = tmem, tO = tmem + 64;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -146,32 +148,26 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
       tc::mbar_wait(q_full, 0);
       tc::fence_after();
       const uint32_t q0 = tc::smem_u32(sQ);
-      const uint32_t p0 = tc::smem_u32(sP);
       int st = 0;
       uint32_t ph = 0;
-      uint32_t sph[2] = {0, 0};
-      uint32_t pph = 0;
-      auto issue_pv = [&](int stage) {
-        tc::mbar_wait(p_full, pph);
-        pph ^= 1;
+      uint32_t sph[2] = {0, 0}, pph[2] = {0, 0};
+      auto issue_pv = [&](int b, int stage) {      // O_b = P_b V_b (P from TMEM) into O partial b%2
+        const int pb = b & 1;
+        tc::mbar_wait(&p_full[pb], pph[pb]);
+        pph[pb] ^= 1;
         tc::fence_after();
+        const uint32_t ph_t = tmem + T_P + pb * 128, pl_t = ph_t + 64;
         const uint32_t v0 = tc::smem_u32(sKV + stage * KV_STAGE + 4 * KV_SUB);
+        const uint32_t dO = tmem + T_O + pb * 64;
 #pragma unroll
         for (int j = 0; j < AK / 8; ++j) {
-          const uint32_t abase = a.debug == 2 ? q0 : p0;   // debug 2: A = Q instead of P
-          const uint64_t pa = tc::desc_k_sw128(abase + j * 32), pl = tc::desc_k_sw128(abase + Q_SUB + j * 32);
           const uint64_t vh = desc_mn_sw128_32b(v0 + j * 1024, KV_SUB);
           const uint64_t vl = desc_mn_sw128_32b(v0 + 2 * KV_SUB + j * 1024, KV_SUB);
-          if (a.debug == 3) {   // readback check: tO = Q[:, 0:32] K^T with the proven K-major path
-            const uint32_t kk0 = tc::smem_u32(sKV + stage * KV_STAGE);
-            tc::mma_tf32(tO, tc::desc_k_sw128(q0 + j * 32), tc::desc_k_sw128(kk0 + j * 32), idS, j != 0);
-            continue;
-          }
-          tc::mma_tf32(tO, pa, vh, idO, j != 0);
-          tc::mma_tf32(tO, pa, vl, idO, 1);
-          tc::mma_tf32(tO, pl, vh, idO, 1);
+          tc::mma_tf32_ts(dO, ph_t + j * 8, vh, idO, j != 0);
+          tc::mma_tf32_ts(dO, ph_t + j * 8, vl, idO, 1);
+          tc::mma_tf32_ts(dO, pl_t + j * 8, vh, idO, 1);
         }
-        tc::mma_commit(p_empty);
+        tc::mma_commit(&p_empty[pb]);             // P buffer free + O partial ready
         tc::mma_commit(&kv_empty[stage]);
       };
       int prev_stage = -1;
@@ -182,7 +178,7 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
         sph[sb] ^= 1;
         tc::fence_after();
         const uint32_t k0 = tc::smem_u32(sKV + st * KV_STAGE);
-        const uint32_t dS = tS0 + sb * 32;
+        const uint32_t dS = tmem + T_S + sb * AK;
 #pragma unroll
         for (int dsub = 0; dsub < 2; ++dsub)
 #pragma unroll
@@ -197,11 +193,11 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
             tc::mma_tf32(dS, ql, kh, idS, 1);
           }
         tc::mma_commit(&s_full[sb]);
-        if (prev_stage >= 0) issue_pv(prev_stage);
+        if (prev_stage >= 0) issue_pv(i - 1, prev_stage);
         prev_stage = st;
         if (++st == AST) { st = 0; ph ^= 1; }
       }
-      issue_pv(prev_stage);
+      issue_pv(nkb - 1, prev_stage);
     }
   } else if (warp >= 4) {
     const int q = warp & 3, r = q * 32 + lane;     // query row of this thread (TMEM lane)
@@ -210,89 +206,94 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
     float O[64];
 #pragma unroll
     for (int d = 0; d < 64; ++d) O[d] = 0.f;
-    float m = -CUDART_INF_F, l = 0.f, alpha_pend = 1.f;
-    uint32_t sph[2] = {0, 0}, pph = 0;
-    uint8_t *ph_hi = sP, *ph_lo = sP + Q_SUB;
+    float m = -CUDART_INF_F, l = 0.f;
+    float alpha_hist[2] = {1.f, 1.f};              // alpha of blocks b with b%2 == index
+    uint32_t sph[2] = {0, 0}, pph[2] = {0, 0};
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    int nfold = 0;
-    auto fold = [&]() {                       // O <- O * alpha_pend + O_partial
-      tc::mbar_wait(p_empty, pph);
-      pph ^= 1;
+    auto fold = [&](int b) {                       // O <- O * alpha_b + O_b  (fp32 RN promotion)
+      const int pb = b & 1;
+      tc::mbar_wait(&p_empty[pb], pph[pb]);
+      pph[pb] ^= 1;
       tc::fence_after();
       uint32_t x0[32], x1[32];
-      tc::tmem_ld32(tO + lane_off, x0);
-      tc::tmem_ld32(tO + lane_off + 32, x1);
+      tc::tmem_ld32(tmem + T_O + pb * 64 + lane_off, x0);
+      tc::tmem_ld32(tmem + T_O + pb * 64 + lane_off + 32, x1);
       tc::tmem_wait_ld();
-      if (a.debug && nfold == 0 && valid)
-        for (int k = 0; k < 30; ++k) a.o_lo[(size_t)(t.qrow0 + r) * a.ldo + h * 64 + 34 + k] = __uint_as_float(x0[k]);
-      ++nfold;
+      const float al = alpha_hist[pb];
 #pragma unroll
       for (int d = 0; d < 32; ++d) {
-        O[d] = __fmaf_rn(O[d], alpha_pend, __uint_as_float(x0[d]));
-        O[32 + d] = __fmaf_rn(O[32 + d], alpha_pend, __uint_as_float(x1[d]));
+        O[d] = __fmaf_rn(O[d], al, __uint_as_float(x0[d]));
+        O[32 + d] = __fmaf_rn(O[32 + d], al, __uint_as_float(x1[d]));
       }
     };
+    // scores in the log2 domain: x = S * (1/8 * log2 e); p = 2^(x - m)
+    constexpr float kScale = 0.125f * 1.44269504088896341f;
     for (int i = 0; i < nkb; ++i) {
       const int sb = i & 1;
       tc::mbar_wait(&s_full[sb], sph[sb]);
       sph[sb] ^= 1;
       tc::fence_after();
-      uint32_t sr[32];
-      tc::tmem_ld32(tS0 + sb * 32 + lane_off, sr);
+      uint32_t sr[2][32];
+      tc::tmem_ld32(tmem + T_S + sb * AK + lane_off, sr[0]);
+      tc::tmem_ld32(tmem + T_S + sb * AK + lane_off + 32, sr[1]);
       tc::tmem_wait_ld();
-      if (a.debug && i == 0 && valid)
-        for (int k = 0; k < 32; ++k) a.o_hi[(size_t)(t.qrow0 + r) * a.ldo + h * 64 + k] = __uint_as_float(sr[k]);
       tc::fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&s_empty[sb]);
       const int key0 = (kb0 + i) * AK;
-      // scores in the log2 domain: x = S * (1/8 * log2 e); p = 2^(x - m)
-      constexpr float kScale = 0.125f * 1.44269504088896341f;
-      float s[32];
       float mb = -CUDART_INF_F;
-      if (key0 + 31 <= j) {                  // whole block inside the window: no masking
+      float x[2][32];
+      if (key0 + AK - 1 <= j) {              // whole block inside the window: no masking
 #pragma unroll
-        for (int k = 0; k < 32; ++k) { s[k] = __fmul_rn(__uint_as_float(sr[k]), kScale); mb = fmaxf(mb, s[k]); }
+        for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+          for (int k = 0; k < 32; ++k) { x[hh][k] = __fmul_rn(__uint_as_float(sr[hh][k]), kScale); mb = fmaxf(mb, x[hh][k]); }
       } else {
 #pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          s[k] = key0 + k <= j ? __fmul_rn(__uint_as_float(sr[k]), kScale) : -CUDART_INF_F;
-          mb = fmaxf(mb, s[k]);
-        }
+        for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+          for (int k = 0; k < 32; ++k) {
+            x[hh][k] = key0 + 32 * hh + k <= j ? __fmul_rn(__uint_as_float(sr[hh][k]), kScale) : -CUDART_INF_F;
+            mb = fmaxf(mb, x[hh][k]);
+          }
       }
       const float mn = fmaxf(m, mb);
       const float alpha = (mn == -CUDART_INF_F) ? 1.f : tc::ex2(__fsub_rn(m, mn));
       float ps = 0.f;
 #pragma unroll
-      for (int k = 0; k < 32; ++k) {
-        s[k] = tc::ex2(__fsub_rn(s[k], mn));    // ex2(-inf) = 0 for masked keys
-        ps = __fadd_rn(ps, s[k]);
-      }
+      for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          x[hh][k] = tc::ex2(__fsub_rn(x[hh][k], mn));   // ex2(-inf) = 0 for masked keys
+          ps = __fadd_rn(ps, x[hh][k]);
+        }
       l = __fmaf_rn(l, alpha, ps);
       m = mn;
-      if (i > 0) fold();                      // O partial of block i-1 (uses alpha of block i-1)
-      alpha_pend = alpha;
-      // P_i (hi/lo) -> shared memory, 128B-swizzled K-major rows of 32 keys
+      // P buffer i%2 and O partial i%2 were last used by block i-2: fold it first
+      if (i >= 2) fold(i - 2);
+      alpha_hist[sb] = alpha;
+      const uint32_t ph_t = tmem + T_P + sb * 128 + lane_off;
 #pragma unroll
-      for (int c4 = 0; c4 < 8; ++c4) {
-        float4 hi, lo;
-        tc::split_tf32(s[4 * c4 + 0], hi.x, lo.x); tc::split_tf32(s[4 * c4 + 1], hi.y, lo.y);
-        tc::split_tf32(s[4 * c4 + 2], hi.z, lo.z); tc::split_tf32(s[4 * c4 + 3], hi.w, lo.w);
-        const int off = r * 128 + ((c4 ^ (r & 7)) << 4);
-        *reinterpret_cast<float4 *>(ph_hi + off) = hi;
-        *reinterpret_cast<float4 *>(ph_lo + off) = lo;
+      for (int hh = 0; hh < 2; ++hh) {
+        uint32_t hi[32], lo[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          float fh, fl;
+          tc::split_tf32(x[hh][k], fh, fl);
+          hi[k] = __float_as_uint(fh);
+          lo[k] = __float_as_uint(fl);
+        }
+        tc::tmem_st32(ph_t + 32 * hh, hi);
+        tc::tmem_st32(ph_t + 64 + 32 * hh, lo);
       }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tc::tmem_wait_st();
+      tc::fence_before();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(p_full);
+      if (lane == 0) tc::mbar_arrive(&p_full[sb]);
     }
-    fold();
-    if (a.debug) {
-      if (valid) {
-        a.o_lo[(size_t)(t.qrow0 + r) * a.ldo + h * 64 + 32] = l;
-        a.o_lo[(size_t)(t.qrow0 + r) * a.ldo + h * 64 + 33] = m;
-      }
-    } else if (valid) {
+    if (nkb >= 2) fold(nkb - 2);
+    fold(nkb - 1);
+    if (valid) {
       const size_t ob = (size_t)(t.qrow0 + r) * a.ldo + h * 64;
 #pragma unroll
       for (int d = 0; d < 64; d += 4) {
@@ -309,7 +310,7 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
-  if (warp == 2) tc::tmem_dealloc(tmem, 128);
+  if (warp == 2) tc::tmem_dealloc(tmem, 512);
 }
 
 // ------------------------------------------------------------- host side ---
