@@ -244,7 +244,10 @@ void model_load(nc_model *m, const std::string &path, int device) {
   const char *ga = std::getenv("NC_ATTN");
   m->use_tc_attn = m->use_tc && !(ga && std::string(ga) == "simt");
   ensure_rope(m, 4096);
-  NC_CUDA(cudaStreamCreateWithFlags(&m->walk_stream, cudaStreamNonBlocking));
+  int lo_prio = 0, hi_prio = 0;
+  NC_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+  // the walk is the sequential critical path: its clusters go first when SMs free up
+  NC_CUDA(cudaStreamCreateWithPriority(&m->walk_stream, cudaStreamNonBlocking, hi_prio));
   NC_CUDA(cudaStreamCreateWithFlags(&m->ng_stream, cudaStreamNonBlocking));
 }
 
@@ -591,7 +594,8 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
   NC_CUDA(cudaStreamWaitEvent(ws, ev_init, 0));
   // the walk keeps one SM per chunk busy for a whole slab: leave those SMs out of
   // the persistent GEMM grids so every GEMM CTA is resident at once
-  set_reserved_sms(n_slabs > 1 ? n_chunks * walk_ctas_per_chunk(S.V) : 0);
+  // GEMM tiles are claimed dynamically, so the persistent grids need no SM reservation
+  set_reserved_sms(0);
   WalkArgs wbase{};
   wbase.logits = nullptr; wbase.ldl = S.V;
   wbase.tokens = tokens_dev; wbase.tok_off = tok_off_d;

@@ -17,6 +17,7 @@ struct TcGemmArgs {
   int layer, n_q_cols, n_kv_cols;
   RowMeta rows; KvRing ring;
   const float *rope_cos, *rope_sin;
+  int *tile_ctr;               // set by the launcher
 };
 
 struct TcOperands {

@@ -160,13 +160,15 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
         const uint32_t v0 = tc::smem_u32(sKV + stage * KV_STAGE + 4 * KV_SUB);
         const uint32_t dO = tmem + T_O + pb * 64;
 #pragma unroll
-        for (int j = 0; j < AK / 8; ++j) {
+        for (int j = 0; j < AK / 8; ++j) {          // corrections first, hi*hi last (see k_gemm_tc.cu)
           const uint64_t vh = desc_mn_sw128_32b(v0 + j * 1024, KV_SUB);
           const uint64_t vl = desc_mn_sw128_32b(v0 + 2 * KV_SUB + j * 1024, KV_SUB);
-          tc::mma_tf32_ts(dO, ph_t + j * 8, vh, idO, j != 0);
-          tc::mma_tf32_ts(dO, ph_t + j * 8, vl, idO, 1);
+          tc::mma_tf32_ts(dO, ph_t + j * 8, vl, idO, j != 0);
           tc::mma_tf32_ts(dO, pl_t + j * 8, vh, idO, 1);
         }
+#pragma unroll
+        for (int j = 0; j < AK / 8; ++j)
+          tc::mma_tf32_ts(dO, ph_t + j * 8, desc_mn_sw128_32b(v0 + j * 1024, KV_SUB), idO, 1);
         tc::mma_commit(&p_empty[pb]);             // P buffer free + O partial ready
         tc::mma_commit(&kv_empty[stage]);
       };
@@ -180,7 +182,7 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
         const uint32_t k0 = tc::smem_u32(sKV + st * KV_STAGE);
         const uint32_t dS = tmem + T_S + sb * AK;
 #pragma unroll
-        for (int dsub = 0; dsub < 2; ++dsub)
+        for (int dsub = 0; dsub < 2; ++dsub)     // corrections first, hi*hi last (see k_gemm_tc.cu)
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             const uint32_t adv = j * 32;
@@ -188,9 +190,16 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
             const uint64_t ql = tc::desc_k_sw128(q0 + (2 + dsub) * Q_SUB + adv);
             const uint64_t kh = tc::desc_k_sw128(k0 + dsub * KV_SUB + adv);
             const uint64_t kl = tc::desc_k_sw128(k0 + (2 + dsub) * KV_SUB + adv);
-            tc::mma_tf32(dS, qh, kh, idS, (dsub | j) != 0);
-            tc::mma_tf32(dS, qh, kl, idS, 1);
+            tc::mma_tf32(dS, qh, kl, idS, (dsub | j) != 0);
             tc::mma_tf32(dS, ql, kh, idS, 1);
+          }
+#pragma unroll
+        for (int dsub = 0; dsub < 2; ++dsub)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t adv = j * 32;
+            tc::mma_tf32(dS, tc::desc_k_sw128(q0 + dsub * Q_SUB + adv), tc::desc_k_sw128(k0 + dsub * KV_SUB + adv),
+                         idS, 1);
           }
         tc::mma_commit(&s_full[sb]);
         if (prev_stage >= 0) issue_pv(i - 1, prev_stage);

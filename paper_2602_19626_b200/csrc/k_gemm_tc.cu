@@ -3,7 +3,7 @@
 // accumulator in TMEM, and the layer's epilogue fused on the TMEM read-out.
 //
 //   C[m, n] = epi( sum_k A[m,k] B[n,k] ),  A = A_hi + A_lo, B = B_hi + B_lo (tf32 planes)
-//   per 8-wide k step:  D += A_hi B_hi ; D += A_hi B_lo ; D += A_lo B_hi   (fixed order)
+//   per 32-wide k block: D = sum_k (A_hi B_lo + A_lo B_hi), then D += sum_k A_hi B_hi (fixed order)
 //
 // Precision: every tcgen05.mma that accumulates into D rounds the sum toward
 // zero (measured: relative bias -1.6e-5 at K = 1536 on positive data, i.e.
@@ -17,8 +17,11 @@
 //   warp 1  MMA issuer  (one thread): 12 tcgen05.mma per 32-wide k block into a partial buffer
 //   warp 2  TMEM allocator (4 x 128 fp32 columns: rotating partial buffers)
 //   warps 4-7 promotion + epilogue: tcgen05.ld partials -> fp32 RN sums -> fused epilogue -> global
-// Tiles 128 x 128, tile index t -> (m = t % num_m, n = t / num_m) so the CTAs
-// resident at one time share B (weights) tiles through L2.
+// Tiles 128 x 128 are claimed dynamically (atomic counter; the last CTA to exit
+// resets it), so CTAs that start late -- e.g. on SMs a concurrently running walk
+// held -- find no work instead of stalling the GEMM.  Claim order streams the
+// larger operand once: M-fastest when there are at least as many N tiles as M
+// tiles (weights / vocab head), N-fastest otherwise (A tile reused from L2).
 //
 // Row results do not depend on which other rows share the tile (each output
 // element is one fixed sequence of MMAs), so prefill and decode agree bit for
@@ -38,11 +41,11 @@
 
 namespace nc {
 
-constexpr int TBM = 128, TBN = 128, TBK = 32, TSTAGES = 3, NPART = 4;
+constexpr int TBM = 128, TBN = 128, TBK = 32, TSTAGES = 3, NPART = 4, NSCHED = 4;
 constexpr int TILE_A_BYTES = TBM * TBK * 4;   // 16 KB
 constexpr int TILE_B_BYTES = TBN * TBK * 4;   // 16 KB
 constexpr int STAGE_BYTES = 2 * TILE_A_BYTES + 2 * TILE_B_BYTES;
-constexpr int TC_SMEM = TSTAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int TC_SMEM = TSTAGES * STAGE_BYTES + 1024 /*align*/ + 512 /*barriers, schedule*/;
 constexpr int TC_THREADS = 256;
 
 template <int EPI>
@@ -57,17 +60,24 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
   uint64_t *empty = full + TSTAGES;
   uint64_t *tfull = empty + TSTAGES;
   uint64_t *tempty = tfull + NPART;
-  uint32_t *tmem_base_smem = reinterpret_cast<uint32_t *>(tempty + NPART);
+  uint64_t *sch_full = tempty + NPART, *sch_empty = sch_full + NSCHED;
+  int *sch_tile = reinterpret_cast<int *>(sch_empty + NSCHED);
+  uint32_t *tmem_base_smem = reinterpret_cast<uint32_t *>(sch_tile + NSCHED);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int num_m = (a.M + TBM - 1) / TBM, num_n = (a.N + TBN - 1) / TBN;
   const int n_tiles = num_m * num_n;
   const int nk = a.K / TBK;
+  const bool m_fast = num_n >= num_m;
+  auto tile_mn = [&](int t, int &mb, int &nb) {
+    if (m_fast) { mb = t % num_m; nb = t / num_m; } else { nb = t % num_n; mb = t / num_n; }
+  };
 
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch(&tmAh); tc::tma_prefetch(&tmAl); tc::tma_prefetch(&tmBh); tc::tma_prefetch(&tmBl);
     for (int s = 0; s < TSTAGES; ++s) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
     for (int s = 0; s < NPART; ++s) { tc::mbar_init(&tfull[s], 1); tc::mbar_init(&tempty[s], 4); }
+    for (int s = 0; s < NSCHED; ++s) { tc::mbar_init(&sch_full[s], 1); tc::mbar_init(&sch_empty[s], 5); }
     tc::fence_barrier_init();
   }
   if (warp == 2) tc::tmem_alloc(tmem_base_smem, NPART * TBN);
@@ -81,8 +91,16 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-        const int mb = t % num_m, nb = t / num_m;
+      for (int jt = 0;; ++jt) {
+        const int slot = jt % NSCHED;
+        tc::mbar_wait(&sch_empty[slot], ((jt / NSCHED) & 1) ^ 1);
+        const int claimed = atomicAdd(a.tile_ctr, 1);
+        const int t = claimed < n_tiles ? claimed : -1;
+        sch_tile[slot] = t;
+        tc::mbar_arrive(&sch_full[slot]);
+        if (t < 0) break;
+        int mb, nb;
+        tile_mn(t, mb, nb);
         for (int kb = 0; kb < nk; ++kb) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t *st = smem + stage * STAGE_BYTES;
@@ -103,7 +121,12 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
       uint32_t phase = 0;
       int buf = 0;
       uint32_t buf_phase = 0;
-      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      for (int jt = 0;; ++jt) {
+        const int slot = jt % NSCHED;
+        tc::mbar_wait(&sch_full[slot], (jt / NSCHED) & 1);
+        const int t = sch_tile[slot];
+        tc::mbar_arrive(&sch_empty[slot]);
+        if (t < 0) break;
         for (int kb = 0; kb < nk; ++kb) {
           tc::mbar_wait(&tempty[buf], buf_phase ^ 1);     // partial buffer drained by the epilogue
           tc::mbar_wait(&full[stage], phase);
@@ -113,12 +136,19 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
           const uint64_t dah = tc::desc_k_sw128(s0), dal = tc::desc_k_sw128(s0 + TILE_A_BYTES);
           const uint64_t dbh = tc::desc_k_sw128(s0 + 2 * TILE_A_BYTES);
           const uint64_t dbl = tc::desc_k_sw128(s0 + 2 * TILE_A_BYTES + TILE_B_BYTES);
+          // the small correction products first, hi*hi last: each accumulate rounds
+          // toward zero relative to the running sum, which stays ~2^-11 smaller
+          // while the corrections are added (4 large-magnitude truncations, not 12)
 #pragma unroll
           for (int j = 0; j < TBK / 8; ++j) {
             const uint64_t adv = (uint64_t)(j * 32) >> 4;   // 8 tf32 = 32 bytes along K
-            tc::mma_tf32(d, dah + adv, dbh + adv, idesc, j != 0);
-            tc::mma_tf32(d, dah + adv, dbl + adv, idesc, 1);
+            tc::mma_tf32(d, dah + adv, dbl + adv, idesc, j != 0);
             tc::mma_tf32(d, dal + adv, dbh + adv, idesc, 1);
+          }
+#pragma unroll
+          for (int j = 0; j < TBK / 8; ++j) {
+            const uint64_t adv = (uint64_t)(j * 32) >> 4;
+            tc::mma_tf32(d, dah + adv, dbh + adv, idesc, 1);
           }
           tc::mma_commit(&empty[stage]);
           tc::mma_commit(&tfull[buf]);
@@ -132,8 +162,15 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
     const int q = warp & 3;   // TMEM lanes 32q .. 32q+31
     int buf = 0;
     uint32_t buf_phase = 0;
-    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-      const int mb = t % num_m, nb = t / num_m;
+    for (int jt = 0;; ++jt) {
+      const int slot = jt % NSCHED;
+      tc::mbar_wait(&sch_full[slot], (jt / NSCHED) & 1);
+      const int t = sch_tile[slot];
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&sch_empty[slot]);
+      if (t < 0) break;
+      int mb, nb;
+      tile_mn(t, mb, nb);
       float acc[TBN];
 #pragma unroll
       for (int j = 0; j < TBN; ++j) acc[j] = 0.f;
@@ -266,6 +303,14 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
   __syncthreads();
   tc::fence_after();
   if (warp == 2) tc::tmem_dealloc(tmem_base, NPART * TBN);
+  if (threadIdx.x == 0) {            // last CTA out resets the tile counter for the next launch
+    __threadfence();
+    if (atomicAdd(a.tile_ctr + 1, 1) == (int)gridDim.x - 1) {
+      a.tile_ctr[0] = 0;
+      a.tile_ctr[1] = 0;
+      __threadfence();
+    }
+  }
 }
 
 // ------------------------------------------------------------- host side ---
@@ -314,6 +359,16 @@ const CUtensorMap *tmap_2d(const float *ptr, uint64_t rows, uint64_t cols, uint3
 static int g_reserved_sms = 0;
 void set_reserved_sms(int n) { g_reserved_sms = n; }
 
+static int *tile_counter() {   // {next tile, CTAs done}; zero between launches
+  static int *ctr = nullptr;
+  if (!ctr) {
+    if (cudaMalloc(&ctr, 2 * sizeof(int)) != cudaSuccess) throw std::runtime_error("cudaMalloc tile counter");
+    cudaMemset(ctr, 0, 2 * sizeof(int));
+    cudaDeviceSynchronize();
+  }
+  return ctr;
+}
+
 static int num_sms() {
   static int n = 0;
   if (!n) {
@@ -335,7 +390,9 @@ static void launch_tc(const TcGemmArgs &a, const TcOperands &op, cudaStream_t s)
   const CUtensorMap *bh = tmap_2d(op.B_hi, a.N, a.K, TBN), *bl = tmap_2d(op.B_lo, a.N, a.K, TBN);
   const int tiles = ((a.M + TBM - 1) / TBM) * ((a.N + TBN - 1) / TBN);
   const int grid = std::min(tiles, std::max(1, num_sms() - g_reserved_sms));
-  gemm_tc_kernel<EPI><<<grid, TC_THREADS, TC_SMEM, s>>>(*ah, *al, *bh, *bl, a);
+  TcGemmArgs aa = a;
+  aa.tile_ctr = tile_counter();
+  gemm_tc_kernel<EPI><<<grid, TC_THREADS, TC_SMEM, s>>>(*ah, *al, *bh, *bl, aa);
 }
 
 void launch_gemm_tc(GemmEpi epi, const TcGemmArgs &a, const TcOperands &op, cudaStream_t s) {
