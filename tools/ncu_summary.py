@@ -23,7 +23,8 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__warps_active.avg.pct_of_peak_sustained_active", "smsp__issue_active.avg.pct_of_peak_sustained_active",
         "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
         "l1tex__t_bytes.sum", "lts__t_bytes.sum", "sm__cycles_elapsed.avg.per_second"]
-CLASS = {"attention_kernel": "attention", "walk_kernel": "walk", "gemm_tc_kernel<0>": "gemm_qkv",
+CLASS = {"attention_kernel": "attention", "walk_kernel": "walk", "attn_tc_kernel": "attention",
+         "walk_cl_kernel<4>": "walk", "gemm_tc_kernel<0>": "gemm_qkv",
          "gemm_tc_kernel<1>": "gemm_o|gemm_down", "gemm_tc_kernel<2>": "gemm_gateup", "gemm_tc_kernel<3>": "gemm_head"}
 
 
@@ -72,7 +73,7 @@ def full(tag, name, rep):
         wr = float(r[idx["dram__bytes_write.sum"]].replace(",", "")) * (1e6 if units[idx["dram__bytes_write.sum"]] == "Mbyte" else 1e3 if units[idx["dram__bytes_write.sum"]] == "Kbyte" else 1e9 if units[idx["dram__bytes_write.sum"]] == "Gbyte" else 1)
         base = kn.split("(")[0].replace("void ", "").strip()
         for c in CLASS.get(base, base).split("|"):
-            traffic.setdefault(c, rd + wr)
+            traffic[c] = rd + wr
         lines.append("")
     open(os.path.join(PROF, f"{tag}_{name}.md"), "w").write("\n".join(lines) + "\n")
     tpath = os.path.join(PROF, "ncu_traffic.json")
