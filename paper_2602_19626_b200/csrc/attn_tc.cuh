@@ -18,4 +18,7 @@ struct AttnTcArgs {
 
 void launch_attention_tc(const AttnTcArgs &a, cudaStream_t s);
 
+// diagnostics build (-DNC_ATT_TIMING): print per-phase cycle sums to stderr
+void attn_timing_report();
+
 }  // namespace nc

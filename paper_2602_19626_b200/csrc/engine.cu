@@ -2,6 +2,7 @@
 // one-row-per-chunk decode-step driver (decompress), host WNC + NC05 assembly.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -864,6 +865,34 @@ void debug_gemm(int device, const float *A, const float *B, uint32_t M, uint32_t
     g.M = (int)M; g.N = (int)N; g.K = (int)K; g.rinv = r_d; g.C = c_d; g.ldc = (int)N;
     TcOperands op{ah, al, (uint64_t)M, bh, bl};
     launch_gemm_tc(EPI_HEAD, g, op, s);
+    // diagnostics: NC_GEMM_REPS=n times n launches (NC_GEMM_EPI=resid: the residual
+    // epilogue on a scratch h; NC_GEMM_NOSTORE=1: no epilogue writes) -> stderr
+    if (const char *reps_s = getenv("NC_GEMM_REPS")) {
+      const int reps = std::max(1, atoi(reps_s));
+      const char *epi_s = getenv("NC_GEMM_EPI");
+      const bool resid = epi_s && std::string(epi_s) == "resid";
+      TcGemmArgs t = g;
+      t.no_store = getenv("NC_GEMM_NOSTORE") ? 1 : 0;
+      float *h = nullptr;
+      if (resid) {
+        h = bag.get<float>((size_t)M * N * 3);
+        NC_CUDA(cudaMemsetAsync(h, 0, (size_t)M * N * 12, s));
+        t.C = h; t.C_hi = h + (size_t)M * N; t.C_lo = h + 2 * (size_t)M * N;
+      }
+      cudaEvent_t e0, e1;
+      cudaEventCreate(&e0); cudaEventCreate(&e1);
+      for (int w = 0; w < 3; ++w) launch_gemm_tc(resid ? EPI_RESID : EPI_HEAD, t, op, s);
+      cudaEventRecord(e0, s);
+      for (int r = 0; r < reps; ++r) launch_gemm_tc(resid ? EPI_RESID : EPI_HEAD, t, op, s);
+      cudaEventRecord(e1, s);
+      NC_CUDA(cudaEventSynchronize(e1));
+      float ms = 0;
+      cudaEventElapsedTime(&ms, e0, e1);
+      cudaEventDestroy(e0); cudaEventDestroy(e1);
+      const double us = 1e3 * ms / reps;
+      fprintf(stderr, "gemm_tc M=%u N=%u K=%u epi=%s nostore=%d: %.1f us/launch, %.1f TFLOP/s (algorithmic)\n", M, N,
+              K, resid ? "resid" : "head", t.no_store, us, 2.0 * M * N * K / (us * 1e-6) / 1e12);
+    }
   } else {
     GemmArgs g{};
     g.A = a_d; g.lda = (int)K; g.B = b_d; g.ldb = (int)K; g.M = (int)M; g.N = (int)N; g.K = (int)K;
@@ -921,6 +950,7 @@ void debug_attention(int device, const float *q, const float *k, const float *v,
       PROF(K_ATTN, fl, launch_attention_tc(at, s));
     }
     if (prof().on) { NC_CUDA(cudaStreamSynchronize(s)); prof().collect(); }
+    if (std::getenv("NC_ATTN_REPS")) attn_timing_report();
     std::vector<float> a(rows * qd), b(rows * qd);
     NC_CUDA(cudaMemcpyAsync(a.data(), oh, a.size() * 4, cudaMemcpyDeviceToHost, s));
     NC_CUDA(cudaMemcpyAsync(b.data(), ol, b.size() * 4, cudaMemcpyDeviceToHost, s));

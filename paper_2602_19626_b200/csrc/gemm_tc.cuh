@@ -18,6 +18,7 @@ struct TcGemmArgs {
   RowMeta rows; KvRing ring;
   const float *rope_cos, *rope_sin;
   int *tile_ctr;               // set by the launcher
+  int no_store;                // diagnostics only (debug_gemm timing): skip the epilogue's global writes
 };
 
 struct TcOperands {

@@ -9,7 +9,9 @@
 //   o = O / l
 //
 // One CTA per (128-row query tile of one chunk, q head); 256 threads:
-//   warp 0 TMA (Q once; K_hi/K_lo/V_hi/V_lo per 64-key block, 2 stages) from the tf32 planes
+//   warp 0 TMA: Q once, then K_hi/K_lo per 64-key block (3 stages, freed when S(i) completes)
+//   warp 3 TMA: V_hi/V_lo per 64-key block (2 stages, freed when PV(i) completes) -- split so
+//          the K loads run ahead of the late V consumer (one shared ring stalled S on the loads)
 //   warp 1 tcgen05.mma issuer; warp 2 TMEM allocator;
 //   warps 4-7 softmax + promotion, thread = query row (TMEM lane); P (hi/lo) goes back
 //   into TMEM (tcgen05.st) and is the A operand of the PV MMA.
@@ -26,6 +28,7 @@
 #include <math_constants.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -38,15 +41,27 @@ namespace nc {
 
 constexpr int AQ = 128;          // query rows per tile
 constexpr int AK = 64;           // keys per block
-constexpr int AST = 2;           // K/V stages
+constexpr int KST = 3;           // K stages
+constexpr int VST = 2;           // V stages
 constexpr int Q_SUB = AQ * 128;  // one [128 rows x 32 fp32] swizzled sub-tile: 16 KB
 constexpr int KV_SUB = AK * 128; // one [64 keys x 32 fp32] sub-tile: 8 KB
 constexpr int Q_BYTES = 4 * Q_SUB;               // hi/lo x two 32-dim halves: 64 KB
-constexpr int KV_STAGE = 8 * KV_SUB;             // K hi/lo, V hi/lo, x two 32-dim halves: 64 KB
-constexpr int ATT_SMEM = Q_BYTES + AST * KV_STAGE + 1024 + 256;
+constexpr int K_STAGE = 4 * KV_SUB;              // K hi/lo x two 32-dim halves: 32 KB
+constexpr int V_STAGE = 4 * KV_SUB;              // V hi/lo x two 32-dim halves: 32 KB
+constexpr int ATT_SMEM = Q_BYTES + KST * K_STAGE + VST * V_STAGE + 1024 + 256;
 constexpr int ATT_THREADS = 256;
 // TMEM columns: S[2] (64 each) | P[2] (hi 64 + lo 64 each) | O partial[2] (64 each) = 512
 constexpr uint32_t T_S = 0, T_P = 128, T_O = 384;
+
+#ifdef NC_ATT_TIMING
+// diagnostics build only: per-phase cycle sums (softmax warp 4 lane 0, MMA thread)
+__device__ unsigned long long g_att_clk[16];
+#define ATT_T0() const long long _t0 = clock64()
+#define ATT_ACC(i, t) atomicAdd(&g_att_clk[i], (unsigned long long)(clock64() - (t)))
+#else
+#define ATT_T0()
+#define ATT_ACC(i, t)
+#endif
 
 __device__ __forceinline__ int wstart(int j, int L, int C) {
   const int over = j + 1 - L;
@@ -87,10 +102,12 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *sQ = smem;                                  // [hi d0-31][hi d32-63][lo d0-31][lo d32-63]
-  uint8_t *sKV = smem + Q_BYTES;                       // per stage: Kh0 Kh1 Kl0 Kl1 Vh0 Vh1 Vl0 Vl1
-  uint64_t *bars = reinterpret_cast<uint64_t *>(sKV + AST * KV_STAGE);
-  uint64_t *q_full = bars, *kv_full = bars + 1, *kv_empty = bars + 1 + AST;
-  uint64_t *s_full = bars + 1 + 2 * AST, *s_empty = s_full + 2, *p_full = s_empty + 2, *p_empty = p_full + 2;
+  uint8_t *sK = smem + Q_BYTES;                        // per stage: Kh0 Kh1 Kl0 Kl1
+  uint8_t *sV = sK + KST * K_STAGE;                     // per stage: Vh0 Vh1 Vl0 Vl1
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sV + VST * V_STAGE);
+  uint64_t *q_full = bars, *k_full = bars + 1, *k_empty = k_full + KST, *v_full = k_empty + KST,
+           *v_empty = v_full + VST;
+  uint64_t *s_full = v_empty + VST, *s_empty = s_full + 2, *p_full = s_empty + 2, *p_empty = p_full + 2;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(p_empty + 2);
 
   const AttnTile t = a.tiles[blockIdx.x];
@@ -105,7 +122,8 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
   if (threadIdx.x == 0) {
     tc::tma_prefetch(&tmQh); tc::tma_prefetch(&tmKh); tc::tma_prefetch(&tmVh);
     tc::mbar_init(q_full, 1);
-    for (int s = 0; s < AST; ++s) { tc::mbar_init(&kv_full[s], 1); tc::mbar_init(&kv_empty[s], 1); }
+    for (int s = 0; s < KST; ++s) { tc::mbar_init(&k_full[s], 1); tc::mbar_init(&k_empty[s], 1); }
+    for (int s = 0; s < VST; ++s) { tc::mbar_init(&v_full[s], 1); tc::mbar_init(&v_empty[s], 1); }
     for (int s = 0; s < 2; ++s) { tc::mbar_init(&s_full[s], 1); tc::mbar_init(&s_empty[s], 4); }
     for (int s = 0; s < 2; ++s) { tc::mbar_init(&p_full[s], 4); tc::mbar_init(&p_empty[s], 1); }
     tc::fence_barrier_init();
@@ -115,6 +133,9 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
+#ifdef NC_ATT_TIMING
+  const long long t_cta = clock64();
+#endif
 
   if (warp == 0) {
     if (lane == 0) {
@@ -126,88 +147,110 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
       int st = 0;
       uint32_t ph = 0;
       for (int i = 0; i < nkb; ++i) {
-        tc::mbar_wait(&kv_empty[st], ph ^ 1);
-        uint8_t *b = sKV + st * KV_STAGE;
+        tc::mbar_wait(&k_empty[st], ph ^ 1);
+        uint8_t *b = sK + st * K_STAGE;
         const int slot = ((kb0 + i) * AK) % a.ring;
-        tc::mbar_expect_tx(&kv_full[st], KV_STAGE);
-        tma_load_4d(b + 0 * KV_SUB, &tmKh, 0, g, slot, zc, &kv_full[st]);
-        tma_load_4d(b + 1 * KV_SUB, &tmKh, 32, g, slot, zc, &kv_full[st]);
-        tma_load_4d(b + 2 * KV_SUB, &tmKl, 0, g, slot, zc, &kv_full[st]);
-        tma_load_4d(b + 3 * KV_SUB, &tmKl, 32, g, slot, zc, &kv_full[st]);
-        tma_load_4d(b + 4 * KV_SUB, &tmVh, 0, g, slot, zc, &kv_full[st]);
-        tma_load_4d(b + 5 * KV_SUB, &tmVh, 32, g, slot, zc, &kv_full[st]);
-        tma_load_4d(b + 6 * KV_SUB, &tmVl, 0, g, slot, zc, &kv_full[st]);
-        tma_load_4d(b + 7 * KV_SUB, &tmVl, 32, g, slot, zc, &kv_full[st]);
-        if (++st == AST) { st = 0; ph ^= 1; }
+        tc::mbar_expect_tx(&k_full[st], K_STAGE);
+        tma_load_4d(b + 0 * KV_SUB, &tmKh, 0, g, slot, zc, &k_full[st]);
+        tma_load_4d(b + 1 * KV_SUB, &tmKh, 32, g, slot, zc, &k_full[st]);
+        tma_load_4d(b + 2 * KV_SUB, &tmKl, 0, g, slot, zc, &k_full[st]);
+        tma_load_4d(b + 3 * KV_SUB, &tmKl, 32, g, slot, zc, &k_full[st]);
+        if (++st == KST) { st = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp == 3) {
+    if (lane == 0) {
+      int st = 0;
+      uint32_t ph = 0;
+      for (int i = 0; i < nkb; ++i) {
+        tc::mbar_wait(&v_empty[st], ph ^ 1);
+        uint8_t *b = sV + st * V_STAGE;
+        const int slot = ((kb0 + i) * AK) % a.ring;
+        tc::mbar_expect_tx(&v_full[st], V_STAGE);
+        tma_load_4d(b + 0 * KV_SUB, &tmVh, 0, g, slot, zc, &v_full[st]);
+        tma_load_4d(b + 1 * KV_SUB, &tmVh, 32, g, slot, zc, &v_full[st]);
+        tma_load_4d(b + 2 * KV_SUB, &tmVl, 0, g, slot, zc, &v_full[st]);
+        tma_load_4d(b + 3 * KV_SUB, &tmVl, 32, g, slot, zc, &v_full[st]);
+        if (++st == VST) { st = 0; ph ^= 1; }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idS = tc::idesc_tf32(AQ, AK);                  // S: K-major A and B
-      constexpr uint32_t idO = tc::idesc_tf32(AQ, 64) | (1u << 16);     // O: B (V) MN-major
-      tc::mbar_wait(q_full, 0);
+    // MMA issuer: the whole warp runs the loop on warp-uniform values; one elected
+    // lane issues each tcgen05 instruction (see tc::elect_one)
+    constexpr uint32_t idS = tc::idesc_tf32(AQ, AK);                  // S: K-major A and B
+    constexpr uint32_t idO = tc::idesc_tf32(AQ, 64) | (1u << 16);     // O: B (V) MN-major
+    tc::mbar_wait(q_full, 0);
+    tc::fence_after();
+    const uint64_t q_desc = tc::desc_k_sw128(tc::smem_u32(sQ));
+    const uint64_t k_desc0 = tc::desc_k_sw128(tc::smem_u32(sK));
+    const uint64_t v_desc0 = desc_mn_sw128_32b(tc::smem_u32(sV), KV_SUB);
+    // descriptor start addresses are in 16-byte units: constant byte offsets add as (bytes >> 4)
+    auto off = [](uint32_t bytes) { return (uint64_t)(bytes >> 4); };
+    int st = 0;
+    uint32_t ph = 0;
+    uint32_t sph[2] = {0, 0}, pph[2] = {0, 0};
+    int vst = 0;
+    uint32_t vph = 0;
+    auto issue_pv = [&](int b) {                 // O_b = P_b V_b (P from TMEM) into O partial b%2
+      const int pb = b & 1;
+      tc::mbar_wait(&p_full[pb], pph[pb]);
+      pph[pb] ^= 1;
+      tc::mbar_wait(&v_full[vst], vph);
       tc::fence_after();
-      const uint32_t q0 = tc::smem_u32(sQ);
-      int st = 0;
-      uint32_t ph = 0;
-      uint32_t sph[2] = {0, 0}, pph[2] = {0, 0};
-      auto issue_pv = [&](int b, int stage) {      // O_b = P_b V_b (P from TMEM) into O partial b%2
-        const int pb = b & 1;
-        tc::mbar_wait(&p_full[pb], pph[pb]);
-        pph[pb] ^= 1;
-        tc::fence_after();
-        const uint32_t ph_t = tmem + T_P + pb * 128, pl_t = ph_t + 64;
-        const uint32_t v0 = tc::smem_u32(sKV + stage * KV_STAGE + 4 * KV_SUB);
-        const uint32_t dO = tmem + T_O + pb * 64;
+      const uint32_t ph_t = tmem + T_P + pb * 128, pl_t = ph_t + 64;
+      const uint64_t vd = v_desc0 + off(vst * V_STAGE);
+      const uint32_t dO = tmem + T_O + pb * 64;
 #pragma unroll
-        for (int j = 0; j < AK / 8; ++j) {          // corrections first, hi*hi last (see k_gemm_tc.cu)
-          const uint64_t vh = desc_mn_sw128_32b(v0 + j * 1024, KV_SUB);
-          const uint64_t vl = desc_mn_sw128_32b(v0 + 2 * KV_SUB + j * 1024, KV_SUB);
-          tc::mma_tf32_ts(dO, ph_t + j * 8, vl, idO, j != 0);
-          tc::mma_tf32_ts(dO, pl_t + j * 8, vh, idO, 1);
+      for (int j = 0; j < AK / 8; ++j) {          // corrections first, hi*hi last (see k_gemm_tc.cu)
+        if (tc::elect_one()) tc::mma_tf32_ts(dO, ph_t + j * 8, vd + off(2 * KV_SUB + j * 1024), idO, j != 0);
+        if (tc::elect_one()) tc::mma_tf32_ts(dO, pl_t + j * 8, vd + off(j * 1024), idO, 1);
+      }
+#pragma unroll
+      for (int j = 0; j < AK / 8; ++j)
+        if (tc::elect_one()) tc::mma_tf32_ts(dO, ph_t + j * 8, vd + off(j * 1024), idO, 1);
+      if (tc::elect_one()) {
+        tc::mma_commit(&p_empty[pb]);             // P buffer free + O partial ready
+        tc::mma_commit(&v_empty[vst]);
+      }
+      __syncwarp();
+      if (++vst == VST) { vst = 0; vph ^= 1; }
+    };
+    for (int i = 0; i < nkb; ++i) {
+      tc::mbar_wait(&k_full[st], ph);
+      const int sb = i & 1;
+      tc::mbar_wait(&s_empty[sb], sph[sb] ^ 1);
+      sph[sb] ^= 1;
+      tc::fence_after();
+      const uint64_t kd = k_desc0 + off(st * K_STAGE);
+      const uint32_t dS = tmem + T_S + sb * AK;
+#pragma unroll
+      for (int dsub = 0; dsub < 2; ++dsub)     // corrections first, hi*hi last (see k_gemm_tc.cu)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t adv = j * 32;
+          if (tc::elect_one())
+            tc::mma_tf32(dS, q_desc + off(dsub * Q_SUB + adv), kd + off((2 + dsub) * KV_SUB + adv), idS,
+                         (dsub | j) != 0);
+          if (tc::elect_one())
+            tc::mma_tf32(dS, q_desc + off((2 + dsub) * Q_SUB + adv), kd + off(dsub * KV_SUB + adv), idS, 1);
         }
 #pragma unroll
-        for (int j = 0; j < AK / 8; ++j)
-          tc::mma_tf32_ts(dO, ph_t + j * 8, desc_mn_sw128_32b(v0 + j * 1024, KV_SUB), idO, 1);
-        tc::mma_commit(&p_empty[pb]);             // P buffer free + O partial ready
-        tc::mma_commit(&kv_empty[stage]);
-      };
-      int prev_stage = -1;
-      for (int i = 0; i < nkb; ++i) {
-        tc::mbar_wait(&kv_full[st], ph);
-        const int sb = i & 1;
-        tc::mbar_wait(&s_empty[sb], sph[sb] ^ 1);
-        sph[sb] ^= 1;
-        tc::fence_after();
-        const uint32_t k0 = tc::smem_u32(sKV + st * KV_STAGE);
-        const uint32_t dS = tmem + T_S + sb * AK;
+      for (int dsub = 0; dsub < 2; ++dsub)
 #pragma unroll
-        for (int dsub = 0; dsub < 2; ++dsub)     // corrections first, hi*hi last (see k_gemm_tc.cu)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const uint32_t adv = j * 32;
-            const uint64_t qh = tc::desc_k_sw128(q0 + dsub * Q_SUB + adv);
-            const uint64_t ql = tc::desc_k_sw128(q0 + (2 + dsub) * Q_SUB + adv);
-            const uint64_t kh = tc::desc_k_sw128(k0 + dsub * KV_SUB + adv);
-            const uint64_t kl = tc::desc_k_sw128(k0 + (2 + dsub) * KV_SUB + adv);
-            tc::mma_tf32(dS, qh, kl, idS, (dsub | j) != 0);
-            tc::mma_tf32(dS, ql, kh, idS, 1);
-          }
-#pragma unroll
-        for (int dsub = 0; dsub < 2; ++dsub)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const uint32_t adv = j * 32;
-            tc::mma_tf32(dS, tc::desc_k_sw128(q0 + dsub * Q_SUB + adv), tc::desc_k_sw128(k0 + dsub * KV_SUB + adv),
-                         idS, 1);
-          }
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t adv = j * 32;
+          if (tc::elect_one())
+            tc::mma_tf32(dS, q_desc + off(dsub * Q_SUB + adv), kd + off(dsub * KV_SUB + adv), idS, 1);
+        }
+      if (tc::elect_one()) {
         tc::mma_commit(&s_full[sb]);
-        if (prev_stage >= 0) issue_pv(i - 1, prev_stage);
-        prev_stage = st;
-        if (++st == AST) { st = 0; ph ^= 1; }
+        tc::mma_commit(&k_empty[st]);
       }
-      issue_pv(nkb - 1, prev_stage);
+      __syncwarp();
+      if (i > 0) issue_pv(i - 1);
+      if (++st == KST) { st = 0; ph ^= 1; }
     }
+    issue_pv(nkb - 1);
   } else if (warp >= 4) {
     const int q = warp & 3, r = q * 32 + lane;     // query row of this thread (TMEM lane)
     const bool valid = r < t.nrows;
@@ -219,11 +262,14 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
     float alpha_hist[2] = {1.f, 1.f};              // alpha of blocks b with b%2 == index
     uint32_t sph[2] = {0, 0}, pph[2] = {0, 0};
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    auto fold = [&](int b) {                       // O <- O * alpha_b + O_b  (fp32 RN promotion)
+    auto fold_wait = [&](int b) {                  // PV(b) complete: P buffer b%2 free, O partial b%2 ready
       const int pb = b & 1;
       tc::mbar_wait(&p_empty[pb], pph[pb]);
       pph[pb] ^= 1;
       tc::fence_after();
+    };
+    auto fold_apply = [&](int b) {                 // O <- O * alpha_b + O_b  (fp32 RN promotion)
+      const int pb = b & 1;
       uint32_t x0[32], x1[32];
       tc::tmem_ld32(tmem + T_O + pb * 64 + lane_off, x0);
       tc::tmem_ld32(tmem + T_O + pb * 64 + lane_off + 32, x1);
@@ -235,12 +281,28 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
         O[32 + d] = __fmaf_rn(O[32 + d], al, __uint_as_float(x1[d]));
       }
     };
+    auto fold = [&](int b) { fold_wait(b); fold_apply(b); };
     // scores in the log2 domain: x = S * (1/8 * log2 e); p = 2^(x - m)
     constexpr float kScale = 0.125f * 1.44269504088896341f;
     for (int i = 0; i < nkb; ++i) {
       const int sb = i & 1;
+#ifdef NC_ATT_TIMING
+      long long tp = clock64();
+#endif
       tc::mbar_wait(&s_full[sb], sph[sb]);
+#ifdef NC_ATT_TIMING
+      if (threadIdx.x == 128) { atomicAdd(&g_att_clk[0], (unsigned long long)(clock64() - tp)); atomicAdd(&g_att_clk[7], 1ull); }
+      tp = clock64();
+#endif
       sph[sb] ^= 1;
+      if (a.debug == 9) {      // diagnostics: handshakes only (no TMEM traffic, no math)
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&s_empty[sb]);
+        if (i >= 2) { const int pb = i & 1; tc::mbar_wait(&p_empty[pb], pph[pb]); pph[pb] ^= 1; }
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&p_full[sb]);
+        continue;
+      }
       tc::fence_after();
       uint32_t sr[2][32];
       tc::tmem_ld32(tmem + T_S + sb * AK + lane_off, sr[0]);
@@ -250,37 +312,52 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&s_empty[sb]);
       const int key0 = (kb0 + i) * AK;
-      float mb = -CUDART_INF_F;
+      // raw scores; masked keys -> -inf.  Max first on the raw scores (kScale > 0 and RN
+      // rounding is monotone, so max(S) * kScale == max(S * kScale) exactly), as a tree.
       float x[2][32];
       if (key0 + AK - 1 <= j) {              // whole block inside the window: no masking
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh)
 #pragma unroll
-          for (int k = 0; k < 32; ++k) { x[hh][k] = __fmul_rn(__uint_as_float(sr[hh][k]), kScale); mb = fmaxf(mb, x[hh][k]); }
+          for (int k = 0; k < 32; ++k) x[hh][k] = __uint_as_float(sr[hh][k]);
       } else {
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh)
 #pragma unroll
-          for (int k = 0; k < 32; ++k) {
-            x[hh][k] = key0 + 32 * hh + k <= j ? __fmul_rn(__uint_as_float(sr[hh][k]), kScale) : -CUDART_INF_F;
-            mb = fmaxf(mb, x[hh][k]);
-          }
+          for (int k = 0; k < 32; ++k)
+            x[hh][k] = key0 + 32 * hh + k <= j ? __uint_as_float(sr[hh][k]) : -CUDART_INF_F;
       }
+      float t[32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) t[k] = fmaxf(x[0][k], x[1][k]);
+#pragma unroll
+      for (int w2 = 16; w2 >= 1; w2 >>= 1)
+#pragma unroll
+        for (int k = 0; k < w2; ++k) t[k] = fmaxf(t[k], t[k + w2]);
+      const float mb = __fmul_rn(t[0], kScale);
       const float mn = fmaxf(m, mb);
       const float alpha = (mn == -CUDART_INF_F) ? 1.f : tc::ex2(__fsub_rn(m, mn));
-      float ps = 0.f;
+      // p = 2^(S * kScale - m) with one FFMA per score; -inf scores give ex2(-inf) = 0.
+      // (mn == -inf only when every key so far is masked: p = 0 then too.)
+      const float nmn = mn == -CUDART_INF_F ? 0.f : -mn;
+      float ps4[4] = {0.f, 0.f, 0.f, 0.f};   // 4 independent partial sums (latency), fixed order
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh)
 #pragma unroll
         for (int k = 0; k < 32; ++k) {
-          x[hh][k] = tc::ex2(__fsub_rn(x[hh][k], mn));   // ex2(-inf) = 0 for masked keys
-          ps = __fadd_rn(ps, x[hh][k]);
+          x[hh][k] = tc::ex2(__fmaf_rn(x[hh][k], kScale, nmn));
+          ps4[k & 3] = __fadd_rn(ps4[k & 3], x[hh][k]);
         }
+      const float ps = __fadd_rn(__fadd_rn(ps4[0], ps4[1]), __fadd_rn(ps4[2], ps4[3]));
       l = __fmaf_rn(l, alpha, ps);
       m = mn;
-      // P buffer i%2 and O partial i%2 were last used by block i-2: fold it first
-      if (i >= 2) fold(i - 2);
-      alpha_hist[sb] = alpha;
+#ifdef NC_ATT_TIMING
+      if (threadIdx.x == 128) atomicAdd(&g_att_clk[1], (unsigned long long)(clock64() - tp));
+      tp = clock64();
+#endif
+      // P buffer i%2 was last read by PV(i-2): wait for it, store P(i), then fold O
+      // partial i-2 while the stores drain
+      if (i >= 2) fold_wait(i - 2);
       const uint32_t ph_t = tmem + T_P + sb * 128 + lane_off;
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
@@ -295,13 +372,26 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
         tc::tmem_st32(ph_t + 32 * hh, hi);
         tc::tmem_st32(ph_t + 64 + 32 * hh, lo);
       }
+#ifdef NC_ATT_TIMING
+      if (threadIdx.x == 128) atomicAdd(&g_att_clk[3], (unsigned long long)(clock64() - tp));
+      tp = clock64();
+#endif
+      if (i >= 2) fold_apply(i - 2);
+      alpha_hist[sb] = alpha;
       tc::tmem_wait_st();
       tc::fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&p_full[sb]);
+#ifdef NC_ATT_TIMING
+      if (threadIdx.x == 128) atomicAdd(&g_att_clk[2], (unsigned long long)(clock64() - tp));
+#endif
     }
-    if (nkb >= 2) fold(nkb - 2);
-    fold(nkb - 1);
+    if (a.debug == 9) {
+      for (int b = (nkb >= 2 ? nkb - 2 : 0); b < nkb; ++b) { const int pb = b & 1; tc::mbar_wait(&p_empty[pb], pph[pb]); pph[pb] ^= 1; }
+    } else {
+      if (nkb >= 2) fold(nkb - 2);
+      fold(nkb - 1);
+    }
     if (valid) {
       const size_t ob = (size_t)(t.qrow0 + r) * a.ldo + h * 64;
 #pragma unroll
@@ -320,7 +410,29 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
   __syncthreads();
   tc::fence_after();
   if (warp == 2) tc::tmem_dealloc(tmem, 512);
+#ifdef NC_ATT_TIMING
+  if (threadIdx.x == 0) { atomicAdd(&g_att_clk[11], (unsigned long long)(clock64() - t_cta)); atomicAdd(&g_att_clk[12], 1ull); }
+#endif
 }
+
+#ifdef NC_ATT_TIMING
+void attn_timing_report() {
+  unsigned long long h[16];
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(h, g_att_clk, sizeof(h));
+  const double nb = (double)(h[7] ? h[7] : 1), nc = (double)(h[12] ? h[12] : 1);
+  fprintf(stderr,
+          "attn timing per block (softmax warp): wait S %.0f | max/exp/sum %.0f | fold+wait_st %.0f (wait %.0f) | "
+          "pwait+split+st %.0f ; MMA thread per block: wait kv %.0f, wait s_empty %.0f, wait p_full %.0f ; per CTA %.0f "
+          "cycles, %.1f blocks\n",
+          h[0] / nb, h[1] / nb, h[2] / nb, h[4] / nb, h[3] / nb, h[9] / nb, h[10] / nb, h[8] / nb, h[11] / nc, nb / nc);
+  cudaMemset(g_att_clk, 0, 0);
+  unsigned long long z[16] = {};
+  cudaMemcpyToSymbol(g_att_clk, z, sizeof(z));
+}
+#else
+void attn_timing_report() {}
+#endif
 
 // ------------------------------------------------------------- host side ---
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn2() {

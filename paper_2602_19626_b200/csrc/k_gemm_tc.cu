@@ -12,16 +12,28 @@
 // partials in fp32 round-to-nearest registers ("promotion"), which restores
 // ~fp32 accuracy (D14).
 //
-// Persistent, warp-specialised CTA (256 threads, 1 CTA / SM):
-//   warp 0  TMA producer (one thread): 4 tiles per stage (A_hi, A_lo, B_hi, B_lo), 3 stages
-//   warp 1  MMA issuer  (one thread): 12 tcgen05.mma per 32-wide k block into a partial buffer
-//   warp 2  TMEM allocator (4 x 128 fp32 columns: rotating partial buffers)
-//   warps 4-7 promotion + epilogue: tcgen05.ld partials -> fp32 RN sums -> fused epilogue -> global
-// Tiles 128 x 128 are claimed dynamically (atomic counter; the last CTA to exit
-// resets it), so CTAs that start late -- e.g. on SMs a concurrently running walk
-// held -- find no work instead of stalling the GEMM.  Claim order streams the
-// larger operand once: M-fastest when there are at least as many N tiles as M
-// tiles (weights / vocab head), N-fastest otherwise (A tile reused from L2).
+// Tile shape.  A tcgen05.mma costs the same ~153 cycles for every N up to 256
+// (tools/micro/mma_bench.cu: M=128 tf32 N=64/128/256 all 153 cycles), and the
+// chip's TMA/L2 service rate (~6.3 KB/cycle, B300_MICROARCH) cannot feed 148
+// SMs streaming four fp32 planes for 128 x 256 tiles.  So a CTA PAIR
+// (cluster of 2, cta_group::2) computes a 256 x 256 tile: each CTA stages its
+// 128 rows of A and 128 of the 256 rows of B (64 KB per 32-wide k block), the
+// leader issues M=256 N=256 MMAs that read both CTAs' shared memory, and each
+// CTA's TMEM holds its 128 x 256 accumulator rows.
+//
+// Warp roles (320 threads = 10 warps per CTA, 1 CTA / SM):
+//   warps 0-7 promotion + epilogue (both CTAs): warp w reads TMEM lanes 32(w%4).. and
+//           column half w/4; tcgen05.ld partials -> fp32 RN sums (128 registers)
+//           -> fused epilogue -> global
+//   warp 8  TMA producer (one thread; both CTAs load their halves, bytes land on the
+//           leader's barrier) and TMEM allocator (2 x 256 fp32 columns, pair alloc)
+//   warp 9  MMA issuer (leader only): 12 pair MMAs per 32-wide k block into a partial buffer
+// Tiles are claimed dynamically by the leader's producer (atomic counter; the
+// last CTA to exit resets it) and broadcast to the peer through DSMEM, so CTAs
+// that start late -- e.g. on SMs a concurrently running walk held -- find no
+// work instead of stalling the GEMM.  Claim order streams the larger operand
+// once: M-fastest when there are at least as many N tiles as M tiles (weights /
+// vocab head), N-fastest otherwise (A tile reused from L2).
 //
 // Row results do not depend on which other rows share the tile (each output
 // element is one fixed sequence of MMAs), so prefill and decode agree bit for
@@ -41,12 +53,91 @@
 
 namespace nc {
 
-constexpr int TBM = 128, TBN = 128, TBK = 32, TSTAGES = 3, NPART = 4, NSCHED = 4;
-constexpr int TILE_A_BYTES = TBM * TBK * 4;   // 16 KB
-constexpr int TILE_B_BYTES = TBN * TBK * 4;   // 16 KB
-constexpr int STAGE_BYTES = 2 * TILE_A_BYTES + 2 * TILE_B_BYTES;
-constexpr int TC_SMEM = TSTAGES * STAGE_BYTES + 1024 /*align*/ + 512 /*barriers, schedule*/;
-constexpr int TC_THREADS = 256;
+constexpr int TBM = 128;              // rows per CTA (pair tile: 256)
+constexpr int TBN = 256;              // pair tile columns (MMA N); each CTA stages TBN / 2 rows of B
+constexpr int TBK = 32, TSTAGES = 3, NPART = 2, NSCHED = 4;
+// k blocks per TMEM partial.  Promotion reads the whole 128 x 256 fp32 partial
+// (128 KB) per CTA; tcgen05.ld moves ~64 B/cycle/SM (B300_MICROARCH), i.e.
+// 2048 cycles, against 12 * 128 = 1536 MMA cycles per 32-wide k block -- so a
+// partial spans 2 k blocks (3072 MMA cycles) to keep the tensor pipe the bound.
+constexpr int KPP = 2;
+constexpr int EPI_WARPS = 8, EPI_COLS = TBN / 2;
+constexpr int TILE_A_BYTES = TBM * TBK * 4;          // 16 KB
+constexpr int TILE_B_BYTES = (TBN / 2) * TBK * 4;    // 16 KB
+constexpr int STAGE_BYTES = 2 * TILE_A_BYTES + 2 * TILE_B_BYTES;   // 64 KB per CTA
+constexpr int OUT_STAGE_BYTES = EPI_WARPS * 32 * 32 * 4;   // 32 KB: epilogue transpose tiles
+constexpr int TC_SMEM = TSTAGES * STAGE_BYTES + OUT_STAGE_BYTES + 1024 /*align*/ + 512 /*barriers, schedule*/;
+constexpr int TC_THREADS = 320;
+constexpr int W_TMA = 8, W_MMA = 9;
+// sch_empty arrivals per tile claim: leader MMA + 8 epilogue warps per CTA + the peer's producer
+constexpr int SCHED_CONSUMERS = 1 + 2 * EPI_WARPS + 1;
+
+// Row-contiguous output through a per-warp 32 x 32 shared tile.  Lane l holds
+// 32 consecutive outputs v[0..31] of row l (its TMEM lane); written to the
+// tile as 8 float4 chunks swizzled by (l & 7), read back 4 rows per
+// instruction (lanes 8i..8i+7 -> row 4i'+i, chunk lane&7), so each global
+// access covers 128 contiguous bytes of one row.  d0 (d1, d2) are the row's
+// destinations (this lane's row); d0 == nullptr skips the row.
+//   ST_PLAIN  d0 = v
+//   ST_SPLIT  d0 = tf32 hi(v), d1 = lo(v)
+//   ST_RESID  d0 = v (the updated residual h), d1 = hi(v), d2 = lo(v)
+enum { ST_PLAIN = 0, ST_SPLIT = 1, ST_RESID = 2 };
+template <int MODE>
+__device__ __forceinline__ void store_rows32(float *stg, const float *v, float *d0, float *d1, float *d2, int lane) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    *reinterpret_cast<float4 *>(stg + lane * 32 + 4 * (k ^ (lane & 7))) =
+        make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+  __syncwarp();
+  const int c4 = lane & 7;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = 4 * i + (lane >> 3);
+    float *p0 = reinterpret_cast<float *>(__shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(d0), r));
+    float *p1 = MODE != ST_PLAIN
+                    ? reinterpret_cast<float *>(__shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(d1), r))
+                    : nullptr;
+    float *p2 = MODE == ST_RESID
+                    ? reinterpret_cast<float *>(__shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(d2), r))
+                    : nullptr;
+    if (p0) {
+      float4 y = *reinterpret_cast<const float4 *>(stg + r * 32 + 4 * (c4 ^ (r & 7)));
+      if (MODE == ST_PLAIN) {
+        *reinterpret_cast<float4 *>(p0 + 4 * c4) = y;
+      } else {
+        if (MODE == ST_RESID) *reinterpret_cast<float4 *>(p0 + 4 * c4) = y;
+        float4 hi, lo;
+        tc::split_tf32(y.x, hi.x, lo.x); tc::split_tf32(y.y, hi.y, lo.y);
+        tc::split_tf32(y.z, hi.z, lo.z); tc::split_tf32(y.w, hi.w, lo.w);
+        float *ph = MODE == ST_RESID ? p1 : p0, *pl = MODE == ST_RESID ? p2 : p1;
+        *reinterpret_cast<float4 *>(ph + 4 * c4) = hi;
+        *reinterpret_cast<float4 *>(pl + 4 * c4) = lo;
+      }
+    }
+  }
+  __syncwarp();
+}
+
+// The inverse: v[0..31] (this lane's row) = src row [0, 32) read row-contiguously
+// through the same tile; src == nullptr gives zeros.
+__device__ __forceinline__ void load_rows32(float *stg, float *v, const float *src, int lane) {
+  const int c4 = lane & 7;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = 4 * i + (lane >> 3);
+    const float *p =
+        reinterpret_cast<const float *>(__shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(src), r));
+    *reinterpret_cast<float4 *>(stg + r * 32 + 4 * (c4 ^ (r & 7))) =
+        p ? *reinterpret_cast<const float4 *>(p + 4 * c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const float4 y = *reinterpret_cast<const float4 *>(stg + lane * 32 + 4 * (k ^ (lane & 7)));
+    v[4 * k] = y.x; v[4 * k + 1] = y.y; v[4 * k + 2] = y.z; v[4 * k + 3] = y.w;
+  }
+  __syncwarp();
+}
 
 template <int EPI>
 __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_constant__ CUtensorMap tmAh,
@@ -56,7 +147,8 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
                                                                 TcGemmArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + TSTAGES * STAGE_BYTES);
+  float *stage_out = reinterpret_cast<float *>(smem + TSTAGES * STAGE_BYTES);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + TSTAGES * STAGE_BYTES + OUT_STAGE_BYTES);
   uint64_t *empty = full + TSTAGES;
   uint64_t *tfull = empty + TSTAGES;
   uint64_t *tempty = tfull + NPART;
@@ -65,7 +157,8 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
   uint32_t *tmem_base_smem = reinterpret_cast<uint32_t *>(sch_tile + NSCHED);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int num_m = (a.M + TBM - 1) / TBM, num_n = (a.N + TBN - 1) / TBN;
+  const uint32_t rank = tc::cluster_ctarank();      // 0 = leader of the pair
+  const int num_m = (a.M + 2 * TBM - 1) / (2 * TBM), num_n = (a.N + TBN - 1) / TBN;
   const int n_tiles = num_m * num_n;
   const int nk = a.K / TBK;
   const bool m_fast = num_n >= num_m;
@@ -73,50 +166,60 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
     if (m_fast) { mb = t % num_m; nb = t / num_m; } else { nb = t % num_n; mb = t / num_n; }
   };
 
-  if (warp == 0 && lane == 0) {
+  if (warp == W_TMA && lane == 0) {
     tc::tma_prefetch(&tmAh); tc::tma_prefetch(&tmAl); tc::tma_prefetch(&tmBh); tc::tma_prefetch(&tmBl);
     for (int s = 0; s < TSTAGES; ++s) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
-    for (int s = 0; s < NPART; ++s) { tc::mbar_init(&tfull[s], 1); tc::mbar_init(&tempty[s], 4); }
-    for (int s = 0; s < NSCHED; ++s) { tc::mbar_init(&sch_full[s], 1); tc::mbar_init(&sch_empty[s], 5); }
+    for (int s = 0; s < NPART; ++s) { tc::mbar_init(&tfull[s], 1); tc::mbar_init(&tempty[s], 2 * EPI_WARPS); }
+    for (int s = 0; s < NSCHED; ++s) { tc::mbar_init(&sch_full[s], 1); tc::mbar_init(&sch_empty[s], SCHED_CONSUMERS); }
     tc::fence_barrier_init();
   }
-  if (warp == 2) tc::tmem_alloc(tmem_base_smem, NPART * TBN);
+  if (warp == W_TMA) tc::tmem_alloc_pair(tmem_base_smem, NPART * TBN);
   tc::fence_before();
-  __syncthreads();
+  tc::cluster_sync();
   tc::fence_after();
   const uint32_t tmem_base = *tmem_base_smem;
 
-  if (warp == 0) {
+  if (warp == W_TMA) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
       for (int jt = 0;; ++jt) {
         const int slot = jt % NSCHED;
-        tc::mbar_wait(&sch_empty[slot], ((jt / NSCHED) & 1) ^ 1);
-        const int claimed = atomicAdd(a.tile_ctr, 1);
-        const int t = claimed < n_tiles ? claimed : -1;
-        sch_tile[slot] = t;
-        tc::mbar_arrive(&sch_full[slot]);
+        int t;
+        if (rank == 0) {
+          tc::mbar_wait(&sch_empty[slot], ((jt / NSCHED) & 1) ^ 1);
+          const int claimed = atomicAdd(a.tile_ctr, 1);
+          t = claimed < n_tiles ? claimed : -1;
+          sch_tile[slot] = t;
+          tc::st_cluster_s32(tc::mapa(&sch_tile[slot], 1), t);
+          tc::mbar_arrive(&sch_full[slot]);
+          tc::mbar_arrive_cluster(tc::mapa(&sch_full[slot], 1));
+        } else {
+          tc::mbar_wait_cluster(&sch_full[slot], (jt / NSCHED) & 1);
+          t = sch_tile[slot];
+          tc::mbar_arrive_remote(tc::mapa(&sch_empty[slot], 0));
+        }
         if (t < 0) break;
         int mb, nb;
         tile_mn(t, mb, nb);
+        const int row_a = mb * 2 * TBM + (int)rank * TBM, row_b = nb * TBN + (int)rank * (TBN / 2);
         for (int kb = 0; kb < nk; ++kb) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t *st = smem + stage * STAGE_BYTES;
-          tc::mbar_expect_tx(&full[stage], STAGE_BYTES);
-          tc::tma_load_2d(st, &tmAh, kb * TBK, mb * TBM, &full[stage]);
-          tc::tma_load_2d(st + TILE_A_BYTES, &tmAl, kb * TBK, mb * TBM, &full[stage]);
-          tc::tma_load_2d(st + 2 * TILE_A_BYTES, &tmBh, kb * TBK, nb * TBN, &full[stage]);
-          tc::tma_load_2d(st + 2 * TILE_A_BYTES + TILE_B_BYTES, &tmBl, kb * TBK, nb * TBN, &full[stage]);
+          if (rank == 0) tc::mbar_expect_tx(&full[stage], 2 * STAGE_BYTES);   // both CTAs' bytes
+          tc::tma_load_2d_pair(st, &tmAh, kb * TBK, row_a, &full[stage]);
+          tc::tma_load_2d_pair(st + TILE_A_BYTES, &tmAl, kb * TBK, row_a, &full[stage]);
+          tc::tma_load_2d_pair(st + 2 * TILE_A_BYTES, &tmBh, kb * TBK, row_b, &full[stage]);
+          tc::tma_load_2d_pair(st + 2 * TILE_A_BYTES + TILE_B_BYTES, &tmBl, kb * TBK, row_b, &full[stage]);
           if (++stage == TSTAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
-  } else if (warp == 1) {
-    // -------------------------------------------------------------- MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc = tc::idesc_tf32(TBM, TBN);
+  } else if (warp == W_MMA) {
+    // ------------------------------------------------------ MMA issuer (leader)
+    if (rank == 0 && lane == 0) {
+      constexpr uint32_t idesc = tc::idesc_tf32(2 * TBM, TBN);
       int stage = 0;
       uint32_t phase = 0;
       int buf = 0;
@@ -127,172 +230,159 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
         const int t = sch_tile[slot];
         tc::mbar_arrive(&sch_empty[slot]);
         if (t < 0) break;
-        for (int kb = 0; kb < nk; ++kb) {
-          tc::mbar_wait(&tempty[buf], buf_phase ^ 1);     // partial buffer drained by the epilogue
-          tc::mbar_wait(&full[stage], phase);
-          tc::fence_after();
+        // one TMEM partial per KPP k blocks: all correction products of the span
+        // first (the partial is still ~2^-11 of its final size, so their
+        // truncations are negligible), then the hi*hi products -- 4 * KPP large-
+        // magnitude truncations per partial; each stage is released after its hi*hi
+        for (int kb0 = 0; kb0 < nk; kb0 += KPP) {
+          const int nkp = min(KPP, nk - kb0);
+          tc::mbar_wait(&tempty[buf], buf_phase ^ 1);   // partial drained by both CTAs' epilogues
           const uint32_t d = tmem_base + buf * TBN;
-          const uint32_t s0 = tc::smem_u32(smem + stage * STAGE_BYTES);
-          const uint64_t dah = tc::desc_k_sw128(s0), dal = tc::desc_k_sw128(s0 + TILE_A_BYTES);
-          const uint64_t dbh = tc::desc_k_sw128(s0 + 2 * TILE_A_BYTES);
-          const uint64_t dbl = tc::desc_k_sw128(s0 + 2 * TILE_A_BYTES + TILE_B_BYTES);
-          // the small correction products first, hi*hi last: each accumulate rounds
-          // toward zero relative to the running sum, which stays ~2^-11 smaller
-          // while the corrections are added (4 large-magnitude truncations, not 12)
+          int st = stage;
+          uint32_t ph = phase;
+          for (int i = 0; i < nkp; ++i) {
+            tc::mbar_wait(&full[st], ph);
+            tc::fence_after();
+            const uint32_t s0 = tc::smem_u32(smem + st * STAGE_BYTES);
+            const uint64_t dah = tc::desc_k_sw128(s0), dal = tc::desc_k_sw128(s0 + TILE_A_BYTES);
+            const uint64_t dbh = tc::desc_k_sw128(s0 + 2 * TILE_A_BYTES);
+            const uint64_t dbl = tc::desc_k_sw128(s0 + 2 * TILE_A_BYTES + TILE_B_BYTES);
 #pragma unroll
-          for (int j = 0; j < TBK / 8; ++j) {
-            const uint64_t adv = (uint64_t)(j * 32) >> 4;   // 8 tf32 = 32 bytes along K
-            tc::mma_tf32(d, dah + adv, dbl + adv, idesc, j != 0);
-            tc::mma_tf32(d, dal + adv, dbh + adv, idesc, 1);
+            for (int j = 0; j < TBK / 8; ++j) {
+              const uint64_t adv = (uint64_t)(j * 32) >> 4;   // 8 tf32 = 32 bytes along K
+              tc::mma_tf32_pair(d, dah + adv, dbl + adv, idesc, (i | j) != 0);
+              tc::mma_tf32_pair(d, dal + adv, dbh + adv, idesc, 1);
+            }
+            if (++st == TSTAGES) { st = 0; ph ^= 1; }
           }
+          for (int i = 0; i < nkp; ++i) {
+            const uint32_t s0 = tc::smem_u32(smem + stage * STAGE_BYTES);
+            const uint64_t dah = tc::desc_k_sw128(s0), dbh = tc::desc_k_sw128(s0 + 2 * TILE_A_BYTES);
 #pragma unroll
-          for (int j = 0; j < TBK / 8; ++j) {
-            const uint64_t adv = (uint64_t)(j * 32) >> 4;
-            tc::mma_tf32(d, dah + adv, dbh + adv, idesc, 1);
+            for (int j = 0; j < TBK / 8; ++j) {
+              const uint64_t adv = (uint64_t)(j * 32) >> 4;
+              tc::mma_tf32_pair(d, dah + adv, dbh + adv, idesc, 1);
+            }
+            tc::mma_commit_pair(&empty[stage]);
+            if (++stage == TSTAGES) { stage = 0; phase ^= 1; }
           }
-          tc::mma_commit(&empty[stage]);
-          tc::mma_commit(&tfull[buf]);
-          if (++stage == TSTAGES) { stage = 0; phase ^= 1; }
+          tc::mma_commit_pair(&tfull[buf]);
           if (++buf == NPART) { buf = 0; buf_phase ^= 1; }
         }
       }
     }
-  } else if (warp >= 4) {
+  } else {
     // ---------------------------------------------------------------- epilogue
-    const int q = warp & 3;   // TMEM lanes 32q .. 32q+31
+    const int q = warp & 3;     // TMEM lanes 32q .. 32q+31
+    const int hc = warp >> 2;   // column half of the 256-wide tile
+    const uint32_t sch_empty_leader = tc::mapa(&sch_empty[0], 0);
+    const uint32_t tempty_leader = tc::mapa(&tempty[0], 0);
     int buf = 0;
     uint32_t buf_phase = 0;
     for (int jt = 0;; ++jt) {
       const int slot = jt % NSCHED;
-      tc::mbar_wait(&sch_full[slot], (jt / NSCHED) & 1);
+      tc::mbar_wait_cluster(&sch_full[slot], (jt / NSCHED) & 1);
       const int t = sch_tile[slot];
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&sch_empty[slot]);
+      if (lane == 0) tc::mbar_arrive_remote(sch_empty_leader + slot * 8);
       if (t < 0) break;
       int mb, nb;
       tile_mn(t, mb, nb);
-      float acc[TBN];
+      const int m = mb * (2 * TBM) + (int)rank * TBM + q * 32 + lane;
+      const bool row_ok = m < a.M;
+      const float rs = (EPI != EPI_RESID && row_ok && a.rinv) ? a.rinv[m] : 1.f;   // loaded under the k loop
+      float acc[EPI_COLS];
+      float *stg = stage_out + warp * 32 * 32;   // this warp's 32 x 32 transpose tile
+      if (EPI == EPI_RESID) {
+        // h_new = ((h + P0) + P1) + ...: the promotion sum starts from the residual row
+        // (read now, under the first partials' MMAs; the output is then store-only)
 #pragma unroll
-      for (int j = 0; j < TBN; ++j) acc[j] = 0.f;
-      for (int kb = 0; kb < nk; ++kb) {
+        for (int sl = 0; sl < EPI_COLS / 32; ++sl) {
+          const int c0 = nb * TBN + hc * EPI_COLS + sl * 32;
+          load_rows32(stg, acc + sl * 32, (row_ok && c0 < a.N) ? a.C + (size_t)m * a.ldc + c0 : nullptr, lane);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < EPI_COLS; ++j) acc[j] = 0.f;
+      }
+      for (int kb0 = 0; kb0 < nk; kb0 += KPP) {
         tc::mbar_wait(&tfull[buf], buf_phase);
         tc::fence_after();
-        const uint32_t taddr = tmem_base + buf * TBN + ((uint32_t)(q * 32) << 16);
+        const uint32_t taddr = tmem_base + buf * TBN + hc * EPI_COLS + ((uint32_t)(q * 32) << 16);
 #pragma unroll
-        for (int c = 0; c < TBN / 32; ++c) {
-          uint32_t r[32];
-          tc::tmem_ld32(taddr + c * 32, r);
+        for (int c = 0; c < EPI_COLS / 16; ++c) {
+          uint32_t r[16];
+          tc::tmem_ld16(taddr + c * 16, r);
           tc::tmem_wait_ld();
 #pragma unroll
-          for (int j = 0; j < 32; ++j) acc[c * 32 + j] = __fadd_rn(acc[c * 32 + j], __uint_as_float(r[j]));
+          for (int j = 0; j < 16; ++j) acc[c * 16 + j] = __fadd_rn(acc[c * 16 + j], __uint_as_float(r[j]));
         }
         tc::fence_before();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&tempty[buf]);
+        if (lane == 0) tc::mbar_arrive_remote(tempty_leader + buf * 8);
         if (++buf == NPART) { buf = 0; buf_phase ^= 1; }
       }
-      const int m = mb * TBM + q * 32 + lane;
-      const bool row_ok = m < a.M;
-      const float rs = (EPI != EPI_RESID && row_ok && a.rinv) ? a.rinv[m] : 1.f;
 #pragma unroll
-      for (int half = 0; half < TBN / 64; ++half) {
-        const int cb = nb * TBN + half * 64;        // first column of this 64-wide block
-        if (!row_ok || cb >= a.N) continue;
-        float x[64];
+      if (a.no_store) continue;
 #pragma unroll
-        for (int j = 0; j < 64; ++j) x[j] = acc[half * 64 + j];
+      for (int half = 0; half < EPI_COLS / 64; ++half) {
+        const int cb = nb * TBN + hc * EPI_COLS + half * 64;   // first column of this 64-wide block
+        if (cb >= a.N) continue;                              // warp-uniform
+        float *x = acc + half * 64;   // in place: the block's partial sums are dead after it
         if (EPI == EPI_RESID) {
-          float *hp = a.C + (size_t)m * a.ldc + cb;
-          float *hh = a.C_hi + (size_t)m * a.ldc + cb;
-          float *hl = a.C_lo + (size_t)m * a.ldc + cb;
-#pragma unroll
-          for (int j = 0; j < 64; j += 4) {
-            float4 o = *reinterpret_cast<float4 *>(hp + j);
-            o.x = __fadd_rn(o.x, x[j]); o.y = __fadd_rn(o.y, x[j + 1]);
-            o.z = __fadd_rn(o.z, x[j + 2]); o.w = __fadd_rn(o.w, x[j + 3]);
-            *reinterpret_cast<float4 *>(hp + j) = o;
-            float4 h4, l4;
-            tc::split_tf32(o.x, h4.x, l4.x); tc::split_tf32(o.y, h4.y, l4.y);
-            tc::split_tf32(o.z, h4.z, l4.z); tc::split_tf32(o.w, h4.w, l4.w);
-            *reinterpret_cast<float4 *>(hh + j) = h4;
-            *reinterpret_cast<float4 *>(hl + j) = l4;
-          }
+          const size_t o = (size_t)m * a.ldc + cb;
+          float *hp = row_ok ? a.C + o : nullptr;
+          store_rows32<ST_RESID>(stg, x, hp, a.C_hi + o, a.C_lo + o, lane);
+          store_rows32<ST_RESID>(stg, x + 32, hp ? hp + 32 : nullptr, a.C_hi + o + 32, a.C_lo + o + 32, lane);
         } else {
 #pragma unroll
           for (int j = 0; j < 64; ++j) x[j] = __fmul_rn(x[j], rs);
           if (EPI == EPI_HEAD) {
-            float *dst = a.C + (size_t)m * a.ldc + cb;
-#pragma unroll
-            for (int j = 0; j < 64; j += 4)
-              *reinterpret_cast<float4 *>(dst + j) = make_float4(x[j], x[j + 1], x[j + 2], x[j + 3]);
+            float *dst = row_ok ? a.C + (size_t)m * a.ldc + cb : nullptr;
+            store_rows32<ST_PLAIN>(stg, x, dst, nullptr, nullptr, lane);
+            store_rows32<ST_PLAIN>(stg, x + 32, dst ? dst + 32 : nullptr, nullptr, nullptr, lane);
           } else if (EPI == EPI_SWIGLU) {
             // columns [cb, cb+32) are gate rows, [cb+32, cb+64) the matching up rows
-            float *dh = a.C_hi + (size_t)m * a.ldc + cb / 2;
-            float *dl = a.C_lo + (size_t)m * a.ldc + cb / 2;
 #pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              float4 h4, l4;
-              float y[4];
-#pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                const float g = x[j + u], up = x[32 + j + u];
-                const float sg = __fdiv_rn(g, __fadd_rn(1.f, expf(-g)));
-                y[u] = __fmul_rn(sg, up);
-              }
-              tc::split_tf32(y[0], h4.x, l4.x); tc::split_tf32(y[1], h4.y, l4.y);
-              tc::split_tf32(y[2], h4.z, l4.z); tc::split_tf32(y[3], h4.w, l4.w);
-              *reinterpret_cast<float4 *>(dh + j) = h4;
-              *reinterpret_cast<float4 *>(dl + j) = l4;
+            for (int j = 0; j < 32; ++j) {
+              const float g = x[j], up = x[32 + j];
+              const float sg = __fdiv_rn(g, __fadd_rn(1.f, expf(-g)));
+              x[j] = __fmul_rn(sg, up);
             }
+            const size_t o = (size_t)m * a.ldc + cb / 2;
+            store_rows32<ST_SPLIT>(stg, x, row_ok ? a.C_hi + o : nullptr, a.C_lo + o, nullptr, lane);
           } else {  // EPI_QKV
-            const int pos = a.rows.pos[m];
-            if (pos >= 0) {
-              const int nq = a.n_q_cols, nkv = a.n_kv_cols;
-              if (cb < nq + nkv) {   // q or k head: RoPE on the rotate-half pairs (d, d+32)
-                const float *cs = a.rope_cos + (size_t)pos * 32;
-                const float *sn = a.rope_sin + (size_t)pos * 32;
+            const int pos = row_ok ? a.rows.pos[m] : -1;
+            const int nq = a.n_q_cols, nkv = a.n_kv_cols;
+            if (pos >= 0 && cb < nq + nkv) {   // q or k head: RoPE on the rotate-half pairs (d, d+32)
+              const float *cs = a.rope_cos + (size_t)pos * 32;
+              const float *sn = a.rope_sin + (size_t)pos * 32;
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                  const float c = cs[j], s = sn[j], x1 = x[j], x2 = x[j + 32];
-                  x[j] = __fmaf_rn(x1, c, __fmul_rn(-x2, s));
-                  x[j + 32] = __fmaf_rn(x2, c, __fmul_rn(x1, s));
-                }
+              for (int j = 0; j < 32; ++j) {
+                const float c = cs[j], s = sn[j], x1 = x[j], x2 = x[j + 32];
+                x[j] = __fmaf_rn(x1, c, __fmul_rn(-x2, s));
+                x[j + 32] = __fmaf_rn(x2, c, __fmul_rn(x1, s));
               }
-              if (a.planes) {
-                float *dh, *dl;
-                if (cb < nq) {
-                  dh = a.C_hi + (size_t)m * a.ldc + cb;
-                  dl = a.C_lo + (size_t)m * a.ldc + cb;
-                } else {
-                  const int ch = a.rows.chunk[m];
-                  const bool isk = cb < nq + nkv;
-                  const int kvh = (cb - nq - (isk ? 0 : nkv)) / 64;
-                  const size_t o = a.ring.off(ch, a.layer, pos) + kvh * 64;
-                  dh = (isk ? a.ring.k_hi : a.ring.v_hi) + o;
-                  dl = (isk ? a.ring.k_lo : a.ring.v_lo) + o;
-                }
-#pragma unroll
-                for (int j = 0; j < 64; j += 4) {
-                  float4 h4, l4;
-                  tc::split_tf32(x[j], h4.x, l4.x); tc::split_tf32(x[j + 1], h4.y, l4.y);
-                  tc::split_tf32(x[j + 2], h4.z, l4.z); tc::split_tf32(x[j + 3], h4.w, l4.w);
-                  *reinterpret_cast<float4 *>(dh + j) = h4;
-                  *reinterpret_cast<float4 *>(dl + j) = l4;
-                }
-              } else {
-                float *dst;
-                if (cb < nq) {
-                  dst = a.C + (size_t)m * a.ldc + cb;
-                } else {
-                  const int ch = a.rows.chunk[m];
-                  const bool isk = cb < nq + nkv;
-                  const int kvh = (cb - nq - (isk ? 0 : nkv)) / 64;
-                  dst = (isk ? a.ring.k : a.ring.v) + a.ring.off(ch, a.layer, pos) + kvh * 64;
-                }
-#pragma unroll
-                for (int j = 0; j < 64; j += 4)
-                  *reinterpret_cast<float4 *>(dst + j) = make_float4(x[j], x[j + 1], x[j + 2], x[j + 3]);
-              }
+            }
+            size_t o = 0;
+            bool ring = false, isk = false;
+            if (cb < nq) {
+              o = (size_t)m * a.ldc + cb;
+            } else if (pos >= 0) {
+              ring = true;
+              isk = cb < nq + nkv;
+              const int kvh = (cb - nq - (isk ? 0 : nkv)) / 64;
+              o = a.ring.off(a.rows.chunk[m], a.layer, pos) + kvh * 64;
+            }
+            if (a.planes) {
+              float *dh = pos < 0 ? nullptr : (ring ? (isk ? a.ring.k_hi : a.ring.v_hi) : a.C_hi) + o;
+              float *dl = pos < 0 ? nullptr : (ring ? (isk ? a.ring.k_lo : a.ring.v_lo) : a.C_lo) + o;
+              store_rows32<ST_SPLIT>(stg, x, dh, dl, nullptr, lane);
+              store_rows32<ST_SPLIT>(stg, x + 32, dh ? dh + 32 : nullptr, dl ? dl + 32 : nullptr, nullptr, lane);
+            } else {
+              float *dst = pos < 0 ? nullptr : (ring ? (isk ? a.ring.k : a.ring.v) : a.C) + o;
+              store_rows32<ST_PLAIN>(stg, x, dst, nullptr, nullptr, lane);
+              store_rows32<ST_PLAIN>(stg, x + 32, dst ? dst + 32 : nullptr, nullptr, nullptr, lane);
             }
           }
         }
@@ -300,9 +390,9 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
     }
   }
   tc::fence_before();
-  __syncthreads();
+  tc::cluster_sync();          // no CTA leaves while its pair may still signal or read it
   tc::fence_after();
-  if (warp == 2) tc::tmem_dealloc(tmem_base, NPART * TBN);
+  if (warp == W_TMA) tc::tmem_dealloc_pair(tmem_base, NPART * TBN);
   if (threadIdx.x == 0) {            // last CTA out resets the tile counter for the next launch
     __threadfence();
     if (atomicAdd(a.tile_ctr + 1, 1) == (int)gridDim.x - 1) {
@@ -387,12 +477,25 @@ static void launch_tc(const TcGemmArgs &a, const TcOperands &op, cudaStream_t s)
     attr = true;
   }
   const CUtensorMap *ah = tmap_2d(op.A_hi, op.a_rows, a.K, TBM), *al = tmap_2d(op.A_lo, op.a_rows, a.K, TBM);
-  const CUtensorMap *bh = tmap_2d(op.B_hi, a.N, a.K, TBN), *bl = tmap_2d(op.B_lo, a.N, a.K, TBN);
-  const int tiles = ((a.M + TBM - 1) / TBM) * ((a.N + TBN - 1) / TBN);
-  const int grid = std::min(tiles, std::max(1, num_sms() - g_reserved_sms));
+  const CUtensorMap *bh = tmap_2d(op.B_hi, a.N, a.K, TBN / 2), *bl = tmap_2d(op.B_lo, a.N, a.K, TBN / 2);
+  const int tiles = ((a.M + 2 * TBM - 1) / (2 * TBM)) * ((a.N + TBN - 1) / TBN);
+  const int pairs = std::min(tiles, std::max(1, (num_sms() - g_reserved_sms) / 2));
   TcGemmArgs aa = a;
   aa.tile_ctr = tile_counter();
-  gemm_tc_kernel<EPI><<<grid, TC_THREADS, TC_SMEM, s>>>(*ah, *al, *bh, *bl, aa);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(TC_THREADS);
+  cfg.dynamicSmemBytes = TC_SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_tc_kernel<EPI>, *ah, *al, *bh, *bl, aa);
+  if (e != cudaSuccess) throw std::runtime_error(std::string("gemm_tc launch: ") + cudaGetErrorString(e));
 }
 
 void launch_gemm_tc(GemmEpi epi, const TcGemmArgs &a, const TcOperands &op, cudaStream_t s) {
