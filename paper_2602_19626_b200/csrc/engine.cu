@@ -439,11 +439,12 @@ static double ctx_sum(int64_t p0, int64_t p1, int64_t L, int64_t C) {
   return s;
 }
 
-__global__ void slab_rows_kernel(const uint32_t *tokens, const int64_t *tok_off, const uint32_t *ntok, int R, int s,
-                                 int M, uint32_t bos, uint32_t *x, int32_t *chunk, int32_t *pos) {
+// rows of a slab: chunk c's positions [pos0, pos0 + len) are rows c * len + r
+__global__ void slab_rows_kernel(const uint32_t *tokens, const int64_t *tok_off, const uint32_t *ntok, int len,
+                                 int pos0, int M, uint32_t bos, uint32_t *x, int32_t *chunk, int32_t *pos) {
   int m = blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= M) return;
-  int c = m / R, r = m % R, p = s * R + r;
+  int c = m / len, r = m % len, p = pos0 + r;
   bool valid = p < (int)ntok[c];
   x[m] = (!valid || p == 0) ? bos : tokens[tok_off[c] + p - 1];
   chunk[m] = c;
@@ -542,9 +543,35 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
   int per_chunk = std::max(128, (int)(p.max_slab_rows / n_chunks) / 128 * 128);
   int want = (int)((max_n + kPipeSlabs - 1) / kPipeSlabs);
   const int R = std::max(128, std::min<int>(((want + 127) / 128) * 128, per_chunk));
-  const int n_slabs = (int)((max_n + R - 1) / R);
+  // Slab plan: slabs of R positions, optionally ending in a geometric tail of
+  // R/2, R/4, ..., m positions (NC_SLAB_MIN=m; off by default: the small slabs'
+  // forward costs more than the shorter final walk saves, measured on config2).
+  // Every slab but the last is a multiple of 128 positions and starts at one, so
+  // no 128-row attention tile crosses a retained-window step (C | 128 * k).
+  std::vector<int> slab_pos0, slab_len;
+  {
+    const char *ms = std::getenv("NC_SLAB_MIN");
+    const int mn = ms ? std::max(128, std::atoi(ms) / 128 * 128) : (1 << 30);
+    std::vector<int> tail;
+    int tsum = 0;
+    for (int t = R / 2 / 128 * 128; t >= mn && tsum + t < (int)max_n; t = t / 2 / 128 * 128) {
+      tail.push_back(t);
+      tsum += t;
+    }
+    const int nb = ((int)max_n - tsum + R - 1) / R;
+    std::vector<int> lens(nb, R);
+    lens.insert(lens.end(), tail.begin(), tail.end());
+    int pos0 = 0;
+    for (int len : lens) {
+      if (pos0 >= (int)max_n) break;
+      slab_pos0.push_back(pos0);
+      slab_len.push_back(std::min(len, (int)max_n - pos0));
+      pos0 += len;
+    }
+  }
+  const int n_slabs = (int)slab_len.size();
   const int ring_len = (int)p.window + R;
-  const int M = n_chunks * R;
+  const int M = n_chunks * R;   // buffer rows (the largest slab)
   ensure_rope(m, (int)max_n + 1);
 
   Bag bag(s);
@@ -564,14 +591,15 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
     tile_off[sl] = (int)tiles.size();
     w_off[sl] = (int)w_chunk.size();
     const int TR = m->attn_tile_rows();
+    const int len = slab_len[sl], q0 = slab_pos0[sl];
     for (int c = 0; c < n_chunks; ++c) {
-      for (int b0 = 0; b0 < R; b0 += TR) {
-        int p0 = sl * R + b0;
-        int nr = std::min<int>(TR, (int)ntok[c] - p0);
-        if (nr > 0) tiles.push_back(AttnTile{c, p0, nr, c * R + b0});
+      for (int b0 = 0; b0 < len; b0 += TR) {
+        int p0 = q0 + b0;
+        int nr = std::min<int>(std::min(TR, len - b0), (int)ntok[c] - p0);
+        if (nr > 0) tiles.push_back(AttnTile{c, p0, nr, c * len + b0});
       }
-      int cnt = std::min<int>(R, (int)ntok[c] - sl * R);
-      if (cnt > 0) { w_chunk.push_back(c); w_row0.push_back(c * R); w_count.push_back(cnt); }
+      int cnt = std::min<int>(len, (int)ntok[c] - q0);
+      if (cnt > 0) { w_chunk.push_back(c); w_row0.push_back(c * len); w_count.push_back(cnt); }
     }
   }
   tile_off[n_slabs] = (int)tiles.size();
@@ -616,16 +644,17 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
     if (sl >= 2) NC_CUDA(cudaStreamWaitEvent(s, ev[4 * (sl - 2) + 3], 0));   // logits buffer free again
     fw.logits = fw.lbuf[sl & 1];
     NC_CUDA(cudaEventRecord(ev[4 * sl], s));
-    PROF(K_MISC, 0, (slab_rows_kernel<<<(M + 255) / 256, 256, 0, s>>>(tokens_dev, tok_off_d, ntok_d, R, sl, M, S.bos,
-                                                                      xs, rchunk, rpos)));
+    const int len = slab_len[sl], q0 = slab_pos0[sl], Ms = n_chunks * len;
+    PROF(K_MISC, 0, (slab_rows_kernel<<<(Ms + 255) / 256, 256, 0, s>>>(tokens_dev, tok_off_d, ntok_d, len, q0, Ms,
+                                                                       S.bos, xs, rchunk, rpos)));
     st.launches++;
     RowMeta rows{xs, rchunk, rpos};
     double valid = 0, ctx = 0;
     for (int c = 0; c < n_chunks; ++c) {
-      int64_t a0 = (int64_t)sl * R, a1 = std::min<int64_t>((int64_t)(sl + 1) * R, ntok[c]);
+      int64_t a0 = q0, a1 = std::min<int64_t>((int64_t)q0 + len, ntok[c]);
       if (a1 > a0) { valid += (double)(a1 - a0); ctx += ctx_sum(a0, a1, p.window, p.slide); }
     }
-    fw.run(M, valid, 4.0 * S.H * S.dh * ctx, rows, tiles_d + tile_off[sl], tile_off[sl + 1] - tile_off[sl], p,
+    fw.run(Ms, valid, 4.0 * S.H * S.dh * ctx, rows, tiles_d + tile_off[sl], tile_off[sl + 1] - tile_off[sl], p,
            nullptr);
     NC_CUDA(cudaEventRecord(ev[4 * sl + 1], s));
     NC_CUDA(cudaStreamWaitEvent(ws, ev[4 * sl + 1], 0));
@@ -651,6 +680,7 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
   NC_CUDA(cudaMemcpyAsync(hs.data(), wb.st, n_chunks * sizeof(WalkState), cudaMemcpyDeviceToHost, s));
   NC_CUDA(cudaStreamSynchronize(s));
   if (prof().on) prof().collect();
+  if (std::getenv("NC_WALK_REPORT")) walk_timing_report();
   for (int c = 0; c < n_chunks; ++c) out.err[c] = hs[c].err;
   for (int sl = 0; sl < n_slabs; ++sl) {
     float a = 0, b = 0;
@@ -824,7 +854,7 @@ void debug_forward(nc_model *m, const uint32_t *x, uint32_t rows, const Params &
         if (nr > 0) tiles.push_back(AttnTile{0, p0, nr, b0});
       }
       AttnTile *td = bag.upload(tiles);
-      slab_rows_kernel<<<(Rr + 255) / 256, 256, 0, s>>>(t_d, off_d, nt_d, Rr, sl, Rr, x[0], xs, rc, rp);
+      slab_rows_kernel<<<(Rr + 255) / 256, 256, 0, s>>>(t_d, off_d, nt_d, Rr, sl * Rr, Rr, x[0], xs, rc, rp);
       RowMeta rm{xs, rc, rp};
       fw.run(Rr, 0, 0, rm, td, (int)tiles.size(), p, nullptr);
       int cnt = std::min<int>(Rr, (int)rows - sl * Rr);

@@ -26,6 +26,7 @@
 // arithmetic; every float op is an explicit round-to-nearest intrinsic and
 // every reduction has a fixed tree, so the decoder reproduces the encoder's
 // counts bit for bit (D15).
+#include <cstdio>
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
@@ -322,6 +323,21 @@ __device__ __forceinline__ uint32_t cl_ld(const void *local_smem, uint32_t rank)
   return v;
 }
 
+#ifdef NC_WALK_TIMING
+// diagnostics build only: encode-loop phase cycle sums (thread 0 of rank-0 CTAs)
+__device__ unsigned long long g_walk_clk[8];
+#define WALK_MARK(k)                                                                            \
+  do {                                                                                          \
+    if (tid == 0 && rank == 0) {                                                                \
+      const long long _n = clock64();                                                           \
+      atomicAdd(&g_walk_clk[k], (unsigned long long)(_n - _wt));                                \
+      _wt = _n;                                                                                 \
+    }                                                                                           \
+  } while (0)
+#else
+#define WALK_MARK(k) do {} while (0)
+#endif
+
 template <int CS>
 __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
   extern __shared__ __align__(16) uint8_t dsm[];
@@ -518,6 +534,10 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
       __syncthreads();
     }
     for (int it = 0; it < count; ++it) {
+#ifdef NC_WALK_TIMING
+      long long _wt = clock64();
+      if (tid == 0 && rank == 0) atomicAdd(&g_walk_clk[7], 1ull);
+#endif
       const float *z = a.logits + (size_t)(row0 + it) * a.ldl;
       const bool has_next = it + 1 < count;
       const float *zn = a.logits + (size_t)(row0 + it + 1) * a.ldl;
@@ -571,6 +591,7 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
           for (int j = 0; j < 4; ++j) ms_push(tm, ts, u[j]);
         }
       }
+      WALK_MARK(0);
       if (wid == 1 && pre_next) prefetch_wait();
       unsigned long long c1 = 0, c2 = 0;
       Best cb{};
@@ -582,7 +603,9 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
         x.has_tok = (ltok >= 0 && ltok < (int)Vc) ? 1 : 0;
       }
       __syncthreads();
+      WALK_MARK(1);
       if (CS > 1) cl_sync();
+      WALK_MARK(2);
       if (wid == 0) {
         gather(par);
         if (lane == 0) {
@@ -616,7 +639,9 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
         __syncwarp();
         if (has_next) scatter_list(i + 1);
       }
+      WALK_MARK(3);
       __syncthreads();
+      WALK_MARK(4);
     }
     if (tid == 0) s_i = i0 + count;
   } else {
@@ -893,6 +918,21 @@ static void launch_walk_cs(const WalkArgs &a, cudaStream_t s) {
 }
 
 int walk_ctas_per_chunk(uint32_t V) { return walk_cluster_size(V); }
+
+void walk_timing_report() {
+#ifdef NC_WALK_TIMING
+  unsigned long long h[8];
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(h, g_walk_clk, sizeof(h));
+  const double n = (double)(h[7] ? h[7] : 1);
+  fprintf(stderr,
+          "walk encode per token (cycles): fused pass %.0f | CTA reductions %.0f | cluster barrier %.0f | "
+          "combine+mixer+lists %.0f | final sync %.0f | tokens %.0f\n",
+          h[0] / n, h[1] / n, h[2] / n, h[3] / n, h[4] / n, n);
+  unsigned long long z[8] = {};
+  cudaMemcpyToSymbol(g_walk_clk, z, sizeof(z));
+#endif
+}
 
 void launch_walk(const WalkArgs &a, cudaStream_t s) {
   if (a.n_entries <= 0) return;

@@ -67,6 +67,7 @@ struct WalkArgs {
 
 void launch_walk(const WalkArgs &a, cudaStream_t s);
 int walk_ctas_per_chunk(uint32_t V);   // CTAs (one cluster) per chunk in the walk
+void walk_timing_report();            // diagnostics build (-DNC_WALK_TIMING): phase cycles -> stderr
 // encode only: N-gram predictions for the entries' tokens (one warp per chunk)
 void launch_ngram_precompute(const WalkArgs &a, cudaStream_t s);
 void launch_walk_init(WalkState *st, int n_chunks, cudaStream_t s);
