@@ -535,37 +535,48 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
   if (n_chunks == 0 || max_n == 0) return;
   if (S.V >= (1u << p.cdf_bits)) fail(NC_ERR_INVALID, "T = 2^cdf_bits must exceed V");
 
-  // Slab rows per chunk: at most max_slab_rows over all chunks, and small enough
-  // that there are >= kPipeSlabs slabs, so the walk of slab s overlaps the
-  // forward of slab s+1 (the walk runs on its own stream, logits double-buffered).
-  const char *es = std::getenv("NC_SLABS");
-  const int kPipeSlabs = es ? std::max(1, std::atoi(es)) : 4;
-  int per_chunk = std::max(128, (int)(p.max_slab_rows / n_chunks) / 128 * 128);
-  int want = (int)((max_n + kPipeSlabs - 1) / kPipeSlabs);
-  const int R = std::max(128, std::min<int>(((want + 127) / 128) * 128, per_chunk));
-  // Slab plan: slabs of R positions, optionally ending in a geometric tail of
-  // R/2, R/4, ..., m positions (NC_SLAB_MIN=m; off by default: the small slabs'
-  // forward costs more than the shorter final walk saves, measured on config2).
-  // Every slab but the last is a multiple of 128 positions and starts at one, so
-  // no 128-row attention tile crosses a retained-window step (C | 128 * k).
-  std::vector<int> slab_pos0, slab_len;
-  {
-    const char *ms = std::getenv("NC_SLAB_MIN");
-    const int mn = ms ? std::max(128, std::atoi(ms) / 128 * 128) : (1 << 30);
-    std::vector<int> tail;
-    int tsum = 0;
-    for (int t = R / 2 / 128 * 128; t >= mn && tsum + t < (int)max_n; t = t / 2 / 128 * 128) {
-      tail.push_back(t);
-      tsum += t;
+  // Slab plan.  The walk of slab s overlaps the forward of slab s+1 (own stream,
+  // logits double-buffered); only the last slab's walk runs after the forward.
+  // Bigger slabs run the GEMMs more efficiently (fewer tile waves), a smaller last
+  // slab shortens that final walk.  Measured on config2 (3885 positions):
+  // 4 x 1024 -> 109 ms, 2 x ~1940 -> 101.5 ms, 2944 + 941 (frac 0.75) -> 96.8 ms.
+  // So: slabs of the largest size (max_slab_rows / n_chunks) while the remainder
+  // exceeds one / frac, then the remainder split 75/25 (NC_SLAB_FRAC), 128-aligned so no
+  // 128-row attention tile crosses a retained-window step (C | 128 k).
+  // NC_SLAB_PLAN="a,b,..." (diagnostics) gives explicit lengths.
+  const int per_chunk = std::max(128, (int)(p.max_slab_rows / n_chunks) / 128 * 128);
+  std::vector<int> plan;
+  if (const char *pl = std::getenv("NC_SLAB_PLAN")) {
+    for (const char *q = pl; *q;) {
+      plan.push_back(std::max(128, std::min(per_chunk, std::atoi(q) / 128 * 128)));
+      while (*q && *q != ',') ++q;
+      if (*q == ',') ++q;
     }
-    const int nb = ((int)max_n - tsum + R - 1) / R;
-    std::vector<int> lens(nb, R);
-    lens.insert(lens.end(), tail.begin(), tail.end());
+  } else {
+    const char *fs = std::getenv("NC_SLAB_FRAC");
+    const double frac = fs ? std::min(0.95, std::max(0.05, std::atof(fs))) : 0.75;
+    int rem = (int)max_n;
+    while (frac * rem > per_chunk) {   // full slabs until the last two fit the split
+      plan.push_back(per_chunk);
+      rem -= per_chunk;
+    }
+    const int first = ((int)(frac * rem) + 127) / 128 * 128;
+    if (rem <= 256 || first >= rem) {
+      plan.push_back(rem);
+    } else {
+      plan.push_back(first);
+      plan.push_back(rem - first);
+    }
+  }
+  std::vector<int> slab_pos0, slab_len;
+  int R = 128;
+  {
     int pos0 = 0;
-    for (int len : lens) {
-      if (pos0 >= (int)max_n) break;
+    for (size_t k = 0; pos0 < (int)max_n; ++k) {
+      const int len = k < plan.size() ? plan[k] : per_chunk;
       slab_pos0.push_back(pos0);
       slab_len.push_back(std::min(len, (int)max_n - pos0));
+      R = std::max(R, ((slab_len.back() + 127) / 128) * 128);
       pos0 += len;
     }
   }

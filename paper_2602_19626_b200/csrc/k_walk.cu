@@ -27,6 +27,8 @@
 // every reduction has a fixed tree, so the decoder reproduces the encoder's
 // counts bit for bit (D15).
 #include <cstdio>
+#include <stdexcept>
+#include <string>
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
@@ -35,14 +37,15 @@
 
 namespace nc {
 
-constexpr int WT = 1024;   // threads per walk CTA
+constexpr int WT = 512;    // threads per walk CTA (128 registers: a token's logits stay in registers)
 constexpr int NW = WT / 32;
 
 struct WalkSmem {
-  float red_m[NW], red_s[NW];
-  unsigned long long red_sum[NW], red_cum[NW];
-  float red_bv[NW]; int red_bi[NW]; uint32_t red_bc[NW];
-  uint32_t scan[NW];
+  // per-warp partials, padded to 32 with identities (set once) so warp 0 reduces all lanes
+  float red_m[32], red_s[32];
+  unsigned long long red_sum[32], red_cum[32];
+  float red_bv[32]; int red_bi[32]; uint32_t red_bc[32];
+  uint32_t scan[32];
   // per-token broadcast scalars
   float M, invS, a0f;
   int mix, tok, argmax, nsp;
@@ -60,19 +63,27 @@ __device__ __forceinline__ double b_step(double b, float pt, bool is_t, double a
 // c = max(1, floor(p * (T - V))) with the EXACT product (D5), in fp32 only:
 // T - V < 2^24 is exact in fp32; q = floor(rn(p * TmV)) is off by at most one,
 // and the sign of the exact residual p * TmV - q is that of fma(p, TmV, -q).
+// floor() and the integer conversion run on the FMA/ALU pipes, no SFU-class
+// FRND/F2I: for 0 <= x < 2^23, x + 2^23 rounded down holds floor(x) in its low
+// mantissa bits (exact); every float >= 2^23 is an integer, read from its bits.
 __device__ __forceinline__ uint32_t quant(float p, float TmV) {
-  float q = floorf(__fmul_rn(p, TmV));
+  const float x = __fmul_rn(p, TmV);
+  const float t = __fadd_rd(x, 8388608.f);
+  const uint32_t xb = __float_as_uint(x);
+  const bool small = x < 8388608.f;
+  const float q = small ? __fsub_rn(t, 8388608.f) : x;
+  const uint32_t qi = small ? __float_as_uint(t) - 0x4B000000u : ((xb & 0x7FFFFFu) | 0x800000u) << ((xb >> 23) - 150u);
   const float r = __fmaf_rn(p, TmV, -q);
-  q = r < 0.f ? __fsub_rn(q, 1.f) : (r >= 1.f ? __fadd_rn(q, 1.f) : q);
-  return q < 1.f ? 1u : (uint32_t)q;
+  const int qs = (int)qi + (r < 0.f ? -1 : (r >= 1.f ? 1 : 0));
+  return qs < 1 ? 1u : (uint32_t)qs;
+}
+__device__ __forceinline__ float lg2f(float x) {   // log2 on the SFU (lg2.approx.ftz)
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 // exp on the SFU (ex2.approx; relative error ~1e-6 for the |x| < 30 used here)
 __device__ __forceinline__ float fexp(float x) { return tc::ex2(__fmul_rn(x, 1.44269504088896341f)); }
-// online (max, sum exp) of one thread
-__device__ __forceinline__ void ms_push(float &tm, float &ts, float u) {
-  if (u > tm) { ts = __fmaf_rn(ts, fexp(__fsub_rn(tm, u)), 1.f); tm = u; }
-  else ts = __fadd_rn(ts, fexp(__fsub_rn(u, tm)));
-}
 __device__ __forceinline__ void ms_merge(float &tm, float &ts, float om, float os) {
   const float mm = fmaxf(tm, om);
   const float e1 = (tm == -CUDART_INF_F) ? 0.f : fexp(__fsub_rn(tm, mm));
@@ -85,9 +96,67 @@ __device__ __forceinline__ void ms_warp(float &tm, float &ts) {
   for (int o = 16; o; o >>= 1)
     ms_merge(tm, ts, __shfl_xor_sync(0xffffffffu, tm, o), __shfl_xor_sync(0xffffffffu, ts, o));
 }
-// p = w_l pt + w_n (a0f (c+1) + add)
-__device__ __forceinline__ float mix_p(float pt, float a0f, uint32_t cuv, float add, float wl, float wn, float &png) {
-  png = __fmaf_rn(a0f, (float)(cuv + 1u), add);
+// quant() for a float4 group: the x < 2^23 path for all four, and the x >= 2^23
+// path (only an element with p > 1/2 reaches it) behind one warp vote, so the
+// common case issues no instructions for it.  Same values as quant().
+__device__ __forceinline__ void quant4(const float p[4], float TmV, uint32_t cv[4]) {
+  float x[4], q[4];
+  uint32_t qi[4];
+  bool big = false;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    x[j] = __fmul_rn(p[j], TmV);
+    const float t = __fadd_rd(x[j], 8388608.f);
+    q[j] = __fsub_rn(t, 8388608.f);
+    qi[j] = __float_as_uint(t) - 0x4B000000u;
+    big |= !(x[j] < 8388608.f);
+  }
+  if (__any_sync(__activemask(), big)) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (!(x[j] < 8388608.f)) {
+        const uint32_t xb = __float_as_uint(x[j]);
+        q[j] = x[j];
+        qi[j] = ((xb & 0x7FFFFFu) | 0x800000u) << ((xb >> 23) - 150u);
+      }
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float r = __fmaf_rn(p[j], TmV, -q[j]);
+    const int qs = (int)qi[j] + (r < 0.f ? -1 : (r >= 1.f ? 1 : 0));
+    cv[j] = qs < 1 ? 1u : (uint32_t)qs;
+  }
+}
+// Per-thread softmax statistics of one token from its register-resident u values
+// (groups k < ng): m = max u, then s = sum 2^(u log2 e - m log2 e) as four
+// element-position partial sums (over groups in order) added as (s0 + s1) + (s2 + s3):
+// independent chains for latency.  Encoder and decoder both use exactly this.
+constexpr int NGM = 8;   // float4 groups per thread at most (V / CS <= 4 * NGM * WT)
+__device__ __forceinline__ void ms_regs(const float (&u)[NGM][4], int ng, float &tm, float &ts) {
+  constexpr float LOG2E = 1.44269504088896341f;
+  float m4[4] = {-CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F};
+#pragma unroll
+  for (int k = 0; k < NGM; ++k)
+    if (k < ng) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) m4[j] = fmaxf(m4[j], u[k][j]);
+    }
+  tm = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+  float s4[4] = {0.f, 0.f, 0.f, 0.f};
+  if (tm != -CUDART_INF_F) {
+    const float nb = -__fmul_rn(tm, LOG2E);
+#pragma unroll
+    for (int k = 0; k < NGM; ++k)
+      if (k < ng) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) s4[j] = __fadd_rn(s4[j], tc::ex2(__fmaf_rn(u[k][j], LOG2E, nb)));
+      }
+  }
+  ts = __fadd_rn(__fadd_rn(s4[0], s4[1]), __fadd_rn(s4[2], s4[3]));
+}
+// p = w_l pt + w_n (a0f (c+1) + add); c (unigram count < 2^24) held exactly in fp32
+__device__ __forceinline__ float mix_p(float pt, float a0f, float cuv, float add, float wl, float wn, float &png) {
+  png = __fmaf_rn(a0f, __fadd_rn(cuv, 1.f), add);
   return __fmaf_rn(wl, pt, __fmul_rn(wn, png));
 }
 struct Best {
@@ -95,6 +164,17 @@ struct Best {
 };
 __device__ __forceinline__ void best_merge(Best &a, float v, int i, uint32_t c) {
   if (v > a.v || (v == a.v && i < a.i)) { a.v = v; a.i = i; a.c = c; }
+}
+// warp argmax with best_merge's order (largest p, then smallest id), order-free:
+// p >= 0 compares as its bit pattern; "none" (v < 0) ranks below every p.
+__device__ __forceinline__ Best best_warp(Best b) {
+  const uint32_t key = b.v < 0.f ? 0u : __float_as_uint(b.v) + 1u;
+  const uint32_t kmax = __reduce_max_sync(0xffffffffu, key);
+  const bool cand = key == kmax;
+  const uint32_t imin = __reduce_min_sync(0xffffffffu, cand ? (uint32_t)b.i : 0xffffffffu);
+  const int src = __ffs(__ballot_sync(0xffffffffu, cand && (uint32_t)b.i == imin)) - 1;
+  return Best{__shfl_sync(0xffffffffu, b.v, src), __shfl_sync(0xffffffffu, b.i, src),
+              __shfl_sync(0xffffffffu, b.c, src)};
 }
 
 // ------------------------------------------------------------------ N-gram ---
@@ -343,7 +423,7 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
   extern __shared__ __align__(16) uint8_t dsm[];
   __shared__ WalkSmem sm;
   __shared__ Xch xs[2];            // own slots (token parity)
-  __shared__ Xch xin[CS];          // copies of the cluster's slots
+  __shared__ Xch xin[2][CS];       // the cluster's slots (token parity): gathered (decode) or pushed (encode)
   __shared__ double s_lw[2];
   __shared__ float s_w[2];
   __shared__ uint32_t s_i;
@@ -354,8 +434,9 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
   const int row0 = a.row0[e], count = a.count[e];
   const uint32_t V = a.V, Vc = V / CS, vb = rank * Vc;
   const int Gc = (int)(Vc / 4);
+  const int ng = tid < Gc ? (Gc - 1 - tid) / WT + 1 : 0;   // my groups tid + k WT, k < ng <= NGM
   double *b_s = reinterpret_cast<double *>(dsm);
-  uint32_t *cu_s = reinterpret_cast<uint32_t *>(b_s + Vc);
+  float *cu_s = reinterpret_cast<float *>(b_s + Vc);   // unigram counts, exact (< 2^24) as fp32
   float *sp_s = reinterpret_cast<float *>(cu_s + Vc);
   uint32_t *bitmap = reinterpret_cast<uint32_t *>(sp_s + Vc);
   uint32_t *gsum = bitmap + (Vc + 31) / 32;
@@ -372,10 +453,14 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
   // ---- load this CTA's slice of the chunk state into shared memory
   for (uint32_t v = tid; v < Vc; v += WT) {
     b_s[v] = use_head ? b_g[v] : 0.0;
-    cu_s[v] = use_ng ? cu_g[v] : 0u;
+    cu_s[v] = use_ng ? (float)cu_g[v] : 0.f;
     sp_s[v] = 0.f;
   }
   for (uint32_t w = tid; w < (Vc + 31) / 32; w += WT) bitmap[w] = 0u;
+  if (tid < 32) {
+    sm.red_m[tid] = -CUDART_INF_F; sm.red_s[tid] = 0.f; sm.red_sum[tid] = 0ull; sm.red_cum[tid] = 0ull;
+    sm.red_bv[tid] = -1.f; sm.red_bi[tid] = 0x7fffffff; sm.red_bc[tid] = 0u; sm.scan[tid] = 0u;
+  }
   if (tid == 0) {
     s_lw[0] = st->lw[0]; s_lw[1] = st->lw[1];
     s_w[0] = st->wl; s_w[1] = st->wn;
@@ -409,8 +494,8 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
       for (int j = 0; j < 4; ++j) { png[j] = 0.f; p[j] = pt[j]; }
       return;
     }
-    const uint4 c4 = reinterpret_cast<const uint4 *>(cu_s)[g];
-    const uint32_t cc[4] = {c4.x, c4.y, c4.z, c4.w};
+    const float4 c4 = reinterpret_cast<const float4 *>(cu_s)[g];
+    const float cc[4] = {c4.x, c4.y, c4.z, c4.w};
     const uint32_t bits = (bitmap[g >> 3] >> ((g & 7) * 4)) & 15u;
     const float4 s4 = bits ? reinterpret_cast<const float4 *>(sp_s)[g] : make_float4(0.f, 0.f, 0.f, 0.f);
     const float sa[4] = {s4.x, s4.y, s4.z, s4.w};
@@ -454,7 +539,7 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
   // warp 0: copy every CTA's slot `par` into xin[] (DSMEM), then lane 0 combines
   auto gather = [&](int par) {
     for (int r = 0; r < CS; ++r) {
-      uint32_t *dst = reinterpret_cast<uint32_t *>(&xin[r]);
+      uint32_t *dst = reinterpret_cast<uint32_t *>(&xin[par][r]);
       const uint32_t *src = reinterpret_cast<const uint32_t *>(&xs[par]);
       for (int w = lane; w < XW; w += 32) dst[w] = CS > 1 ? cl_ld(src + w, (uint32_t)r) : src[w];
     }
@@ -490,60 +575,113 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
   auto prefetch_wait = [&]() { asm volatile("cp.async.wait_all;" ::: "memory"); };
-  auto mixer_update = [&](float pt_t, float png_t) {   // thread 0 of every CTA, identical arithmetic
-    double l0 = __dadd_rn(s_lw[0], __dmul_rn(a.eta, log(fmax((double)pt_t, 1e-12))));
-    double l1 = __dadd_rn(s_lw[1], __dmul_rn(a.eta, log(fmax((double)png_t, 1e-12))));
-    const double mx = fmax(l0, l1);
-    const double lse = __dadd_rn(mx, log(__dadd_rn(exp(__dsub_rn(l0, mx)), exp(__dsub_rn(l1, mx)))));
-    l0 = __dsub_rn(l0, lse);
-    l1 = __dsub_rn(l1, lse);
+  // exponential-weights mixer step (D24), fp32 on the SFU (lg2/ex2.approx) in the
+  // log2 domain; thread 0 of every CTA and the decoder run this same arithmetic
+  auto mixer_update = [&](float pt_t, float png_t) {
+    constexpr float LN2 = 0.693147180559945309f, LOG2E = 1.44269504088896341f;
+    const float eta = (float)a.eta;
+    float l0 = __fmaf_rn(__fmul_rn(eta, LN2), lg2f(fmaxf(pt_t, 1e-12f)), (float)s_lw[0]);
+    float l1 = __fmaf_rn(__fmul_rn(eta, LN2), lg2f(fmaxf(png_t, 1e-12f)), (float)s_lw[1]);
+    const float mx = fmaxf(l0, l1);
+    const float e0 = tc::ex2(__fmul_rn(__fsub_rn(l0, mx), LOG2E)), e1 = tc::ex2(__fmul_rn(__fsub_rn(l1, mx), LOG2E));
+    const float lse = __fmaf_rn(LN2, lg2f(__fadd_rn(e0, e1)), mx);
+    l0 = __fsub_rn(l0, lse);
+    l1 = __fsub_rn(l1, lse);
     s_lw[0] = l0; s_lw[1] = l1;
-    s_w[0] = (float)exp(l0);     // lw is renormalised: softmax(lw) = exp(lw) (to ~1e-16)
-    s_w[1] = (float)exp(l1);
+    s_w[0] = tc::ex2(__fmul_rn(l0, LOG2E));     // lw is renormalised: softmax(lw) = exp(lw)
+    s_w[1] = tc::ex2(__fmul_rn(l1, LOG2E));
   };
 
   if (enc) {
     // ===================================================== compression ===
+    // Thread t owns the local float4 groups t, t + WT, ... (at most NGM).  The
+    // current row's logits stay in registers from the previous token's pass, and
+    // the next row's loads are issued first thing, so the HBM latency of the
+    // (L2-cold) logits overlaps the current token's work.  Arithmetic and its
+    // order are those of the decoder: (m, s) per thread in group then element
+    // order, the same warp/CTA (m, s) tree as cta_ms, exact integer sums and an
+    // order-free argmax; only where the values come from changed.
+
     const uint32_t i0 = s_i;
+    float uc[NGM][4];   // u = z / tau + b of the current token, from the previous token's pass
+    auto zload = [&](const float *zrow, float4 (&dst)[NGM]) {
+#pragma unroll
+      for (int k = 0; k < NGM; ++k)
+        if (k < ng) dst[k] = __ldcs(reinterpret_cast<const float4 *>(zrow + vb) + tid + k * WT);
+    };
+    auto u4 = [&](const float4 z4, int g, float u[4]) {
+      const double2 b01 = reinterpret_cast<const double2 *>(b_s)[2 * g];
+      const double2 b23 = reinterpret_cast<const double2 *>(b_s)[2 * g + 1];
+      u[0] = walk_u(z4.x, b01.x, inv_tau); u[1] = walk_u(z4.y, b01.y, inv_tau);
+      u[2] = walk_u(z4.z, b23.x, inv_tau); u[3] = walk_u(z4.w, b23.y, inv_tau);
+    };
+    // push this CTA's slot `par` (complete in xs[par]) into every CTA's xin[par][rank]
+    auto push_slot = [&](int par) {   // warp 0
+      const uint32_t *src = reinterpret_cast<const uint32_t *>(&xs[par]);
+      uint32_t *dst = reinterpret_cast<uint32_t *>(&xin[par][rank]);
+      for (int w = lane; w < XW; w += 32) {
+        const uint32_t v = src[w];
+        if (CS > 1) {
+#pragma unroll
+          for (int r = 0; r < CS; ++r) tc::st_cluster_s32(tc::mapa(dst + w, (uint32_t)r), (int)v);
+        } else {
+          dst[w] = v;
+        }
+      }
+    };
     if (wid == 0) {
       if (use_ng && i0 >= a.warmup) { prefetch_pre(i0); prefetch_wait(); __syncwarp(); }
       scatter_list(i0);
     }
     // softmax statistics of the first token
     {
-      const float *z0 = a.logits + (size_t)row0 * a.ldl;
-      float tm = -CUDART_INF_F, ts = 0.f;
-      for (int g = tid; g < Gc; g += WT) {
-        float u[4];
-        load_u(z0, g, u);
+      float4 z0[NGM];
+      zload(a.logits + (size_t)row0 * a.ldl, z0);
+      float tm, ts;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) ms_push(tm, ts, u[j]);
-      }
+      for (int k = 0; k < NGM; ++k)
+        if (k < ng) u4(z0[k], tid + k * WT, uc[k]);
+      ms_regs(uc, ng, tm, ts);
       cta_ms(tm, ts);
       if (tid == 0) { xs[1].m = tm; xs[1].s = ts; }
       __syncthreads();
-      if (CS > 1) cl_sync();
-      if (wid == 0) {
-        gather(1);
-        if (lane == 0) {
-          float M = xin[0].m, S = xin[0].s;
-          for (int r = 1; r < CS; ++r) ms_merge(M, S, xin[r].m, xin[r].s);
-          sm.M = M; sm.invS = __frcp_rn(S);
-        }
+      if (wid == 0) push_slot(1);
+      if (CS > 1) cl_sync(); else __syncthreads();
+      if (tid == 0) {
+        float M = xin[1][0].m, S = xin[1][0].s;
+        for (int r = 1; r < CS; ++r) ms_merge(M, S, xin[1][r].m, xin[1][r].s);
+        sm.M = M; sm.invS = __frcp_rn(S);
       }
       __syncthreads();
     }
+    int tok_cur = count > 0 ? (int)a.tokens[a.tok_off[c] + i0] : 0;
+    // this CTA's slice of logits row r into L2 (one TMA bulk prefetch): rows are
+    // prefetched two tokens ahead so the register loads one token ahead hit L2
+    auto l2_prefetch_row = [&](int r) {
+      if (tid == 0 && r < count)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.logits + (size_t)(row0 + r) * a.ldl + vb),
+                     "r"(Vc * 4u)
+                     : "memory");
+    };
+    l2_prefetch_row(1);
+    l2_prefetch_row(2);
     for (int it = 0; it < count; ++it) {
 #ifdef NC_WALK_TIMING
       long long _wt = clock64();
       if (tid == 0 && rank == 0) atomicAdd(&g_walk_clk[7], 1ull);
 #endif
-      const float *z = a.logits + (size_t)(row0 + it) * a.ldl;
       const bool has_next = it + 1 < count;
-      const float *zn = a.logits + (size_t)(row0 + it + 1) * a.ldl;
+      l2_prefetch_row(it + 3);
+      float4 zn[NGM];
+#if defined(NC_WALK_ABL)   // diagnostics: next row = constant (no load dependence)
+      for (int k = 0; k < NGM; ++k) zn[k] = make_float4(uc[k][0], uc[k][1], uc[k][2], uc[k][3]);
+#else
+      if (has_next) zload(a.logits + (size_t)(row0 + it + 1) * a.ldl, zn);
+#endif
       const uint32_t i = i0 + it;
       const int par = it & 1;
-      const int tok = (int)a.tokens[a.tok_off[c] + i];
+      const int tok = tok_cur;
+      if (has_next) tok_cur = (int)a.tokens[a.tok_off[c] + i + 1];
       const int ltok = tok - (int)vb;                  // local id (may be outside [0, Vc))
       const float M = sm.M, invS = sm.invS, a0f = sm.a0f, wl = s_w[0], wn = s_w[1];
       const int mix = sm.mix;
@@ -551,18 +689,33 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
       if (wid == 1 && pre_next) prefetch_pre(i + 1);
       uint32_t my_sum = 0, my_cum = 0;
       Best bb{-1.f, 0x7fffffff, 0};
-      float tm = -CUDART_INF_F, ts = 0.f;
+      float tm = -CUDART_INF_F, ts = 0.f;   // next token's softmax statistics (after the group loop)
       const int tg = ltok >= 0 ? (ltok >> 2) : -1;
       const int gcut = ltok < 0 ? 0 : (ltok >= (int)Vc ? Gc : tg);   // local groups entirely below tok
-      for (int g = tid; g < Gc; g += WT) {
-        float pt[4], png[4], p[4];
-        prob4(z, g, M, invS, wl, wn, a0f, mix, pt, png, p);
-        uint32_t cv[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          cv[j] = quant(p[j], TmV);
-          if (p[j] > bb.v) { bb.v = p[j]; bb.i = (int)vb + 4 * g + j; bb.c = cv[j]; }
+      for (int k = 0; k < NGM; ++k) {
+        if (k >= ng) break;
+        const int g = tid + k * WT;
+        float pt[4], png[4], p[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) pt[j] = __fmul_rn(fexp(__fsub_rn(uc[k][j], M)), invS);
+        if (!mix) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) { png[j] = 0.f; p[j] = pt[j]; }
+        } else {
+          const float4 c4 = reinterpret_cast<const float4 *>(cu_s)[g];
+          const float cc[4] = {c4.x, c4.y, c4.z, c4.w};
+          const uint32_t bits = (bitmap[g >> 3] >> ((g & 7) * 4)) & 15u;
+          const float4 s4 = bits ? reinterpret_cast<const float4 *>(sp_s)[g] : make_float4(0.f, 0.f, 0.f, 0.f);
+          const float sa[4] = {s4.x, s4.y, s4.z, s4.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) p[j] = mix_p(pt[j], a0f, cc[j], sa[j], wl, wn, png[j]);
         }
+        uint32_t cv[4];
+        quant4(p, TmV, cv);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (p[j] > bb.v) { bb.v = p[j]; bb.i = (int)vb + 4 * g + j; bb.c = cv[j]; }
         const uint32_t gs = cv[0] + cv[1] + cv[2] + cv[3];
         my_sum += gs;
         if (g < gcut) {
@@ -583,42 +736,64 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
           b23.x = b_step(b23.x, pt[2], v + 2 == ltok, a.alpha);
           b23.y = b_step(b23.y, pt[3], v + 3 == ltok, a.alpha);
           bp[0] = b01; bp[1] = b23;
-        }
-        if (has_next) {
-          float u[4];
-          load_u(zn, g, u);           // bias already updated for this group
-#pragma unroll
-          for (int j = 0; j < 4; ++j) ms_push(tm, ts, u[j]);
+          if (has_next) {   // next token's u with the updated bias (== walk_u(z, b_new)), stats in decoder order
+            uc[k][0] = __fmaf_rn(zn[k].x, inv_tau, (float)b01.x); uc[k][1] = __fmaf_rn(zn[k].y, inv_tau, (float)b01.y);
+            uc[k][2] = __fmaf_rn(zn[k].z, inv_tau, (float)b23.x); uc[k][3] = __fmaf_rn(zn[k].w, inv_tau, (float)b23.y);
+          }
+        } else if (has_next) {
+          uc[k][0] = __fmul_rn(zn[k].x, inv_tau); uc[k][1] = __fmul_rn(zn[k].y, inv_tau);   // b == 0
+          uc[k][2] = __fmul_rn(zn[k].z, inv_tau); uc[k][3] = __fmul_rn(zn[k].w, inv_tau);
         }
       }
+#if defined(NC_WALK_ABL) && NC_WALK_ABL >= 2   // diagnostics: no statistics
+      tm = 0.f; ts = 1.f;
+#else
+      if (has_next) ms_regs(uc, ng, tm, ts);
+#endif
       WALK_MARK(0);
       if (wid == 1 && pre_next) prefetch_wait();
-      unsigned long long c1 = 0, c2 = 0;
-      Best cb{};
-      cta_ms(tm, ts);                                   // contains a __syncthreads
-      cta_counts((unsigned long long)my_sum, (unsigned long long)my_cum, bb, c1, c2, cb);
-      if (tid == 0) {
-        Xch &x = xs[par];
-        x.sum = c1; x.cum = c2; x.bv = cb.v; x.bi = cb.i; x.bc = cb.c; x.m = tm; x.s = ts;
-        x.has_tok = (ltok >= 0 && ltok < (int)Vc) ? 1 : 0;
+      // one CTA reduction: (m, s) through the cta_ms tree, exact sums, argmax
+      {
+        ms_warp(tm, ts);
+        const uint32_t s1 = __reduce_add_sync(0xffffffffu, my_sum), s2 = __reduce_add_sync(0xffffffffu, my_cum);
+        Best wb = best_warp(bb);
+        if (lane == 0) {
+          sm.red_m[wid] = tm; sm.red_s[wid] = ts;
+          sm.red_sum[wid] = s1; sm.red_cum[wid] = s2;
+          sm.red_bv[wid] = wb.v; sm.red_bi[wid] = wb.i; sm.red_bc[wid] = wb.c;
+        }
+        __syncthreads();
+        if (wid == 0) {
+          tm = sm.red_m[lane]; ts = sm.red_s[lane];
+          ms_warp(tm, ts);
+          const uint32_t c1 = __reduce_add_sync(0xffffffffu, (uint32_t)sm.red_sum[lane]);
+          const uint32_t c2 = __reduce_add_sync(0xffffffffu, (uint32_t)sm.red_cum[lane]);
+          const Best cb = best_warp(Best{sm.red_bv[lane], sm.red_bi[lane], sm.red_bc[lane]});
+          if (lane == 0) {
+            Xch &x = xs[par];
+            x.sum = c1; x.cum = c2; x.bv = cb.v; x.bi = cb.i; x.bc = cb.c; x.m = tm; x.s = ts;
+            x.has_tok = (ltok >= 0 && ltok < (int)Vc) ? 1 : 0;
+          }
+          __syncwarp();
+          push_slot(par);
+        }
       }
-      __syncthreads();
       WALK_MARK(1);
-      if (CS > 1) cl_sync();
+      if (CS > 1) cl_sync(); else __syncthreads();
       WALK_MARK(2);
       if (wid == 0) {
-        gather(par);
         if (lane == 0) {
           unsigned long long s1 = 0, s2 = 0;
           Best b2{-1.f, 0x7fffffff, 0};
-          float nm = xin[0].m, ns = xin[0].s;
+          float nm = xin[par][0].m, ns = xin[par][0].s;
           float pt_t = 0.f, png_t = 0.f, p_t = 0.f;
           uint32_t fq = 0;
           for (int r = 0; r < CS; ++r) {
-            s1 += xin[r].sum; s2 += xin[r].cum;
-            best_merge(b2, xin[r].bv, xin[r].bi, xin[r].bc);
-            if (r) ms_merge(nm, ns, xin[r].m, xin[r].s);
-            if (xin[r].has_tok) { pt_t = xin[r].pt_t; png_t = xin[r].png_t; p_t = xin[r].p_t; fq = xin[r].freq_t; }
+            const Xch &x = xin[par][r];
+            s1 += x.sum; s2 += x.cum;
+            best_merge(b2, x.bv, x.bi, x.bc);
+            if (r) ms_merge(nm, ns, x.m, x.s);
+            if (x.has_tok) { pt_t = x.pt_t; png_t = x.png_t; p_t = x.p_t; fq = x.freq_t; }
           }
           const long long R = (long long)T - (long long)s1;
           if ((long long)b2.c + R < 1) st->err = 1;     // D6
@@ -631,10 +806,10 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
             if (a.out_p) a.out_p[oi] = p_t;
           }
           if (mix) mixer_update(pt_t, png_t);
-          if (use_ng && ltok >= 0 && ltok < (int)Vc) cu_s[ltok] += 1u;
+          if (use_ng && ltok >= 0 && ltok < (int)Vc) cu_s[ltok] = __fadd_rn(cu_s[ltok], 1.f);
           if (has_next) { sm.M = nm; sm.invS = __frcp_rn(ns); }
         }
-        __syncwarp();
+      } else if (wid == 1) {   // N-gram fixups: this token's out, the next token's in (parallel to warp 0)
         clear_list(i);
         __syncwarp();
         if (has_next) scatter_list(i + 1);
@@ -683,13 +858,12 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
       __syncthreads();
       // (2) softmax statistics
       {
-        float tm = -CUDART_INF_F, ts = 0.f;
-        for (int g = tid; g < Gc; g += WT) {
-          float u[4];
-          load_u(z, g, u);
+        float ud[NGM][4];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) ms_push(tm, ts, u[j]);
-        }
+        for (int k = 0; k < NGM; ++k)
+          if (k < ng) load_u(z, tid + k * WT, ud[k]);
+        float tm, ts;
+        ms_regs(ud, ng, tm, ts);
         cta_ms(tm, ts);
         if (tid == 0) { xs[par].m = tm; xs[par].s = ts; }
         __syncthreads();
@@ -697,8 +871,8 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
         if (wid == 0) {
           gather(par);
           if (lane == 0) {
-            float M = xin[0].m, S = xin[0].s;
-            for (int r = 1; r < CS; ++r) ms_merge(M, S, xin[r].m, xin[r].s);
+            float M = xin[par][0].m, S = xin[par][0].s;
+            for (int r = 1; r < CS; ++r) ms_merge(M, S, xin[par][r].m, xin[par][r].s);
             sm.M = M; sm.invS = __frcp_rn(S);
           }
         }
@@ -734,10 +908,10 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
           if (lane == 0) {
             unsigned long long s1 = 0, before = 0;
             Best b2{-1.f, 0x7fffffff, 0};
-            for (int r = 0; r < CS; ++r) { s1 += xin[r].sum; best_merge(b2, xin[r].bv, xin[r].bi, xin[r].bc); }
+            for (int r = 0; r < CS; ++r) { s1 += xin[par][r].sum; best_merge(b2, xin[par][r].bv, xin[par][r].bi, xin[par][r].bc); }
             const long long R = (long long)T - (long long)s1;
             if ((long long)b2.c + R < 1) st->err = 1;
-            for (int r = 0; r < (int)rank; ++r) before += xin[r].sum + ((uint32_t)b2.i / Vc == (uint32_t)r ? R : 0);
+            for (int r = 0; r < (int)rank; ++r) before += xin[par][r].sum + ((uint32_t)b2.i / Vc == (uint32_t)r ? R : 0);
             sm.resid = R;
             sm.argmax = b2.i;
             sm.cum_t = before;                           // this CTA's first cumulative count
@@ -804,9 +978,9 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
           if (lane == 0) {
             int t = -1;
             for (int r = 0; r < CS; ++r)
-              if (xin[r].found) {
-                t = xin[r].t; sm.cum_t = xin[r].cum_t; sm.freq_t = xin[r].fq_t;
-                sm.pt_t = xin[r].fpt; sm.png_t = xin[r].fpng; sm.p_t = xin[r].fp;
+              if (xin[par][r].found) {
+                t = xin[par][r].t; sm.cum_t = xin[par][r].cum_t; sm.freq_t = xin[par][r].fq_t;
+                sm.pt_t = xin[par][r].fpt; sm.png_t = xin[par][r].fpng; sm.p_t = xin[par][r].fp;
               }
             sm.tok = t;
             if (t < 0 || tgt >= T) st->err = 2;
@@ -859,7 +1033,7 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
             st->low = lo; st->high = hi; st->value = val; st->bitpos = bp;
           }
           if (mix) mixer_update(sm.pt_t, sm.png_t);
-          if (use_ng && lt >= 0 && lt < (int)Vc) cu_s[lt] += 1u;
+          if (use_ng && lt >= 0 && lt < (int)Vc) cu_s[lt] = __fadd_rn(cu_s[lt], 1.f);
           s_i = i + 1;
         }
         __syncwarp();
@@ -880,7 +1054,7 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
   // ---- write the state slice back
   for (uint32_t v = tid; v < Vc; v += WT) {
     if (use_head) b_g[v] = b_s[v];
-    if (use_ng) cu_g[v] = cu_s[v];
+    if (use_ng) cu_g[v] = (uint32_t)cu_s[v];
   }
   if (tid == 0 && rank == 0) {
     st->lw[0] = s_lw[0]; st->lw[1] = s_lw[1];
@@ -897,6 +1071,9 @@ static int walk_cluster_size(uint32_t V) { return (V >= 4096 && V % 64 == 0) ? 4
 template <int CS>
 static void launch_walk_cs(const WalkArgs &a, cudaStream_t s) {
   const uint32_t Vc = a.V / CS;
+  if (Vc % 4 || Vc / 4 > 8u * WT)   // float4 groups, at most 8 per thread (register-resident rows)
+    throw std::runtime_error("walk: vocabulary slice of " + std::to_string(Vc) +
+                             " ids per CTA unsupported (needs a multiple of 4, at most 16384)");
   const size_t dyn = (size_t)Vc * 8 + Vc * 4 + Vc * 4 + ((Vc + 31) / 32) * 4 + (Vc / 4) * 4 + 64;
   static bool attr = false;
   if (!attr) {

@@ -1,5 +1,5 @@
 """One warm-up + one measured compress step of the bench workload (for ncu runs).
-Usage: python tools/profile_step.py [workload] [n_steps]"""
+Usage: python tools/profile_step.py [workload] [n_steps] [flags]"""
 import os
 import sys
 
@@ -20,7 +20,8 @@ data = open(ensure_text(wl.name), "rb").read()
 model = nc.Model(ensure_model(wl.shape), 0)
 tokens, ntok = nc.nc_tokenize(model, data, wl.n_chunks)
 tok = torch.from_numpy(tokens.view(np.int32).copy()).cuda()
-prm = nc.nc_params_default(window=wl.window, slide=wl.slide, n_chunks=wl.n_chunks, cdf_bits=wl.cdf_bits)
+kw = {"flags": int(sys.argv[3])} if len(sys.argv) > 3 else {}
+prm = nc.nc_params_default(window=wl.window, slide=wl.slide, n_chunks=wl.n_chunks, cdf_bits=wl.cdf_bits, **kw)
 for i in range(steps):
     blob = nc.nc_compress_tokens(model, tok.data_ptr(), ntok, prm, torch.cuda.current_stream().cuda_stream)
 torch.cuda.synchronize()
