@@ -31,9 +31,7 @@
 // Tiles are claimed dynamically by the leader's producer (atomic counter; the
 // last CTA to exit resets it) and broadcast to the peer through DSMEM, so CTAs
 // that start late -- e.g. on SMs a concurrently running walk held -- find no
-// work instead of stalling the GEMM.  Claim order streams the larger operand
-// once: M-fastest when there are at least as many N tiles as M tiles (weights /
-// vocab head), N-fastest otherwise (A tile reused from L2).
+// work instead of stalling the GEMM.  Claim order: see tile_mn.
 //
 // Row results do not depend on which other rows share the tile (each output
 // element is one fixed sequence of MMAs), so prefill and decode agree bit for
@@ -161,9 +159,23 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
   const int num_m = (a.M + 2 * TBM - 1) / (2 * TBM), num_n = (a.N + TBN - 1) / TBN;
   const int n_tiles = num_m * num_n;
   const int nk = a.K / TBK;
+  // Claim order.  Many N tiles (vocab head, gate/up): bands of RB M tiles, M-fastest
+  // inside a band, sweeping every N tile -- the band's A rows (RB x 256 rows, ~37 MB of
+  // tf32 planes at K = 576) stay in L2 while B streams once per band.  (Plain
+  // M-fastest re-read all of A from DRAM for every N tile on the head: 25.8 GB per
+  // launch.)  Few N tiles: N-fastest, the A tile is reused across them from L2.
+  constexpr int RB = 32;
   const bool m_fast = num_n >= num_m;
   auto tile_mn = [&](int t, int &mb, int &nb) {
-    if (m_fast) { mb = t % num_m; nb = t / num_m; } else { nb = t % num_n; mb = t / num_n; }
+    if (m_fast) {
+      const int band = t / (RB * num_n), r = t - band * RB * num_n;
+      const int rows = min(RB, num_m - band * RB);
+      mb = band * RB + r % rows;
+      nb = r / rows;
+    } else {
+      nb = t % num_n;
+      mb = t / num_n;
+    }
   };
 
   if (warp == W_TMA && lane == 0) {

@@ -22,9 +22,11 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
         "sm__warps_active.avg.pct_of_peak_sustained_active", "smsp__issue_active.avg.pct_of_peak_sustained_active",
         "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
-        "l1tex__t_bytes.sum", "lts__t_bytes.sum", "sm__cycles_elapsed.avg.per_second"]
+        "l1tex__t_bytes.sum", "lts__t_bytes.sum", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
+        "launch__cluster_dim_x", "sm__cycles_elapsed.avg.per_second"]
 CLASS = {"attention_kernel": "attention", "walk_kernel": "walk", "attn_tc_kernel": "attention",
-         "walk_cl_kernel<4>": "walk", "gemm_tc_kernel<0>": "gemm_qkv",
+         "walk_cl_kernel<4>": "walk", "nc::walk_cl_kernel<(int)4>": "walk", "nc::attn_tc_kernel": "attention", "gemm_tc_kernel<0>": "gemm_qkv",
          "gemm_tc_kernel<1>": "gemm_o|gemm_down", "gemm_tc_kernel<2>": "gemm_gateup", "gemm_tc_kernel<3>": "gemm_head"}
 
 
@@ -63,6 +65,7 @@ def full(tag, name, rep):
     idx = {h: i for i, h in enumerate(hdr)}
     lines = [f"# {tag}: ncu --set full, {name} ({os.path.basename(rep)})", ""]
     traffic = {}
+    seen = {}
     for r in rows[2:]:
         kn = r[idx["Kernel Name"]]
         lines.append(f"## {kn}")
@@ -72,8 +75,10 @@ def full(tag, name, rep):
         rd = float(r[idx["dram__bytes_read.sum"]].replace(",", "")) * (1e6 if units[idx["dram__bytes_read.sum"]] == "Mbyte" else 1e3 if units[idx["dram__bytes_read.sum"]] == "Kbyte" else 1e9 if units[idx["dram__bytes_read.sum"]] == "Gbyte" else 1)
         wr = float(r[idx["dram__bytes_write.sum"]].replace(",", "")) * (1e6 if units[idx["dram__bytes_write.sum"]] == "Mbyte" else 1e3 if units[idx["dram__bytes_write.sum"]] == "Kbyte" else 1e9 if units[idx["dram__bytes_write.sum"]] == "Gbyte" else 1)
         base = kn.split("(")[0].replace("void ", "").strip()
-        for c in CLASS.get(base, base).split("|"):
-            traffic[c] = rd + wr
+        alts = CLASS.get(base, base).split("|")   # several classes share a kernel: capture order
+        k_ = seen.get(base, 0)
+        seen[base] = k_ + 1
+        traffic[alts[min(k_, len(alts) - 1)]] = rd + wr
         lines.append("")
     open(os.path.join(PROF, f"{tag}_{name}.md"), "w").write("\n".join(lines) + "\n")
     tpath = os.path.join(PROF, "ncu_traffic.json")
