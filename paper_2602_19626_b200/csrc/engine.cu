@@ -933,6 +933,7 @@ void debug_gemm(int device, const float *A, const float *B, uint32_t M, uint32_t
       const double us = 1e3 * ms / reps;
       fprintf(stderr, "gemm_tc M=%u N=%u K=%u epi=%s nostore=%d: %.1f us/launch, %.1f TFLOP/s (algorithmic)\n", M, N,
               K, resid ? "resid" : "head", t.no_store, us, 2.0 * M * N * K / (us * 1e-6) / 1e12);
+      gemm_timing_report();
     }
   } else {
     GemmArgs g{};

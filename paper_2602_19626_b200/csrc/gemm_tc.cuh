@@ -30,6 +30,8 @@ struct TcOperands {
 void launch_gemm_tc(GemmEpi epi, const TcGemmArgs &a, const TcOperands &op, cudaStream_t s);
 // SMs left out of persistent grids (occupied by a concurrently running walk)
 void set_reserved_sms(int n);
+// diagnostics build (-DNC_GEMM_TIMING): epilogue phase cycles -> stderr
+void gemm_timing_report();
 void launch_split_planes(const float *x, float *hi, float *lo, size_t n, cudaStream_t s);
 
 }  // namespace nc

@@ -41,6 +41,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -52,19 +53,26 @@
 namespace nc {
 
 constexpr int TBM = 128;              // rows per CTA (pair tile: 256)
-constexpr int TBN = 256;              // pair tile columns (MMA N); each CTA stages TBN / 2 rows of B
+// BN = pair tile columns (MMA N; each CTA stages BN / 2 rows of B): 256, or 192 for
+// the N = 576 residual GEMMs (576 = 3 x 192: no padded MMA work, smaller output bursts)
 constexpr int TBK = 32, TSTAGES = 3, NPART = 2, NSCHED = 4;
 // k blocks per TMEM partial.  Promotion reads the whole 128 x 256 fp32 partial
 // (128 KB) per CTA; tcgen05.ld moves ~64 B/cycle/SM (B300_MICROARCH), i.e.
 // 2048 cycles, against 12 * 128 = 1536 MMA cycles per 32-wide k block -- so a
 // partial spans 2 k blocks (3072 MMA cycles) to keep the tensor pipe the bound.
 constexpr int KPP = 2;
-constexpr int EPI_WARPS = 8, EPI_COLS = TBN / 2;
+constexpr int EPI_WARPS = 8;
 constexpr int TILE_A_BYTES = TBM * TBK * 4;          // 16 KB
-constexpr int TILE_B_BYTES = (TBN / 2) * TBK * 4;    // 16 KB
-constexpr int STAGE_BYTES = 2 * TILE_A_BYTES + 2 * TILE_B_BYTES;   // 64 KB per CTA
 constexpr int OUT_STAGE_BYTES = EPI_WARPS * 32 * 32 * 4;   // 32 KB: epilogue transpose tiles
-constexpr int TC_SMEM = TSTAGES * STAGE_BYTES + OUT_STAGE_BYTES + 1024 /*align*/ + 512 /*barriers, schedule*/;
+constexpr int TMEM_COLS = 512;                              // NPART x BN <= 512, power of two
+template <int BN>
+struct TileCfg {
+  static constexpr int EPI_COLS = BN / 2;                                // columns per epilogue warp
+  static constexpr int TILE_B_BYTES = (BN / 2) * TBK * 4;                // 16 / 12 KB
+  static constexpr int STAGE_BYTES = 2 * TILE_A_BYTES + 2 * TILE_B_BYTES;   // 64 / 56 KB per CTA
+  static constexpr int SMEM = TSTAGES * STAGE_BYTES + OUT_STAGE_BYTES + 1024 /*align*/ + 512 /*barriers*/;
+  static_assert(NPART * BN <= TMEM_COLS && BN % 32 == 0, "tile");
+};
 constexpr int TC_THREADS = 320;
 constexpr int W_TMA = 8, W_MMA = 9;
 // sch_empty arrivals per tile claim: leader MMA + 8 epilogue warps per CTA + the peer's producer
@@ -78,7 +86,7 @@ constexpr int SCHED_CONSUMERS = 1 + 2 * EPI_WARPS + 1;
 // destinations (this lane's row); d0 == nullptr skips the row.
 //   ST_PLAIN  d0 = v
 //   ST_SPLIT  d0 = tf32 hi(v), d1 = lo(v)
-//   ST_RESID  d0 = v (the updated residual h), d1 = hi(v), d2 = lo(v)
+//   ST_RESID  h = d0 + v (fp32 RN); d0 = h, d1 = hi(h), d2 = lo(h)
 enum { ST_PLAIN = 0, ST_SPLIT = 1, ST_RESID = 2 };
 template <int MODE>
 __device__ __forceinline__ void store_rows32(float *stg, const float *v, float *d0, float *d1, float *d2, int lane) {
@@ -88,6 +96,16 @@ __device__ __forceinline__ void store_rows32(float *stg, const float *v, float *
         make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
   __syncwarp();
   const int c4 = lane & 7;
+  float4 hin[MODE == ST_RESID ? 8 : 1];
+  if (MODE == ST_RESID) {   // residual rows (L2-resident: prefetched at tile start); all loads before any store
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int r = 4 * i + (lane >> 3);
+      const float *p0 =
+          reinterpret_cast<const float *>(__shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(d0), r));
+      hin[i] = p0 ? *reinterpret_cast<const float4 *>(p0 + 4 * c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const int r = 4 * i + (lane >> 3);
@@ -103,7 +121,11 @@ __device__ __forceinline__ void store_rows32(float *stg, const float *v, float *
       if (MODE == ST_PLAIN) {
         *reinterpret_cast<float4 *>(p0 + 4 * c4) = y;
       } else {
-        if (MODE == ST_RESID) *reinterpret_cast<float4 *>(p0 + 4 * c4) = y;
+        if (MODE == ST_RESID) {
+          y.x = __fadd_rn(hin[i].x, y.x); y.y = __fadd_rn(hin[i].y, y.y);
+          y.z = __fadd_rn(hin[i].z, y.z); y.w = __fadd_rn(hin[i].w, y.w);
+          *reinterpret_cast<float4 *>(p0 + 4 * c4) = y;
+        }
         float4 hi, lo;
         tc::split_tf32(y.x, hi.x, lo.x); tc::split_tf32(y.y, hi.y, lo.y);
         tc::split_tf32(y.z, hi.z, lo.z); tc::split_tf32(y.w, hi.w, lo.w);
@@ -116,33 +138,29 @@ __device__ __forceinline__ void store_rows32(float *stg, const float *v, float *
   __syncwarp();
 }
 
-// The inverse: v[0..31] (this lane's row) = src row [0, 32) read row-contiguously
-// through the same tile; src == nullptr gives zeros.
-__device__ __forceinline__ void load_rows32(float *stg, float *v, const float *src, int lane) {
-  const int c4 = lane & 7;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int r = 4 * i + (lane >> 3);
-    const float *p =
-        reinterpret_cast<const float *>(__shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(src), r));
-    *reinterpret_cast<float4 *>(stg + r * 32 + 4 * (c4 ^ (r & 7))) =
-        p ? *reinterpret_cast<const float4 *>(p + 4 * c4) : make_float4(0.f, 0.f, 0.f, 0.f);
-  }
-  __syncwarp();
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const float4 y = *reinterpret_cast<const float4 *>(stg + lane * 32 + 4 * (k ^ (lane & 7)));
-    v[4 * k] = y.x; v[4 * k + 1] = y.y; v[4 * k + 2] = y.z; v[4 * k + 3] = y.w;
-  }
-  __syncwarp();
-}
+#ifdef NC_GEMM_TIMING
+// diagnostics build only: epilogue phase cycle sums of warp 0 lane 0 (per tile)
+__device__ unsigned long long g_gemm_clk[8];
+#define GEMM_MARK(k)                                                                        \
+  do {                                                                                      \
+    if (threadIdx.x == 0) {                                                                 \
+      const long long _n = clock64();                                                       \
+      atomicAdd(&g_gemm_clk[k], (unsigned long long)(_n - _gt));                            \
+      _gt = _n;                                                                             \
+    }                                                                                       \
+  } while (0)
+#else
+#define GEMM_MARK(k) do {} while (0)
+#endif
 
-template <int EPI>
+template <int EPI, int BN>
 __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_constant__ CUtensorMap tmAh,
                                                                 const __grid_constant__ CUtensorMap tmAl,
                                                                 const __grid_constant__ CUtensorMap tmBh,
                                                                 const __grid_constant__ CUtensorMap tmBl,
                                                                 TcGemmArgs a) {
+  using C_ = TileCfg<BN>;
+  constexpr int TBN = BN, EPI_COLS = C_::EPI_COLS, TILE_B_BYTES = C_::TILE_B_BYTES, STAGE_BYTES = C_::STAGE_BYTES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float *stage_out = reinterpret_cast<float *>(smem + TSTAGES * STAGE_BYTES);
@@ -185,7 +203,7 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
     for (int s = 0; s < NSCHED; ++s) { tc::mbar_init(&sch_full[s], 1); tc::mbar_init(&sch_empty[s], SCHED_CONSUMERS); }
     tc::fence_barrier_init();
   }
-  if (warp == W_TMA) tc::tmem_alloc_pair(tmem_base_smem, NPART * TBN);
+  if (warp == W_TMA) tc::tmem_alloc_pair(tmem_base_smem, TMEM_COLS);
   tc::fence_before();
   tc::cluster_sync();
   tc::fence_after();
@@ -249,7 +267,7 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
         for (int kb0 = 0; kb0 < nk; kb0 += KPP) {
           const int nkp = min(KPP, nk - kb0);
           tc::mbar_wait(&tempty[buf], buf_phase ^ 1);   // partial drained by both CTAs' epilogues
-          const uint32_t d = tmem_base + buf * TBN;
+          const uint32_t d = tmem_base + buf * BN;
           int st = stage;
           uint32_t ph = phase;
           for (int i = 0; i < nkp; ++i) {
@@ -293,11 +311,18 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
     uint32_t buf_phase = 0;
     for (int jt = 0;; ++jt) {
       const int slot = jt % NSCHED;
+#ifdef NC_GEMM_TIMING
+      long long _gt = clock64();
+#endif
       tc::mbar_wait_cluster(&sch_full[slot], (jt / NSCHED) & 1);
+      GEMM_MARK(0);   // wait for the tile
       const int t = sch_tile[slot];
       __syncwarp();
       if (lane == 0) tc::mbar_arrive_remote(sch_empty_leader + slot * 8);
       if (t < 0) break;
+#ifdef NC_GEMM_TIMING
+      if (threadIdx.x == 0) atomicAdd(&g_gemm_clk[7], 1ull);
+#endif
       int mb, nb;
       tile_mn(t, mb, nb);
       const int m = mb * (2 * TBM) + (int)rank * TBM + q * 32 + lane;
@@ -305,22 +330,26 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
       const float rs = (EPI != EPI_RESID && row_ok && a.rinv) ? a.rinv[m] : 1.f;   // loaded under the k loop
       float acc[EPI_COLS];
       float *stg = stage_out + warp * 32 * 32;   // this warp's 32 x 32 transpose tile
-      if (EPI == EPI_RESID) {
-        // h_new = ((h + P0) + P1) + ...: the promotion sum starts from the residual row
-        // (read now, under the first partials' MMAs; the output is then store-only)
+      if (EPI == EPI_RESID && !a.no_store) {
+        // residual rows of this warp's 32 x 128 block into L2 now (no registers); they
+        // are read (from L2) and added after the promotion sum: h_new = h + sum_p P_p
+        if (row_ok) {
+          const char *hrow = reinterpret_cast<const char *>(a.C + (size_t)m * a.ldc + nb * TBN + hc * EPI_COLS);
 #pragma unroll
-        for (int sl = 0; sl < EPI_COLS / 32; ++sl) {
-          const int c0 = nb * TBN + hc * EPI_COLS + sl * 32;
-          load_rows32(stg, acc + sl * 32, (row_ok && c0 < a.N) ? a.C + (size_t)m * a.ldc + c0 : nullptr, lane);
+          for (int l = 0; l < EPI_COLS * 4 / 128; ++l)
+            if (nb * TBN + hc * EPI_COLS + l * 32 < a.N) asm volatile("prefetch.global.L2 [%0];" ::"l"(hrow + l * 128));
         }
-      } else {
+      }
+      {
 #pragma unroll
         for (int j = 0; j < EPI_COLS; ++j) acc[j] = 0.f;
       }
+      GEMM_MARK(1);   // residual seed
       for (int kb0 = 0; kb0 < nk; kb0 += KPP) {
         tc::mbar_wait(&tfull[buf], buf_phase);
+        GEMM_MARK(2);   // waiting for partials
         tc::fence_after();
-        const uint32_t taddr = tmem_base + buf * TBN + hc * EPI_COLS + ((uint32_t)(q * 32) << 16);
+        const uint32_t taddr = tmem_base + buf * BN + hc * EPI_COLS + ((uint32_t)(q * 32) << 16);
 #pragma unroll
         for (int c = 0; c < EPI_COLS / 16; ++c) {
           uint32_t r[16];
@@ -335,18 +364,24 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
         if (++buf == NPART) { buf = 0; buf_phase ^= 1; }
       }
 #pragma unroll
+      GEMM_MARK(3);   // draining partials
       if (a.no_store) continue;
+      if (EPI == EPI_RESID) {   // residual: h += acc and the next tf32 planes, by 32-column slices
+#pragma unroll
+        for (int sl = 0; sl < EPI_COLS / 32; ++sl) {
+          const int cb = nb * TBN + hc * EPI_COLS + sl * 32;
+          if (cb >= a.N) continue;                              // warp-uniform
+          const size_t o = (size_t)m * a.ldc + cb;
+          store_rows32<ST_RESID>(stg, acc + sl * 32, row_ok ? a.C + o : nullptr, a.C_hi + o, a.C_lo + o, lane);
+        }
+      } else {
+        static_assert(EPI == EPI_RESID || BN % 128 == 0, "64-column epilogue blocks");
 #pragma unroll
       for (int half = 0; half < EPI_COLS / 64; ++half) {
         const int cb = nb * TBN + hc * EPI_COLS + half * 64;   // first column of this 64-wide block
         if (cb >= a.N) continue;                              // warp-uniform
         float *x = acc + half * 64;   // in place: the block's partial sums are dead after it
-        if (EPI == EPI_RESID) {
-          const size_t o = (size_t)m * a.ldc + cb;
-          float *hp = row_ok ? a.C + o : nullptr;
-          store_rows32<ST_RESID>(stg, x, hp, a.C_hi + o, a.C_lo + o, lane);
-          store_rows32<ST_RESID>(stg, x + 32, hp ? hp + 32 : nullptr, a.C_hi + o + 32, a.C_lo + o + 32, lane);
-        } else {
+        {
 #pragma unroll
           for (int j = 0; j < 64; ++j) x[j] = __fmul_rn(x[j], rs);
           if (EPI == EPI_HEAD) {
@@ -399,12 +434,14 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
           }
         }
       }
+      }
+      GEMM_MARK(4);   // output
     }
   }
   tc::fence_before();
   tc::cluster_sync();          // no CTA leaves while its pair may still signal or read it
   tc::fence_after();
-  if (warp == W_TMA) tc::tmem_dealloc_pair(tmem_base, NPART * TBN);
+  if (warp == W_TMA) tc::tmem_dealloc_pair(tmem_base, TMEM_COLS);
   if (threadIdx.x == 0) {            // last CTA out resets the tile counter for the next launch
     __threadfence();
     if (atomicAdd(a.tile_ctr + 1, 1) == (int)gridDim.x - 1) {
@@ -481,23 +518,23 @@ static int num_sms() {
   return n;
 }
 
-template <int EPI>
+template <int EPI, int BN>
 static void launch_tc(const TcGemmArgs &a, const TcOperands &op, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(gemm_tc_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
+    cudaFuncSetAttribute(gemm_tc_kernel<EPI, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, TileCfg<BN>::SMEM);
     attr = true;
   }
   const CUtensorMap *ah = tmap_2d(op.A_hi, op.a_rows, a.K, TBM), *al = tmap_2d(op.A_lo, op.a_rows, a.K, TBM);
-  const CUtensorMap *bh = tmap_2d(op.B_hi, a.N, a.K, TBN / 2), *bl = tmap_2d(op.B_lo, a.N, a.K, TBN / 2);
-  const int tiles = ((a.M + 2 * TBM - 1) / (2 * TBM)) * ((a.N + TBN - 1) / TBN);
+  const CUtensorMap *bh = tmap_2d(op.B_hi, a.N, a.K, BN / 2), *bl = tmap_2d(op.B_lo, a.N, a.K, BN / 2);
+  const int tiles = ((a.M + 2 * TBM - 1) / (2 * TBM)) * ((a.N + BN - 1) / BN);
   const int pairs = std::min(tiles, std::max(1, (num_sms() - g_reserved_sms) / 2));
   TcGemmArgs aa = a;
   aa.tile_ctr = tile_counter();
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * pairs);
   cfg.blockDim = dim3(TC_THREADS);
-  cfg.dynamicSmemBytes = TC_SMEM;
+  cfg.dynamicSmemBytes = TileCfg<BN>::SMEM;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -506,18 +543,33 @@ static void launch_tc(const TcGemmArgs &a, const TcOperands &op, cudaStream_t s)
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_tc_kernel<EPI>, *ah, *al, *bh, *bl, aa);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_tc_kernel<EPI, BN>, *ah, *al, *bh, *bl, aa);
   if (e != cudaSuccess) throw std::runtime_error(std::string("gemm_tc launch: ") + cudaGetErrorString(e));
+}
+
+void gemm_timing_report() {
+#ifdef NC_GEMM_TIMING
+  unsigned long long h[8];
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(h, g_gemm_clk, sizeof(h));
+  const double n = (double)(h[7] ? h[7] : 1);
+  fprintf(stderr,
+          "gemm epilogue warp per tile (cycles): wait tile %.0f | residual seed %.0f | wait partials %.0f | "
+          "drain %.0f | output %.0f | tiles %.0f\n",
+          h[0] / n, h[1] / n, h[2] / n, h[3] / n, h[4] / n, n);
+  unsigned long long z[8] = {};
+  cudaMemcpyToSymbol(g_gemm_clk, z, sizeof(z));
+#endif
 }
 
 void launch_gemm_tc(GemmEpi epi, const TcGemmArgs &a, const TcOperands &op, cudaStream_t s) {
   if (a.M <= 0) return;
   if (a.K % TBK) throw std::runtime_error("tcgen05 GEMM needs K % 32 == 0");
   switch (epi) {
-    case EPI_QKV: launch_tc<EPI_QKV>(a, op, s); break;
-    case EPI_RESID: launch_tc<EPI_RESID>(a, op, s); break;
-    case EPI_SWIGLU: launch_tc<EPI_SWIGLU>(a, op, s); break;
-    case EPI_HEAD: launch_tc<EPI_HEAD>(a, op, s); break;
+    case EPI_QKV: launch_tc<EPI_QKV, 256>(a, op, s); break;
+    case EPI_RESID: launch_tc<EPI_RESID, 192>(a, op, s); break;   // N = 576 = 3 x 192
+    case EPI_SWIGLU: launch_tc<EPI_SWIGLU, 256>(a, op, s); break;
+    case EPI_HEAD: launch_tc<EPI_HEAD, 256>(a, op, s); break;
   }
 }
 
