@@ -692,6 +692,7 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
   NC_CUDA(cudaStreamSynchronize(s));
   if (prof().on) prof().collect();
   if (std::getenv("NC_WALK_REPORT")) walk_timing_report();
+  if (std::getenv("NC_GEMM_REPORT")) gemm_timing_report();
   for (int c = 0; c < n_chunks; ++c) out.err[c] = hs[c].err;
   for (int sl = 0; sl < n_slabs; ++sl) {
     float a = 0, b = 0;
@@ -768,7 +769,7 @@ void decompress_device(nc_model *m, const uint8_t *blob, const Nc05View &view, c
   ensure_rope(m, (int)max_n + 1);
   Bag bag(s);
   Forward fw{m, s};
-  const int ring_len = (int)p.window + 64;
+  const int ring_len = (int)p.window + 128;   // 128-key attention blocks never wrap
   fw.alloc(bag, n_chunks, n_chunks, ring_len);
   std::vector<uint8_t> bl(blob, blob + blob_len);
   uint8_t *blob_d = bag.upload(bl);
@@ -872,7 +873,7 @@ void debug_forward(nc_model *m, const uint32_t *x, uint32_t rows, const Params &
       NC_CUDA(cudaMemcpyAsync(out + (size_t)sl * Rr * S.V, fw.logits, (size_t)cnt * S.V * 4, cudaMemcpyDeviceToHost, s));
     }
   } else {
-    fw.alloc(bag, 1, 1, (int)p.window + 64);
+    fw.alloc(bag, 1, 1, (int)p.window + 128);
     int32_t *rc = bag.get<int32_t>(1), *rp = bag.get<int32_t>(1);
     AttnTile *tiles = bag.get<AttnTile>(1);
     int32_t *wc = bag.get<int32_t>(1), *wr = bag.get<int32_t>(1), *wn = bag.get<int32_t>(1);

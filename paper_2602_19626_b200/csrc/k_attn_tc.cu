@@ -1,27 +1,28 @@
 // Block-window causal GQA attention on the tensor cores (
 // P:482-502 retained-KV window, D9-D12), fp32-accurate via 3xTF32:
 //
-//   for each 64-key block b of keys [w(j), j] (blocks aligned to absolute positions):
-//     S_b  = Q K_b^T              tcgen05 kind::tf32, 3 products x 8 k-steps  -> TMEM
-//     m_b  = max(m_{b-1}, rowmax(S_b / 8)), P_b = exp(S_b/8 - m_b) (masked), l updated
-//     O_b  = P_b V_b              tcgen05 kind::tf32 (V as an MN-major B operand) -> fresh TMEM partial
-//     O   <- O * exp(m_{b-1} - m_b) + O_b     in fp32 RN registers (promotion, see k_gemm_tc.cu)
-//   o = O / l
+//   for each 128-key block b of keys [w(j), j] (blocks aligned to absolute positions;
+//   the window start w(j) is a multiple of C >= 128, so no block straddles it):
+//     S_b = Q K_b^T                     tcgen05 kind::tf32, 3 products x 8 k-steps, N = 128 -> TMEM
+//   and independently for each half X of the block's keys (X = keys 0-63 / 64-127):
+//     m_X = max(m_X, rowmax(S_bX / 8)), P_bX = exp(S_bX / 8 - m_X) (masked), l_X updated
+//     O_bX = P_bX V_bX                  tcgen05 kind::tf32 (P from TMEM, V MN-major) -> fresh TMEM partial
+//     O_X <- O_X * exp(m_X,old - m_X) + O_bX      in fp32 RN registers (promotion, see k_gemm_tc.cu)
+//   o = (O_A 2^(m_A - m) + O_B 2^(m_B - m)) / (l_A 2^(m_A - m) + l_B 2^(m_B - m)),  m = max(m_A, m_B)
 //
-// One CTA per (128-row query tile of one chunk, q head); 256 threads:
-//   warp 0 TMA: Q once, then K_hi/K_lo per 64-key block (3 stages, freed when S(i) completes)
-//   warp 3 TMA: V_hi/V_lo per 64-key block (2 stages, freed when PV(i) completes) -- split so
-//          the K loads run ahead of the late V consumer (one shared ring stalled S on the loads)
-//   warp 1 tcgen05.mma issuer; warp 2 TMEM allocator;
-//   warps 4-7 softmax + promotion, thread = query row (TMEM lane); P (hi/lo) goes back
-//   into TMEM (tcgen05.st) and is the A operand of the PV MMA.
-// Two-deep software pipeline (S, P and O partials double-buffered in TMEM): S(i)
-// is issued before PV(i-1), so the softmax of block i overlaps the PV of block i-1.
-// Measured: a kind::tf32 M128 MMA costs >= ~64 cycles even at N = 32, so 64-key
-// blocks (S: N = 64) halve the score-MMA cost of 32-key blocks.
-// A row's arithmetic depends only on its own q row and the key blocks up to its
-// position (later, fully masked blocks are exact no-ops: alpha = 1, P = 0), so the
-// decode step (tiles of one row) reproduces the prefill bit for bit (D15).
+// The two halves are two exact online softmaxes over disjoint key sets, merged
+// once at the end -- the same arithmetic for every row whatever tile it is in,
+// so decode (tiles of one row) reproduces prefill bit for bit (D15); later,
+// fully masked keys are exact no-ops (alpha = 1, P = 0).
+//
+// One CTA per (128-row query tile of one chunk, q head); 384 threads:
+//   warp 0  TMA: Q once (hi/lo, 64 KB), then K of each 128-key block (64 KB, one buffer)
+//   warp 3  TMA: V in 64-key granules (32 KB) through a ring of 3
+//   warp 1  MMA issue (whole warp, one elected lane per instruction): S(i), then PV(i-1) of both halves
+//   warp 2  TMEM allocator: S (128 cols) | P_A hi,lo | P_B hi,lo (64 each) | O_A, O_B partials (64 each)
+//   warps 4-7 / 8-11  softmax + promotion of key half A / B, thread = query row (TMEM lane)
+// Measured (tools/micro): an N = 128 tf32 MMA costs 64 cycles, N = 64 costs 48-57, so S runs at
+// full rate; per 128-key block the MMAs take ~4.2k cycles, which the two softmax groups cover.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -40,27 +41,32 @@
 namespace nc {
 
 constexpr int AQ = 128;          // query rows per tile
-constexpr int AK = 64;           // keys per block
-constexpr int KST = 3;           // K stages
-constexpr int VST = 2;           // V stages
+constexpr int AK = 128;          // keys per block (S: one N = 128 MMA chain)
+constexpr int AH = 64;           // keys per half (softmax group / PV MMA chain)
+constexpr int VG = 3;            // V ring granules (64 keys each)
 constexpr int Q_SUB = AQ * 128;  // one [128 rows x 32 fp32] swizzled sub-tile: 16 KB
-constexpr int KV_SUB = AK * 128; // one [64 keys x 32 fp32] sub-tile: 8 KB
+constexpr int K_SUB = AK * 128;  // one [128 keys x 32 fp32] sub-tile: 16 KB
+constexpr int KV_SUB = AH * 128; // one [64 keys x 32 fp32] sub-tile: 8 KB (TMA box, V granule part)
 constexpr int Q_BYTES = 4 * Q_SUB;               // hi/lo x two 32-dim halves: 64 KB
-constexpr int K_STAGE = 4 * KV_SUB;              // K hi/lo x two 32-dim halves: 32 KB
-constexpr int V_STAGE = 4 * KV_SUB;              // V hi/lo x two 32-dim halves: 32 KB
-constexpr int ATT_SMEM = Q_BYTES + KST * K_STAGE + VST * V_STAGE + 1024 + 256;
-constexpr int ATT_THREADS = 256;
-// TMEM columns: S[2] (64 each) | P[2] (hi 64 + lo 64 each) | O partial[2] (64 each) = 512
-constexpr uint32_t T_S = 0, T_P = 128, T_O = 384;
+constexpr int K_BYTES = 4 * K_SUB;               // hi/lo x two 32-dim halves: 64 KB
+constexpr int V_GRAN = 4 * KV_SUB;               // V hi/lo x two 32-dim halves, 64 keys: 32 KB
+constexpr int ATT_SMEM = Q_BYTES + K_BYTES + VG * V_GRAN + 1024 + 256;
+constexpr int ATT_THREADS = 384;
+// TMEM columns
+constexpr uint32_t T_S = 0, T_P = 128, T_O = 384;   // P half X at T_P + 128 X (hi, lo +64); O half X at T_O + 64 X
 
 #ifdef NC_ATT_TIMING
-// diagnostics build only: per-phase cycle sums (softmax warp 4 lane 0, MMA thread)
-__device__ unsigned long long g_att_clk[16];
-#define ATT_T0() const long long _t0 = clock64()
-#define ATT_ACC(i, t) atomicAdd(&g_att_clk[i], (unsigned long long)(clock64() - (t)))
+__device__ unsigned long long g_att_clk[16];   // diagnostics build only
+#define AT_BEGIN long long _at = clock64()
+#define AT_ACC(k, cond)                                                                   \
+  do {                                                                                    \
+    const long long _n = clock64();                                                       \
+    if (cond) atomicAdd(&g_att_clk[k], (unsigned long long)(_n - _at));                   \
+    _at = _n;                                                                             \
+  } while (0)
 #else
-#define ATT_T0()
-#define ATT_ACC(i, t)
+#define AT_BEGIN do {} while (0)
+#define AT_ACC(k, cond) do {} while (0)
 #endif
 
 __device__ __forceinline__ int wstart(int j, int L, int C) {
@@ -92,6 +98,10 @@ __device__ __forceinline__ void tma_load_4d(void *smem_dst, const CUtensorMap *m
       : "memory");
 }
 
+__device__ __forceinline__ void named_bar(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
 __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_constant__ CUtensorMap tmQh,
                                                                 const __grid_constant__ CUtensorMap tmQl,
                                                                 const __grid_constant__ CUtensorMap tmKh,
@@ -101,14 +111,15 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
                                                                 AttnTcArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t *sQ = smem;                                  // [hi d0-31][hi d32-63][lo d0-31][lo d32-63]
-  uint8_t *sK = smem + Q_BYTES;                        // per stage: Kh0 Kh1 Kl0 Kl1
-  uint8_t *sV = sK + KST * K_STAGE;                     // per stage: Vh0 Vh1 Vl0 Vl1
-  uint64_t *bars = reinterpret_cast<uint64_t *>(sV + VST * V_STAGE);
-  uint64_t *q_full = bars, *k_full = bars + 1, *k_empty = k_full + KST, *v_full = k_empty + KST,
-           *v_empty = v_full + VST;
-  uint64_t *s_full = v_empty + VST, *s_empty = s_full + 2, *p_full = s_empty + 2, *p_empty = p_full + 2;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(p_empty + 2);
+  uint8_t *sQ = smem;                                  // [hi d0-31][hi d32-63][lo d0-31][lo d32-63], 128 rows each
+  uint8_t *sK = smem + Q_BYTES;                        // same, 128 keys each (granule g at +8 KB g)
+  uint8_t *sV = sK + K_BYTES;                          // VG granules: [Vh0][Vh1][Vl0][Vl1], 64 keys each
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sV + VG * V_GRAN);
+  uint64_t *q_full = bars, *k_full = bars + 1, *k_empty = bars + 2;
+  uint64_t *v_full = bars + 3, *v_empty = v_full + VG;
+  uint64_t *s_full = v_empty + VG, *s_empty = s_full + 1;
+  uint64_t *p_full = s_empty + 1, *pv_done = p_full + 2;   // per key half
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(pv_done + 2);
 
   const AttnTile t = a.tiles[blockIdx.x];
   if (t.nrows <= 0) return;                        // inactive chunk in a decode step
@@ -122,10 +133,10 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
   if (threadIdx.x == 0) {
     tc::tma_prefetch(&tmQh); tc::tma_prefetch(&tmKh); tc::tma_prefetch(&tmVh);
     tc::mbar_init(q_full, 1);
-    for (int s = 0; s < KST; ++s) { tc::mbar_init(&k_full[s], 1); tc::mbar_init(&k_empty[s], 1); }
-    for (int s = 0; s < VST; ++s) { tc::mbar_init(&v_full[s], 1); tc::mbar_init(&v_empty[s], 1); }
-    for (int s = 0; s < 2; ++s) { tc::mbar_init(&s_full[s], 1); tc::mbar_init(&s_empty[s], 4); }
-    for (int s = 0; s < 2; ++s) { tc::mbar_init(&p_full[s], 4); tc::mbar_init(&p_empty[s], 1); }
+    tc::mbar_init(k_full, 1); tc::mbar_init(k_empty, 1);
+    for (int s = 0; s < VG; ++s) { tc::mbar_init(&v_full[s], 1); tc::mbar_init(&v_empty[s], 1); }
+    tc::mbar_init(s_full, 1); tc::mbar_init(s_empty, 8);
+    for (int s = 0; s < 2; ++s) { tc::mbar_init(&p_full[s], 4); tc::mbar_init(&pv_done[s], 1); }
     tc::fence_barrier_init();
   }
   if (warp == 2) tc::tmem_alloc(tmem_slot, 512);
@@ -133,9 +144,6 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
-#ifdef NC_ATT_TIMING
-  const long long t_cta = clock64();
-#endif
 
   if (warp == 0) {
     if (lane == 0) {
@@ -144,95 +152,100 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
       tc::tma_load_2d(sQ + Q_SUB, &tmQh, h * 64 + 32, t.qrow0, q_full);
       tc::tma_load_2d(sQ + 2 * Q_SUB, &tmQl, h * 64, t.qrow0, q_full);
       tc::tma_load_2d(sQ + 3 * Q_SUB, &tmQl, h * 64 + 32, t.qrow0, q_full);
-      int st = 0;
-      uint32_t ph = 0;
       for (int i = 0; i < nkb; ++i) {
-        tc::mbar_wait(&k_empty[st], ph ^ 1);
-        uint8_t *b = sK + st * K_STAGE;
-        const int slot = ((kb0 + i) * AK) % a.ring;
-        tc::mbar_expect_tx(&k_full[st], K_STAGE);
-        tma_load_4d(b + 0 * KV_SUB, &tmKh, 0, g, slot, zc, &k_full[st]);
-        tma_load_4d(b + 1 * KV_SUB, &tmKh, 32, g, slot, zc, &k_full[st]);
-        tma_load_4d(b + 2 * KV_SUB, &tmKl, 0, g, slot, zc, &k_full[st]);
-        tma_load_4d(b + 3 * KV_SUB, &tmKl, 32, g, slot, zc, &k_full[st]);
-        if (++st == KST) { st = 0; ph ^= 1; }
+        tc::mbar_wait(k_empty, (i & 1) ^ 1);
+        const int slot = ((kb0 + i) * AK) % a.ring;  // ring is a multiple of 128: no wrap inside a block
+        tc::mbar_expect_tx(k_full, K_BYTES);
+#pragma unroll
+        for (int gg = 0; gg < 2; ++gg) {
+          tma_load_4d(sK + 0 * K_SUB + gg * KV_SUB, &tmKh, 0, g, slot + gg * AH, zc, k_full);
+          tma_load_4d(sK + 1 * K_SUB + gg * KV_SUB, &tmKh, 32, g, slot + gg * AH, zc, k_full);
+          tma_load_4d(sK + 2 * K_SUB + gg * KV_SUB, &tmKl, 0, g, slot + gg * AH, zc, k_full);
+          tma_load_4d(sK + 3 * K_SUB + gg * KV_SUB, &tmKl, 32, g, slot + gg * AH, zc, k_full);
+        }
       }
     }
   } else if (warp == 3) {
     if (lane == 0) {
       int st = 0;
       uint32_t ph = 0;
-      for (int i = 0; i < nkb; ++i) {
-        tc::mbar_wait(&v_empty[st], ph ^ 1);
-        uint8_t *b = sV + st * V_STAGE;
-        const int slot = ((kb0 + i) * AK) % a.ring;
-        tc::mbar_expect_tx(&v_full[st], V_STAGE);
-        tma_load_4d(b + 0 * KV_SUB, &tmVh, 0, g, slot, zc, &v_full[st]);
-        tma_load_4d(b + 1 * KV_SUB, &tmVh, 32, g, slot, zc, &v_full[st]);
-        tma_load_4d(b + 2 * KV_SUB, &tmVl, 0, g, slot, zc, &v_full[st]);
-        tma_load_4d(b + 3 * KV_SUB, &tmVl, 32, g, slot, zc, &v_full[st]);
-        if (++st == VST) { st = 0; ph ^= 1; }
-      }
+      for (int i = 0; i < nkb; ++i)
+#pragma unroll
+        for (int gg = 0; gg < 2; ++gg) {
+          tc::mbar_wait(&v_empty[st], ph ^ 1);
+          uint8_t *b = sV + st * V_GRAN;
+          const int slot = ((kb0 + i) * AK) % a.ring + gg * AH;
+          tc::mbar_expect_tx(&v_full[st], V_GRAN);
+          tma_load_4d(b + 0 * KV_SUB, &tmVh, 0, g, slot, zc, &v_full[st]);
+          tma_load_4d(b + 1 * KV_SUB, &tmVh, 32, g, slot, zc, &v_full[st]);
+          tma_load_4d(b + 2 * KV_SUB, &tmVl, 0, g, slot, zc, &v_full[st]);
+          tma_load_4d(b + 3 * KV_SUB, &tmVl, 32, g, slot, zc, &v_full[st]);
+          if (++st == VG) { st = 0; ph ^= 1; }
+        }
     }
   } else if (warp == 1) {
     // MMA issuer: the whole warp runs the loop on warp-uniform values; one elected
     // lane issues each tcgen05 instruction (see tc::elect_one)
-    constexpr uint32_t idS = tc::idesc_tf32(AQ, AK);                  // S: K-major A and B
-    constexpr uint32_t idO = tc::idesc_tf32(AQ, 64) | (1u << 16);     // O: B (V) MN-major
+    constexpr uint32_t idS = tc::idesc_tf32(AQ, AK);                  // S: K-major A and B, N = 128
+    constexpr uint32_t idO = tc::idesc_tf32(AQ, 64) | (1u << 16);     // O: B (V) MN-major, N = 64
     tc::mbar_wait(q_full, 0);
     tc::fence_after();
     const uint64_t q_desc = tc::desc_k_sw128(tc::smem_u32(sQ));
-    const uint64_t k_desc0 = tc::desc_k_sw128(tc::smem_u32(sK));
+    const uint64_t k_desc = tc::desc_k_sw128(tc::smem_u32(sK));
     const uint64_t v_desc0 = desc_mn_sw128_32b(tc::smem_u32(sV), KV_SUB);
-    // descriptor start addresses are in 16-byte units: constant byte offsets add as (bytes >> 4)
-    auto off = [](uint32_t bytes) { return (uint64_t)(bytes >> 4); };
-    int st = 0;
-    uint32_t ph = 0;
-    uint32_t sph[2] = {0, 0}, pph[2] = {0, 0};
+    auto off = [](uint32_t bytes) { return (uint64_t)(bytes >> 4); };   // descriptor address units
     int vst = 0;
     uint32_t vph = 0;
-    auto issue_pv = [&](int b) {                 // O_b = P_b V_b (P from TMEM) into O partial b%2
-      const int pb = b & 1;
-      tc::mbar_wait(&p_full[pb], pph[pb]);
-      pph[pb] ^= 1;
-      tc::mbar_wait(&v_full[vst], vph);
-      tc::fence_after();
-      const uint32_t ph_t = tmem + T_P + pb * 128, pl_t = ph_t + 64;
-      const uint64_t vd = v_desc0 + off(vst * V_STAGE);
-      const uint32_t dO = tmem + T_O + pb * 64;
+    auto issue_pv = [&](int b) {                 // O_bX = P_bX V_bX for both key halves
 #pragma unroll
-      for (int j = 0; j < AK / 8; ++j) {          // corrections first, hi*hi last (see k_gemm_tc.cu)
-        if (tc::elect_one()) tc::mma_tf32_ts(dO, ph_t + j * 8, vd + off(2 * KV_SUB + j * 1024), idO, j != 0);
-        if (tc::elect_one()) tc::mma_tf32_ts(dO, pl_t + j * 8, vd + off(j * 1024), idO, 1);
-      }
+      for (int x = 0; x < 2; ++x) {
+#ifdef NC_ATT_TIMING
+        long long _pw = clock64();
+#endif
+        tc::mbar_wait(&p_full[x], b & 1);
+        tc::mbar_wait(&v_full[vst], vph);
+#ifdef NC_ATT_TIMING
+        if (lane == 0) atomicAdd(&g_att_clk[4], (unsigned long long)(clock64() - _pw));
+#endif
+        tc::fence_after();
+        const uint32_t ph_t = tmem + T_P + 128 * x, pl_t = ph_t + 64;
+        const uint64_t vd = v_desc0 + off(vst * V_GRAN);
+        const uint32_t dO = tmem + T_O + 64 * x;
 #pragma unroll
-      for (int j = 0; j < AK / 8; ++j)
-        if (tc::elect_one()) tc::mma_tf32_ts(dO, ph_t + j * 8, vd + off(j * 1024), idO, 1);
-      if (tc::elect_one()) {
-        tc::mma_commit(&p_empty[pb]);             // P buffer free + O partial ready
-        tc::mma_commit(&v_empty[vst]);
+        for (int j = 0; j < AH / 8; ++j) {          // corrections first, hi*hi last (see k_gemm_tc.cu)
+          if (tc::elect_one()) tc::mma_tf32_ts(dO, ph_t + j * 8, vd + off(2 * KV_SUB + j * 1024), idO, j != 0);
+          if (tc::elect_one()) tc::mma_tf32_ts(dO, pl_t + j * 8, vd + off(j * 1024), idO, 1);
+        }
+#pragma unroll
+        for (int j = 0; j < AH / 8; ++j)
+          if (tc::elect_one()) tc::mma_tf32_ts(dO, ph_t + j * 8, vd + off(j * 1024), idO, 1);
+        if (tc::elect_one()) {
+          tc::mma_commit(&pv_done[x]);             // P_X buffer free + O_X partial ready
+          tc::mma_commit(&v_empty[vst]);
+        }
+        __syncwarp();
+        if (++vst == VG) { vst = 0; vph ^= 1; }
       }
-      __syncwarp();
-      if (++vst == VST) { vst = 0; vph ^= 1; }
     };
+    const bool tm0 = lane == 0;
     for (int i = 0; i < nkb; ++i) {
-      tc::mbar_wait(&k_full[st], ph);
-      const int sb = i & 1;
-      tc::mbar_wait(&s_empty[sb], sph[sb] ^ 1);
-      sph[sb] ^= 1;
+      AT_BEGIN;
+      tc::mbar_wait(k_full, i & 1);
+      AT_ACC(0, tm0);
+      if (i > 0) tc::mbar_wait(s_empty, (i - 1) & 1);   // both softmax groups read S(i-1)
+      AT_ACC(1, tm0);
       tc::fence_after();
-      const uint64_t kd = k_desc0 + off(st * K_STAGE);
-      const uint32_t dS = tmem + T_S + sb * AK;
 #pragma unroll
       for (int dsub = 0; dsub < 2; ++dsub)     // corrections first, hi*hi last (see k_gemm_tc.cu)
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const uint32_t adv = j * 32;
           if (tc::elect_one())
-            tc::mma_tf32(dS, q_desc + off(dsub * Q_SUB + adv), kd + off((2 + dsub) * KV_SUB + adv), idS,
-                         (dsub | j) != 0);
+            tc::mma_tf32(tmem + T_S, q_desc + off(dsub * Q_SUB + adv), k_desc + off((2 + dsub) * K_SUB + adv),
+                         idS, (dsub | j) != 0);
           if (tc::elect_one())
-            tc::mma_tf32(dS, q_desc + off((2 + dsub) * Q_SUB + adv), kd + off(dsub * KV_SUB + adv), idS, 1);
+            tc::mma_tf32(tmem + T_S, q_desc + off((2 + dsub) * Q_SUB + adv), k_desc + off(dsub * K_SUB + adv), idS,
+                         1);
         }
 #pragma unroll
       for (int dsub = 0; dsub < 2; ++dsub)
@@ -240,165 +253,148 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
         for (int j = 0; j < 4; ++j) {
           const uint32_t adv = j * 32;
           if (tc::elect_one())
-            tc::mma_tf32(dS, q_desc + off(dsub * Q_SUB + adv), kd + off(dsub * KV_SUB + adv), idS, 1);
+            tc::mma_tf32(tmem + T_S, q_desc + off(dsub * Q_SUB + adv), k_desc + off(dsub * K_SUB + adv), idS, 1);
         }
       if (tc::elect_one()) {
-        tc::mma_commit(&s_full[sb]);
-        tc::mma_commit(&k_empty[st]);
+        tc::mma_commit(s_full);
+        tc::mma_commit(k_empty);
       }
       __syncwarp();
+      AT_ACC(2, tm0);   // S issue
       if (i > 0) issue_pv(i - 1);
-      if (++st == KST) { st = 0; ph ^= 1; }
+      AT_ACC(3, tm0);   // PV (incl. its waits)
     }
     issue_pv(nkb - 1);
   } else if (warp >= 4) {
+    const int x = (warp - 4) >> 2;                 // key half of this softmax group
     const int q = warp & 3, r = q * 32 + lane;     // query row of this thread (TMEM lane)
-    const bool valid = r < t.nrows;
     const int j = t.p0 + r;
     float O[64];
 #pragma unroll
     for (int d = 0; d < 64; ++d) O[d] = 0.f;
-    float m = -CUDART_INF_F, l = 0.f;
-    float alpha_hist[2] = {1.f, 1.f};              // alpha of blocks b with b%2 == index
-    uint32_t sph[2] = {0, 0}, pph[2] = {0, 0};
+    float m = -CUDART_INF_F, l = 0.f, alpha_prev = 1.f;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    auto fold_wait = [&](int b) {                  // PV(b) complete: P buffer b%2 free, O partial b%2 ready
-      const int pb = b & 1;
-      tc::mbar_wait(&p_empty[pb], pph[pb]);
-      pph[pb] ^= 1;
-      tc::fence_after();
-    };
-    auto fold_apply = [&](int b) {                 // O <- O * alpha_b + O_b  (fp32 RN promotion)
-      const int pb = b & 1;
+    auto fold = [&](float al) {                    // O <- O * alpha + O_partial  (fp32 RN promotion)
       uint32_t x0[32], x1[32];
-      tc::tmem_ld32(tmem + T_O + pb * 64 + lane_off, x0);
-      tc::tmem_ld32(tmem + T_O + pb * 64 + lane_off + 32, x1);
+      tc::tmem_ld32(tmem + T_O + 64 * x + lane_off, x0);
+      tc::tmem_ld32(tmem + T_O + 64 * x + lane_off + 32, x1);
       tc::tmem_wait_ld();
-      const float al = alpha_hist[pb];
 #pragma unroll
       for (int d = 0; d < 32; ++d) {
         O[d] = __fmaf_rn(O[d], al, __uint_as_float(x0[d]));
         O[32 + d] = __fmaf_rn(O[32 + d], al, __uint_as_float(x1[d]));
       }
     };
-    auto fold = [&](int b) { fold_wait(b); fold_apply(b); };
     // scores in the log2 domain: x = S * (1/8 * log2 e); p = 2^(x - m)
     constexpr float kScale = 0.125f * 1.44269504088896341f;
+    const bool ts0 = threadIdx.x == 128 || threadIdx.x == 256;   // one thread per key half
     for (int i = 0; i < nkb; ++i) {
-      const int sb = i & 1;
-#ifdef NC_ATT_TIMING
-      long long tp = clock64();
-#endif
-      tc::mbar_wait(&s_full[sb], sph[sb]);
-#ifdef NC_ATT_TIMING
-      if (threadIdx.x == 128) { atomicAdd(&g_att_clk[0], (unsigned long long)(clock64() - tp)); atomicAdd(&g_att_clk[7], 1ull); }
-      tp = clock64();
-#endif
-      sph[sb] ^= 1;
-      if (a.debug == 9) {      // diagnostics: handshakes only (no TMEM traffic, no math)
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&s_empty[sb]);
-        if (i >= 2) { const int pb = i & 1; tc::mbar_wait(&p_empty[pb], pph[pb]); pph[pb] ^= 1; }
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&p_full[sb]);
-        continue;
-      }
+      AT_BEGIN;
+      tc::mbar_wait(s_full, i & 1);
+      AT_ACC(5 + 5 * x, ts0);
       tc::fence_after();
       uint32_t sr[2][32];
-      tc::tmem_ld32(tmem + T_S + sb * AK + lane_off, sr[0]);
-      tc::tmem_ld32(tmem + T_S + sb * AK + lane_off + 32, sr[1]);
+      tc::tmem_ld32(tmem + T_S + 64 * x + lane_off, sr[0]);
+      tc::tmem_ld32(tmem + T_S + 64 * x + lane_off + 32, sr[1]);
       tc::tmem_wait_ld();
       tc::fence_before();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&s_empty[sb]);
-      const int key0 = (kb0 + i) * AK;
-      // raw scores; masked keys -> -inf.  Max first on the raw scores (kScale > 0 and RN
-      // rounding is monotone, so max(S) * kScale == max(S * kScale) exactly), as a tree.
-      float x[2][32];
-      if (key0 + AK - 1 <= j) {              // whole block inside the window: no masking
+      if (lane == 0) tc::mbar_arrive(s_empty);
+      const int key0 = (kb0 + i) * AK + AH * x;
+      float xs[2][32];
+      if (key0 + AH - 1 <= j) {              // whole half inside the window: no masking
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh)
 #pragma unroll
-          for (int k = 0; k < 32; ++k) x[hh][k] = __uint_as_float(sr[hh][k]);
+          for (int k = 0; k < 32; ++k) xs[hh][k] = __uint_as_float(sr[hh][k]);
       } else {
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh)
 #pragma unroll
           for (int k = 0; k < 32; ++k)
-            x[hh][k] = key0 + 32 * hh + k <= j ? __uint_as_float(sr[hh][k]) : -CUDART_INF_F;
+            xs[hh][k] = key0 + 32 * hh + k <= j ? __uint_as_float(sr[hh][k]) : -CUDART_INF_F;
       }
-      float t[32];
+      // max on the raw scores (kScale > 0, RN monotone: exact), as a tree
+      float tt[32];
 #pragma unroll
-      for (int k = 0; k < 32; ++k) t[k] = fmaxf(x[0][k], x[1][k]);
+      for (int k = 0; k < 32; ++k) tt[k] = fmaxf(xs[0][k], xs[1][k]);
 #pragma unroll
       for (int w2 = 16; w2 >= 1; w2 >>= 1)
 #pragma unroll
-        for (int k = 0; k < w2; ++k) t[k] = fmaxf(t[k], t[k + w2]);
-      const float mb = __fmul_rn(t[0], kScale);
+        for (int k = 0; k < w2; ++k) tt[k] = fmaxf(tt[k], tt[k + w2]);
+      const float mb = __fmul_rn(tt[0], kScale);
       const float mn = fmaxf(m, mb);
       const float alpha = (mn == -CUDART_INF_F) ? 1.f : tc::ex2(__fsub_rn(m, mn));
-      // p = 2^(S * kScale - m) with one FFMA per score; -inf scores give ex2(-inf) = 0.
-      // (mn == -inf only when every key so far is masked: p = 0 then too.)
       const float nmn = mn == -CUDART_INF_F ? 0.f : -mn;
       float ps4[4] = {0.f, 0.f, 0.f, 0.f};   // 4 independent partial sums (latency), fixed order
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh)
 #pragma unroll
         for (int k = 0; k < 32; ++k) {
-          x[hh][k] = tc::ex2(__fmaf_rn(x[hh][k], kScale, nmn));
-          ps4[k & 3] = __fadd_rn(ps4[k & 3], x[hh][k]);
+          xs[hh][k] = tc::ex2(__fmaf_rn(xs[hh][k], kScale, nmn));   // masked: ex2(-inf) = 0
+          ps4[k & 3] = __fadd_rn(ps4[k & 3], xs[hh][k]);
         }
       const float ps = __fadd_rn(__fadd_rn(ps4[0], ps4[1]), __fadd_rn(ps4[2], ps4[3]));
       l = __fmaf_rn(l, alpha, ps);
       m = mn;
-#ifdef NC_ATT_TIMING
-      if (threadIdx.x == 128) atomicAdd(&g_att_clk[1], (unsigned long long)(clock64() - tp));
-      tp = clock64();
-#endif
-      // P buffer i%2 was last read by PV(i-2): wait for it, store P(i), then fold O
-      // partial i-2 while the stores drain
-      if (i >= 2) fold_wait(i - 2);
-      const uint32_t ph_t = tmem + T_P + sb * 128 + lane_off;
+      // P_X buffer and O_X partial were last used by PV(i-1): wait for it, store P(i),
+      // fold O partial (i-1) while the stores drain
+      AT_ACC(6 + 5 * x, ts0);   // S load + max/exp/sum
+      if (i >= 1) {
+        tc::mbar_wait(&pv_done[x], (i - 1) & 1);
+        tc::fence_after();
+      }
+      AT_ACC(7 + 5 * x, ts0);   // wait PV(i-1)
+      const uint32_t ph_t = tmem + T_P + 128 * x + lane_off;
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
         uint32_t hi[32], lo[32];
 #pragma unroll
         for (int k = 0; k < 32; ++k) {
           float fh, fl;
-          tc::split_tf32(x[hh][k], fh, fl);
+          tc::split_tf32(xs[hh][k], fh, fl);
           hi[k] = __float_as_uint(fh);
           lo[k] = __float_as_uint(fl);
         }
         tc::tmem_st32(ph_t + 32 * hh, hi);
         tc::tmem_st32(ph_t + 64 + 32 * hh, lo);
       }
-#ifdef NC_ATT_TIMING
-      if (threadIdx.x == 128) atomicAdd(&g_att_clk[3], (unsigned long long)(clock64() - tp));
-      tp = clock64();
-#endif
-      if (i >= 2) fold_apply(i - 2);
-      alpha_hist[sb] = alpha;
+      if (i >= 1) fold(alpha_prev);
+      alpha_prev = alpha;
       tc::tmem_wait_st();
       tc::fence_before();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&p_full[sb]);
+      if (lane == 0) tc::mbar_arrive(&p_full[x]);
+      AT_ACC(8 + 5 * x, ts0);   // P store + fold
 #ifdef NC_ATT_TIMING
-      if (threadIdx.x == 128) atomicAdd(&g_att_clk[2], (unsigned long long)(clock64() - tp));
+      if (ts0) atomicAdd(&g_att_clk[9 + 5 * x], 1ull);
 #endif
     }
-    if (a.debug == 9) {
-      for (int b = (nkb >= 2 ? nkb - 2 : 0); b < nkb; ++b) { const int pb = b & 1; tc::mbar_wait(&p_empty[pb], pph[pb]); pph[pb] ^= 1; }
-    } else {
-      if (nkb >= 2) fold(nkb - 2);
-      fold(nkb - 1);
+    tc::mbar_wait(&pv_done[x], (nkb - 1) & 1);
+    tc::fence_after();
+    fold(alpha_prev);
+    // merge the two halves: B hands (m, l, O) to A through shared memory (the K buffer is idle)
+    float *xb = reinterpret_cast<float *>(sK) + (size_t)r * 66;
+    if (x == 1) {
+      xb[0] = m; xb[1] = l;
+#pragma unroll
+      for (int d = 0; d < 64; ++d) xb[2 + d] = O[d];
     }
-    if (valid) {
+    named_bar(1, 256);
+    if (x == 0 && r < t.nrows) {
+      const float mB = xb[0], lB = xb[1];
+      const float mm = fmaxf(m, mB);
+      const float fa = (m == -CUDART_INF_F) ? 0.f : tc::ex2(__fsub_rn(m, mm));
+      const float fb = (mB == -CUDART_INF_F) ? 0.f : tc::ex2(__fsub_rn(mB, mm));
+      const float lt = __fmaf_rn(l, fa, __fmul_rn(lB, fb));
       const size_t ob = (size_t)(t.qrow0 + r) * a.ldo + h * 64;
 #pragma unroll
       for (int d = 0; d < 64; d += 4) {
         float4 hi, lo, v;
-        v.x = __fdiv_rn(O[d], l); v.y = __fdiv_rn(O[d + 1], l);
-        v.z = __fdiv_rn(O[d + 2], l); v.w = __fdiv_rn(O[d + 3], l);
+        v.x = __fdiv_rn(__fmaf_rn(O[d], fa, __fmul_rn(xb[2 + d], fb)), lt);
+        v.y = __fdiv_rn(__fmaf_rn(O[d + 1], fa, __fmul_rn(xb[3 + d], fb)), lt);
+        v.z = __fdiv_rn(__fmaf_rn(O[d + 2], fa, __fmul_rn(xb[4 + d], fb)), lt);
+        v.w = __fdiv_rn(__fmaf_rn(O[d + 3], fa, __fmul_rn(xb[5 + d], fb)), lt);
         tc::split_tf32(v.x, hi.x, lo.x); tc::split_tf32(v.y, hi.y, lo.y);
         tc::split_tf32(v.z, hi.z, lo.z); tc::split_tf32(v.w, hi.w, lo.w);
         *reinterpret_cast<float4 *>(a.o_hi + ob + d) = hi;
@@ -410,31 +406,27 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
   __syncthreads();
   tc::fence_after();
   if (warp == 2) tc::tmem_dealloc(tmem, 512);
-#ifdef NC_ATT_TIMING
-  if (threadIdx.x == 0) { atomicAdd(&g_att_clk[11], (unsigned long long)(clock64() - t_cta)); atomicAdd(&g_att_clk[12], 1ull); }
-#endif
 }
-
-#ifdef NC_ATT_TIMING
-void attn_timing_report() {
-  unsigned long long h[16];
-  cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(h, g_att_clk, sizeof(h));
-  const double nb = (double)(h[7] ? h[7] : 1), nc = (double)(h[12] ? h[12] : 1);
-  fprintf(stderr,
-          "attn timing per block (softmax warp): wait S %.0f | max/exp/sum %.0f | fold+wait_st %.0f (wait %.0f) | "
-          "pwait+split+st %.0f ; MMA thread per block: wait kv %.0f, wait s_empty %.0f, wait p_full %.0f ; per CTA %.0f "
-          "cycles, %.1f blocks\n",
-          h[0] / nb, h[1] / nb, h[2] / nb, h[4] / nb, h[3] / nb, h[9] / nb, h[10] / nb, h[8] / nb, h[11] / nc, nb / nc);
-  cudaMemset(g_att_clk, 0, 0);
-  unsigned long long z[16] = {};
-  cudaMemcpyToSymbol(g_att_clk, z, sizeof(z));
-}
-#else
-void attn_timing_report() {}
-#endif
 
 // ------------------------------------------------------------- host side ---
+void attn_timing_report() {
+#ifdef NC_ATT_TIMING
+  unsigned long long hh[16];
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(hh, g_att_clk, sizeof(hh));
+  const double n = (double)(hh[9] ? hh[9] : 1);
+  fprintf(stderr,
+          "attn per 128-key block (cycles): MMA thread: wait K %.0f | wait s_empty %.0f | S issue %.0f | PV incl "
+          "waits %.0f (p_full/V waits %.0f)\n  softmax A: wait S %.0f | ld+max/exp/sum %.0f | wait PV %.0f | "
+          "store+fold %.0f\n  softmax B: wait S %.0f | ld+max/exp/sum %.0f | wait PV %.0f | store+fold %.0f  "
+          "(blocks %.0f)\n",
+          hh[0] / n, hh[1] / n, hh[2] / n, hh[3] / n, hh[4] / n, hh[5] / n, hh[6] / n, hh[7] / n, hh[8] / n,
+          hh[10] / n, hh[11] / n, hh[12] / n, hh[13] / n, n);
+  unsigned long long z[16] = {};
+  cudaMemcpyToSymbol(g_att_clk, z, sizeof(z));
+#endif
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn2() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -497,7 +489,7 @@ void launch_attention_tc(const AttnTcArgs &a, cudaStream_t s) {
   const uint64_t qd[2] = {(uint64_t)a.ldq, (uint64_t)a.q_rows};
   const uint32_t qb[2] = {32, AQ};
   const uint64_t kd[4] = {64, (uint64_t)a.KV, (uint64_t)a.ring, (uint64_t)a.n_chunks * a.n_layers};
-  const uint32_t kbx[4] = {32, 1, AK, 1};
+  const uint32_t kbx[4] = {32, 1, AH, 1};   // 64-key granules (a 128-key K block is two)
   const CUtensorMap *qh = tmap_nd(a.q_hi, 2, qd, qb), *ql = tmap_nd(a.q_lo, 2, qd, qb);
   const CUtensorMap *kh = tmap_nd(a.k_hi, 4, kd, kbx), *kl = tmap_nd(a.k_lo, 4, kd, kbx);
   const CUtensorMap *vh = tmap_nd(a.v_hi, 4, kd, kbx, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);

@@ -138,14 +138,76 @@ __device__ __forceinline__ void store_rows32(float *stg, const float *v, float *
   __syncwarp();
 }
 
+// One 64-column head (q, k or v) of this warp's 32 rows: both 32-column halves
+// go through the swizzled tile so every lane holds the rotate-half pairs
+// (d, d + 32) of 4 rows x 4 columns; RoPE then reads each row's cos/sin as
+// row-contiguous float4s (per-lane scalar table reads were 64 uncoalesced loads
+// per head and dominated the QKV GEMM).  Same per-element arithmetic as before:
+//   y1 = fma(x1, c, -x2 s),  y2 = fma(x2, c, x1 s).
+// PLANES: d0/d1 = tf32 hi/lo destinations of the row; else d0 = fp32 destination.
+template <bool PLANES>
+__device__ __forceinline__ void store_head64(float *stg, const float *x, int pos, bool rope, const float *cos_t,
+                                             const float *sin_t, float *d0, float *d1, int lane) {
+  const int c4 = lane & 7;
+  float4 t[2][8];
+#pragma unroll
+  for (int hf = 0; hf < 2; ++hf) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      *reinterpret_cast<float4 *>(stg + lane * 32 + 4 * (k ^ (lane & 7))) =
+          make_float4(x[32 * hf + 4 * k], x[32 * hf + 4 * k + 1], x[32 * hf + 4 * k + 2], x[32 * hf + 4 * k + 3]);
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int r = 4 * i + (lane >> 3);
+      t[hf][i] = *reinterpret_cast<const float4 *>(stg + r * 32 + 4 * (c4 ^ (r & 7)));
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = 4 * i + (lane >> 3);
+    const int pr = __shfl_sync(0xffffffffu, pos, r);
+    float *p0 = reinterpret_cast<float *>(__shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(d0), r));
+    float *p1 = PLANES ? reinterpret_cast<float *>(
+                             __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(d1), r))
+                       : nullptr;
+    if (pr < 0 || !p0) continue;
+    float4 y1 = t[0][i], y2 = t[1][i];
+    if (rope) {
+      const float4 c = *reinterpret_cast<const float4 *>(cos_t + (size_t)pr * 32 + 4 * c4);
+      const float4 sn = *reinterpret_cast<const float4 *>(sin_t + (size_t)pr * 32 + 4 * c4);
+      const float4 x1 = y1, x2 = y2;
+      y1.x = __fmaf_rn(x1.x, c.x, __fmul_rn(-x2.x, sn.x)); y2.x = __fmaf_rn(x2.x, c.x, __fmul_rn(x1.x, sn.x));
+      y1.y = __fmaf_rn(x1.y, c.y, __fmul_rn(-x2.y, sn.y)); y2.y = __fmaf_rn(x2.y, c.y, __fmul_rn(x1.y, sn.y));
+      y1.z = __fmaf_rn(x1.z, c.z, __fmul_rn(-x2.z, sn.z)); y2.z = __fmaf_rn(x2.z, c.z, __fmul_rn(x1.z, sn.z));
+      y1.w = __fmaf_rn(x1.w, c.w, __fmul_rn(-x2.w, sn.w)); y2.w = __fmaf_rn(x2.w, c.w, __fmul_rn(x1.w, sn.w));
+    }
+    if (PLANES) {
+      float4 h1, l1, h2, l2;
+      tc::split_tf32(y1.x, h1.x, l1.x); tc::split_tf32(y1.y, h1.y, l1.y);
+      tc::split_tf32(y1.z, h1.z, l1.z); tc::split_tf32(y1.w, h1.w, l1.w);
+      tc::split_tf32(y2.x, h2.x, l2.x); tc::split_tf32(y2.y, h2.y, l2.y);
+      tc::split_tf32(y2.z, h2.z, l2.z); tc::split_tf32(y2.w, h2.w, l2.w);
+      *reinterpret_cast<float4 *>(p0 + 4 * c4) = h1;
+      *reinterpret_cast<float4 *>(p1 + 4 * c4) = l1;
+      *reinterpret_cast<float4 *>(p0 + 32 + 4 * c4) = h2;
+      *reinterpret_cast<float4 *>(p1 + 32 + 4 * c4) = l2;
+    } else {
+      *reinterpret_cast<float4 *>(p0 + 4 * c4) = y1;
+      *reinterpret_cast<float4 *>(p0 + 32 + 4 * c4) = y2;
+    }
+  }
+}
+
 #ifdef NC_GEMM_TIMING
 // diagnostics build only: epilogue phase cycle sums of warp 0 lane 0 (per tile)
-__device__ unsigned long long g_gemm_clk[8];
+__device__ unsigned long long g_gemm_clk[4 * 8];   // [EPI][phase]
 #define GEMM_MARK(k)                                                                        \
   do {                                                                                      \
     if (threadIdx.x == 0) {                                                                 \
       const long long _n = clock64();                                                       \
-      atomicAdd(&g_gemm_clk[k], (unsigned long long)(_n - _gt));                            \
+      atomicAdd(&g_gemm_clk[EPI * 8 + (k)], (unsigned long long)(_n - _gt));                 \
       _gt = _n;                                                                             \
     }                                                                                       \
   } while (0)
@@ -321,7 +383,7 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
       if (lane == 0) tc::mbar_arrive_remote(sch_empty_leader + slot * 8);
       if (t < 0) break;
 #ifdef NC_GEMM_TIMING
-      if (threadIdx.x == 0) atomicAdd(&g_gemm_clk[7], 1ull);
+      if (threadIdx.x == 0) atomicAdd(&g_gemm_clk[EPI * 8 + 7], 1ull);
 #endif
       int mb, nb;
       tile_mn(t, mb, nb);
@@ -393,7 +455,8 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
               const float g = x[j], up = x[32 + j];
-              const float sg = __fdiv_rn(g, __fadd_rn(1.f, expf(-g)));
+              // silu(g) = g / (1 + e^-g) on the SFU (ex2, fast divide): ~2 ulp, same code in prefill and decode
+              const float sg = __fdividef(g, __fadd_rn(1.f, tc::ex2(__fmul_rn(g, -1.44269504088896341f))));
               x[j] = __fmul_rn(sg, up);
             }
             const size_t o = (size_t)m * a.ldc + cb / 2;
@@ -401,16 +464,7 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
           } else {  // EPI_QKV
             const int pos = row_ok ? a.rows.pos[m] : -1;
             const int nq = a.n_q_cols, nkv = a.n_kv_cols;
-            if (pos >= 0 && cb < nq + nkv) {   // q or k head: RoPE on the rotate-half pairs (d, d+32)
-              const float *cs = a.rope_cos + (size_t)pos * 32;
-              const float *sn = a.rope_sin + (size_t)pos * 32;
-#pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                const float c = cs[j], s = sn[j], x1 = x[j], x2 = x[j + 32];
-                x[j] = __fmaf_rn(x1, c, __fmul_rn(-x2, s));
-                x[j + 32] = __fmaf_rn(x2, c, __fmul_rn(x1, s));
-              }
-            }
+            const bool rope = cb < nq + nkv;   // q or k head (warp-uniform): RoPE on the rotate-half pairs
             size_t o = 0;
             bool ring = false, isk = false;
             if (cb < nq) {
@@ -424,12 +478,10 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
             if (a.planes) {
               float *dh = pos < 0 ? nullptr : (ring ? (isk ? a.ring.k_hi : a.ring.v_hi) : a.C_hi) + o;
               float *dl = pos < 0 ? nullptr : (ring ? (isk ? a.ring.k_lo : a.ring.v_lo) : a.C_lo) + o;
-              store_rows32<ST_SPLIT>(stg, x, dh, dl, nullptr, lane);
-              store_rows32<ST_SPLIT>(stg, x + 32, dh ? dh + 32 : nullptr, dl ? dl + 32 : nullptr, nullptr, lane);
+              store_head64<true>(stg, x, pos, rope, a.rope_cos, a.rope_sin, dh, dl, lane);
             } else {
               float *dst = pos < 0 ? nullptr : (ring ? (isk ? a.ring.k : a.ring.v) : a.C) + o;
-              store_rows32<ST_PLAIN>(stg, x, dst, nullptr, nullptr, lane);
-              store_rows32<ST_PLAIN>(stg, x + 32, dst ? dst + 32 : nullptr, nullptr, nullptr, lane);
+              store_head64<false>(stg, x, pos, rope, a.rope_cos, a.rope_sin, dst, nullptr, lane);
             }
           }
         }
@@ -549,15 +601,20 @@ static void launch_tc(const TcGemmArgs &a, const TcOperands &op, cudaStream_t s)
 
 void gemm_timing_report() {
 #ifdef NC_GEMM_TIMING
-  unsigned long long h[8];
+  unsigned long long h[32];
   cudaDeviceSynchronize();
   cudaMemcpyFromSymbol(h, g_gemm_clk, sizeof(h));
-  const double n = (double)(h[7] ? h[7] : 1);
-  fprintf(stderr,
-          "gemm epilogue warp per tile (cycles): wait tile %.0f | residual seed %.0f | wait partials %.0f | "
-          "drain %.0f | output %.0f | tiles %.0f\n",
-          h[0] / n, h[1] / n, h[2] / n, h[3] / n, h[4] / n, n);
-  unsigned long long z[8] = {};
+  const char *nm[4] = {"qkv", "resid", "swiglu", "head"};
+  for (int e = 0; e < 4; ++e) {
+    const unsigned long long *x = h + 8 * e;
+    const double n = (double)(x[7] ? x[7] : 1);
+    if (x[7])
+      fprintf(stderr,
+              "gemm %-6s epilogue warp per tile (cycles): wait tile %.0f | residual prefetch %.0f | wait partials "
+              "%.0f | drain %.0f | output %.0f | tiles %.0f\n",
+              nm[e], x[0] / n, x[1] / n, x[2] / n, x[3] / n, x[4] / n, n);
+  }
+  unsigned long long z[32] = {};
   cudaMemcpyToSymbol(g_gemm_clk, z, sizeof(z));
 #endif
 }
