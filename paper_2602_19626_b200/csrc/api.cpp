@@ -1,5 +1,7 @@
 // extern "C" boundary of libnc.so (include/nc.h).  Argument marshalling,
 // error capture and container plumbing only; all compute is in the engine.
+#include <cstdio>
+#include <chrono>
 #include <cuda_runtime.h>
 
 #include <cstdlib>
@@ -149,11 +151,19 @@ nc_status nc_compress_tokens(nc_model *m, const uint32_t *tokens_dev, const uint
     nc::Params q = nc::validate(p);
     std::vector<uint32_t> ntok(chunk_ntok, chunk_ntok + n_chunks);
     nc::CompressOut co;
+    const auto t0 = std::chrono::steady_clock::now();
     nc::compress_device(m, tokens_dev, ntok, q, (cudaStream_t)cuda_stream, co);
+    const auto t1 = std::chrono::steady_clock::now();
     std::vector<uint8_t> blob;
     nc::encode_container(q, ntok, co, blob);
     *out = dup_out(blob);
     *out_n = blob.size();
+    if (std::getenv("NC_TIMELINE")) {
+      const auto t2 = std::chrono::steady_clock::now();
+      fprintf(stderr, "host: compress_device %.2f ms, range coder + container %.2f ms\n",
+              std::chrono::duration<double, std::milli>(t1 - t0).count(),
+              std::chrono::duration<double, std::milli>(t2 - t1).count());
+    }
   });
 }
 

@@ -1,6 +1,7 @@
 // Engine: model upload, the slabbed prefill + walk driver (compress), the
 // one-row-per-chunk decode-step driver (decompress), host WNC + NC05 assembly.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -516,6 +517,7 @@ struct WalkBufs {
 // --------------------------------------------------------------- compress ---
 void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<uint32_t> &ntok,
                      const Params &p, cudaStream_t s, CompressOut &out) {
+  const auto t_entry = std::chrono::steady_clock::now();
   NC_CUDA(cudaSetDevice(m->device));
   const Shape &S = m->s;
   const int n_chunks = (int)ntok.size();
@@ -630,6 +632,7 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
   for (auto &e : ev) NC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDefault));
   cudaEvent_t ev_init = ev[5 * n_slabs];
   NC_CUDA(cudaEventRecord(ev_init, s));
+  const auto t_setup = std::chrono::steady_clock::now();
   NC_CUDA(cudaStreamWaitEvent(ns, ev_init, 0));
   NC_CUDA(cudaStreamWaitEvent(ws, ev_init, 0));
   // the walk keeps one SM per chunk busy for a whole slab: leave those SMs out of
@@ -700,6 +703,20 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
     cudaEventElapsedTime(&b, ev[4 * sl + 2], ev[4 * sl + 3]);
     st.forward_ms += a;
     st.walk_ms += b;
+  }
+  if (std::getenv("NC_TIMELINE")) {   // diagnostics: stream timeline of this compression (ms from the start)
+    fprintf(stderr, "host: setup before the first launch %.2f ms, launch..sync %.2f ms\n",
+            std::chrono::duration<double, std::milli>(t_setup - t_entry).count(),
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_setup).count());
+    auto at = [&](cudaEvent_t e) {
+      float t = 0;
+      cudaEventElapsedTime(&t, ev_init, e);
+      return t;
+    };
+    for (int sl = 0; sl < n_slabs; ++sl)
+      fprintf(stderr, "slab %d (%d positions): forward %.2f-%.2f  ngram done %.2f  walk %.2f-%.2f\n", sl,
+              slab_len[sl], at(ev[4 * sl]), at(ev[4 * sl + 1]), use_ng ? at(ev[4 * n_slabs + sl]) : 0.f,
+              at(ev[4 * sl + 2]), at(ev[4 * sl + 3]));
   }
   for (auto &e : ev) cudaEventDestroy(e);
 }

@@ -27,6 +27,7 @@
 // every reduction has a fixed tree, so the decoder reproduces the encoder's
 // counts bit for bit (D15).
 #include <cstdio>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 #include <cuda_runtime.h>
@@ -1066,7 +1067,14 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
 
 // Cluster size used for a vocabulary: fixed per V (never per batch), so that the
 // reduction trees of compression and decompression are the same.
-static int walk_cluster_size(uint32_t V) { return (V >= 4096 && V % 64 == 0) ? 4 : 1; }
+static int walk_cluster_size(uint32_t V) {
+  static const int forced = [] {   // diagnostics: NC_WALK_CS=4|8 (compress and decompress must agree)
+    const char *e = std::getenv("NC_WALK_CS");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (V < 4096 || V % 64) return 1;
+  return forced == 8 ? 8 : 4;
+}
 
 template <int CS>
 static void launch_walk_cs(const WalkArgs &a, cudaStream_t s) {
@@ -1113,7 +1121,9 @@ void walk_timing_report() {
 
 void launch_walk(const WalkArgs &a, cudaStream_t s) {
   if (a.n_entries <= 0) return;
-  if (walk_cluster_size(a.V) == 4) launch_walk_cs<4>(a, s);
+  const int cs = walk_cluster_size(a.V);
+  if (cs == 8) launch_walk_cs<8>(a, s);
+  else if (cs == 4) launch_walk_cs<4>(a, s);
   else launch_walk_cs<1>(a, s);
 }
 
