@@ -13,7 +13,8 @@ struct AttnTcArgs {
   int ring, n_chunks, n_layers, layer;
   float *o_hi, *o_lo; int ldo;               // output tf32 planes [rows, H*64]
   int H, KV, window, slide;
-  int debug;                                 // test only: dump S/l/m/O-partial of block 0
+  int debug;                                 // unused
+  int *item_ctr;                             // set by the launcher (persistent item scheduler)
 };
 
 void launch_attention_tc(const AttnTcArgs &a, cudaStream_t s);

@@ -614,6 +614,10 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
       int cnt = std::min<int>(len, (int)ntok[c] - q0);
       if (cnt > 0) { w_chunk.push_back(c); w_row0.push_back(c * len); w_count.push_back(cnt); }
     }
+    // the persistent attention kernel claims tiles in list order: heaviest (latest positions,
+    // most keys) first so the last claims are short
+    std::stable_sort(tiles.begin() + tile_off[sl], tiles.end(),
+                     [](const AttnTile &x, const AttnTile &y) { return x.p0 > y.p0; });
   }
   tile_off[n_slabs] = (int)tiles.size();
   w_off[n_slabs] = (int)w_chunk.size();

@@ -102,6 +102,9 @@ __device__ __forceinline__ void named_bar(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
+constexpr int NSCH = 2;          // item schedule ring
+constexpr int SCH_CONSUMERS = 10;  // V producer, MMA warp, 8 softmax warps
+
 __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_constant__ CUtensorMap tmQh,
                                                                 const __grid_constant__ CUtensorMap tmQl,
                                                                 const __grid_constant__ CUtensorMap tmKh,
@@ -115,28 +118,25 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
   uint8_t *sK = smem + Q_BYTES;                        // same, 128 keys each (granule g at +8 KB g)
   uint8_t *sV = sK + K_BYTES;                          // VG granules: [Vh0][Vh1][Vl0][Vl1], 64 keys each
   uint64_t *bars = reinterpret_cast<uint64_t *>(sV + VG * V_GRAN);
-  uint64_t *q_full = bars, *k_full = bars + 1, *k_empty = bars + 2;
-  uint64_t *v_full = bars + 3, *v_empty = v_full + VG;
+  uint64_t *q_full = bars, *q_empty = bars + 1, *k_full = bars + 2, *k_empty = bars + 3;
+  uint64_t *v_full = bars + 4, *v_empty = v_full + VG;
   uint64_t *s_full = v_empty + VG, *s_empty = s_full + 1;
   uint64_t *p_full = s_empty + 1, *pv_done = p_full + 2;   // per key half
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(pv_done + 2);
+  uint64_t *sch_full = pv_done + 2, *sch_empty = sch_full + NSCH;
+  int *sch_item = reinterpret_cast<int *>(sch_empty + NSCH);
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sch_item + NSCH);
 
-  const AttnTile t = a.tiles[blockIdx.x];
-  if (t.nrows <= 0) return;                        // inactive chunk in a decode step
-  const int h = blockIdx.y, g = h / (a.H / a.KV);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int w = wstart(t.p0, a.window, a.slide);
-  const int kb0 = w / AK, kb1 = (t.p0 + t.nrows - 1) / AK;
-  const int nkb = kb1 - kb0 + 1;
-  const int zc = t.chunk * a.n_layers + a.layer;   // (chunk, layer) coordinate of the ring maps
+  const int n_items = a.n_tiles * a.H;
 
   if (threadIdx.x == 0) {
     tc::tma_prefetch(&tmQh); tc::tma_prefetch(&tmKh); tc::tma_prefetch(&tmVh);
-    tc::mbar_init(q_full, 1);
+    tc::mbar_init(q_full, 1); tc::mbar_init(q_empty, 1);
     tc::mbar_init(k_full, 1); tc::mbar_init(k_empty, 1);
     for (int s = 0; s < VG; ++s) { tc::mbar_init(&v_full[s], 1); tc::mbar_init(&v_empty[s], 1); }
     tc::mbar_init(s_full, 1); tc::mbar_init(s_empty, 8);
     for (int s = 0; s < 2; ++s) { tc::mbar_init(&p_full[s], 4); tc::mbar_init(&pv_done[s], 1); }
+    for (int s = 0; s < NSCH; ++s) { tc::mbar_init(&sch_full[s], 1); tc::mbar_init(&sch_empty[s], SCH_CONSUMERS); }
     tc::fence_barrier_init();
   }
   if (warp == 2) tc::tmem_alloc(tmem_slot, 512);
@@ -145,68 +145,104 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  // item -> (tile, head, geometry); every role derives the same numbers
+  struct Item { AttnTile t; int h, g, kb0, nkb, zc; };
+  auto item_of = [&](int it) {
+    Item x;
+    x.t = a.tiles[it / a.H];
+    x.h = it % a.H;
+    x.g = x.h / (a.H / a.KV);
+    const int w = wstart(x.t.p0, a.window, a.slide);
+    x.kb0 = w / AK;
+    x.nkb = x.t.nrows > 0 ? (x.t.p0 + x.t.nrows - 1) / AK - x.kb0 + 1 : 0;   // 0: inactive decode chunk
+    x.zc = x.t.chunk * a.n_layers + a.layer;
+    return x;
+  };
+  // consumers: next claimed item from the schedule ring (-1 = done)
+  auto next_item = [&](int jt, bool arrive) {
+    const int slot = jt % NSCH;
+    tc::mbar_wait(&sch_full[slot], (jt / NSCH) & 1);
+    const int it = sch_item[slot];
+    __syncwarp();
+    if (arrive) tc::mbar_arrive(&sch_empty[slot]);
+    return it;
+  };
+
   if (warp == 0) {
+    // ---------------------------------------------- scheduler + Q/K producer
     if (lane == 0) {
-      tc::mbar_expect_tx(q_full, Q_BYTES);
-      tc::tma_load_2d(sQ, &tmQh, h * 64, t.qrow0, q_full);
-      tc::tma_load_2d(sQ + Q_SUB, &tmQh, h * 64 + 32, t.qrow0, q_full);
-      tc::tma_load_2d(sQ + 2 * Q_SUB, &tmQl, h * 64, t.qrow0, q_full);
-      tc::tma_load_2d(sQ + 3 * Q_SUB, &tmQl, h * 64 + 32, t.qrow0, q_full);
-      for (int i = 0; i < nkb; ++i) {
-        tc::mbar_wait(k_empty, (i & 1) ^ 1);
-        const int slot = ((kb0 + i) * AK) % a.ring;  // ring is a multiple of 128: no wrap inside a block
-        tc::mbar_expect_tx(k_full, K_BYTES);
+      int gb = 0, qi = 0;
+      for (int jt = 0;; ++jt) {
+        const int slot = jt % NSCH;
+        tc::mbar_wait(&sch_empty[slot], ((jt / NSCH) & 1) ^ 1);
+        const int claimed = atomicAdd(a.item_ctr, 1);
+        const int it = claimed < n_items ? claimed : -1;
+        sch_item[slot] = it;
+        tc::mbar_arrive(&sch_full[slot]);
+        if (it < 0) break;
+        const Item x = item_of(it);
+        if (x.nkb == 0) continue;
+        tc::mbar_wait(q_empty, (qi & 1) ^ 1);           // all S MMAs of the previous item done
+        tc::mbar_expect_tx(q_full, Q_BYTES);
+        tc::tma_load_2d(sQ, &tmQh, x.h * 64, x.t.qrow0, q_full);
+        tc::tma_load_2d(sQ + Q_SUB, &tmQh, x.h * 64 + 32, x.t.qrow0, q_full);
+        tc::tma_load_2d(sQ + 2 * Q_SUB, &tmQl, x.h * 64, x.t.qrow0, q_full);
+        tc::tma_load_2d(sQ + 3 * Q_SUB, &tmQl, x.h * 64 + 32, x.t.qrow0, q_full);
+        ++qi;
+        for (int i = 0; i < x.nkb; ++i, ++gb) {
+          tc::mbar_wait(k_empty, (gb & 1) ^ 1);
+          const int slot_k = ((x.kb0 + i) * AK) % a.ring;   // ring is a multiple of 128: no wrap inside a block
+          tc::mbar_expect_tx(k_full, K_BYTES);
 #pragma unroll
-        for (int gg = 0; gg < 2; ++gg) {
-          tma_load_4d(sK + 0 * K_SUB + gg * KV_SUB, &tmKh, 0, g, slot + gg * AH, zc, k_full);
-          tma_load_4d(sK + 1 * K_SUB + gg * KV_SUB, &tmKh, 32, g, slot + gg * AH, zc, k_full);
-          tma_load_4d(sK + 2 * K_SUB + gg * KV_SUB, &tmKl, 0, g, slot + gg * AH, zc, k_full);
-          tma_load_4d(sK + 3 * K_SUB + gg * KV_SUB, &tmKl, 32, g, slot + gg * AH, zc, k_full);
+          for (int gg = 0; gg < 2; ++gg) {
+            tma_load_4d(sK + 0 * K_SUB + gg * KV_SUB, &tmKh, 0, x.g, slot_k + gg * AH, x.zc, k_full);
+            tma_load_4d(sK + 1 * K_SUB + gg * KV_SUB, &tmKh, 32, x.g, slot_k + gg * AH, x.zc, k_full);
+            tma_load_4d(sK + 2 * K_SUB + gg * KV_SUB, &tmKl, 0, x.g, slot_k + gg * AH, x.zc, k_full);
+            tma_load_4d(sK + 3 * K_SUB + gg * KV_SUB, &tmKl, 32, x.g, slot_k + gg * AH, x.zc, k_full);
+          }
         }
       }
     }
   } else if (warp == 3) {
-    if (lane == 0) {
-      int st = 0;
-      uint32_t ph = 0;
-      for (int i = 0; i < nkb; ++i)
+    // ---------------------------------------------------------- V producer
+    int st = 0;
+    uint32_t ph = 0;
+    for (int jt = 0;; ++jt) {
+      const int it = next_item(jt, lane == 0);
+      if (it < 0) break;
+      const Item x = item_of(it);
+      if (lane == 0)
+        for (int i = 0; i < x.nkb; ++i)
 #pragma unroll
-        for (int gg = 0; gg < 2; ++gg) {
-          tc::mbar_wait(&v_empty[st], ph ^ 1);
-          uint8_t *b = sV + st * V_GRAN;
-          const int slot = ((kb0 + i) * AK) % a.ring + gg * AH;
-          tc::mbar_expect_tx(&v_full[st], V_GRAN);
-          tma_load_4d(b + 0 * KV_SUB, &tmVh, 0, g, slot, zc, &v_full[st]);
-          tma_load_4d(b + 1 * KV_SUB, &tmVh, 32, g, slot, zc, &v_full[st]);
-          tma_load_4d(b + 2 * KV_SUB, &tmVl, 0, g, slot, zc, &v_full[st]);
-          tma_load_4d(b + 3 * KV_SUB, &tmVl, 32, g, slot, zc, &v_full[st]);
-          if (++st == VG) { st = 0; ph ^= 1; }
-        }
+          for (int gg = 0; gg < 2; ++gg) {
+            tc::mbar_wait(&v_empty[st], ph ^ 1);
+            uint8_t *b = sV + st * V_GRAN;
+            const int slot = ((x.kb0 + i) * AK) % a.ring + gg * AH;
+            tc::mbar_expect_tx(&v_full[st], V_GRAN);
+            tma_load_4d(b + 0 * KV_SUB, &tmVh, 0, x.g, slot, x.zc, &v_full[st]);
+            tma_load_4d(b + 1 * KV_SUB, &tmVh, 32, x.g, slot, x.zc, &v_full[st]);
+            tma_load_4d(b + 2 * KV_SUB, &tmVl, 0, x.g, slot, x.zc, &v_full[st]);
+            tma_load_4d(b + 3 * KV_SUB, &tmVl, 32, x.g, slot, x.zc, &v_full[st]);
+            if (++st == VG) { st = 0; ph ^= 1; }
+          }
+      __syncwarp();
     }
   } else if (warp == 1) {
     // MMA issuer: the whole warp runs the loop on warp-uniform values; one elected
     // lane issues each tcgen05 instruction (see tc::elect_one)
     constexpr uint32_t idS = tc::idesc_tf32(AQ, AK);                  // S: K-major A and B, N = 128
     constexpr uint32_t idO = tc::idesc_tf32(AQ, 64) | (1u << 16);     // O: B (V) MN-major, N = 64
-    tc::mbar_wait(q_full, 0);
-    tc::fence_after();
     const uint64_t q_desc = tc::desc_k_sw128(tc::smem_u32(sQ));
     const uint64_t k_desc = tc::desc_k_sw128(tc::smem_u32(sK));
     const uint64_t v_desc0 = desc_mn_sw128_32b(tc::smem_u32(sV), KV_SUB);
     auto off = [](uint32_t bytes) { return (uint64_t)(bytes >> 4); };   // descriptor address units
     int vst = 0;
     uint32_t vph = 0;
-    auto issue_pv = [&](int b) {                 // O_bX = P_bX V_bX for both key halves
+    auto issue_pv = [&](int b) {                 // O_bX = P_bX V_bX for both key halves (b: global block)
 #pragma unroll
       for (int x = 0; x < 2; ++x) {
-#ifdef NC_ATT_TIMING
-        long long _pw = clock64();
-#endif
         tc::mbar_wait(&p_full[x], b & 1);
         tc::mbar_wait(&v_full[vst], vph);
-#ifdef NC_ATT_TIMING
-        if (lane == 0) atomicAdd(&g_att_clk[4], (unsigned long long)(clock64() - _pw));
-#endif
         tc::fence_after();
         const uint32_t ph_t = tmem + T_P + 128 * x, pl_t = ph_t + 64;
         const uint64_t vd = v_desc0 + off(vst * V_GRAN);
@@ -227,178 +263,207 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
         if (++vst == VG) { vst = 0; vph ^= 1; }
       }
     };
-    const bool tm0 = lane == 0;
-    for (int i = 0; i < nkb; ++i) {
-      AT_BEGIN;
-      tc::mbar_wait(k_full, i & 1);
-      AT_ACC(0, tm0);
-      if (i > 0) tc::mbar_wait(s_empty, (i - 1) & 1);   // both softmax groups read S(i-1)
-      AT_ACC(1, tm0);
-      tc::fence_after();
+    int gb = 0, qi = 0;
+    for (int jt = 0;; ++jt) {
+      const int it = next_item(jt, lane == 0);
+      if (it < 0) break;
+      const Item x = item_of(it);
+      if (x.nkb == 0) continue;
+      tc::mbar_wait(q_full, qi & 1);
+      for (int i = 0; i < x.nkb; ++i, ++gb) {
+        tc::mbar_wait(k_full, gb & 1);
+        if (gb > 0) tc::mbar_wait(s_empty, (gb - 1) & 1);   // both softmax groups read S(gb-1)
+        tc::fence_after();
 #pragma unroll
-      for (int dsub = 0; dsub < 2; ++dsub)     // corrections first, hi*hi last (see k_gemm_tc.cu)
+        for (int dsub = 0; dsub < 2; ++dsub)     // corrections first, hi*hi last (see k_gemm_tc.cu)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const uint32_t adv = j * 32;
-          if (tc::elect_one())
-            tc::mma_tf32(tmem + T_S, q_desc + off(dsub * Q_SUB + adv), k_desc + off((2 + dsub) * K_SUB + adv),
-                         idS, (dsub | j) != 0);
-          if (tc::elect_one())
-            tc::mma_tf32(tmem + T_S, q_desc + off((2 + dsub) * Q_SUB + adv), k_desc + off(dsub * K_SUB + adv), idS,
-                         1);
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t adv = j * 32;
+            if (tc::elect_one())
+              tc::mma_tf32(tmem + T_S, q_desc + off(dsub * Q_SUB + adv), k_desc + off((2 + dsub) * K_SUB + adv),
+                           idS, (dsub | j) != 0);
+            if (tc::elect_one())
+              tc::mma_tf32(tmem + T_S, q_desc + off((2 + dsub) * Q_SUB + adv), k_desc + off(dsub * K_SUB + adv),
+                           idS, 1);
+          }
+#pragma unroll
+        for (int dsub = 0; dsub < 2; ++dsub)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t adv = j * 32;
+            if (tc::elect_one())
+              tc::mma_tf32(tmem + T_S, q_desc + off(dsub * Q_SUB + adv), k_desc + off(dsub * K_SUB + adv), idS, 1);
+          }
+        if (tc::elect_one()) {
+          tc::mma_commit(s_full);
+          tc::mma_commit(k_empty);
+          if (i == x.nkb - 1) tc::mma_commit(q_empty);   // Q buffer free for the next item
         }
-#pragma unroll
-      for (int dsub = 0; dsub < 2; ++dsub)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const uint32_t adv = j * 32;
-          if (tc::elect_one())
-            tc::mma_tf32(tmem + T_S, q_desc + off(dsub * Q_SUB + adv), k_desc + off(dsub * K_SUB + adv), idS, 1);
-        }
-      if (tc::elect_one()) {
-        tc::mma_commit(s_full);
-        tc::mma_commit(k_empty);
+        __syncwarp();
+        if (i > 0) issue_pv(gb - 1);
       }
-      __syncwarp();
-      AT_ACC(2, tm0);   // S issue
-      if (i > 0) issue_pv(i - 1);
-      AT_ACC(3, tm0);   // PV (incl. its waits)
+      issue_pv(gb - 1);                           // the item's last block, before the next item's S
+      ++qi;
     }
-    issue_pv(nkb - 1);
   } else if (warp >= 4) {
+    // ------------------------------------------- softmax groups (key halves)
     const int x = (warp - 4) >> 2;                 // key half of this softmax group
     const int q = warp & 3, r = q * 32 + lane;     // query row of this thread (TMEM lane)
-    const int j = t.p0 + r;
-    float O[64];
-#pragma unroll
-    for (int d = 0; d < 64; ++d) O[d] = 0.f;
-    float m = -CUDART_INF_F, l = 0.f, alpha_prev = 1.f;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    auto fold = [&](float al) {                    // O <- O * alpha + O_partial  (fp32 RN promotion)
-      uint32_t x0[32], x1[32];
-      tc::tmem_ld32(tmem + T_O + 64 * x + lane_off, x0);
-      tc::tmem_ld32(tmem + T_O + 64 * x + lane_off + 32, x1);
-      tc::tmem_wait_ld();
-#pragma unroll
-      for (int d = 0; d < 32; ++d) {
-        O[d] = __fmaf_rn(O[d], al, __uint_as_float(x0[d]));
-        O[32 + d] = __fmaf_rn(O[32 + d], al, __uint_as_float(x1[d]));
-      }
-    };
     // scores in the log2 domain: x = S * (1/8 * log2 e); p = 2^(x - m)
     constexpr float kScale = 0.125f * 1.44269504088896341f;
-    const bool ts0 = threadIdx.x == 128 || threadIdx.x == 256;   // one thread per key half
-    for (int i = 0; i < nkb; ++i) {
-      AT_BEGIN;
-      tc::mbar_wait(s_full, i & 1);
-      AT_ACC(5 + 5 * x, ts0);
-      tc::fence_after();
-      uint32_t sr[2][32];
-      tc::tmem_ld32(tmem + T_S + 64 * x + lane_off, sr[0]);
-      tc::tmem_ld32(tmem + T_S + 64 * x + lane_off + 32, sr[1]);
-      tc::tmem_wait_ld();
-      tc::fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(s_empty);
-      const int key0 = (kb0 + i) * AK + AH * x;
-      float xs[2][32];
-      if (key0 + AH - 1 <= j) {              // whole half inside the window: no masking
+    int gb = 0;
+    for (int jt = 0;; ++jt) {
+      const int it = next_item(jt, lane == 0);
+      if (it < 0) break;
+      const Item xi = item_of(it);
+      if (xi.nkb == 0) continue;
+      const int j = xi.t.p0 + r;
+      float O[64];
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh)
+      for (int d = 0; d < 64; ++d) O[d] = 0.f;
+      float m = -CUDART_INF_F, l = 0.f, alpha_prev = 1.f;
+      auto fold = [&](float al) {                  // O <- O * alpha + O_partial  (fp32 RN promotion)
+        uint32_t x0[32], x1[32];
+        tc::tmem_ld32(tmem + T_O + 64 * x + lane_off, x0);
+        tc::tmem_ld32(tmem + T_O + 64 * x + lane_off + 32, x1);
+        tc::tmem_wait_ld();
 #pragma unroll
-          for (int k = 0; k < 32; ++k) xs[hh][k] = __uint_as_float(sr[hh][k]);
-      } else {
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh)
-#pragma unroll
-          for (int k = 0; k < 32; ++k)
-            xs[hh][k] = key0 + 32 * hh + k <= j ? __uint_as_float(sr[hh][k]) : -CUDART_INF_F;
-      }
-      // max on the raw scores (kScale > 0, RN monotone: exact), as a tree
-      float tt[32];
-#pragma unroll
-      for (int k = 0; k < 32; ++k) tt[k] = fmaxf(xs[0][k], xs[1][k]);
-#pragma unroll
-      for (int w2 = 16; w2 >= 1; w2 >>= 1)
-#pragma unroll
-        for (int k = 0; k < w2; ++k) tt[k] = fmaxf(tt[k], tt[k + w2]);
-      const float mb = __fmul_rn(tt[0], kScale);
-      const float mn = fmaxf(m, mb);
-      const float alpha = (mn == -CUDART_INF_F) ? 1.f : tc::ex2(__fsub_rn(m, mn));
-      const float nmn = mn == -CUDART_INF_F ? 0.f : -mn;
-      float ps4[4] = {0.f, 0.f, 0.f, 0.f};   // 4 independent partial sums (latency), fixed order
-#pragma unroll
-      for (int hh = 0; hh < 2; ++hh)
-#pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          xs[hh][k] = tc::ex2(__fmaf_rn(xs[hh][k], kScale, nmn));   // masked: ex2(-inf) = 0
-          ps4[k & 3] = __fadd_rn(ps4[k & 3], xs[hh][k]);
+        for (int d = 0; d < 32; ++d) {
+          O[d] = __fmaf_rn(O[d], al, __uint_as_float(x0[d]));
+          O[32 + d] = __fmaf_rn(O[32 + d], al, __uint_as_float(x1[d]));
         }
-      const float ps = __fadd_rn(__fadd_rn(ps4[0], ps4[1]), __fadd_rn(ps4[2], ps4[3]));
-      l = __fmaf_rn(l, alpha, ps);
-      m = mn;
-      // P_X buffer and O_X partial were last used by PV(i-1): wait for it, store P(i),
-      // fold O partial (i-1) while the stores drain
-      AT_ACC(6 + 5 * x, ts0);   // S load + max/exp/sum
-      if (i >= 1) {
-        tc::mbar_wait(&pv_done[x], (i - 1) & 1);
+      };
+      for (int i = 0; i < xi.nkb; ++i, ++gb) {
+        tc::mbar_wait(s_full, gb & 1);
         tc::fence_after();
-      }
-      AT_ACC(7 + 5 * x, ts0);   // wait PV(i-1)
-      const uint32_t ph_t = tmem + T_P + 128 * x + lane_off;
+        uint32_t sr[2][32];
+        tc::tmem_ld32(tmem + T_S + 64 * x + lane_off, sr[0]);
+        tc::tmem_ld32(tmem + T_S + 64 * x + lane_off + 32, sr[1]);
+        tc::tmem_wait_ld();
+        tc::fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(s_empty);
+        const int key0 = (xi.kb0 + i) * AK + AH * x;
+        float xs[2][32];
+        if (key0 + AH - 1 <= j) {              // whole half inside the window: no masking
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        uint32_t hi[32], lo[32];
+          for (int hh = 0; hh < 2; ++hh)
 #pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          float fh, fl;
-          tc::split_tf32(xs[hh][k], fh, fl);
-          hi[k] = __float_as_uint(fh);
-          lo[k] = __float_as_uint(fl);
+            for (int k = 0; k < 32; ++k) xs[hh][k] = __uint_as_float(sr[hh][k]);
+        } else {
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+            for (int k = 0; k < 32; ++k)
+              xs[hh][k] = key0 + 32 * hh + k <= j ? __uint_as_float(sr[hh][k]) : -CUDART_INF_F;
         }
-        tc::tmem_st32(ph_t + 32 * hh, hi);
-        tc::tmem_st32(ph_t + 64 + 32 * hh, lo);
+        // max on the raw scores (kScale > 0, RN monotone: exact), as a tree
+        float tt[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) tt[k] = fmaxf(xs[0][k], xs[1][k]);
+#pragma unroll
+        for (int w2 = 16; w2 >= 1; w2 >>= 1)
+#pragma unroll
+          for (int k = 0; k < w2; ++k) tt[k] = fmaxf(tt[k], tt[k + w2]);
+        const float mb = __fmul_rn(tt[0], kScale);
+        const float mn = fmaxf(m, mb);
+        const float alpha = (mn == -CUDART_INF_F) ? 1.f : tc::ex2(__fsub_rn(m, mn));
+        const float nmn = mn == -CUDART_INF_F ? 0.f : -mn;
+        float ps4[4] = {0.f, 0.f, 0.f, 0.f};   // 4 independent partial sums (latency), fixed order
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+          for (int k = 0; k < 32; ++k) {
+            xs[hh][k] = tc::ex2(__fmaf_rn(xs[hh][k], kScale, nmn));   // masked: ex2(-inf) = 0
+            ps4[k & 3] = __fadd_rn(ps4[k & 3], xs[hh][k]);
+          }
+        const float ps = __fadd_rn(__fadd_rn(ps4[0], ps4[1]), __fadd_rn(ps4[2], ps4[3]));
+        l = __fmaf_rn(l, alpha, ps);
+        m = mn;
+        // P_X buffer and O_X partial were last used by PV(gb-1): wait for it (within the
+        // item; the previous item's last PV was waited for at its end), store P, fold
+        if (i >= 1) {
+          tc::mbar_wait(&pv_done[x], (gb - 1) & 1);
+          tc::fence_after();
+        }
+        const uint32_t ph_t = tmem + T_P + 128 * x + lane_off;
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          uint32_t hi[32], lo[32];
+#pragma unroll
+          for (int k = 0; k < 32; ++k) {
+            float fh, fl;
+            tc::split_tf32(xs[hh][k], fh, fl);
+            hi[k] = __float_as_uint(fh);
+            lo[k] = __float_as_uint(fl);
+          }
+          tc::tmem_st32(ph_t + 32 * hh, hi);
+          tc::tmem_st32(ph_t + 64 + 32 * hh, lo);
+        }
+        if (i >= 1) fold(alpha_prev);
+        alpha_prev = alpha;
+        tc::tmem_wait_st();
+        tc::fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&p_full[x]);
       }
-      if (i >= 1) fold(alpha_prev);
-      alpha_prev = alpha;
-      tc::tmem_wait_st();
-      tc::fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&p_full[x]);
-      AT_ACC(8 + 5 * x, ts0);   // P store + fold
-#ifdef NC_ATT_TIMING
-      if (ts0) atomicAdd(&g_att_clk[9 + 5 * x], 1ull);
-#endif
-    }
-    tc::mbar_wait(&pv_done[x], (nkb - 1) & 1);
-    tc::fence_after();
-    fold(alpha_prev);
-    // merge the two halves: B hands (m, l, O) to A through shared memory (the K buffer is idle)
-    float *xb = reinterpret_cast<float *>(sK) + (size_t)r * 66;
-    if (x == 1) {
-      xb[0] = m; xb[1] = l;
+      tc::mbar_wait(&pv_done[x], (gb - 1) & 1);
+      tc::fence_after();
+      fold(alpha_prev);
+      // merge the halves: B hands (m, l, O) to A through its own (now idle) P region of TMEM
+      const uint32_t mt = tmem + T_P + 128 + lane_off;
+      if (x == 1) {
+        uint32_t w0[32], w1[32], w2[32];
 #pragma unroll
-      for (int d = 0; d < 64; ++d) xb[2 + d] = O[d];
-    }
-    named_bar(1, 256);
-    if (x == 0 && r < t.nrows) {
-      const float mB = xb[0], lB = xb[1];
-      const float mm = fmaxf(m, mB);
-      const float fa = (m == -CUDART_INF_F) ? 0.f : tc::ex2(__fsub_rn(m, mm));
-      const float fb = (mB == -CUDART_INF_F) ? 0.f : tc::ex2(__fsub_rn(mB, mm));
-      const float lt = __fmaf_rn(l, fa, __fmul_rn(lB, fb));
-      const size_t ob = (size_t)(t.qrow0 + r) * a.ldo + h * 64;
+        for (int d = 0; d < 32; ++d) { w0[d] = __float_as_uint(O[d]); w1[d] = __float_as_uint(O[32 + d]); w2[d] = 0u; }
+        w2[0] = __float_as_uint(m);
+        w2[1] = __float_as_uint(l);
+        tc::tmem_st32(mt, w0);
+        tc::tmem_st32(mt + 32, w1);
+        tc::tmem_st32(mt + 64, w2);
+        tc::tmem_wait_st();
+        tc::fence_before();
+      }
+      named_bar(1, 256);
+      if (x == 0) {                                // merge in 32-column pieces (registers)
+        tc::fence_after();
+        uint32_t w[32];
+        tc::tmem_ld32(mt + 64, w);
+        tc::tmem_wait_ld();
+        const float mB = __uint_as_float(w[0]), lB = __uint_as_float(w[1]);
+        const float mm = fmaxf(m, mB);
+        const float fa = (m == -CUDART_INF_F) ? 0.f : tc::ex2(__fsub_rn(m, mm));
+        const float fb = (mB == -CUDART_INF_F) ? 0.f : tc::ex2(__fsub_rn(mB, mm));
+        const float lt = __fmaf_rn(l, fa, __fmul_rn(lB, fb));
+        const bool row_ok = r < xi.t.nrows;
+        const size_t ob = (size_t)(xi.t.qrow0 + r) * a.ldo + xi.h * 64;
 #pragma unroll
-      for (int d = 0; d < 64; d += 4) {
-        float4 hi, lo, v;
-        v.x = __fdiv_rn(__fmaf_rn(O[d], fa, __fmul_rn(xb[2 + d], fb)), lt);
-        v.y = __fdiv_rn(__fmaf_rn(O[d + 1], fa, __fmul_rn(xb[3 + d], fb)), lt);
-        v.z = __fdiv_rn(__fmaf_rn(O[d + 2], fa, __fmul_rn(xb[4 + d], fb)), lt);
-        v.w = __fdiv_rn(__fmaf_rn(O[d + 3], fa, __fmul_rn(xb[5 + d], fb)), lt);
-        tc::split_tf32(v.x, hi.x, lo.x); tc::split_tf32(v.y, hi.y, lo.y);
-        tc::split_tf32(v.z, hi.z, lo.z); tc::split_tf32(v.w, hi.w, lo.w);
-        *reinterpret_cast<float4 *>(a.o_hi + ob + d) = hi;
-        *reinterpret_cast<float4 *>(a.o_lo + ob + d) = lo;
+        for (int hf = 0; hf < 2; ++hf) {
+          tc::tmem_ld32(mt + 32 * hf, w);
+          tc::tmem_wait_ld();
+          if (hf == 1) {
+            tc::fence_before();
+            named_bar(2, 256);                     // B may reuse its P region (next item) only now
+          }
+          if (row_ok) {
+#pragma unroll
+            for (int d = 0; d < 32; d += 4) {
+              const int dd = 32 * hf + d;
+              float4 hi, lo, v;
+              v.x = __fdiv_rn(__fmaf_rn(O[dd], fa, __fmul_rn(__uint_as_float(w[d]), fb)), lt);
+              v.y = __fdiv_rn(__fmaf_rn(O[dd + 1], fa, __fmul_rn(__uint_as_float(w[d + 1]), fb)), lt);
+              v.z = __fdiv_rn(__fmaf_rn(O[dd + 2], fa, __fmul_rn(__uint_as_float(w[d + 2]), fb)), lt);
+              v.w = __fdiv_rn(__fmaf_rn(O[dd + 3], fa, __fmul_rn(__uint_as_float(w[d + 3]), fb)), lt);
+              tc::split_tf32(v.x, hi.x, lo.x); tc::split_tf32(v.y, hi.y, lo.y);
+              tc::split_tf32(v.z, hi.z, lo.z); tc::split_tf32(v.w, hi.w, lo.w);
+              *reinterpret_cast<float4 *>(a.o_hi + ob + dd) = hi;
+              *reinterpret_cast<float4 *>(a.o_lo + ob + dd) = lo;
+            }
+          }
+        }
+      } else {
+        named_bar(2, 256);
       }
     }
   }
@@ -406,6 +471,14 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
   __syncthreads();
   tc::fence_after();
   if (warp == 2) tc::tmem_dealloc(tmem, 512);
+  if (threadIdx.x == 0) {            // last CTA out resets the item counter for the next launch
+    __threadfence();
+    if (atomicAdd(a.item_ctr + 1, 1) == (int)gridDim.x - 1) {
+      a.item_ctr[0] = 0;
+      a.item_ctr[1] = 0;
+      __threadfence();
+    }
+  }
 }
 
 // ------------------------------------------------------------- host side ---
@@ -494,8 +567,20 @@ void launch_attention_tc(const AttnTcArgs &a, cudaStream_t s) {
   const CUtensorMap *kh = tmap_nd(a.k_hi, 4, kd, kbx), *kl = tmap_nd(a.k_lo, 4, kd, kbx);
   const CUtensorMap *vh = tmap_nd(a.v_hi, 4, kd, kbx, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   const CUtensorMap *vl = tmap_nd(a.v_lo, 4, kd, kbx, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
-  dim3 grid(a.n_tiles, a.H);
-  attn_tc_kernel<<<grid, ATT_THREADS, ATT_SMEM, s>>>(*qh, *ql, *kh, *kl, *vh, *vl, a);
+  static int *ctr = nullptr;   // {next item, CTAs done}; zero between launches (last CTA resets)
+  static int n_sms = 0;
+  if (!ctr) {
+    if (cudaMalloc(&ctr, 2 * sizeof(int)) != cudaSuccess) throw std::runtime_error("cudaMalloc attention counter");
+    cudaMemset(ctr, 0, 2 * sizeof(int));
+    cudaDeviceSynchronize();
+    int dev;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  AttnTcArgs aa = a;
+  aa.item_ctr = ctr;
+  const int grid = std::min(a.n_tiles * a.H, n_sms);   // persistent: one CTA per SM claims (tile, head) items
+  attn_tc_kernel<<<grid, ATT_THREADS, ATT_SMEM, s>>>(*qh, *ql, *kh, *kl, *vh, *vl, aa);
 }
 
 }  // namespace nc
