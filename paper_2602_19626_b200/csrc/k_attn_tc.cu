@@ -56,17 +56,15 @@ constexpr int ATT_THREADS = 384;
 constexpr uint32_t T_S = 0, T_P = 128, T_O = 384;   // P half X at T_P + 128 X (hi, lo +64); O half X at T_O + 64 X
 
 #ifdef NC_ATT_TIMING
-__device__ unsigned long long g_att_clk[16];   // diagnostics build only
-#define AT_BEGIN long long _at = clock64()
-#define AT_ACC(k, cond)                                                                   \
-  do {                                                                                    \
-    const long long _n = clock64();                                                       \
-    if (cond) atomicAdd(&g_att_clk[k], (unsigned long long)(_n - _at));                   \
-    _at = _n;                                                                             \
-  } while (0)
+// diagnostics build only: per-thread phase cycles accumulated in registers, flushed once per CTA
+__device__ unsigned long long g_att_clk[32];
+#define AT_DECL unsigned long long _acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}; long long _at = clock64()
+#define AT_T(k) do { const long long _n = clock64(); _acc[k] += (unsigned long long)(_n - _at); _at = _n; } while (0)
+#define AT_FLUSH(base, cond) do { if (cond) for (int _k = 0; _k < 8; ++_k) atomicAdd(&g_att_clk[(base) + _k], _acc[_k]); } while (0)
 #else
-#define AT_BEGIN do {} while (0)
-#define AT_ACC(k, cond) do {} while (0)
+#define AT_DECL do {} while (0)
+#define AT_T(k) do {} while (0)
+#define AT_FLUSH(base, cond) do {} while (0)
 #endif
 
 __device__ __forceinline__ int wstart(int j, int L, int C) {
@@ -264,15 +262,20 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
       }
     };
     int gb = 0, qi = 0;
+    AT_DECL;
     for (int jt = 0;; ++jt) {
       const int it = next_item(jt, lane == 0);
       if (it < 0) break;
       const Item x = item_of(it);
       if (x.nkb == 0) continue;
+      AT_T(6);
       tc::mbar_wait(q_full, qi & 1);
+      AT_T(0);   // wait Q
       for (int i = 0; i < x.nkb; ++i, ++gb) {
         tc::mbar_wait(k_full, gb & 1);
+        AT_T(1);   // wait K
         if (gb > 0) tc::mbar_wait(s_empty, (gb - 1) & 1);   // both softmax groups read S(gb-1)
+        AT_T(2);   // wait s_empty
         tc::fence_after();
 #pragma unroll
         for (int dsub = 0; dsub < 2; ++dsub)     // corrections first, hi*hi last (see k_gemm_tc.cu)
@@ -300,11 +303,18 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
           if (i == x.nkb - 1) tc::mma_commit(q_empty);   // Q buffer free for the next item
         }
         __syncwarp();
+        AT_T(3);   // S issue
         if (i > 0) issue_pv(gb - 1);
+        AT_T(4);   // PV (incl p_full/V waits)
       }
       issue_pv(gb - 1);                           // the item's last block, before the next item's S
+      AT_T(4);
       ++qi;
+#ifdef NC_ATT_TIMING
+      _acc[7] += x.nkb;
+#endif
     }
+    AT_FLUSH(0, lane == 0);
   } else if (warp >= 4) {
     // ------------------------------------------- softmax groups (key halves)
     const int x = (warp - 4) >> 2;                 // key half of this softmax group
@@ -313,11 +323,13 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
     // scores in the log2 domain: x = S * (1/8 * log2 e); p = 2^(x - m)
     constexpr float kScale = 0.125f * 1.44269504088896341f;
     int gb = 0;
+    AT_DECL;
     for (int jt = 0;; ++jt) {
       const int it = next_item(jt, lane == 0);
       if (it < 0) break;
       const Item xi = item_of(it);
       if (xi.nkb == 0) continue;
+      AT_T(6);   // item gap
       const int j = xi.t.p0 + r;
       float O[64];
 #pragma unroll
@@ -336,6 +348,7 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
       };
       for (int i = 0; i < xi.nkb; ++i, ++gb) {
         tc::mbar_wait(s_full, gb & 1);
+        AT_T(0);   // wait S
         tc::fence_after();
         uint32_t sr[2][32];
         tc::tmem_ld32(tmem + T_S + 64 * x + lane_off, sr[0]);
@@ -381,12 +394,14 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
         const float ps = __fadd_rn(__fadd_rn(ps4[0], ps4[1]), __fadd_rn(ps4[2], ps4[3]));
         l = __fmaf_rn(l, alpha, ps);
         m = mn;
+        AT_T(1);   // S load + max/exp/sum
         // P_X buffer and O_X partial were last used by PV(gb-1): wait for it (within the
         // item; the previous item's last PV was waited for at its end), store P, fold
         if (i >= 1) {
           tc::mbar_wait(&pv_done[x], (gb - 1) & 1);
           tc::fence_after();
         }
+        AT_T(2);   // wait PV(i-1)
         const uint32_t ph_t = tmem + T_P + 128 * x + lane_off;
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
@@ -407,8 +422,10 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
         tc::fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&p_full[x]);
+        AT_T(3);   // P store + fold
       }
       tc::mbar_wait(&pv_done[x], (gb - 1) & 1);
+      AT_T(4);   // wait last PV
       tc::fence_after();
       fold(alpha_prev);
       // merge the halves: B hands (m, l, O) to A through its own (now idle) P region of TMEM
@@ -465,7 +482,12 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
       } else {
         named_bar(2, 256);
       }
+      AT_T(5);   // merge + output
+#ifdef NC_ATT_TIMING
+      _acc[7] += xi.nkb;
+#endif
     }
+    AT_FLUSH(x == 0 ? 8 : 16, lane == 0 && q == 0);
   }
   tc::fence_before();
   __syncthreads();
@@ -484,18 +506,21 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
 // ------------------------------------------------------------- host side ---
 void attn_timing_report() {
 #ifdef NC_ATT_TIMING
-  unsigned long long hh[16];
+  unsigned long long h[32];
   cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(hh, g_att_clk, sizeof(hh));
-  const double n = (double)(hh[9] ? hh[9] : 1);
-  fprintf(stderr,
-          "attn per 128-key block (cycles): MMA thread: wait K %.0f | wait s_empty %.0f | S issue %.0f | PV incl "
-          "waits %.0f (p_full/V waits %.0f)\n  softmax A: wait S %.0f | ld+max/exp/sum %.0f | wait PV %.0f | "
-          "store+fold %.0f\n  softmax B: wait S %.0f | ld+max/exp/sum %.0f | wait PV %.0f | store+fold %.0f  "
-          "(blocks %.0f)\n",
-          hh[0] / n, hh[1] / n, hh[2] / n, hh[3] / n, hh[4] / n, hh[5] / n, hh[6] / n, hh[7] / n, hh[8] / n,
-          hh[10] / n, hh[11] / n, hh[12] / n, hh[13] / n, n);
-  unsigned long long z[16] = {};
+  cudaMemcpyFromSymbol(h, g_att_clk, sizeof(h));
+  const char *nm[3] = {"MMA   ", "soft A", "soft B"};
+  const char *ph[3][7] = {{"wait Q", "wait K", "wait s_empty", "S issue", "PV", "-", "item gap"},
+                          {"wait S", "ld+exp", "wait PV", "store+fold", "wait last PV", "merge+out", "item gap"},
+                          {"wait S", "ld+exp", "wait PV", "store+fold", "wait last PV", "merge+out", "item gap"}};
+  for (int w = 0; w < 3; ++w) {
+    const unsigned long long *x = h + 8 * w;
+    const double n = (double)(x[7] ? x[7] : 1);
+    fprintf(stderr, "attn %s per block:", nm[w]);
+    for (int k = 0; k < 7; ++k) fprintf(stderr, " %s %.0f |", ph[w][k], x[k] / n);
+    fprintf(stderr, " (blocks %.0f)\n", n);
+  }
+  unsigned long long z[32] = {};
   cudaMemcpyToSymbol(g_att_clk, z, sizeof(z));
 #endif
 }
