@@ -5,7 +5,10 @@ Per token i of a chunk (canonical algorithm of SURVEY.md §8(c)):
   log p_llm = log_softmax(z / tau)                       (eq:lm)
   pt  = softmax(log p_llm + b)                           (head)
   if i < W (warmup) or N-gram off:  p = pt
-  else: p_ng = NGram.predict();  w = exp(lw - logsumexp(lw));  p = w_l pt + w_n p_ng
+  else: p_ng = NGram.predict()
+        if skip on and H(p_ng) < 1.5 bits:  p = p_ng   (confidence skip, alg:compress lines 5-6,
+                                                        P:452-469; reading D32)
+        else: w = exp(lw - logsumexp(lw));  p = w_l pt + w_n p_ng
   c = quantize(p, T)                                     (P:338-349)
   emit (cum_t, freq_t) to the WNC coder
   b -= alpha (pt - onehot(t))                            (uses pt, D25)
@@ -13,7 +16,9 @@ Per token i of a chunk (canonical algorithm of SURVEY.md §8(c)):
                                                          (P:411-418; D24-D26; S:301)
   NGram.update(t)                                        (P:375-378)
 
-The skip branch (alg:compress lines 5-6) is NEXT-1 and not modelled.
+Reading D32 (the skip): the LLM forward still runs for a skipped token
+(its retained K/V are needed by later tokens), so pt exists and, per alg:compress line 12
+("Update: N-gram, Mixer, AdaptiveHead with t_i"), all three update on every token.
 """
 from dataclasses import dataclass
 
@@ -25,6 +30,20 @@ from .ngram import NGram
 
 FLAG_NGRAM = 1
 FLAG_HEAD = 2
+FLAG_SKIP = 4          # confidence-based LLM skip, container flags bit 2
+SKIP_TAU_BITS = 1.5    # "H(p_ng) < tau bits, with tau = 1.5"
+
+
+def entropy_bits_fp64(p):
+    """Shannon entropy in bits, -sum p log2 p over p > 0 (the skip test's H)."""
+    p = np.asarray(p, dtype=np.float64)
+    nz = p[p > 0]
+    return float(-(nz * np.log2(nz)).sum())
+
+
+def should_skip(p_ng, tau=SKIP_TAU_BITS):
+    """true iff entropy_bits(p_ng) < tau."""
+    return entropy_bits_fp64(p_ng) < tau
 
 
 @dataclass
@@ -71,6 +90,9 @@ class ChunkModel:
         self.V, self.prm = V, prm
         self.use_ng = bool(prm.flags & FLAG_NGRAM)
         self.use_head = bool(prm.flags & FLAG_HEAD)
+        self.use_skip = bool(prm.flags & FLAG_SKIP) and self.use_ng
+        self.last_skipped = False
+        self.n_skipped = 0
         self.b = np.zeros(V)
         self.ng = NGram(V, prm.ngram_orders, cap=prm.ngram_cap) if self.use_ng else None
         self.lw = np.log(np.array([prm.w_llm0, 1.0 - prm.w_llm0]))
@@ -81,8 +103,13 @@ class ChunkModel:
         zt = np.asarray(z, dtype=np.float64) / self.prm.tau
         logp = zt - logsumexp(zt)
         pt = softmax(logp + self.b) if self.use_head else softmax(logp)
+        self.last_skipped = False
         if self.use_ng and self.i >= self.prm.warmup:
             png = self.ng.predict()
+            if self.use_skip and should_skip(png):
+                self.last_skipped = True
+                self.n_skipped += 1
+                return png, pt, png
             w = np.exp(self.lw - logsumexp(self.lw))
             return w[0] * pt + w[1] * png, pt, png
         return pt, pt, None
@@ -107,10 +134,12 @@ def encode_tokens(Z, toks, V, prm: Params, keep_rows=()):
     Returns dict(stream, bits, cum, freq, p_true, pt_true, rows={j: p}) ."""
     cm = ChunkModel(V, prm)
     enc = Encoder()
-    cum, freq, p_true, pt_true, rows = [], [], [], [], {}
+    cum, freq, p_true, pt_true, rows, skipped, h_ng = [], [], [], [], {}, [], []
     keep = set(keep_rows)
     for j, t in enumerate(toks):
         p, pt, png = cm.distribution(Z[j])
+        skipped.append(cm.last_skipped)
+        h_ng.append(entropy_bits_fp64(png) if (png is not None and cm.use_skip) else None)
         c = quantize(p, prm.T)
         lo = int(c[:t].sum())
         enc.encode(lo, int(c[t]), prm.T)
@@ -123,7 +152,7 @@ def encode_tokens(Z, toks, V, prm: Params, keep_rows=()):
         cm.update(t, pt, png)
     stream, bits = enc.finish()
     return dict(stream=stream, bits=bits, cum=cum, freq=freq, p_true=p_true,
-                pt_true=pt_true, rows=rows, min_range=enc.min_range)
+                pt_true=pt_true, rows=rows, min_range=enc.min_range, skipped=skipped, h_ng=h_ng)
 
 
 def decode_tokens(step, n, stream, V, prm: Params):

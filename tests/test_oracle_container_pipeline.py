@@ -68,7 +68,8 @@ def test_tokenizer_greedy_longest_match():
     assert [vocab[i] for i in tk.encode(b"abd")] == [b"ab", b"d"]
 
 
-@pytest.mark.parametrize("flags,bits,chunks", [(3, 24, 1), (3, 24, 3), (0, 16, 2), (1, 24, 2), (2, 16, 1)])
+@pytest.mark.parametrize("flags,bits,chunks", [(3, 24, 1), (3, 24, 3), (0, 16, 2), (1, 24, 2), (2, 16, 1),
+                                              (7, 24, 2), (5, 16, 1)])   # 4 = confidence skip (NEXT-1)
 def test_pipeline_roundtrip(tiny_weights, flags, bits, chunks):
     from synth import make_text
     data = make_text("alice", 900, 77 + flags)
