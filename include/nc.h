@@ -50,9 +50,13 @@ typedef enum {
 /* Feature flags (NC05 flags byte). */
 #define NC_FLAG_NGRAM 1u /* bit0: N-gram + mixer            */
 #define NC_FLAG_HEAD 2u  /* bit1: adaptive log-space bias head */
-#define NC_FLAG_SKIP 4u  /* bit2: confidence skip -- reserved,
-                            not implemented (NEXT-1): rejected with
-                            NC_ERR_INVALID                              */
+#define NC_FLAG_SKIP 4u  /* bit2: confidence-based LLM skip (P:452-469,
+                            alg:compress lines 5-6): after the warmup, a
+                            token with H(p_ng) < 1.5 bits is coded with
+                            p = p_ng.  Needs NC_FLAG_NGRAM (ignored
+                            without it).  The forward still runs (its K/V
+                            are retained) and every model updates on
+                            every token (alg:compress line 12; DESIGN D32) */
 
 typedef struct {
   uint32_t cdf_bits;     /* 24 (default) or 16; T = 2^cdf_bits */

@@ -207,7 +207,6 @@ nc_status nc_decompress(nc_model *m, const uint8_t *in, size_t n, const nc_param
     require_device();
     nc::Params q = nc::validate(p);
     nc::Nc05View view = nc::read_nc05(in, n);
-    if (view.flags & NC_FLAG_SKIP) nc::fail(NC_ERR_FORMAT, "confidence-skip streams are not supported (NEXT-1)");
     q.flags = view.flags;
     q.tau_milli = view.tau_milli;
     q.inv_tau = 1000.0 / view.tau_milli;

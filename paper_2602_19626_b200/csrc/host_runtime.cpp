@@ -244,7 +244,7 @@ Params validate(const nc_params *p) {
   q.cdf_bits = p->cdf_bits;
   q.flags = p->flags;
   if (!(q.cdf_bits == 16 || q.cdf_bits == 24)) fail(NC_ERR_INVALID, "cdf_bits must be 16 or 24");
-  if (q.flags & ~3u) fail(NC_ERR_INVALID, "only NGRAM|HEAD flags are implemented (skip is NEXT-1)");
+  if (q.flags & ~7u) fail(NC_ERR_INVALID, "flags: only NGRAM | HEAD | SKIP (bits 0-2) are defined");
   if (!(p->temperature > 0.f)) fail(NC_ERR_INVALID, "temperature must be > 0");
   double tm = std::nearbyint((double)p->temperature * 1000.0);
   if (tm < 1 || tm > 65535) fail(NC_ERR_INVALID, "temperature out of the u16 milli range");

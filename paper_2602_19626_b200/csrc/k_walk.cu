@@ -47,6 +47,7 @@ struct WalkSmem {
   unsigned long long red_sum[32], red_cum[32];
   float red_bv[32]; int red_bi[32]; uint32_t red_bc[32];
   uint32_t scan[32];
+  float red_h[32];   // N-gram entropy partials (skip test)
   // per-token broadcast scalars
   float M, invS, a0f;
   int mix, tok, argmax, nsp;
@@ -156,10 +157,13 @@ __device__ __forceinline__ void ms_regs(const float (&u)[NGM][4], int ng, float 
   ts = __fadd_rn(__fadd_rn(s4[0], s4[1]), __fadd_rn(s4[2], s4[3]));
 }
 // p = w_l pt + w_n (a0f (c+1) + add); c (unigram count < 2^24) held exactly in fp32
-__device__ __forceinline__ float mix_p(float pt, float a0f, float cuv, float add, float wl, float wn, float &png) {
+// skip (confidence-based LLM skip): p = p_ng
+__device__ __forceinline__ float mix_p(float pt, float a0f, float cuv, float add, float wl, float wn, float &png,
+                                       bool skip = false) {
   png = __fmaf_rn(a0f, __fadd_rn(cuv, 1.f), add);
-  return __fmaf_rn(wl, pt, __fmul_rn(wn, png));
+  return skip ? png : __fmaf_rn(wl, pt, __fmul_rn(wn, png));
 }
+constexpr float kSkipTauBits = 1.5f;   // "H(p_ng) < tau bits, with tau = 1.5"
 struct Best {
   float v; int i; uint32_t c;
 };
@@ -425,6 +429,7 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
   __shared__ WalkSmem sm;
   __shared__ Xch xs[2];            // own slots (token parity)
   __shared__ Xch xin[2][CS];       // the cluster's slots (token parity): gathered (decode) or pushed (encode)
+  __shared__ float xh[2][CS];      // the cluster's N-gram entropy partials (token parity), pushed
   __shared__ double s_lw[2];
   __shared__ float s_w[2];
   __shared__ uint32_t s_i;
@@ -445,6 +450,7 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
   double *b_g = a.b + (size_t)c * V + vb;
   uint32_t *cu_g = a.cu + (size_t)c * V + vb;
   const bool use_ng = a.flags & 1u, use_head = a.flags & 2u;
+  const bool use_skip = use_ng && (a.flags & 4u);   // confidence-based LLM skip
   const bool enc = a.mode == 0;
   const uint64_t T = 1ull << a.cdf_bits;
   const float TmV = (float)(T - V);
@@ -461,6 +467,7 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
   if (tid < 32) {
     sm.red_m[tid] = -CUDART_INF_F; sm.red_s[tid] = 0.f; sm.red_sum[tid] = 0ull; sm.red_cum[tid] = 0ull;
     sm.red_bv[tid] = -1.f; sm.red_bi[tid] = 0x7fffffff; sm.red_bc[tid] = 0u; sm.scan[tid] = 0u;
+    sm.red_h[tid] = 0.f;
   }
   if (tid == 0) {
     s_lw[0] = st->lw[0]; s_lw[1] = st->lw[1];
@@ -484,7 +491,8 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
     u[0] = walk_u(z4.x, b01.x, inv_tau); u[1] = walk_u(z4.y, b01.y, inv_tau);
     u[2] = walk_u(z4.z, b23.x, inv_tau); u[3] = walk_u(z4.w, b23.y, inv_tau);
   };
-  auto prob4 = [&](const float *z, int g, float M, float invS, float wl, float wn, float a0f, int mix, float pt[4],
+  auto prob4 = [&](const float *z, int g, float M, float invS, float wl, float wn, float a0f, int mix, bool skip,
+                   float pt[4],
                    float png[4], float p[4]) {
     float u[4];
     load_u(z, g, u);
@@ -501,7 +509,7 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
     const float4 s4 = bits ? reinterpret_cast<const float4 *>(sp_s)[g] : make_float4(0.f, 0.f, 0.f, 0.f);
     const float sa[4] = {s4.x, s4.y, s4.z, s4.w};
 #pragma unroll
-    for (int j = 0; j < 4; ++j) p[j] = mix_p(pt[j], a0f, cc[j], sa[j], wl, wn, png[j]);
+    for (int j = 0; j < 4; ++j) p[j] = mix_p(pt[j], a0f, cc[j], sa[j], wl, wn, png[j], skip);
   };
   // CTA reduction of (m, s) into warp 0 (all lanes hold the CTA value)
   auto cta_ms = [&](float &tm, float &ts) {
@@ -576,6 +584,50 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
   auto prefetch_wait = [&]() { asm volatile("cp.async.wait_all;" ::: "memory"); };
+  // H(p_ng) in bits of the current token (skip test; D32).  All threads call it,
+  // with the token's N-gram fixups scattered; compression and decompression run this same
+  // arithmetic: per thread over its groups (four element-position partial sums), lane 0 of
+  // a fixed warp xor tree, the same over the warps, then the cluster's CTAs in rank order.
+  auto ng_entropy = [&](int par, float a0f) -> float {
+    float h4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int k = 0; k < NGM; ++k)
+      if (k < ng) {
+        const int g = tid + k * WT;
+        const float4 c4 = reinterpret_cast<const float4 *>(cu_s)[g];
+        const uint32_t bits = (bitmap[g >> 3] >> ((g & 7) * 4)) & 15u;
+        const float4 s4 = bits ? reinterpret_cast<const float4 *>(sp_s)[g] : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float cc[4] = {c4.x, c4.y, c4.z, c4.w}, sa[4] = {s4.x, s4.y, s4.z, s4.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float q = __fmaf_rn(a0f, __fadd_rn(cc[j], 1.f), sa[j]);   // p_ng(v), as in mix_p
+          h4[j] = __fsub_rn(h4[j], __fmul_rn(q, lg2f(q)));
+        }
+      }
+    float h = __fadd_rn(__fadd_rn(h4[0], h4[1]), __fadd_rn(h4[2], h4[3]));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) h = __fadd_rn(h, __shfl_xor_sync(0xffffffffu, h, o));
+    if (lane == 0) sm.red_h[wid] = h;
+    __syncthreads();
+    if (wid == 0) {
+      h = sm.red_h[lane];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) h = __fadd_rn(h, __shfl_xor_sync(0xffffffffu, h, o));
+      if (lane == 0) {
+        if (CS > 1) {
+#pragma unroll
+          for (int r = 0; r < CS; ++r) tc::st_cluster_s32(tc::mapa(&xh[par][rank], (uint32_t)r), __float_as_int(h));
+        } else {
+          xh[par][0] = h;
+        }
+      }
+    }
+    if (CS > 1) cl_sync(); else __syncthreads();
+    float H = xh[par][0];
+    for (int r = 1; r < CS; ++r) H = __fadd_rn(H, xh[par][r]);
+    return H;
+  };
+
   // exponential-weights mixer step (D24), fp32 on the SFU (lg2/ex2.approx) in the
   // log2 domain; thread 0 of every CTA and the decoder run this same arithmetic
   auto mixer_update = [&](float pt_t, float png_t) {
@@ -686,6 +738,7 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
       const int ltok = tok - (int)vb;                  // local id (may be outside [0, Vc))
       const float M = sm.M, invS = sm.invS, a0f = sm.a0f, wl = s_w[0], wn = s_w[1];
       const int mix = sm.mix;
+      const bool skip = (use_skip && mix) ? ng_entropy(par, a0f) < kSkipTauBits : false;
       const bool pre_next = has_next && use_ng && i + 1 >= a.warmup;
       if (wid == 1 && pre_next) prefetch_pre(i + 1);
       uint32_t my_sum = 0, my_cum = 0;
@@ -710,7 +763,7 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
           const float4 s4 = bits ? reinterpret_cast<const float4 *>(sp_s)[g] : make_float4(0.f, 0.f, 0.f, 0.f);
           const float sa[4] = {s4.x, s4.y, s4.z, s4.w};
 #pragma unroll
-          for (int j = 0; j < 4; ++j) p[j] = mix_p(pt[j], a0f, cc[j], sa[j], wl, wn, png[j]);
+          for (int j = 0; j < 4; ++j) p[j] = mix_p(pt[j], a0f, cc[j], sa[j], wl, wn, png[j], skip);
         }
         uint32_t cv[4];
         quant4(p, TmV, cv);
@@ -857,6 +910,8 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
         }
       }
       __syncthreads();
+      // skip test for this token (same arithmetic as compression)
+      const bool skip = (use_skip && sm.mix) ? ng_entropy(par, sm.a0f) < kSkipTauBits : false;
       // (2) softmax statistics
       {
         float ud[NGM][4];
@@ -886,7 +941,7 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
       Best bb{-1.f, 0x7fffffff, 0};
       for (int g = tid; g < Gc; g += WT) {
         float pt[4], png[4], p[4];
-        prob4(z, g, M, invS, wl, wn, a0f, mix, pt, png, p);
+        prob4(z, g, M, invS, wl, wn, a0f, mix, skip, pt, png, p);
         uint32_t gs = 0;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -957,7 +1012,7 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
             accm += gsum[gf];
           }
           float pt[4], png[4], p[4];
-          prob4(z, gf, M, invS, wl, wn, a0f, mix, pt, png, p);
+          prob4(z, gf, M, invS, wl, wn, a0f, mix, skip, pt, png, p);
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             const int v = 4 * gf + j;
@@ -995,7 +1050,7 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
       if (use_head)
         for (int g = tid; g < Gc; g += WT) {
           float pt[4], png[4], p[4];
-          prob4(z, g, M, invS, wl, wn, a0f, mix, pt, png, p);
+          prob4(z, g, M, invS, wl, wn, a0f, mix, skip, pt, png, p);
           double2 *bp = reinterpret_cast<double2 *>(b_s) + 2 * g;
           double2 b01 = bp[0], b23 = bp[1];
           const int v = 4 * g;

@@ -176,6 +176,44 @@ def test_config1_roundtrip_size_and_p(nc, m2, w2, n_chunks, flags, bits):
         assert (np.abs(p_gpu - p_ref) / p_ref).max() < P_TOL
 
 
+@pytest.mark.parametrize("n_chunks", [1, 2])
+def test_skip_roundtrip_size_and_p(nc, m2, w2, n_chunks):
+    """confidence-based LLM skip (NEXT-1, flags bit 2): round trip on repetitive text (the
+    N-gram becomes confident), size within 0.5 % of the oracle, p(t) within P_TOL of the
+    oracle on every token whose oracle H(p_ng) is not within 1e-3 of 1.5 bits (there fp32
+    and fp64 may decide the skip differently: compare what is unique)."""
+    from oracle.ensemble import Params
+    from synth import make_text
+    data = make_text("alice", 300, 4242) * 14       # oracle: 562 (1 chunk) / 256 (2 chunks) skips
+    prm = nc.nc_params_default(window=512, slide=128, n_chunks=n_chunks, flags=7, cdf_bits=24)
+    blob = nc.nc_compress(m2, data, prm)
+    assert nc.nc_decompress(m2, blob, prm) == data
+    prm_o = Params(window=512, slide=128, n_chunks=n_chunks, flags=7, cdf_bits=24)
+    from oracle.chunking import split_chunks
+    from oracle.lm import LM
+    from oracle.ensemble import encode_tokens
+    from oracle.tokenizer import Tokenizer
+    tk, lm = Tokenizer(w2.vocab), LM(w2)
+    size, n_cmp, n_all, n_skip = 0, 0, 0, 0
+    for ch in split_chunks(data, n_chunks):
+        t = tk.encode(ch)
+        x = [w2.bos] + t[:-1] if t else []
+        Z = lm.forward_blocked(x, 512, 128)
+        r = encode_tokens(Z, t, w2.V, prm_o)
+        size += 12 + (r["bits"] + 7) // 8
+        n_skip += sum(r["skipped"])
+        z = nc.nc_debug_forward(m2, x, prm, 0)
+        _, _, p_gpu = nc.nc_debug_walk(z, t, prm)
+        p_ref = np.array(r["p_true"])
+        ok = np.array([h is None or abs(h - 1.5) > 1e-3 for h in r["h_ng"]])
+        n_cmp += int(ok.sum())
+        n_all += len(t)
+        assert (np.abs(p_gpu[ok] - p_ref[ok]) / p_ref[ok]).max() < P_TOL
+    assert n_skip > 100, n_skip                       # the skip path is exercised
+    assert n_cmp >= 0.98 * n_all
+    assert abs(len(blob) - (9 + size)) <= 0.005 * size, (len(blob), size)
+
+
 def test_edge_inputs_roundtrip(nc, m2):
     prm = nc.nc_params_default(window=256, slide=128, n_chunks=4)
     for data in (b"", b"a", b"\x00\x00\xff\n", b"\n" * 9, bytes(range(256)) * 3):
