@@ -302,3 +302,22 @@ def test_tc_gemm_op_vs_numpy(nc, K):
     Q = rng.random((128, K)).astype(np.float32)
     r2 = P.astype(np.float64) @ Q.astype(np.float64).T
     assert abs(((nc.nc_debug_gemm(P, Q, 0) - r2) / r2).mean()) < 1e-6
+
+
+def test_shard_path_one_rank_nccl(nc, m2):
+    """nc_compress_shard / nc_decompress_shard through a real 1-rank NCCL communicator
+    (SURVEY 8(e)): the part equals nc_compress with the same n_chunks, covers [0, total),
+    and decompresses back.  (Several ranks need several GPUs; the multi-rank host plan is
+    covered by tests/test_multi_gloo.py.)"""
+    from synth import make_text
+    data = make_text("alice", 2500, 606)
+    prm = nc.nc_params_default(window=256, slide=128, n_chunks=3)
+    comm = nc.Comm(0, 1, nc.Comm.unique_id(), 0)
+    try:
+        part, off, tot = nc.nc_compress_shard(m2, comm, data, prm)
+        ref = nc.nc_compress(m2, data, prm)
+        assert off == 0 and tot == len(part) and part == ref
+        out, o2, t2 = nc.nc_decompress_shard(m2, comm, part, prm)
+        assert o2 == 0 and t2 == len(data) and out == data
+    finally:
+        comm.close()
