@@ -78,6 +78,38 @@ constexpr int W_TMA = 8, W_MMA = 9;
 // sch_empty arrivals per tile claim: leader MMA + 8 epilogue warps per CTA + the peer's producer
 constexpr int SCHED_CONSUMERS = 1 + 2 * EPI_WARPS + 1;
 
+// This lane's 32 row values -> the warp's swizzled staging tile -> one TMA bulk tensor
+// store of the warp's 32 x 32 box at (c0, r0) (the tile layout is exactly the
+// SWIZZLE_128B box layout; rows past the tensor's extent are clipped).  The warp waits
+// only until the previous store has READ the tile, never for global writes.
+__device__ __forceinline__ void tma_store32(float *stg, const CUtensorMap *map, int c0, int r0, const float *v,
+                                            int lane) {
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    *reinterpret_cast<float4 *>(stg + lane * 32 + 4 * (k ^ (lane & 7))) =
+        make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  if (lane == 0) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(r0), "r"(tc::smem_u32(stg))
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+}
+// tf32 hi/lo planes of 32 values through two TMA stores
+__device__ __forceinline__ void tma_store32_planes(float *stg, const CUtensorMap *mh, const CUtensorMap *ml, int c0,
+                                                   int r0, const float *v, int lane) {
+  float hi[32], lo[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) tc::split_tf32(v[k], hi[k], lo[k]);
+  tma_store32(stg, mh, c0, r0, hi, lane);
+  tma_store32(stg, ml, c0, r0, lo, lane);
+}
+
 // Row-contiguous output through a per-warp 32 x 32 shared tile.  Lane l holds
 // 32 consecutive outputs v[0..31] of row l (its TMEM lane); written to the
 // tile as 8 float4 chunks swizzled by (l & 7), read back 4 rows per
@@ -220,6 +252,9 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
                                                                 const __grid_constant__ CUtensorMap tmAl,
                                                                 const __grid_constant__ CUtensorMap tmBh,
                                                                 const __grid_constant__ CUtensorMap tmBl,
+                                                                const __grid_constant__ CUtensorMap tmC0,
+                                                                const __grid_constant__ CUtensorMap tmC1,
+                                                                const __grid_constant__ CUtensorMap tmC2,
                                                                 TcGemmArgs a) {
   using C_ = TileCfg<BN>;
   constexpr int TBN = BN, EPI_COLS = C_::EPI_COLS, TILE_B_BYTES = C_::TILE_B_BYTES, STAGE_BYTES = C_::STAGE_BYTES;
@@ -388,6 +423,7 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
       int mb, nb;
       tile_mn(t, mb, nb);
       const int m = mb * (2 * TBM) + (int)rank * TBM + q * 32 + lane;
+      const int row0 = mb * (2 * TBM) + (int)rank * TBM + q * 32;   // this warp's first row (TMA stores)
       const bool row_ok = m < a.M;
       const float rs = (EPI != EPI_RESID && row_ok && a.rinv) ? a.rinv[m] : 1.f;   // loaded under the k loop
       float acc[EPI_COLS];
@@ -433,6 +469,7 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
         for (int sl = 0; sl < EPI_COLS / 32; ++sl) {
           const int cb = nb * TBN + hc * EPI_COLS + sl * 32;
           if (cb >= a.N) continue;                              // warp-uniform
+          // (TMA stores measured slower here: three serialized stores per slice)
           const size_t o = (size_t)m * a.ldc + cb;
           store_rows32<ST_RESID>(stg, acc + sl * 32, row_ok ? a.C + o : nullptr, a.C_hi + o, a.C_lo + o, lane);
         }
@@ -446,10 +483,9 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
         {
 #pragma unroll
           for (int j = 0; j < 64; ++j) x[j] = __fmul_rn(x[j], rs);
-          if (EPI == EPI_HEAD) {
-            float *dst = row_ok ? a.C + (size_t)m * a.ldc + cb : nullptr;
-            store_rows32<ST_PLAIN>(stg, x, dst, nullptr, nullptr, lane);
-            store_rows32<ST_PLAIN>(stg, x + 32, dst ? dst + 32 : nullptr, nullptr, nullptr, lane);
+          if (EPI == EPI_HEAD) {   // logits through TMA bulk tensor stores (rows >= M clipped)
+            tma_store32(stg, &tmC0, cb, row0, x, lane);
+            tma_store32(stg, &tmC0, cb + 32, row0, x + 32, lane);
           } else if (EPI == EPI_SWIGLU) {
             // columns [cb, cb+32) are gate rows, [cb+32, cb+64) the matching up rows
 #pragma unroll
@@ -459,8 +495,7 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
               const float sg = __fdividef(g, __fadd_rn(1.f, tc::ex2(__fmul_rn(g, -1.44269504088896341f))));
               x[j] = __fmul_rn(sg, up);
             }
-            const size_t o = (size_t)m * a.ldc + cb / 2;
-            store_rows32<ST_SPLIT>(stg, x, row_ok ? a.C_hi + o : nullptr, a.C_lo + o, nullptr, lane);
+            tma_store32_planes(stg, &tmC1, &tmC2, cb / 2, row0, x, lane);   // act tf32 planes
           } else {  // EPI_QKV
             const int pos = row_ok ? a.rows.pos[m] : -1;
             const int nq = a.n_q_cols, nkv = a.n_kv_cols;
@@ -490,6 +525,8 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
       GEMM_MARK(4);   // output
     }
   }
+  if ((EPI == EPI_HEAD || EPI == EPI_SWIGLU) && warp < EPI_WARPS && lane == 0)
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // bulk stores complete before exit
   tc::fence_before();
   tc::cluster_sync();          // no CTA leaves while its pair may still signal or read it
   tc::fence_after();
@@ -595,7 +632,14 @@ static void launch_tc(const TcGemmArgs &a, const TcOperands &op, cudaStream_t s)
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_tc_kernel<EPI, BN>, *ah, *al, *bh, *bl, aa);
+  // output maps of the TMA-store epilogues: rows = M (clips the tile tail), 32 x 32 boxes
+  const CUtensorMap *c0 = bh, *c1 = bh, *c2 = bh;
+  if (EPI == EPI_HEAD) c0 = tmap_2d(a.C, (uint64_t)a.M, (uint64_t)a.ldc, 32);
+  if (EPI == EPI_SWIGLU) {
+    c1 = tmap_2d(a.C_hi, (uint64_t)a.M, (uint64_t)a.ldc, 32);
+    c2 = tmap_2d(a.C_lo, (uint64_t)a.M, (uint64_t)a.ldc, 32);
+  }
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_tc_kernel<EPI, BN>, *ah, *al, *bh, *bl, *c0, *c1, *c2, aa);
   if (e != cudaSuccess) throw std::runtime_error(std::string("gemm_tc launch: ") + cudaGetErrorString(e));
 }
 

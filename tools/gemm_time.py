@@ -17,6 +17,8 @@ if len(sys.argv) > 1 and sys.argv[1] == "one":
     B = rng.standard_normal((N, K), dtype=np.float32)
     nc.nc_debug_gemm(A, B, 0)
     sys.exit(0)
+if len(sys.argv) > 1 and sys.argv[1] == "cases":
+    CASES = [tuple([c.split(":")[0]] + [int(v) for v in c.split(":")[1:]]) for c in sys.argv[2:]]
 for name, M, N, K in CASES:
     for epi in (["head", "resid"] if name in ("o", "down") else ["head"]):
         for nostore in (0, 1):
