@@ -76,7 +76,9 @@ def _markov_tokens(V, n, seed, k=8):
 
 
 @pytest.mark.parametrize("V,n,flags,bits", [(49152, 400, 3, 24), (49152, 300, 1, 16), (256, 1500, 3, 24),
-                                            (256, 800, 2, 24), (16, 600, 3, 24), (4, 300, 3, 16)])
+                                            (256, 800, 2, 24), (16, 600, 3, 24), (4, 300, 3, 16),
+                                            (8192, 600, 3, 24),      # 4-CTA clusters (4096 <= V < 32768)
+                                            (16, 800, 7, 24)])       # skip flag (tiny V: confident N-gram)
 def test_walk_parity_synthetic(nc, V, n, flags, bits):
     from oracle.ensemble import Params, encode_tokens
     rng = np.random.default_rng(V + n)
