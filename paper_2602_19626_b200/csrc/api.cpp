@@ -1,12 +1,13 @@
 // extern "C" boundary of libnc.so (include/nc.h).  Argument marshalling,
 // error capture and container plumbing only; all compute is in the engine.
-#include <cstdio>
-#include <chrono>
 #include <cuda_runtime.h>
 
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "engine.hpp"
@@ -116,13 +117,31 @@ nc_status nc_model_info(const nc_model *m, uint32_t *vocab, uint32_t *n_layers, 
 static void tokenize_all(const nc_model *m, const uint8_t *in, size_t n, uint32_t n_chunks,
                          std::vector<uint32_t> &tokens, std::vector<uint32_t> &ntok) {
   std::vector<uint64_t> cuts = nc::split_chunks(in, n, n_chunks ? n_chunks : 1);
+  const size_t nc_ = cuts.size() - 1;
+  // chunks are independent: tokenize them on host threads (the trie is read-only)
+  std::vector<std::vector<uint32_t>> per(nc_);
+  const unsigned nt = std::max(1u, std::min<unsigned>((unsigned)nc_, std::thread::hardware_concurrency()));
+  auto work = [&](unsigned t) {
+    for (size_t c = t; c < nc_; c += nt) m->tok.encode(in + cuts[c], cuts[c + 1] - cuts[c], per[c]);
+  };
+  if (nt <= 1 || n < (1u << 16)) {
+    work(0);
+    if (nt > 1)
+      for (unsigned t = 1; t < nt; ++t) work(t);
+  } else {
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < nt; ++t) th.emplace_back(work, t);
+    for (auto &x : th) x.join();
+  }
   tokens.clear();
   ntok.clear();
-  for (size_t c = 0; c + 1 < cuts.size(); ++c) {
-    size_t before = tokens.size();
-    m->tok.encode(in + cuts[c], cuts[c + 1] - cuts[c], tokens);
-    if (tokens.size() - before > 0xFFFFFFFFull) nc::fail(NC_ERR_INVALID, "chunk too long");
-    ntok.push_back((uint32_t)(tokens.size() - before));
+  size_t total = 0;
+  for (auto &v : per) total += v.size();
+  tokens.reserve(total);
+  for (auto &v : per) {
+    if (v.size() > 0xFFFFFFFFull) nc::fail(NC_ERR_INVALID, "chunk too long");
+    ntok.push_back((uint32_t)v.size());
+    tokens.insert(tokens.end(), v.begin(), v.end());
   }
 }
 
