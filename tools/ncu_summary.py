@@ -10,6 +10,7 @@ import collections
 import csv
 import json
 import os
+import re
 import subprocess
 import sys
 
@@ -26,7 +27,8 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
         "launch__cluster_dim_x", "sm__cycles_elapsed.avg.per_second"]
 CLASS = {"attention_kernel": "attention", "walk_kernel": "walk", "attn_tc_kernel": "attention",
-         "walk_cl_kernel<4>": "walk", "nc::walk_cl_kernel<(int)4>": "walk", "nc::attn_tc_kernel": "attention", "gemm_tc_kernel<0>": "gemm_qkv",
+         "walk_cl_kernel<4>": "walk", "nc::walk_cl_kernel<(int)4>": "walk", "walk_cl_kernel<8>": "walk",
+         "nc::walk_cl_kernel<(int)8>": "walk", "nc::attn_tc_kernel": "attention", "gemm_tc_kernel<0>": "gemm_qkv",
          "gemm_tc_kernel<1>": "gemm_o|gemm_down", "gemm_tc_kernel<2>": "gemm_gateup", "gemm_tc_kernel<3>": "gemm_head"}
 
 
@@ -75,6 +77,7 @@ def full(tag, name, rep):
         rd = float(r[idx["dram__bytes_read.sum"]].replace(",", "")) * (1e6 if units[idx["dram__bytes_read.sum"]] == "Mbyte" else 1e3 if units[idx["dram__bytes_read.sum"]] == "Kbyte" else 1e9 if units[idx["dram__bytes_read.sum"]] == "Gbyte" else 1)
         wr = float(r[idx["dram__bytes_write.sum"]].replace(",", "")) * (1e6 if units[idx["dram__bytes_write.sum"]] == "Mbyte" else 1e3 if units[idx["dram__bytes_write.sum"]] == "Kbyte" else 1e9 if units[idx["dram__bytes_write.sum"]] == "Gbyte" else 1)
         base = kn.split("(")[0].replace("void ", "").strip()
+        base = re.sub(r"gemm_tc_kernel<(\d+), \d+>", r"gemm_tc_kernel<\1>", base)
         alts = CLASS.get(base, base).split("|")   # several classes share a kernel: capture order
         k_ = seen.get(base, 0)
         seen[base] = k_ + 1
