@@ -335,11 +335,16 @@ __device__ __forceinline__ void ng_hist_push(WalkState *st, uint32_t t) {
 }
 
 // ---------------------------------------------------- N-gram precompute ---
+// One warp per chunk, NGW warps (chunks) per CTA: each warp is a chain of dependent L2
+// round trips, so packing them onto few SMs costs little and leaves the SMs to the
+// forward running beside it.
+constexpr int NGW = 8;
 __global__ void ngram_pre_kernel(WalkArgs a) {
-  extern __shared__ uint32_t bitmap[];   // V/32 words
-  const int lane = threadIdx.x;
-  const int e = blockIdx.x;
+  extern __shared__ uint32_t ng_smem[];   // per warp: V/32 bitmap words
+  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+  const int e = blockIdx.x * NGW + wq;
   if (e >= a.n_entries) return;
+  uint32_t *bitmap = ng_smem + (size_t)wq * ((a.V + 31) / 32);
   const int c = a.chunk_of[e], count = a.count[e];
   WalkState *st = a.st + c;
   for (int w = lane; w < (int)((a.V + 31) / 32); w += 32) bitmap[w] = 0u;
@@ -370,7 +375,13 @@ __global__ void ngram_pre_kernel(WalkArgs a) {
 
 void launch_ngram_precompute(const WalkArgs &a, cudaStream_t s) {
   if (a.n_entries <= 0) return;
-  ngram_pre_kernel<<<a.n_entries, 32, ((a.V + 31) / 32) * sizeof(uint32_t), s>>>(a);
+  const size_t smem = (size_t)NGW * ((a.V + 31) / 32) * sizeof(uint32_t);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(ngram_pre_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  ngram_pre_kernel<<<(a.n_entries + NGW - 1) / NGW, 32 * NGW, smem, s>>>(a);
 }
 
 // ---------------------------------------------------------------- walk ---
