@@ -162,6 +162,12 @@ nc_status nc_profile(int cls, uint64_t *launches, double *ms, double *work, cons
 
 /* ---- test-only entry points (no side effects on models) ------------------ */
 
+/* Split-K policy of the tcgen05 GEMM (process-wide): 1 = automatic (default:
+ * split the k loop across CTAs when the tile grid would leave most SMs idle,
+ * e.g. decode steps), 0 = never.  Both give bit-identical results (the span
+ * partials are summed in the same order, D15); tests compare the two. */
+nc_status nc_debug_set_splitk(int mode);
+
 /* GPU quantizer on caller floats (host array p[V]): counts_out[V] (host) per
  * c_i = max(1, floor(p_i (T-V))) + residual to argmax (D4-D6).
  * "Integer CDFs bit-exact given identical float inputs" is checked with it. */

@@ -21,7 +21,7 @@ EXPORTS = [
     "nc_comm_init", "nc_comm_free", "nc_compress_shard", "nc_decompress_shard", "nc_free",
     "nc_last_error", "nc_last_stats", "nc_debug_quantize", "nc_debug_walk", "nc_debug_forward",
     "nc_host_split", "nc_host_wnc_encode", "nc_host_tokenize_vocab", "nc_host_shard_range",
-    "nc_host_shard_part", "nc_set_profiling", "nc_profile", "nc_debug_gemm", "nc_debug_attention",
+    "nc_host_shard_part", "nc_set_profiling", "nc_profile", "nc_debug_set_splitk", "nc_debug_gemm", "nc_debug_attention",
 ]
 
 
@@ -67,6 +67,7 @@ def lib():
             "nc_decompress_shard": (C.c_int, [P, P, P, C.c_size_t, C.POINTER(nc_params), P, pp, szp, u64p, u64p]),
             "nc_free": (None, [P]),
             "nc_set_profiling": (C.c_int, [C.c_int]),
+            "nc_debug_set_splitk": (C.c_int, [C.c_int]),
             "nc_profile": (C.c_int, [C.c_int, u64p, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                      C.POINTER(C.c_char_p)]),
             "nc_last_error": (C.c_char_p, []),
@@ -189,6 +190,10 @@ def nc_last_stats():
     k, w, f, h = C.c_uint64(), C.c_double(), C.c_double(), C.c_double()
     _check(lib().nc_last_stats(C.byref(k), C.byref(w), C.byref(f), C.byref(h)))
     return dict(kernel_launches=k.value, walk_ms=w.value, forward_ms=f.value, head_ms=h.value)
+
+
+def nc_debug_set_splitk(mode: int):
+    _check(lib().nc_debug_set_splitk(int(mode)))
 
 
 def nc_set_profiling(on: bool):

@@ -248,6 +248,10 @@ nc_status nc_last_stats(uint64_t *kernel_launches, double *walk_ms, double *forw
   return NC_OK;
 }
 
+nc_status nc_debug_set_splitk(int mode) {
+  return guard([&] { nc::set_splitk_mode(mode); });
+}
+
 nc_status nc_set_profiling(int on) {
   return guard([&] {
     nc::prof().reset();

@@ -465,6 +465,23 @@ __global__ void step_rows_kernel(const uint32_t *ntok, int n_chunks, int j, int3
   count[c] = act ? 1 : 0;
 }
 
+// decode step rows with the step index on the device (graph-replayable): reads j, then bumps it
+__global__ void step_rows_dev_kernel(const uint32_t *ntok, int n_chunks, int *jctr, int32_t *chunk, int32_t *pos,
+                                     AttnTile *tiles, int32_t *chunk_of, int32_t *row0, int32_t *count) {
+  const int j = *jctr;
+  for (int c = threadIdx.x; c < n_chunks; c += blockDim.x) {
+    const bool act = j < (int)ntok[c];
+    chunk[c] = c;
+    pos[c] = act ? j : -1;
+    tiles[c] = AttnTile{c, j, act ? 1 : 0, c};
+    chunk_of[c] = c;
+    row0[c] = c;
+    count[c] = act ? 1 : 0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *jctr = j + 1;
+}
+
 static uint32_t pow2_at_least(uint64_t x) {
   uint32_t p = 32;
   while (p < x) p <<= 1;
@@ -763,9 +780,29 @@ void encode_container(const Params &p, const std::vector<uint32_t> &ntok, const 
 }
 
 // ------------------------------------------------------------- decompress ---
+// A non-blocking stream owned by one decompression (a CUDA graph cannot be captured
+// on the legacy default stream the caller may pass); ordered after the caller's work.
+struct OwnStream {
+  cudaStream_t s = nullptr;
+  explicit OwnStream(cudaStream_t after) {
+    NC_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    cudaEvent_t e;
+    NC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    NC_CUDA(cudaEventRecord(e, after));
+    NC_CUDA(cudaStreamWaitEvent(s, e, 0));
+    cudaEventDestroy(e);
+  }
+  ~OwnStream() {
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+  }
+};
+
 void decompress_device(nc_model *m, const uint8_t *blob, const Nc05View &view, const Params &p,
-                       cudaStream_t s, std::vector<std::vector<uint32_t>> &toks) {
+                       cudaStream_t s_caller, std::vector<std::vector<uint32_t>> &toks) {
   NC_CUDA(cudaSetDevice(m->device));
+  OwnStream own(s_caller);
+  cudaStream_t s = own.s;
   const Shape &S = m->s;
   const int n_chunks = (int)view.ents.size();
   toks.assign(n_chunks, {});
@@ -811,23 +848,53 @@ void decompress_device(nc_model *m, const uint8_t *blob, const Nc05View &view, c
   wa.tok_off = tok_off_d; wa.streams = blob_d; wa.stream_off = s_off_d; wa.stream_bits = s_bits_d;
   wa.out_tok = out_tok; wa.next_x = x_cur; wa.mode = 1;
   wb.fill(wa, p, S.V);
+  int *jctr = bag.get<int>(1);
+  NC_CUDA(cudaMemsetAsync(jctr, 0, sizeof(int), s));
   cudaEvent_t e0, e1;
   NC_CUDA(cudaEventCreate(&e0));
   NC_CUDA(cudaEventCreate(&e1));
   NC_CUDA(cudaEventRecord(e0, s));
-  for (uint32_t j = 0; j < max_n; ++j) {
+  // one decode step: rows of step j (j on the device), forward of one row per chunk, walk
+  auto step = [&](uint32_t j) {
     double valid = 0;
     for (int c = 0; c < n_chunks; ++c) valid += j < ntok[c] ? 1 : 0;
     const double ctx = (double)j - window_start_h(j, p.window, p.slide) + 1;
-    PROF(K_MISC, 0, (step_rows_kernel<<<(n_chunks + 127) / 128, 128, 0, s>>>(ntok_d, n_chunks, (int)j, rchunk, rpos,
-                                                                           tiles, wc, wr, wn)));
+    PROF(K_MISC, 0, (step_rows_dev_kernel<<<1, 256, 0, s>>>(ntok_d, n_chunks, jctr, rchunk, rpos, tiles, wc, wr, wn)));
     RowMeta rows{x_cur, rchunk, rpos};
     fw.run(n_chunks, valid, 4.0 * S.H * S.dh * ctx * valid, rows, tiles, n_chunks, p, nullptr);
     PROF(K_WALK, 4.0 * S.V * valid, launch_walk(wa, s));
     st.launches += 2;
-    if ((j & 255) == 255) {
-      NC_CUDA(cudaGetLastError());
-      if (prof().on) { NC_CUDA(cudaStreamSynchronize(s)); prof().collect(); }
+  };
+  // Every step launches the same kernels with the same arguments (the step index lives
+  // on the device), so after one eager step (which also sizes every lazily allocated
+  // launcher buffer) the step is captured once as a CUDA graph and replayed.  Per-launch
+  // profiling (CUDA events around every kernel) runs eagerly instead.
+  const bool graph = !prof().on && !std::getenv("NC_DECODE_NO_GRAPH");
+  step(0);
+  if (graph && max_n > 1) {
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ge = nullptr;
+    const uint64_t l0 = st.launches;
+    NC_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    step(1);
+    NC_CUDA(cudaStreamEndCapture(s, &g));
+    const uint64_t per_step = st.launches - l0;
+    st.launches = l0;
+    NC_CUDA(cudaGraphInstantiate(&ge, g, 0));
+    for (uint32_t j = 1; j < max_n; ++j) {
+      NC_CUDA(cudaGraphLaunch(ge, s));
+      st.launches += per_step;
+      if ((j & 255) == 255) NC_CUDA(cudaGetLastError());
+    }
+    cudaGraphExecDestroy(ge);
+    cudaGraphDestroy(g);
+  } else {
+    for (uint32_t j = 1; j < max_n; ++j) {
+      step(j);
+      if ((j & 255) == 255) {
+        NC_CUDA(cudaGetLastError());
+        if (prof().on) { NC_CUDA(cudaStreamSynchronize(s)); prof().collect(); }
+      }
     }
   }
   NC_CUDA(cudaEventRecord(e1, s));
@@ -932,6 +999,7 @@ void debug_gemm(int device, const float *A, const float *B, uint32_t M, uint32_t
     // epilogue on a scratch h; NC_GEMM_NOSTORE=1: no epilogue writes) -> stderr
     if (const char *reps_s = getenv("NC_GEMM_REPS")) {
       const int reps = std::max(1, atoi(reps_s));
+      if (const char *sp = getenv("NC_GEMM_SPLIT")) set_splitk_mode(atoi(sp));
       const char *epi_s = getenv("NC_GEMM_EPI");
       const bool resid = epi_s && std::string(epi_s) == "resid";
       TcGemmArgs t = g;
@@ -953,6 +1021,7 @@ void debug_gemm(int device, const float *A, const float *B, uint32_t M, uint32_t
       cudaEventElapsedTime(&ms, e0, e1);
       cudaEventDestroy(e0); cudaEventDestroy(e1);
       const double us = 1e3 * ms / reps;
+      set_splitk_mode(1);
       fprintf(stderr, "gemm_tc M=%u N=%u K=%u epi=%s nostore=%d: %.1f us/launch, %.1f TFLOP/s (algorithmic)\n", M, N,
               K, resid ? "resid" : "head", t.no_store, us, 2.0 * M * N * K / (us * 1e-6) / 1e12);
       gemm_timing_report();

@@ -38,6 +38,8 @@ void check_cuda(cudaError_t e, const char *what);
 void *dev_alloc(size_t bytes, cudaStream_t s);
 void dev_free(void *p, cudaStream_t s);
 void set_allocator(void *(*a)(size_t, void *), void (*f)(void *, void *), void *ctx);
+// tcgen05 GEMM split-K policy (k_gemm_tc.cu): 1 automatic, 0 never
+void set_splitk_mode(int mode);
 
 struct Stats {
   uint64_t launches = 0;

@@ -18,6 +18,13 @@ struct TcGemmArgs {
   RowMeta rows; KvRing ring;
   const float *rope_cos, *rope_sin;
   int *tile_ctr;               // set by the launcher
+  // split-K (set by the launcher when the tile grid is much smaller than the SM count,
+  // e.g. decode steps of one row per chunk): sps = 64-wide k spans per work item (0 = off),
+  // ws = raw span partials [span][M][N] fp32, fix_ctr = per (tile, epilogue warp) arrival counters
+  int sps;
+  int a_box;                   // set by the launcher: rows of the A TMA box when M <= 128 (else 0)
+  float *ws;
+  int *fix_ctr;
   int no_store;                // diagnostics only (debug_gemm timing): skip the epilogue's global writes
 };
 
@@ -30,6 +37,8 @@ struct TcOperands {
 void launch_gemm_tc(GemmEpi epi, const TcGemmArgs &a, const TcOperands &op, cudaStream_t s);
 // SMs left out of persistent grids (occupied by a concurrently running walk)
 void set_reserved_sms(int n);
+// split-K policy: 1 automatic (default), 0 never (tests: bit identity of the two)
+void set_splitk_mode(int mode);
 // diagnostics build (-DNC_GEMM_TIMING): epilogue phase cycles -> stderr
 void gemm_timing_report();
 void launch_split_planes(const float *x, float *hi, float *lo, size_t n, cudaStream_t s);

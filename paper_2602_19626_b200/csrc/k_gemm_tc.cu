@@ -36,6 +36,14 @@
 // Row results do not depend on which other rows share the tile (each output
 // element is one fixed sequence of MMAs), so prefill and decode agree bit for
 // bit (D15).
+//
+// Split-K (decode: a few rows, a handful of tiles on 148 SMs).  A work item is
+// (tile, run of sps 64-wide k spans).  Every span still gets its own fresh TMEM
+// partial from the same MMA sequence; the epilogue warps write the raw partials
+// to a workspace instead of summing them, and the last warp to arrive for its
+// (tile, warp) region re-reads all partials and sums them in span order --
+// exactly the promotion sum of the unsplit kernel -- before running the same
+// epilogue code.  So split and unsplit launches give identical bits.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -61,6 +69,8 @@ constexpr int TBK = 32, TSTAGES = 3, NPART = 2, NSCHED = 4;
 // 2048 cycles, against 12 * 128 = 1536 MMA cycles per 32-wide k block -- so a
 // partial spans 2 k blocks (3072 MMA cycles) to keep the tensor pipe the bound.
 constexpr int KPP = 2;
+// split-K fixup: rows folded at once (all spans in flight) and the largest span count
+constexpr int SK_ROWS = 2, SK_MIN_SPANS = 16, SK_MAX_SPANS = 24;
 constexpr int EPI_WARPS = 8;
 constexpr int TILE_A_BYTES = TBM * TBK * 4;          // 16 KB
 constexpr int OUT_STAGE_BYTES = EPI_WARPS * 32 * 32 * 4;   // 32 KB: epilogue transpose tiles
@@ -247,7 +257,7 @@ __device__ unsigned long long g_gemm_clk[4 * 8];   // [EPI][phase]
 #define GEMM_MARK(k) do {} while (0)
 #endif
 
-template <int EPI, int BN>
+template <int EPI, int BN, bool SPLIT>
 __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_constant__ CUtensorMap tmAh,
                                                                 const __grid_constant__ CUtensorMap tmAl,
                                                                 const __grid_constant__ CUtensorMap tmBh,
@@ -274,6 +284,17 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
   const int num_m = (a.M + 2 * TBM - 1) / (2 * TBM), num_n = (a.N + TBN - 1) / TBN;
   const int n_tiles = num_m * num_n;
   const int nk = a.K / TBK;
+  const int nspan = (nk + KPP - 1) / KPP;
+  const int sps = (SPLIT && a.sps > 0) ? a.sps : nspan;      // spans per work item
+  const int nsplit = (nspan + sps - 1) / sps;
+  const int n_items = n_tiles * nsplit;
+  // work item -> tile, k-block range [kb_lo, kb_hi)
+  auto item_k = [&](int t, int &tile, int &kb_lo, int &kb_hi) {
+    tile = t / nsplit;
+    const int sp = t - tile * nsplit;
+    kb_lo = sp * sps * KPP;
+    kb_hi = min(nk, (sp + 1) * sps * KPP);
+  };
   // Claim order.  Many N tiles (vocab head, gate/up): bands of RB M tiles, M-fastest
   // inside a band, sweeping every N tile -- the band's A rows (RB x 256 rows, ~37 MB of
   // tf32 planes at K = 576) stay in L2 while B streams once per band.  (Plain
@@ -311,13 +332,18 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      // few rows (decode, M <= 128): A comes as an a_box-row box into the first rows of the
+      // leader's A tile and the peer loads no A at all (its rows 128.. are all >= M); the
+      // MMA still reads 128 rows, the extra rows only feed output rows that are never stored
+      const bool load_a = a.a_box == 0 || rank == 0;
+      const uint32_t stage_tx = a.a_box == 0 ? 2 * STAGE_BYTES : 2 * 2 * TILE_B_BYTES + 2 * a.a_box * TBK * 4;
       for (int jt = 0;; ++jt) {
         const int slot = jt % NSCHED;
         int t;
         if (rank == 0) {
           tc::mbar_wait(&sch_empty[slot], ((jt / NSCHED) & 1) ^ 1);
           const int claimed = atomicAdd(a.tile_ctr, 1);
-          t = claimed < n_tiles ? claimed : -1;
+          t = claimed < n_items ? claimed : -1;
           sch_tile[slot] = t;
           tc::st_cluster_s32(tc::mapa(&sch_tile[slot], 1), t);
           tc::mbar_arrive(&sch_full[slot]);
@@ -328,15 +354,18 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
           tc::mbar_arrive_remote(tc::mapa(&sch_empty[slot], 0));
         }
         if (t < 0) break;
-        int mb, nb;
-        tile_mn(t, mb, nb);
+        int mb, nb, tile, kb_lo, kb_hi;
+        item_k(t, tile, kb_lo, kb_hi);
+        tile_mn(tile, mb, nb);
         const int row_a = mb * 2 * TBM + (int)rank * TBM, row_b = nb * TBN + (int)rank * (TBN / 2);
-        for (int kb = 0; kb < nk; ++kb) {
+        for (int kb = kb_lo; kb < kb_hi; ++kb) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t *st = smem + stage * STAGE_BYTES;
-          if (rank == 0) tc::mbar_expect_tx(&full[stage], 2 * STAGE_BYTES);   // both CTAs' bytes
-          tc::tma_load_2d_pair(st, &tmAh, kb * TBK, row_a, &full[stage]);
-          tc::tma_load_2d_pair(st + TILE_A_BYTES, &tmAl, kb * TBK, row_a, &full[stage]);
+          if (rank == 0) tc::mbar_expect_tx(&full[stage], stage_tx);   // both CTAs' bytes
+          if (load_a) {
+            tc::tma_load_2d_pair(st, &tmAh, kb * TBK, row_a, &full[stage]);
+            tc::tma_load_2d_pair(st + TILE_A_BYTES, &tmAl, kb * TBK, row_a, &full[stage]);
+          }
           tc::tma_load_2d_pair(st + 2 * TILE_A_BYTES, &tmBh, kb * TBK, row_b, &full[stage]);
           tc::tma_load_2d_pair(st + 2 * TILE_A_BYTES + TILE_B_BYTES, &tmBl, kb * TBK, row_b, &full[stage]);
           if (++stage == TSTAGES) { stage = 0; phase ^= 1; }
@@ -357,12 +386,14 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
         const int t = sch_tile[slot];
         tc::mbar_arrive(&sch_empty[slot]);
         if (t < 0) break;
+        int tile, kb_lo, kb_hi;
+        item_k(t, tile, kb_lo, kb_hi);
         // one TMEM partial per KPP k blocks: all correction products of the span
         // first (the partial is still ~2^-11 of its final size, so their
         // truncations are negligible), then the hi*hi products -- 4 * KPP large-
         // magnitude truncations per partial; each stage is released after its hi*hi
-        for (int kb0 = 0; kb0 < nk; kb0 += KPP) {
-          const int nkp = min(KPP, nk - kb0);
+        for (int kb0 = kb_lo; kb0 < kb_hi; kb0 += KPP) {
+          const int nkp = min(KPP, kb_hi - kb0);
           tc::mbar_wait(&tempty[buf], buf_phase ^ 1);   // partial drained by both CTAs' epilogues
           const uint32_t d = tmem_base + buf * BN;
           int st = stage;
@@ -420,22 +451,25 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
 #ifdef NC_GEMM_TIMING
       if (threadIdx.x == 0) atomicAdd(&g_gemm_clk[EPI * 8 + 7], 1ull);
 #endif
-      int mb, nb;
-      tile_mn(t, mb, nb);
+      int mb, nb, tile, kb_lo, kb_hi;
+      item_k(t, tile, kb_lo, kb_hi);
+      tile_mn(tile, mb, nb);
       const int m = mb * (2 * TBM) + (int)rank * TBM + q * 32 + lane;
       const int row0 = mb * (2 * TBM) + (int)rank * TBM + q * 32;   // this warp's first row (TMA stores)
       const bool row_ok = m < a.M;
       const float rs = (EPI != EPI_RESID && row_ok && a.rinv) ? a.rinv[m] : 1.f;   // loaded under the k loop
+      constexpr bool split = SPLIT;   // (a split launch always has nsplit >= 2)
+      const int col0 = nb * TBN + hc * EPI_COLS;   // this warp's first column
       float acc[EPI_COLS];
       float *stg = stage_out + warp * 32 * 32;   // this warp's 32 x 32 transpose tile
       if (EPI == EPI_RESID && !a.no_store) {
         // residual rows of this warp's 32 x 128 block into L2 now (no registers); they
         // are read (from L2) and added after the promotion sum: h_new = h + sum_p P_p
         if (row_ok) {
-          const char *hrow = reinterpret_cast<const char *>(a.C + (size_t)m * a.ldc + nb * TBN + hc * EPI_COLS);
+          const char *hrow = reinterpret_cast<const char *>(a.C + (size_t)m * a.ldc + col0);
 #pragma unroll
           for (int l = 0; l < EPI_COLS * 4 / 128; ++l)
-            if (nb * TBN + hc * EPI_COLS + l * 32 < a.N) asm volatile("prefetch.global.L2 [%0];" ::"l"(hrow + l * 128));
+            if (col0 + l * 32 < a.N) asm volatile("prefetch.global.L2 [%0];" ::"l"(hrow + l * 128));
         }
       }
       {
@@ -443,25 +477,89 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
         for (int j = 0; j < EPI_COLS; ++j) acc[j] = 0.f;
       }
       GEMM_MARK(1);   // residual seed
-      for (int kb0 = 0; kb0 < nk; kb0 += KPP) {
+      for (int kb0 = kb_lo; kb0 < kb_hi; kb0 += KPP) {
         tc::mbar_wait(&tfull[buf], buf_phase);
         GEMM_MARK(2);   // waiting for partials
         tc::fence_after();
         const uint32_t taddr = tmem_base + buf * BN + hc * EPI_COLS + ((uint32_t)(q * 32) << 16);
+        if (split) {   // raw span partial -> workspace [span][M][N] (row-major per span)
+          float *wp = a.ws + ((size_t)(kb0 / KPP) * a.M + m) * a.N + col0;
 #pragma unroll
-        for (int c = 0; c < EPI_COLS / 16; ++c) {
-          uint32_t r[16];
-          tc::tmem_ld16(taddr + c * 16, r);
-          tc::tmem_wait_ld();
+          for (int c = 0; c < EPI_COLS / 16; ++c) {
+            uint32_t r[16];
+            tc::tmem_ld16(taddr + c * 16, r);
+            tc::tmem_wait_ld();
+            if (row_ok && col0 + c * 16 < a.N)   // N % 16 == 0: whole 16-column groups
 #pragma unroll
-          for (int j = 0; j < 16; ++j) acc[c * 16 + j] = __fadd_rn(acc[c * 16 + j], __uint_as_float(r[j]));
+              for (int j = 0; j < 16; j += 4)
+                __stcg(reinterpret_cast<float4 *>(wp + c * 16 + j),
+                       make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
+                                   __uint_as_float(r[j + 3])));
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < EPI_COLS / 16; ++c) {
+            uint32_t r[16];
+            tc::tmem_ld16(taddr + c * 16, r);
+            tc::tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) acc[c * 16 + j] = __fadd_rn(acc[c * 16 + j], __uint_as_float(r[j]));
+          }
         }
         tc::fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive_remote(tempty_leader + buf * 8);
         if (++buf == NPART) { buf = 0; buf_phase ^= 1; }
       }
+      GEMM_MARK(5);   // partials drained / written
+      if (split) {
+        // the last of the nsplit warps covering this (tile, warp) region sums every span's
+        // partial in span order (= the unsplit promotion sum) and runs the epilogue
+        if (!__any_sync(0xffffffffu, row_ok) || col0 >= a.N) continue;   // same decision in every split
+        __threadfence();
+        __syncwarp();
+        int last = 0;
+        if (lane == 0) {
+          int *ctr = a.fix_ctr + ((size_t)tile * 2 + rank) * EPI_WARPS + warp;
+          last = atomicAdd(ctr, 1) == nsplit - 1;
+          if (last) *ctr = 0;   // every arrival of this launch is in: reset for the next launch
+        }
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (!last) continue;
+        __threadfence();
+      }
+      // split-K fixup (only the last warp of a region gets here): dst[0..31] (lane = row) =
+      // (((0 + P_0) + P_1) + ...) of columns cc..cc+31, exactly the unsplit promotion sum.
+      // Folded with lane = column (coalesced 128 B workspace rows), every span of SK_ROWS
+      // rows in flight, through the warp's smem tile; done per epilogue block just before
+      // the block is consumed, so no more than one block of sums is live at a time.
+      auto fold32 = [&](float *dst, int cc) {
+        const int nr = min(32, a.M - row0);
+        const size_t sstride = (size_t)a.M * a.N;
+        const float *col_base = a.ws + col0 + cc + lane;
+        for (int r0 = 0; r0 < nr; r0 += SK_ROWS) {
+          float v[SK_ROWS][SK_MAX_SPANS];
 #pragma unroll
+          for (int rr = 0; rr < SK_ROWS; ++rr)
+#pragma unroll
+            for (int sp = 0; sp < SK_MAX_SPANS; ++sp)
+              v[rr][sp] = (sp < nspan && r0 + rr < nr)
+                              ? __ldcg(col_base + sp * sstride + (size_t)(row0 + r0 + rr) * a.N)
+                              : 0.f;
+#pragma unroll
+          for (int rr = 0; rr < SK_ROWS; ++rr) {
+            float sum = 0.f;
+#pragma unroll
+            for (int sp = 0; sp < SK_MAX_SPANS; ++sp)
+              if (sp < nspan) sum = __fadd_rn(sum, v[rr][sp]);
+            if (r0 + rr < nr) stg[(r0 + rr) * 32 + (lane ^ (r0 + rr))] = sum;
+          }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) dst[j] = stg[lane * 32 + (j ^ lane)];
+        __syncwarp();
+      };
       GEMM_MARK(3);   // draining partials
       if (a.no_store) continue;
       if (EPI == EPI_RESID) {   // residual: h += acc and the next tf32 planes, by 32-column slices
@@ -471,6 +569,7 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
           if (cb >= a.N) continue;                              // warp-uniform
           // (TMA stores measured slower here: three serialized stores per slice)
           const size_t o = (size_t)m * a.ldc + cb;
+          if (split) fold32(acc + sl * 32, sl * 32);
           store_rows32<ST_RESID>(stg, acc + sl * 32, row_ok ? a.C + o : nullptr, a.C_hi + o, a.C_lo + o, lane);
         }
       } else {
@@ -480,6 +579,10 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
         const int cb = nb * TBN + hc * EPI_COLS + half * 64;   // first column of this 64-wide block
         if (cb >= a.N) continue;                              // warp-uniform
         float *x = acc + half * 64;   // in place: the block's partial sums are dead after it
+        if (split) {
+          fold32(x, half * 64);
+          fold32(x + 32, half * 64 + 32);
+        }
         {
 #pragma unroll
           for (int j = 0; j < 64; ++j) x[j] = __fmul_rn(x[j], rs);
@@ -586,12 +689,46 @@ const CUtensorMap *tmap_2d(const float *ptr, uint64_t rows, uint64_t cols, uint3
 
 static int g_reserved_sms = 0;
 void set_reserved_sms(int n) { g_reserved_sms = n; }
+static int g_splitk_mode = 1;
+void set_splitk_mode(int mode) { g_splitk_mode = mode; }
 
 static int *tile_counter() {   // {next tile, CTAs done}; zero between launches
   static int *ctr = nullptr;
   if (!ctr) {
     if (cudaMalloc(&ctr, 2 * sizeof(int)) != cudaSuccess) throw std::runtime_error("cudaMalloc tile counter");
     cudaMemset(ctr, 0, 2 * sizeof(int));
+    cudaDeviceSynchronize();
+  }
+  return ctr;
+}
+
+// split-K workspace / fixup counters: grown on demand, never while a graph is captured
+static bool capturing(cudaStream_t s) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &st);
+  return st != cudaStreamCaptureStatusNone;
+}
+static cudaStream_t g_launch_stream = nullptr;
+static float *splitk_workspace(size_t floats) {
+  static float *ws = nullptr;
+  static size_t cap = 0;
+  if (floats > cap) {
+    if (capturing(g_launch_stream)) throw std::runtime_error("split-K workspace must be sized before graph capture");
+    if (ws) cudaFree(ws);
+    cap = std::max(floats, (size_t)1 << 20);
+    if (cudaMalloc(&ws, cap * sizeof(float)) != cudaSuccess) throw std::runtime_error("cudaMalloc split-K workspace");
+  }
+  return ws;
+}
+static int *splitk_counters(size_t n) {
+  static int *ctr = nullptr;
+  static size_t cap = 0;
+  if (n > cap) {
+    if (capturing(g_launch_stream)) throw std::runtime_error("split-K counters must be sized before graph capture");
+    if (ctr) cudaFree(ctr);
+    cap = std::max(n, (size_t)1 << 16);
+    if (cudaMalloc(&ctr, cap * sizeof(int)) != cudaSuccess) throw std::runtime_error("cudaMalloc split-K counters");
+    cudaMemset(ctr, 0, cap * sizeof(int));
     cudaDeviceSynchronize();
   }
   return ctr;
@@ -609,17 +746,46 @@ static int num_sms() {
 
 template <int EPI, int BN>
 static void launch_tc(const TcGemmArgs &a, const TcOperands &op, cudaStream_t s) {
+  g_launch_stream = s;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(gemm_tc_kernel<EPI, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, TileCfg<BN>::SMEM);
+    cudaFuncSetAttribute(gemm_tc_kernel<EPI, BN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         TileCfg<BN>::SMEM);
+    cudaFuncSetAttribute(gemm_tc_kernel<EPI, BN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         TileCfg<BN>::SMEM);
     attr = true;
   }
-  const CUtensorMap *ah = tmap_2d(op.A_hi, op.a_rows, a.K, TBM), *al = tmap_2d(op.A_lo, op.a_rows, a.K, TBM);
+  TcGemmArgs aa = a;
+  aa.a_box = a.M <= TBM ? (a.M + 7) / 8 * 8 : 0;   // rows of the A box (0: the full 128-row tile)
+  const uint32_t a_rows_box = aa.a_box ? aa.a_box : TBM;
+  const CUtensorMap *ah = tmap_2d(op.A_hi, op.a_rows, a.K, a_rows_box), *al = tmap_2d(op.A_lo, op.a_rows, a.K, a_rows_box);
   const CUtensorMap *bh = tmap_2d(op.B_hi, a.N, a.K, BN / 2), *bl = tmap_2d(op.B_lo, a.N, a.K, BN / 2);
   const int tiles = ((a.M + 2 * TBM - 1) / (2 * TBM)) * ((a.N + BN - 1) / BN);
-  const int pairs = std::min(tiles, std::max(1, (num_sms() - g_reserved_sms) / 2));
-  TcGemmArgs aa = a;
+  const int pairs_avail = std::max(1, (num_sms() - g_reserved_sms) / 2);
   aa.tile_ctr = tile_counter();
+  // split-K when the tile grid would leave most SMs idle (decode steps); bit-identical
+  // to the unsplit sum (see the kernel header); nc_debug_set_splitk(0) disables it.
+  const int nspan = (a.K / TBK + KPP - 1) / KPP;
+  int nsplit = 1;
+  aa.sps = 0;
+  // Measured at M = 8 (tools/splitk_time.py): every launch costs ~8 us fixed and each 32-wide
+  // k block ~0.9 us on one pair; the fixup's fold is a few dependent L2 round trips per 32
+  // columns, so splitting wins only for long k loops (down: K = 1536, 47 -> 37 us) and
+  // loses at K = 576 (25 -> 33-40 us).
+  if (g_splitk_mode != 0 && nspan >= SK_MIN_SPANS && nspan <= SK_MAX_SPANS && 2 * tiles <= pairs_avail &&
+      !a.no_store && a.N % 32 == 0) {
+    nsplit = std::min(nspan, pairs_avail / tiles);
+    aa.sps = (nspan + nsplit - 1) / nsplit;
+    nsplit = (nspan + aa.sps - 1) / aa.sps;
+    if (nsplit < 2) {
+      nsplit = 1;
+      aa.sps = 0;
+    } else {
+      aa.ws = splitk_workspace((size_t)nspan * a.N * a.M);
+      aa.fix_ctr = splitk_counters((size_t)tiles * 2 * EPI_WARPS);
+    }
+  }
+  const int pairs = std::min(tiles * nsplit, pairs_avail);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * pairs);
   cfg.blockDim = dim3(TC_THREADS);
@@ -639,7 +805,9 @@ static void launch_tc(const TcGemmArgs &a, const TcOperands &op, cudaStream_t s)
     c1 = tmap_2d(a.C_hi, (uint64_t)a.M, (uint64_t)a.ldc, 32);
     c2 = tmap_2d(a.C_lo, (uint64_t)a.M, (uint64_t)a.ldc, 32);
   }
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_tc_kernel<EPI, BN>, *ah, *al, *bh, *bl, *c0, *c1, *c2, aa);
+  const cudaError_t e =
+      nsplit > 1 ? cudaLaunchKernelEx(&cfg, gemm_tc_kernel<EPI, BN, true>, *ah, *al, *bh, *bl, *c0, *c1, *c2, aa)
+                 : cudaLaunchKernelEx(&cfg, gemm_tc_kernel<EPI, BN, false>, *ah, *al, *bh, *bl, *c0, *c1, *c2, aa);
   if (e != cudaSuccess) throw std::runtime_error(std::string("gemm_tc launch: ") + cudaGetErrorString(e));
 }
 
@@ -655,8 +823,8 @@ void gemm_timing_report() {
     if (x[7])
       fprintf(stderr,
               "gemm %-6s epilogue warp per tile (cycles): wait tile %.0f | residual prefetch %.0f | wait partials "
-              "%.0f | drain %.0f | output %.0f | tiles %.0f\n",
-              nm[e], x[0] / n, x[1] / n, x[2] / n, x[3] / n, x[4] / n, n);
+              "%.0f | drain %.0f | output %.0f | split write %.0f | split fixup %.0f | tiles %.0f\n",
+              nm[e], x[0] / n, x[1] / n, x[2] / n, x[3] / n, x[4] / n, x[5] / n, x[6] / n, n);
   }
   unsigned long long z[32] = {};
   cudaMemcpyToSymbol(g_gemm_clk, z, sizeof(z));

@@ -141,6 +141,28 @@ def test_prefill_decode_bit_identity(nc, m2, w2):
     assert np.array_equal(a, nc.nc_debug_forward(m2, x, prm2, 0))     # slab size invariance
 
 
+def test_splitk_bit_identity(nc, m2, w2):
+    """Split-K GEMMs (decode steps: a few rows, the k loop spread over CTAs) sum the
+    same per-span TMEM partials in the same order as the unsplit kernel (D15), so the
+    logits are bit-identical whichever way every GEMM of the forward runs."""
+    rng = np.random.default_rng(9)
+    n = 300
+    x = [0] + list(rng.integers(3, w2.V, n - 1))
+    prm = nc.nc_params_default(window=256, slide=128, max_slab_rows=256)
+    try:
+        nc.nc_debug_set_splitk(0)
+        a = nc.nc_debug_forward(m2, x, prm, 0)          # prefill, no split
+        b0 = nc.nc_debug_forward(m2, x[:40], prm, 1)    # decode, no split
+        nc.nc_debug_set_splitk(1)
+        b = nc.nc_debug_forward(m2, x, prm, 1)          # decode, split-K
+        c = nc.nc_debug_forward(m2, x, prm, 0)          # prefill, split where the grid is small
+    finally:
+        nc.nc_debug_set_splitk(1)
+    assert np.array_equal(a[:40], b0)
+    assert np.array_equal(a, b)
+    assert np.array_equal(a, c)
+
+
 # ------------------------------------------------------------ end to end ---
 def _oracle_size_and_p(w, data, prm_o):
     from oracle.chunking import split_chunks
