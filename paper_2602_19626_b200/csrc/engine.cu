@@ -571,6 +571,12 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
       while (*q && *q != ',') ++q;
       if (*q == ',') ++q;
     }
+  } else if (n_chunks <= 2) {
+    // Few chunks: the walk (~5 us per position, latency-bound, one cluster per chunk)
+    // outlasts the forward (~2.3 us per position per chunk), so start it early: a small
+    // first slab, then doubling -- the later forwards hide under the walk.
+    int len = 1024;
+    for (int pos = 0; pos < (int)max_n; pos += len, len = std::min(per_chunk, 2 * len)) plan.push_back(len);
   } else {
     const char *fs = std::getenv("NC_SLAB_FRAC");
     const double frac = fs ? std::min(0.95, std::max(0.05, std::atof(fs))) : 0.75;

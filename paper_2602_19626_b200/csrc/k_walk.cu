@@ -335,53 +335,232 @@ __device__ __forceinline__ void ng_hist_push(WalkState *st, uint32_t t) {
 }
 
 // ---------------------------------------------------- N-gram precompute ---
-// One warp per chunk, NGW warps (chunks) per CTA: each warp is a chain of dependent L2
-// round trips, so packing them onto few SMs costs little and leaves the SMs to the
-// forward running beside it.
-constexpr int NGW = 8;
+// Compression knows every token, so the N-gram side of the walk (predictions and count
+// updates) runs ahead of it.  Per token it is a chain of dependent L2 round
+// trips (hash probe -> record), so latency is what matters: each chunk gets FOUR warps,
+// warp k-1 owning order k's table.  Per token i:
+//   A  warp k: probe context k (hist) once -- the same key serves the prediction and the
+//      update -- and stage the record (n, nslot, tok[64], cnt[64]) in shared memory;
+//      mu_k, beta_k as in ng_predict_warp (f64)
+//   -- chunk barrier --
+//   B  warp 0: a0, a_k and the merged sparse list from the staged records, in the same
+//      order and with the same arithmetic as ng_predict_warp (first appearance over
+//      k = 1..4 then slots, adds accumulated in k order), into the ring entry
+//   C  warp k: the count update of order k from the staged record, writes only (same
+//      insert / increment / append / evict rules as ng_update_warp)
+//   -- chunk barrier --
+// so a token costs ~3 round trips instead of ~40 (one warp doing all orders twice).
+// The decoder runs ng_predict_warp / ng_update_warp inline on the same tables; both
+// produce identical lists and table states (round-trip tests).
+constexpr int NGC = 4;           // chunks per CTA (4 warps each)
+constexpr int NG_HASH = 512;     // merge position hash (>= 2 x kMaxSparse)
+struct NgStage {
+  uint32_t tok[kMaxOrders][kSlots], cnt[kMaxOrders][kSlots];
+  uint32_t n[kMaxOrders], ns[kMaxOrders], nrec[kMaxOrders], es[kMaxOrders];
+  int r[kMaxOrders];
+  double mu[kMaxOrders], beta[kMaxOrders];
+  unsigned long long key[kMaxOrders];
+  uint32_t hist[4];
+  uint32_t hkey[NG_HASH], hpos[NG_HASH];
+  uint32_t mtok[kMaxSparse];
+  float madd[kMaxSparse];
+};
+__host__ __device__ constexpr size_t ng_group_bytes(uint32_t V) {   // one chunk's shared memory, 16 B aligned
+  return (sizeof(NgStage) + ((V + 31) / 32) * 4 + 15) / 16 * 16;
+}
+__device__ __forceinline__ uint32_t ng_hslot(uint32_t tk) { return (tk * 2654435761u) >> (32 - 9); }
+
 __global__ void ngram_pre_kernel(WalkArgs a) {
-  extern __shared__ uint32_t ng_smem[];   // per warp: V/32 bitmap words
-  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
-  const int e = blockIdx.x * NGW + wq;
-  if (e >= a.n_entries) return;
-  uint32_t *bitmap = ng_smem + (size_t)wq * ((a.V + 31) / 32);
+  extern __shared__ __align__(16) uint8_t ng_raw[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int lc = w >> 2, kw = w & 3, k = kw + 1;     // chunk in CTA, order of this warp
+  const int e = blockIdx.x * NGC + lc;
+  if (e >= a.n_entries) return;                       // whole 4-warp groups exit together
+  const uint32_t nbw = (a.V + 31) / 32;
+  NgStage &S = *reinterpret_cast<NgStage *>(ng_raw + (size_t)lc * ng_group_bytes(a.V));
+  uint32_t *bitmap = reinterpret_cast<uint32_t *>(&S + 1);
+  const int bar = 1 + lc;
   const int c = a.chunk_of[e], count = a.count[e];
   WalkState *st = a.st + c;
-  for (int w = lane; w < (int)((a.V + 31) / 32); w += 32) bitmap[w] = 0u;
-  __syncwarp();
-  float *spadd = a.ng_spadd + (size_t)c * a.V;
+  const bool active = k <= (int)a.orders;
+  const size_t tb = (size_t)c * kMaxOrders + kw;
+  unsigned long long *keys = a.ng_keys + tb * a.hcap;
+  uint32_t *vals = a.ng_vals + tb * a.hcap;
+  NgRecord *recs = a.ng_recs + tb * a.rcap;
+  if (kw == 0) {
+    for (uint32_t x = lane; x < nbw; x += 32) bitmap[x] = 0u;
+    for (int x = lane; x < NG_HASH; x += 32) S.hkey[x] = 0xffffffffu;
+    if (lane < 4) S.hist[lane] = st->hist[lane];
+  }
+  if (lane == 0) S.nrec[kw] = st->nrec[kw];
+  const uint32_t i0 = st->ng_i;
+  asm volatile("bar.sync %0, 128;" ::"r"(bar) : "memory");
   for (int it = 0; it < count; ++it) {
-    const uint32_t i = st->ng_i;
-    const uint32_t t = a.tokens[a.tok_off[c] + i];
-    uint32_t hist[4];
+    const uint32_t i = i0 + it;
+    const uint32_t t = a.tokens[a.tok_off[c] + i];   // issued early: needed only by the update
+    // ---- A: probe + stage (order k)
+    if (active && i >= (uint32_t)k) {
+      uint32_t h[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) hist[j] = st->hist[j];
-    NgTok *out = a.ng_pre + (size_t)c * a.ng_ring + (i % a.ng_ring);
-    if (i >= a.warmup) {
-      ng_predict_warp(a, c, i, hist, spadd, bitmap, out, lane);
+      for (int j = 0; j < 4; ++j) h[j] = S.hist[j];
+      const unsigned long long key = fnv_ctx(k, h);
+      uint32_t es = 0xffffffffu;
+      const int r = ng_probe(keys, vals, a.hcap, key, lane, &es);
+      uint32_t ns = 0, n = 0, s = 0;
+      if (r >= 0) {
+        const NgRecord *R = recs + r;
+        ns = R->nslot;
+        n = R->n;
+        const uint32_t t0 = R->tok[lane], t1 = R->tok[lane + 32], c0 = R->cnt[lane], c1 = R->cnt[lane + 32];
+        S.tok[kw][lane] = t0; S.tok[kw][lane + 32] = t1;
+        S.cnt[kw][lane] = c0; S.cnt[kw][lane + 32] = c1;
+        if ((uint32_t)lane < ns) s += c0;
+        if ((uint32_t)lane + 32 < ns) s += c1;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      }
+      if (lane == 0) {
+        S.r[kw] = r; S.es[kw] = es; S.ns[kw] = ns; S.n[kw] = n; S.key[kw] = key;
+        if (r >= 0) {
+          const double nd = (double)n;
+          const double lam = __ddiv_rn(nd, __dadd_rn(nd, 5.0));
+          S.mu[kw] = __dsub_rn(1.0, __ddiv_rn(__dmul_rn(lam, (double)s), nd));
+          S.beta[kw] = __ddiv_rn(lam, nd);
+        } else {
+          S.mu[kw] = 1.0;
+          S.beta[kw] = 0.0;
+        }
+      }
     } else if (lane == 0) {
-      out->n = 0;
-      out->a0f = 0.f;
+      S.r[kw] = -1; S.ns[kw] = 0; S.mu[kw] = 1.0; S.beta[kw] = 0.0; S.es[kw] = 0xffffffffu;
     }
-    ng_update_warp(a, c, i, hist, t, st, lane);
-    if (lane == 0) {
-      ng_hist_push(st, t);
-      st->ng_i = i + 1;
+    asm volatile("bar.sync %0, 128;" ::"r"(bar) : "memory");
+    // ---- B: merged prediction (warp 0)
+    if (kw == 0) {
+      NgTok *out = a.ng_pre + (size_t)c * a.ng_ring + (i % a.ng_ring);
+      if (i >= a.warmup) {
+        double a0 = 1.0;
+        for (int kk = 1; kk <= (int)a.orders; ++kk) a0 = __dmul_rn(a0, S.mu[kk - 1]);
+        uint32_t nout = 0;
+        for (int kk = 1; kk <= (int)a.orders; ++kk) {
+          if (S.r[kk - 1] < 0) continue;
+          double ak = S.beta[kk - 1];
+          for (int j = kk + 1; j <= (int)a.orders; ++j) ak = __dmul_rn(ak, S.mu[j - 1]);
+          const uint32_t ns = S.ns[kk - 1];
+          for (uint32_t s0 = 0; s0 < ns; s0 += 32) {
+            const uint32_t sl = s0 + lane;
+            const bool act = sl < ns;
+            uint32_t tk = 0, pos = 0;
+            bool first = false;
+            float add = 0.f;
+            if (act) {
+              tk = S.tok[kk - 1][sl];
+              add = (float)__dmul_rn(ak, (double)S.cnt[kk - 1][sl]);
+              const uint32_t bit = 1u << (tk & 31);
+              first = !(atomicOr(&bitmap[tk >> 5], bit) & bit);
+            }
+            const unsigned fm = __ballot_sync(0xffffffffu, act && first);
+            if (act && first) {
+              pos = nout + __popc(fm & ((1u << lane) - 1));
+              S.mtok[pos] = tk;
+              S.madd[pos] = add;
+              uint32_t hs = ng_hslot(tk);
+              while (atomicCAS(&S.hkey[hs], 0xffffffffu, tk) != 0xffffffffu) hs = (hs + 1) & (NG_HASH - 1);
+              S.hpos[hs] = pos;
+            }
+            __syncwarp();
+            if (act && !first) {   // seen in a lower order (ids are unique within one order)
+              uint32_t hs = ng_hslot(tk);
+              while (S.hkey[hs] != tk) hs = (hs + 1) & (NG_HASH - 1);
+              pos = S.hpos[hs];
+              S.madd[pos] = __fadd_rn(S.madd[pos], add);
+            }
+            nout += __popc(fm);
+            __syncwarp();
+          }
+        }
+        __syncwarp();
+        for (uint32_t j = lane; j < nout; j += 32) {
+          const uint32_t tk = S.mtok[j];
+          out->tok[j] = tk;
+          out->add[j] = S.madd[j];
+          bitmap[tk >> 5] = 0u;
+        }
+        for (int x = lane; x < NG_HASH; x += 32) S.hkey[x] = 0xffffffffu;
+        if (lane == 0) {
+          out->n = nout;
+          out->a0f = (float)__ddiv_rn(a0, (double)i + (double)a.V);
+        }
+      } else if (lane == 0) {
+        out->n = 0;
+        out->a0f = 0.f;
+      }
+    }
+    // ---- C: count update of order k with token t (writes only)
+    if (active && i >= (uint32_t)k) {
+      int r = S.r[kw];
+      bool fresh = false;
+      if (r < 0) {
+        const uint32_t used = S.nrec[kw], es = S.es[kw];
+        if (!(used >= a.cap || used >= a.rcap || es == 0xffffffffu)) {   // capacity freeze (D22)
+          r = (int)used;
+          fresh = true;
+          if (lane == 0) {
+            S.nrec[kw] = used + 1;
+            keys[es] = S.key[kw];
+            vals[es] = (uint32_t)r;
+          }
+        }
+      }
+      if (r >= 0) {
+        NgRecord *R = recs + r;
+        const uint32_t ns = fresh ? 0u : S.ns[kw];
+        const uint32_t n = fresh ? 0u : S.n[kw];
+        const bool h0 = (uint32_t)lane < ns && S.tok[kw][lane] == t;
+        const bool h1 = (uint32_t)lane + 32 < ns && S.tok[kw][lane + 32] == t;
+        const unsigned m0 = __ballot_sync(0xffffffffu, h0), m1 = __ballot_sync(0xffffffffu, h1);
+        if (m0 | m1) {
+          if (h0) R->cnt[lane] = S.cnt[kw][lane] + 1;
+          if (h1) R->cnt[lane + 32] = S.cnt[kw][lane + 32] + 1;
+        } else if (ns < kSlots) {
+          if (lane == 0) { R->tok[ns] = t; R->cnt[ns] = 1; R->nslot = ns + 1; }
+        } else {   // evict the lowest count, ties -> lowest slot (D21)
+          uint32_t bcnt = S.cnt[kw][lane], bidx = lane;
+          if (S.cnt[kw][lane + 32] < bcnt) { bcnt = S.cnt[kw][lane + 32]; bidx = lane + 32; }
+#pragma unroll
+          for (int o = 16; o; o >>= 1) {
+            const uint32_t oc = __shfl_xor_sync(0xffffffffu, bcnt, o), oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+            if (oc < bcnt || (oc == bcnt && oi < bidx)) { bcnt = oc; bidx = oi; }
+          }
+          if (lane == 0) { R->tok[bidx] = t; R->cnt[bidx] = 1; }
+        }
+        if (lane == 0) R->n = n + 1;
+      }
     }
     __syncwarp();
     __threadfence_block();
+    if (kw == 0 && lane == 0) {
+      S.hist[0] = S.hist[1]; S.hist[1] = S.hist[2]; S.hist[2] = S.hist[3]; S.hist[3] = t;
+    }
+    asm volatile("bar.sync %0, 128;" ::"r"(bar) : "memory");
+  }
+  if (lane == 0) st->nrec[kw] = S.nrec[kw];
+  if (kw == 0 && lane == 0) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) st->hist[j] = S.hist[j];
+    st->ng_i = i0 + (uint32_t)count;
   }
 }
 
 void launch_ngram_precompute(const WalkArgs &a, cudaStream_t s) {
   if (a.n_entries <= 0) return;
-  const size_t smem = (size_t)NGW * ((a.V + 31) / 32) * sizeof(uint32_t);
+  const size_t smem = (size_t)NGC * ng_group_bytes(a.V);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(ngram_pre_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  ngram_pre_kernel<<<(a.n_entries + NGW - 1) / NGW, 32 * NGW, smem, s>>>(a);
+  ngram_pre_kernel<<<(a.n_entries + NGC - 1) / NGC, 128 * NGC, smem, s>>>(a);
 }
 
 // ---------------------------------------------------------------- walk ---

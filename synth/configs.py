@@ -68,6 +68,10 @@ WORKLOADS = {
                         notes="10 MB, 64 chunks per GPU"),
     "config4": Workload("config4", "smollm2-135m", "enwik", 100_000_000, 1004, 2048, 512, 512,
                         notes="100 MB enwik8-shaped, 8x64 chunks"),
+    # one rank's share of config 4 (100 MB / 8 GPUs, 64 chunks): what each GPU of the 8-GPU
+    # run compresses (weak scaling); bench.py --gpus N runs N such shares
+    "config4_shard": Workload("config4_shard", "smollm2-135m", "enwik", 12_500_000, 1004, 2048, 512, 64,
+                              notes="12.5 MB enwik8-shaped, 64 chunks: one GPU's share of config 4"),
     "config5_l512": Workload("config5_l512", "smollm2-135m", "alice", 152089, 1002, 512, 128, 8),
     "config5_l1024": Workload("config5_l1024", "smollm2-135m", "alice", 152089, 1002, 1024, 256, 8),
     "config5_cdf16": Workload("config5_cdf16", "smollm2-135m", "alice", 152089, 1002, 2048, 512, 8,
