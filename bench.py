@@ -135,7 +135,7 @@ def main():
     args = ap.parse_args()
     rank, world, local = dist_env()
 
-    from synth import WORKLOADS, ensure_model, ensure_text, make_text
+    from synth import SHAPES, WORKLOADS, ensure_model, ensure_text, make_text
     wl = WORKLOADS[args.workload]
     metric, unit = "compress_bytes_per_sec", "B/s"
 
@@ -196,6 +196,7 @@ def main():
         ntok.append(len(t))
     tokens = np.concatenate(toks) if toks else np.zeros(0, np.uint32)
     tok_dev = torch.from_numpy(tokens.view(np.int32).copy()).to(f"cuda:{local}")
+    my_chunks = c1 - c0
     my_prm = nc.nc_params_default(window=wl.window, slide=wl.slide, n_chunks=max(1, c1 - c0), cdf_bits=wl.cdf_bits)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=f"cuda:{local}")   # > 126 MB L2
 
@@ -289,7 +290,12 @@ def main():
     # 3xTF32 on tcgen05: algorithmic FLOPs run as 3 tf32 MMAs; tf32 dense = bf16 dense / 2
     # (B200_PROFILING.md nominal ratio).  Kernels are timed inside a long step -> sustained peak.
     tc_peak = float(pk.get("bf16_tflops_sustained", pk["bf16_tflops"])) / 2.0 / 3.0
-    dom = max(kernels, key=lambda k: kernels[k]["ms_per_step"]) if kernels else None
+    # dominant kernel = largest share of the GPU's SM-time.  Every forward kernel runs on
+    # all SMs; the walk holds one thread-block cluster per chunk (walk_ctas_per_chunk SMs)
+    # and overlaps the next slab's forward, so its device time alone overstates its share.
+    walk_sms = min(N_SM, my_chunks * nc.nc_host_walk_ctas(SHAPES[wl.shape].vocab)) if my_chunks else N_SM
+    sm_share = {k: kernels[k]["ms_per_step"] * (walk_sms if k == "walk" else N_SM) for k in kernels}
+    dom = max(kernels, key=lambda k: sm_share[k]) if kernels else None
     roof = None
     traffic = None
     try:
@@ -321,6 +327,11 @@ def main():
     walk = kernels.get("walk")
     if walk:
         kernels["walk"]["hbm_gbs"] = walk["work_per_step"] / (walk["ms_per_step"] / 1e3) / 1e9
+        kernels["walk"]["hbm_frac"] = kernels["walk"]["hbm_gbs"] / pk["hbm_gbs"]
+        kernels["walk"]["sms"] = walk_sms
+        kernels["walk"]["us_per_token_per_chunk"] = 1e3 * walk["ms_per_step"] / max(1, max(ntok) if ntok else 1)
+    for k in kernels:
+        kernels[k]["sm_time_share"] = sm_share[k] / (N_SM * 1000 * t_val / args.steps)
     for k in flop_classes & set(kernels):
         kernels[k]["tflops"] = kernels[k]["work_per_step"] / (kernels[k]["ms_per_step"] / 1e3) / 1e12
 

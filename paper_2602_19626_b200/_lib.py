@@ -20,7 +20,7 @@ EXPORTS = [
     "nc_compress", "nc_decompress", "nc_tokenize", "nc_compress_tokens", "nc_comm_unique_id",
     "nc_comm_init", "nc_comm_free", "nc_compress_shard", "nc_decompress_shard", "nc_free",
     "nc_last_error", "nc_last_stats", "nc_debug_quantize", "nc_debug_walk", "nc_debug_forward",
-    "nc_host_split", "nc_host_wnc_encode", "nc_host_tokenize_vocab", "nc_host_shard_range",
+    "nc_host_split", "nc_host_wnc_encode", "nc_host_tokenize_vocab", "nc_host_shard_range", "nc_host_walk_ctas",
     "nc_host_shard_part", "nc_set_profiling", "nc_profile", "nc_debug_set_splitk", "nc_debug_gemm", "nc_debug_attention",
 ]
 
@@ -83,6 +83,7 @@ def lib():
             "nc_host_wnc_encode": (C.c_int, [u32p, u32p, C.c_size_t, C.c_uint32, pp, szp, u64p]),
             "nc_host_tokenize_vocab": (C.c_int, [P, u32p, C.c_uint32, C.c_uint32, P, C.c_size_t, pp, szp]),
             "nc_host_shard_range": (C.c_int, [C.c_uint32, C.c_int, C.c_int, u32p, u32p]),
+            "nc_host_walk_ctas": (C.c_int, [C.c_uint32, u32p]),
             "nc_host_shard_part": (C.c_int, [u32p, C.c_uint32, C.c_uint8, C.c_uint16, C.c_int, C.c_int, P,
                                              C.c_size_t, pp, szp, u64p, u64p]),
         }
@@ -281,6 +282,12 @@ def nc_host_tokenize_vocab(vocab, data: bytes, n_special: int = 3):
     t, nt = C.c_void_p(), C.c_size_t()
     _check(lib().nc_host_tokenize_vocab(blob, lp, len(vocab), n_special, data, len(data), C.byref(t), C.byref(nt)))
     return _take_array(t.value, nt.value, np.uint32).tolist()
+
+
+def nc_host_walk_ctas(V: int) -> int:
+    n = C.c_uint32()
+    _check(lib().nc_host_walk_ctas(V, C.byref(n)))
+    return n.value
 
 
 def nc_host_shard_range(n_chunks: int, world: int, rank: int):

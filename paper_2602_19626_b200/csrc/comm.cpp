@@ -13,6 +13,7 @@
 #include <numeric>
 
 #include "engine.hpp"
+#include "walk.cuh"
 
 struct nc_comm {
   ncclComm_t comm = nullptr;
@@ -264,6 +265,12 @@ nc_status nc_decompress_shard(nc_model *m, nc_comm *c, const uint8_t *in, size_t
 }
 
 // host-only pieces of the shard plan, exported for the gloo multi-process tests
+nc_status nc_host_walk_ctas(uint32_t V, uint32_t *ctas) {
+  if (!ctas) return NC_ERR_INVALID;
+  *ctas = (uint32_t)nc::walk_ctas_per_chunk(V);
+  return NC_OK;
+}
+
 nc_status nc_host_shard_range(uint32_t n_chunks, int world, int rank, uint32_t *c0, uint32_t *c1) {
   if (!c0 || !c1 || world < 1 || rank < 0 || rank >= world) return NC_ERR_INVALID;
   nc::shard_range(n_chunks, world, rank, *c0, *c1);

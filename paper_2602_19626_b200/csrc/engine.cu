@@ -674,7 +674,13 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
   wb.fill(wbase, p, S.V);
   for (int sl = 0; sl < n_slabs; ++sl) {
     if (use_ng) {
-      if (sl >= 2) NC_CUDA(cudaStreamWaitEvent(ns, ev[4 * (sl - 2) + 3], 0));   // ring slots free again
+      // ring slot p % ng_ring of this slab's positions last held position p - ng_ring: wait
+      // for the walk of the last slab holding such a position (none while within the ring)
+      const int64_t need = (int64_t)slab_pos0[sl] + slab_len[sl] - (int64_t)wb.ng_ring;
+      int q = -1;
+      for (int k2 = 0; k2 < sl; ++k2)
+        if (slab_pos0[k2] < need) q = k2;
+      if (q >= 0) NC_CUDA(cudaStreamWaitEvent(ns, ev[4 * q + 3], 0));
       WalkArgs na = wbase;
       na.chunk_of = wc_d + w_off[sl]; na.row0 = wr_d + w_off[sl]; na.count = wn_d + w_off[sl];
       na.n_entries = w_off[sl + 1] - w_off[sl];

@@ -68,7 +68,10 @@ constexpr int TBK = 32, TSTAGES = 3, NPART = 2, NSCHED = 4;
 // (128 KB) per CTA; tcgen05.ld moves ~64 B/cycle/SM (B300_MICROARCH), i.e.
 // 2048 cycles, against 12 * 128 = 1536 MMA cycles per 32-wide k block -- so a
 // partial spans 2 k blocks (3072 MMA cycles) to keep the tensor pipe the bound.
-constexpr int KPP = 2;
+#ifndef NC_KPP
+#define NC_KPP 2
+#endif
+constexpr int KPP = NC_KPP;
 // split-K fixup: rows folded at once (all spans in flight) and the largest span count
 constexpr int SK_ROWS = 2, SK_MIN_SPANS = 16, SK_MAX_SPANS = 24;
 constexpr int EPI_WARPS = 8;
