@@ -29,7 +29,10 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
 CLASS = {"attention_kernel": "attention", "walk_kernel": "walk", "attn_tc_kernel": "attention",
          "walk_cl_kernel<4>": "walk", "nc::walk_cl_kernel<(int)4>": "walk", "walk_cl_kernel<8>": "walk",
          "nc::walk_cl_kernel<(int)8>": "walk", "nc::attn_tc_kernel": "attention", "gemm_tc_kernel<0>": "gemm_qkv",
-         "gemm_tc_kernel<1>": "gemm_o|gemm_down", "gemm_tc_kernel<2>": "gemm_gateup", "gemm_tc_kernel<3>": "gemm_head"}
+         "gemm_tc_kernel<1>": "gemm_o|gemm_down", "gemm_tc_kernel<2>": "gemm_gateup", "gemm_tc_kernel<3>": "gemm_head",
+         "nc::gemm_tc_kernel<0>": "gemm_qkv", "nc::gemm_tc_kernel<1>": "gemm_o|gemm_down",
+         "nc::gemm_tc_kernel<2>": "gemm_gateup", "nc::gemm_tc_kernel<3>": "gemm_head",
+         "ngram_pre_kernel": "ngram", "nc::ngram_pre_kernel": "ngram"}
 
 
 def to_ns(v, u):
@@ -77,7 +80,7 @@ def full(tag, name, rep):
         rd = float(r[idx["dram__bytes_read.sum"]].replace(",", "")) * (1e6 if units[idx["dram__bytes_read.sum"]] == "Mbyte" else 1e3 if units[idx["dram__bytes_read.sum"]] == "Kbyte" else 1e9 if units[idx["dram__bytes_read.sum"]] == "Gbyte" else 1)
         wr = float(r[idx["dram__bytes_write.sum"]].replace(",", "")) * (1e6 if units[idx["dram__bytes_write.sum"]] == "Mbyte" else 1e3 if units[idx["dram__bytes_write.sum"]] == "Kbyte" else 1e9 if units[idx["dram__bytes_write.sum"]] == "Gbyte" else 1)
         base = kn.split("(")[0].replace("void ", "").strip()
-        base = re.sub(r"gemm_tc_kernel<(\d+), \d+>", r"gemm_tc_kernel<\1>", base)
+        base = re.sub(r"gemm_tc_kernel<\(?\w*\)?(\d+), \(?\w*\)?\d+(, \(?\w*\)?\w+)?>", r"gemm_tc_kernel<\1>", base)
         alts = CLASS.get(base, base).split("|")   # several classes share a kernel: capture order
         k_ = seen.get(base, 0)
         seen[base] = k_ + 1
