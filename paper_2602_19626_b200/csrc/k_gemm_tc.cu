@@ -63,7 +63,7 @@ namespace nc {
 constexpr int TBM = 128;              // rows per CTA (pair tile: 256)
 // BN = pair tile columns (MMA N; each CTA stages BN / 2 rows of B): 256, or 192 for
 // the N = 576 residual GEMMs (576 = 3 x 192: no padded MMA work, smaller output bursts)
-constexpr int TBK = 32, TSTAGES = 3, NPART = 2, NSCHED = 4;
+constexpr int TBK = 32, NPART = 2, NSCHED = 4;
 // k blocks per TMEM partial.  Promotion reads the whole 128 x 256 fp32 partial
 // (128 KB) per CTA; tcgen05.ld moves ~64 B/cycle/SM (B300_MICROARCH), i.e.
 // 2048 cycles, against 12 * 128 = 1536 MMA cycles per 32-wide k block -- so a
@@ -83,7 +83,10 @@ struct TileCfg {
   static constexpr int EPI_COLS = BN / 2;                                // columns per epilogue warp
   static constexpr int TILE_B_BYTES = (BN / 2) * TBK * 4;                // 16 / 12 KB
   static constexpr int STAGE_BYTES = 2 * TILE_A_BYTES + 2 * TILE_B_BYTES;   // 64 / 56 KB per CTA
-  static constexpr int SMEM = TSTAGES * STAGE_BYTES + OUT_STAGE_BYTES + 1024 /*align*/ + 512 /*barriers*/;
+  // pipeline depth: 3 stages of 64 / 56 KB; the 128-wide tiles (decode steps, whose k loop
+  // is bound by TMA round trips rather than MMAs) fit a fourth 48 KB stage
+  static constexpr int STAGES = BN == 128 ? 4 : 3;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + OUT_STAGE_BYTES + 1024 /*align*/ + 512 /*barriers*/;
   static_assert(NPART * BN <= TMEM_COLS && BN % 32 == 0, "tile");
 };
 constexpr int TC_THREADS = 320;
@@ -271,6 +274,8 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
                                                                 TcGemmArgs a) {
   using C_ = TileCfg<BN>;
   constexpr int TBN = BN, EPI_COLS = C_::EPI_COLS, TILE_B_BYTES = C_::TILE_B_BYTES, STAGE_BYTES = C_::STAGE_BYTES;
+  constexpr int TSTAGES = C_::STAGES;
+  static_assert(KPP <= TSTAGES, "a partial's k blocks must fit the pipeline (corrections-first MMA order)");
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float *stage_out = reinterpret_cast<float *>(smem + TSTAGES * STAGE_BYTES);
@@ -473,6 +478,15 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
 #pragma unroll
           for (int l = 0; l < EPI_COLS * 4 / 128; ++l)
             if (col0 + l * 32 < a.N) asm volatile("prefetch.global.L2 [%0];" ::"l"(hrow + l * 128));
+        }
+      }
+      if (EPI == EPI_QKV && !a.no_store && row_ok && col0 < a.n_q_cols + a.n_kv_cols) {
+        // this row's RoPE cos/sin lines into L1 under the k loop: the epilogue reads them
+        // (4 rows per instruction) once per head; each was an exposed L2 round trip
+        const int pr = a.rows.pos[m];
+        if (pr >= 0) {
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(a.rope_cos + (size_t)pr * 32));
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(a.rope_sin + (size_t)pr * 32));
         }
       }
       {
@@ -838,9 +852,22 @@ void launch_gemm_tc(GemmEpi epi, const TcGemmArgs &a, const TcOperands &op, cuda
   if (a.M <= 0) return;
   if (a.K % TBK) throw std::runtime_error("tcgen05 GEMM needs K % 32 == 0");
   switch (epi) {
-    case EPI_QKV: launch_tc<EPI_QKV, 256>(a, op, s); break;
-    case EPI_RESID: launch_tc<EPI_RESID, 192>(a, op, s); break;   // N = 576 = 3 x 192
-    case EPI_SWIGLU: launch_tc<EPI_SWIGLU, 256>(a, op, s); break;
+    // Few rows (decode steps, M <= 128): a tile's time is its k loop of pair MMAs, which
+    // cost in proportion to N (128 cycles at N = 256, 64 at N = 128), so 128-wide tiles halve
+    // it and double the tiles in flight.  Each output element is the same MMA sequence
+    // whatever the tile width (D15; test_splitk_bit_identity compares prefill and decode).
+    case EPI_QKV:
+      if (a.M <= TBM) launch_tc<EPI_QKV, 128>(a, op, s);
+      else launch_tc<EPI_QKV, 256>(a, op, s);
+      break;
+    case EPI_RESID:
+      if (a.M <= TBM) launch_tc<EPI_RESID, 128>(a, op, s);
+      else launch_tc<EPI_RESID, 192>(a, op, s);   // N = 576 = 3 x 192
+      break;
+    case EPI_SWIGLU:
+      if (a.M <= TBM) launch_tc<EPI_SWIGLU, 128>(a, op, s);
+      else launch_tc<EPI_SWIGLU, 256>(a, op, s);
+      break;
     case EPI_HEAD: launch_tc<EPI_HEAD, 256>(a, op, s); break;
   }
 }
