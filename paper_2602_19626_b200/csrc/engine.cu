@@ -409,7 +409,7 @@ struct Forward {
         gd.C = h; gd.ldc = S.d;
         PROF(K_DOWN, 2.0 * valid * d * S.d_ff, launch_gemm(EPI_RESID, gd, s));
       }
-      st.launches += 6;
+      st.launches += 7;   // 2 RMSNorm scales, QKV, attention, O, gate/up, down
     }
     if (ev_head) NC_CUDA(cudaEventRecord(ev_head, s));
     PROF(K_RMS, 4.0 * d * valid, launch_rms(h, M, S.d, (float)S.eps, rinv, s));
