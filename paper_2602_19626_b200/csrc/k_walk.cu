@@ -133,7 +133,8 @@ __device__ __forceinline__ void quant4(const float p[4], float TmV, uint32_t cv[
 // (groups k < ng): m = max u, then s = sum 2^(u log2 e - m log2 e) as four
 // element-position partial sums (over groups in order) added as (s0 + s1) + (s2 + s3):
 // independent chains for latency.  Encoder and decoder both use exactly this.
-constexpr int NGM = 8;   // float4 groups per thread at most (V / CS <= 4 * NGM * WT)
+constexpr int NGMAX = 8;   // float4 groups per thread at most (V / CS <= 4 * NGMAX * WT)
+template <int NGM>
 __device__ __forceinline__ void ms_regs(const float (&u)[NGM][4], int ng, float &tm, float &ts) {
   constexpr float LOG2E = 1.44269504088896341f;
   float m4[4] = {-CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F};
@@ -613,7 +614,10 @@ __device__ unsigned long long g_walk_clk[8];
 #define WALK_MARK(k) do {} while (0)
 #endif
 
-template <int CS>
+// NGM: float4 groups per thread the kernel is compiled for (>= the launch's; the register
+// arrays are sized by it -- 3 at V / CS = 6,144 keeps the 128-register budget spill-free).
+// The arithmetic does not depend on it (loops run over the thread's ng groups).
+template <int CS, int NGM>
 __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
   extern __shared__ __align__(16) uint8_t dsm[];
   __shared__ WalkSmem sm;
@@ -637,6 +641,7 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
   uint32_t *bitmap = reinterpret_cast<uint32_t *>(sp_s + Vc);
   uint32_t *gsum = bitmap + (Vc + 31) / 32;
   WalkState *st = a.st + c;
+  const int64_t toff = a.tok_off[c];   // hoisted: the per-token loads below depend on it
   double *b_g = a.b + (size_t)c * V + vb;
   uint32_t *cu_g = a.cu + (size_t)c * V + vb;
   const bool use_ng = a.flags & 1u, use_head = a.flags & 2u;
@@ -897,7 +902,7 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
       }
       __syncthreads();
     }
-    int tok_cur = count > 0 ? (int)a.tokens[a.tok_off[c] + i0] : 0;
+    int tok_cur = count > 0 ? (int)a.tokens[toff + i0] : 0;
     // this CTA's slice of logits row r into L2 (one TMA bulk prefetch): rows are
     // prefetched two tokens ahead so the register loads one token ahead hit L2
     auto l2_prefetch_row = [&](int r) {
@@ -924,7 +929,7 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
       const uint32_t i = i0 + it;
       const int par = it & 1;
       const int tok = tok_cur;
-      if (has_next) tok_cur = (int)a.tokens[a.tok_off[c] + i + 1];
+      if (has_next) tok_cur = (int)a.tokens[toff + i + 1];
       const int ltok = tok - (int)vb;                  // local id (may be outside [0, Vc))
       const float M = sm.M, invS = sm.invS, a0f = sm.a0f, wl = s_w[0], wn = s_w[1];
       const int mix = sm.mix;
@@ -1044,7 +1049,7 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
           const unsigned long long cum_t = s2 + (b2.i < tok ? R : 0);
           const unsigned long long freq_t = (unsigned long long)((long long)fq + (b2.i == tok ? R : 0));
           if (rank == 0) {
-            const size_t oi = (size_t)a.tok_off[c] + i;
+            const size_t oi = (size_t)toff + i;
             a.out_cum[oi] = (uint32_t)cum_t;
             a.out_freq[oi] = (uint32_t)freq_t;
             if (a.out_p) a.out_p[oi] = p_t;
@@ -1256,7 +1261,7 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
         if (lane == 0) {
           const uint32_t tt = (uint32_t)max(t, 0);
           if (rank == 0) {
-            const size_t oi = (size_t)a.tok_off[c] + i;
+            const size_t oi = (size_t)toff + i;
             a.out_tok[oi] = tt;
             if (a.next_x) a.next_x[c] = tt;
             if (a.out_p) a.out_p[oi] = sm.p_t;
@@ -1324,17 +1329,17 @@ static int walk_cluster_size(uint32_t V) {
   return (V >= 32768 && V % 256 == 0) ? 8 : 4;
 }
 
-template <int CS>
+template <int CS, int NGM>
 static void launch_walk_cs(const WalkArgs &a, cudaStream_t s) {
   const uint32_t Vc = a.V / CS;
-  if (Vc % 4 || Vc / 4 > 8u * WT)   // float4 groups, at most 8 per thread (register-resident rows)
+  if (Vc % 4 || Vc / 4 > (uint32_t)NGM * WT)   // float4 groups, at most NGM per thread (register-resident rows)
     throw std::runtime_error("walk: vocabulary slice of " + std::to_string(Vc) +
                              " ids per CTA unsupported (needs a multiple of 4, at most 16384)");
   const size_t dyn = (size_t)Vc * 8 + Vc * 4 + Vc * 4 + ((Vc + 31) / 32) * 4 + (Vc / 4) * 4 + 64;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(walk_cl_kernel<CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
-    if (CS > 1) cudaFuncSetAttribute(walk_cl_kernel<CS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(walk_cl_kernel<CS, NGM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+    if (CS > 1) cudaFuncSetAttribute(walk_cl_kernel<CS, NGM>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     attr = true;
   }
   cudaLaunchConfig_t cfg{};
@@ -1347,7 +1352,7 @@ static void launch_walk_cs(const WalkArgs &a, cudaStream_t s) {
   at[0].val.clusterDim.x = CS; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, walk_cl_kernel<CS>, a);
+  cudaLaunchKernelEx(&cfg, walk_cl_kernel<CS, NGM>, a);
 }
 
 int walk_ctas_per_chunk(uint32_t V) { return walk_cluster_size(V); }
@@ -1370,9 +1375,17 @@ void walk_timing_report() {
 void launch_walk(const WalkArgs &a, cudaStream_t s) {
   if (a.n_entries <= 0) return;
   const int cs = walk_cluster_size(a.V);
-  if (cs == 8) launch_walk_cs<8>(a, s);
-  else if (cs == 4) launch_walk_cs<4>(a, s);
-  else launch_walk_cs<1>(a, s);
+  const uint32_t groups = (a.V / cs / 4 + WT - 1) / WT;   // float4 groups per thread
+  if (cs == 8) {
+    if (groups <= 3) launch_walk_cs<8, 3>(a, s);
+    else launch_walk_cs<8, NGMAX>(a, s);
+  } else if (cs == 4) {
+    if (groups <= 6) launch_walk_cs<4, 6>(a, s);
+    else launch_walk_cs<4, NGMAX>(a, s);
+  } else {
+    if (groups <= 2) launch_walk_cs<1, 2>(a, s);
+    else launch_walk_cs<1, NGMAX>(a, s);
+  }
 }
 
 __global__ void walk_init_kernel(WalkState *st, int n, double lw0, double lw1) {
