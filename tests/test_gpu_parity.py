@@ -238,6 +238,32 @@ def test_skip_roundtrip_size_and_p(nc, m2, w2, n_chunks):
     assert abs(len(blob) - (9 + size)) <= 0.005 * size, (len(blob), size)
 
 
+def test_chunk_streams_independent_of_batch(nc, m2):
+    """Chunks are independent: a chunk's bitstream inside a 16-chunk container
+    (slabs of 16 x len rows, 16 decode rows per step) equals the stream of that chunk
+    compressed alone (1 chunk: the geometric slab plan, 1-row decode steps) -- batch and
+    slab independence of every kernel (D15) -- and the 16-chunk container round-trips."""
+    import struct
+    from synth import make_text
+    data = make_text("alice", 24000, 77)
+    prm = nc.nc_params_default(window=256, slide=128, n_chunks=16)
+    blob = nc.nc_compress(m2, data, prm)
+    assert nc.nc_decompress(m2, blob, prm) == data
+    n = struct.unpack_from("<BHH", blob, 4)[2]   # NC05 header: magic, flags u8, tau u16, chunks u16
+    assert n == len(nc.nc_host_split(data, 16)) - 1
+    table = [struct.unpack_from("<III", blob, 9 + 12 * c) for c in range(n)]
+    offs = [9 + 12 * n]
+    for t in table:
+        offs.append(offs[-1] + t[2])
+    cuts = nc.nc_host_split(data, 16)
+    prm1 = nc.nc_params_default(window=256, slide=128, n_chunks=1)
+    for c in (0, 7, n - 1):
+        one = nc.nc_compress(m2, data[cuts[c]:cuts[c + 1]], prm1)
+        t1 = struct.unpack_from("<III", one, 9)
+        assert t1 == table[c], (c, t1, table[c])
+        assert one[21:21 + t1[2]] == blob[offs[c]:offs[c + 1]], c
+
+
 def test_edge_inputs_roundtrip(nc, m2):
     prm = nc.nc_params_default(window=256, slide=128, n_chunks=4)
     for data in (b"", b"a", b"\x00\x00\xff\n", b"\n" * 9, bytes(range(256)) * 3):
