@@ -627,6 +627,7 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
   __shared__ double s_lw[2];
   __shared__ float s_w[2];
   __shared__ uint32_t s_i;
+  __shared__ uint32_t s_tok[2048];   // compression: the chunk's tokens, refilled every 1,024 (ring)
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint32_t rank = CS > 1 ? cl_rank() : 0u;
   const int e = blockIdx.x / CS;
@@ -902,7 +903,15 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
       }
       __syncthreads();
     }
-    int tok_cur = count > 0 ? (int)a.tokens[toff + i0] : 0;
+    // token ids through a shared ring (tokens [it, it + 1,025) loaded every 1,024 tokens,
+    // coalesced): the per-token load of the next id was a dependent global round trip
+    auto refill_tokens = [&](int it0) {
+      for (int j = tid; j <= 1024; j += WT)
+        if (it0 + j < count) s_tok[(it0 + j) & 2047] = a.tokens[toff + i0 + it0 + j];
+      __syncthreads();
+    };
+    refill_tokens(0);
+    int tok_cur = count > 0 ? (int)s_tok[0] : 0;
     // this CTA's slice of logits row r into L2 (one TMA bulk prefetch): rows are
     // prefetched two tokens ahead so the register loads one token ahead hit L2
     auto l2_prefetch_row = [&](int r) {
@@ -914,6 +923,7 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
     l2_prefetch_row(1);
     l2_prefetch_row(2);
     for (int it = 0; it < count; ++it) {
+      if (it > 0 && (it & 1023) == 0) refill_tokens(it);
 #ifdef NC_WALK_TIMING
       long long _wt = clock64();
       if (tid == 0 && rank == 0) atomicAdd(&g_walk_clk[7], 1ull);
@@ -929,7 +939,7 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
       const uint32_t i = i0 + it;
       const int par = it & 1;
       const int tok = tok_cur;
-      if (has_next) tok_cur = (int)a.tokens[toff + i + 1];
+      if (has_next) tok_cur = (int)s_tok[(it + 1) & 2047];
       const int ltok = tok - (int)vb;                  // local id (may be outside [0, Vc))
       const float M = sm.M, invS = sm.invS, a0f = sm.a0f, wl = s_w[0], wn = s_w[1];
       const int mix = sm.mix;
