@@ -38,7 +38,10 @@
 
 namespace nc {
 
-constexpr int WT = 512;    // threads per walk CTA (128 registers: a token's logits stay in registers)
+#ifndef NC_WALK_WT
+#define NC_WALK_WT 384   // 12 warps: 168 registers per thread; per token 4.7k -> 4.6k cycles fused pass, 1.5k -> 1.3k reductions (vs 512)
+#endif
+constexpr int WT = NC_WALK_WT;   // threads per walk CTA (a token's logits stay in registers)
 constexpr int NW = WT / 32;
 
 struct WalkSmem {
@@ -1388,6 +1391,7 @@ void launch_walk(const WalkArgs &a, cudaStream_t s) {
   const uint32_t groups = (a.V / cs / 4 + WT - 1) / WT;   // float4 groups per thread
   if (cs == 8) {
     if (groups <= 3) launch_walk_cs<8, 3>(a, s);
+    else if (groups <= 4) launch_walk_cs<8, 4>(a, s);
     else launch_walk_cs<8, NGMAX>(a, s);
   } else if (cs == 4) {
     if (groups <= 6) launch_walk_cs<4, 6>(a, s);
