@@ -910,6 +910,7 @@ void decompress_device(nc_model *m, const uint8_t *blob, const Nc05View &view, c
     }
   }
   NC_CUDA(cudaEventRecord(e1, s));
+  if (std::getenv("NC_ATT_REPORT")) attn_timing_report();   // diagnostics builds (-DNC_ATT_TIMING)
   std::vector<uint32_t> all(total);
   NC_CUDA(cudaMemcpyAsync(all.data(), out_tok, total * 4, cudaMemcpyDeviceToHost, s));
   std::vector<WalkState> hs(n_chunks);
