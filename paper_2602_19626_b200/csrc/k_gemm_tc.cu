@@ -74,25 +74,28 @@ constexpr int TBK = 32, NPART = 2, NSCHED = 4;
 constexpr int KPP = NC_KPP;
 // split-K fixup: rows folded at once (all spans in flight) and the largest span count
 constexpr int SK_ROWS = 2, SK_MIN_SPANS = 16, SK_MAX_SPANS = 24;
-constexpr int EPI_WARPS = 8;
 constexpr int TILE_A_BYTES = TBM * TBK * 4;          // 16 KB
-constexpr int OUT_STAGE_BYTES = EPI_WARPS * 32 * 32 * 4;   // 32 KB: epilogue transpose tiles
 constexpr int TMEM_COLS = 512;                              // NPART x BN <= 512, power of two
 template <int BN>
 struct TileCfg {
-  static constexpr int EPI_COLS = BN / 2;                                // columns per epilogue warp
+  // epilogue warps: 4 TMEM lane quarters x column groups; 192-wide tiles take three groups
+  // of 64 (one attention head / two 32-column residual slices per warp) so their output
+  // phase -- which the MMA of the next tile can only run two partials ahead of -- is short
+  static constexpr int EPI_COLS = BN == 192 ? 64 : BN / 2;               // columns per epilogue warp
+  static constexpr int EPI_WARPS = 4 * (BN / EPI_COLS);                  // 8, or 12 at BN = 192
+  static constexpr int THREADS = 32 * (EPI_WARPS + 2);                   // + TMA/allocator + MMA warps
+  static constexpr int W_TMA = EPI_WARPS, W_MMA = EPI_WARPS + 1;
+  static constexpr int OUT_STAGE_BYTES = EPI_WARPS * 32 * 32 * 4;        // per-warp 32 x 32 transpose tiles
+  // sch_empty arrivals per tile claim: leader MMA + the epilogue warps of both CTAs + the peer's producer
+  static constexpr int SCHED_CONSUMERS = 1 + 2 * EPI_WARPS + 1;
   static constexpr int TILE_B_BYTES = (BN / 2) * TBK * 4;                // 16 / 12 KB
   static constexpr int STAGE_BYTES = 2 * TILE_A_BYTES + 2 * TILE_B_BYTES;   // 64 / 56 KB per CTA
   // pipeline depth: 3 stages of 64 / 56 KB; the 128-wide tiles (decode steps, whose k loop
   // is bound by TMA round trips rather than MMAs) fit a fourth 48 KB stage
   static constexpr int STAGES = BN == 128 ? 4 : 3;
   static constexpr int SMEM = STAGES * STAGE_BYTES + OUT_STAGE_BYTES + 1024 /*align*/ + 512 /*barriers*/;
-  static_assert(NPART * BN <= TMEM_COLS && BN % 32 == 0, "tile");
+  static_assert(NPART * BN <= TMEM_COLS && BN % 32 == 0 && EPI_COLS % 32 == 0, "tile");
 };
-constexpr int TC_THREADS = 320;
-constexpr int W_TMA = 8, W_MMA = 9;
-// sch_empty arrivals per tile claim: leader MMA + 8 epilogue warps per CTA + the peer's producer
-constexpr int SCHED_CONSUMERS = 1 + 2 * EPI_WARPS + 1;
 
 // This lane's 32 row values -> the warp's swizzled staging tile -> one TMA bulk tensor
 // store of the warp's 32 x 32 box at (c0, r0) (the tile layout is exactly the
@@ -264,7 +267,7 @@ __device__ unsigned long long g_gemm_clk[4 * 8];   // [EPI][phase]
 #endif
 
 template <int EPI, int BN, bool SPLIT>
-__global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_constant__ CUtensorMap tmAh,
+__global__ __launch_bounds__(TileCfg<BN>::THREADS, 1) void gemm_tc_kernel(const __grid_constant__ CUtensorMap tmAh,
                                                                 const __grid_constant__ CUtensorMap tmAl,
                                                                 const __grid_constant__ CUtensorMap tmBh,
                                                                 const __grid_constant__ CUtensorMap tmBl,
@@ -275,6 +278,8 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
   using C_ = TileCfg<BN>;
   constexpr int TBN = BN, EPI_COLS = C_::EPI_COLS, TILE_B_BYTES = C_::TILE_B_BYTES, STAGE_BYTES = C_::STAGE_BYTES;
   constexpr int TSTAGES = C_::STAGES;
+  constexpr int EPI_WARPS = C_::EPI_WARPS, W_TMA = C_::W_TMA, W_MMA = C_::W_MMA;
+  constexpr int OUT_STAGE_BYTES = C_::OUT_STAGE_BYTES, SCHED_CONSUMERS = C_::SCHED_CONSUMERS;
   static_assert(KPP <= TSTAGES, "a partial's k blocks must fit the pipeline (corrections-first MMA order)");
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -440,7 +445,7 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
   } else {
     // ---------------------------------------------------------------- epilogue
     const int q = warp & 3;     // TMEM lanes 32q .. 32q+31
-    const int hc = warp >> 2;   // column half of the 256-wide tile
+    const int hc = warp >> 2;   // column group of the tile (EPI_COLS wide)
     const uint32_t sch_empty_leader = tc::mapa(&sch_empty[0], 0);
     const uint32_t tempty_leader = tc::mapa(&tempty[0], 0);
     int buf = 0;
@@ -590,7 +595,7 @@ __global__ __launch_bounds__(TC_THREADS, 1) void gemm_tc_kernel(const __grid_con
           store_rows32<ST_RESID>(stg, acc + sl * 32, row_ok ? a.C + o : nullptr, a.C_hi + o, a.C_lo + o, lane);
         }
       } else {
-        static_assert(EPI == EPI_RESID || BN % 128 == 0, "64-column epilogue blocks");
+        static_assert(EPI == EPI_RESID || EPI_COLS % 64 == 0, "64-column epilogue blocks");
 #pragma unroll
       for (int half = 0; half < EPI_COLS / 64; ++half) {
         const int cb = nb * TBN + hc * EPI_COLS + half * 64;   // first column of this 64-wide block
@@ -799,13 +804,13 @@ static void launch_tc(const TcGemmArgs &a, const TcOperands &op, cudaStream_t s)
       aa.sps = 0;
     } else {
       aa.ws = splitk_workspace((size_t)nspan * a.N * a.M);
-      aa.fix_ctr = splitk_counters((size_t)tiles * 2 * EPI_WARPS);
+      aa.fix_ctr = splitk_counters((size_t)tiles * 2 * TileCfg<BN>::EPI_WARPS);
     }
   }
   const int pairs = std::min(tiles * nsplit, pairs_avail);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * pairs);
-  cfg.blockDim = dim3(TC_THREADS);
+  cfg.blockDim = dim3(TileCfg<BN>::THREADS);
   cfg.dynamicSmemBytes = TileCfg<BN>::SMEM;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
@@ -858,7 +863,7 @@ void launch_gemm_tc(GemmEpi epi, const TcGemmArgs &a, const TcOperands &op, cuda
     // whatever the tile width (D15; test_splitk_bit_identity compares prefill and decode).
     case EPI_QKV:
       if (a.M <= TBM) launch_tc<EPI_QKV, 128>(a, op, s);
-      else launch_tc<EPI_QKV, 256>(a, op, s);
+      else launch_tc<EPI_QKV, 192>(a, op, s);   // N = 960 = 5 x 192: three heads per tile, no padding
       break;
     case EPI_RESID:
       if (a.M <= TBM) launch_tc<EPI_RESID, 128>(a, op, s);
