@@ -401,16 +401,44 @@ __global__ __launch_bounds__(TileCfg<BN>::THREADS, 1) void gemm_tc_kernel(const 
         if (t < 0) break;
         int tile, kb_lo, kb_hi;
         item_k(t, tile, kb_lo, kb_hi);
-        // one TMEM partial per KPP k blocks: all correction products of the span
-        // first (the partial is still ~2^-11 of its final size, so their
-        // truncations are negligible), then the hi*hi products -- 4 * KPP large-
-        // magnitude truncations per partial; each stage is released after its hi*hi
+        // one TMEM partial per KPP k blocks (a fresh accumulator, promoted in fp32 RN by
+        // the epilogue); within it see the two orders below
         for (int kb0 = kb_lo; kb0 < kb_hi; kb0 += KPP) {
           const int nkp = min(KPP, kb_hi - kb0);
           tc::mbar_wait(&tempty[buf], buf_phase ^ 1);   // partial drained by both CTAs' epilogues
           const uint32_t d = tmem_base + buf * BN;
           int st = stage;
           uint32_t ph = phase;
+#ifndef NC_MMA_CORR_FIRST
+          // per k block its corrections then its hi*hi, the stage released right after: the
+          // producer runs a k block further ahead than with all of a span's corrections first
+          // (measured: QKV/O/down GEMMs -4 to -5 %, step -1 ms), at 12 instead of 8 large-
+          // magnitude truncations per partial (GEMM max rel. error 4.3e-7 -> 5.9e-7 at K = 576,
+          // tools/gemm_precision.py).  -DNC_MMA_CORR_FIRST restores the corrections-first order.
+          for (int i = 0; i < nkp; ++i) {
+            tc::mbar_wait(&full[st], ph);
+            tc::fence_after();
+            const uint32_t s0 = tc::smem_u32(smem + st * STAGE_BYTES);
+            const uint64_t dah = tc::desc_k_sw128(s0), dal = tc::desc_k_sw128(s0 + TILE_A_BYTES);
+            const uint64_t dbh = tc::desc_k_sw128(s0 + 2 * TILE_A_BYTES);
+            const uint64_t dbl = tc::desc_k_sw128(s0 + 2 * TILE_A_BYTES + TILE_B_BYTES);
+#pragma unroll
+            for (int j = 0; j < TBK / 8; ++j) {
+              const uint64_t adv = (uint64_t)(j * 32) >> 4;
+              tc::mma_tf32_pair(d, dah + adv, dbl + adv, idesc, (i | j) != 0);
+              tc::mma_tf32_pair(d, dal + adv, dbh + adv, idesc, 1);
+            }
+#pragma unroll
+            for (int j = 0; j < TBK / 8; ++j) {
+              const uint64_t adv = (uint64_t)(j * 32) >> 4;
+              tc::mma_tf32_pair(d, dah + adv, dbh + adv, idesc, 1);
+            }
+            tc::mma_commit_pair(&empty[st]);
+            if (++st == TSTAGES) { st = 0; ph ^= 1; }
+          }
+          stage = st;
+          phase = ph;
+#else
           for (int i = 0; i < nkp; ++i) {
             tc::mbar_wait(&full[st], ph);
             tc::fence_after();
@@ -437,6 +465,7 @@ __global__ __launch_bounds__(TileCfg<BN>::THREADS, 1) void gemm_tc_kernel(const 
             tc::mma_commit_pair(&empty[stage]);
             if (++stage == TSTAGES) { stage = 0; phase ^= 1; }
           }
+#endif
           tc::mma_commit_pair(&tfull[buf]);
           if (++buf == NPART) { buf = 0; buf_phase ^= 1; }
         }
