@@ -729,6 +729,7 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
   if (prof().on) prof().collect();
   if (std::getenv("NC_WALK_REPORT")) walk_timing_report();
   if (std::getenv("NC_GEMM_REPORT")) gemm_timing_report();
+  if (std::getenv("NC_ATT_REPORT")) attn_timing_report();
   for (int c = 0; c < n_chunks; ++c) out.err[c] = hs[c].err;
   for (int sl = 0; sl < n_slabs; ++sl) {
     float a = 0, b = 0;
