@@ -558,9 +558,10 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
   // logits double-buffered); only the last slab's walk runs after the forward.
   // Bigger slabs run the GEMMs more efficiently (fewer tile waves), a smaller last
   // slab shortens that final walk.  Measured on config2 (3885 positions):
-  // 4 x 1024 -> 109 ms, 2 x ~1940 -> 101.5 ms, 2944 + 941 (frac 0.75) -> 96.8 ms.
-  // So: slabs of the largest size (max_slab_rows / n_chunks) while the remainder
-  // exceeds one / frac, then the remainder split 75/25 (NC_SLAB_FRAC), 128-aligned so no
+  // 4 x 1024 -> 109 ms, 2 x ~1940 -> 101.5 ms, 2944 + 941 (frac 0.75) -> 96.8 ms (early
+  // kernels); with the faster walk of r01f, frac 0.70 / 0.75 / 0.80 / 0.85 -> 75.0 / 74.2 /
+  // 73.1 / 73.6 ms.  So: slabs of the largest size (max_slab_rows / n_chunks) while the
+  // remainder exceeds one / frac, then the remainder split 80/20 (NC_SLAB_FRAC), 128-aligned so no
   // 128-row attention tile crosses a retained-window step (C | 128 k).
   // NC_SLAB_PLAN="a,b,..." (diagnostics) gives explicit lengths.
   const int per_chunk = std::max(128, (int)(p.max_slab_rows / n_chunks) / 128 * 128);
@@ -579,7 +580,7 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
     for (int pos = 0; pos < (int)max_n; pos += len, len = std::min(per_chunk, 2 * len)) plan.push_back(len);
   } else {
     const char *fs = std::getenv("NC_SLAB_FRAC");
-    const double frac = fs ? std::min(0.95, std::max(0.05, std::atof(fs))) : 0.75;
+    const double frac = fs ? std::min(0.95, std::max(0.05, std::atof(fs))) : 0.80;
     int rem = (int)max_n;
     while (frac * rem > per_chunk) {   // full slabs until the last two fit the split
       plan.push_back(per_chunk);
