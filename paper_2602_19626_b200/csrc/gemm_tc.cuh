@@ -39,6 +39,8 @@ void launch_gemm_tc(GemmEpi epi, const TcGemmArgs &a, const TcOperands &op, cuda
 void set_reserved_sms(int n);
 // split-K policy: 1 automatic (default), 0 never (tests: bit identity of the two)
 void set_splitk_mode(int mode);
+// programmatic dependent launch for the persistent grids (on unless NC_PDL=0)
+bool pdl_enabled();
 // diagnostics build (-DNC_GEMM_TIMING): epilogue phase cycles -> stderr
 void gemm_timing_report();
 void launch_split_planes(const float *x, float *hi, float *lo, size_t n, cudaStream_t s);

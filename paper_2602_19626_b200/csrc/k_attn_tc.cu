@@ -36,6 +36,7 @@
 #include <unordered_map>
 
 #include "attn_tc.cuh"
+#include "gemm_tc.cuh"
 #include "tc_common.cuh"
 
 namespace nc {
@@ -142,6 +143,8 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
+  tc::pdl_launch_dependents();
+  tc::pdl_wait();   // q planes and the KV ring come from the QKV GEMM
 
   // item -> (tile, head, geometry); every role derives the same numbers
   struct Item { AttnTile t; int h, g, kb0, nkb, zc; };
@@ -605,7 +608,17 @@ void launch_attention_tc(const AttnTcArgs &a, cudaStream_t s) {
   AttnTcArgs aa = a;
   aa.item_ctr = ctr;
   const int grid = std::min(a.n_tiles * a.H, n_sms);   // persistent: one CTA per SM claims (tile, head) items
-  attn_tc_kernel<<<grid, ATT_THREADS, ATT_SMEM, s>>>(*qh, *ql, *kh, *kl, *vh, *vl, aa);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(ATT_THREADS);
+  cfg.dynamicSmemBytes = ATT_SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, attn_tc_kernel, *qh, *ql, *kh, *kl, *vh, *vl, aa);
 }
 
 }  // namespace nc

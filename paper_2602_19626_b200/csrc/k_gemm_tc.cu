@@ -49,6 +49,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <mutex>
 #include <stdexcept>
@@ -339,6 +340,8 @@ __global__ __launch_bounds__(TileCfg<BN>::THREADS, 1) void gemm_tc_kernel(const 
   tc::cluster_sync();
   tc::fence_after();
   const uint32_t tmem_base = *tmem_base_smem;
+  tc::pdl_launch_dependents();
+  tc::pdl_wait();   // everything below reads what earlier kernels wrote (or claims tiles)
 
   if (warp == W_TMA) {
     // ------------------------------------------------------------ TMA producer
@@ -741,6 +744,9 @@ const CUtensorMap *tmap_2d(const float *ptr, uint64_t rows, uint64_t cols, uint3
 static int g_reserved_sms = 0;
 void set_reserved_sms(int n) { g_reserved_sms = n; }
 static int g_splitk_mode = 1;
+// programmatic dependent launch of the persistent GEMM / attention grids (NC_PDL=0: off)
+static const bool g_pdl = !(std::getenv("NC_PDL") && std::getenv("NC_PDL")[0] == '0');
+bool pdl_enabled() { return g_pdl; }
 void set_splitk_mode(int mode) { g_splitk_mode = mode; }
 
 static int *tile_counter() {   // {next tile, CTAs done}; zero between launches
@@ -842,13 +848,15 @@ static void launch_tc(const TcGemmArgs &a, const TcOperands &op, cudaStream_t s)
   cfg.blockDim = dim3(TileCfg<BN>::THREADS);
   cfg.dynamicSmemBytes = TileCfg<BN>::SMEM;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = 2;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // prologue under the previous tail
+  at[1].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   // output maps of the TMA-store epilogues: rows = M (clips the tile tail), 32 x 32 boxes
   const CUtensorMap *c0 = bh, *c1 = bh, *c2 = bh;
   if (EPI == EPI_HEAD) c0 = tmap_2d(a.C, (uint64_t)a.M, (uint64_t)a.ldc, 32);

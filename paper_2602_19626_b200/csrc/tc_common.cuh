@@ -26,6 +26,14 @@ __device__ __forceinline__ bool elect_one() {
   return p != 0;
 }
 
+// ------------------------------------------------- programmatic dependent launch ---
+// The next kernel in the stream (launched with programmatic stream serialization) may be
+// scheduled once every CTA of this grid has signalled; it runs its prologue (barrier init,
+// TMEM allocation, descriptor prefetch) on SMs this grid's tail leaves idle and then waits
+// in pdl_wait() until this grid has completed and its memory is visible.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ------------------------------------------------------------- mbarrier ---
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
