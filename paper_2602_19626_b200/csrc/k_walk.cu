@@ -89,17 +89,24 @@ __device__ __forceinline__ float lg2f(float x) {   // log2 on the SFU (lg2.appro
 }
 // exp on the SFU (ex2.approx; relative error ~1e-6 for the |x| < 30 used here)
 __device__ __forceinline__ float fexp(float x) { return tc::ex2(__fmul_rn(x, 1.44269504088896341f)); }
-__device__ __forceinline__ void ms_merge(float &tm, float &ts, float om, float os) {
-  const float mm = fmaxf(tm, om);
-  const float e1 = (tm == -CUDART_INF_F) ? 0.f : fexp(__fsub_rn(tm, mm));
-  const float e2 = (om == -CUDART_INF_F) ? 0.f : fexp(__fsub_rn(om, mm));
-  ts = __fadd_rn(__fmul_rn(ts, e1), __fmul_rn(os, e2));
-  tm = mm;
+// Warp (max, sum-of-exp) statistics: the max first (order-free, one redux on an order-
+// preserving integer key), then every lane's sum rescaled once to it and added through a
+// fixed xor tree (identical in every lane) -- one exponential per lane instead of two per
+// tree level.  Compression and decompression both use exactly this.
+__device__ __forceinline__ uint32_t fkey(float x) {
+  const uint32_t b = __float_as_uint(x);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float fkey_inv(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
 }
 __device__ __forceinline__ void ms_warp(float &tm, float &ts) {
+  const float M = fkey_inv(__reduce_max_sync(0xffffffffu, fkey(tm)));
+  float s = (tm == -CUDART_INF_F) ? 0.f : __fmul_rn(ts, fexp(__fsub_rn(tm, M)));
 #pragma unroll
-  for (int o = 16; o; o >>= 1)
-    ms_merge(tm, ts, __shfl_xor_sync(0xffffffffu, tm, o), __shfl_xor_sync(0xffffffffu, ts, o));
+  for (int o = 16; o; o >>= 1) s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
+  tm = M;
+  ts = s;
 }
 // quant() for a float4 group: the x < 2^23 path for all four, and the x >= 2^23
 // path (only an element with p > 1/2 reaches it) behind one warp vote, so the
@@ -584,6 +591,21 @@ struct Xch {                  // one CTA's per-token partials, read by the whole
   int found, t; unsigned long long cum_t, fq_t; float fpt, fpng, fp;
   uint32_t pad;
 };
+// the cluster's (max, sum) partials in rank order: max, then the rescaled sums added in order
+template <int CS>
+__device__ __forceinline__ void ms_cluster(const Xch *x, float &M, float &S) {
+  float m = x[0].m;
+#pragma unroll
+  for (int r = 1; r < CS; ++r) m = fmaxf(m, x[r].m);
+  float e[CS];
+#pragma unroll
+  for (int r = 0; r < CS; ++r) e[r] = x[r].m == -CUDART_INF_F ? 0.f : __fmul_rn(x[r].s, fexp(__fsub_rn(x[r].m, m)));
+  float sum = e[0];
+#pragma unroll
+  for (int r = 1; r < CS; ++r) sum = __fadd_rn(sum, e[r]);
+  M = m;
+  S = sum;
+}
 constexpr int XW = sizeof(Xch) / 4;
 static_assert(sizeof(Xch) % 4 == 0, "Xch words");
 
@@ -900,8 +922,8 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
       if (wid == 0) push_slot(1);
       if (CS > 1) cl_sync(); else __syncthreads();
       if (tid == 0) {
-        float M = xin[1][0].m, S = xin[1][0].s;
-        for (int r = 1; r < CS; ++r) ms_merge(M, S, xin[1][r].m, xin[1][r].s);
+        float M, S;
+        ms_cluster<CS>(xin[1], M, S);
         sm.M = M; sm.invS = __frcp_rn(S);
       }
       __syncthreads();
@@ -1047,14 +1069,14 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
         if (lane == 0) {
           unsigned long long s1 = 0, s2 = 0;
           Best b2{-1.f, 0x7fffffff, 0};
-          float nm = xin[par][0].m, ns = xin[par][0].s;
+          float nm, ns;
+          ms_cluster<CS>(xin[par], nm, ns);
           float pt_t = 0.f, png_t = 0.f, p_t = 0.f;
           uint32_t fq = 0;
           for (int r = 0; r < CS; ++r) {
             const Xch &x = xin[par][r];
             s1 += x.sum; s2 += x.cum;
             best_merge(b2, x.bv, x.bi, x.bc);
-            if (r) ms_merge(nm, ns, x.m, x.s);
             if (x.has_tok) { pt_t = x.pt_t; png_t = x.png_t; p_t = x.p_t; fq = x.freq_t; }
           }
           const long long R = (long long)T - (long long)s1;
@@ -1135,8 +1157,8 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
         if (wid == 0) {
           gather(par);
           if (lane == 0) {
-            float M = xin[par][0].m, S = xin[par][0].s;
-            for (int r = 1; r < CS; ++r) ms_merge(M, S, xin[par][r].m, xin[par][r].s);
+            float M, S;
+            ms_cluster<CS>(xin[par], M, S);
             sm.M = M; sm.invS = __frcp_rn(S);
           }
         }
