@@ -573,11 +573,14 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
       if (*q == ',') ++q;
     }
   } else if (n_chunks <= 2) {
-    // Few chunks: the walk (~5 us per position, latency-bound, one cluster per chunk)
-    // outlasts the forward (~2.3 us per position per chunk), so start it early: a small
-    // first slab, then doubling -- the later forwards hide under the walk.
+    // Few chunks: the walk (~4 us per position, latency-bound, one cluster per chunk) and
+    // the N-gram precompute feeding it (~4 us per token) outlast the forward (~2.8 us per
+    // position per chunk at 4,096 rows), so start them early: a small first slab, then
+    // doubling up to 4,096 positions -- the walk of a slab then never waits long for its
+    // N-gram slab (config2 with 1 chunk: unbounded doubling 185 ms, capped at 2,048 207 ms
+    // (the forward of small slabs is inefficient), at 4,096 145 ms).
     int len = 1024;
-    for (int pos = 0; pos < (int)max_n; pos += len, len = std::min(per_chunk, 2 * len)) plan.push_back(len);
+    for (int pos = 0; pos < (int)max_n; pos += len, len = std::min({per_chunk, 2 * len, 4096})) plan.push_back(len);
   } else {
     const char *fs = std::getenv("NC_SLAB_FRAC");
     const double frac = fs ? std::min(0.95, std::max(0.05, std::atof(fs))) : 0.80;
