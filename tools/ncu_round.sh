@@ -4,7 +4,7 @@
 # from the second step).  Outputs land in gpurun_out/; tools/ncu_summary.py condenses them
 # into profiles/.   usage: bash tools/ncu_round.sh <tag>
 set -x
-TAG=${1:-r01g}
+TAG=${1:-r01h}
 O=gpurun_out
 NCU=ncu
 $NCU --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_$TAG.csv \
