@@ -167,6 +167,43 @@ __device__ __forceinline__ void ms_regs(const float (&u)[NGM][4], int ng, float 
   }
   ts = __fadd_rn(__fadd_rn(s4[0], s4[1]), __fadd_rn(s4[2], s4[3]));
 }
+// ms_regs that also leaves e = 2^(u log2 e - m log2 e) in place of u (m = the thread's max):
+// the token's probabilities are then p~ = e * (2^((m - M) log2 e) / S) -- one exponential per
+// element instead of two (compression); the decoder forms the same e from u and m (tc_pt)
+template <int NGM>
+__device__ __forceinline__ void ms_regs_e(float (&u)[NGM][4], int ng, float &tm, float &ts) {
+  constexpr float LOG2E = 1.44269504088896341f;
+  float m4[4] = {-CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F};
+#pragma unroll
+  for (int k = 0; k < NGM; ++k)
+    if (k < ng) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) m4[j] = fmaxf(m4[j], u[k][j]);
+    }
+  tm = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+  float s4[4] = {0.f, 0.f, 0.f, 0.f};
+  if (tm != -CUDART_INF_F) {
+    const float nb = -__fmul_rn(tm, LOG2E);
+#pragma unroll
+    for (int k = 0; k < NGM; ++k)
+      if (k < ng) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          u[k][j] = tc::ex2(__fmaf_rn(u[k][j], LOG2E, nb));
+          s4[j] = __fadd_rn(s4[j], u[k][j]);
+        }
+      }
+  }
+  ts = __fadd_rn(__fadd_rn(s4[0], s4[1]), __fadd_rn(s4[2], s4[3]));
+}
+// the thread's rescale of its e values to probabilities: 2^((m - M) log2 e) / S
+__device__ __forceinline__ float pt_scale(float m_thread, float M, float invS) {
+  return __fmul_rn(tc::ex2(__fmul_rn(__fsub_rn(m_thread, M), 1.44269504088896341f)), invS);
+}
+// p~ of one element from its u, the thread's max and scale (decoder; = e * scale of the encoder)
+__device__ __forceinline__ float pt_from_u(float u, float m_thread, float scale) {
+  return __fmul_rn(tc::ex2(__fmaf_rn(u, 1.44269504088896341f, -__fmul_rn(m_thread, 1.44269504088896341f))), scale);
+}
 // p = w_l pt + w_n (a0f (c+1) + add); c (unigram count < 2^24) held exactly in fp32
 // skip (confidence-based LLM skip): p = p_ng
 __device__ __forceinline__ float mix_p(float pt, float a0f, float cuv, float add, float wl, float wn, float &png,
@@ -653,6 +690,7 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
   __shared__ float s_w[2];
   __shared__ uint32_t s_i;
   __shared__ uint32_t s_tok[2048];   // compression: the chunk's tokens, refilled every 1,024 (ring)
+  __shared__ float s_mth[WT];        // decompression: every thread's max of its u (pt_from_u of any group)
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint32_t rank = CS > 1 ? cl_rank() : 0u;
   const int e = blockIdx.x / CS;
@@ -712,13 +750,13 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
     u[0] = walk_u(z4.x, b01.x, inv_tau); u[1] = walk_u(z4.y, b01.y, inv_tau);
     u[2] = walk_u(z4.z, b23.x, inv_tau); u[3] = walk_u(z4.w, b23.y, inv_tau);
   };
-  auto prob4 = [&](const float *z, int g, float M, float invS, float wl, float wn, float a0f, int mix, bool skip,
+  auto prob4 = [&](const float *z, int g, float mth, float scale, float wl, float wn, float a0f, int mix, bool skip,
                    float pt[4],
                    float png[4], float p[4]) {
     float u[4];
     load_u(z, g, u);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) pt[j] = __fmul_rn(fexp(__fsub_rn(u[j], M)), invS);
+    for (int j = 0; j < 4; ++j) pt[j] = pt_from_u(u[j], mth, scale);
     if (!mix) {
 #pragma unroll
       for (int j = 0; j < 4; ++j) { png[j] = 0.f; p[j] = pt[j]; }
@@ -877,7 +915,8 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
     // order-free argmax; only where the values come from changed.
 
     const uint32_t i0 = s_i;
-    float uc[NGM][4];   // u = z / tau + b of the current token, from the previous token's pass
+    float uc[NGM][4];   // e = 2^((u - mth) log2 e) of the current token (u = z / tau + b), from the previous pass
+    float mth = -CUDART_INF_F;   // this thread's max of the current token's u
     auto zload = [&](const float *zrow, float4 (&dst)[NGM]) {
 #pragma unroll
       for (int k = 0; k < NGM; ++k)
@@ -915,7 +954,8 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
 #pragma unroll
       for (int k = 0; k < NGM; ++k)
         if (k < ng) u4(z0[k], tid + k * WT, uc[k]);
-      ms_regs(uc, ng, tm, ts);
+      ms_regs_e(uc, ng, tm, ts);   // uc now holds e = 2^((u - m) log2 e)
+      mth = tm;
       cta_ms(tm, ts);
       if (tid == 0) { xs[1].m = tm; xs[1].s = ts; }
       __syncthreads();
@@ -967,6 +1007,7 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
       if (has_next) tok_cur = (int)s_tok[(it + 1) & 2047];
       const int ltok = tok - (int)vb;                  // local id (may be outside [0, Vc))
       const float M = sm.M, invS = sm.invS, a0f = sm.a0f, wl = s_w[0], wn = s_w[1];
+      const float scale = pt_scale(mth, M, invS);   // p~ = e * scale for this thread's elements
       const int mix = sm.mix;
       const bool skip = (use_skip && mix) ? ng_entropy(par, a0f) < kSkipTauBits : false;
       const bool pre_next = has_next && use_ng && i + 1 >= a.warmup;
@@ -982,7 +1023,7 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
         const int g = tid + k * WT;
         float pt[4], png[4], p[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) pt[j] = __fmul_rn(fexp(__fsub_rn(uc[k][j], M)), invS);
+        for (int j = 0; j < 4; ++j) pt[j] = __fmul_rn(uc[k][j], scale);
         if (!mix) {
 #pragma unroll
           for (int j = 0; j < 4; ++j) { png[j] = 0.f; p[j] = pt[j]; }
@@ -1032,7 +1073,10 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
 #if defined(NC_WALK_ABL) && NC_WALK_ABL >= 2   // diagnostics: no statistics
       tm = 0.f; ts = 1.f;
 #else
-      if (has_next) ms_regs(uc, ng, tm, ts);
+      if (has_next) {
+        ms_regs_e(uc, ng, tm, ts);
+        mth = tm;
+      }
 #endif
       WALK_MARK(0);
       if (wid == 1 && pre_next) prefetch_wait();
@@ -1150,6 +1194,7 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
           if (k < ng) load_u(z, tid + k * WT, ud[k]);
         float tm, ts;
         ms_regs(ud, ng, tm, ts);
+        s_mth[tid] = tm;
         cta_ms(tm, ts);
         if (tid == 0) { xs[par].m = tm; xs[par].s = ts; }
         __syncthreads();
@@ -1166,12 +1211,13 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
       }
       const float M = sm.M, invS = sm.invS, a0f = sm.a0f, wl = s_w[0], wn = s_w[1];
       const int mix = sm.mix;
+      const float mth = s_mth[tid], scale = pt_scale(mth, M, invS);   // this thread's groups tid + k WT
       // (3) counts
       uint32_t my_sum = 0;
       Best bb{-1.f, 0x7fffffff, 0};
       for (int g = tid; g < Gc; g += WT) {
         float pt[4], png[4], p[4];
-        prob4(z, g, M, invS, wl, wn, a0f, mix, skip, pt, png, p);
+        prob4(z, g, mth, scale, wl, wn, a0f, mix, skip, pt, png, p);
         uint32_t gs = 0;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -1242,7 +1288,8 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
             accm += gsum[gf];
           }
           float pt[4], png[4], p[4];
-          prob4(z, gf, M, invS, wl, wn, a0f, mix, skip, pt, png, p);
+          const float mo = s_mth[gf % WT];   // the max of the thread that owns group gf
+          prob4(z, gf, mo, pt_scale(mo, M, invS), wl, wn, a0f, mix, skip, pt, png, p);
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             const int v = 4 * gf + j;
@@ -1280,7 +1327,7 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
       if (use_head)
         for (int g = tid; g < Gc; g += WT) {
           float pt[4], png[4], p[4];
-          prob4(z, g, M, invS, wl, wn, a0f, mix, skip, pt, png, p);
+          prob4(z, g, mth, scale, wl, wn, a0f, mix, skip, pt, png, p);
           double2 *bp = reinterpret_cast<double2 *>(b_s) + 2 * g;
           double2 b01 = bp[0], b23 = bp[1];
           const int v = 4 * g;
