@@ -1109,19 +1109,20 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
       WALK_MARK(1);
       if (CS > 1) cl_sync(); else __syncthreads();
       WALK_MARK(2);
-      if (wid == 0) {
-        if (lane == 0) {
+      if (wid == 0 || wid == 2 || wid == 3) {
+        // the combine, split over three warps that run concurrently (same arithmetic as one
+        // thread in sequence): warp 0 codes the token, warp 2 runs the mixer, warp 3 the
+        // next token's softmax statistics (warp 1 swaps the N-gram fixups meanwhile)
+        if (wid == 0 && lane == 0) {
           unsigned long long s1 = 0, s2 = 0;
           Best b2{-1.f, 0x7fffffff, 0};
-          float nm, ns;
-          ms_cluster<CS>(xin[par], nm, ns);
-          float pt_t = 0.f, png_t = 0.f, p_t = 0.f;
+          float p_t = 0.f;
           uint32_t fq = 0;
           for (int r = 0; r < CS; ++r) {
             const Xch &x = xin[par][r];
             s1 += x.sum; s2 += x.cum;
             best_merge(b2, x.bv, x.bi, x.bc);
-            if (x.has_tok) { pt_t = x.pt_t; png_t = x.png_t; p_t = x.p_t; fq = x.freq_t; }
+            if (x.has_tok) { p_t = x.p_t; fq = x.freq_t; }
           }
           const long long R = (long long)T - (long long)s1;
           if ((long long)b2.c + R < 1) st->err = 1;     // D6
@@ -1133,9 +1134,21 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
             a.out_freq[oi] = (uint32_t)freq_t;
             if (a.out_p) a.out_p[oi] = p_t;
           }
-          if (mix) mixer_update(pt_t, png_t);
           if (use_ng && ltok >= 0 && ltok < (int)Vc) cu_s[ltok] = __fadd_rn(cu_s[ltok], 1.f);
-          if (has_next) { sm.M = nm; sm.invS = __frcp_rn(ns); }
+        } else if (wid == 2 && lane == 0) {
+          if (mix) {
+            float pt_t = 0.f, png_t = 0.f;
+            for (int r = 0; r < CS; ++r)
+              if (xin[par][r].has_tok) { pt_t = xin[par][r].pt_t; png_t = xin[par][r].png_t; }
+            mixer_update(pt_t, png_t);
+          }
+        } else if (wid == 3 && lane == 0) {
+          if (has_next) {
+            float nm, ns;
+            ms_cluster<CS>(xin[par], nm, ns);
+            sm.M = nm;
+            sm.invS = __frcp_rn(ns);
+          }
         }
       } else if (wid == 1) {   // N-gram fixups: this token's out, the next token's in (parallel to warp 0)
         clear_list(i);
