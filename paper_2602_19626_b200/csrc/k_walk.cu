@@ -26,6 +26,7 @@
 // arithmetic; every float op is an explicit round-to-nearest intrinsic and
 // every reduction has a fixed tree, so the decoder reproduces the encoder's
 // counts bit for bit (D15).
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 #include <stdexcept>
@@ -63,7 +64,9 @@ struct WalkSmem {
 // ------------------------------------------------------------ elementwise ---
 __device__ __forceinline__ float walk_u(float z, double b, float inv_tau) { return __fmaf_rn(z, inv_tau, (float)b); }
 __device__ __forceinline__ double b_step(double b, float pt, bool is_t, double alpha) {
-  return __fma_rn(-alpha, __dsub_rn((double)pt, is_t ? 1.0 : 0.0), b);
+  // b - alpha (p~ - 1[t]) in f64 (D17); the subtraction only for the coded token (pt - 0 = pt)
+  const double d = (double)pt;
+  return __fma_rn(-alpha, is_t ? __dsub_rn(d, 1.0) : d, b);
 }
 // c = max(1, floor(p * (T - V))) with the EXACT product (D5), in fp32 only:
 // T - V < 2^24 is exact in fp32; q = floor(rn(p * TmV)) is off by at most one,
@@ -644,6 +647,8 @@ __device__ __forceinline__ void ms_cluster(const Xch *x, float &M, float &S) {
   S = sum;
 }
 constexpr int XW = sizeof(Xch) / 4;
+constexpr int XWE = 14;   // compression reads only the prefix sum .. freq_t of a slot
+static_assert(offsetof(Xch, freq_t) + 4 == 4 * XWE, "Xch compression prefix");
 static_assert(sizeof(Xch) % 4 == 0, "Xch words");
 
 __device__ __forceinline__ uint32_t cl_rank() {
@@ -932,7 +937,7 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
     auto push_slot = [&](int par) {   // warp 0
       const uint32_t *src = reinterpret_cast<const uint32_t *>(&xs[par]);
       uint32_t *dst = reinterpret_cast<uint32_t *>(&xin[par][rank]);
-      for (int w = lane; w < XW; w += 32) {
+      for (int w = lane; w < XWE; w += 32) {   // compression: the prefix the combine reads
         const uint32_t v = src[w];
         if (CS > 1) {
 #pragma unroll
