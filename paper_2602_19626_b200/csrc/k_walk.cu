@@ -403,15 +403,17 @@ __device__ __forceinline__ void ng_hist_push(WalkState *st, uint32_t t) {
 // so a token costs ~3 round trips instead of ~40 (one warp doing all orders twice).
 // The decoder runs ng_predict_warp / ng_update_warp inline on the same tables; both
 // produce identical lists and table states (round-trip tests).
-constexpr int NGC = 4;           // chunks per CTA (4 warps each)
+constexpr int NGC = 4;           // chunks per CTA (5 warps each: 4 orders + the merge warp)
+constexpr int NGWC = 5;          // warps per chunk
 constexpr int NG_HASH = 512;     // merge position hash (>= 2 x kMaxSparse)
-struct NgStage {
+struct NgSlot {                  // one token's staged lookups (double-buffered by token parity)
   uint32_t tok[kMaxOrders][kSlots], cnt[kMaxOrders][kSlots];
-  uint32_t n[kMaxOrders], ns[kMaxOrders], nrec[kMaxOrders], es[kMaxOrders];
+  uint32_t ns[kMaxOrders];
   int r[kMaxOrders];
   double mu[kMaxOrders], beta[kMaxOrders];
-  unsigned long long key[kMaxOrders];
-  uint32_t hist[4];
+};
+struct NgStage {
+  NgSlot slot[2];
   uint32_t hkey[NG_HASH], hpos[NG_HASH];
   uint32_t mtok[kMaxSparse];
   float madd[kMaxSparse];
@@ -421,83 +423,140 @@ __host__ __device__ constexpr size_t ng_group_bytes(uint32_t V) {   // one chunk
 }
 __device__ __forceinline__ uint32_t ng_hslot(uint32_t tk) { return (tk * 2654435761u) >> (32 - 9); }
 
+// Per token i (slot b = i & 1):
+//   order warps k-1 (k = 1..4): probe context k once -- the key serves the prediction and the
+//     update -- stage the record in slot b; chunk barrier; then the count update from what
+//     they staged (writes only), and on to token i + 1 (staging into the other slot)
+//   merge warp (the fifth): after the barrier, the merged prediction of token i from slot b
+//     into the ring entry -- concurrently with the order warps' update and next lookups
+// One barrier per token: slot b is rewritten (token i + 2) only after the barrier of token
+// i + 1, which the merge warp reaches after finishing token i.
 __global__ void ngram_pre_kernel(WalkArgs a) {
   extern __shared__ __align__(16) uint8_t ng_raw[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int lc = w >> 2, kw = w & 3, k = kw + 1;     // chunk in CTA, order of this warp
+  const int lc = w / NGWC, kw = w % NGWC, k = kw + 1;   // chunk in CTA; order (kw < 4) or merge warp (kw == 4)
+  const bool merger = kw == kMaxOrders;
   const int e = blockIdx.x * NGC + lc;
-  if (e >= a.n_entries) return;                       // whole 4-warp groups exit together
+  if (e >= a.n_entries) return;                       // whole 5-warp groups exit together
   const uint32_t nbw = (a.V + 31) / 32;
   NgStage &S = *reinterpret_cast<NgStage *>(ng_raw + (size_t)lc * ng_group_bytes(a.V));
   uint32_t *bitmap = reinterpret_cast<uint32_t *>(&S + 1);
   const int bar = 1 + lc;
+  constexpr int BAR_THREADS = 32 * NGWC;
   const int c = a.chunk_of[e], count = a.count[e];
   WalkState *st = a.st + c;
-  const bool active = k <= (int)a.orders;
-  const size_t tb = (size_t)c * kMaxOrders + kw;
+  const bool active = !merger && k <= (int)a.orders;
+  const size_t tb = (size_t)c * kMaxOrders + (merger ? 0 : kw);
   unsigned long long *keys = a.ng_keys + tb * a.hcap;
   uint32_t *vals = a.ng_vals + tb * a.hcap;
   NgRecord *recs = a.ng_recs + tb * a.rcap;
-  if (kw == 0) {
+  if (merger) {
     for (uint32_t x = lane; x < nbw; x += 32) bitmap[x] = 0u;
     for (int x = lane; x < NG_HASH; x += 32) S.hkey[x] = 0xffffffffu;
-    if (lane < 4) S.hist[lane] = st->hist[lane];
   }
-  if (lane == 0) S.nrec[kw] = st->nrec[kw];
+  uint32_t hist[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) hist[j] = st->hist[j];
+  uint32_t nrec = merger ? 0u : st->nrec[kw];
   const uint32_t i0 = st->ng_i;
-  asm volatile("bar.sync %0, 128;" ::"r"(bar) : "memory");
+  const int64_t toff = a.tok_off[c];
+  asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(BAR_THREADS) : "memory");
   for (int it = 0; it < count; ++it) {
     const uint32_t i = i0 + it;
-    const uint32_t t = a.tokens[a.tok_off[c] + i];   // issued early: needed only by the update
-    // ---- A: probe + stage (order k)
-    if (active && i >= (uint32_t)k) {
-      uint32_t h[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) h[j] = S.hist[j];
-      const unsigned long long key = fnv_ctx(k, h);
-      uint32_t es = 0xffffffffu;
-      const int r = ng_probe(keys, vals, a.hcap, key, lane, &es);
-      uint32_t ns = 0, n = 0, s = 0;
-      if (r >= 0) {
-        const NgRecord *R = recs + r;
-        ns = R->nslot;
-        n = R->n;
-        const uint32_t t0 = R->tok[lane], t1 = R->tok[lane + 32], c0 = R->cnt[lane], c1 = R->cnt[lane + 32];
-        S.tok[kw][lane] = t0; S.tok[kw][lane + 32] = t1;
-        S.cnt[kw][lane] = c0; S.cnt[kw][lane + 32] = c1;
-        if ((uint32_t)lane < ns) s += c0;
-        if ((uint32_t)lane + 32 < ns) s += c1;
-#pragma unroll
-        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      }
-      if (lane == 0) {
-        S.r[kw] = r; S.es[kw] = es; S.ns[kw] = ns; S.n[kw] = n; S.key[kw] = key;
+    NgSlot &Q = S.slot[i & 1];
+    if (!merger) {
+      const uint32_t t = a.tokens[toff + i];   // issued early: needed only by the update
+      // ---- lookup + stage (order k)
+      int r = -1;
+      uint32_t es = 0xffffffffu, ns = 0, n = 0;
+      unsigned long long key = 0;
+      uint32_t t0 = 0, t1 = 0, c0 = 0, c1 = 0;
+      if (active && i >= (uint32_t)k) {
+        key = fnv_ctx(k, hist);
+        r = ng_probe(keys, vals, a.hcap, key, lane, &es);
+        uint32_t s = 0;
         if (r >= 0) {
-          const double nd = (double)n;
-          const double lam = __ddiv_rn(nd, __dadd_rn(nd, 5.0));
-          S.mu[kw] = __dsub_rn(1.0, __ddiv_rn(__dmul_rn(lam, (double)s), nd));
-          S.beta[kw] = __ddiv_rn(lam, nd);
-        } else {
-          S.mu[kw] = 1.0;
-          S.beta[kw] = 0.0;
+          const NgRecord *R = recs + r;
+          ns = R->nslot;
+          n = R->n;
+          t0 = R->tok[lane]; t1 = R->tok[lane + 32]; c0 = R->cnt[lane]; c1 = R->cnt[lane + 32];
+          Q.tok[kw][lane] = t0; Q.tok[kw][lane + 32] = t1;
+          Q.cnt[kw][lane] = c0; Q.cnt[kw][lane + 32] = c1;
+          if ((uint32_t)lane < ns) s += c0;
+          if ((uint32_t)lane + 32 < ns) s += c1;
+#pragma unroll
+          for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        }
+        if (lane == 0) {
+          Q.r[kw] = r; Q.ns[kw] = ns;
+          if (r >= 0) {
+            const double nd = (double)n;
+            const double lam = __ddiv_rn(nd, __dadd_rn(nd, 5.0));
+            Q.mu[kw] = __dsub_rn(1.0, __ddiv_rn(__dmul_rn(lam, (double)s), nd));
+            Q.beta[kw] = __ddiv_rn(lam, nd);
+          } else {
+            Q.mu[kw] = 1.0;
+            Q.beta[kw] = 0.0;
+          }
+        }
+      } else if (lane == 0) {
+        Q.r[kw] = -1; Q.ns[kw] = 0; Q.mu[kw] = 1.0; Q.beta[kw] = 0.0;
+      }
+      asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(BAR_THREADS) : "memory");
+      // ---- count update of order k with token t (writes only, from this warp's registers)
+      if (active && i >= (uint32_t)k) {
+        bool fresh = false;
+        if (r < 0) {
+          if (!(nrec >= a.cap || nrec >= a.rcap || es == 0xffffffffu)) {   // capacity freeze (D22)
+            r = (int)nrec;
+            fresh = true;
+            if (lane == 0) {
+              keys[es] = key;
+              vals[es] = (uint32_t)r;
+            }
+            ++nrec;
+          }
+        }
+        if (r >= 0) {
+          NgRecord *R = recs + r;
+          if (fresh) { ns = 0; n = 0; }
+          const bool h0 = (uint32_t)lane < ns && t0 == t;
+          const bool h1 = (uint32_t)lane + 32 < ns && t1 == t;
+          const unsigned m0 = __ballot_sync(0xffffffffu, h0), m1 = __ballot_sync(0xffffffffu, h1);
+          if (m0 | m1) {
+            if (h0) R->cnt[lane] = c0 + 1;
+            if (h1) R->cnt[lane + 32] = c1 + 1;
+          } else if (ns < kSlots) {
+            if (lane == 0) { R->tok[ns] = t; R->cnt[ns] = 1; R->nslot = ns + 1; }
+          } else {   // evict the lowest count, ties -> lowest slot (D21)
+            uint32_t bcnt = c0, bidx = lane;
+            if (c1 < bcnt) { bcnt = c1; bidx = lane + 32; }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+              const uint32_t oc = __shfl_xor_sync(0xffffffffu, bcnt, o), oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+              if (oc < bcnt || (oc == bcnt && oi < bidx)) { bcnt = oc; bidx = oi; }
+            }
+            if (lane == 0) { R->tok[bidx] = t; R->cnt[bidx] = 1; }
+          }
+          if (lane == 0) R->n = n + 1;
         }
       }
-    } else if (lane == 0) {
-      S.r[kw] = -1; S.ns[kw] = 0; S.mu[kw] = 1.0; S.beta[kw] = 0.0; S.es[kw] = 0xffffffffu;
-    }
-    asm volatile("bar.sync %0, 128;" ::"r"(bar) : "memory");
-    // ---- B: merged prediction (warp 0)
-    if (kw == 0) {
+      __syncwarp();
+      __threadfence_block();
+      hist[0] = hist[1]; hist[1] = hist[2]; hist[2] = hist[3]; hist[3] = t;
+    } else {
+      asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(BAR_THREADS) : "memory");
+      // ---- merged prediction of token i (same order and arithmetic as ng_predict_warp)
       NgTok *out = a.ng_pre + (size_t)c * a.ng_ring + (i % a.ng_ring);
       if (i >= a.warmup) {
         double a0 = 1.0;
-        for (int kk = 1; kk <= (int)a.orders; ++kk) a0 = __dmul_rn(a0, S.mu[kk - 1]);
+        for (int kk = 1; kk <= (int)a.orders; ++kk) a0 = __dmul_rn(a0, Q.mu[kk - 1]);
         uint32_t nout = 0;
         for (int kk = 1; kk <= (int)a.orders; ++kk) {
-          if (S.r[kk - 1] < 0) continue;
-          double ak = S.beta[kk - 1];
-          for (int j = kk + 1; j <= (int)a.orders; ++j) ak = __dmul_rn(ak, S.mu[j - 1]);
-          const uint32_t ns = S.ns[kk - 1];
+          if (Q.r[kk - 1] < 0) continue;
+          double ak = Q.beta[kk - 1];
+          for (int j = kk + 1; j <= (int)a.orders; ++j) ak = __dmul_rn(ak, Q.mu[j - 1]);
+          const uint32_t ns = Q.ns[kk - 1];
           for (uint32_t s0 = 0; s0 < ns; s0 += 32) {
             const uint32_t sl = s0 + lane;
             const bool act = sl < ns;
@@ -505,8 +564,8 @@ __global__ void ngram_pre_kernel(WalkArgs a) {
             bool first = false;
             float add = 0.f;
             if (act) {
-              tk = S.tok[kk - 1][sl];
-              add = (float)__dmul_rn(ak, (double)S.cnt[kk - 1][sl]);
+              tk = Q.tok[kk - 1][sl];
+              add = (float)__dmul_rn(ak, (double)Q.cnt[kk - 1][sl]);
               const uint32_t bit = 1u << (tk & 31);
               first = !(atomicOr(&bitmap[tk >> 5], bit) & bit);
             }
@@ -542,63 +601,17 @@ __global__ void ngram_pre_kernel(WalkArgs a) {
           out->n = nout;
           out->a0f = (float)__ddiv_rn(a0, (double)i + (double)a.V);
         }
+        __syncwarp();
       } else if (lane == 0) {
         out->n = 0;
         out->a0f = 0.f;
       }
     }
-    // ---- C: count update of order k with token t (writes only)
-    if (active && i >= (uint32_t)k) {
-      int r = S.r[kw];
-      bool fresh = false;
-      if (r < 0) {
-        const uint32_t used = S.nrec[kw], es = S.es[kw];
-        if (!(used >= a.cap || used >= a.rcap || es == 0xffffffffu)) {   // capacity freeze (D22)
-          r = (int)used;
-          fresh = true;
-          if (lane == 0) {
-            S.nrec[kw] = used + 1;
-            keys[es] = S.key[kw];
-            vals[es] = (uint32_t)r;
-          }
-        }
-      }
-      if (r >= 0) {
-        NgRecord *R = recs + r;
-        const uint32_t ns = fresh ? 0u : S.ns[kw];
-        const uint32_t n = fresh ? 0u : S.n[kw];
-        const bool h0 = (uint32_t)lane < ns && S.tok[kw][lane] == t;
-        const bool h1 = (uint32_t)lane + 32 < ns && S.tok[kw][lane + 32] == t;
-        const unsigned m0 = __ballot_sync(0xffffffffu, h0), m1 = __ballot_sync(0xffffffffu, h1);
-        if (m0 | m1) {
-          if (h0) R->cnt[lane] = S.cnt[kw][lane] + 1;
-          if (h1) R->cnt[lane + 32] = S.cnt[kw][lane + 32] + 1;
-        } else if (ns < kSlots) {
-          if (lane == 0) { R->tok[ns] = t; R->cnt[ns] = 1; R->nslot = ns + 1; }
-        } else {   // evict the lowest count, ties -> lowest slot (D21)
-          uint32_t bcnt = S.cnt[kw][lane], bidx = lane;
-          if (S.cnt[kw][lane + 32] < bcnt) { bcnt = S.cnt[kw][lane + 32]; bidx = lane + 32; }
-#pragma unroll
-          for (int o = 16; o; o >>= 1) {
-            const uint32_t oc = __shfl_xor_sync(0xffffffffu, bcnt, o), oi = __shfl_xor_sync(0xffffffffu, bidx, o);
-            if (oc < bcnt || (oc == bcnt && oi < bidx)) { bcnt = oc; bidx = oi; }
-          }
-          if (lane == 0) { R->tok[bidx] = t; R->cnt[bidx] = 1; }
-        }
-        if (lane == 0) R->n = n + 1;
-      }
-    }
-    __syncwarp();
-    __threadfence_block();
-    if (kw == 0 && lane == 0) {
-      S.hist[0] = S.hist[1]; S.hist[1] = S.hist[2]; S.hist[2] = S.hist[3]; S.hist[3] = t;
-    }
-    asm volatile("bar.sync %0, 128;" ::"r"(bar) : "memory");
   }
-  if (lane == 0) st->nrec[kw] = S.nrec[kw];
+  if (!merger && lane == 0) st->nrec[kw] = nrec;
   if (kw == 0 && lane == 0) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) st->hist[j] = S.hist[j];
+    for (int j = 0; j < 4; ++j) st->hist[j] = hist[j];
     st->ng_i = i0 + (uint32_t)count;
   }
 }
@@ -611,7 +624,7 @@ void launch_ngram_precompute(const WalkArgs &a, cudaStream_t s) {
     cudaFuncSetAttribute(ngram_pre_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  ngram_pre_kernel<<<(a.n_entries + NGC - 1) / NGC, 128 * NGC, smem, s>>>(a);
+  ngram_pre_kernel<<<(a.n_entries + NGC - 1) / NGC, 32 * NGWC * NGC, smem, s>>>(a);
 }
 
 // ---------------------------------------------------------------- walk ---
