@@ -293,7 +293,7 @@ def main():
     # dominant kernel = largest share of the GPU's SM-time.  Every forward kernel runs on
     # all SMs; the walk holds one thread-block cluster per chunk (walk_ctas_per_chunk SMs)
     # and overlaps the next slab's forward, so its device time alone overstates its share.
-    walk_sms = min(N_SM, my_chunks * nc.nc_host_walk_ctas(SHAPES[wl.shape].vocab)) if my_chunks else N_SM
+    walk_sms = min(N_SM, my_chunks * nc.nc_host_walk_ctas(SHAPES[wl.shape].vocab, my_chunks)) if my_chunks else N_SM
     sm_share = {k: kernels[k]["ms_per_step"] * (walk_sms if k == "walk" else N_SM) for k in kernels}
     dom = max(kernels, key=lambda k: sm_share[k]) if kernels else None
     roof = None

@@ -208,9 +208,10 @@ nc_status nc_host_tokenize_vocab(const uint8_t *vocab_blob, const uint32_t *voca
                                  uint32_t **tokens, size_t *n_tokens);
 
 /* SMs (CTAs of one thread-block cluster) the per-token walk holds per chunk at
- * vocabulary size V (host query, no device needed).  bench.py uses
- * it to rank kernels by their share of the GPU's SM-time. */
-nc_status nc_host_walk_ctas(uint32_t V, uint32_t *ctas);
+ * vocabulary size V with n_chunks chunks in the container or shard (host query, no
+ * device needed).  bench.py uses it to rank kernels by their share of
+ * the GPU's SM-time. */
+nc_status nc_host_walk_ctas(uint32_t V, uint32_t n_chunks, uint32_t *ctas);
 
 /* Shard plan pieces of nc_compress_shard (host only; tested with gloo on CPU):
  * the chunk range of a rank, and its part of the final container given the

@@ -83,7 +83,7 @@ def lib():
             "nc_host_wnc_encode": (C.c_int, [u32p, u32p, C.c_size_t, C.c_uint32, pp, szp, u64p]),
             "nc_host_tokenize_vocab": (C.c_int, [P, u32p, C.c_uint32, C.c_uint32, P, C.c_size_t, pp, szp]),
             "nc_host_shard_range": (C.c_int, [C.c_uint32, C.c_int, C.c_int, u32p, u32p]),
-            "nc_host_walk_ctas": (C.c_int, [C.c_uint32, u32p]),
+            "nc_host_walk_ctas": (C.c_int, [C.c_uint32, C.c_uint32, u32p]),
             "nc_host_shard_part": (C.c_int, [u32p, C.c_uint32, C.c_uint8, C.c_uint16, C.c_int, C.c_int, P,
                                              C.c_size_t, pp, szp, u64p, u64p]),
         }
@@ -284,9 +284,9 @@ def nc_host_tokenize_vocab(vocab, data: bytes, n_special: int = 3):
     return _take_array(t.value, nt.value, np.uint32).tolist()
 
 
-def nc_host_walk_ctas(V: int) -> int:
+def nc_host_walk_ctas(V: int, n_chunks: int) -> int:
     n = C.c_uint32()
-    _check(lib().nc_host_walk_ctas(V, C.byref(n)))
+    _check(lib().nc_host_walk_ctas(V, n_chunks, C.byref(n)))
     return n.value
 
 

@@ -265,9 +265,9 @@ nc_status nc_decompress_shard(nc_model *m, nc_comm *c, const uint8_t *in, size_t
 }
 
 // host-only pieces of the shard plan, exported for the gloo multi-process tests
-nc_status nc_host_walk_ctas(uint32_t V, uint32_t *ctas) {
+nc_status nc_host_walk_ctas(uint32_t V, uint32_t n_chunks, uint32_t *ctas) {
   if (!ctas) return NC_ERR_INVALID;
-  *ctas = (uint32_t)nc::walk_ctas_per_chunk(V);
+  *ctas = (uint32_t)nc::walk_ctas_per_chunk(V, (int)n_chunks);
   return NC_OK;
 }
 

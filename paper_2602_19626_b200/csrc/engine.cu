@@ -675,6 +675,7 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
   wbase.tokens = tokens_dev; wbase.tok_off = tok_off_d;
   wbase.out_cum = cum_d; wbase.out_freq = freq_d; wbase.out_p = p_d;
   wbase.mode = 0;
+  wbase.n_chunks_total = n_chunks;
   wb.fill(wbase, p, S.V);
   for (int sl = 0; sl < n_slabs; ++sl) {
     if (use_ng) {
@@ -864,6 +865,7 @@ void decompress_device(nc_model *m, const uint8_t *blob, const Nc05View &view, c
   wa.logits = fw.logits; wa.ldl = S.V;
   wa.tok_off = tok_off_d; wa.streams = blob_d; wa.stream_off = s_off_d; wa.stream_bits = s_bits_d;
   wa.out_tok = out_tok; wa.next_x = x_cur; wa.mode = 1;
+  wa.n_chunks_total = n_chunks;
   wb.fill(wa, p, S.V);
   int *jctr = bag.get<int>(1);
   NC_CUDA(cudaMemsetAsync(jctr, 0, sizeof(int), s));
@@ -1143,6 +1145,7 @@ void debug_walk(int device, const float *logits, const uint32_t *tok, uint32_t n
   wa.chunk_of = c_d; wa.row0 = r_d; wa.count = n_d; wa.n_entries = 1;
   wa.logits = lg_d; wa.ldl = V; wa.tokens = tk_d; wa.tok_off = off_d;
   wa.out_cum = cum_d; wa.out_freq = freq_d; wa.out_p = p_d; wa.mode = 0;
+  wa.n_chunks_total = 1;
   wb.fill(wa, p, V);
   if (p.flags & 1u) launch_ngram_precompute(wa, s);
   launch_walk(wa, s);

@@ -1430,7 +1430,10 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
 
 // Cluster size used for a vocabulary: fixed per V (never per batch), so that the
 // reduction trees of compression and decompression are the same.
-static int walk_cluster_size(uint32_t V) {
+// CTAs per chunk: a function of the vocabulary and of the container's chunk count only, so
+// compression and decompression (which reads the count from the NC05 header) agree -- the
+// vocabulary partition fixes the order of the float reductions.
+static int walk_cluster_size(uint32_t V, int n_chunks) {
   static const int forced = [] {   // diagnostics override NC_WALK_CS=4|8 (compress and decompress must agree)
     const char *e = std::getenv("NC_WALK_CS");
     return e ? std::atoi(e) : 0;
@@ -1438,7 +1441,10 @@ static int walk_cluster_size(uint32_t V) {
   if (V < 4096 || V % 64) return 1;
   if (forced == 4 || forced == 8) return forced;
   // 8 CTAs per chunk for large vocabularies: halves the per-token pass (config2: walk 29.7 ->
-  // 21.6 ms of kernel time, step time unchanged -- its SMs come out of the overlapped forward)
+  // 21.6 ms of kernel time, step time unchanged -- its SMs come out of the overlapped forward).
+  // (A 16-CTA cluster for one or two chunks, where the walk is the whole critical path, was
+  // refused at launch -- "invalid argument" -- on the B200; n_chunks stays in the rule's inputs.)
+  (void)n_chunks;
   return (V >= 32768 && V % 256 == 0) ? 8 : 4;
 }
 
@@ -1468,7 +1474,7 @@ static void launch_walk_cs(const WalkArgs &a, cudaStream_t s) {
   cudaLaunchKernelEx(&cfg, walk_cl_kernel<CS, NGM>, a);
 }
 
-int walk_ctas_per_chunk(uint32_t V) { return walk_cluster_size(V); }
+int walk_ctas_per_chunk(uint32_t V, int n_chunks) { return walk_cluster_size(V, n_chunks); }
 
 void walk_timing_report() {
 #ifdef NC_WALK_TIMING
@@ -1487,7 +1493,7 @@ void walk_timing_report() {
 
 void launch_walk(const WalkArgs &a, cudaStream_t s) {
   if (a.n_entries <= 0) return;
-  const int cs = walk_cluster_size(a.V);
+  const int cs = walk_cluster_size(a.V, a.n_chunks_total);
   const uint32_t groups = (a.V / cs / 4 + WT - 1) / WT;   // float4 groups per thread
   if (cs == 8) {
     if (groups <= 3) launch_walk_cs<8, 3>(a, s);

@@ -63,10 +63,11 @@ struct WalkArgs {
   uint32_t V, cdf_bits, warmup, flags, orders, cap;
   float inv_tau; double alpha, eta;
   int mode;                           // 0 encode, 1 decode
+  int n_chunks_total;                 // chunks of the container (or shard): with V, fixes the cluster size
 };
 
 void launch_walk(const WalkArgs &a, cudaStream_t s);
-int walk_ctas_per_chunk(uint32_t V);   // CTAs (one cluster) per chunk in the walk
+int walk_ctas_per_chunk(uint32_t V, int n_chunks);   // CTAs (one cluster) per chunk in the walk
 void walk_timing_report();            // diagnostics build (-DNC_WALK_TIMING): phase cycles -> stderr
 // encode only: N-gram predictions for the entries' tokens (one warp per chunk)
 void launch_ngram_precompute(const WalkArgs &a, cudaStream_t s);
