@@ -7,6 +7,9 @@ c5       : config 5 on the config-2 input: compress B/s and bpb at L = 512 / 102
            (C = L/4, 8 chunks), CDF-16 vs CDF-24 (delta bits/token vs log2(T/(T-V))),
            and sequential decode (decompress) with 64 chunks at each window.
 c2chunks : config 2 with 1 vs 8 chunks (compress B/s, bpb, walk us/token/chunk).
+slabs    : config 2 (8 chunks) under explicit slab plans (NC_SLAB_PLAN), median of 5 with a
+           256 MB L2 flush between runs: the first slab's 256-row tile count against the
+           74 CTA pairs of the GEMMs vs the length of the last slab's walk.
 Configs 3 and 4 run through bench.py (--workload config3 / config4_shard).
 Timing: CUDA events on the launching stream around nc_compress_tokens (device-resident
 token ids, like bench.py's value), median of 3 after 1 warm-up; decompress: wall clock of
@@ -46,13 +49,21 @@ def tokens_dev(data, n_chunks):
     return torch.from_numpy(tok.view(np.int32).copy()).cuda(), ntok
 
 
-def compress_timed(data, prm, n_chunks, reps=3):
+_flush = None
+
+
+def compress_timed(data, prm, n_chunks, reps=3, flush=False):
+    global _flush
+    if flush and _flush is None:
+        _flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     td, ntok = tokens_dev(data, n_chunks)
     f = lambda: nc.nc_compress_tokens(model, td.data_ptr(), np.array(ntok, np.uint32), prm, stream.cuda_stream)
     f()
     ts = []
     blob = None
     for _ in range(reps):
+        if flush:
+            _flush.fill_(1)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -78,6 +89,18 @@ if "c2chunks" in args:
         line(config="config2", chunks=n_chunks, bytes=len(data2), tokens=ntok, compress_Bps=len(data2) / t,
              ms=1e3 * t, bpb=8.0 * len(blob) / len(data2),
              walk_us_per_token_per_chunk=1e3 * st["walk_ms"] / (ntok / n_chunks))
+
+if "slabs" in args:
+    prm = nc.nc_params_default(window=2048, slide=512, n_chunks=8)
+    for plan in ("", "2944", "3072", "3200", "3328", "3456", "3584", "3072,640", "2560,1024"):
+        if plan:
+            os.environ["NC_SLAB_PLAN"] = plan
+        else:
+            os.environ.pop("NC_SLAB_PLAN", None)
+        t, blob, ntok, st = compress_timed(data2, prm, 8, reps=5, flush=True)
+        line(config="config2", chunks=8, slab_plan=plan or "default", compress_Bps=len(data2) / t, ms=1e3 * t,
+             bytes=len(blob))
+    os.environ.pop("NC_SLAB_PLAN", None)
 
 if "c5" in args:
     bits = {}
