@@ -371,3 +371,60 @@ def test_shard_path_one_rank_nccl(nc, m2):
         assert o2 == 0 and t2 == len(data) and out == data
     finally:
         comm.close()
+
+
+@pytest.mark.slow
+def test_config2_full_size_chunk0(nc):
+    """config2 at full size in bench.py's launch configuration (152,089 B, 30 layers,
+    L = 2048 / C = 512, 8 chunks, the two-slab plan, 8-CTA walk clusters): the container
+    round-trips; chunk 0 (~3.9K tokens, two window slides) is recomputed by the oracle
+    (blocked fp64 LM + the step-by-step walk) -- p(t) within 1e-4 at every row, logits
+    within 1e-5 of max|z| on sampled rows, bit count within 0.5 %; and the chunk's stream
+    in the 8-chunk container equals the host WNC encoding of the (cum, freq) the debug
+    forward + walk give for that chunk alone (batch / slab independence at full size), so
+    the §8(c) coder bound can be checked on the container's own bit count."""
+    import struct
+    from oracle.chunking import split_chunks
+    from oracle.ensemble import Params, encode_tokens
+    from oracle.lm import LM
+    from oracle.ncw import Weights
+    from oracle.tokenizer import Tokenizer
+    from synth import WORKLOADS, ensure_model, ensure_text
+    wl = WORKLOADS["config2"]
+    path = ensure_model(wl.shape)
+    data = open(ensure_text("config2"), "rb").read()
+    m = nc.Model(path, 0)
+    prm = nc.nc_params_default(window=wl.window, slide=wl.slide, n_chunks=wl.n_chunks)
+    blob = nc.nc_compress(m, data, prm)
+    assert nc.nc_decompress(m, blob, prm) == data
+    n = struct.unpack_from("<BHH", blob, 4)[2]
+    assert n == wl.n_chunks
+    table = [struct.unpack_from("<III", blob, 9 + 12 * c) for c in range(n)]
+    assert all(t[2] == (t[1] + 7) // 8 for t in table)
+    assert len(blob) == 9 + 12 * n + sum(t[2] for t in table)
+    s0 = blob[9 + 12 * n:9 + 12 * n + table[0][2]]
+
+    w = Weights(path)
+    ch0 = split_chunks(data, n)[0]
+    toks = Tokenizer(w.vocab).encode(ch0)
+    assert len(toks) == table[0][0] and len(toks) > 2 * wl.window
+    x = [w.bos] + toks[:-1]
+    z = nc.nc_debug_forward(m, x, prm, 0)
+    cum, freq, p_gpu = nc.nc_debug_walk(z, toks, prm)
+    stream, bits = nc.nc_host_wnc_encode(cum, freq, 24)
+    assert bits == table[0][1] and stream == s0
+    T = 1 << 24
+    f = freq.astype(np.float64)
+    bound = (-np.log2(f / T) - np.log2(1.0 - 2.0 ** (24 - 30) / f)).sum() + 64
+    assert bits <= bound, (bits, bound)
+
+    Z = LM(w).forward_blocked(x, wl.window, wl.slide)
+    rows = sorted(set([0, 1, 99, 100, 2047, 2048, 2559, 2560, len(x) - 1] + list(range(0, len(x), 97))))
+    zerr = np.abs(z[rows] - Z[rows]).max() / np.abs(Z[rows]).max()
+    assert zerr < Z_TOL, zerr
+    ref = encode_tokens(Z, toks, w.V, Params(window=wl.window, slide=wl.slide, n_chunks=1))
+    p_ref = np.array(ref["p_true"])
+    rel = np.abs(p_gpu - p_ref) / p_ref
+    assert rel.max() < P_TOL, rel.max()
+    assert abs(bits - ref["bits"]) <= 0.005 * ref["bits"], (bits, ref["bits"])
+    m.close()
