@@ -335,6 +335,18 @@ def main():
     for k in flop_classes & set(kernels):
         kernels[k]["tflops"] = kernels[k]["work_per_step"] / (kernels[k]["ms_per_step"] / 1e3) / 1e12
 
+    # ---- fused roofline of the whole step: the algorithmic FLOPs of the
+    # forward at the 3xTF32 sustained tensor rate plus the walk's 8V bytes per token (logits
+    # written by the head, read by the walk) at measured HBM bandwidth, against the step time
+    fused = None
+    if kernels and flop_classes & set(kernels):
+        f_step = sum(kernels[k]["work_per_step"] for k in flop_classes & set(kernels))
+        b_step = 8.0 * SHAPES[wl.shape].vocab * float(sum(ntok))
+        t_roof = f_step / (tc_peak * 1e12) + b_step / (pk["hbm_gbs"] * 1e9)
+        fused = {"flop_per_step": f_step, "bytes_per_step": b_step, "ms_roofline": 1e3 * t_roof,
+                 "frac": t_roof / (t_val / args.steps),
+                 "peaks": f"{tc_peak:.1f} TFLOP/s (3xTF32 sustained), {pk['hbm_gbs']:.0f} GB/s"}
+
     # ---- CPU oracle baseline (rank 0, N = 1 only, bounded sample)
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
@@ -363,6 +375,7 @@ def main():
                     "d2h_bytes_per_step": 8 * n_tok_total},
             "gpu_launches": launches,
             "roofline": roof,
+            "fused_roofline": fused,
             "cpu_baseline": cpu,
             "clocks": clk,
             "bpb": bpb,
