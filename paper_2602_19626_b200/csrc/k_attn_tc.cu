@@ -595,14 +595,20 @@ void launch_attention_tc(const AttnTcArgs &a, cudaStream_t s) {
   const CUtensorMap *kh = tmap_nd(a.k_hi, 4, kd, kbx), *kl = tmap_nd(a.k_lo, 4, kd, kbx);
   const CUtensorMap *vh = tmap_nd(a.v_hi, 4, kd, kbx, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   const CUtensorMap *vl = tmap_nd(a.v_lo, 4, kd, kbx, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
-  static int *ctr = nullptr;   // {next item, CTAs done}; zero between launches (last CTA resets)
-  static int n_sms = 0;
+  // {next item, CTAs done}, zero between launches (last CTA resets); one per device, since
+  // one process may drive models on several GPUs (nc_model_load takes a device)
+  constexpr int kMaxDevices = 64;
+  static int *ctrs[kMaxDevices] = {};
+  static int sms[kMaxDevices] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDevices) throw std::runtime_error("device index out of range");
+  int *&ctr = ctrs[dev];
+  int &n_sms = sms[dev];
   if (!ctr) {
     if (cudaMalloc(&ctr, 2 * sizeof(int)) != cudaSuccess) throw std::runtime_error("cudaMalloc attention counter");
     cudaMemset(ctr, 0, 2 * sizeof(int));
     cudaDeviceSynchronize();
-    int dev;
-    cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev);
   }
   AttnTcArgs aa = a;

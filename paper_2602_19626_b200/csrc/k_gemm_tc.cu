@@ -749,8 +749,19 @@ static const bool g_pdl = !(std::getenv("NC_PDL") && std::getenv("NC_PDL")[0] ==
 bool pdl_enabled() { return g_pdl; }
 void set_splitk_mode(int mode) { g_splitk_mode = mode; }
 
+// Per-device state below: nc_model_load takes a device, so one process may drive several
+// GPUs; each device gets its own counters / workspace (indexed by the current device).
+constexpr int kMaxDevices = 64;
+static int cur_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDevices) throw std::runtime_error("device index out of range");
+  return dev;
+}
+
 static int *tile_counter() {   // {next tile, CTAs done}; zero between launches
-  static int *ctr = nullptr;
+  static int *ctrs[kMaxDevices] = {};
+  int *&ctr = ctrs[cur_device()];
   if (!ctr) {
     if (cudaMalloc(&ctr, 2 * sizeof(int)) != cudaSuccess) throw std::runtime_error("cudaMalloc tile counter");
     cudaMemset(ctr, 0, 2 * sizeof(int));
@@ -767,8 +778,11 @@ static bool capturing(cudaStream_t s) {
 }
 static cudaStream_t g_launch_stream = nullptr;
 static float *splitk_workspace(size_t floats) {
-  static float *ws = nullptr;
-  static size_t cap = 0;
+  static float *wss[kMaxDevices] = {};
+  static size_t caps[kMaxDevices] = {};
+  const int dev = cur_device();
+  float *&ws = wss[dev];
+  size_t &cap = caps[dev];
   if (floats > cap) {
     if (capturing(g_launch_stream)) throw std::runtime_error("split-K workspace must be sized before graph capture");
     if (ws) cudaFree(ws);
@@ -778,8 +792,11 @@ static float *splitk_workspace(size_t floats) {
   return ws;
 }
 static int *splitk_counters(size_t n) {
-  static int *ctr = nullptr;
-  static size_t cap = 0;
+  static int *ctrs[kMaxDevices] = {};
+  static size_t caps[kMaxDevices] = {};
+  const int dev = cur_device();
+  int *&ctr = ctrs[dev];
+  size_t &cap = caps[dev];
   if (n > cap) {
     if (capturing(g_launch_stream)) throw std::runtime_error("split-K counters must be sized before graph capture");
     if (ctr) cudaFree(ctr);
