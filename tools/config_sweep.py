@@ -7,6 +7,8 @@ c5       : config 5 on the config-2 input: compress B/s and bpb at L = 512 / 102
            (C = L/4, 8 chunks), CDF-16 vs CDF-24 (delta bits/token vs log2(T/(T-V))),
            and sequential decode (decompress) with 64 chunks at each window.
 c2chunks : config 2 with 1 vs 8 chunks (compress B/s, bpb, walk us/token/chunk).
+c3 [rows]: config 3 (10 MB, 64 chunks) with max_slab_rows = rows (default 32768); run under
+           NC_WALK_CS=4|8 to compare walk cluster sizes (read once per process).
 slabs    : config 2 (8 chunks) under explicit slab plans (NC_SLAB_PLAN), median of 5 with a
            256 MB L2 flush between runs: the first slab's 256-row tile count against the
            74 CTA pairs of the GEMMs vs the length of the last slab's walk.
@@ -79,7 +81,8 @@ def line(**kw):
     print(json.dumps(kw), flush=True)
 
 
-args = set(sys.argv[1:]) or {"c5", "c2chunks"}
+args = set(a for a in sys.argv[1:] if not a.isdigit()) or {"c5", "c2chunks"}
+nums = [int(a) for a in sys.argv[1:] if a.isdigit()]
 data2 = open(ensure_text("config2"), "rb").read()
 
 if "c2chunks" in args:
@@ -89,6 +92,14 @@ if "c2chunks" in args:
         line(config="config2", chunks=n_chunks, bytes=len(data2), tokens=ntok, compress_Bps=len(data2) / t,
              ms=1e3 * t, bpb=8.0 * len(blob) / len(data2),
              walk_us_per_token_per_chunk=1e3 * st["walk_ms"] / (ntok / n_chunks))
+
+if "c3" in args:
+    data3 = open(ensure_text("config3"), "rb").read()
+    rows = nums[0] if nums else 32768
+    prm = nc.nc_params_default(window=2048, slide=512, n_chunks=64, max_slab_rows=rows)
+    t, blob, ntok, st = compress_timed(data3, prm, 64, reps=2, flush=True)
+    line(config="config3", chunks=64, max_slab_rows=rows, walk_cs=os.environ.get("NC_WALK_CS", "default"),
+         compress_Bps=len(data3) / t, ms=1e3 * t, bytes=len(blob))
 
 if "slabs" in args:
     prm = nc.nc_params_default(window=2048, slide=512, n_chunks=8)
