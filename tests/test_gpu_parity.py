@@ -428,3 +428,34 @@ def test_config2_full_size_chunk0(nc):
     assert rel.max() < P_TOL, rel.max()
     assert abs(bits - ref["bits"]) <= 0.005 * ref["bits"], (bits, ref["bits"])
     m.close()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("L,bits", [(512, 24), (1024, 16)])
+def test_config5_windows_full_model(nc, L, bits):
+    """Config 5 variants on the 30-layer model: window L with C = L/4 (D11) over enough
+    rows for several slides, CDF-16 and CDF-24 -- GPU logits within 1e-5 of max|z| of the
+    blocked fp64 oracle, and the walk's p(t) within 1e-4 of the oracle walk on them."""
+    from oracle.ensemble import Params, encode_tokens
+    from oracle.lm import LM
+    from oracle.ncw import Weights
+    from synth import ensure_model, make_text
+    path = ensure_model("smollm2-135m")
+    m = nc.Model(path, 0)
+    w = Weights(path)
+    C = L // 4
+    toks, _ = nc.nc_tokenize(m, make_text("alice", 12000, 1005), 1)
+    assert len(toks) >= L + 3 * C + 37
+    toks = [int(t) for t in toks[:L + 3 * C + 37]]          # three slides and a ragged tail
+    x = [w.bos] + toks[:-1]
+    prm = nc.nc_params_default(window=L, slide=C, cdf_bits=bits)
+    z = nc.nc_debug_forward(m, x, prm, 0)
+    Z = LM(w).forward_blocked(x, L, C)
+    err = np.abs(z - Z).max() / np.abs(Z).max()
+    assert err < Z_TOL, err
+    _, freq, p_gpu = nc.nc_debug_walk(z, toks, prm)
+    ref = encode_tokens(z.astype(np.float64), toks, w.V, Params(window=L, slide=C, cdf_bits=bits))
+    rel = np.abs(p_gpu - np.array(ref["p_true"])) / np.array(ref["p_true"])
+    assert rel.max() < P_TOL, rel.max()
+    assert (freq >= 1).all()
+    m.close()
