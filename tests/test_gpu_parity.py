@@ -459,3 +459,22 @@ def test_config5_windows_full_model(nc, L, bits):
     assert rel.max() < P_TOL, rel.max()
     assert (freq >= 1).all()
     m.close()
+
+
+def test_enwik_shaped_roundtrip_size_and_p(nc, m2, w2):
+    """Config 4's input kind (MediaWiki XML with ~1-2 % non-ASCII UTF-8, which exercises the
+    byte-fallback tokens) on the 2-layer model, 3 chunks: GPU round trip, size within 0.5 %
+    of the oracle, p(t) within 1e-4 at every row."""
+    from oracle.ensemble import Params
+    from synth import make_text
+    data = make_text("enwik", 6000, 1004)
+    assert any(b >= 0x80 for b in data)
+    prm = nc.nc_params_default(window=512, slide=128, n_chunks=3)
+    blob = nc.nc_compress(m2, data, prm)
+    assert nc.nc_decompress(m2, blob, prm) == data
+    size, ps, xs, ts = _oracle_size_and_p(w2, data, Params(window=512, slide=128, n_chunks=3))
+    assert abs(len(blob) - size) <= 0.005 * size, (len(blob), size)
+    for x, t, p_ref in zip(xs, ts, ps):
+        z = nc.nc_debug_forward(m2, x, prm, 0)
+        _, _, p_gpu = nc.nc_debug_walk(z, t, prm)
+        assert (np.abs(p_gpu - p_ref) / p_ref).max() < P_TOL
