@@ -478,3 +478,25 @@ def test_enwik_shaped_roundtrip_size_and_p(nc, m2, w2):
         z = nc.nc_debug_forward(m2, x, prm, 0)
         _, _, p_gpu = nc.nc_debug_walk(z, t, prm)
         assert (np.abs(p_gpu - p_ref) / p_ref).max() < P_TOL
+
+
+@pytest.mark.parametrize("V,n,over", [(49152, 400, {"temperature": 0.7}), (49152, 400, {"temperature": 1.3}),
+                                      (8192, 600, {"eta": 0.1}), (8192, 600, {"alpha": 5e-3}),
+                                      (256, 1500, {"ngram_orders": 3}),      # SPEC's reading of D18
+                                      (256, 1500, {"ngram_cap": 16}),        # capacity freeze, D22
+                                      (16, 800, {"ngram_orders": 1, "eta": 0.5})])
+def test_walk_parity_param_variants(nc, V, n, over):
+    """The walk under the non-default parameters nc_params carries (temperature D29, mixer
+    rate eta D24, head rate alpha, number of N-gram context tables D18, table capacity D22):
+    p(t) within 1e-4 of the oracle walk on the same fp32 logits, counts valid."""
+    from oracle.ensemble import Params, encode_tokens
+    rng = np.random.default_rng(V + n + len(over))
+    Z = (rng.standard_normal((n, V)) * (1.0 + rng.random((n, 1)) * 2)).astype(np.float32)
+    toks = _markov_tokens(V, n, V + 1)
+    prm = nc.nc_params_default(warmup=50, **over)
+    cum, freq, p_gpu = nc.nc_debug_walk(Z, toks, prm)
+    ref = encode_tokens(Z.astype(np.float64), toks, V, Params(warmup=50, **over))
+    p_ref = np.array(ref["p_true"])
+    rel = np.abs(p_gpu - p_ref) / p_ref
+    assert rel.max() < P_TOL, rel.max()
+    assert (freq >= 1).all() and (cum.astype(np.int64) + freq <= (1 << 24)).all()
