@@ -500,3 +500,29 @@ def test_walk_parity_param_variants(nc, V, n, over):
     rel = np.abs(p_gpu - p_ref) / p_ref
     assert rel.max() < P_TOL, rel.max()
     assert (freq >= 1).all() and (cum.astype(np.int64) + freq <= (1 << 24)).all()
+
+
+def test_many_chunks_roundtrip(nc, m2):
+    """300 chunks in one call (chunk_count > 255 in the u16 header field; walk clusters in
+    several waves; ~30-token chunks, most shorter than the warmup): round trip, and chunks
+    0 / 150 / 299 carry the same stream as when compressed alone."""
+    import struct
+    from synth import make_text
+    data = make_text("alice", 45000, 55)
+    prm = nc.nc_params_default(window=256, slide=128, n_chunks=300)
+    blob = nc.nc_compress(m2, data, prm)
+    assert nc.nc_decompress(m2, blob, prm) == data
+    n = struct.unpack_from("<BHH", blob, 4)[2]
+    cuts = nc.nc_host_split(data, 300)
+    assert n == len(cuts) - 1 == 300
+    table = [struct.unpack_from("<III", blob, 9 + 12 * c) for c in range(n)]
+    offs = [9 + 12 * n]
+    for t in table:
+        offs.append(offs[-1] + t[2])
+    assert offs[-1] == len(blob)
+    prm1 = nc.nc_params_default(window=256, slide=128, n_chunks=1)
+    for c in (0, 150, n - 1):
+        one = nc.nc_compress(m2, data[cuts[c]:cuts[c + 1]], prm1)
+        t1 = struct.unpack_from("<III", one, 9)
+        assert t1 == table[c], (c, t1, table[c])
+        assert one[21:21 + t1[2]] == blob[offs[c]:offs[c + 1]], c
