@@ -526,3 +526,23 @@ def test_many_chunks_roundtrip(nc, m2):
         t1 = struct.unpack_from("<III", one, 9)
         assert t1 == table[c], (c, t1, table[c])
         assert one[21:21 + t1[2]] == blob[offs[c]:offs[c + 1]], c
+
+
+def test_compress_tokens_equals_compress(nc, m2):
+    """The entry point bench.py times as `value` (nc_compress_tokens: token ids already in
+    HBM) produces the same container as the public nc_compress on host bytes (`e2e`)."""
+    from synth import make_text
+    data = make_text("alice", 20000, 66)
+    prm = nc.nc_params_default(window=256, slide=128, n_chunks=5)
+    blob = nc.nc_compress(m2, data, prm)
+    cuts = nc.nc_host_split(data, 5)
+    toks, ntok = [], []
+    for c in range(len(cuts) - 1):
+        t, _ = nc.nc_tokenize(m2, data[cuts[c]:cuts[c + 1]], 1)
+        toks.append(t)
+        ntok.append(len(t))
+    td = torch.from_numpy(np.concatenate(toks).view(np.int32).copy()).cuda()
+    s = torch.cuda.current_stream()
+    blob2 = nc.nc_compress_tokens(m2, td.data_ptr(), np.array(ntok, np.uint32), prm, s.cuda_stream)
+    torch.cuda.synchronize()
+    assert blob2 == blob
