@@ -16,8 +16,11 @@
  *     buffer is returned (the out pointers are set to NULL / 0).
  *   - Errors: every call returns nc_status; nc_last_error() returns a
  *     thread-local message describing the last non-OK status of this thread.
- *   - Device memory comes from the allocator hook (nc_set_allocator), by
- *     default cudaMallocAsync/cudaFreeAsync on the call's stream.
+ *   - Device memory comes from the allocator hook (nc_set_allocator) when one
+ *     is set.  The default is the library's own pool over cudaMalloc: blocks are
+ *     cached per (device, size) after a call returns and reused by later calls
+ *     (a block may be up to twice the requested size); the pool grows and never
+ *     returns memory to the driver while the process runs.
  *   - A model is bound to one CUDA device and is not safe for concurrent calls;
  *     use one model per GPU and one process per GPU for multi-GPU runs.
  *   - There is no CPU fallback: without a usable CUDA device every compute
@@ -180,6 +183,25 @@ nc_status nc_debug_quantize(const float *p, uint32_t V, uint32_t cdf_bits, uint3
 nc_status nc_debug_walk(int device, const float *logits, const uint32_t *tok, uint32_t n_tok,
                         uint32_t V, const nc_params *p, uint32_t *cum, uint32_t *freq,
                         float *p_true);
+
+/* nc_debug_walk plus the walk's internals, for the parity tests of SURVEY §8(d)
+ * ("probability-parity sampling"):
+ *   pt_true[n_tok] (host): p~(t_j), the bias-head softmax of the true token BEFORE the
+ *     N-gram mix, for every row;
+ *   rows[n_rows] (host, strictly ascending, each < n_tok): rows whose full vectors are
+ *     dumped; for the k-th of them, at offset k*V of each (host) array:
+ *       pt_rows = p~ (fp32), p_rows = the quantized distribution p (fp32, mixed after the
+ *       warmup), counts_rows = the walk's integer counts c (after the
+ *       residual is added to the argmax, D4-D6) -- what the coder used for that row.
+ * n_rows = 0 dumps nothing (rows / pt_rows / p_rows / counts_rows may then be NULL).
+ * n_logit_rows: logits holds n_logit_rows x V floats and token j uses row j % n_logit_rows
+ *   (long sequential walks without an n_tok x V array); 0 = n_tok rows.
+ * Errors: NC_ERR_INVALID on null or unsorted arguments; NC_ERR_INTEGRITY as nc_debug_walk. */
+nc_status nc_debug_walk_dump(int device, const float *logits, uint32_t n_logit_rows, const uint32_t *tok,
+                             uint32_t n_tok, uint32_t V,
+                             const nc_params *p, uint32_t *cum, uint32_t *freq, float *p_true, float *pt_true,
+                             const uint32_t *rows, uint32_t n_rows, float *pt_rows, float *p_rows,
+                             uint32_t *counts_rows);
 
 /* Forward only: logits (host, rows x V fp32) of ONE chunk for LM input ids x
  * (host, x[0] = BOS), window from params.  mode 0 = prefill kernels (slabbed),

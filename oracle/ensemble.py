@@ -131,13 +131,15 @@ class ChunkModel:
 def encode_tokens(Z, toks, V, prm: Params, keep_rows=()):
     """Walk one chunk given its logits rows Z[j] (row j predicts toks[j]).
 
-    Returns dict(stream, bits, cum, freq, p_true, pt_true, rows={j: p}) ."""
+    Returns dict(stream, bits, cum, freq, p_true, pt_true, rows={j: (p, pt)}, w_llm) -- w_llm[j] is
+    the mixer's LLM weight used for row j (None where no mix happens)."""
     cm = ChunkModel(V, prm)
     enc = Encoder()
-    cum, freq, p_true, pt_true, rows, skipped, h_ng = [], [], [], [], {}, [], []
+    cum, freq, p_true, pt_true, rows, skipped, h_ng, w_llm = [], [], [], [], {}, [], [], []
     keep = set(keep_rows)
     for j, t in enumerate(toks):
         p, pt, png = cm.distribution(Z[j])
+        w_llm.append(float(np.exp(cm.lw[0] - logsumexp(cm.lw))) if png is not None else None)
         skipped.append(cm.last_skipped)
         h_ng.append(entropy_bits_fp64(png) if (png is not None and cm.use_skip) else None)
         c = quantize(p, prm.T)
@@ -152,7 +154,8 @@ def encode_tokens(Z, toks, V, prm: Params, keep_rows=()):
         cm.update(t, pt, png)
     stream, bits = enc.finish()
     return dict(stream=stream, bits=bits, cum=cum, freq=freq, p_true=p_true,
-                pt_true=pt_true, rows=rows, min_range=enc.min_range, skipped=skipped, h_ng=h_ng)
+                pt_true=pt_true, rows=rows, min_range=enc.min_range, skipped=skipped, h_ng=h_ng,
+                w_llm=w_llm)
 
 
 def decode_tokens(step, n, stream, V, prm: Params):

@@ -3,7 +3,9 @@
 The paper tokenizes with SmolLM2's HF BPE, unavailable offline.  Our
 reading: greedy longest match over the model vocabulary, specials (ids <
 n_special) never matched; every byte is a token, so tokenize is total and
-detokenize(tokenize(x)) == x (the round-trip contract).
+detokenize(tokenize(x)) == x (the round-trip contract).  A string present under
+several ids maps to the LOWEST id (D30; pinned by
+test_tokenizer_duplicate_string_lowest_id_wins).
 """
 
 
@@ -13,7 +15,7 @@ class Tokenizer:
         self.n_special = n_special
         self.lookup = {}
         for i, s in enumerate(self.vocab):
-            if i >= n_special and s not in self.lookup:   # first id wins
+            if i >= n_special and s not in self.lookup:   # lowest id wins (D30)
                 self.lookup[s] = i
         self.max_len = max(len(s) for s in self.vocab[n_special:])
 

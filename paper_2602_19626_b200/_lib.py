@@ -19,7 +19,7 @@ EXPORTS = [
     "nc_params_default", "nc_set_allocator", "nc_model_load", "nc_model_free", "nc_model_info",
     "nc_compress", "nc_decompress", "nc_tokenize", "nc_compress_tokens", "nc_comm_unique_id",
     "nc_comm_init", "nc_comm_free", "nc_compress_shard", "nc_decompress_shard", "nc_free",
-    "nc_last_error", "nc_last_stats", "nc_debug_quantize", "nc_debug_walk", "nc_debug_forward",
+    "nc_last_error", "nc_last_stats", "nc_debug_quantize", "nc_debug_walk", "nc_debug_walk_dump", "nc_debug_forward",
     "nc_host_split", "nc_host_wnc_encode", "nc_host_tokenize_vocab", "nc_host_shard_range", "nc_host_walk_ctas",
     "nc_host_shard_part", "nc_set_profiling", "nc_profile", "nc_debug_set_splitk", "nc_debug_gemm", "nc_debug_attention",
 ]
@@ -75,6 +75,8 @@ def lib():
             "nc_debug_quantize": (C.c_int, [f32p, C.c_uint32, C.c_uint32, u32p]),
             "nc_debug_walk": (C.c_int, [C.c_int, f32p, u32p, C.c_uint32, C.c_uint32, C.POINTER(nc_params),
                                         u32p, u32p, f32p]),
+            "nc_debug_walk_dump": (C.c_int, [C.c_int, f32p, C.c_uint32, u32p, C.c_uint32, C.c_uint32, C.POINTER(nc_params),
+                                             u32p, u32p, f32p, f32p, u32p, C.c_uint32, f32p, f32p, u32p]),
             "nc_debug_forward": (C.c_int, [P, u32p, C.c_uint32, C.POINTER(nc_params), C.c_int, f32p]),
             "nc_debug_attention": (C.c_int, [C.c_int, f32p, f32p, f32p, C.c_uint32, C.c_uint32, C.c_uint32,
                                              C.c_uint32, C.c_uint32, C.c_int, f32p]),
@@ -228,6 +230,31 @@ def nc_debug_walk(logits, tok, params: nc_params, device=0):
     _check(lib().nc_debug_walk(device, lp, tp, n, V, C.byref(params), cum.ctypes.data_as(C.POINTER(C.c_uint32)),
                                freq.ctypes.data_as(C.POINTER(C.c_uint32)), pt.ctypes.data_as(C.POINTER(C.c_float))))
     return cum, freq, pt
+
+
+def nc_debug_walk_dump(logits, tok, params: nc_params, rows=(), device=0):
+    """nc_debug_walk + p~(t) of every row + full (p~, p, counts) vectors of `rows`.
+    len(logits) < len(tok): token j uses logits[j % len(logits)] (cyclic rows).
+
+    Returns dict(cum, freq, p_true, pt_true, rows, pt_rows [k,V], p_rows [k,V], c_rows [k,V])."""
+    lg, lp = _f32(logits)
+    n_lr, V = lg.shape
+    tk, tp = _u32(tok)
+    n = len(tk)
+    if n_lr < n and n_lr == 0:
+        raise NcError(NC_ERR_INVALID, "no logits rows")
+    rv, rp = _u32(sorted(set(int(r) for r in rows)))
+    k = len(rv)
+    cum, freq = np.zeros(n, np.uint32), np.zeros(n, np.uint32)
+    p_true, pt_true = np.zeros(n, np.float32), np.zeros(n, np.float32)
+    pt_rows, p_rows = np.zeros((k, V), np.float32), np.zeros((k, V), np.float32)
+    c_rows = np.zeros((k, V), np.uint32)
+    u32 = lambda a: a.ctypes.data_as(C.POINTER(C.c_uint32))
+    f32 = lambda a: a.ctypes.data_as(C.POINTER(C.c_float))
+    _check(lib().nc_debug_walk_dump(device, lp, min(n_lr, n), tp, n, V, C.byref(params), u32(cum), u32(freq), f32(p_true),
+                                    f32(pt_true), rp, k, f32(pt_rows), f32(p_rows), u32(c_rows)))
+    return dict(cum=cum, freq=freq, p_true=p_true, pt_true=pt_true, rows=rv.tolist(), pt_rows=pt_rows,
+                p_rows=p_rows, c_rows=c_rows)
 
 
 def nc_debug_forward(model: Model, x, params: nc_params, mode: int = 0):

@@ -16,7 +16,7 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", 
          "--expt-relaxed-constexpr", f"-I{PKG.parent / 'include'}"]
 # diagnostics builds only (e.g. NC_NVCC_EXTRA=-DNC_ATT_TIMING); a change of flags rebuilds everything
 EXTRA = os.environ.get("NC_NVCC_EXTRA", "").split()
-SOURCES = ["host_runtime.cpp", "api.cpp", "comm.cpp", "engine.cu", "k_forward_simt.cu", "k_walk.cu",
+SOURCES = ["host_runtime.cpp", "api.cpp", "comm.cpp", "engine.cu", "k_embed_rms.cu", "k_walk.cu",
            "k_gemm_tc.cu", "k_attn_tc.cu"]
 
 

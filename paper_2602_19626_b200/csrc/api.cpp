@@ -169,6 +169,9 @@ nc_status nc_compress_tokens(nc_model *m, const uint32_t *tokens_dev, const uint
     require_device();
     nc::Params q = nc::validate(p);
     std::vector<uint32_t> ntok(chunk_ntok, chunk_ntok + n_chunks);
+    size_t total = 0;
+    for (uint32_t c : ntok) total += c;
+    nc::check_tokens_device(m, tokens_dev, total, (cudaStream_t)cuda_stream);
     nc::CompressOut co;
     const auto t0 = std::chrono::steady_clock::now();
     nc::compress_device(m, tokens_dev, ntok, q, (cudaStream_t)cuda_stream, co);
@@ -300,7 +303,23 @@ nc_status nc_debug_walk(int device, const float *logits, const uint32_t *tok, ui
   return guard([&] {
     require_device();
     nc::Params q = nc::validate(p);
-    nc::debug_walk(device, logits, tok, n_tok, V, q, cum, freq, p_true);
+    nc::debug_walk(device, logits, 0, tok, n_tok, V, q, cum, freq, p_true);
+  });
+}
+
+nc_status nc_debug_walk_dump(int device, const float *logits, uint32_t n_logit_rows, const uint32_t *tok,
+                             uint32_t n_tok, uint32_t V,
+                             const nc_params *p, uint32_t *cum, uint32_t *freq, float *p_true, float *pt_true,
+                             const uint32_t *rows, uint32_t n_rows, float *pt_rows, float *p_rows,
+                             uint32_t *counts_rows) {
+  if ((!logits || !tok || !cum || !freq || !p_true || !pt_true) && n_tok) return set_err(NC_ERR_INVALID, "null argument");
+  if (n_rows && (!rows || !pt_rows || !p_rows || !counts_rows)) return set_err(NC_ERR_INVALID, "null dump argument");
+  return guard([&] {
+    require_device();
+    nc::Params q = nc::validate(p);
+    nc::debug_walk(device, logits, n_logit_rows, tok, n_tok, V, q, cum, freq, p_true, pt_true, rows, n_rows, pt_rows,
+                   p_rows,
+                   counts_rows);
   });
 }
 

@@ -100,6 +100,7 @@ void shard_part(const uint32_t *table, uint32_t n, uint8_t flags, uint16_t tau_m
     else if (c < c1) mine += table[3 * c + 2];
   }
   if (mine != my_len) fail(NC_ERR_INTEGRITY, "own stream bytes do not match the gathered table");
+  if (n > 0xFFFFu) fail(NC_ERR_INVALID, "too many chunks for NC05 (u16 chunk_count)");
   const uint64_t hdr = 9 + 12ull * n;
   total_n = hdr + all;
   part.clear();
@@ -179,6 +180,7 @@ nc_status nc_compress_shard(nc_model *m, nc_comm *c, const uint8_t *in, size_t n
     cudaStream_t s = (cudaStream_t)cuda_stream;
     NC_CUDA(cudaSetDevice(m->device));
     const uint32_t want = q.n_chunks ? q.n_chunks : (uint32_t)c->world * q.chunks_per_gpu;
+    if (want > 0xFFFFu) nc::fail(NC_ERR_INVALID, "too many chunks for NC05 (u16 chunk_count)");
     std::vector<uint64_t> cuts = nc::split_chunks(in, n, want);
     const uint32_t nch = (uint32_t)cuts.size() - 1;
     uint32_t c0, c1;

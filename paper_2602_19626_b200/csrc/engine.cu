@@ -18,6 +18,10 @@ namespace nc {
 void check_cuda(cudaError_t e, const char *what) {
   if (e != cudaSuccess) fail(NC_ERR_BACKEND, std::string(what) + ": " + cudaGetErrorString(e));
 }
+void throw_launch_error(cudaError_t e, const char *what) {
+  cudaGetLastError();   // clear the sticky-free launch error
+  fail(NC_ERR_BACKEND, std::string(what) + ": " + cudaGetErrorString(e));
+}
 
 // ------------------------------------------------------------- allocator ---
 static void *(*g_alloc)(size_t, void *) = nullptr;
@@ -31,10 +35,10 @@ void set_allocator(void *(*a)(size_t, void *), void (*f)(void *, void *), void *
 // mapped or unmapped again (cudaMallocAsync with a zero release threshold
 // re-mapped GBs of slab buffers per call).  Blocks are returned after the
 // owning call has synchronised its stream.
-struct DevCache {
+struct DevCache {   // keyed by (device, size): a block is only reused on the device it lives on
   std::mutex mu;
-  std::multimap<size_t, void *> free_;
-  std::map<void *, size_t> size_;
+  std::multimap<std::pair<int, size_t>, void *> free_;
+  std::map<void *, std::pair<int, size_t>> size_;
 };
 static DevCache &cache() {
   static DevCache c;
@@ -51,10 +55,12 @@ void *dev_alloc(size_t bytes, cudaStream_t s) {
     return p;
   }
   DevCache &c = cache();
+  int dev = 0;
+  NC_CUDA(cudaGetDevice(&dev));
   {
     std::lock_guard<std::mutex> lk(c.mu);
-    auto it = c.free_.lower_bound(bytes);
-    if (it != c.free_.end() && it->first <= 2 * bytes) {
+    auto it = c.free_.lower_bound({dev, bytes});
+    if (it != c.free_.end() && it->first.first == dev && it->first.second <= 2 * bytes) {
       p = it->second;
       c.free_.erase(it);
       return p;
@@ -63,15 +69,18 @@ void *dev_alloc(size_t bytes, cudaStream_t s) {
   cudaError_t e = cudaMalloc(&p, bytes);
   if (e != cudaSuccess) {
     cudaGetLastError();
-    // release cached blocks and retry once
+    // release this device's cached blocks and retry once
     std::lock_guard<std::mutex> lk(c.mu);
-    for (auto &kv : c.free_) { cudaFree(kv.second); c.size_.erase(kv.second); }
-    c.free_.clear();
+    for (auto it = c.free_.lower_bound({dev, 0}); it != c.free_.end() && it->first.first == dev;) {
+      cudaFree(it->second);
+      c.size_.erase(it->second);
+      it = c.free_.erase(it);
+    }
     e = cudaMalloc(&p, bytes);
     if (e != cudaSuccess) fail(NC_ERR_NOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
   }
   std::lock_guard<std::mutex> lk(c.mu);
-  c.size_[p] = bytes;
+  c.size_[p] = {dev, bytes};
   return p;
 }
 void dev_free(void *p, cudaStream_t s) {
@@ -136,11 +145,15 @@ void Prof::reset() {
     prof().end(s);                    \
   } while (0)
 
-// RAII bag of device buffers for one call
+// RAII bag of device buffers for one call.  The buffers go back to the pool only after
+// every stream that may still use them (the call's stream plus any registered with
+// also()) has drained -- also on the error path.
 struct Bag {
   cudaStream_t s;
+  std::vector<cudaStream_t> extra;
   std::vector<void *> ptrs;
   explicit Bag(cudaStream_t st) : s(st) {}
+  void also(cudaStream_t x) { extra.push_back(x); }
   template <class T>
   T *get(size_t n) {
     T *p = static_cast<T *>(dev_alloc(n * sizeof(T), s));
@@ -155,10 +168,49 @@ struct Bag {
   }
   ~Bag() {
     cudaStreamSynchronize(s);
+    for (cudaStream_t x : extra) cudaStreamSynchronize(x);
     for (void *p : ptrs) dev_free(p, s);
     cudaStreamSynchronize(s);
   }
 };
+// RAII set of CUDA events (destroyed on every path)
+struct Events {
+  std::vector<cudaEvent_t> ev;
+  explicit Events(size_t n) : ev(n, nullptr) {
+    for (auto &e : ev) NC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDefault));
+  }
+  ~Events() {
+    for (auto &e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+  cudaEvent_t &operator[](size_t i) { return ev[i]; }
+};
+
+// ---------------------------------------------------------- token check ---
+__global__ void token_max_kernel(const uint32_t *t, size_t n, uint32_t *mx) {
+  uint32_t m = 0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    m = max(m, t[i]);
+  m = __reduce_max_sync(0xffffffffu, m);
+  if ((threadIdx.x & 31) == 0) atomicMax(mx, m);
+}
+void check_tokens_device(nc_model *m, const uint32_t *tokens_dev, size_t n, cudaStream_t s) {
+  if (n == 0) return;
+  NC_CUDA(cudaSetDevice(m->device));
+  uint32_t *mx = static_cast<uint32_t *>(dev_alloc(4, s));
+  uint32_t h = 0;
+  cudaError_t e = cudaMemsetAsync(mx, 0, 4, s);
+  if (e == cudaSuccess) {
+    token_max_kernel<<<(unsigned)std::min<size_t>((n + 255) / 256, 1184), 256, 0, s>>>(tokens_dev, n, mx);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&h, mx, 4, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  dev_free(mx, s);
+  NC_CUDA(e);
+  stats().launches++;
+  if (h >= m->s.V) fail(NC_ERR_INVALID, "token id " + std::to_string(h) + " >= vocabulary size");
+}
 
 // ------------------------------------------------------------------ model ---
 void model_load(nc_model *m, const std::string &path, int device) {
@@ -174,18 +226,40 @@ void model_load(nc_model *m, const std::string &path, int device) {
   m->vocab = f.vocab;
   m->tok.build(f.vocab, s.n_special);
   const size_t d = s.d, V = s.V, qd = (size_t)s.H * s.dh, kvd = (size_t)s.KV * s.dh, ff = s.d_ff;
-  auto up = [&](const std::vector<float> &h) {
+  // device memory of the model: through the allocator hook when one is set (nc_set_allocator),
+  // else cudaMalloc; released in model_free
+  auto alloc = [&](size_t bytes) {
     void *p = nullptr;
-    NC_CUDA(cudaMalloc(&p, h.size() * sizeof(float)));
-    NC_CUDA(cudaMemcpy(p, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice));
+    if (g_alloc) {
+      p = g_alloc(bytes, g_ctx);
+      if (!p) fail(NC_ERR_NOMEM, "device allocation failed (hook)");
+    } else {
+      NC_CUDA(cudaMalloc(&p, bytes));
+    }
     m->owned.push_back(p);
+    m->owned_hook.push_back(g_alloc != nullptr);
     return static_cast<float *>(p);
+  };
+  // fp32 staging buffer on the device: the tf32 planes are split from it, then it is reused
+  size_t stage_n = std::max<size_t>(V * d, 2 * ff * d);
+  float *stage = nullptr;
+  NC_CUDA(cudaMalloc(&stage, stage_n * sizeof(float)));
+  auto planes = [&](const std::vector<float> &h, float *&hi, float *&lo) {
+    NC_CUDA(cudaMemcpy(stage, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice));
+    hi = alloc(h.size() * 4);
+    lo = alloc(h.size() * 4);
+    launch_split_planes(stage, hi, lo, h.size(), nullptr);
+    NC_CUDA(cudaDeviceSynchronize());
   };
   size_t off = 0;
   const float *E = f.tensor(0);
   off += V * d;
   std::vector<float> buf(E, E + V * d);
-  m->E = up(buf);
+  m->E = alloc(V * d * 4);
+  NC_CUDA(cudaMemcpy(m->E, buf.data(), V * d * 4, cudaMemcpyHostToDevice));
+  m->wqkv_hi.resize(s.n_layers); m->wqkv_lo.resize(s.n_layers); m->wo_hi.resize(s.n_layers);
+  m->wo_lo.resize(s.n_layers); m->wgu_hi.resize(s.n_layers); m->wgu_lo.resize(s.n_layers);
+  m->wd_hi.resize(s.n_layers); m->wd_lo.resize(s.n_layers);
   for (uint32_t l = 0; l < s.n_layers; ++l) {
     const float *g1 = f.tensor(off); off += d;
     const float *wq = f.tensor(off); off += qd * d;
@@ -202,9 +276,9 @@ void model_load(nc_model *m, const std::string &path, int device) {
       const float *src = r < qd ? wq + r * d : (r < qd + kvd ? wk + (r - qd) * d : wv + (r - qd - kvd) * d);
       for (size_t k = 0; k < d; ++k) buf[r * d + k] = src[k] * g1[k];
     }
-    m->wqkv.push_back(up(buf));
+    planes(buf, m->wqkv_hi[l], m->wqkv_lo[l]);
     buf.assign(wo, wo + d * qd);
-    m->wo.push_back(up(buf));
+    planes(buf, m->wo_hi[l], m->wo_lo[l]);
     // gate/up interleaved in groups of 32 rows, MLP RMSNorm gain folded in
     buf.assign(2 * ff * d, 0.f);
     for (size_t gi = 0; gi < ff / 32; ++gi)
@@ -213,38 +287,16 @@ void model_load(nc_model *m, const std::string &path, int device) {
           buf[(64 * gi + j) * d + k] = wg[(32 * gi + j) * d + k] * g2[k];
           buf[(64 * gi + 32 + j) * d + k] = wu[(32 * gi + j) * d + k] * g2[k];
         }
-    m->wgu.push_back(up(buf));
+    planes(buf, m->wgu_hi[l], m->wgu_lo[l]);
     buf.assign(wd, wd + d * ff);
-    m->wd.push_back(up(buf));
+    planes(buf, m->wd_hi[l], m->wd_lo[l]);
   }
   const float *gf = f.tensor(off);
   buf.assign(V * d, 0.f);
   for (size_t v = 0; v < V; ++v)
     for (size_t k = 0; k < d; ++k) buf[v * d + k] = E[v * d + k] * gf[k];
-  m->E_head = up(buf);
-  // tf32 planes for the tensor-core path (split on device: same code as the activations)
-  auto planes = [&](const float *src, size_t n, float *&hi, float *&lo) {
-    NC_CUDA(cudaMalloc(&hi, n * 4));
-    NC_CUDA(cudaMalloc(&lo, n * 4));
-    m->owned.push_back(hi);
-    m->owned.push_back(lo);
-    launch_split_planes(src, hi, lo, n, nullptr);
-  };
-  planes(m->E_head, V * d, m->E_head_hi, m->E_head_lo);
-  m->wqkv_hi.resize(s.n_layers); m->wqkv_lo.resize(s.n_layers); m->wo_hi.resize(s.n_layers);
-  m->wo_lo.resize(s.n_layers); m->wgu_hi.resize(s.n_layers); m->wgu_lo.resize(s.n_layers);
-  m->wd_hi.resize(s.n_layers); m->wd_lo.resize(s.n_layers);
-  for (uint32_t l = 0; l < s.n_layers; ++l) {
-    planes(m->wqkv[l], (qd + 2 * kvd) * d, m->wqkv_hi[l], m->wqkv_lo[l]);
-    planes(m->wo[l], d * qd, m->wo_hi[l], m->wo_lo[l]);
-    planes(m->wgu[l], 2 * ff * d, m->wgu_hi[l], m->wgu_lo[l]);
-    planes(m->wd[l], d * ff, m->wd_hi[l], m->wd_lo[l]);
-  }
-  NC_CUDA(cudaDeviceSynchronize());
-  const char *g = std::getenv("NC_GEMM");
-  m->use_tc = !(g && std::string(g) == "simt");
-  const char *ga = std::getenv("NC_ATTN");
-  m->use_tc_attn = m->use_tc && !(ga && std::string(ga) == "simt");
+  planes(buf, m->E_head_hi, m->E_head_lo);
+  cudaFree(stage);
   ensure_rope(m, 4096);
   int lo_prio = 0, hi_prio = 0;
   NC_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
@@ -255,7 +307,12 @@ void model_load(nc_model *m, const std::string &path, int device) {
 
 void model_free(nc_model *m) {
   cudaSetDevice(m->device);
-  for (void *p : m->owned) cudaFree(p);
+  cudaDeviceSynchronize();
+  for (size_t i = 0; i < m->owned.size(); ++i) {
+    if (i < m->owned_hook.size() && m->owned_hook[i] && g_free) g_free(m->owned[i], g_ctx);
+    else cudaFree(m->owned[i]);
+  }
+  m->owned_hook.clear();
   if (m->rope_cos) cudaFree(m->rope_cos);
   if (m->rope_sin) cudaFree(m->rope_sin);
   if (m->walk_stream) cudaStreamDestroy(m->walk_stream);
@@ -265,9 +322,10 @@ void model_free(nc_model *m) {
 }
 
 // cos/sin of pos * theta^(-2i/64) computed in fp64, stored fp32 (D12)
-void ensure_rope(nc_model *m, int max_pos) {
+void ensure_rope(nc_model *m, int64_t max_pos) {
   if (max_pos <= m->rope_len) return;
-  int len = ((max_pos + 4095) / 4096) * 4096;
+  if (max_pos > (int64_t)INT32_MAX - 4096) fail(NC_ERR_INVALID, "positions beyond the RoPE table range");
+  const int len = (int)(((max_pos + 4095) / 4096) * 4096);
   std::vector<float> c((size_t)len * 32), sn((size_t)len * 32);
   for (int p = 0; p < len; ++p)
     for (int i = 0; i < 32; ++i) {
@@ -291,7 +349,7 @@ struct Forward {
   nc_model *m;
   cudaStream_t s;
   int Mmax = 0;
-  float *h, *rinv, *q, *o, *act, *logits, *lbuf[2];
+  float *h, *rinv, *logits, *lbuf[2];
   float *h_hi, *h_lo, *o_hi, *o_lo, *act_hi, *act_lo;   // tf32 planes (tensor-core GEMM operands)
   float *q_hi = nullptr, *q_lo = nullptr;               // tf32 planes of q (tensor-core attention)
   int n_chunks_ = 0;
@@ -301,9 +359,6 @@ struct Forward {
     const Shape &S = m->s;
     h = bag.get<float>((size_t)Mmax * S.d);
     rinv = bag.get<float>((size_t)Mmax);
-    q = bag.get<float>((size_t)Mmax * S.H * S.dh);
-    o = bag.get<float>((size_t)Mmax * S.H * S.dh);
-    act = bag.get<float>((size_t)Mmax * S.d_ff);
     h_hi = bag.get<float>((size_t)Mmax * S.d);
     h_lo = bag.get<float>((size_t)Mmax * S.d);
     o_hi = bag.get<float>((size_t)Mmax * S.H * S.dh);
@@ -317,22 +372,15 @@ struct Forward {
     ring.kv = S.KV;
     size_t rn = (size_t)n_chunks * S.n_layers * ring_len * S.KV * S.dh;
     n_chunks_ = n_chunks;
-    if (m->use_tc_attn) {
-      q_hi = bag.get<float>((size_t)Mmax * S.H * S.dh);
-      q_lo = bag.get<float>((size_t)Mmax * S.H * S.dh);
-      ring.k = ring.v = nullptr;
-      ring.k_hi = bag.get<float>(rn); ring.k_lo = bag.get<float>(rn);
-      ring.v_hi = bag.get<float>(rn); ring.v_lo = bag.get<float>(rn);
-      // The PV MMA multiplies masked keys by P = 0; a ring slot not written yet
-      // (past the chunk end, or ahead of the decode position) must hold a finite
-      // value or 0 * NaN poisons the row.  Masked K slots never reach P.
-      NC_CUDA(cudaMemsetAsync(ring.v_hi, 0, rn * sizeof(float), s));
-      NC_CUDA(cudaMemsetAsync(ring.v_lo, 0, rn * sizeof(float), s));
-    } else {
-      ring.k = bag.get<float>(rn);
-      ring.v = bag.get<float>(rn);
-      ring.k_hi = ring.k_lo = ring.v_hi = ring.v_lo = nullptr;
-    }
+    q_hi = bag.get<float>((size_t)Mmax * S.H * S.dh);
+    q_lo = bag.get<float>((size_t)Mmax * S.H * S.dh);
+    ring.k_hi = bag.get<float>(rn); ring.k_lo = bag.get<float>(rn);
+    ring.v_hi = bag.get<float>(rn); ring.v_lo = bag.get<float>(rn);
+    // The PV MMA multiplies masked keys by P = 0; a ring slot not written yet
+    // (past the chunk end, or ahead of the decode position) must hold a finite
+    // value or 0 * NaN poisons the row.  Masked K slots never reach P.
+    NC_CUDA(cudaMemsetAsync(ring.v_hi, 0, rn * sizeof(float), s));
+    NC_CUDA(cudaMemsetAsync(ring.v_lo, 0, rn * sizeof(float), s));
   }
   // embed -> n_layers x {QKV, attention, O, gate-up, down} -> head into `logits`.
   // valid = rows that are real tokens (algorithmic work), attn_flops = sum over
@@ -343,28 +391,20 @@ struct Forward {
     Stats &st = stats();
     const int qd = S.H * S.dh, kvd = S.KV * S.dh;
     const double d = S.d;
-    const bool tcm = m->use_tc;
-    PROF(K_EMBED, 4.0 * d * valid, launch_embed(rows.x, M, m->E, S.d, h, tcm ? h_hi : nullptr, tcm ? h_lo : nullptr, s));
+    PROF(K_EMBED, 4.0 * d * valid, launch_embed(rows.x, M, m->E, S.d, h, h_hi, h_lo, s));
     st.launches++;
     for (uint32_t l = 0; l < S.n_layers; ++l) {
       PROF(K_RMS, 4.0 * d * valid, launch_rms(h, M, S.d, (float)S.eps, rinv, s));
-      // RMSNorm + QKV + RoPE + KV-ring scatter
-      if (tcm) {
+      {  // RMSNorm scale + QKV + RoPE + KV-ring scatter (q and K/V as tf32 planes)
         TcGemmArgs g{};
-        g.M = M; g.N = qd + 2 * kvd; g.K = S.d; g.rinv = rinv; g.C = q; g.ldc = qd;
+        g.M = M; g.N = qd + 2 * kvd; g.K = S.d; g.rinv = rinv; g.C = nullptr; g.ldc = qd;
         g.layer = (int)l; g.n_q_cols = qd; g.n_kv_cols = kvd; g.rows = rows; g.ring = ring;
         g.rope_cos = m->rope_cos; g.rope_sin = m->rope_sin;
-        g.planes = m->use_tc_attn ? 1 : 0; g.C_hi = q_hi; g.C_lo = q_lo;
+        g.C_hi = q_hi; g.C_lo = q_lo;
         TcOperands op{h_hi, h_lo, (uint64_t)Mmax, m->wqkv_hi[l], m->wqkv_lo[l]};
         PROF(K_QKV, 2.0 * valid * (qd + 2 * kvd) * d, launch_gemm_tc(EPI_QKV, g, op, s));
-      } else {
-        GemmArgs g{};
-        g.A = h; g.lda = S.d; g.B = m->wqkv[l]; g.ldb = S.d; g.M = M; g.N = qd + 2 * kvd; g.K = S.d;
-        g.rinv = rinv; g.C = q; g.ldc = qd; g.layer = (int)l; g.n_q_cols = qd; g.n_kv_cols = kvd;
-        g.rows = rows; g.ring = ring; g.rope_cos = m->rope_cos; g.rope_sin = m->rope_sin;
-        PROF(K_QKV, 2.0 * valid * (qd + 2 * kvd) * d, launch_gemm(EPI_QKV, g, s));
       }
-      if (m->use_tc_attn) {
+      {
         AttnTcArgs at{};
         at.tiles = tiles; at.n_tiles = n_tiles; at.q_hi = q_hi; at.q_lo = q_lo; at.ldq = qd; at.q_rows = Mmax;
         at.k_hi = ring.k_hi; at.k_lo = ring.k_lo; at.v_hi = ring.v_hi; at.v_lo = ring.v_lo;
@@ -372,25 +412,15 @@ struct Forward {
         at.o_hi = o_hi; at.o_lo = o_lo; at.ldo = qd;
         at.H = S.H; at.KV = S.KV; at.window = (int)p.window; at.slide = (int)p.slide;
         PROF(K_ATTN, attn_flops, launch_attention_tc(at, s));
-      } else {
-        AttnArgs at{};
-        at.tiles = tiles; at.n_tiles = n_tiles; at.q = q; at.o = o; at.ldq = qd; at.ring = ring; at.layer = (int)l;
-        at.H = S.H; at.KV = S.KV; at.window = (int)p.window; at.slide = (int)p.slide;
-        at.o_hi = tcm ? o_hi : nullptr; at.o_lo = tcm ? o_lo : nullptr;
-        PROF(K_ATTN, attn_flops, launch_attention(at, s));
       }
-      if (tcm) {
+      {
         TcGemmArgs g{};
         g.M = M; g.N = S.d; g.K = qd; g.C = h; g.ldc = S.d; g.C_hi = h_hi; g.C_lo = h_lo;
         TcOperands op{o_hi, o_lo, (uint64_t)Mmax, m->wo_hi[l], m->wo_lo[l]};
         PROF(K_OPROJ, 2.0 * valid * d * qd, launch_gemm_tc(EPI_RESID, g, op, s));
-      } else {
-        GemmArgs go{};
-        go.A = o; go.lda = qd; go.B = m->wo[l]; go.ldb = qd; go.M = M; go.N = S.d; go.K = qd; go.C = h; go.ldc = S.d;
-        PROF(K_OPROJ, 2.0 * valid * d * qd, launch_gemm(EPI_RESID, go, s));
       }
       PROF(K_RMS, 4.0 * d * valid, launch_rms(h, M, S.d, (float)S.eps, rinv, s));
-      if (tcm) {
+      {
         TcGemmArgs g{};
         g.M = M; g.N = 2 * S.d_ff; g.K = S.d; g.rinv = rinv; g.C_hi = act_hi; g.C_lo = act_lo; g.ldc = S.d_ff;
         TcOperands op{h_hi, h_lo, (uint64_t)Mmax, m->wgu_hi[l], m->wgu_lo[l]};
@@ -399,30 +429,16 @@ struct Forward {
         g2.M = M; g2.N = S.d; g2.K = S.d_ff; g2.C = h; g2.ldc = S.d; g2.C_hi = h_hi; g2.C_lo = h_lo;
         TcOperands op2{act_hi, act_lo, (uint64_t)Mmax, m->wd_hi[l], m->wd_lo[l]};
         PROF(K_DOWN, 2.0 * valid * d * S.d_ff, launch_gemm_tc(EPI_RESID, g2, op2, s));
-      } else {
-        GemmArgs gu{};
-        gu.A = h; gu.lda = S.d; gu.B = m->wgu[l]; gu.ldb = S.d; gu.M = M; gu.N = 2 * S.d_ff; gu.K = S.d;
-        gu.rinv = rinv; gu.C = act; gu.ldc = S.d_ff;
-        PROF(K_GATEUP, 2.0 * valid * 2 * S.d_ff * d, launch_gemm(EPI_SWIGLU, gu, s));
-        GemmArgs gd{};
-        gd.A = act; gd.lda = S.d_ff; gd.B = m->wd[l]; gd.ldb = S.d_ff; gd.M = M; gd.N = S.d; gd.K = S.d_ff;
-        gd.C = h; gd.ldc = S.d;
-        PROF(K_DOWN, 2.0 * valid * d * S.d_ff, launch_gemm(EPI_RESID, gd, s));
       }
       st.launches += 7;   // 2 RMSNorm scales, QKV, attention, O, gate/up, down
     }
     if (ev_head) NC_CUDA(cudaEventRecord(ev_head, s));
     PROF(K_RMS, 4.0 * d * valid, launch_rms(h, M, S.d, (float)S.eps, rinv, s));
-    if (tcm) {
+    {
       TcGemmArgs g{};
       g.M = M; g.N = S.V; g.K = S.d; g.rinv = rinv; g.C = logits; g.ldc = S.V;
       TcOperands op{h_hi, h_lo, (uint64_t)Mmax, m->E_head_hi, m->E_head_lo};
       PROF(K_HEAD, 2.0 * valid * S.V * d, launch_gemm_tc(EPI_HEAD, g, op, s));
-    } else {
-      GemmArgs gh{};
-      gh.A = h; gh.lda = S.d; gh.B = m->E_head; gh.ldb = S.d; gh.M = M; gh.N = S.V; gh.K = S.d;
-      gh.rinv = rinv; gh.C = logits; gh.ldc = S.V;
-      PROF(K_HEAD, 2.0 * valid * S.V * d, launch_gemm(EPI_HEAD, gh, s));
     }
     st.launches += 2;
     NC_CUDA(cudaGetLastError());
@@ -612,9 +628,11 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
   const int n_slabs = (int)slab_len.size();
   const int ring_len = (int)p.window + R;
   const int M = n_chunks * R;   // buffer rows (the largest slab)
-  ensure_rope(m, (int)max_n + 1);
+  ensure_rope(m, (int64_t)max_n + 1);
 
   Bag bag(s);
+  bag.also(m->walk_stream);
+  bag.also(m->ng_stream);
   Forward fw{m, s};
   fw.alloc(bag, M, n_chunks, ring_len, n_slabs > 1);
   std::vector<uint32_t> ntok_v(ntok);
@@ -659,8 +677,7 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
   // streams: forward (s), N-gram precompute (ns, runs ahead; ring of 2 slabs), walk (ws)
   // events: per slab forward start/end, walk start/end, N-gram done
   cudaStream_t ws = m->walk_stream, ns = m->ng_stream;
-  std::vector<cudaEvent_t> ev(5 * n_slabs + 1);
-  for (auto &e : ev) NC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDefault));
+  Events ev(5 * n_slabs + 1);
   cudaEvent_t ev_init = ev[5 * n_slabs];
   NC_CUDA(cudaEventRecord(ev_init, s));
   const auto t_setup = std::chrono::steady_clock::now();
@@ -757,7 +774,6 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
               slab_len[sl], at(ev[4 * sl]), at(ev[4 * sl + 1]), use_ng ? at(ev[4 * n_slabs + sl]) : 0.f,
               at(ev[4 * sl + 2]), at(ev[4 * sl + 3]));
   }
-  for (auto &e : ev) cudaEventDestroy(e);
 }
 
 // --------------------------------------------------------------- container ---
@@ -841,8 +857,17 @@ void decompress_device(nc_model *m, const uint8_t *blob, const Nc05View &view, c
   }
   if (n_chunks == 0 || max_n == 0) return;
   if (S.V >= (1u << p.cdf_bits)) fail(NC_ERR_INVALID, "T = 2^cdf_bits must exceed V");
+  // a token costs at least -log2(1 - (V - 1)/T) bits (the largest count is T - (V - 1)), and
+  // the coder adds at most ~2 bits: reject token counts the stream cannot hold BEFORE
+  // sizing any buffer from them (a crafted header could ask for 2^32 tokens in 0 bits)
+  {
+    const double min_bits = -std::log2(1.0 - (double)(S.V - 1) / (double)(1ull << p.cdf_bits));
+    for (int c = 0; c < n_chunks; ++c)
+      if ((double)ntok[c] * min_bits > (double)s_bits[c] + 64.0)
+        fail(NC_ERR_INTEGRITY, "chunk " + std::to_string(c) + " claims more tokens than its bit_count can code");
+  }
   Stats &st = stats();
-  ensure_rope(m, (int)max_n + 1);
+  ensure_rope(m, (int64_t)max_n + 1);
   Bag bag(s);
   Forward fw{m, s};
   const int ring_len = (int)p.window + 128;   // 128-key attention blocks never wrap
@@ -935,6 +960,20 @@ void decompress_device(nc_model *m, const uint8_t *blob, const Nc05View &view, c
     // bit_count = steps + 2 (finish emits 1 + (pending+1) bits)  (D8)
     if (ntok[c] && hs[c].bitpos - 32 + 2 != s_bits[c])
       fail(NC_ERR_INTEGRITY, "bit_count mismatch in chunk " + std::to_string(c) + " (wrong params or corrupt stream)");
+    // and the stream must END exactly as the encoder's finish() leaves it from the decoder's
+    // final state: bit b = [low >= QUARTER], then (pending + 1) copies of !b, then zero padding
+    // (D8; "tampering ... never silent partial corruption past the integrity checks")
+    if (ntok[c]) {
+      const uint8_t *sp = blob + s_off[c];
+      const uint64_t steps = hs[c].bitpos - 32, pend = hs[c].pend;
+      auto bit_at = [&](uint64_t k) { return (uint32_t)(sp[k >> 3] >> (7 - (k & 7))) & 1u; };
+      const uint32_t b = hs[c].low < (1ull << 30) ? 0u : 1u;
+      bool ok = pend <= steps;
+      for (uint64_t k = steps - std::min<uint64_t>(pend, steps); ok && k < steps + 2; ++k)
+        ok = bit_at(k) == (k == steps - pend ? b : (b ^ 1u));
+      for (uint64_t k = steps + 2; ok && k < (uint64_t)view.ents[c].len * 8; ++k) ok = bit_at(k) == 0u;
+      if (!ok) fail(NC_ERR_INTEGRITY, "stream tail of chunk " + std::to_string(c) + " is not the coder's finish (corrupt stream)");
+    }
     toks[c].assign(all.begin() + tok_off[c], all.begin() + tok_off[c] + ntok[c]);
   }
 }
@@ -945,7 +984,7 @@ void debug_forward(nc_model *m, const uint32_t *x, uint32_t rows, const Params &
   const Shape &S = m->s;
   cudaStream_t s = nullptr;
   if (rows == 0) return;
-  ensure_rope(m, (int)rows + 1);
+  ensure_rope(m, (int64_t)rows + 1);
   Bag bag(s);
   std::vector<uint32_t> xv(x, x + rows);
   uint32_t *x_d = bag.upload(xv);
@@ -1001,6 +1040,7 @@ void debug_gemm(int device, const float *A, const float *B, uint32_t M, uint32_t
                 float *out) {
   NC_CUDA(cudaSetDevice(device));
   if (K % 32 || N % 64) fail(NC_ERR_INVALID, "debug_gemm needs K % 32 == 0 and N % 64 == 0");
+  if (mode != 0) fail(NC_ERR_INVALID, "debug_gemm: mode 0 (tcgen05 3xTF32) is the only GEMM");
   cudaStream_t s = nullptr;
   Bag bag(s);
   std::vector<float> a(A, A + (size_t)M * K), b(B, B + (size_t)N * K), ones(M, 1.f);
@@ -1046,11 +1086,6 @@ void debug_gemm(int device, const float *A, const float *B, uint32_t M, uint32_t
               K, resid ? "resid" : "head", t.no_store, us, 2.0 * M * N * K / (us * 1e-6) / 1e12);
       gemm_timing_report();
     }
-  } else {
-    GemmArgs g{};
-    g.A = a_d; g.lda = (int)K; g.B = b_d; g.ldb = (int)K; g.M = (int)M; g.N = (int)N; g.K = (int)K;
-    g.rinv = r_d; g.C = c_d; g.ldc = (int)N;
-    launch_gemm(EPI_HEAD, g, s);
   }
   NC_CUDA(cudaGetLastError());
   NC_CUDA(cudaMemcpyAsync(out, c_d, (size_t)M * N * 4, cudaMemcpyDeviceToHost, s));
@@ -1060,6 +1095,7 @@ void debug_gemm(int device, const float *A, const float *B, uint32_t M, uint32_t
 void debug_attention(int device, const float *q, const float *k, const float *v, uint32_t n, uint32_t H, uint32_t KV,
                      uint32_t window, uint32_t slide, int mode, float *o) {
   NC_CUDA(cudaSetDevice(device));
+  if (mode != 0) fail(NC_ERR_INVALID, "debug_attention: mode 0 (tcgen05 3xTF32) is the only attention");
   if (!n) return;
   cudaStream_t s = nullptr;
   Bag bag(s);
@@ -1072,9 +1108,8 @@ void debug_attention(int device, const float *q, const float *k, const float *v,
   std::copy(kv.begin(), kv.end(), kpad.begin());
   std::copy(vv.begin(), vv.end(), vpad.begin());
   float *q_d = bag.upload(qpad), *k_d = bag.upload(kpad), *v_d = bag.upload(vpad);
-  float *o_d = bag.get<float>((size_t)rows * qd);
   float *oh = bag.get<float>((size_t)rows * qd), *ol = bag.get<float>((size_t)rows * qd);
-  const int TR = mode == 0 ? 128 : 64;
+  const int TR = 128;
   std::vector<AttnTile> tiles;
   for (uint32_t p0 = 0; p0 < n; p0 += TR) tiles.push_back(AttnTile{0, (int)p0, (int)std::min<uint32_t>(TR, n - p0), (int)p0});
   AttnTile *t_d = bag.upload(tiles);
@@ -1109,50 +1144,68 @@ void debug_attention(int device, const float *q, const float *k, const float *v,
     NC_CUDA(cudaMemcpyAsync(b.data(), ol, b.size() * 4, cudaMemcpyDeviceToHost, s));
     NC_CUDA(cudaStreamSynchronize(s));
     for (size_t i = 0; i < n * qd; ++i) o[i] = a[i] + b[i];
-  } else {
-    AttnArgs at{};
-    KvRing rg{};
-    rg.k = k_d; rg.v = v_d; rg.n_layers = 1; rg.ring = ring; rg.kv = (int)KV;
-    at.tiles = t_d; at.n_tiles = (int)tiles.size(); at.q = q_d; at.o = o_d; at.ldq = (int)qd; at.ring = rg;
-    at.layer = 0; at.H = (int)H; at.KV = (int)KV; at.window = (int)window; at.slide = (int)slide;
-    launch_attention(at, s);
-    NC_CUDA(cudaMemcpyAsync(o, o_d, n * qd * 4, cudaMemcpyDeviceToHost, s));
-    NC_CUDA(cudaStreamSynchronize(s));
   }
   NC_CUDA(cudaGetLastError());
 }
 
-void debug_walk(int device, const float *logits, const uint32_t *tok, uint32_t n, uint32_t V, const Params &p,
-                uint32_t *cum, uint32_t *freq, float *p_true) {
+void debug_walk(int device, const float *logits, uint32_t n_lrows, const uint32_t *tok, uint32_t n, uint32_t V,
+                const Params &p, uint32_t *cum, uint32_t *freq, float *p_true, float *pt_true, const uint32_t *rows,
+                uint32_t n_rows, float *pt_rows, float *p_rows, uint32_t *c_rows) {
   NC_CUDA(cudaSetDevice(device));
   if (n == 0) return;
   if (V >= (1u << p.cdf_bits)) fail(NC_ERR_INVALID, "T = 2^cdf_bits must exceed V");
+  for (uint32_t k = 0; k < n_rows; ++k)
+    if (rows[k] >= n || (k && rows[k] <= rows[k - 1])) fail(NC_ERR_INVALID, "dump rows must be ascending and < n_tok");
+  const uint32_t R = (n_lrows == 0 || n_lrows > n) ? n : n_lrows;   // token j uses logits row j % R
   cudaStream_t s = nullptr;
   Bag bag(s);
-  std::vector<float> lg(logits, logits + (size_t)n * V);
+  std::vector<float> lg(logits, logits + (size_t)R * V);
   float *lg_d = bag.upload(lg);
   std::vector<uint32_t> tk(tok, tok + n);
   uint32_t *tk_d = bag.upload(tk);
   std::vector<int64_t> off{0};
   int64_t *off_d = bag.upload(off);
-  std::vector<int32_t> zero{0}, cnt{(int32_t)n};
-  int32_t *c_d = bag.upload(zero), *r_d = bag.upload(zero), *n_d = bag.upload(cnt);
+  std::vector<int32_t> zero{0};
+  int32_t *c_d = bag.upload(zero), *r_d = bag.upload(zero);
   WalkBufs wb;
-  wb.alloc(bag, 1, V, n, p, s, n);
+  wb.alloc(bag, 1, V, n, p, s, R);
   uint32_t *cum_d = bag.get<uint32_t>(n), *freq_d = bag.get<uint32_t>(n);
-  float *p_d = bag.get<float>(n);
+  float *p_d = bag.get<float>(n), *pt_d = bag.get<float>(n);
   WalkArgs wa{};
-  wa.chunk_of = c_d; wa.row0 = r_d; wa.count = n_d; wa.n_entries = 1;
+  wa.chunk_of = c_d; wa.row0 = r_d; wa.n_entries = 1;
   wa.logits = lg_d; wa.ldl = V; wa.tokens = tk_d; wa.tok_off = off_d;
-  wa.out_cum = cum_d; wa.out_freq = freq_d; wa.out_p = p_d; wa.mode = 0;
+  wa.out_cum = cum_d; wa.out_freq = freq_d; wa.out_p = p_d; wa.out_pt = pt_d; wa.mode = 0;
   wa.n_chunks_total = 1;
+  const size_t dn = (size_t)n_rows * V;
+  if (n_rows) {
+    std::vector<uint32_t> rv(rows, rows + n_rows);
+    wa.dump_rows = bag.upload(rv);
+    wa.n_dump = n_rows;
+    wa.dump_chunk = 0;
+    wa.dump_pt = bag.get<float>(dn);
+    wa.dump_p = bag.get<float>(dn);
+    wa.dump_c = bag.get<uint32_t>(dn);
+  }
   wb.fill(wa, p, V);
-  if (p.flags & 1u) launch_ngram_precompute(wa, s);
-  launch_walk(wa, s);
-  NC_CUDA(cudaGetLastError());
+  // segments of R tokens over the same R logits rows (the walk state carries over, as between slabs)
+  std::vector<int32_t> cnts;
+  for (uint32_t j0 = 0; j0 < n; j0 += R) cnts.push_back((int32_t)std::min(R, n - j0));
+  int32_t *n_d = bag.upload(cnts);
+  for (size_t k = 0; k < cnts.size(); ++k) {
+    wa.count = n_d + k;
+    if (p.flags & 1u) launch_ngram_precompute(wa, s);
+    launch_walk(wa, s);
+    NC_CUDA(cudaGetLastError());
+  }
   NC_CUDA(cudaMemcpyAsync(cum, cum_d, n * 4, cudaMemcpyDeviceToHost, s));
   NC_CUDA(cudaMemcpyAsync(freq, freq_d, n * 4, cudaMemcpyDeviceToHost, s));
   NC_CUDA(cudaMemcpyAsync(p_true, p_d, n * 4, cudaMemcpyDeviceToHost, s));
+  if (pt_true) NC_CUDA(cudaMemcpyAsync(pt_true, pt_d, n * 4, cudaMemcpyDeviceToHost, s));
+  if (n_rows) {
+    if (pt_rows) NC_CUDA(cudaMemcpyAsync(pt_rows, wa.dump_pt, dn * 4, cudaMemcpyDeviceToHost, s));
+    if (p_rows) NC_CUDA(cudaMemcpyAsync(p_rows, wa.dump_p, dn * 4, cudaMemcpyDeviceToHost, s));
+    if (c_rows) NC_CUDA(cudaMemcpyAsync(c_rows, wa.dump_c, dn * 4, cudaMemcpyDeviceToHost, s));
+  }
   WalkState hs;
   NC_CUDA(cudaMemcpyAsync(&hs, wb.st, sizeof(hs), cudaMemcpyDeviceToHost, s));
   NC_CUDA(cudaStreamSynchronize(s));

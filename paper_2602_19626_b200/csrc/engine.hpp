@@ -14,17 +14,16 @@ struct nc_model {
   nc::Shape s{};
   nc::Tokenizer tok;
   std::vector<std::string> vocab;
-  float *E = nullptr, *E_head = nullptr;                 // [V, d]
-  std::vector<float *> wqkv, wo, wgu, wd;                // per layer, fp32 (SIMT path)
-  // tf32 hi/lo planes of every projection for the tcgen05 3xTF32 GEMM (D14)
+  float *E = nullptr;                                    // [V, d] fp32 (embedding gather)
+  // tf32 hi/lo planes of every projection for the tcgen05 3xTF32 GEMM (D14); the fp32
+  // staging copies (gains folded) are freed once the planes exist
   float *E_head_hi = nullptr, *E_head_lo = nullptr;
   std::vector<float *> wqkv_hi, wqkv_lo, wo_hi, wo_lo, wgu_hi, wgu_lo, wd_hi, wd_lo;
-  bool use_tc = true;                                    // NC_GEMM=simt selects the SIMT GEMMs
-  bool use_tc_attn = true;                               // NC_ATTN=simt selects the SIMT attention
-  int attn_tile_rows() const { return use_tc_attn ? 128 : 64; }
+  static constexpr int attn_tile_rows() { return 128; }
   float *rope_cos = nullptr, *rope_sin = nullptr;        // [rope_len, 32]
   int rope_len = 0;
-  std::vector<void *> owned;                             // cudaFree on destruction
+  std::vector<void *> owned;                             // model_free releases them (allocator hook / cudaFree)
+  std::vector<bool> owned_hook;                          // owned[i] came from the allocator hook
   cudaStream_t walk_stream = nullptr;                    // the walk runs beside the next slab's forward
   cudaStream_t ng_stream = nullptr;                      // the N-gram precompute runs ahead of the walk
 };
@@ -67,8 +66,10 @@ Prof &prof();
 
 void model_load(nc_model *m, const std::string &path, int device);
 void model_free(nc_model *m);
-void ensure_rope(nc_model *m, int max_pos);
+void ensure_rope(nc_model *m, int64_t max_pos);
 
+// NC_ERR_INVALID unless every device token id is < V (caller-supplied ids index E, b, cu)
+void check_tokens_device(nc_model *m, const uint32_t *tokens_dev, size_t n, cudaStream_t s);
 // Compress pre-tokenized chunks whose tokens live in device memory.
 struct CompressOut {
   std::vector<uint32_t> cum, freq;   // per token, all chunks concatenated
@@ -89,7 +90,9 @@ void debug_gemm(int device, const float *A, const float *B, uint32_t M, uint32_t
 void debug_attention(int device, const float *q, const float *k, const float *v, uint32_t n, uint32_t H, uint32_t KV,
                      uint32_t window, uint32_t slide, int mode, float *o);
 void debug_forward(nc_model *m, const uint32_t *x, uint32_t rows, const Params &p, int mode, float *out);
-void debug_walk(int device, const float *logits, const uint32_t *tok, uint32_t n, uint32_t V,
-                const Params &p, uint32_t *cum, uint32_t *freq, float *p_true);
+void debug_walk(int device, const float *logits, uint32_t n_logit_rows, const uint32_t *tok, uint32_t n, uint32_t V,
+                const Params &p, uint32_t *cum, uint32_t *freq, float *p_true, float *pt_true = nullptr,
+                const uint32_t *rows = nullptr, uint32_t n_rows = 0, float *pt_rows = nullptr,
+                float *p_rows = nullptr, uint32_t *c_rows = nullptr);
 
 }  // namespace nc

@@ -13,7 +13,6 @@ struct TcGemmArgs {
   const float *rinv;          // per-row RMSNorm scale (QKV, SWIGLU, HEAD)
   float *C; int ldc;          // fp32 output: logits (HEAD), residual h in/out (RESID), q (QKV)
   float *C_hi, *C_lo;         // tf32 planes written for the next GEMM (RESID: h, SWIGLU: act; QKV: q planes)
-  int planes;                 // QKV: 1 = write q and K/V as tf32 planes (tensor-core attention)
   int layer, n_q_cols, n_kv_cols;
   RowMeta rows; KvRing ring;
   const float *rope_cos, *rope_sin;

@@ -227,6 +227,7 @@ Nc05View read_nc05(const uint8_t *in, size_t n) {
     const uint8_t *e = in + 9 + 12 * i;
     Nc05View::Ent ent{get_u32(e), get_u32(e + 4), get_u32(e + 8), off};
     if (ent.len != (ent.bits + 7ull) / 8) fail(NC_ERR_FORMAT, "stream_len != ceil(bit_count/8)");
+    if (ent.tokens > (uint32_t)INT32_MAX) fail(NC_ERR_FORMAT, "token_count out of range");
     off += ent.len;
     if (off > n) fail(NC_ERR_TRUNCATED, "NC05 stream truncated");
     v.ents.push_back(ent);

@@ -582,11 +582,10 @@ static const CUtensorMap *tmap_nd(const float *ptr, int rank, const uint64_t *di
 
 void launch_attention_tc(const AttnTcArgs &a, cudaStream_t s) {
   if (a.n_tiles <= 0) return;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ATT_SMEM);
-    attr = true;
-  }
+  static unsigned long long attr = 0;
+  if (first_on_device(attr))
+    check_launch(cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ATT_SMEM),
+                 "attention smem attribute");
   const uint64_t qd[2] = {(uint64_t)a.ldq, (uint64_t)a.q_rows};
   const uint32_t qb[2] = {32, AQ};
   const uint64_t kd[4] = {64, (uint64_t)a.KV, (uint64_t)a.ring, (uint64_t)a.n_chunks * a.n_layers};
@@ -624,7 +623,7 @@ void launch_attention_tc(const AttnTcArgs &a, cudaStream_t s) {
   at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, attn_tc_kernel, *qh, *ql, *kh, *kl, *vh, *vl, aa);
+  check_launch(cudaLaunchKernelEx(&cfg, attn_tc_kernel, *qh, *ql, *kh, *kl, *vh, *vl, aa), "attention launch");
 }
 
 }  // namespace nc

@@ -667,14 +667,9 @@ __global__ __launch_bounds__(TileCfg<BN>::THREADS, 1) void gemm_tc_kernel(const 
               const int kvh = (cb - nq - (isk ? 0 : nkv)) / 64;
               o = a.ring.off(a.rows.chunk[m], a.layer, pos) + kvh * 64;
             }
-            if (a.planes) {
-              float *dh = pos < 0 ? nullptr : (ring ? (isk ? a.ring.k_hi : a.ring.v_hi) : a.C_hi) + o;
-              float *dl = pos < 0 ? nullptr : (ring ? (isk ? a.ring.k_lo : a.ring.v_lo) : a.C_lo) + o;
-              store_head64<true>(stg, x, pos, rope, a.rope_cos, a.rope_sin, dh, dl, lane);
-            } else {
-              float *dst = pos < 0 ? nullptr : (ring ? (isk ? a.ring.k : a.ring.v) : a.C) + o;
-              store_head64<false>(stg, x, pos, rope, a.rope_cos, a.rope_sin, dst, nullptr, lane);
-            }
+            float *dh = pos < 0 ? nullptr : (ring ? (isk ? a.ring.k_hi : a.ring.v_hi) : a.C_hi) + o;
+            float *dl = pos < 0 ? nullptr : (ring ? (isk ? a.ring.k_lo : a.ring.v_lo) : a.C_lo) + o;
+            store_head64<true>(stg, x, pos, rope, a.rope_cos, a.rope_sin, dh, dl, lane);
           }
         }
       }
@@ -821,13 +816,12 @@ static int num_sms() {
 template <int EPI, int BN>
 static void launch_tc(const TcGemmArgs &a, const TcOperands &op, cudaStream_t s) {
   g_launch_stream = s;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(gemm_tc_kernel<EPI, BN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         TileCfg<BN>::SMEM);
-    cudaFuncSetAttribute(gemm_tc_kernel<EPI, BN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         TileCfg<BN>::SMEM);
-    attr = true;
+  static unsigned long long attr = 0;
+  if (first_on_device(attr)) {
+    check_launch(cudaFuncSetAttribute(gemm_tc_kernel<EPI, BN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      TileCfg<BN>::SMEM), "gemm smem attribute");
+    check_launch(cudaFuncSetAttribute(gemm_tc_kernel<EPI, BN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      TileCfg<BN>::SMEM), "gemm smem attribute");
   }
   TcGemmArgs aa = a;
   aa.a_box = a.M <= TBM ? (a.M + 7) / 8 * 8 : 0;   // rows of the A box (0: the full 128-row tile)

@@ -619,12 +619,12 @@ __global__ void ngram_pre_kernel(WalkArgs a) {
 void launch_ngram_precompute(const WalkArgs &a, cudaStream_t s) {
   if (a.n_entries <= 0) return;
   const size_t smem = (size_t)NGC * ng_group_bytes(a.V);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(ngram_pre_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  static unsigned long long attr = 0;
+  if (first_on_device(attr))
+    check_launch(cudaFuncSetAttribute(ngram_pre_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
+                 "ngram smem attribute");
   ngram_pre_kernel<<<(a.n_entries + NGC - 1) / NGC, 32 * NGWC * NGC, smem, s>>>(a);
+  check_launch(cudaGetLastError(), "ngram precompute launch");
 }
 
 // ---------------------------------------------------------------- walk ---
@@ -755,7 +755,7 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
       const unsigned long long nb = a.stream_bits[c];
       unsigned long long v = 0;
       for (int k = 0; k < 32; ++k) v = 2 * v + ((unsigned long long)k < nb ? (s[k >> 3] >> (7 - (k & 7))) & 1u : 0u);
-      st->low = 0; st->high = 0xFFFFFFFFull; st->value = v; st->bitpos = 32;
+      st->low = 0; st->high = 0xFFFFFFFFull; st->value = v; st->bitpos = 32; st->pend = 0;
     }
   }
   __syncthreads();
@@ -905,21 +905,21 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
     return H;
   };
 
-  // exponential-weights mixer step (D24), fp32 on the SFU (lg2/ex2.approx) in the
-  // log2 domain; thread 0 of every CTA and the decoder run this same arithmetic
+  // exponential-weights mixer step (D24-D26), one thread, in f64 (SURVEY §8(c):
+  // "the scalars ... are computed in f64 by one thread").  With two experts the weights depend
+  // only on the log-odds d = lw_l - lw_n (the renormalisation subtracts the same lse from
+  // both), so lw += eta [ln max(pt_t, 1e-12), ln max(png_t, 1e-12)] is d += eta ln(ratio) and
+  // softmax(lw) = (1 / (1 + e^-d), e^-d / (1 + e^-d)) -- equal in real arithmetic to the
+  // oracle's literal form.  Thread 0 of every CTA and the decoder run this same arithmetic.
   auto mixer_update = [&](float pt_t, float png_t) {
-    constexpr float LN2 = 0.693147180559945309f, LOG2E = 1.44269504088896341f;
-    const float eta = (float)a.eta;
-    float l0 = __fmaf_rn(__fmul_rn(eta, LN2), lg2f(fmaxf(pt_t, 1e-12f)), (float)s_lw[0]);
-    float l1 = __fmaf_rn(__fmul_rn(eta, LN2), lg2f(fmaxf(png_t, 1e-12f)), (float)s_lw[1]);
-    const float mx = fmaxf(l0, l1);
-    const float e0 = tc::ex2(__fmul_rn(__fsub_rn(l0, mx), LOG2E)), e1 = tc::ex2(__fmul_rn(__fsub_rn(l1, mx), LOG2E));
-    const float lse = __fmaf_rn(LN2, lg2f(__fadd_rn(e0, e1)), mx);
-    l0 = __fsub_rn(l0, lse);
-    l1 = __fsub_rn(l1, lse);
-    s_lw[0] = l0; s_lw[1] = l1;
-    s_w[0] = tc::ex2(__fmul_rn(l0, LOG2E));     // lw is renormalised: softmax(lw) = exp(lw)
-    s_w[1] = tc::ex2(__fmul_rn(l1, LOG2E));
+    const double r = __ddiv_rn(fmax((double)pt_t, 1e-12), fmax((double)png_t, 1e-12));
+    const double d = __fma_rn(a.eta, log(r), s_lw[0]);
+    s_lw[0] = d;
+    s_lw[1] = 0.0;
+    const double e = exp(-fabs(d));
+    const double big = __drcp_rn(__dadd_rn(1.0, e)), small = __dmul_rn(e, big);
+    s_w[0] = (float)(d >= 0.0 ? big : small);
+    s_w[1] = (float)(d >= 0.0 ? small : big);
   };
 
   if (enc) {
@@ -933,6 +933,17 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
     // order-free argmax; only where the values come from changed.
 
     const uint32_t i0 = s_i;
+    // test-only full-vector dumps (a.n_dump > 0): the next dumped token index of this chunk
+    uint32_t dslot = 0, drow = 0xffffffffu;
+    if (a.n_dump && c == a.dump_chunk) {
+      uint32_t lo = 0, hi = a.n_dump;   // first dump row >= i0
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) / 2;
+        if (a.dump_rows[mid] < i0) lo = mid + 1; else hi = mid;
+      }
+      dslot = lo;
+      drow = lo < a.n_dump ? a.dump_rows[lo] : 0xffffffffu;
+    }
     float uc[NGM][4];   // e = 2^((u - mth) log2 e) of the current token (u = z / tau + b), from the previous pass
     float mth = -CUDART_INF_F;   // this thread's max of the current token's u
     auto zload = [&](const float *zrow, float4 (&dst)[NGM]) {
@@ -1023,6 +1034,7 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
       const int par = it & 1;
       const int tok = tok_cur;
       if (has_next) tok_cur = (int)s_tok[(it + 1) & 2047];
+      const bool dump = drow == i;
       const int ltok = tok - (int)vb;                  // local id (may be outside [0, Vc))
       const float M = sm.M, invS = sm.invS, a0f = sm.a0f, wl = s_w[0], wn = s_w[1];
       const float scale = pt_scale(mth, M, invS);   // p~ = e * scale for this thread's elements
@@ -1056,6 +1068,12 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
         }
         uint32_t cv[4];
         quant4(p, TmV, cv);
+        if (dump) {
+          const size_t o = (size_t)dslot * V + vb + 4 * g;
+          *reinterpret_cast<float4 *>(a.dump_pt + o) = make_float4(pt[0], pt[1], pt[2], pt[3]);
+          *reinterpret_cast<float4 *>(a.dump_p + o) = make_float4(p[0], p[1], p[2], p[3]);
+          *reinterpret_cast<uint4 *>(a.dump_c + o) = make_uint4(cv[0], cv[1], cv[2], cv[3]);
+        }
 #pragma unroll
         for (int j = 0; j < 4; ++j)
           if (p[j] > bb.v) { bb.v = p[j]; bb.i = (int)vb + 4 * g + j; bb.c = cv[j]; }
@@ -1134,16 +1152,18 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
         if (wid == 0 && lane == 0) {
           unsigned long long s1 = 0, s2 = 0;
           Best b2{-1.f, 0x7fffffff, 0};
-          float p_t = 0.f;
+          float p_t = 0.f, pt_t = 0.f;
           uint32_t fq = 0;
           for (int r = 0; r < CS; ++r) {
             const Xch &x = xin[par][r];
             s1 += x.sum; s2 += x.cum;
             best_merge(b2, x.bv, x.bi, x.bc);
-            if (x.has_tok) { p_t = x.p_t; fq = x.freq_t; }
+            if (x.has_tok) { p_t = x.p_t; pt_t = x.pt_t; fq = x.freq_t; }
           }
           const long long R = (long long)T - (long long)s1;
           if ((long long)b2.c + R < 1) st->err = 1;     // D6
+          if (dump && (uint32_t)b2.i / Vc == rank)       // the argmax's final count (its owner CTA)
+            a.dump_c[(size_t)dslot * V + b2.i] = (uint32_t)((long long)b2.c + R);
           const unsigned long long cum_t = s2 + (b2.i < tok ? R : 0);
           const unsigned long long freq_t = (unsigned long long)((long long)fq + (b2.i == tok ? R : 0));
           if (rank == 0) {
@@ -1151,6 +1171,7 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
             a.out_cum[oi] = (uint32_t)cum_t;
             a.out_freq[oi] = (uint32_t)freq_t;
             if (a.out_p) a.out_p[oi] = p_t;
+            if (a.out_pt) a.out_pt[oi] = pt_t;
           }
           if (use_ng && ltok >= 0 && ltok < (int)Vc) cu_s[ltok] = __fadd_rn(cu_s[ltok], 1.f);
         } else if (wid == 2 && lane == 0) {
@@ -1174,6 +1195,10 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
         if (has_next) scatter_list(i + 1);
       }
       WALK_MARK(3);
+      if (dump) {
+        ++dslot;
+        drow = dslot < a.n_dump ? a.dump_rows[dslot] : 0xffffffffu;
+      }
       __syncthreads();
       WALK_MARK(4);
     }
@@ -1378,23 +1403,25 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
             a.out_tok[oi] = tt;
             if (a.next_x) a.next_x[c] = tt;
             if (a.out_p) a.out_p[oi] = sm.p_t;
+            if (a.out_pt) a.out_pt[oi] = sm.pt_t;
             const unsigned long long Rg = st->high - st->low + 1;
             unsigned long long lo = st->low, hi = st->low + ((Rg * (sm.cum_t + sm.freq_t)) >> a.cdf_bits) - 1;
             lo = lo + ((Rg * sm.cum_t) >> a.cdf_bits);
             unsigned long long val = st->value, bp = st->bitpos;
+            uint32_t pend = st->pend;
             const uint8_t *s = a.streams + a.stream_off[c];
             const unsigned long long nb = a.stream_bits[c];
             for (;;) {
-              if (hi < HALF) {
-              } else if (lo >= HALF) { lo -= HALF; hi -= HALF; val -= HALF; }
-              else if (lo >= QTR && hi < 3 * QTR) { lo -= QTR; hi -= QTR; val -= QTR; }
+              if (hi < HALF) { pend = 0; }
+              else if (lo >= HALF) { lo -= HALF; hi -= HALF; val -= HALF; pend = 0; }
+              else if (lo >= QTR && hi < 3 * QTR) { lo -= QTR; hi -= QTR; val -= QTR; ++pend; }
               else break;
               lo = 2 * lo; hi = 2 * hi + 1;
               const unsigned long long bit = bp < nb ? (s[bp >> 3] >> (7 - (bp & 7))) & 1u : 0u;
               val = 2 * val + bit;
               ++bp;
             }
-            st->low = lo; st->high = hi; st->value = val; st->bitpos = bp;
+            st->low = lo; st->high = hi; st->value = val; st->bitpos = bp; st->pend = pend;
           }
           if (mix) mixer_update(sm.pt_t, sm.png_t);
           if (use_ng && lt >= 0 && lt < (int)Vc) cu_s[lt] = __fadd_rn(cu_s[lt], 1.f);
@@ -1455,11 +1482,13 @@ static void launch_walk_cs(const WalkArgs &a, cudaStream_t s) {
     throw std::runtime_error("walk: vocabulary slice of " + std::to_string(Vc) +
                              " ids per CTA unsupported (needs a multiple of 4, at most 16384)");
   const size_t dyn = (size_t)Vc * 8 + Vc * 4 + Vc * 4 + ((Vc + 31) / 32) * 4 + (Vc / 4) * 4 + 64;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(walk_cl_kernel<CS, NGM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
-    if (CS > 1) cudaFuncSetAttribute(walk_cl_kernel<CS, NGM>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    attr = true;
+  static unsigned long long attr = 0;
+  if (first_on_device(attr)) {
+    check_launch(cudaFuncSetAttribute(walk_cl_kernel<CS, NGM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024),
+                 "walk smem attribute");
+    if (CS > 1)
+      check_launch(cudaFuncSetAttribute(walk_cl_kernel<CS, NGM>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+                   "walk cluster attribute");
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(a.n_entries * CS);
@@ -1471,7 +1500,7 @@ static void launch_walk_cs(const WalkArgs &a, cudaStream_t s) {
   at[0].val.clusterDim.x = CS; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, walk_cl_kernel<CS, NGM>, a);
+  check_launch(cudaLaunchKernelEx(&cfg, walk_cl_kernel<CS, NGM>, a), "walk launch");
 }
 
 int walk_ctas_per_chunk(uint32_t V, int n_chunks) { return walk_cluster_size(V, n_chunks); }
@@ -1508,22 +1537,23 @@ void launch_walk(const WalkArgs &a, cudaStream_t s) {
   }
 }
 
-__global__ void walk_init_kernel(WalkState *st, int n, double lw0, double lw1) {
+__global__ void walk_init_kernel(WalkState *st, int n, double d0) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= n) return;
   WalkState w;
   memset(&w, 0, sizeof(w));
-  w.lw[0] = lw0; w.lw[1] = lw1;
-  const double mx = fmax(lw0, lw1);
-  const double lse = __dadd_rn(mx, log(__dadd_rn(exp(__dsub_rn(lw0, mx)), exp(__dsub_rn(lw1, mx)))));
-  w.wl = (float)exp(__dsub_rn(lw0, lse));
-  w.wn = (float)exp(__dsub_rn(lw1, lse));
+  w.lw[0] = d0;   // log-odds of the initial weights (0.85, 0.15); same formula as mixer_update
+  w.lw[1] = 0.0;
+  const double e = exp(-fabs(d0));
+  const double big = __drcp_rn(__dadd_rn(1.0, e)), small = __dmul_rn(e, big);
+  w.wl = (float)(d0 >= 0.0 ? big : small);
+  w.wn = (float)(d0 >= 0.0 ? small : big);
   w.high = 0xFFFFFFFFull;
   st[c] = w;
 }
 void launch_walk_init(WalkState *st, int n_chunks, cudaStream_t s) {
   if (n_chunks <= 0) return;
-  walk_init_kernel<<<(n_chunks + 127) / 128, 128, 0, s>>>(st, n_chunks, std::log(0.85), std::log(0.15));
+  walk_init_kernel<<<(n_chunks + 127) / 128, 128, 0, s>>>(st, n_chunks, std::log(0.85) - std::log(0.15));
 }
 
 // -------------------------------------------------- debug quantizer (D5) ---

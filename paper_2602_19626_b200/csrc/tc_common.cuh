@@ -8,6 +8,24 @@
 #include <cstdint>
 
 namespace nc {
+
+// Per-device "done once" flags for host-side kernel setup (cudaFuncSetAttribute is tracked
+// per device, and one process may drive several GPUs): true the first time for the current
+// device.  `mask` is the caller's static bit set (devices 0..63).
+inline bool first_on_device(unsigned long long &mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (mask & bit) return false;
+  mask |= bit;
+  return true;
+}
+// launch-error check of the kernel launchers (surfaces as NC_ERR_BACKEND through the API)
+void throw_launch_error(cudaError_t e, const char *what);
+inline void check_launch(cudaError_t e, const char *what) {
+  if (e != cudaSuccess) throw_launch_error(e, what);
+}
+
 namespace tc {
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {

@@ -28,14 +28,14 @@ struct __align__(16) NgTok {
 };
 
 struct WalkState {                    // per chunk, device resident
-  double lw[2];                       // mixer log-weights
+  double lw[2];                       // mixer: lw[0] = log-odds d = lw_llm - lw_ng (f64), lw[1] = 0
   uint32_t i;                         // tokens walked so far (walk kernel)
   uint32_t ng_i;                      // tokens seen by the N-gram (precompute / inline)
   uint32_t hist[4];                   // last 4 tokens (oldest first), N-gram side
   uint32_t nrec[kMaxOrders];          // records in use per order
   uint32_t err;                       // nonzero = integrity failure
   float wl, wn;                       // current mixer weights (softmax of lw) as f32
-  uint32_t pad;
+  uint32_t pend;                      // decoder: pending E3 (underflow) steps, as the encoder counts them
   // device WNC decoder (D27)
   unsigned long long low, high, value, bitpos;
 };
@@ -49,6 +49,12 @@ struct WalkArgs {
   // encode inputs / outputs, indexed by tok_off[c] + i
   const uint32_t *tokens; const int64_t *tok_off;
   uint32_t *out_cum, *out_freq; float *out_p;
+  float *out_pt;                      // test only (may be NULL): p~(t) of every token, before mixing
+  // test only: full vectors of chunk dump_chunk at the sorted token indices dump_rows[0, n_dump):
+  // dump_pt / dump_p = p~ and the quantized p (fp32), dump_c = the walk's final counts (after the
+  // residual), each [n_dump][V]
+  const uint32_t *dump_rows; uint32_t n_dump; int dump_chunk;
+  float *dump_pt, *dump_p; uint32_t *dump_c;
   NgTok *ng_pre;                      // encode: precomputed N-gram predictions, ring of ng_ring per chunk:
   uint32_t ng_ring;                   //   token i of chunk c at ng_pre[c * ng_ring + i % ng_ring]
   float *ng_spadd;                    // precompute scratch (separate from the walk's spadd)

@@ -21,6 +21,7 @@ class ModelShape:
     rms_eps: float = 1e-5
     weight_seed: int = 7
     init_std: float = 1.0 / 24.0
+    gain_range: tuple = None      # None: norm gains 1 (D16); (lo, hi): gains ~ U(lo, hi), own seed
 
     @property
     def n_params(self) -> int:
@@ -38,6 +39,10 @@ SHAPES = {
     # tiny shapes for fast CPU oracle pins only (never used by the GPU path)
     "tiny": ModelShape("tiny", 2, 64, 4, 2, 16, 128, 512),
     "tiny1": ModelShape("tiny1", 1, 64, 4, 2, 16, 128, 512),
+    # non-unit RMSNorm gains (U(0.5, 1.5)): pins the gain handling (the GPU folds each gain
+    # into the following projection on load) that unit gains cannot see
+    "tiny-g": ModelShape("tiny-g", 2, 64, 4, 2, 16, 128, 512, gain_range=(0.5, 1.5)),
+    "smollm2-2l-g": ModelShape("smollm2-2l-g", 2, 576, 9, 3, 64, 1536, 49152, gain_range=(0.5, 1.5)),
 }
 
 

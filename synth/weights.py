@@ -16,7 +16,8 @@ NCW1 layout (little-endian; our own flat format):
   then    u32 V, then V x (u16 len, bytes)          -- the vocabulary (token id order)
 
 Weights: every matrix ~ N(0, (1/24)^2) from numpy PCG64(seed) drawn in file
-order; norm gains 1.  The head is tied to ``embed`` (D16).
+order; norm gains 1, or U(lo, hi) from PCG64(seed + 1000) in file
+order for shapes with ``gain_range`` (test variants).  The head is tied to ``embed`` (D16).
 """
 import os
 import struct
@@ -53,6 +54,7 @@ def tensor_layout(s: ModelShape):
 def write_ncw(path, s: ModelShape, seed: int = None):
     seed = s.weight_seed if seed is None else seed
     rng = np.random.default_rng(seed)
+    grng = np.random.default_rng(seed + 1000)
     vocab = make_vocab(s.vocab)
     tmp = str(path) + ".tmp"
     with open(tmp, "wb") as f:
@@ -63,7 +65,8 @@ def write_ncw(path, s: ModelShape, seed: int = None):
         f.write(hdr)
         for name, shape in tensor_layout(s):
             if len(shape) == 1:
-                a = np.ones(shape, dtype=np.float32)
+                a = np.ones(shape, dtype=np.float32) if s.gain_range is None else \
+                    grng.uniform(s.gain_range[0], s.gain_range[1], shape).astype(np.float32)
             else:
                 a = (rng.standard_normal(shape, dtype=np.float32) * np.float32(s.init_std))
             f.write(np.ascontiguousarray(a, dtype="<f4").tobytes())

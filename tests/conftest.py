@@ -25,3 +25,10 @@ def tiny1_weights():
     from synth import ensure_model
     from oracle.ncw import Weights
     return Weights(ensure_model("tiny1"))
+
+
+@pytest.fixture(scope="session")
+def tinyg_weights():
+    from synth import ensure_model
+    from oracle.ncw import Weights
+    return Weights(ensure_model("tiny-g"))

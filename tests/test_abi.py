@@ -81,6 +81,13 @@ def test_host_tokenizer_matches_oracle():
     assert nc.nc_host_tokenize_vocab(vocab, data) == tk.encode(data)
 
 
+def test_host_tokenizer_duplicate_lowest_id():
+    """D30: duplicate vocabulary strings -> the lowest id (same rule as oracle/tokenizer.py)."""
+    vocab = [b"<0>", b"<1>", b"<2>"] + [bytes([i]) for i in range(256)] + [b"xy", b"q", b"xy"]
+    assert nc.nc_host_tokenize_vocab(vocab, b"xy") == [259]
+    assert nc.nc_host_tokenize_vocab(vocab, b"q") == [ord("q") + 3]
+
+
 def test_shard_range_covers():
     for n in range(0, 40):
         for world in (1, 2, 3, 8):

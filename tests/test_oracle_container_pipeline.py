@@ -68,6 +68,17 @@ def test_tokenizer_greedy_longest_match():
     assert [vocab[i] for i in tk.encode(b"abd")] == [b"ab", b"d"]
 
 
+def test_tokenizer_duplicate_string_lowest_id_wins():
+    """D30: a string present under several ids tokenizes to the LOWEST id.  The
+    synthetic vocabulary has no duplicates (synth/vocab.py), so this only fixes the rule
+    the oracle and the C++ tokenizer share; the C++ side is checked in test_abi.py."""
+    vocab = [b"<0>", b"<1>", b"<2>"] + [bytes([i]) for i in range(256)] + [b"xy", b"q", b"xy"]
+    tk = Tokenizer(vocab)
+    assert tk.encode(b"xy") == [259]
+    assert tk.encode(b"q") == [ord("q") + 3]                     # the byte token (id 116) beats id 260
+    assert tk.decode(tk.encode(b"xyqxy")) == b"xyqxy"
+
+
 @pytest.mark.parametrize("flags,bits,chunks", [(3, 24, 1), (3, 24, 3), (0, 16, 2), (1, 24, 2), (2, 16, 1),
                                               (7, 24, 2), (5, 16, 1)])   # 4 = confidence skip (NEXT-1)
 def test_pipeline_roundtrip(tiny_weights, flags, bits, chunks):

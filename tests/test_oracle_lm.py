@@ -64,8 +64,13 @@ def _hf_model(w):
     return m
 
 
-def test_hf_llama_window_mask_matches_blocked(tiny_weights):
-    w = tiny_weights
+@pytest.mark.parametrize("wname", ["tiny_weights", "tinyg_weights"])
+def test_hf_llama_window_mask_matches_blocked(request, wname):
+    """unit gains (D16) and non-unit gains U(0.5, 1.5) (tiny-g): a wrong gain axis or a
+    dropped gain in the oracle fails the second case."""
+    w = request.getfixturevalue(wname)
+    if wname == "tinyg_weights":
+        assert np.abs(w.final_norm - 1).max() > 0.1 and np.abs(w.layers[0]["attn_norm"] - 1).max() > 0.1
     L, C, n = 16, 4, 40
     x = list(np.random.default_rng(3).integers(0, w.V, n))
     ours = LM(w).forward_blocked(x, L, C)

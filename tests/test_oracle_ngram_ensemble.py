@@ -144,6 +144,57 @@ def test_mixer_paper_example():
     assert abs(w[0] * g["p_llm"] + w[1] * 0.0 - g["p_mix_min"]) < 1e-15
 
 
+class _FixedNGram:
+    """stands in for the N-gram inside ChunkModel: predict() returns a fixed vector."""
+
+    def __init__(self, png):
+        self.png = np.asarray(png, dtype=np.float64)
+
+    def predict(self):
+        return self.png
+
+    def update(self, tok):
+        pass
+
+
+def _mixed(lw, z, b, png):
+    cm = ChunkModel(4, Params(warmup=0))
+    cm.ng = _FixedNGram(png)
+    cm.lw = np.log(np.asarray(lw, dtype=np.float64))
+    cm.b = np.asarray(b, dtype=np.float64)
+    return cm.distribution(np.log(np.asarray(z, dtype=np.float64)))
+
+
+def test_mixer_distribution_paper_0765():
+    """ChunkModel.distribution's post-warmup branch on P:403-406's example: initial weights
+    (0.85, 0.15), p_llm(t) = 0.90, p_ng(t) = 0 -> p_mix(t) = 0.765 exactly
+    (written out, not recomputed from the oracle's formula)."""
+    p, pt, png = _mixed([0.85, 0.15], [0.9, 0.05, 0.03, 0.02], [0, 0, 0, 0], [0.0, 0.5, 0.25, 0.25])
+    assert abs(pt[0] - 0.9) < 1e-15
+    assert abs(p[0] - 0.765) < 1e-15
+    assert np.allclose(p, [0.765, 0.1175, 0.063, 0.0545], atol=1e-15, rtol=0)
+
+
+def test_mixer_distribution_hand_mixture():
+    """Weights (0.3, 0.7) given as unnormalised log-weights, a non-zero head bias b and a
+    known p_ng: p = w_l * p~ + w_n * p_ng with p~ = softmax(log p_llm + b) (D25: the head is
+    applied BEFORE mixing).  p_llm = (1/2, 1/4, 1/8, 1/8), b = (ln 2, 0, 0, 0) -> p~ = (2/3,
+    1/6, 1/12, 1/12); p_ng = (0.1, 0.2, 0.3, 0.4) -> p = (0.27, 0.19, 0.235, 0.305).  A swapped
+    w_l/w_n gives (0.5367, ...), mixing p_llm instead of p~ gives (0.22, ...)."""
+    lw = np.array([0.3, 0.7]) * math.e ** 5                      # unnormalised: renormalised inside
+    p, pt, png = _mixed(lw, [0.5, 0.25, 0.125, 0.125], [math.log(2), 0, 0, 0], [0.1, 0.2, 0.3, 0.4])
+    assert np.allclose(pt, [2 / 3, 1 / 6, 1 / 12, 1 / 12], atol=1e-15, rtol=0)
+    assert np.allclose(p, [0.27, 0.19, 0.235, 0.305], atol=1e-15, rtol=0)
+
+
+def test_mixer_warmup_branch_ignores_ngram():
+    """i < W: p = p~ and no N-gram prediction is taken."""
+    cm = ChunkModel(4, Params(warmup=5))
+    cm.ng = _FixedNGram([0.1, 0.2, 0.3, 0.4])
+    p, pt, png = cm.distribution(np.log(np.array([0.5, 0.25, 0.125, 0.125])))
+    assert png is None and np.allclose(p, [0.5, 0.25, 0.125, 0.125], atol=1e-15, rtol=0)
+
+
 def _mixer_after(p1, p2, eta, steps=1):
     prm = Params(eta=eta, warmup=0)
     cm = ChunkModel(4, prm)

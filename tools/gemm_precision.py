@@ -11,7 +11,7 @@ for K in (64, 576, 1536):
         else:
             A = rng.random((M, K)).astype(np.float32); B = rng.random((N, K)).astype(np.float32)
         ref = A.astype(np.float64) @ B.astype(np.float64).T
-        for mode in (0, 1):
+        for mode in (0,):
             out = nc.nc_debug_gemm(A, B, mode)
             err = out - ref
             scale = np.abs(ref).max()
