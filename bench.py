@@ -1,20 +1,26 @@
 #!/usr/bin/env python
 """Benchmark: compress bytes/s of the Nacrith hot path on B200 (BASELINE.json metric).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload config2]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload config3]
 
 One step = one full compression of the workload (SURVEY.md §8(a) rows a1-a10:
 embed, 30 x {RMSNorm+QKV+RoPE, window attention, O, RMSNorm+SwiGLU MLP},
 head, the per-token CDF walk, host range coding, NC05 assembly).
 
+Workloads (synth/configs.py, BASELINE.json configs): the default is config3 -- the
+metric's "1/2/4/8 B200" workload: 10 MB alice-shaped text, 64 chunks per GPU,
+STRONG scaling (the same 10 MB at every N, 64 N chunks: SURVEY §8(d)/(e)).
+config4_shard (12.5 MB enwik-shaped per GPU, 64 chunks per GPU) and config2
+(152 KB, 8 chunks per GPU) scale weakly (each rank owns its own copy-sized share).
+
 value : device-resident inputs (token ids already in HBM) -> NC05 container
         through nc_compress_tokens; CUDA events on the launching stream,
         barrier + synchronize around every step, max over ranks.
-e2e   : the same through nc_compress (host bytes in, container out:
-        tokenization, H2D of the token ids, D2H of the (cum, freq) pairs).
-For N > 1 (torchrun) each rank compresses its own contiguous chunk range
-(weak scaling, no data-path collective); e2e uses nc_compress_shard, whose
-only collective is one NCCL allgather of the chunk table.
+e2e   : the same through nc_compress / nc_compress_shard (host bytes in,
+        container out: tokenization, H2D of the token ids, D2H of the (cum, freq)
+        pairs, the NCCL allgather of the chunk table for N > 1).
+--gpus N without a torchrun environment re-launches itself under
+torch.distributed.run with N ranks (one per GPU, NCCL); rank 0 prints the line.
 """
 import argparse
 import json
@@ -32,7 +38,6 @@ import numpy as np  # noqa: E402
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "sm_max_mhz": 1965.0}
 N_SM = 148
-FP32_LANES_PER_SM = 128          # B200: 4 SMSPs x 32 FP32 lanes (B300_MICROARCH.md / guide)
 
 
 def peaks():
@@ -94,31 +99,103 @@ class Clocks:
 
 
 # ------------------------------------------------------------------ oracle ---
-def oracle_sample(workload, path, data, n_tokens):
-    """CPU oracle (as it stands) on the first n_tokens of chunk 0 of the workload:
-    blocked fp64 forward + ensemble walk + WNC.  Returns (bytes, seconds, cores)."""
-    from oracle.chunking import split_chunks
+def _oracle_worker(job):
+    """one chunk's sample through the CPU oracle (as it stands): blocked fp64 forward +
+    ensemble walk + WNC on the first n tokens of the chunk.  Runs in a pool process."""
+    path, chunk, n_tokens, window, slide, cdf_bits = job
     from oracle.ensemble import Params, encode_tokens
     from oracle.lm import LM
     from oracle.ncw import Weights
     from oracle.tokenizer import Tokenizer
-    try:
-        from threadpoolctl import threadpool_info
-        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
-    except Exception:
-        cores = os.cpu_count()
-    w = Weights(path)
-    ch = split_chunks(data, workload.n_chunks)[0]
+    w = _oracle_worker.cache.get(path)
+    if w is None:
+        w = _oracle_worker.cache[path] = Weights(path)
     tk = Tokenizer(w.vocab)
-    t = tk.encode(ch)[:n_tokens]
-    nbytes = len(tk.decode(t))
-    prm = Params(window=workload.window, slide=workload.slide, cdf_bits=workload.cdf_bits)
+    t = tk.encode(chunk)[:n_tokens]
+    prm = Params(window=window, slide=slide, cdf_bits=cdf_bits)
     t0 = time.perf_counter()
-    x = [w.bos] + t[:-1]
-    Z = LM(w).forward_blocked(x, prm.window, prm.slide)
+    Z = LM(w).forward_blocked([w.bos] + t[:-1], prm.window, prm.slide)
     encode_tokens(Z, t, w.V, prm)
-    dt = time.perf_counter() - t0
-    return nbytes, dt, cores, len(t)
+    return len(tk.decode(t)), len(t), time.perf_counter() - t0
+
+
+_oracle_worker.cache = {}
+
+
+class OraclePool:
+    """SURVEY §8(d) oracle timing: chunk-parallel multiprocessing, P = min(8, cores) workers
+    (one chunk each, the first P chunks of the workload), BLAS threads = cores / P."""
+
+    def __init__(self, path, data, wl, n_chunks):
+        import multiprocessing as mp
+        from oracle.chunking import split_chunks
+        cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+        self.P = max(1, min(8, cores, n_chunks))
+        self.blas = max(1, cores // self.P)
+        self.cores = self.P * self.blas
+        for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+            os.environ[k] = str(self.blas)
+        self.chunks = split_chunks(data, n_chunks)[:self.P]
+        self.wl, self.path = wl, path
+        self.pool = mp.get_context("fork").Pool(self.P)
+
+    def step(self, n_tokens):
+        """one timed pass: every worker runs its chunk's first n_tokens; wall seconds."""
+        jobs = [(str(self.path), ch, n_tokens, self.wl.window, self.wl.slide, self.wl.cdf_bits) for ch in self.chunks]
+        t0 = time.perf_counter()
+        res = self.pool.map(_oracle_worker, jobs)
+        dt = time.perf_counter() - t0
+        return sum(r[0] for r in res), sum(r[1] for r in res), dt
+
+    def sample(self, n_tokens):
+        return (f"first {n_tokens} tokens of each of the first {self.P} chunks, one oracle process per chunk "
+                f"({self.P} processes x {self.blas} BLAS threads): blocked fp64 {self.wl.shape} LM + walk + WNC")
+
+    def close(self):
+        self.pool.terminate()
+
+
+def relaunch(args):
+    """--gpus N > 1 outside torchrun: run this script under torch.distributed.run, N ranks."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def dry_run(args, wl, rank, world):
+    """--dry-run (CPU, gloo): the launcher, rendezvous, shard plan, byte accounting and the
+    max-over-ranks reduction of a GPU run, without a GPU or the model (tests/test_bench_contract)."""
+    import torch
+    import torch.distributed as dist
+    import paper_2602_19626_b200 as nc
+    from synth import make_text
+    if world > 1:
+        dist.init_process_group("gloo", init_method="env://")
+    n_bytes = min(wl.n_bytes, 200_000)
+    data = make_text(wl.text_kind, n_bytes * (1 if wl.name == "config3" else world), wl.text_seed)
+    n_chunks = wl.n_chunks * world
+    cuts = nc.nc_host_split(data, n_chunks)
+    c0, c1 = nc.nc_host_shard_range(len(cuts) - 1, world, rank)
+    mine = cuts[c1] - cuts[c0] if c1 > c0 else 0
+    t = torch.tensor([float(mine), 1.0 + rank], dtype=torch.float64)
+    tot = torch.tensor([float(mine)], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t[1:], op=dist.ReduceOp.MAX)
+        dist.all_reduce(tot)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "workload": wl.name, "scaling": scaling_of(wl),
+                          "chunks": len(cuts) - 1, "bytes": len(data), "bytes_sum_over_ranks": int(tot.item()),
+                          "max_over_ranks": float(t[1].item())}))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def scaling_of(wl):
+    return "strong" if wl.name == "config3" else "weak"
 
 
 def main():
@@ -127,37 +204,46 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="config2")
+    ap.add_argument("--workload", default="config3")
     ap.add_argument("--no-decompress", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--oracle-tokens", type=int, default=1024, help="tokens per --impl reference step")
-    ap.add_argument("--baseline-tokens", type=int, default=2560, help="tokens of the cpu_baseline sample")
+    ap.add_argument("--dry-run", action="store_true", help="CPU/gloo launcher + plan check (no GPU)")
+    ap.add_argument("--oracle-tokens", type=int, default=192,
+                    help="tokens per chunk per --impl reference step (chunk-parallel)")
+    ap.add_argument("--baseline-tokens", type=int, default=1024, help="tokens per chunk of the cpu_baseline sample")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
     rank, world, local = dist_env()
 
     from synth import SHAPES, WORKLOADS, ensure_model, ensure_text, make_text
     wl = WORKLOADS[args.workload]
     metric, unit = "compress_bytes_per_sec", "B/s"
+    if args.dry_run:
+        return dry_run(args, wl, rank, world)
 
     if args.impl == "reference":
         if rank != 0:
             return
         path = ensure_model(wl.shape)
         data = open(ensure_text(args.workload), "rb").read()
-        times, nb = [], 0
-        for i in range(args.warmup + args.steps):
-            nb, dt, cores, ntok = oracle_sample(wl, path, data, args.oracle_tokens)
-            if i >= args.warmup:
-                times.append(dt)
+        op = OraclePool(path, data, wl, wl.n_chunks)
+        times, nb, ntk = [], 0, 0
+        try:
+            for i in range(args.warmup + args.steps):
+                nb, ntk, dt = op.step(args.oracle_tokens)
+                if i >= args.warmup:
+                    times.append(dt)
+        finally:
+            op.close()
         v = nb * len(times) / sum(times)
         line = {"impl": "reference", "metric": metric, "value": v, "unit": unit, "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * statistics.mean(times),
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "higher_is_better": True, "scaling": scaling_of(wl), "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic", "config": {"workload": args.workload, "model": wl.shape,
-                                                "sample": f"first {ntok} tokens of chunk 0"},
-                "cpu_baseline": {"value": v, "unit": unit, "cores": cores, "kind": "oracle",
-                                 "sample": f"first {ntok} tokens ({nb} B) of chunk 0 of {args.workload}, "
-                                           "blocked fp64 LM + walk + WNC, per step"},
+                                                "sample": op.sample(args.oracle_tokens)},
+                "cpu_baseline": {"value": v, "unit": unit, "cores": op.cores, "kind": "oracle",
+                                 "sample": op.sample(args.oracle_tokens) + f" ({ntk} tokens, {nb} B per step)"},
                 "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
         return
@@ -176,8 +262,10 @@ def main():
         dist.barrier()
     import paper_2602_19626_b200 as nc
     path = ensure_model(wl.shape)
-    # weak scaling: each rank owns wl.n_bytes of input and wl.n_chunks chunks
-    data = open(ensure_text(args.workload), "rb").read() if world == 1 else \
+    # config3: strong scaling (the same 10 MB at every N, wl.n_chunks chunks per rank);
+    # otherwise weak scaling (each rank owns wl.n_bytes of input and wl.n_chunks chunks)
+    strong = scaling_of(wl) == "strong"
+    data = open(ensure_text(args.workload), "rb").read() if (world == 1 or strong) else \
         make_text(wl.text_kind, wl.n_bytes * world, wl.text_seed)
     n_chunks = wl.n_chunks * world
     prm = nc.nc_params_default(window=wl.window, slide=wl.slide, n_chunks=n_chunks, cdf_bits=wl.cdf_bits)
@@ -242,7 +330,8 @@ def main():
     t_val, blob_part, launches, _, clk = timed(run_value, args.steps, args.warmup, clocks=clocks)
     # per-kernel-class device time (roofline, breakdown): a separate pass with the library's
     # CUDA events around every launch, so the timed value above carries no profiling overhead
-    _, _, _, prof, _ = timed(run_value, args.steps, 0, profile=True)
+    n_prof = min(args.steps, 2)
+    _, _, _, prof, _ = timed(run_value, n_prof, 0, profile=True)
     total_bytes = len(data)
     value = total_bytes * args.steps / t_val
 
@@ -279,13 +368,11 @@ def main():
 
     # ---- roofline of the dominant kernel class (live CUDA events over the timed region)
     pk, pk_kind = peaks()
-    sm_max = float(pk.get("sm_max_mhz", 1965.0))
-    alu_peak = N_SM * FP32_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12       # TFLOP/s fp32 FFMA
     kernels = {}
     for name, r in (prof or {}).items():
         if r["launches"]:
-            kernels[name] = {"launches": r["launches"] // args.steps, "ms_per_step": r["ms"] / args.steps,
-                             "work_per_step": r["work"] / args.steps}
+            kernels[name] = {"launches": r["launches"] // n_prof, "ms_per_step": r["ms"] / n_prof,
+                             "work_per_step": r["work"] / n_prof}
     flop_classes = {"gemm_qkv", "gemm_o", "gemm_gateup", "gemm_down", "gemm_head", "attention"}
     # 3xTF32 on tcgen05: algorithmic FLOPs run as 3 tf32 MMAs; tf32 dense = bf16 dense / 2
     # (B200_PROFILING.md nominal ratio).  Kernels are timed inside a long step -> sustained peak.
@@ -307,18 +394,12 @@ def main():
         r = kernels[dom]
         per_launch_ms = r["ms_per_step"] / max(1, r["launches"])
         work_launch = r["work_per_step"] / max(1, r["launches"])
-        if dom in flop_classes and os.environ.get("NC_GEMM") != "simt":
+        if dom in flop_classes:
             ach = work_launch / (per_launch_ms / 1e3) / 1e12
             roof = {"kernel": dom, "bound": "tensor", "achieved": ach, "peak": tc_peak, "unit": "TFLOP/s",
                     "frac": ach / tc_peak, "traffic": traffic,
                     "peak_source": f"{pk_kind} bf16 sustained {pk.get('bf16_tflops_sustained')} TF/s / 2 (tf32) / 3 "
                                    "(3xTF32 passes), algorithmic FLOPs"}
-        elif dom in flop_classes:
-            ach = work_launch / (per_launch_ms / 1e3) / 1e12
-            roof = {"kernel": dom, "bound": "alu", "achieved": ach, "peak": alu_peak, "unit": "TFLOP/s",
-                    "frac": ach / alu_peak, "traffic": traffic,
-                    "peak_source": f"derived: {N_SM} SMs x {FP32_LANES_PER_SM} FP32 lanes x 2 x {sm_max:.0f} MHz "
-                                   "(SIMT fp32 FFMA path, DESIGN.md)"}
         else:
             ach = work_launch / (per_launch_ms / 1e3) / 1e9
             roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
@@ -350,10 +431,13 @@ def main():
     # ---- CPU oracle baseline (rank 0, N = 1 only, bounded sample)
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        nb, dt, cores, ntk = oracle_sample(wl, path, data, args.baseline_tokens)
-        cpu = {"value": nb / dt, "unit": unit, "cores": cores, "kind": "oracle",
-               "sample": f"first {ntk} tokens ({nb} B) of chunk 0 (one window slide), blocked fp64 30-layer "
-                         f"LM + walk + WNC, {dt:.1f} s"}
+        op = OraclePool(path, data, wl, n_chunks)
+        try:
+            nb, ntk, dt = op.step(args.baseline_tokens)
+        finally:
+            op.close()
+        cpu = {"value": nb / dt, "unit": unit, "cores": op.cores, "kind": "oracle",
+               "sample": op.sample(args.baseline_tokens) + f": {ntk} tokens, {nb} B in {dt:.1f} s"}
 
     n_tok_total = int(sum(ntok))
     if world > 1:
@@ -364,9 +448,10 @@ def main():
         line = {
             "metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1000 * t_val / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": scaling_of(wl), "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": args.workload, "model": wl.shape, "text": wl.text_kind,
-                       "bytes_per_gpu": wl.n_bytes, "chunks_per_gpu": wl.n_chunks, "window": wl.window,
+                       "bytes_total": len(data), "chunks_total": nch,
+                       "bytes_per_gpu": my_bytes, "chunks_per_gpu": my_chunks, "window": wl.window,
                        "slide": wl.slide, "cdf_bits": wl.cdf_bits, "tokens": n_tok_total,
                        "l2": "256 MB buffer written between timed steps; working set (538 MB weights, "
                              "logit slabs) > 126 MB L2",

@@ -63,7 +63,7 @@ def check_dump(d, ref, toks, V, bits, warmup):
         e_p = np.abs(d["p_rows"][k] - p_o) / p_o
         assert e_pt.max() < P_TOL, ("p~ vector", r, e_pt.max())
         assert e_p.max() < P_TOL, ("p vector", r, e_p.max())
-        if r < warmup or not ref["w_llm"][r]:
+        if r < warmup or ref["w_llm"][r] is None:
             assert np.array_equal(d["p_rows"][k], d["pt_rows"][k])      # p = p~ before mixing
     # code length: the ideal bits of the GPU's (cum, freq) within 0.5 % of the oracle's
     ideal = -np.log2(freq / T).sum()
