@@ -2,7 +2,8 @@
 S:501-538).  Each chunk: tokenize, x = [BOS] ++ tokens (D13), LM logits for rows
 0..n-1 with the retained-KV window (D9-D10), ensemble walk, WNC encode; then the
 NC05 container.  Decompression mirrors it with the literal
-incremental LM, so the token being decoded is never seen in advance.
+incremental LM, so the token being decoded is never seen in advance.  The window
+variants of NEXT-4 (Params.refresh, Params.lmax_minus_one; oracle/lm.py) apply to both.
 
 bpb on the paper's real data is *parity unpinned* here (needs the real weights
 and datasets); the synthetic pipeline is pinned by round trip and by the
@@ -25,10 +26,13 @@ def compress(data: bytes, weights, prm: Params, lm_mode="blocked", collect=None)
         t = tok.encode(ch)
         n = len(t)
         x = [weights.bos] + t[:-1] if n else []
-        if lm_mode == "blocked":
-            Z = lm.forward_blocked(x, prm.window, prm.slide)
+        if prm.refresh:
+            Z = lm.forward_refresh_blocked(x, prm.window, prm.slide, prm.lmax) if lm_mode == "blocked" else \
+                lm.forward_literal(x, prm.window, prm.slide, prm.lmax, refresh=True)
+        elif lm_mode == "blocked":
+            Z = lm.forward_blocked(x, prm.lmax, prm.slide)
         else:
-            Z = lm.forward_literal(x, prm.window, prm.slide)
+            Z = lm.forward_literal(x, prm.window, prm.slide, prm.lmax)
         r = encode_tokens(Z, t, weights.V, prm)
         if collect is not None:
             collect.append(dict(tokens=t, **r))
@@ -43,7 +47,7 @@ def decompress(blob: bytes, weights, prm: Params):
     lm = LM(weights)
     out = []
     for n, bits, stream in chunks:
-        inc = lm.incremental(prm.window, prm.slide)
+        inc = lm.incremental(prm.window, prm.slide, prm.lmax, prm.refresh)
 
         def step(x, inc=inc):
             return inc.step(weights.bos if x is None else x)

@@ -60,6 +60,12 @@ class Params:
     ngram_cap: int = 500_000
     n_chunks: int = 1
     w_llm0: float = 0.85
+    lmax_minus_one: bool = False    # NEXT-4 / D10: L_max = L - 1 instead of L
+    refresh: bool = False           # NEXT-4: refresh window semantics (naive re-evaluation)
+
+    @property
+    def lmax(self):
+        return self.window - 1 if self.lmax_minus_one else self.window
 
     @property
     def tau_milli(self):

@@ -20,12 +20,23 @@ Two implementations:
   positions: row j attends keys [w(j), j], w(j) = C*ceil(max(0, j+1-L)/C)
   (D10).  Pinned equal to ``forward_literal`` and to HF LlamaForCausalLM with a
   4-D window mask in tests/test_oracle_lm.py.
+
+Window variants:
+* ``lmax`` (D10's other reading): the cache holds at most L_max entries, the slide
+  trigger is "adding a token would exceed L_max" and w(j) = C*ceil(max(0, j+1-L_max)/C).
+  L_max = L (default) or L - 1 ("slide when full, then re-evaluate the final token").
+* refresh semantics (``refresh=True``): the naive re-evaluation of P:489-492 -- on a slide
+  the cache is cleared and the surviving L_max - C tokens are re-evaluated from scratch
+  (fresh positions 0..), so every retained K/V is recomputed with the new window as its
+  whole context; SPEC's "window equivalence" holds by construction: row j's logits
+  are those of a fresh evaluation of x[w(j) .. j].  ``forward_refresh_blocked`` computes
+  the same as one fresh causal pass per window block.
 """
 import numpy as np
 
 
 def window_start(j: int, L: int, C: int) -> int:
-    """w(j) = C * ceil(max(0, j+1-L) / C)   (L_max = L)."""
+    """w(j) = C * ceil(max(0, j+1-L) / C)   (L here is L_max, = L by default)."""
     over = j + 1 - L
     if over <= 0:
         return 0
@@ -112,12 +123,33 @@ class LM:
             h = self._mlp(lw, h)
         return self._head(h)
 
-    # ---- literal incremental evaluation (paper's llama.cpp loop) -------------
-    def incremental(self, L, C):
-        return _Incremental(self, L, C)
+    # ---- refresh semantics, blocked (NEXT-4) ----------------------------------
+    def forward_refresh_blocked(self, x, L, C, lmax=None):
+        """logits [n, V] under refresh semantics: the rows sharing window start w are
+        computed by ONE fresh causal pass over x[w .. last row of the block] at fresh
+        positions 0.. (the naive re-evaluation of P:489-492); lmax as in window_start."""
+        lmax = L if lmax is None else lmax
+        x = np.asarray(x, dtype=np.int64)
+        n = len(x)
+        out = np.zeros((n, self.w.V))
+        ws = [window_start(j, lmax, C) for j in range(n)]
+        j = 0
+        while j < n:
+            w0 = ws[j]
+            j1 = j
+            while j1 < n and ws[j1] == w0:
+                j1 += 1
+            z = self.forward_blocked(x[w0:j1], 10 ** 9, 1)     # no window inside one block
+            out[j:j1] = z[j - w0:j1 - w0]
+            j = j1
+        return out
 
-    def forward_literal(self, x, L, C):
-        inc = self.incremental(L, C)
+    # ---- literal incremental evaluation (paper's llama.cpp loop) -------------
+    def incremental(self, L, C, lmax=None, refresh=False):
+        return _Incremental(self, L, C, lmax, refresh)
+
+    def forward_literal(self, x, L, C, lmax=None, refresh=False):
+        inc = self.incremental(L, C, lmax, refresh)
         return np.stack([inc.step(t) for t in x]) if len(x) else np.zeros((0, self.w.V))
 
 
@@ -129,11 +161,14 @@ class _Incremental:
     the absolute-position reading D12 used by forward_blocked and the GPU.
     """
 
-    def __init__(self, lm, L, C):
+    def __init__(self, lm, L, C, lmax=None, refresh=False):
         self.lm, self.L, self.C = lm, L, C
+        self.lmax = L if lmax is None else lmax      # D10: slide when adding would exceed L_max
+        self.refresh = refresh                       # NEXT-4: re-evaluate the survivors on a slide
         w = lm.w
         self.K = [np.zeros((0, w.KV, w.dh)) for _ in w.layers]
         self.V = [np.zeros((0, w.KV, w.dh)) for _ in w.layers]
+        self.toks = []                               # tokens whose K/V are in the cache
 
     def _shift(self):
         """kv_cache_seq_rm(0, 0, C) then kv_cache_seq_shift(0, C, -1, -C)."""
@@ -145,10 +180,29 @@ class _Incremental:
             self.K[i] = apply_rope(self.K[i][C:], cos, sin)   # K-shift: rotate by -C
             self.V[i] = self.V[i][C:]
 
+    def _refresh(self):
+        """naive slide: drop the C oldest tokens, clear the cache and
+        re-evaluate the survivors from scratch at positions 0.."""
+        w = self.lm.w
+        keep = self.toks[self.C:]
+        self.K = [np.zeros((0, w.KV, w.dh)) for _ in w.layers]
+        self.V = [np.zeros((0, w.KV, w.dh)) for _ in w.layers]
+        self.toks = []
+        for t in keep:
+            self._eval(t)
+
     def step(self, tok):
+        if self.K[0].shape[0] + 1 > self.lmax:
+            if self.refresh:
+                self._refresh()
+            else:
+                self._shift()
+                self.toks = self.toks[self.C:]
+        return self._eval(tok)
+
+    def _eval(self, tok):
         lm, w = self.lm, self.lm.w
-        if self.K[0].shape[0] + 1 > self.L:
-            self._shift()
+        self.toks.append(tok)
         p = self.K[0].shape[0]                 # relative position of the new token
         h = w.embed[[tok]].copy()
         scale = 1.0 / np.sqrt(w.dh)

@@ -91,6 +91,20 @@ def test_pipeline_roundtrip(tiny_weights, flags, bits, chunks):
     assert f == flags and tau == 1000 and len(ents) <= chunks
 
 
+@pytest.mark.parametrize("refresh,lm1", [(True, False), (False, True), (True, True)])
+def test_pipeline_window_variants_roundtrip(tiny_weights, refresh, lm1):
+    """NEXT-4 window variants through the whole oracle pipeline: blocked compress and the
+    literal incremental decompress agree (round trip), and both literal and blocked LM
+    modes give the same stream."""
+    from synth import make_text
+    data = make_text("alice", 700, 77)
+    prm = Params(window=16, slide=4, n_chunks=2, refresh=refresh, lmax_minus_one=lm1)
+    blob = compress(data, tiny_weights, prm)
+    assert decompress(blob, tiny_weights, prm) == data
+    assert compress(data, tiny_weights, prm, lm_mode="literal") == blob
+    assert blob != compress(data, tiny_weights, Params(window=16, slide=4, n_chunks=2))
+
+
 def test_pipeline_empty_and_binary(tiny_weights):
     prm = Params(window=16, slide=4, warmup=5, n_chunks=2)
     for data in (b"", b"\x00\x01\xff" * 10, b"\n\n\n"):

@@ -127,3 +127,65 @@ def test_rope_relative_invariance():
         return float((apply_rope(q, cq, sq) * apply_rope(k, ck, sk)).sum())
     assert abs(score(10, 3) - score(510, 503)) < 1e-10
     assert abs(score(10, 3) - score(10, 4)) > 1e-6
+
+
+# ---------------------------------------------------------------- NEXT-4 variants ---
+@pytest.mark.parametrize("lmax", [16, 15])
+def test_refresh_literal_equals_blocked(tiny_weights, lmax):
+    """refresh semantics (the naive re-evaluation of P:489-492): the literal loop that clears
+    the cache and re-evaluates the survivors on every slide == one fresh causal pass per
+    window block (1e-12); for L_max = L and L - 1 (D10)."""
+    lm = LM(tiny_weights)
+    x = list(np.random.default_rng(40 + lmax).integers(0, tiny_weights.V, 45))
+    a = lm.forward_literal(x, 16, 4, lmax=lmax, refresh=True)
+    b = lm.forward_refresh_blocked(x, 16, 4, lmax=lmax)
+    assert np.abs(a - b).max() < 1e-12 * max(1.0, np.abs(a).max())
+
+
+@pytest.mark.parametrize("lmax", [16, 15])
+def test_refresh_equals_hf_fresh_window(tiny_weights, lmax):
+    """S:361's window equivalence, which holds exactly under refresh semantics: row j equals
+    a FRESH evaluation of the surviving window x[w(j) .. j] -- computed here by HF
+    LlamaForCausalLM (a library routine, fp64) on that slice alone."""
+    w = tiny_weights
+    x = list(np.random.default_rng(7).integers(0, w.V, 40))
+    ours = LM(w).forward_refresh_blocked(x, 16, 4, lmax=lmax)
+    m = _hf_model(w)
+    for j in (0, 5, lmax - 1, lmax, lmax + 1, 22, 30, 39):
+        s = window_start(j, lmax, 4)
+        with torch.no_grad():
+            hf = m(torch.tensor([x[s:j + 1]])).logits[0, -1].numpy()
+        assert np.abs(hf - ours[j]).max() / np.abs(ours[j]).max() < 1e-5, j
+    # and it differs from retained-KV semantics once a slide has happened (>= 2 layers, D9)
+    ret = LM(w).forward_blocked(x, lmax, 4)
+    assert np.abs(ret[:lmax] - ours[:lmax]).max() < 1e-12
+    assert np.abs(ret[lmax + 4:] - ours[lmax + 4:]).max() > 1e-6
+
+
+def test_lmax_minus_one_window_arithmetic():
+    """L_max = L - 1 (D10's other reading): the first slide happens one row earlier, context
+    <= L - 1, slides every C rows after it."""
+    L, C = 2048, 512
+    lmax = L - 1
+    assert window_start(L - 2, lmax, C) == 0 and window_start(L - 1, lmax, C) == C
+    ctx = [j - window_start(j, lmax, C) + 1 for j in range(lmax, 6 * L)]
+    assert min(ctx) == lmax - C + 1 and max(ctx) == lmax
+    slides = [j for j in range(1, 6 * L) if window_start(j, lmax, C) != window_start(j - 1, lmax, C)]
+    assert slides[0] == L - 1 and all(b - a == C for a, b in zip(slides, slides[1:]))
+
+
+def test_lmax_minus_one_literal_equals_blocked_and_hf(tiny_weights):
+    """retained KV with L_max = L - 1: the literal rm/shift loop (slide when the cache would
+    exceed L - 1) == the blocked pass with w(j) on L_max == HF with the 4-D window mask."""
+    w = tiny_weights
+    L, C, n = 16, 4, 40
+    x = list(np.random.default_rng(9).integers(0, w.V, n))
+    a = LM(w).forward_literal(x, L, C, lmax=L - 1)
+    b = LM(w).forward_blocked(x, L - 1, C)
+    assert np.abs(a - b).max() < 1e-12 * max(1.0, np.abs(a).max())
+    mask = torch.full((1, 1, n, n), float("-inf"), dtype=torch.float64)
+    for j in range(n):
+        mask[0, 0, j, window_start(j, L - 1, C):j + 1] = 0.0
+    with torch.no_grad():
+        hf = _hf_model(w)(torch.tensor([x]), attention_mask=mask).logits[0].numpy()
+    assert np.abs(hf - b).max() / np.abs(b).max() < 1e-5
