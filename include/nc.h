@@ -78,7 +78,20 @@ typedef struct {
   uint32_t max_slab_rows;  /* forward slab size in rows over all chunks
                               (default 32768); 0 = default                    */
   uint32_t debug_dump;   /* test only: nonzero -> keep per-token p(t) values  */
+  uint32_t window_variant; /* NC_WINDOW_* bits, default 0 = retained KV with
+                              L_max = L (D9-D10, what the paper ran) */
 } nc_params;
+
+/* Window variants, nc_params.window_variant.  Not stored in the
+ * container: the decoder must pass the same value (a mismatch fails the integrity checks). */
+#define NC_WINDOW_REFRESH 1u /* refresh semantics: on every slide the surviving window is
+                                re-evaluated from scratch (the naive re-evaluation of
+                                P:489-492), so row j's logits are those of a fresh
+                                evaluation of x[w(j) .. j] (S:361's window equivalence);
+                                ~L/C times the prefill FLOPs of retained KV */
+#define NC_WINDOW_LMAX_M1 2u /* L_max = L - 1 (D10's other reading: the cache slides when
+                                full, so the context is at most L - 1 tokens):
+                                w(j) = C ceil(max(0, j + 1 - L_max) / C) */
 
 void nc_params_default(nc_params *p);
 

@@ -13,6 +13,7 @@ NC_OK, NC_ERR_FORMAT, NC_ERR_BACKEND, NC_ERR_INVALID, NC_ERR_NOMEM, NC_ERR_TRUNC
 STATUS_NAMES = {0: "NC_OK", 1: "NC_ERR_FORMAT", 2: "NC_ERR_BACKEND", 3: "NC_ERR_INVALID", 4: "NC_ERR_NOMEM",
                 5: "NC_ERR_TRUNCATED", 6: "NC_ERR_INTEGRITY"}
 FLAG_NGRAM, FLAG_HEAD, FLAG_SKIP = 1, 2, 4
+WINDOW_REFRESH, WINDOW_LMAX_M1 = 1, 2          # nc_params.window_variant (NEXT-4)
 
 # every symbol declared in include/nc.h (checked by tests/test_abi.py)
 EXPORTS = [
@@ -36,7 +37,8 @@ class nc_params(C.Structure):
                 ("window", C.c_uint32), ("slide", C.c_uint32), ("warmup", C.c_uint32),
                 ("eta", C.c_double), ("alpha", C.c_double), ("ngram_orders", C.c_uint32),
                 ("ngram_cap", C.c_uint32), ("n_chunks", C.c_uint32), ("chunks_per_gpu", C.c_uint32),
-                ("max_slab_rows", C.c_uint32), ("debug_dump", C.c_uint32)]
+                ("max_slab_rows", C.c_uint32), ("debug_dump", C.c_uint32),
+                ("window_variant", C.c_uint32)]
 
 
 _lib = None

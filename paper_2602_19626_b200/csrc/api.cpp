@@ -75,6 +75,7 @@ void nc_params_default(nc_params *p) {
   p->chunks_per_gpu = 64;
   p->max_slab_rows = 32768;
   p->debug_dump = 0;
+  p->window_variant = 0;
 }
 
 nc_status nc_set_allocator(void *(*alloc)(size_t, void *), void (*free_fn)(void *, void *), void *ctx) {

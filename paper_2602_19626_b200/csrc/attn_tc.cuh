@@ -12,7 +12,7 @@ struct AttnTcArgs {
   const float *k_hi, *k_lo, *v_hi, *v_lo;    // ring planes [chunk][layer][ring][KV][64]
   int ring, n_chunks, n_layers, layer;
   float *o_hi, *o_lo; int ldo;               // output tf32 planes [rows, H*64]
-  int H, KV, window, slide;
+  int H, KV, window, slide;                  // window = L_max of the w(j) formula (D10)
   int debug;                                 // unused
   int *item_ctr;                             // set by the launcher (persistent item scheduler)
 };

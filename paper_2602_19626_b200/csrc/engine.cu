@@ -354,7 +354,10 @@ struct Forward {
   float *q_hi = nullptr, *q_lo = nullptr;               // tf32 planes of q (tensor-core attention)
   int n_chunks_ = 0;
   KvRing ring{};
-  void alloc(Bag &bag, int Mmax_, int n_chunks, int ring_len, bool double_logits = false) {
+  // shared_ring: use another Forward's KV ring instead of allocating one (refresh re-prefill);
+  // with_logits = false: no logits buffer (a forward run without the head)
+  void alloc(Bag &bag, int Mmax_, int n_chunks, int ring_len, bool double_logits = false,
+             const KvRing *shared_ring = nullptr, bool with_logits = true) {
     Mmax = Mmax_;
     const Shape &S = m->s;
     h = bag.get<float>((size_t)Mmax * S.d);
@@ -365,7 +368,7 @@ struct Forward {
     o_lo = bag.get<float>((size_t)Mmax * S.H * S.dh);
     act_hi = bag.get<float>((size_t)Mmax * S.d_ff);
     act_lo = bag.get<float>((size_t)Mmax * S.d_ff);
-    logits = lbuf[0] = bag.get<float>((size_t)Mmax * S.V);
+    logits = lbuf[0] = with_logits ? bag.get<float>((size_t)Mmax * S.V) : nullptr;
     lbuf[1] = double_logits ? bag.get<float>((size_t)Mmax * S.V) : lbuf[0];
     ring.n_layers = S.n_layers;
     ring.ring = ring_len;
@@ -374,6 +377,10 @@ struct Forward {
     n_chunks_ = n_chunks;
     q_hi = bag.get<float>((size_t)Mmax * S.H * S.dh);
     q_lo = bag.get<float>((size_t)Mmax * S.H * S.dh);
+    if (shared_ring) {
+      ring = *shared_ring;
+      return;
+    }
     ring.k_hi = bag.get<float>(rn); ring.k_lo = bag.get<float>(rn);
     ring.v_hi = bag.get<float>(rn); ring.v_lo = bag.get<float>(rn);
     // The PV MMA multiplies masked keys by P = 0; a ring slot not written yet
@@ -386,7 +393,7 @@ struct Forward {
   // valid = rows that are real tokens (algorithmic work), attn_flops = sum over
   // valid rows of 4*H*dh*n_ctx(j) for one layer.
   void run(int M, double valid, double attn_flops, const RowMeta &rows, const AttnTile *tiles, int n_tiles,
-           const Params &p, cudaEvent_t ev_head) {
+           const Params &p, cudaEvent_t ev_head, bool head = true) {
     const Shape &S = m->s;
     Stats &st = stats();
     const int qd = S.H * S.dh, kvd = S.KV * S.dh;
@@ -410,7 +417,7 @@ struct Forward {
         at.k_hi = ring.k_hi; at.k_lo = ring.k_lo; at.v_hi = ring.v_hi; at.v_lo = ring.v_lo;
         at.ring = ring.ring; at.n_chunks = n_chunks_; at.n_layers = (int)S.n_layers; at.layer = (int)l;
         at.o_hi = o_hi; at.o_lo = o_lo; at.ldo = qd;
-        at.H = S.H; at.KV = S.KV; at.window = (int)p.window; at.slide = (int)p.slide;
+        at.H = S.H; at.KV = S.KV; at.window = (int)p.lmax; at.slide = (int)p.slide;
         PROF(K_ATTN, attn_flops, launch_attention_tc(at, s));
       }
       {
@@ -433,6 +440,10 @@ struct Forward {
       st.launches += 7;   // 2 RMSNorm scales, QKV, attention, O, gate/up, down
     }
     if (ev_head) NC_CUDA(cudaEventRecord(ev_head, s));
+    if (!head) {
+      NC_CUDA(cudaGetLastError());
+      return;
+    }
     PROF(K_RMS, 4.0 * d * valid, launch_rms(h, M, S.d, (float)S.eps, rinv, s));
     {
       TcGemmArgs g{};
@@ -456,6 +467,97 @@ static double ctx_sum(int64_t p0, int64_t p1, int64_t L, int64_t C) {
   return s;
 }
 
+// ------------------------------------------------------------- slab plan ---
+// One forward slab: positions [pos0, pos0 + len) of every chunk (rows c * len + r).  w0 >= 0:
+// every row of the slab attends keys [w0, j] (a refresh block, NEXT-4), else w(j) on L_max.
+// The walk consumes the positions [out0, out1) of the slab (all of it under retained KV;
+// the last C rows of a refresh block).
+struct Slab { int pos0, len, w0, out0, out1; };
+
+// Retained KV: full slabs of per_chunk positions while the remainder is large, then the
+// remainder split frac / (1 - frac) (128-aligned); few chunks: a geometric plan (below).
+// Refresh (NEXT-4): window block b = the rows whose window starts at w_b = b C (b = 0: rows
+// [0, L_max); b >= 1: rows [L_max + (b-1) C, L_max + b C)) is evaluated FRESH over positions
+// [w_b, block end) with every row's window start w_b, in sub-slabs of <= per_chunk positions
+// (the K/V of a sub-slab stay in the ring for the next sub-slab of the same block).
+static std::vector<Slab> slab_plan(const Params &p, int max_n, int n_chunks, int per_chunk) {
+  std::vector<Slab> out;
+  if (max_n <= 0) return out;
+  if (p.refresh) {
+    const int L = (int)p.lmax, C = (int)p.slide;
+    for (int b = 0;; ++b) {
+      const int w = b * C;
+      const int o0 = b == 0 ? 0 : L + (b - 1) * C, o1 = std::min(max_n, b == 0 ? L : L + b * C);
+      if (o0 >= max_n) break;
+      for (int q0 = w; q0 < o1; q0 += per_chunk) {
+        const int len = std::min(per_chunk, o1 - q0);
+        out.push_back(Slab{q0, len, w, std::max(q0, o0), std::max(std::max(q0, o0), q0 + len)});
+      }
+    }
+    return out;
+  }
+  std::vector<int> plan;
+  if (const char *pl = std::getenv("NC_SLAB_PLAN")) {
+    for (const char *q = pl; *q;) {
+      plan.push_back(std::max(128, std::min(per_chunk, std::atoi(q) / 128 * 128)));
+      while (*q && *q != ',') ++q;
+      if (*q == ',') ++q;
+    }
+  } else if (n_chunks <= 2) {
+    // Few chunks: the walk (~4 us per position, latency-bound, one cluster per chunk) and
+    // the N-gram precompute feeding it (~4 us per token) outlast the forward (~2.8 us per
+    // position per chunk at 4,096 rows), so start them early: a small first slab, then
+    // doubling up to 4,096 positions -- the walk of a slab then never waits long for its
+    // N-gram slab (config2 with 1 chunk: unbounded doubling 185 ms, capped at 2,048 207 ms
+    // (the forward of small slabs is inefficient), at 4,096 145 ms).
+    int len = 1024;
+    for (int pos = 0; pos < max_n; pos += len, len = std::min({per_chunk, 2 * len, 4096})) plan.push_back(len);
+  } else {
+    const char *fs = std::getenv("NC_SLAB_FRAC");
+    const double frac = fs ? std::min(0.95, std::max(0.05, std::atof(fs))) : 0.80;
+    int rem = max_n;
+    while (frac * rem > per_chunk) {   // full slabs until the last two fit the split
+      plan.push_back(per_chunk);
+      rem -= per_chunk;
+    }
+    const int first = ((int)(frac * rem) + 127) / 128 * 128;
+    if (rem <= 256 || first >= rem) {
+      plan.push_back(rem);
+    } else {
+      plan.push_back(first);
+      plan.push_back(rem - first);
+    }
+  }
+  int pos0 = 0;
+  for (size_t k = 0; pos0 < max_n; ++k) {
+    const int len = std::min(k < plan.size() ? plan[k] : per_chunk, max_n - pos0);
+    out.push_back(Slab{pos0, len, -1, pos0, pos0 + len});
+    pos0 += len;
+  }
+  return out;
+}
+
+// attention tiles of rows [a0, a1) of chunk c in a slab: <= 128 rows each, split where the
+// window start changes (only happens off 128-row boundaries with L_max = L - 1)
+static void push_tiles(std::vector<AttnTile> &tiles, int c, int a0, int a1, int pos0, int len, int w0,
+                       const Params &p) {
+  const int TR = nc_model::attn_tile_rows();
+  for (int b0 = a0; b0 < a1;) {
+    int e = std::min(a1, b0 + TR);
+    if (w0 < 0)
+      for (int j = b0 + 1; j < e; ++j)
+        if (window_start_h(j, p.lmax, p.slide) != window_start_h(b0, p.lmax, p.slide)) { e = j; break; }
+    tiles.push_back(AttnTile{c, b0, e - b0, c * len + (b0 - pos0), w0});
+    b0 = e;
+  }
+}
+// sum over rows [p0, p1) of n_ctx(j) = j - w + 1 (w = w0 of a refresh slab, else w(j))
+static double ctx_sum_slab(int64_t p0, int64_t p1, int w0, const Params &p) {
+  double s = 0;
+  for (int64_t j = p0; j < p1; ++j) s += (double)j - (w0 >= 0 ? (double)w0 : window_start_h(j, p.lmax, p.slide)) + 1;
+  return s;
+}
+
 // rows of a slab: chunk c's positions [pos0, pos0 + len) are rows c * len + r
 __global__ void slab_rows_kernel(const uint32_t *tokens, const int64_t *tok_off, const uint32_t *ntok, int len,
                                  int pos0, int M, uint32_t bos, uint32_t *x, int32_t *chunk, int32_t *pos) {
@@ -475,7 +577,7 @@ __global__ void step_rows_kernel(const uint32_t *ntok, int n_chunks, int j, int3
   bool act = j < (int)ntok[c];
   chunk[c] = c;
   pos[c] = act ? j : -1;
-  tiles[c] = AttnTile{c, j, act ? 1 : 0, c};
+  tiles[c] = AttnTile{c, j, act ? 1 : 0, c, -1};
   chunk_of[c] = c;
   row0[c] = c;
   count[c] = act ? 1 : 0;
@@ -489,7 +591,7 @@ __global__ void step_rows_dev_kernel(const uint32_t *ntok, int n_chunks, int *jc
     const bool act = j < (int)ntok[c];
     chunk[c] = c;
     pos[c] = act ? j : -1;
-    tiles[c] = AttnTile{c, j, act ? 1 : 0, c};
+    tiles[c] = AttnTile{c, j, act ? 1 : 0, c, -1};
     chunk_of[c] = c;
     row0[c] = c;
     count[c] = act ? 1 : 0;
@@ -547,6 +649,61 @@ struct WalkBufs {
   }
 };
 
+// Refresh semantics in the decode direction (NEXT-4): when step j is the first row of window
+// block b >= 1 (j = L_max + (b - 1) C), the surviving positions [w_b, j) (w_b = b C) of every
+// chunk are re-evaluated from scratch -- one slab forward with window start w_b, no head --
+// into the decode forward's KV ring, exactly the rows the compressor's refresh slab computed
+// for them (per-row arithmetic is batch-invariant, D15), so decoding stays bit-identical.
+struct Refill {
+  Forward fw2{nullptr, nullptr};
+  const uint32_t *toks = nullptr;   // token ids in chunk-major layout (tok_off), x_p = toks[p - 1]
+  const int64_t *tok_off = nullptr;
+  const uint32_t *ntok = nullptr;
+  uint32_t *xs = nullptr;
+  int32_t *rc = nullptr, *rp = nullptr;
+  AttnTile *tiles_d = nullptr;
+  int n_chunks = 0, len = 0;
+  uint32_t bos = 0;
+  std::vector<uint32_t> ntok_h;
+  cudaStream_t s = nullptr;
+  void init(nc_model *m, Bag &bag, Forward &fw, int n_ch, const Params &p, const uint32_t *toks_d,
+            const int64_t *tok_off_d, const uint32_t *ntok_d, cudaStream_t st, const uint32_t *ntok_host = nullptr) {
+    s = st;
+    n_chunks = n_ch;
+    len = (int)p.lmax - (int)p.slide;
+    toks = toks_d; tok_off = tok_off_d; ntok = ntok_d;
+    bos = m->s.bos;
+    fw2 = Forward{m, st};
+    const int Mr = n_chunks * ((len + 127) / 128 * 128);
+    fw2.alloc(bag, Mr, n_chunks, fw.ring.ring, false, /*ring=*/&fw.ring, /*logits=*/false);
+    xs = bag.get<uint32_t>(Mr);
+    rc = bag.get<int32_t>(Mr);
+    rp = bag.get<int32_t>(Mr);
+    tiles_d = bag.get<AttnTile>((size_t)n_chunks * ((len + 127) / 128 + 8));
+    if (ntok_host) ntok_h.assign(ntok_host, ntok_host + n_chunks);
+  }
+  // the re-prefill (if step j starts a refresh block); returns true if it ran
+  bool before_step(uint32_t j, const Params &p) {
+    const int L = (int)p.lmax, C = (int)p.slide;
+    if ((int)j < L || ((int)j - L) % C != 0) return false;
+    const int w = ((int)j - L) / C * C + C;
+    std::vector<AttnTile> tiles;
+    for (int c = 0; c < n_chunks; ++c) {
+      const int e = ntok_h.empty() ? (int)j : std::min<int>((int)j, (int)ntok_h[c]);
+      push_tiles(tiles, c, w, e, w, len, w, p);
+    }
+    if (tiles.empty()) return false;
+    NC_CUDA(cudaMemcpyAsync(tiles_d, tiles.data(), tiles.size() * sizeof(AttnTile), cudaMemcpyHostToDevice, s));
+    const int Ms = n_chunks * len;
+    slab_rows_kernel<<<(Ms + 255) / 256, 256, 0, s>>>(toks, tok_off, ntok, len, w, Ms, bos, xs, rc, rp);
+    NC_CUDA(cudaGetLastError());
+    RowMeta rm{xs, rc, rp};
+    fw2.run(Ms, 0, 0, rm, tiles_d, (int)tiles.size(), p, nullptr, /*head=*/false);
+    stats().launches++;
+    return true;
+  }
+};
+
 // --------------------------------------------------------------- compress ---
 void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<uint32_t> &ntok,
                      const Params &p, cudaStream_t s, CompressOut &out) {
@@ -570,62 +727,19 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
   if (n_chunks == 0 || max_n == 0) return;
   if (S.V >= (1u << p.cdf_bits)) fail(NC_ERR_INVALID, "T = 2^cdf_bits must exceed V");
 
-  // Slab plan.  The walk of slab s overlaps the forward of slab s+1 (own stream,
-  // logits double-buffered); only the last slab's walk runs after the forward.
-  // Bigger slabs run the GEMMs more efficiently (fewer tile waves), a smaller last
-  // slab shortens that final walk.  Measured on config2 (3885 positions):
-  // 4 x 1024 -> 109 ms, 2 x ~1940 -> 101.5 ms, 2944 + 941 (frac 0.75) -> 96.8 ms (early
-  // kernels); with the faster walk of r01f, frac 0.70 / 0.75 / 0.80 / 0.85 -> 75.0 / 74.2 /
-  // 73.1 / 73.6 ms.  So: slabs of the largest size (max_slab_rows / n_chunks) while the
-  // remainder exceeds one / frac, then the remainder split 80/20 (NC_SLAB_FRAC), 128-aligned so no
-  // 128-row attention tile crosses a retained-window step (C | 128 k).
+  // Slab plan (slab_plan above).  The walk of slab s overlaps the forward of slab s+1 (own
+  // stream, logits double-buffered); only the last slab's walk runs after the forward.
+  // Bigger slabs run the GEMMs more efficiently (fewer tile waves), a smaller last slab
+  // shortens that final walk.  Measured on config2 (3885 positions): 4 x 1024 -> 109 ms,
+  // 2 x ~1940 -> 101.5 ms, 2944 + 941 (frac 0.75) -> 96.8 ms (early kernels); with the faster
+  // walk of r01f, frac 0.70 / 0.75 / 0.80 / 0.85 -> 75.0 / 74.2 / 73.1 / 73.6 ms.  Slabs are
+  // 128-aligned so no 128-row attention tile crosses a retained-window step (C | 128 k).
   // NC_SLAB_PLAN="a,b,..." (diagnostics) gives explicit lengths.
   const int per_chunk = std::max(128, (int)(p.max_slab_rows / n_chunks) / 128 * 128);
-  std::vector<int> plan;
-  if (const char *pl = std::getenv("NC_SLAB_PLAN")) {
-    for (const char *q = pl; *q;) {
-      plan.push_back(std::max(128, std::min(per_chunk, std::atoi(q) / 128 * 128)));
-      while (*q && *q != ',') ++q;
-      if (*q == ',') ++q;
-    }
-  } else if (n_chunks <= 2) {
-    // Few chunks: the walk (~4 us per position, latency-bound, one cluster per chunk) and
-    // the N-gram precompute feeding it (~4 us per token) outlast the forward (~2.8 us per
-    // position per chunk at 4,096 rows), so start them early: a small first slab, then
-    // doubling up to 4,096 positions -- the walk of a slab then never waits long for its
-    // N-gram slab (config2 with 1 chunk: unbounded doubling 185 ms, capped at 2,048 207 ms
-    // (the forward of small slabs is inefficient), at 4,096 145 ms).
-    int len = 1024;
-    for (int pos = 0; pos < (int)max_n; pos += len, len = std::min({per_chunk, 2 * len, 4096})) plan.push_back(len);
-  } else {
-    const char *fs = std::getenv("NC_SLAB_FRAC");
-    const double frac = fs ? std::min(0.95, std::max(0.05, std::atof(fs))) : 0.80;
-    int rem = (int)max_n;
-    while (frac * rem > per_chunk) {   // full slabs until the last two fit the split
-      plan.push_back(per_chunk);
-      rem -= per_chunk;
-    }
-    const int first = ((int)(frac * rem) + 127) / 128 * 128;
-    if (rem <= 256 || first >= rem) {
-      plan.push_back(rem);
-    } else {
-      plan.push_back(first);
-      plan.push_back(rem - first);
-    }
-  }
-  std::vector<int> slab_pos0, slab_len;
+  const std::vector<Slab> slabs = slab_plan(p, (int)max_n, n_chunks, per_chunk);
   int R = 128;
-  {
-    int pos0 = 0;
-    for (size_t k = 0; pos0 < (int)max_n; ++k) {
-      const int len = k < plan.size() ? plan[k] : per_chunk;
-      slab_pos0.push_back(pos0);
-      slab_len.push_back(std::min(len, (int)max_n - pos0));
-      R = std::max(R, ((slab_len.back() + 127) / 128) * 128);
-      pos0 += len;
-    }
-  }
-  const int n_slabs = (int)slab_len.size();
+  for (const Slab &sb : slabs) R = std::max(R, ((sb.len + 127) / 128) * 128);
+  const int n_slabs = (int)slabs.size();
   const int ring_len = (int)p.window + R;
   const int M = n_chunks * R;   // buffer rows (the largest slab)
   ensure_rope(m, (int64_t)max_n + 1);
@@ -648,16 +762,11 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
   for (int sl = 0; sl < n_slabs; ++sl) {
     tile_off[sl] = (int)tiles.size();
     w_off[sl] = (int)w_chunk.size();
-    const int TR = m->attn_tile_rows();
-    const int len = slab_len[sl], q0 = slab_pos0[sl];
+    const Slab &sb = slabs[sl];
     for (int c = 0; c < n_chunks; ++c) {
-      for (int b0 = 0; b0 < len; b0 += TR) {
-        int p0 = q0 + b0;
-        int nr = std::min<int>(std::min(TR, len - b0), (int)ntok[c] - p0);
-        if (nr > 0) tiles.push_back(AttnTile{c, p0, nr, c * len + b0});
-      }
-      int cnt = std::min<int>(len, (int)ntok[c] - q0);
-      if (cnt > 0) { w_chunk.push_back(c); w_row0.push_back(c * len); w_count.push_back(cnt); }
+      push_tiles(tiles, c, sb.pos0, std::min(sb.pos0 + sb.len, (int)ntok[c]), sb.pos0, sb.len, sb.w0, p);
+      const int o1 = std::min(sb.out1, (int)ntok[c]);
+      if (o1 > sb.out0) { w_chunk.push_back(c); w_row0.push_back(c * sb.len + (sb.out0 - sb.pos0)); w_count.push_back(o1 - sb.out0); }
     }
     // the persistent attention kernel claims tiles in list order: heaviest (latest positions,
     // most keys) first so the last claims are short
@@ -696,12 +805,12 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
   wb.fill(wbase, p, S.V);
   for (int sl = 0; sl < n_slabs; ++sl) {
     if (use_ng) {
-      // ring slot p % ng_ring of this slab's positions last held position p - ng_ring: wait
-      // for the walk of the last slab holding such a position (none while within the ring)
-      const int64_t need = (int64_t)slab_pos0[sl] + slab_len[sl] - (int64_t)wb.ng_ring;
+      // ring slot i % ng_ring of this slab's walked tokens last held token i - ng_ring: wait
+      // for the walk of the last slab holding such a token (none while within the ring)
+      const int64_t need = (int64_t)slabs[sl].out1 - (int64_t)wb.ng_ring;
       int q = -1;
       for (int k2 = 0; k2 < sl; ++k2)
-        if (slab_pos0[k2] < need) q = k2;
+        if (slabs[k2].out0 < need && slabs[k2].out1 > slabs[k2].out0) q = k2;
       if (q >= 0) NC_CUDA(cudaStreamWaitEvent(ns, ev[4 * q + 3], 0));
       WalkArgs na = wbase;
       na.chunk_of = wc_d + w_off[sl]; na.row0 = wr_d + w_off[sl]; na.count = wn_d + w_off[sl];
@@ -713,7 +822,7 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
     if (sl >= 2) NC_CUDA(cudaStreamWaitEvent(s, ev[4 * (sl - 2) + 3], 0));   // logits buffer free again
     fw.logits = fw.lbuf[sl & 1];
     NC_CUDA(cudaEventRecord(ev[4 * sl], s));
-    const int len = slab_len[sl], q0 = slab_pos0[sl], Ms = n_chunks * len;
+    const int len = slabs[sl].len, q0 = slabs[sl].pos0, Ms = n_chunks * len;
     PROF(K_MISC, 0, (slab_rows_kernel<<<(Ms + 255) / 256, 256, 0, s>>>(tokens_dev, tok_off_d, ntok_d, len, q0, Ms,
                                                                        S.bos, xs, rchunk, rpos)));
     st.launches++;
@@ -721,7 +830,7 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
     double valid = 0, ctx = 0;
     for (int c = 0; c < n_chunks; ++c) {
       int64_t a0 = q0, a1 = std::min<int64_t>((int64_t)q0 + len, ntok[c]);
-      if (a1 > a0) { valid += (double)(a1 - a0); ctx += ctx_sum(a0, a1, p.window, p.slide); }
+      if (a1 > a0) { valid += (double)(a1 - a0); ctx += ctx_sum_slab(a0, a1, slabs[sl].w0, p); }
     }
     fw.run(Ms, valid, 4.0 * S.H * S.dh * ctx, rows, tiles_d + tile_off[sl], tile_off[sl + 1] - tile_off[sl], p,
            nullptr);
@@ -771,7 +880,7 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
     };
     for (int sl = 0; sl < n_slabs; ++sl)
       fprintf(stderr, "slab %d (%d positions): forward %.2f-%.2f  ngram done %.2f  walk %.2f-%.2f\n", sl,
-              slab_len[sl], at(ev[4 * sl]), at(ev[4 * sl + 1]), use_ng ? at(ev[4 * n_slabs + sl]) : 0.f,
+              slabs[sl].len, at(ev[4 * sl]), at(ev[4 * sl + 1]), use_ng ? at(ev[4 * n_slabs + sl]) : 0.f,
               at(ev[4 * sl + 2]), at(ev[4 * sl + 3]));
   }
 }
@@ -902,7 +1011,7 @@ void decompress_device(nc_model *m, const uint8_t *blob, const Nc05View &view, c
   auto step = [&](uint32_t j) {
     double valid = 0;
     for (int c = 0; c < n_chunks; ++c) valid += j < ntok[c] ? 1 : 0;
-    const double ctx = (double)j - window_start_h(j, p.window, p.slide) + 1;
+    const double ctx = (double)j - window_start_h(j, p.lmax, p.slide) + 1;
     PROF(K_MISC, 0, (step_rows_dev_kernel<<<1, 256, 0, s>>>(ntok_d, n_chunks, jctr, rchunk, rpos, tiles, wc, wr, wn)));
     RowMeta rows{x_cur, rchunk, rpos};
     fw.run(n_chunks, valid, 4.0 * S.H * S.dh * ctx * valid, rows, tiles, n_chunks, p, nullptr);
@@ -914,6 +1023,8 @@ void decompress_device(nc_model *m, const uint8_t *blob, const Nc05View &view, c
   // launcher buffer) the step is captured once as a CUDA graph and replayed.  Per-launch
   // profiling (CUDA events around every kernel) runs eagerly instead.
   const bool graph = !prof().on && !std::getenv("NC_DECODE_NO_GRAPH");
+  Refill rf;   // refresh semantics: re-evaluate the surviving window at every block start
+  if (p.refresh) rf.init(m, bag, fw, n_chunks, p, out_tok, tok_off_d, ntok_d, s, ntok.data());
   step(0);
   if (graph && max_n > 1) {
     cudaGraph_t g = nullptr;
@@ -926,6 +1037,7 @@ void decompress_device(nc_model *m, const uint8_t *blob, const Nc05View &view, c
     st.launches = l0;
     NC_CUDA(cudaGraphInstantiate(&ge, g, 0));
     for (uint32_t j = 1; j < max_n; ++j) {
+      if (p.refresh) rf.before_step(j, p);
       NC_CUDA(cudaGraphLaunch(ge, s));
       st.launches += per_step;
       if ((j & 255) == 255) NC_CUDA(cudaGetLastError());
@@ -934,6 +1046,7 @@ void decompress_device(nc_model *m, const uint8_t *blob, const Nc05View &view, c
     cudaGraphDestroy(g);
   } else {
     for (uint32_t j = 1; j < max_n; ++j) {
+      if (p.refresh) rf.before_step(j, p);
       step(j);
       if ((j & 255) == 255) {
         NC_CUDA(cudaGetLastError());
@@ -989,44 +1102,42 @@ void debug_forward(nc_model *m, const uint32_t *x, uint32_t rows, const Params &
   std::vector<uint32_t> xv(x, x + rows);
   uint32_t *x_d = bag.upload(xv);
   Forward fw{m, s};
+  // the slab kernel maps x through "tokens[p-1]"; feed x shifted so that x_j = x[j]
+  std::vector<uint32_t> shifted(rows);
+  for (uint32_t j = 0; j + 1 < rows; ++j) shifted[j] = x[j + 1];
+  uint32_t *t_d = bag.upload(shifted);
+  std::vector<int64_t> off{0};
+  int64_t *off_d = bag.upload(off);
+  std::vector<uint32_t> nt{rows};
+  uint32_t *nt_d = bag.upload(nt);
   if (mode == 0) {
-    const int R = std::max(128, (int)p.max_slab_rows / 128 * 128);
-    const int Rr = std::min<int>(((rows + 127) / 128) * 128, R);
-    const int n_slabs = (int)((rows + Rr - 1) / Rr);
+    const int per = std::max(128, (int)p.max_slab_rows / 128 * 128);
+    const std::vector<Slab> slabs = slab_plan(p, (int)rows, 1, per);
+    int Rr = 128;
+    for (const Slab &sb : slabs) Rr = std::max(Rr, (sb.len + 127) / 128 * 128);
     fw.alloc(bag, Rr, 1, (int)p.window + Rr);
-    // the slab kernel maps x through "tokens[p-1]"; feed x shifted so that x_j = x[j]
-    std::vector<uint32_t> shifted(rows);
-    for (uint32_t j = 0; j + 1 < rows; ++j) shifted[j] = x[j + 1];
-    uint32_t *t_d = bag.upload(shifted);
-    std::vector<int64_t> off{0};
-    int64_t *off_d = bag.upload(off);
-    std::vector<uint32_t> nt{rows};
-    uint32_t *nt_d = bag.upload(nt);
     uint32_t *xs = bag.get<uint32_t>(Rr);
     int32_t *rc = bag.get<int32_t>(Rr), *rp = bag.get<int32_t>(Rr);
-    for (int sl = 0; sl < n_slabs; ++sl) {
+    for (const Slab &sb : slabs) {
       std::vector<AttnTile> tiles;
-      const int TR = m->attn_tile_rows();
-      for (int b0 = 0; b0 < Rr; b0 += TR) {
-        int p0 = sl * Rr + b0;
-        int nr = std::min<int>(TR, (int)rows - p0);
-        if (nr > 0) tiles.push_back(AttnTile{0, p0, nr, b0});
-      }
+      push_tiles(tiles, 0, sb.pos0, sb.pos0 + sb.len, sb.pos0, sb.len, sb.w0, p);
       AttnTile *td = bag.upload(tiles);
-      slab_rows_kernel<<<(Rr + 255) / 256, 256, 0, s>>>(t_d, off_d, nt_d, Rr, sl * Rr, Rr, x[0], xs, rc, rp);
+      slab_rows_kernel<<<(sb.len + 255) / 256, 256, 0, s>>>(t_d, off_d, nt_d, sb.len, sb.pos0, sb.len, x[0], xs, rc, rp);
       RowMeta rm{xs, rc, rp};
-      fw.run(Rr, 0, 0, rm, td, (int)tiles.size(), p, nullptr);
-      int cnt = std::min<int>(Rr, (int)rows - sl * Rr);
-      NC_CUDA(cudaMemcpyAsync(out + (size_t)sl * Rr * S.V, fw.logits, (size_t)cnt * S.V * 4, cudaMemcpyDeviceToHost, s));
+      fw.run(sb.len, 0, 0, rm, td, (int)tiles.size(), p, nullptr);
+      if (sb.out1 > sb.out0)
+        NC_CUDA(cudaMemcpyAsync(out + (size_t)sb.out0 * S.V, fw.logits + (size_t)(sb.out0 - sb.pos0) * S.V,
+                                (size_t)(sb.out1 - sb.out0) * S.V * 4, cudaMemcpyDeviceToHost, s));
     }
   } else {
     fw.alloc(bag, 1, 1, (int)p.window + 128);
+    Refill rf;
+    if (p.refresh) rf.init(m, bag, fw, 1, p, t_d, off_d, nt_d, s);
     int32_t *rc = bag.get<int32_t>(1), *rp = bag.get<int32_t>(1);
     AttnTile *tiles = bag.get<AttnTile>(1);
     int32_t *wc = bag.get<int32_t>(1), *wr = bag.get<int32_t>(1), *wn = bag.get<int32_t>(1);
-    std::vector<uint32_t> nt{rows};
-    uint32_t *nt_d = bag.upload(nt);
     for (uint32_t j = 0; j < rows; ++j) {
+      if (p.refresh) rf.before_step(j, p);
       step_rows_kernel<<<1, 32, 0, s>>>(nt_d, 1, (int)j, rc, rp, tiles, wc, wr, wn);
       RowMeta rm{x_d + j, rc, rp};
       fw.run(1, 0, 0, rm, tiles, 1, p, nullptr);

@@ -266,6 +266,9 @@ Params validate(const nc_params *p) {
   q.chunks_per_gpu = p->chunks_per_gpu ? p->chunks_per_gpu : 64;
   q.max_slab_rows = p->max_slab_rows ? p->max_slab_rows : 32768;
   q.debug_dump = p->debug_dump;
+  if (p->window_variant & ~3u) fail(NC_ERR_INVALID, "window_variant: only bits 0-1 are defined");
+  q.refresh = (p->window_variant & NC_WINDOW_REFRESH) != 0;
+  q.lmax = (p->window_variant & NC_WINDOW_LMAX_M1) ? q.window - 1 : q.window;
   return q;
 }
 

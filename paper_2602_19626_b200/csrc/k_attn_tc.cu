@@ -153,7 +153,7 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
     x.t = a.tiles[it / a.H];
     x.h = it % a.H;
     x.g = x.h / (a.H / a.KV);
-    const int w = wstart(x.t.p0, a.window, a.slide);
+    const int w = x.t.w0 >= 0 ? x.t.w0 : wstart(x.t.p0, a.window, a.slide);   // a.window = L_max
     x.kb0 = w / AK;
     x.nkb = x.t.nrows > 0 ? (x.t.p0 + x.t.nrows - 1) / AK - x.kb0 + 1 : 0;   // 0: inactive decode chunk
     x.zc = x.t.chunk * a.n_layers + a.layer;

@@ -29,6 +29,8 @@ void launch_rms(const float *h, int M, int d, float eps, float *rinv, cudaStream
 
 enum GemmEpi { EPI_QKV = 0, EPI_RESID = 1, EPI_SWIGLU = 2, EPI_HEAD = 3 };
 
-struct AttnTile { int chunk, p0, nrows, qrow0; };
+// <= 128 consecutive rows [p0, p0 + nrows) of one chunk at slab rows qrow0..; w0 >= 0: the
+// window start of every row of the tile (refresh slabs, NEXT-4), -1: w(j) of the formula (D10)
+struct AttnTile { int chunk, p0, nrows, qrow0, w0; };
 
 }  // namespace nc

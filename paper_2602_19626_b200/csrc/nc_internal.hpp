@@ -100,6 +100,8 @@ struct Params {
   uint32_t cdf_bits, flags, tau_milli, window, slide, warmup, orders, cap, n_chunks,
       chunks_per_gpu, max_slab_rows, debug_dump;
   double eta, alpha, inv_tau;
+  bool refresh;     // NEXT-4: refresh window semantics (NC_WINDOW_REFRESH)
+  uint32_t lmax;    // D10: L_max = window, or window - 1 (NC_WINDOW_LMAX_M1)
 };
 Params validate(const nc_params *p);
 

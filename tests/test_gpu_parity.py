@@ -588,3 +588,68 @@ def test_compress_tokens_equals_compress(nc, m2):
     blob2 = nc.nc_compress_tokens(m2, td.data_ptr(), np.array(ntok, np.uint32), prm, s.cuda_stream)
     torch.cuda.synchronize()
     assert blob2 == blob
+
+
+# ------------------------------------------------------ NEXT-4 window variants ---
+VARIANTS = [(1, "refresh"), (2, "lmax-1"), (3, "refresh+lmax-1")]
+
+
+@pytest.mark.parametrize("wv,name", VARIANTS)
+def test_forward_window_variants(nc, m2, w2, wv, name):
+    """NEXT-4 on the GPU forward: refresh semantics (every window block evaluated fresh,
+    P:489-492) and/or L_max = L - 1 (D10): logits within 1e-5 of max|z| of the fp64 oracle
+    (oracle/lm.py, pinned to HF on CPU), over several slides with a ragged tail; and the
+    decode-step path (with the refresh re-prefill at every block start) bit-identical to the
+    prefill path (D15)."""
+    from oracle.lm import LM
+    rng = np.random.default_rng(30 + wv)
+    L, C, n = 256, 128, 777
+    x = [0] + list(rng.integers(3, w2.V, n - 1))
+    prm = nc.nc_params_default(window=L, slide=C, max_slab_rows=256, window_variant=wv)
+    z = nc.nc_debug_forward(m2, x, prm, 0)
+    lmax = L - 1 if wv & 2 else L
+    ref = LM(w2).forward_refresh_blocked(x, L, C, lmax) if wv & 1 else LM(w2).forward_blocked(x, lmax, C)
+    err = np.abs(z - ref).max() / np.abs(ref).max()
+    assert err < Z_TOL, err
+    z1 = nc.nc_debug_forward(m2, x, prm, 1)
+    assert np.array_equal(z, z1)
+    # the variant really changes the logits past the first slide
+    base = nc.nc_debug_forward(m2, x, nc.nc_params_default(window=L, slide=C, max_slab_rows=256), 0)
+    assert np.abs(base[L + C:] - z[L + C:]).max() > 1e-4
+
+
+@pytest.mark.parametrize("wv,name", VARIANTS)
+@pytest.mark.parametrize("n_chunks", [1, 3])
+def test_window_variants_roundtrip_size_and_p(nc, m2, w2, wv, name, n_chunks):
+    """NEXT-4 end to end: GPU round trip, size within 0.5 % of the oracle pipeline with the
+    same variant, p(t) within 1e-4 at every row; decoding with the wrong variant fails the
+    integrity checks (the variant is not stored in the container, like L and C)."""
+    from oracle.ensemble import Params
+    from synth import make_text
+    data = make_text("alice", 4096, 1001)
+    prm = nc.nc_params_default(window=512, slide=128, n_chunks=n_chunks, window_variant=wv, max_slab_rows=1024)
+    blob = nc.nc_compress(m2, data, prm)
+    assert nc.nc_decompress(m2, blob, prm) == data
+    po = Params(window=512, slide=128, n_chunks=n_chunks, refresh=bool(wv & 1), lmax_minus_one=bool(wv & 2))
+    from oracle.chunking import split_chunks
+    from oracle.ensemble import encode_tokens
+    from oracle.lm import LM
+    from oracle.tokenizer import Tokenizer
+    tk, lm = Tokenizer(w2.vocab), LM(w2)
+    size = 9
+    for ch in split_chunks(data, n_chunks):
+        t = tk.encode(ch)
+        x = [w2.bos] + t[:-1]
+        Z = lm.forward_refresh_blocked(x, 512, 128, po.lmax) if po.refresh else lm.forward_blocked(x, po.lmax, 128)
+        r = encode_tokens(Z, t, w2.V, po)
+        size += 12 + (r["bits"] + 7) // 8
+        z = nc.nc_debug_forward(m2, x, prm, 0)
+        _, _, p_gpu = nc.nc_debug_walk(z, t, prm)
+        p_ref = np.array(r["p_true"])
+        assert (np.abs(p_gpu - p_ref) / p_ref).max() < P_TOL
+    assert abs(len(blob) - size) <= 0.005 * size, (len(blob), size)
+    if n_chunks == 1:
+        other = nc.nc_params_default(window=512, slide=128, n_chunks=n_chunks, window_variant=wv ^ 1)
+        with pytest.raises(nc.NcError) as ei:
+            nc.nc_decompress(m2, blob, other)
+        assert ei.value.status == nc._lib.NC_ERR_INTEGRITY
