@@ -9,6 +9,9 @@ enwik-shaped: MediaWiki XML pages wrapping the same prose, with [[links]],
 {{templates}}, '''bold''', == headings ==, * lists, &lt;ref&gt; entities, numbers,
 dates and ~1-2 % non-ASCII UTF-8 characters.
 
+mixed: an arbitrary-file-shaped byte stream (text segments alternating with binary
+segments) for the NC06 hybrid format (P:512-528).
+
 Everything is a pure function of (kind, n_bytes, seed).
 """
 import numpy as np
@@ -205,9 +208,44 @@ def _enwik(n_bytes: int, seed: int) -> bytes:
     return data
 
 
+def _mixed(n_bytes: int, seed: int) -> bytes:
+    """An arbitrary-file-shaped input for NC06: alice-shaped text segments
+    (200 B - 6 KB) alternating with binary segments -- random bytes (incompressible),
+    zero runs, small integer tables -- plus the cases the segmenter's rules act on:
+    control-byte gaps of 1-12 bytes inside text, short printable runs (< 64 B) inside
+    binary, and short binary chunks (< 64 B) next to text."""
+    rng = np.random.default_rng(seed)
+    prose = _alice(max(4 * n_bytes, 20000), seed + 1)
+    out, pos = [], 0
+    while sum(len(x) for x in out) < n_bytes:
+        r = rng.random()
+        if r < 0.45:                                       # text, maybe with small gaps
+            ln = int(rng.integers(200, 6000))
+            t = bytearray(prose[pos:pos + ln])
+            pos = (pos + ln) % (len(prose) - 6000)
+            for _ in range(int(rng.integers(0, 3))):
+                at = int(rng.integers(0, max(1, len(t))))
+                t[at:at] = bytes(rng.integers(0, 9, int(rng.integers(1, 13))).astype(np.uint8))
+            out.append(bytes(t))
+        elif r < 0.65:                                     # random bytes
+            out.append(bytes(rng.integers(0, 256, int(rng.integers(16, 3000))).astype(np.uint8)))
+        elif r < 0.8:                                      # zero runs / small tables
+            n = int(rng.integers(8, 2000))
+            out.append(bytes(n) if rng.random() < 0.5 else
+                       np.arange(n // 4, dtype="<u4").tobytes())
+        else:                                              # binary with short printable runs
+            b = bytearray(rng.integers(128, 256, int(rng.integers(20, 400))).astype(np.uint8))
+            at = int(rng.integers(0, len(b)))
+            b[at:at] = b"header" + bytes(rng.integers(48, 58, int(rng.integers(1, 40))).astype(np.uint8))
+            out.append(bytes(b))
+    return b"".join(out)[:n_bytes]
+
+
 def make_text(kind: str, n_bytes: int, seed: int) -> bytes:
     if kind == "alice":
         return _alice(n_bytes, seed)
     if kind == "enwik":
         return _enwik(n_bytes, seed)
+    if kind == "mixed":
+        return _mixed(n_bytes, seed)
     raise ValueError(kind)
