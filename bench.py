@@ -213,7 +213,7 @@ def main():
     ap.add_argument("--dry-run", action="store_true", help="CPU/gloo launcher + plan check (no GPU)")
     ap.add_argument("--oracle-tokens", type=int, default=192,
                     help="tokens per chunk per --impl reference step (chunk-parallel)")
-    ap.add_argument("--baseline-tokens", type=int, default=512, help="tokens per chunk of the cpu_baseline sample")
+    ap.add_argument("--baseline-tokens", type=int, default=1536, help="tokens per chunk of the cpu_baseline sample")
     ap.add_argument("--decompress-bytes", type=int, default=20000,
                     help="decompress sample: the first B bytes of every chunk of this rank (0 = the whole input)")
     args = ap.parse_args()

@@ -130,6 +130,25 @@ nc_status nc_compress(nc_model *m, const uint8_t *in, size_t n, const nc_params 
 nc_status nc_decompress(nc_model *m, const uint8_t *in, size_t n, const nc_params *p,
                         void *cuda_stream, uint8_t **out, size_t *out_n);
 
+/* NC06 hybrid binary format.
+ * nc_compress_file: any bytes -> NC06.  The input is segmented into alternating text and
+ * binary regions by the paper's four rules (printable ASCII + tab/LF/CR is text-like;
+ * text runs < 64 B demoted; binary gaps <= 8 B between text bridged; binary chunks < 64 B
+ * next to text absorbed; DESIGN D33); the binary regions, concatenated, are compressed
+ * with LZMA (>= 4 KB) or DEFLATE, or stored raw if neither is smaller (D34);
+ * the text regions, concatenated, take the nc_compress path (params->n_chunks chunks).
+ * Layout (little-endian): "NC06" | version u8 = 1 | flags u8 | tau_milli u16 |
+ * entry_count u16 | entry_count x {kind u8 (0 binary, 1 text), length u32} |
+ * method u8 (0 raw, 1 DEFLATE, 2 LZMA) | blob_length u32 | blob | the NC05 text section
+ * from its chunk_count field on.  Regions larger than 4 GB are NC_ERR_INVALID.
+ * nc_decompress_file: NC06 (or a plain NC05 container) -> the original bytes; the same
+ * params rules as nc_decompress.  Errors: NC_ERR_FORMAT / NC_ERR_TRUNCATED for a malformed
+ * container, NC_ERR_INTEGRITY if a section does not decode to its entry lengths. */
+nc_status nc_compress_file(nc_model *m, const uint8_t *in, size_t n, const nc_params *p,
+                           void *cuda_stream, uint8_t **out, size_t *out_n);
+nc_status nc_decompress_file(nc_model *m, const uint8_t *in, size_t n, const nc_params *p,
+                             void *cuda_stream, uint8_t **out, size_t *out_n);
+
 /* Split + tokenize only (host; D28 + D30).  tokens: all chunks' token ids
  * concatenated; chunk_ntok[i]: token count of chunk i (n_chunks_out entries). */
 nc_status nc_tokenize(const nc_model *m, const uint8_t *in, size_t n, uint32_t n_chunks,
@@ -241,6 +260,14 @@ nc_status nc_host_wnc_encode(const uint32_t *cum, const uint32_t *freq, size_t n
 nc_status nc_host_tokenize_vocab(const uint8_t *vocab_blob, const uint32_t *vocab_len, uint32_t V,
                                  uint32_t n_special, const uint8_t *in, size_t n,
                                  uint32_t **tokens, size_t *n_tokens);
+
+/* NC06 host pieces (no device needed): the segmentation (kinds[i] 0 binary / 1 text,
+ * lens[i] bytes, in input order), and the binary blob codec (method as in NC06;
+ * decode checks that the payload decodes to exactly expect_n bytes). */
+nc_status nc_host_segment(const uint8_t *in, size_t n, uint8_t **kinds, uint64_t **lens, size_t *n_regions);
+nc_status nc_host_blob_encode(const uint8_t *in, size_t n, uint8_t *method, uint8_t **out, size_t *out_n);
+nc_status nc_host_blob_decode(uint8_t method, const uint8_t *in, size_t n, size_t expect_n, uint8_t **out,
+                              size_t *out_n);
 
 /* SMs (CTAs of one thread-block cluster) the per-token walk holds per chunk at
  * vocabulary size V with n_chunks chunks in the container or shard (host query, no

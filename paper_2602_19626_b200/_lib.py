@@ -18,7 +18,8 @@ WINDOW_REFRESH, WINDOW_LMAX_M1 = 1, 2          # nc_params.window_variant (NEXT-
 # every symbol declared in include/nc.h (checked by tests/test_abi.py)
 EXPORTS = [
     "nc_params_default", "nc_set_allocator", "nc_model_load", "nc_model_free", "nc_model_info",
-    "nc_compress", "nc_decompress", "nc_tokenize", "nc_compress_tokens", "nc_comm_unique_id",
+    "nc_compress", "nc_decompress", "nc_compress_file", "nc_decompress_file", "nc_tokenize",
+    "nc_host_segment", "nc_host_blob_encode", "nc_host_blob_decode", "nc_compress_tokens", "nc_comm_unique_id",
     "nc_comm_init", "nc_comm_free", "nc_compress_shard", "nc_decompress_shard", "nc_free",
     "nc_last_error", "nc_last_stats", "nc_debug_quantize", "nc_debug_walk", "nc_debug_walk_dump", "nc_debug_forward",
     "nc_host_split", "nc_host_wnc_encode", "nc_host_tokenize_vocab", "nc_host_shard_range", "nc_host_walk_ctas",
@@ -60,6 +61,11 @@ def lib():
             "nc_model_info": (C.c_int, [P, u32p, u32p, u32p]),
             "nc_compress": (C.c_int, [P, P, C.c_size_t, C.POINTER(nc_params), P, pp, szp]),
             "nc_decompress": (C.c_int, [P, P, C.c_size_t, C.POINTER(nc_params), P, pp, szp]),
+            "nc_compress_file": (C.c_int, [P, P, C.c_size_t, C.POINTER(nc_params), P, pp, szp]),
+            "nc_decompress_file": (C.c_int, [P, P, C.c_size_t, C.POINTER(nc_params), P, pp, szp]),
+            "nc_host_segment": (C.c_int, [P, C.c_size_t, pp, pp, szp]),
+            "nc_host_blob_encode": (C.c_int, [P, C.c_size_t, u8p, pp, szp]),
+            "nc_host_blob_decode": (C.c_int, [C.c_uint8, P, C.c_size_t, C.c_size_t, pp, szp]),
             "nc_tokenize": (C.c_int, [P, P, C.c_size_t, C.c_uint32, pp, szp, pp, u32p]),
             "nc_compress_tokens": (C.c_int, [P, P, u32p, C.c_uint32, C.POINTER(nc_params), P, pp, szp]),
             "nc_comm_unique_id": (C.c_int, [u8p]),
@@ -173,6 +179,39 @@ def nc_compress(model: Model, data: bytes, params: nc_params, stream=None) -> by
 def nc_decompress(model: Model, blob: bytes, params: nc_params, stream=None) -> bytes:
     out, n = C.c_void_p(), C.c_size_t()
     _check(lib().nc_decompress(model.h, blob, len(blob), C.byref(params), stream, C.byref(out), C.byref(n)))
+    return _take_bytes(out.value, n.value)
+
+
+def nc_compress_file(model: Model, data: bytes, params: nc_params, stream=None) -> bytes:
+    """any bytes -> NC06 (hybrid text / binary, NEXT-3)."""
+    out, n = C.c_void_p(), C.c_size_t()
+    _check(lib().nc_compress_file(model.h, data, len(data), C.byref(params), stream, C.byref(out), C.byref(n)))
+    return _take_bytes(out.value, n.value)
+
+
+def nc_decompress_file(model: Model, blob: bytes, params: nc_params, stream=None) -> bytes:
+    out, n = C.c_void_p(), C.c_size_t()
+    _check(lib().nc_decompress_file(model.h, blob, len(blob), C.byref(params), stream, C.byref(out), C.byref(n)))
+    return _take_bytes(out.value, n.value)
+
+
+def nc_host_segment(data: bytes):
+    k, l_, n = C.c_void_p(), C.c_void_p(), C.c_size_t()
+    _check(lib().nc_host_segment(data, len(data), C.byref(k), C.byref(l_), C.byref(n)))
+    kinds = _take_array(k.value, n.value, np.uint8)
+    lens = _take_array(l_.value, n.value, np.uint64)
+    return [(int(a), int(b)) for a, b in zip(kinds, lens)]
+
+
+def nc_host_blob_encode(data: bytes):
+    m, out, n = C.c_uint8(), C.c_void_p(), C.c_size_t()
+    _check(lib().nc_host_blob_encode(data, len(data), C.byref(m), C.byref(out), C.byref(n)))
+    return m.value, _take_bytes(out.value, n.value)
+
+
+def nc_host_blob_decode(method: int, payload: bytes, expect_n: int):
+    out, n = C.c_void_p(), C.c_size_t()
+    _check(lib().nc_host_blob_decode(method, payload, len(payload), expect_n, C.byref(out), C.byref(n)))
     return _take_bytes(out.value, n.value)
 
 

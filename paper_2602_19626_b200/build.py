@@ -16,7 +16,7 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", 
          "--expt-relaxed-constexpr", f"-I{PKG.parent / 'include'}"]
 # diagnostics builds only (e.g. NC_NVCC_EXTRA=-DNC_ATT_TIMING); a change of flags rebuilds everything
 EXTRA = os.environ.get("NC_NVCC_EXTRA", "").split()
-SOURCES = ["host_runtime.cpp", "api.cpp", "comm.cpp", "engine.cu", "k_embed_rms.cu", "k_walk.cu",
+SOURCES = ["host_runtime.cpp", "host_nc06.cpp", "api.cpp", "comm.cpp", "engine.cu", "k_embed_rms.cu", "k_walk.cu",
            "k_gemm_tc.cu", "k_attn_tc.cu"]
 
 
@@ -52,7 +52,7 @@ def build(verbose: bool = False) -> Path:
     stamp.write_text(" ".join(EXTRA))
     objs = [str(BUILD / (s + ".o")) for s in SOURCES]
     if done or not LIB.exists() or any(Path(o).stat().st_mtime > LIB.stat().st_mtime for o in objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", str(LIB), *objs, "-ldl", "-lpthread"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", str(LIB), *objs, "-ldl", "-lpthread", "-lz"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")

@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "engine.hpp"
+#include "nc06.hpp"
 
 namespace {
 thread_local std::string g_err;
@@ -190,6 +191,41 @@ nc_status nc_compress_tokens(nc_model *m, const uint32_t *tokens_dev, const uint
   });
 }
 
+}  // extern "C"
+
+namespace {
+// the NC05 text path shared by nc_compress and the NC06 text section
+void compress_nc05(nc_model *m, const uint8_t *in, size_t n, const nc::Params &q, cudaStream_t s,
+                   std::vector<uint8_t> &blob) {
+  std::vector<uint32_t> tokens, ntok;
+  tokenize_all(m, in, n, effective_chunks(q, 1), tokens, ntok);
+  NC_CUDA(cudaSetDevice(m->device));
+  uint32_t *tok_d = static_cast<uint32_t *>(nc::dev_alloc(tokens.size() * 4 + 4, s));
+  try {
+    if (!tokens.empty()) NC_CUDA(cudaMemcpyAsync(tok_d, tokens.data(), tokens.size() * 4, cudaMemcpyHostToDevice, s));
+    nc::CompressOut co;
+    nc::compress_device(m, tok_d, ntok, q, s, co);
+    nc::dev_free(tok_d, s);
+    tok_d = nullptr;
+    nc::encode_container(q, ntok, co, blob);
+  } catch (...) {
+    if (tok_d) nc::dev_free(tok_d, s);
+    throw;
+  }
+}
+void decompress_nc05(nc_model *m, const uint8_t *in, size_t n, nc::Params q, cudaStream_t s, std::string &text) {
+  nc::Nc05View view = nc::read_nc05(in, n);
+  q.flags = view.flags;
+  q.tau_milli = view.tau_milli;
+  q.inv_tau = 1000.0 / view.tau_milli;
+  std::vector<std::vector<uint32_t>> toks;
+  nc::decompress_device(m, in, view, q, s, toks);
+  for (auto &t : toks) m->tok.decode(t.data(), t.size(), text);
+}
+}  // namespace
+
+extern "C" {
+
 nc_status nc_compress(nc_model *m, const uint8_t *in, size_t n, const nc_params *p, void *cuda_stream,
                       uint8_t **out, size_t *out_n) {
   if (!m || (!in && n) || !out || !out_n) return set_err(NC_ERR_INVALID, "null argument");
@@ -198,26 +234,10 @@ nc_status nc_compress(nc_model *m, const uint8_t *in, size_t n, const nc_params 
   return guard([&] {
     require_device();
     nc::Params q = nc::validate(p);
-    std::vector<uint32_t> tokens, ntok;
-    tokenize_all(m, in, n, effective_chunks(q, 1), tokens, ntok);
-    cudaStream_t s = (cudaStream_t)cuda_stream;
-    NC_CUDA(cudaSetDevice(m->device));
-    uint32_t *tok_d = static_cast<uint32_t *>(nc::dev_alloc(tokens.size() * 4 + 4, s));
-    try {
-      if (!tokens.empty())
-        NC_CUDA(cudaMemcpyAsync(tok_d, tokens.data(), tokens.size() * 4, cudaMemcpyHostToDevice, s));
-      nc::CompressOut co;
-      nc::compress_device(m, tok_d, ntok, q, s, co);
-      nc::dev_free(tok_d, s);
-      tok_d = nullptr;
-      std::vector<uint8_t> blob;
-      nc::encode_container(q, ntok, co, blob);
-      *out = dup_out(blob);
-      *out_n = blob.size();
-    } catch (...) {
-      if (tok_d) nc::dev_free(tok_d, s);
-      throw;
-    }
+    std::vector<uint8_t> blob;
+    compress_nc05(m, in, n, q, (cudaStream_t)cuda_stream, blob);
+    *out = dup_out(blob);
+    *out_n = blob.size();
   });
 }
 
@@ -229,15 +249,142 @@ nc_status nc_decompress(nc_model *m, const uint8_t *in, size_t n, const nc_param
   return guard([&] {
     require_device();
     nc::Params q = nc::validate(p);
-    nc::Nc05View view = nc::read_nc05(in, n);
-    q.flags = view.flags;
-    q.tau_milli = view.tau_milli;
-    q.inv_tau = 1000.0 / view.tau_milli;
-    std::vector<std::vector<uint32_t>> toks;
-    nc::decompress_device(m, in, view, q, (cudaStream_t)cuda_stream, toks);
     std::string text;
-    for (auto &t : toks) m->tok.decode(t.data(), t.size(), text);
+    decompress_nc05(m, in, n, q, (cudaStream_t)cuda_stream, text);
     std::vector<uint8_t> o(text.begin(), text.end());
+    *out = dup_out(o);
+    *out_n = o.size();
+  });
+}
+
+nc_status nc_compress_file(nc_model *m, const uint8_t *in, size_t n, const nc_params *p, void *cuda_stream,
+                           uint8_t **out, size_t *out_n) {
+  if (!m || (!in && n) || !out || !out_n) return set_err(NC_ERR_INVALID, "null argument");
+  *out = nullptr; *out_n = 0;
+  nc::stats() = nc::Stats{};
+  return guard([&] {
+    require_device();
+    nc::Params q = nc::validate(p);
+    std::vector<nc::Region> regs = nc::segment(in, n);
+    if (regs.size() > 0xFFFF) regs.assign(1, nc::Region{nc::kBinary, (uint64_t)n});   // D34
+    std::vector<uint8_t> text, binary;
+    size_t off = 0;
+    for (const nc::Region &r : regs) {
+      (r.kind == nc::kText ? text : binary).insert((r.kind == nc::kText ? text : binary).end(), in + off,
+                                                   in + off + r.len);
+      off += r.len;
+    }
+    // the binary blob codec (host) runs beside the GPU text path
+    std::vector<uint8_t> payload;
+    uint8_t method = nc::kRaw;
+    std::string err;
+    std::thread codec([&] {
+      try {
+        method = nc::blob_encode(binary.data(), binary.size(), payload);
+      } catch (std::exception &e) { err = e.what(); }
+    });
+    std::vector<uint8_t> t05;
+    try {
+      compress_nc05(m, text.data(), text.size(), q, (cudaStream_t)cuda_stream, t05);
+    } catch (...) {
+      codec.join();
+      throw;
+    }
+    codec.join();
+    if (!err.empty()) nc::fail(NC_ERR_BACKEND, err);
+    std::vector<uint8_t> blob;
+    nc::write_nc06((uint8_t)q.flags, (uint16_t)q.tau_milli, regs, method, payload, t05.data(), t05.size(), blob);
+    *out = dup_out(blob);
+    *out_n = blob.size();
+  });
+}
+
+nc_status nc_decompress_file(nc_model *m, const uint8_t *in, size_t n, const nc_params *p, void *cuda_stream,
+                             uint8_t **out, size_t *out_n) {
+  if (!m || (!in && n) || !out || !out_n) return set_err(NC_ERR_INVALID, "null argument");
+  *out = nullptr; *out_n = 0;
+  nc::stats() = nc::Stats{};
+  return guard([&] {
+    require_device();
+    nc::Params q = nc::validate(p);
+    if (n >= 4 && std::memcmp(in, "NC05", 4) == 0) {   // a plain text container
+      std::string text;
+      decompress_nc05(m, in, n, q, (cudaStream_t)cuda_stream, text);
+      std::vector<uint8_t> o(text.begin(), text.end());
+      *out = dup_out(o);
+      *out_n = o.size();
+      return;
+    }
+    nc::Nc06View v = nc::read_nc06(in, n);
+    std::vector<uint8_t> t05{'N', 'C', '0', '5', v.flags, (uint8_t)(v.tau_milli & 255), (uint8_t)(v.tau_milli >> 8)};
+    t05.insert(t05.end(), in + v.text_off, in + n);
+    std::vector<uint8_t> binary;
+    std::string err;
+    std::thread codec([&] {
+      try {
+        nc::blob_decode(v.method, in + v.payload_off, v.payload_len, v.bin_len, binary);
+      } catch (nc::Error &e) { err = e.what(); }
+        catch (std::exception &e) { err = e.what(); }
+    });
+    std::string text;
+    try {
+      decompress_nc05(m, t05.data(), t05.size(), q, (cudaStream_t)cuda_stream, text);
+    } catch (...) {
+      codec.join();
+      throw;
+    }
+    codec.join();
+    if (!err.empty()) nc::fail(NC_ERR_INTEGRITY, err);
+    if (text.size() != v.text_len) nc::fail(NC_ERR_INTEGRITY, "NC06 text entries do not match the decoded text");
+    std::vector<uint8_t> o;
+    o.reserve(v.text_len + v.bin_len);
+    size_t ti = 0, bi = 0;
+    for (const nc::Region &r : v.regs) {
+      if (r.kind == nc::kText) {
+        o.insert(o.end(), text.begin() + ti, text.begin() + ti + r.len);
+        ti += r.len;
+      } else {
+        o.insert(o.end(), binary.begin() + bi, binary.begin() + bi + r.len);
+        bi += r.len;
+      }
+    }
+    *out = dup_out(o);
+    *out_n = o.size();
+  });
+}
+
+nc_status nc_host_segment(const uint8_t *in, size_t n, uint8_t **kinds, uint64_t **lens, size_t *n_regions) {
+  if ((!in && n) || !kinds || !lens || !n_regions) return set_err(NC_ERR_INVALID, "null argument");
+  *kinds = nullptr; *lens = nullptr; *n_regions = 0;
+  return guard([&] {
+    std::vector<nc::Region> r = nc::segment(in, n);
+    std::vector<uint8_t> k;
+    std::vector<uint64_t> l;
+    for (auto &x : r) { k.push_back(x.kind); l.push_back(x.len); }
+    *kinds = dup_out(k);
+    *lens = dup_out(l);
+    *n_regions = r.size();
+  });
+}
+
+nc_status nc_host_blob_encode(const uint8_t *in, size_t n, uint8_t *method, uint8_t **out, size_t *out_n) {
+  if ((!in && n) || !method || !out || !out_n) return set_err(NC_ERR_INVALID, "null argument");
+  *out = nullptr; *out_n = 0;
+  return guard([&] {
+    std::vector<uint8_t> o;
+    *method = nc::blob_encode(in, n, o);
+    *out = dup_out(o);
+    *out_n = o.size();
+  });
+}
+
+nc_status nc_host_blob_decode(uint8_t method, const uint8_t *in, size_t n, size_t expect_n, uint8_t **out,
+                              size_t *out_n) {
+  if ((!in && n) || !out || !out_n) return set_err(NC_ERR_INVALID, "null argument");
+  *out = nullptr; *out_n = 0;
+  return guard([&] {
+    std::vector<uint8_t> o;
+    nc::blob_decode(method, in, n, expect_n, o);
     *out = dup_out(o);
     *out_n = o.size();
   });

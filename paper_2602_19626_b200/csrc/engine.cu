@@ -1222,7 +1222,7 @@ void debug_attention(int device, const float *q, const float *k, const float *v,
   float *oh = bag.get<float>((size_t)rows * qd), *ol = bag.get<float>((size_t)rows * qd);
   const int TR = 128;
   std::vector<AttnTile> tiles;
-  for (uint32_t p0 = 0; p0 < n; p0 += TR) tiles.push_back(AttnTile{0, (int)p0, (int)std::min<uint32_t>(TR, n - p0), (int)p0});
+  for (uint32_t p0 = 0; p0 < n; p0 += TR) tiles.push_back(AttnTile{0, (int)p0, (int)std::min<uint32_t>(TR, n - p0), (int)p0, -1});
   AttnTile *t_d = bag.upload(tiles);
   if (mode == 0) {
     float *qh = bag.get<float>(rows * qd), *ql = bag.get<float>(rows * qd);

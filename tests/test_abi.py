@@ -101,3 +101,42 @@ def test_params_default():
     assert (p.cdf_bits, p.flags, p.window, p.slide, p.warmup, p.ngram_orders, p.ngram_cap) == \
         (24, 3, 2048, 512, 100, 4, 500000)
     assert p.alpha == 1e-3 and p.eta == 1.0 and p.temperature == 1.0
+
+
+# ------------------------------------------------------------------ NC06 host ---
+def test_host_segment_equals_oracle():
+    """the C++ segmenter (NC06 rules 1-4) is bit-identical with the oracle's on
+    mixed files and on random short inputs"""
+    from oracle import nc06
+    from synth import make_text
+    for seed in range(4):
+        data = make_text("mixed", 40000, 900 + seed)
+        assert nc.nc_host_segment(data) == nc06.segment(data)
+    rng = np.random.default_rng(5)
+    for _ in range(300):
+        d = bytes(rng.choice([0, 1, 9, 65, 97, 200], int(rng.integers(0, 300))).astype(np.uint8))
+        assert nc.nc_host_segment(d) == nc06.segment(d)
+    assert nc.nc_host_segment(b"") == []
+
+
+def test_host_blob_codec_interoperates_with_oracle():
+    """C++ blob codec vs the oracle's (Python lzma / zlib): same method choice, the same
+    DEFLATE / raw bytes (the .xz framing of liblzma's buffer encoder differs from Python's
+    stream encoder by a few header bytes), and each decodes the other's payload."""
+    from oracle import nc06
+    rng = np.random.default_rng(6)
+    cases = [b"", bytes(8192), bytes(rng.integers(0, 256, 100).astype(np.uint8)), b"\x00\x01" * 500,
+             bytes(rng.integers(0, 4, 20000).astype(np.uint8)), bytes(rng.integers(0, 256, 5000).astype(np.uint8))]
+    for blob in cases:
+        m, c = nc.nc_host_blob_encode(blob)
+        mo, co = nc06.blob_encode(blob)
+        assert m == mo, (len(blob), m, mo)
+        if m != 2:
+            assert c == co
+        else:
+            assert abs(len(c) - len(co)) <= 16
+        assert nc.nc_host_blob_decode(mo, co, len(blob)) == blob
+        assert nc06.blob_decode(m, c) == blob
+    with pytest.raises(nc.NcError) as ei:
+        nc.nc_host_blob_decode(1, b"\x78\x9c garbage", 10)
+    assert ei.value.status == nc._lib.NC_ERR_INTEGRITY

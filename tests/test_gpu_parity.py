@@ -649,7 +649,64 @@ def test_window_variants_roundtrip_size_and_p(nc, m2, w2, wv, name, n_chunks):
         assert (np.abs(p_gpu - p_ref) / p_ref).max() < P_TOL
     assert abs(len(blob) - size) <= 0.005 * size, (len(blob), size)
     if n_chunks == 1:
-        other = nc.nc_params_default(window=512, slide=128, n_chunks=n_chunks, window_variant=wv ^ 1)
+        # with the N-gram on, random-init weights leave the LLM a negligible mixer weight after
+        # ~150 tokens, so a wrong variant can still decode; with the head alone (flags = 2)
+        # p = p~ depends on the LLM everywhere, and decoding with the other variant must fail
+        hp = nc.nc_params_default(window=512, slide=128, n_chunks=1, window_variant=wv, flags=2)
+        hblob = nc.nc_compress(m2, data, hp)
+        assert nc.nc_decompress(m2, hblob, hp) == data
+        other = nc.nc_params_default(window=512, slide=128, n_chunks=1, window_variant=wv ^ 1, flags=2)
         with pytest.raises(nc.NcError) as ei:
-            nc.nc_decompress(m2, blob, other)
+            nc.nc_decompress(m2, hblob, other)
         assert ei.value.status == nc._lib.NC_ERR_INTEGRITY
+
+
+# ------------------------------------------------------------- NEXT-3: NC06 ---
+def test_nc06_roundtrip_and_oracle_sections(nc, m2, w2):
+    """NC06 hybrid files through the C ABI: round trip of a mixed text / binary
+    file; the container parses with the oracle's reader, its entry table equals the oracle
+    segmentation (rules 1-4), its binary section decodes (Python lzma / zlib) to the
+    oracle's binary blob with the oracle's method choice, and its text section is within
+    0.5 % of the oracle's NC05 size for the same text document with p(t) within 1e-4."""
+    from oracle import nc06
+    from oracle.ensemble import Params
+    from synth import make_text
+    data = make_text("mixed", 30000, 77)
+    prm = nc.nc_params_default(window=512, slide=128, n_chunks=3)
+    blob = nc.nc_compress_file(m2, data, prm)
+    assert nc.nc_decompress_file(m2, blob, prm) == data
+    flags, tau, regs, method, payload, chunks = nc06.read_nc06(blob)
+    assert regs == nc06.segment(data) and len(regs) > 4
+    text, binary = nc06.split(data, regs)
+    assert method == nc06.blob_encode(binary)[0] and nc06.blob_decode(method, payload) == binary
+    size, ps, xs, ts = _oracle_size_and_p(w2, text, Params(window=512, slide=128, n_chunks=3))
+    text_section = 2 + sum(12 + len(s) for _, _, s in chunks)
+    assert abs(text_section - (size - 7)) <= 0.005 * size, (text_section, size)
+    assert [n for n, _, _ in chunks] == [len(t) for t in ts]
+    for x, t, p_ref in zip(xs, ts, ps):
+        z = nc.nc_debug_forward(m2, x, prm, 0)
+        _, _, p_gpu = nc.nc_debug_walk(z, t, prm)
+        assert (np.abs(p_gpu - p_ref) / p_ref).max() < P_TOL
+    # a corrupted binary section is an integrity error, never silent output
+    off = 10 + 5 * len(regs) + 5
+    bad = bytearray(blob)
+    bad[off + len(payload) // 2] ^= 0x10
+    with pytest.raises(nc.NcError) as ei:
+        nc.nc_decompress_file(m2, bytes(bad), prm)
+    assert ei.value.status == nc._lib.NC_ERR_INTEGRITY
+
+
+def test_nc06_edge_inputs(nc, m2):
+    """pure binary (one binary entry, no text tokens), pure text, empty input; and a plain
+    NC05 container is accepted by nc_decompress_file."""
+    from oracle import nc06
+    from synth import make_text
+    prm = nc.nc_params_default(window=256, slide=128, n_chunks=2)
+    rnd = bytes(np.random.default_rng(3).integers(128, 256, 5000).astype(np.uint8))
+    for data in (rnd, make_text("alice", 3000, 8), b"", b"\x00" * 10000, rnd[:40]):
+        blob = nc.nc_compress_file(m2, data, prm)
+        assert nc.nc_decompress_file(m2, blob, prm) == data
+        regs = nc06.read_nc06(blob)[2]
+        assert sum(ln for _, ln in regs) == len(data)
+    blob5 = nc.nc_compress(m2, b"hello NC05\n" * 40, prm)
+    assert nc.nc_decompress_file(m2, blob5, prm) == b"hello NC05\n" * 40
