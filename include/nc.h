@@ -107,6 +107,17 @@ nc_status nc_set_allocator(void *(*alloc)(size_t bytes, void *ctx),
  * (RMSNorm gains folded into the following projection). */
 nc_status nc_model_load(const char *path, int device, nc_model **out);
 void nc_model_free(nc_model *m);
+
+/* Load an HF-format SmolLM2 checkpoint directory:
+ * model_dir/config.json (LlamaConfig: hidden_size, num_hidden_layers, num_attention_heads,
+ * num_key_value_heads, head_dim, intermediate_size, vocab_size, rms_norm_eps, rope_theta /
+ * rope_parameters, bos_token_id; tie_word_embeddings must be true, default RoPE only),
+ * model_dir/model.safetensors (HF Llama tensor names, F32 / F16 / BF16, converted to fp32)
+ * and model_dir/tokenizer.json (byte-level BPE behind ByteLevel or Digits + ByteLevel
+ * pre-tokenization; the model then tokenizes with it instead of the greedy synthetic-vocab
+ * matcher, D35-D36).  Errors: NC_ERR_INVALID for unsupported configurations, NC_ERR_FORMAT
+ * for malformed files. */
+nc_status nc_model_load_hf(const char *model_dir, int device, nc_model **out);
 /* vocab size, n_layers, d_model of a loaded model (any may be NULL). */
 nc_status nc_model_info(const nc_model *m, uint32_t *vocab, uint32_t *n_layers,
                         uint32_t *d_model);
@@ -268,6 +279,11 @@ nc_status nc_host_segment(const uint8_t *in, size_t n, uint8_t **kinds, uint64_t
 nc_status nc_host_blob_encode(const uint8_t *in, size_t n, uint8_t *method, uint8_t **out, size_t *out_n);
 nc_status nc_host_blob_decode(uint8_t method, const uint8_t *in, size_t n, size_t expect_n, uint8_t **out,
                               size_t *out_n);
+
+/* The byte-level BPE of a tokenizer.json on host bytes (no device; tests compare it with the
+ * HF tokenizers library).  vocab: the model's vocabulary size (ids must be below it). */
+nc_status nc_host_bpe_encode(const char *tokenizer_json_path, uint32_t vocab, const uint8_t *in, size_t n,
+                             uint32_t **tokens, size_t *n_tokens);
 
 /* SMs (CTAs of one thread-block cluster) the per-token walk holds per chunk at
  * vocabulary size V with n_chunks chunks in the container or shard (host query, no

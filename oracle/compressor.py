@@ -18,8 +18,13 @@ from .lm import LM
 from .tokenizer import Tokenizer
 
 
+def _tokenizer(weights):
+    """the model's own tokenizer (HF checkpoints, oracle/hf.py) or the synthetic greedy one (D30)"""
+    return getattr(weights, "tokenizer", None) or Tokenizer(weights.vocab, weights.n_special)
+
+
 def compress(data: bytes, weights, prm: Params, lm_mode="blocked", collect=None):
-    tok = Tokenizer(weights.vocab, weights.n_special)
+    tok = _tokenizer(weights)
     lm = LM(weights)
     entries = []
     for ch in split_chunks(data, prm.n_chunks):
@@ -43,7 +48,7 @@ def compress(data: bytes, weights, prm: Params, lm_mode="blocked", collect=None)
 def decompress(blob: bytes, weights, prm: Params):
     flags, tau_milli, chunks = read_nc05(blob)
     prm = Params(**{**prm.__dict__, "flags": flags, "temperature": tau_milli / 1000.0})
-    tok = Tokenizer(weights.vocab, weights.n_special)
+    tok = _tokenizer(weights)
     lm = LM(weights)
     out = []
     for n, bits, stream in chunks:

@@ -17,7 +17,8 @@ WINDOW_REFRESH, WINDOW_LMAX_M1 = 1, 2          # nc_params.window_variant (NEXT-
 
 # every symbol declared in include/nc.h (checked by tests/test_abi.py)
 EXPORTS = [
-    "nc_params_default", "nc_set_allocator", "nc_model_load", "nc_model_free", "nc_model_info",
+    "nc_params_default", "nc_set_allocator", "nc_model_load", "nc_model_load_hf", "nc_model_free",
+    "nc_host_bpe_encode", "nc_model_info",
     "nc_compress", "nc_decompress", "nc_compress_file", "nc_decompress_file", "nc_tokenize",
     "nc_host_segment", "nc_host_blob_encode", "nc_host_blob_decode", "nc_compress_tokens", "nc_comm_unique_id",
     "nc_comm_init", "nc_comm_free", "nc_compress_shard", "nc_decompress_shard", "nc_free",
@@ -58,6 +59,8 @@ def lib():
             "nc_params_default": (None, [C.POINTER(nc_params)]),
             "nc_model_load": (C.c_int, [C.c_char_p, C.c_int, pp]),
             "nc_model_free": (None, [P]),
+            "nc_model_load_hf": (C.c_int, [C.c_char_p, C.c_int, pp]),
+            "nc_host_bpe_encode": (C.c_int, [C.c_char_p, C.c_uint32, P, C.c_size_t, pp, szp]),
             "nc_model_info": (C.c_int, [P, u32p, u32p, u32p]),
             "nc_compress": (C.c_int, [P, P, C.c_size_t, C.POINTER(nc_params), P, pp, szp]),
             "nc_decompress": (C.c_int, [P, P, C.c_size_t, C.POINTER(nc_params), P, pp, szp]),
@@ -151,8 +154,13 @@ class Model:
     """A loaded NCW1 model on one device (nc_model_load / nc_model_free)."""
 
     def __init__(self, path, device=0):
+        """path: an NCW1 file, or an HF checkpoint directory (config.json, model.safetensors,
+        tokenizer.json; nc_model_load_hf)."""
         h = C.c_void_p()
-        _check(lib().nc_model_load(str(path).encode(), int(device), C.byref(h)))
+        if os.path.isdir(str(path)):
+            _check(lib().nc_model_load_hf(str(path).encode(), int(device), C.byref(h)))
+        else:
+            _check(lib().nc_model_load(str(path).encode(), int(device), C.byref(h)))
         self.h = h
         V, L, d = C.c_uint32(), C.c_uint32(), C.c_uint32()
         _check(lib().nc_model_info(h, C.byref(V), C.byref(L), C.byref(d)))
@@ -349,6 +357,12 @@ def nc_host_tokenize_vocab(vocab, data: bytes, n_special: int = 3):
     lens, lp = _u32([len(v) for v in vocab])
     t, nt = C.c_void_p(), C.c_size_t()
     _check(lib().nc_host_tokenize_vocab(blob, lp, len(vocab), n_special, data, len(data), C.byref(t), C.byref(nt)))
+    return _take_array(t.value, nt.value, np.uint32).tolist()
+
+
+def nc_host_bpe_encode(tokenizer_json, vocab: int, data: bytes):
+    t, nt = C.c_void_p(), C.c_size_t()
+    _check(lib().nc_host_bpe_encode(str(tokenizer_json).encode(), vocab, data, len(data), C.byref(t), C.byref(nt)))
     return _take_array(t.value, nt.value, np.uint32).tolist()
 
 

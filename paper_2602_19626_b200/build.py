@@ -16,14 +16,15 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", 
          "--expt-relaxed-constexpr", f"-I{PKG.parent / 'include'}"]
 # diagnostics builds only (e.g. NC_NVCC_EXTRA=-DNC_ATT_TIMING); a change of flags rebuilds everything
 EXTRA = os.environ.get("NC_NVCC_EXTRA", "").split()
-SOURCES = ["host_runtime.cpp", "host_nc06.cpp", "api.cpp", "comm.cpp", "engine.cu", "k_embed_rms.cu", "k_walk.cu",
+SOURCES = ["host_runtime.cpp", "host_nc06.cpp", "hf_loader.cpp", "api.cpp", "comm.cpp", "engine.cu", "k_embed_rms.cu", "k_walk.cu",
            "k_gemm_tc.cu", "k_attn_tc.cu"]
 
 
 def _stale(obj: Path, src: Path) -> bool:
     if not obj.exists() or _flags_changed:
         return True
-    deps = [src] + list(CSRC.glob("*.hpp")) + list(CSRC.glob("*.cuh")) + [PKG.parent / "include" / "nc.h"]
+    deps = [src] + list(CSRC.glob("*.hpp")) + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.inc")) + \
+        [PKG.parent / "include" / "nc.h"]
     return any(d.stat().st_mtime > obj.stat().st_mtime for d in deps)
 
 

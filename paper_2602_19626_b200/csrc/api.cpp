@@ -6,6 +6,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <fstream>
+#include <iterator>
 #include <string>
 #include <thread>
 #include <vector>
@@ -108,6 +110,42 @@ void nc_model_free(nc_model *m) {
   delete m;
 }
 
+nc_status nc_model_load_hf(const char *model_dir, int device, nc_model **out) {
+  if (!model_dir || !out) return set_err(NC_ERR_INVALID, "null argument");
+  *out = nullptr;
+  nc_model *m = new nc_model();
+  nc_status st = guard([&] {
+    require_device();
+    nc::model_load_hf(m, model_dir, device);
+  });
+  if (st != NC_OK) {
+    nc::model_free(m);
+    delete m;
+    return st;
+  }
+  *out = m;
+  return NC_OK;
+}
+
+nc_status nc_host_bpe_encode(const char *tokenizer_json_path, uint32_t vocab, const uint8_t *in, size_t n,
+                             uint32_t **tokens, size_t *n_tokens) {
+  if (!tokenizer_json_path || (!in && n) || !tokens || !n_tokens) return set_err(NC_ERR_INVALID, "null argument");
+  *tokens = nullptr; *n_tokens = 0;
+  return guard([&] {
+    std::ifstream is(tokenizer_json_path, std::ios::binary);
+    if (!is) nc::fail(NC_ERR_INVALID, std::string("cannot open ") + tokenizer_json_path);
+    std::string js((std::istreambuf_iterator<char>(is)), std::istreambuf_iterator<char>());
+    nc::BpeTokenizer t;
+    std::vector<std::string> vb;
+    uint32_t ns = 0;
+    t.build(js, vocab, vb, ns);
+    std::vector<uint32_t> o;
+    t.encode(in, n, o);
+    *tokens = dup_out(o);
+    *n_tokens = o.size();
+  });
+}
+
 nc_status nc_model_info(const nc_model *m, uint32_t *vocab, uint32_t *n_layers, uint32_t *d_model) {
   if (!m) return set_err(NC_ERR_INVALID, "null model");
   if (vocab) *vocab = m->s.V;
@@ -124,7 +162,7 @@ static void tokenize_all(const nc_model *m, const uint8_t *in, size_t n, uint32_
   std::vector<std::vector<uint32_t>> per(nc_);
   const unsigned nt = std::max(1u, std::min<unsigned>((unsigned)nc_, std::thread::hardware_concurrency()));
   auto work = [&](unsigned t) {
-    for (size_t c = t; c < nc_; c += nt) m->tok.encode(in + cuts[c], cuts[c + 1] - cuts[c], per[c]);
+    for (size_t c = t; c < nc_; c += nt) m->encode(in + cuts[c], cuts[c + 1] - cuts[c], per[c]);
   };
   if (nt <= 1 || n < (1u << 16)) {
     work(0);

@@ -188,7 +188,7 @@ nc_status nc_compress_shard(nc_model *m, nc_comm *c, const uint8_t *in, size_t n
     std::vector<uint32_t> tokens, ntok;
     for (uint32_t k = c0; k < c1; ++k) {
       size_t before = tokens.size();
-      m->tok.encode(in + cuts[k], cuts[k + 1] - cuts[k], tokens);
+      m->encode(in + cuts[k], cuts[k + 1] - cuts[k], tokens);
       ntok.push_back((uint32_t)(tokens.size() - before));
     }
     std::vector<uint8_t> mine_blob;

@@ -215,6 +215,15 @@ void check_tokens_device(nc_model *m, const uint32_t *tokens_dev, size_t n, cuda
 // ------------------------------------------------------------------ model ---
 void model_load(nc_model *m, const std::string &path, int device) {
   NcwFile f = read_ncw(path);
+  model_setup(m, f, device);
+}
+
+void model_load_hf(nc_model *m, const std::string &dir, int device) {
+  NcwFile f = read_hf(dir, m->bpe);
+  model_setup(m, f, device);
+}
+
+void model_setup(nc_model *m, const NcwFile &f, int device) {
   const Shape &s = f.s;
   if (s.dh != (uint32_t)kHeadDim) fail(NC_ERR_INVALID, "kernels are specialised to head_dim 64");
   if (s.H % s.KV || s.H / s.KV > 3) fail(NC_ERR_INVALID, "GQA group must be <= 3");

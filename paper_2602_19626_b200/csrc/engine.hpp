@@ -5,6 +5,7 @@
 #include <string>
 #include <vector>
 
+#include "hf.hpp"
 #include "kernels.cuh"
 #include "nc_internal.hpp"
 #include "walk.cuh"
@@ -12,7 +13,13 @@
 struct nc_model {
   int device = 0;
   nc::Shape s{};
-  nc::Tokenizer tok;
+  nc::Tokenizer tok;                                     // greedy longest match over the vocabulary (D30)
+  std::unique_ptr<nc::BpeTokenizer> bpe;                 // HF byte-level BPE (nc_model_load_hf, NEXT-2)
+  // token ids of a byte string with the model's tokenizer (decode is the vocabulary bytes for both)
+  void encode(const uint8_t *in, size_t n, std::vector<uint32_t> &out) const {
+    if (bpe) bpe->encode(in, n, out);
+    else tok.encode(in, n, out);
+  }
   std::vector<std::string> vocab;
   float *E = nullptr;                                    // [V, d] fp32 (embedding gather)
   // tf32 hi/lo planes of every projection for the tcgen05 3xTF32 GEMM (D14); the fp32
@@ -65,6 +72,8 @@ struct Prof {
 Prof &prof();
 
 void model_load(nc_model *m, const std::string &path, int device);
+void model_load_hf(nc_model *m, const std::string &dir, int device);   // config.json + safetensors + tokenizer.json
+void model_setup(nc_model *m, const NcwFile &f, int device);
 void model_free(nc_model *m);
 void ensure_rope(nc_model *m, int64_t max_pos);
 

@@ -190,7 +190,7 @@ def _oracle_size_and_p(w, data, prm_o):
     from oracle.ensemble import encode_tokens
     from oracle.lm import LM
     from oracle.tokenizer import Tokenizer
-    tk, lm = Tokenizer(w.vocab), LM(w)
+    tk, lm = getattr(w, "tokenizer", None) or Tokenizer(w.vocab), LM(w)
     size, ps, xs, ts = 9, [], [], []
     for ch in split_chunks(data, prm_o.n_chunks):
         t = tk.encode(ch)
@@ -710,3 +710,37 @@ def test_nc06_edge_inputs(nc, m2):
         assert sum(ln for _, ln in regs) == len(data)
     blob5 = nc.nc_compress(m2, b"hello NC05\n" * 40, prm)
     assert nc.nc_decompress_file(m2, blob5, prm) == b"hello NC05\n" * 40
+
+
+# ------------------------------------------------- NEXT-2: HF checkpoint + BPE ---
+def test_hf_checkpoint_forward_tokenizer_roundtrip(nc):
+    """An HF-format SmolLM2-shaped checkpoint (config.json + BF16 model.safetensors +
+    tokenizer.json, synth/hf.py) loaded by nc_model_load_hf: the model's BPE tokenization
+    equals the HF tokenizers library's; logits within 1e-5 of max|z| of the oracle's
+    independent safetensors reader + fp64 LM; GPU round trip; size within 0.5 % of the
+    oracle pipeline (tokenizing with the HF library) and p(t) within 1e-4."""
+    from oracle.ensemble import Params
+    from oracle.hf import HfWeights
+    from oracle.lm import LM
+    from synth import make_text
+    from synth.hf import ensure_hf_model
+    d = ensure_hf_model("hf-smollm2-2l")
+    m = nc.Model(d, 0)
+    w = HfWeights(d)
+    data = make_text("enwik", 6000, 1004)
+    toks, ntok = nc.nc_tokenize(m, data, 1)
+    assert toks.tolist() == w.tokenizer.encode(data)
+    x = [w.bos] + toks.tolist()[:-1]
+    prm = nc.nc_params_default(window=512, slide=128, n_chunks=2)
+    z = nc.nc_debug_forward(m, x, prm, 0)
+    ref = LM(w).forward_blocked(x, 512, 128)
+    assert np.abs(z - ref).max() / np.abs(ref).max() < Z_TOL
+    blob = nc.nc_compress(m, data, prm)
+    assert nc.nc_decompress(m, blob, prm) == data
+    size, ps, xs, ts = _oracle_size_and_p(w, data, Params(window=512, slide=128, n_chunks=2))
+    assert abs(len(blob) - size) <= 0.005 * size, (len(blob), size)
+    for x_, t, p_ref in zip(xs, ts, ps):
+        zz = nc.nc_debug_forward(m, x_, prm, 0)
+        _, _, p_gpu = nc.nc_debug_walk(zz, t, prm)
+        assert (np.abs(p_gpu - p_ref) / p_ref).max() < P_TOL
+    m.close()
