@@ -4,25 +4,27 @@
 //   for each 128-key block b of keys [w(j), j] (blocks aligned to absolute positions;
 //   the window start w(j) is a multiple of C >= 128, so no block straddles it):
 //     S_b = Q K_b^T                     tcgen05 kind::tf32, 3 products x 8 k-steps, N = 128 -> TMEM
-//   and independently for each half X of the block's keys (X = keys 0-63 / 64-127):
-//     m_X = max(m_X, rowmax(S_bX / 8)), P_bX = exp(S_bX / 8 - m_X) (masked), l_X updated
-//     O_bX = P_bX V_bX                  tcgen05 kind::tf32 (P from TMEM, V MN-major) -> fresh TMEM partial
-//     O_X <- O_X * exp(m_X,old - m_X) + O_bX      in fp32 RN registers (promotion, see k_gemm_tc.cu)
-//   o = (O_A 2^(m_A - m) + O_B 2^(m_B - m)) / (l_A 2^(m_A - m) + l_B 2^(m_B - m)),  m = max(m_A, m_B)
+//     m  <- max(m, rowmax(S_b / 8))     (the row's two key halves exchange their maxima)
+//     P_b = exp(S_b / 8 - m) (masked), l_X <- l_X alpha + rowsum(P_bX) per key half X
+//     O_b = P_b V_b                     tcgen05 kind::tf32 (P from TMEM, V MN-major), K = 128 keys
+//                                       -> one fresh TMEM partial per block
+//     O  <- O * alpha + O_b             in fp32 RN registers (promotion, see k_gemm_tc.cu)
+//   o = O / (l_A + l_B)
 //
-// The two halves are two exact online softmaxes over disjoint key sets, merged
-// once at the end -- the same arithmetic for every row whatever tile it is in,
-// so decode (tiles of one row) reproduces prefill bit for bit (D15); later,
-// fully masked keys are exact no-ops (alpha = 1, P = 0).
+// Every row's arithmetic is the same whatever tile it is in, so decode (tiles of one row)
+// reproduces prefill bit for bit (D15); later, fully masked keys are exact no-ops
+// (alpha = 1, P = 0).
 //
 // One CTA per (128-row query tile of one chunk, q head); 384 threads:
 //   warp 0  TMA: Q once (hi/lo, 64 KB), then K of each 128-key block (64 KB, one buffer)
 //   warp 3  TMA: V in 64-key granules (32 KB) through a ring of 3
-//   warp 1  MMA issue (whole warp, one elected lane per instruction): S(i), then PV(i-1) of both halves
-//   warp 2  TMEM allocator: S (128 cols) | P_A hi,lo | P_B hi,lo (64 each) | O_A, O_B partials (64 each)
-//   warps 4-7 / 8-11  softmax + promotion of key half A / B, thread = query row (TMEM lane)
-// Measured (tools/micro): an N = 128 tf32 MMA costs 64 cycles, N = 64 costs 48-57, so S runs at
-// full rate; per 128-key block the MMAs take ~4.2k cycles, which the two softmax groups cover.
+//   warp 1  MMA issue (whole warp, one elected lane per instruction): S(i), then PV(i-1)
+//   warp 2  TMEM allocator: S (128 cols) | P_A hi,lo | P_B hi,lo (64 each) | O partial (64)
+//   warps 4-7 / 8-11  softmax of key half A / B and the promotion of output dims 0-31 / 32-63,
+//                     thread = query row (TMEM lane); the halves share the row max (smem)
+// Measured (tools/micro): an N = 128 tf32 MMA costs 64 cycles, N = 64 costs 48-57.  The
+// softmax side is bound by TMEM reads (~64 B/cycle/SM): per block S (64 KB) and the O
+// partial (32 KB; 64 KB when each key half kept its own partial and max).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -51,10 +53,10 @@ constexpr int KV_SUB = AH * 128; // one [64 keys x 32 fp32] sub-tile: 8 KB (TMA 
 constexpr int Q_BYTES = 4 * Q_SUB;               // hi/lo x two 32-dim halves: 64 KB
 constexpr int K_BYTES = 4 * K_SUB;               // hi/lo x two 32-dim halves: 64 KB
 constexpr int V_GRAN = 4 * KV_SUB;               // V hi/lo x two 32-dim halves, 64 keys: 32 KB
-constexpr int ATT_SMEM = Q_BYTES + K_BYTES + VG * V_GRAN + 1024 + 256;
+constexpr int ATT_SMEM = Q_BYTES + K_BYTES + VG * V_GRAN + 1024 + 256 + 2 * 128 * 4;
 constexpr int ATT_THREADS = 384;
 // TMEM columns
-constexpr uint32_t T_S = 0, T_P = 128, T_O = 384;   // P half X at T_P + 128 X (hi, lo +64); O half X at T_O + 64 X
+constexpr uint32_t T_S = 0, T_P = 128, T_O = 384;   // P half X at T_P + 128 X (hi, lo +64); O partial at T_O
 
 #ifdef NC_ATT_TIMING
 // diagnostics build only: per-thread phase cycles accumulated in registers, flushed once per CTA
@@ -120,10 +122,11 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
   uint64_t *q_full = bars, *q_empty = bars + 1, *k_full = bars + 2, *k_empty = bars + 3;
   uint64_t *v_full = bars + 4, *v_empty = v_full + VG;
   uint64_t *s_full = v_empty + VG, *s_empty = s_full + 1;
-  uint64_t *p_full = s_empty + 1, *pv_done = p_full + 2;   // per key half
-  uint64_t *sch_full = pv_done + 2, *sch_empty = sch_full + NSCH;
+  uint64_t *p_full = s_empty + 1, *pv_done = p_full + 1;   // P of both halves stored / PV done
+  uint64_t *sch_full = pv_done + 1, *sch_empty = sch_full + NSCH;
   int *sch_item = reinterpret_cast<int *>(sch_empty + NSCH);
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sch_item + NSCH);
+  float *xmax = reinterpret_cast<float *>(tmem_slot + 4);   // [2 halves][128 rows] row-max / row-sum exchange
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_items = a.n_tiles * a.H;
@@ -134,7 +137,8 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
     tc::mbar_init(k_full, 1); tc::mbar_init(k_empty, 1);
     for (int s = 0; s < VG; ++s) { tc::mbar_init(&v_full[s], 1); tc::mbar_init(&v_empty[s], 1); }
     tc::mbar_init(s_full, 1); tc::mbar_init(s_empty, 8);
-    for (int s = 0; s < 2; ++s) { tc::mbar_init(&p_full[s], 4); tc::mbar_init(&pv_done[s], 1); }
+    tc::mbar_init(p_full, 8);
+    tc::mbar_init(pv_done, 1);
     for (int s = 0; s < NSCH; ++s) { tc::mbar_init(&sch_full[s], 1); tc::mbar_init(&sch_empty[s], SCH_CONSUMERS); }
     tc::fence_barrier_init();
   }
@@ -239,30 +243,39 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
     auto off = [](uint32_t bytes) { return (uint64_t)(bytes >> 4); };   // descriptor address units
     int vst = 0;
     uint32_t vph = 0;
-    auto issue_pv = [&](int b) {                 // O_bX = P_bX V_bX for both key halves (b: global block)
+    auto issue_pv = [&](int b) {                 // O_b = P_b V_b over the block's 128 keys (b: global block)
+      tc::mbar_wait(p_full, b & 1);
+      const int vs0 = vst;
+      tc::mbar_wait(&v_full[vst], vph);
+      if (++vst == VG) { vst = 0; vph ^= 1; }
+      const int vs1 = vst;
+      tc::mbar_wait(&v_full[vst], vph);
+      if (++vst == VG) { vst = 0; vph ^= 1; }
+      tc::fence_after();
+      const uint32_t dO = tmem + T_O;
+      const uint64_t vd[2] = {v_desc0 + off(vs0 * V_GRAN), v_desc0 + off(vs1 * V_GRAN)};
+#pragma unroll
+      for (int x = 0; x < 2; ++x) {                // corrections first, hi*hi last (see k_gemm_tc.cu)
+        const uint32_t ph_t = tmem + T_P + 128 * x, pl_t = ph_t + 64;
+#pragma unroll
+        for (int j = 0; j < AH / 8; ++j) {
+          if (tc::elect_one()) tc::mma_tf32_ts(dO, ph_t + j * 8, vd[x] + off(2 * KV_SUB + j * 1024), idO, (x | j) != 0);
+          if (tc::elect_one()) tc::mma_tf32_ts(dO, pl_t + j * 8, vd[x] + off(j * 1024), idO, 1);
+        }
+      }
 #pragma unroll
       for (int x = 0; x < 2; ++x) {
-        tc::mbar_wait(&p_full[x], b & 1);
-        tc::mbar_wait(&v_full[vst], vph);
-        tc::fence_after();
-        const uint32_t ph_t = tmem + T_P + 128 * x, pl_t = ph_t + 64;
-        const uint64_t vd = v_desc0 + off(vst * V_GRAN);
-        const uint32_t dO = tmem + T_O + 64 * x;
-#pragma unroll
-        for (int j = 0; j < AH / 8; ++j) {          // corrections first, hi*hi last (see k_gemm_tc.cu)
-          if (tc::elect_one()) tc::mma_tf32_ts(dO, ph_t + j * 8, vd + off(2 * KV_SUB + j * 1024), idO, j != 0);
-          if (tc::elect_one()) tc::mma_tf32_ts(dO, pl_t + j * 8, vd + off(j * 1024), idO, 1);
-        }
+        const uint32_t ph_t = tmem + T_P + 128 * x;
 #pragma unroll
         for (int j = 0; j < AH / 8; ++j)
-          if (tc::elect_one()) tc::mma_tf32_ts(dO, ph_t + j * 8, vd + off(j * 1024), idO, 1);
-        if (tc::elect_one()) {
-          tc::mma_commit(&pv_done[x]);             // P_X buffer free + O_X partial ready
-          tc::mma_commit(&v_empty[vst]);
-        }
-        __syncwarp();
-        if (++vst == VG) { vst = 0; vph ^= 1; }
+          if (tc::elect_one()) tc::mma_tf32_ts(dO, ph_t + j * 8, vd[x] + off(j * 1024), idO, 1);
       }
+      if (tc::elect_one()) {
+        tc::mma_commit(pv_done);                   // P buffers free + O partial ready
+        tc::mma_commit(&v_empty[vs0]);
+        tc::mma_commit(&v_empty[vs1]);
+      }
+      __syncwarp();
     };
     int gb = 0, qi = 0;
     AT_DECL;
@@ -319,8 +332,8 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
     }
     AT_FLUSH(0, lane == 0);
   } else if (warp >= 4) {
-    // ------------------------------------------- softmax groups (key halves)
-    const int x = (warp - 4) >> 2;                 // key half of this softmax group
+    // ----------------------------- softmax groups (key halves) + promotion (dim halves)
+    const int x = (warp - 4) >> 2;                 // key half of this softmax group = output dim half
     const int q = warp & 3, r = q * 32 + lane;     // query row of this thread (TMEM lane)
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     // scores in the log2 domain: x = S * (1/8 * log2 e); p = 2^(x - m)
@@ -334,20 +347,16 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
       if (xi.nkb == 0) continue;
       AT_T(6);   // item gap
       const int j = xi.t.p0 + r;
-      float O[64];
+      float O[32];                                 // output dims [32 x, 32 x + 32) of row r
 #pragma unroll
-      for (int d = 0; d < 64; ++d) O[d] = 0.f;
+      for (int d = 0; d < 32; ++d) O[d] = 0.f;
       float m = -CUDART_INF_F, l = 0.f, alpha_prev = 1.f;
       auto fold = [&](float al) {                  // O <- O * alpha + O_partial  (fp32 RN promotion)
-        uint32_t x0[32], x1[32];
-        tc::tmem_ld32(tmem + T_O + 64 * x + lane_off, x0);
-        tc::tmem_ld32(tmem + T_O + 64 * x + lane_off + 32, x1);
+        uint32_t x0[32];
+        tc::tmem_ld32(tmem + T_O + 32 * x + lane_off, x0);
         tc::tmem_wait_ld();
 #pragma unroll
-        for (int d = 0; d < 32; ++d) {
-          O[d] = __fmaf_rn(O[d], al, __uint_as_float(x0[d]));
-          O[32 + d] = __fmaf_rn(O[32 + d], al, __uint_as_float(x1[d]));
-        }
+        for (int d = 0; d < 32; ++d) O[d] = __fmaf_rn(O[d], al, __uint_as_float(x0[d]));
       };
       for (int i = 0; i < xi.nkb; ++i, ++gb) {
         tc::mbar_wait(s_full, gb & 1);
@@ -382,7 +391,11 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
         for (int w2 = 16; w2 >= 1; w2 >>= 1)
 #pragma unroll
           for (int k = 0; k < w2; ++k) tt[k] = fmaxf(tt[k], tt[k + w2]);
-        const float mb = __fmul_rn(tt[0], kScale);
+        // the row's two halves exchange their maxima
+        xmax[128 * x + r] = __fmul_rn(tt[0], kScale);
+        named_bar(3, 256);
+        const float mb = fmaxf(xmax[r], xmax[128 + r]);   // same operand order in both halves
+        named_bar(3, 256);                         // both read before the next exchange writes
         const float mn = fmaxf(m, mb);
         const float alpha = (mn == -CUDART_INF_F) ? 1.f : tc::ex2(__fsub_rn(m, mn));
         const float nmn = mn == -CUDART_INF_F ? 0.f : -mn;
@@ -398,10 +411,10 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
         l = __fmaf_rn(l, alpha, ps);
         m = mn;
         AT_T(1);   // S load + max/exp/sum
-        // P_X buffer and O_X partial were last used by PV(gb-1): wait for it (within the
+        // the P buffers and the O partial were last used by PV(gb-1): wait for it (within the
         // item; the previous item's last PV was waited for at its end), store P, fold
         if (i >= 1) {
-          tc::mbar_wait(&pv_done[x], (gb - 1) & 1);
+          tc::mbar_wait(pv_done, (gb - 1) & 1);
           tc::fence_after();
         }
         AT_T(2);   // wait PV(i-1)
@@ -424,66 +437,33 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
         tc::tmem_wait_st();
         tc::fence_before();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&p_full[x]);
+        if (lane == 0) tc::mbar_arrive(p_full);
         AT_T(3);   // P store + fold
       }
-      tc::mbar_wait(&pv_done[x], (gb - 1) & 1);
+      tc::mbar_wait(pv_done, (gb - 1) & 1);
       AT_T(4);   // wait last PV
       tc::fence_after();
       fold(alpha_prev);
-      // merge the halves: B hands (m, l, O) to A through its own (now idle) P region of TMEM
-      const uint32_t mt = tmem + T_P + 128 + lane_off;
-      if (x == 1) {
-        uint32_t w0[32], w1[32], w2[32];
+      // row sum: the two halves' partial sums (same order in both), then this half's dims
+      xmax[128 * x + r] = l;
+      named_bar(3, 256);
+      const float lt = __fadd_rn(xmax[r], xmax[128 + r]);
+      named_bar(3, 256);
+      const bool row_ok = r < xi.t.nrows;
+      const size_t ob = (size_t)(xi.t.qrow0 + r) * a.ldo + xi.h * 64 + 32 * x;
+      if (row_ok) {
 #pragma unroll
-        for (int d = 0; d < 32; ++d) { w0[d] = __float_as_uint(O[d]); w1[d] = __float_as_uint(O[32 + d]); w2[d] = 0u; }
-        w2[0] = __float_as_uint(m);
-        w2[1] = __float_as_uint(l);
-        tc::tmem_st32(mt, w0);
-        tc::tmem_st32(mt + 32, w1);
-        tc::tmem_st32(mt + 64, w2);
-        tc::tmem_wait_st();
-        tc::fence_before();
-      }
-      named_bar(1, 256);
-      if (x == 0) {                                // merge in 32-column pieces (registers)
-        tc::fence_after();
-        uint32_t w[32];
-        tc::tmem_ld32(mt + 64, w);
-        tc::tmem_wait_ld();
-        const float mB = __uint_as_float(w[0]), lB = __uint_as_float(w[1]);
-        const float mm = fmaxf(m, mB);
-        const float fa = (m == -CUDART_INF_F) ? 0.f : tc::ex2(__fsub_rn(m, mm));
-        const float fb = (mB == -CUDART_INF_F) ? 0.f : tc::ex2(__fsub_rn(mB, mm));
-        const float lt = __fmaf_rn(l, fa, __fmul_rn(lB, fb));
-        const bool row_ok = r < xi.t.nrows;
-        const size_t ob = (size_t)(xi.t.qrow0 + r) * a.ldo + xi.h * 64;
-#pragma unroll
-        for (int hf = 0; hf < 2; ++hf) {
-          tc::tmem_ld32(mt + 32 * hf, w);
-          tc::tmem_wait_ld();
-          if (hf == 1) {
-            tc::fence_before();
-            named_bar(2, 256);                     // B may reuse its P region (next item) only now
-          }
-          if (row_ok) {
-#pragma unroll
-            for (int d = 0; d < 32; d += 4) {
-              const int dd = 32 * hf + d;
-              float4 hi, lo, v;
-              v.x = __fdiv_rn(__fmaf_rn(O[dd], fa, __fmul_rn(__uint_as_float(w[d]), fb)), lt);
-              v.y = __fdiv_rn(__fmaf_rn(O[dd + 1], fa, __fmul_rn(__uint_as_float(w[d + 1]), fb)), lt);
-              v.z = __fdiv_rn(__fmaf_rn(O[dd + 2], fa, __fmul_rn(__uint_as_float(w[d + 2]), fb)), lt);
-              v.w = __fdiv_rn(__fmaf_rn(O[dd + 3], fa, __fmul_rn(__uint_as_float(w[d + 3]), fb)), lt);
-              tc::split_tf32(v.x, hi.x, lo.x); tc::split_tf32(v.y, hi.y, lo.y);
-              tc::split_tf32(v.z, hi.z, lo.z); tc::split_tf32(v.w, hi.w, lo.w);
-              *reinterpret_cast<float4 *>(a.o_hi + ob + dd) = hi;
-              *reinterpret_cast<float4 *>(a.o_lo + ob + dd) = lo;
-            }
-          }
+        for (int d = 0; d < 32; d += 4) {
+          float4 hi, lo, v;
+          v.x = __fdiv_rn(O[d], lt);
+          v.y = __fdiv_rn(O[d + 1], lt);
+          v.z = __fdiv_rn(O[d + 2], lt);
+          v.w = __fdiv_rn(O[d + 3], lt);
+          tc::split_tf32(v.x, hi.x, lo.x); tc::split_tf32(v.y, hi.y, lo.y);
+          tc::split_tf32(v.z, hi.z, lo.z); tc::split_tf32(v.w, hi.w, lo.w);
+          *reinterpret_cast<float4 *>(a.o_hi + ob + d) = hi;
+          *reinterpret_cast<float4 *>(a.o_lo + ob + d) = lo;
         }
-      } else {
-        named_bar(2, 256);
       }
       AT_T(5);   // merge + output
 #ifdef NC_ATT_TIMING
