@@ -216,8 +216,26 @@ __device__ __forceinline__ void store_head64(float *stg, const float *x, int pos
     }
     __syncwarp();
   }
+  // the rows' cos/sin in two batches of four (read-only path, a batch's loads in flight
+  // together): loaded inside the store loop they sat behind the previous row's stores
+  // (possible aliasing), one L2 round trip per row -- the QKV output phase was ~12k cycles
+  // per tile.  (All eight at once spills at the 128-register cap of the 448-thread CTA.)
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
+  for (int ib = 0; ib < 2; ++ib) {
+    float4 cs[4], sn4[4];
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii) {
+      const int pr = __shfl_sync(0xffffffffu, pos, 4 * (4 * ib + ii) + (lane >> 3));
+      if (rope && pr >= 0) {
+        cs[ii] = __ldg(reinterpret_cast<const float4 *>(cos_t + (size_t)pr * 32 + 4 * c4));
+        sn4[ii] = __ldg(reinterpret_cast<const float4 *>(sin_t + (size_t)pr * 32 + 4 * c4));
+      } else {
+        cs[ii] = sn4[ii] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+#pragma unroll
+  for (int ii = 0; ii < 4; ++ii) {
+    const int i = 4 * ib + ii;
     const int r = 4 * i + (lane >> 3);
     const int pr = __shfl_sync(0xffffffffu, pos, r);
     float *p0 = reinterpret_cast<float *>(__shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(d0), r));
@@ -227,8 +245,7 @@ __device__ __forceinline__ void store_head64(float *stg, const float *x, int pos
     if (pr < 0 || !p0) continue;
     float4 y1 = t[0][i], y2 = t[1][i];
     if (rope) {
-      const float4 c = *reinterpret_cast<const float4 *>(cos_t + (size_t)pr * 32 + 4 * c4);
-      const float4 sn = *reinterpret_cast<const float4 *>(sin_t + (size_t)pr * 32 + 4 * c4);
+      const float4 c = cs[ii], sn = sn4[ii];
       const float4 x1 = y1, x2 = y2;
       y1.x = __fmaf_rn(x1.x, c.x, __fmul_rn(-x2.x, sn.x)); y2.x = __fmaf_rn(x2.x, c.x, __fmul_rn(x1.x, sn.x));
       y1.y = __fmaf_rn(x1.y, c.y, __fmul_rn(-x2.y, sn.y)); y2.y = __fmaf_rn(x2.y, c.y, __fmul_rn(x1.y, sn.y));
@@ -249,6 +266,7 @@ __device__ __forceinline__ void store_head64(float *stg, const float *x, int pos
       *reinterpret_cast<float4 *>(p0 + 4 * c4) = y1;
       *reinterpret_cast<float4 *>(p0 + 32 + 4 * c4) = y2;
     }
+  }
   }
 }
 
