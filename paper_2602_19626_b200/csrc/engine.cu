@@ -9,11 +9,20 @@
 #include <mutex>
 #include <thread>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "engine.hpp"
 #include "attn_tc.cuh"
 #include "gemm_tc.cuh"
 
 namespace nc {
+
+// NVTX ranges around the host-side phases (visible in nsys / ncu --nvtx; header-only NVTX3,
+// a no-op unless a tool injects itself)
+struct Nvtx {
+  explicit Nvtx(const char *name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+};
 
 void check_cuda(cudaError_t e, const char *what) {
   if (e != cudaSuccess) fail(NC_ERR_BACKEND, std::string(what) + ": " + cudaGetErrorString(e));
@@ -224,6 +233,7 @@ void model_load_hf(nc_model *m, const std::string &dir, int device) {
 }
 
 void model_setup(nc_model *m, const NcwFile &f, int device) {
+  Nvtx nv("nc.model upload");
   const Shape &s = f.s;
   if (s.dh != (uint32_t)kHeadDim) fail(NC_ERR_INVALID, "kernels are specialised to head_dim 64");
   if (s.H % s.KV || s.H / s.KV > 3) fail(NC_ERR_INVALID, "GQA group must be <= 3");
@@ -717,6 +727,7 @@ struct Refill {
 void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<uint32_t> &ntok,
                      const Params &p, cudaStream_t s, CompressOut &out) {
   const auto t_entry = std::chrono::steady_clock::now();
+  Nvtx nv_all("nc.compress_device");
   NC_CUDA(cudaSetDevice(m->device));
   const Shape &S = m->s;
   const int n_chunks = (int)ntok.size();
@@ -828,6 +839,7 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
       NC_CUDA(cudaEventRecord(ev[4 * n_slabs + sl], ns));
       st.launches++;
     }
+    Nvtx nv_slab("nc.slab (forward + walk launches)");
     if (sl >= 2) NC_CUDA(cudaStreamWaitEvent(s, ev[4 * (sl - 2) + 3], 0));   // logits buffer free again
     fw.logits = fw.lbuf[sl & 1];
     NC_CUDA(cudaEventRecord(ev[4 * sl], s));
@@ -858,6 +870,7 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
     st.launches++;
     NC_CUDA(cudaGetLastError());
   }
+  Nvtx nv_sync("nc.compress sync + D2H");
   NC_CUDA(cudaStreamWaitEvent(s, ev[4 * (n_slabs - 1) + 3], 0));
   set_reserved_sms(0);
   NC_CUDA(cudaMemcpyAsync(out.cum.data(), cum_d, total * 4, cudaMemcpyDeviceToHost, s));
@@ -897,6 +910,7 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
 // --------------------------------------------------------------- container ---
 void encode_container(const Params &p, const std::vector<uint32_t> &ntok, const CompressOut &co,
                       std::vector<uint8_t> &out) {
+  Nvtx nv("nc.range coder + NC05");
   const size_t n = ntok.size();
   std::vector<Nc05Chunk> chunks(n);
   std::vector<size_t> off(n + 1, 0);
@@ -953,6 +967,7 @@ struct OwnStream {
 void decompress_device(nc_model *m, const uint8_t *blob, const Nc05View &view, const Params &p,
                        cudaStream_t s_caller, std::vector<std::vector<uint32_t>> &toks) {
   NC_CUDA(cudaSetDevice(m->device));
+  Nvtx nv_all("nc.decompress_device");
   OwnStream own(s_caller);
   cudaStream_t s = own.s;
   const Shape &S = m->s;

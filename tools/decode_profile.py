@@ -1,5 +1,6 @@
 """Per-kernel-class device time of one decompression (config2 by default), per decode step.
-python tools/decode_profile.py [workload]"""
+python tools/decode_profile.py [workload] [bytes per chunk: decode only the first B bytes of
+every chunk, as bench.py's decompress sample does]"""
 import os
 import sys
 import time
@@ -14,6 +15,10 @@ from synth import WORKLOADS, ensure_model, ensure_text  # noqa: E402
 
 wl = WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else "config2"]
 data = open(ensure_text(wl.name), "rb").read()
+if len(sys.argv) > 2:
+    cuts = nc.nc_host_split(data, wl.n_chunks)
+    b = int(sys.argv[2])
+    data = b"".join(data[cuts[c]:min(cuts[c + 1], cuts[c] + b)] for c in range(len(cuts) - 1))
 model = nc.Model(ensure_model(wl.shape), 0)
 prm = nc.nc_params_default(window=wl.window, slide=wl.slide, n_chunks=wl.n_chunks, cdf_bits=wl.cdf_bits)
 blob = nc.nc_compress(model, data, prm)
