@@ -19,12 +19,15 @@
 //   warp 0  TMA: Q once (hi/lo, 64 KB), then K of each 128-key block (64 KB, one buffer)
 //   warp 3  TMA: V in 64-key granules (32 KB) through a ring of 3
 //   warp 1  MMA issue (whole warp, one elected lane per instruction): S(i), then PV(i-1)
-//   warp 2  TMEM allocator: S (128 cols) | P_A hi,lo | P_B hi,lo (64 each) | O partials (2 x 64)
+//   warp 2  TMEM allocator: S (128 cols) | P_A hi,lo | P_B hi,lo (64 each) | O partial (64)
 //   warps 4-7 / 8-11  softmax of key half A / B and the promotion of output dims 0-31 / 32-63,
 //                     thread = query row (TMEM lane); the halves share the row max (smem)
-// Measured (tools/micro): an N = 128 tf32 MMA costs 64 cycles, N = 64 costs 48-57.  The
-// softmax side is bound by TMEM reads (~64 B/cycle/SM): per block S (64 KB) and the O
-// partial (32 KB; 64 KB when each key half kept its own partial and max).
+// Measured (tools/micro): an N = 128 tf32 MMA costs 64 cycles, N = 64 costs 48-57.  Per
+// 128-key block the TMEM reads -- S (64 KB) and the O partial (32 KB; 64 KB when each key
+// half kept its own partial and max) by the softmax groups, P (hi twice, lo once: 192 KB) as
+// the PV MMAs' A operand -- at ~64-80 B/cycle/SM are the bound: releasing each half's P
+// early and double-buffering the O partial (so the next P store and the fold overlap PV)
+// measured no gain (145 vs 148 TF/s) and was reverted.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -56,7 +59,7 @@ constexpr int V_GRAN = 4 * KV_SUB;               // V hi/lo x two 32-dim halves,
 constexpr int ATT_SMEM = Q_BYTES + K_BYTES + VG * V_GRAN + 1024 + 256 + 2 * 128 * 4;
 constexpr int ATT_THREADS = 384;
 // TMEM columns
-constexpr uint32_t T_S = 0, T_P = 128, T_O = 384;   // P half X at T_P + 128 X (hi, lo +64); O partial b at T_O + 64 (b & 1)
+constexpr uint32_t T_S = 0, T_P = 128, T_O = 384;   // P half X at T_P + 128 X (hi, lo +64); O partial at T_O
 
 #ifdef NC_ATT_TIMING
 // diagnostics build only: per-thread phase cycles accumulated in registers, flushed once per CTA
@@ -123,8 +126,7 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
   uint64_t *v_full = bars + 4, *v_empty = v_full + VG;
   uint64_t *s_full = v_empty + VG, *s_empty = s_full + 1;
   uint64_t *p_full = s_empty + 1, *pv_done = p_full + 1;   // P of both halves stored / PV done
-  uint64_t *p_free = pv_done + 1;                            // per key half: the PV MMAs read its P
-  uint64_t *sch_full = p_free + 2, *sch_empty = sch_full + NSCH;
+  uint64_t *sch_full = pv_done + 1, *sch_empty = sch_full + NSCH;
   int *sch_item = reinterpret_cast<int *>(sch_empty + NSCH);
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sch_item + NSCH);
   float *xmax = reinterpret_cast<float *>(tmem_slot + 4);   // [2 halves][128 rows] row-max / row-sum exchange
@@ -140,8 +142,6 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
     tc::mbar_init(s_full, 1); tc::mbar_init(s_empty, 8);
     tc::mbar_init(p_full, 8);
     tc::mbar_init(pv_done, 1);
-    tc::mbar_init(&p_free[0], 1);
-    tc::mbar_init(&p_free[1], 1);
     for (int s = 0; s < NSCH; ++s) { tc::mbar_init(&sch_full[s], 1); tc::mbar_init(&sch_empty[s], SCH_CONSUMERS); }
     tc::fence_barrier_init();
   }
@@ -255,28 +255,30 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
       tc::mbar_wait(&v_full[vst], vph);
       if (++vst == VG) { vst = 0; vph ^= 1; }
       tc::fence_after();
-      const uint32_t dO = tmem + T_O + 64 * (b & 1);   // double-buffered partial: fold(b-1) runs beside PV(b)
+      const uint32_t dO = tmem + T_O;
       const uint64_t vd[2] = {v_desc0 + off(vs0 * V_GRAN), v_desc0 + off(vs1 * V_GRAN)};
-      // half A's products (corrections first, hi*hi last), release P_A and its V granule, then
-      // half B's: softmax A may store its next P while the tensor pipe still runs half B
 #pragma unroll
-      for (int x = 0; x < 2; ++x) {
+      for (int x = 0; x < 2; ++x) {                // corrections first, hi*hi last (see k_gemm_tc.cu)
         const uint32_t ph_t = tmem + T_P + 128 * x, pl_t = ph_t + 64;
 #pragma unroll
         for (int j = 0; j < AH / 8; ++j) {
           if (tc::elect_one()) tc::mma_tf32_ts(dO, ph_t + j * 8, vd[x] + off(2 * KV_SUB + j * 1024), idO, (x | j) != 0);
           if (tc::elect_one()) tc::mma_tf32_ts(dO, pl_t + j * 8, vd[x] + off(j * 1024), idO, 1);
         }
+      }
+#pragma unroll
+      for (int x = 0; x < 2; ++x) {
+        const uint32_t ph_t = tmem + T_P + 128 * x;
 #pragma unroll
         for (int j = 0; j < AH / 8; ++j)
           if (tc::elect_one()) tc::mma_tf32_ts(dO, ph_t + j * 8, vd[x] + off(j * 1024), idO, 1);
-        if (tc::elect_one()) {
-          tc::mma_commit(&p_free[x]);
-          tc::mma_commit(&v_empty[x ? vs1 : vs0]);
-          if (x) tc::mma_commit(pv_done);          // the block's O partial is complete
-        }
-        __syncwarp();
       }
+      if (tc::elect_one()) {
+        tc::mma_commit(pv_done);                   // P buffers free + O partial ready
+        tc::mma_commit(&v_empty[vs0]);
+        tc::mma_commit(&v_empty[vs1]);
+      }
+      __syncwarp();
     };
     int gb = 0, qi = 0;
     AT_DECL;
@@ -352,9 +354,9 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
 #pragma unroll
       for (int d = 0; d < 32; ++d) O[d] = 0.f;
       float m = -CUDART_INF_F, l = 0.f, alpha_prev = 1.f;
-      auto fold = [&](float al, int pb) {          // O <- O * alpha + O_partial[pb]  (fp32 RN promotion)
+      auto fold = [&](float al) {                  // O <- O * alpha + O_partial  (fp32 RN promotion)
         uint32_t x0[32];
-        tc::tmem_ld32(tmem + T_O + 64 * pb + 32 * x + lane_off, x0);
+        tc::tmem_ld32(tmem + T_O + 32 * x + lane_off, x0);
         tc::tmem_wait_ld();
 #pragma unroll
         for (int d = 0; d < 32; ++d) O[d] = __fmaf_rn(O[d], al, __uint_as_float(x0[d]));
@@ -412,11 +414,10 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
         l = __fmaf_rn(l, alpha, ps);
         m = mn;
         AT_T(1);   // S load + max/exp/sum
-        // this half's P buffer was last read by PV(gb-1): wait for its half of the chain, store
-        // P, signal; then fold the O partial of the item's previous block (PV(gb-1) complete)
-        // while PV(gb) runs into the other partial buffer
+        // the P buffers and the O partial were last used by PV(gb-1): wait for it (within the
+        // item; the previous item's last PV was waited for at its end), store P, fold
         if (i >= 1) {
-          tc::mbar_wait(&p_free[x], (gb - 1) & 1);
+          tc::mbar_wait(pv_done, (gb - 1) & 1);
           tc::fence_after();
         }
         AT_T(2);   // wait PV(i-1)
@@ -434,23 +435,18 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
           tc::tmem_st32(ph_t + 32 * hh, hi);
           tc::tmem_st32(ph_t + 64 + 32 * hh, lo);
         }
+        if (i >= 1) fold(alpha_prev);
+        alpha_prev = alpha;
         tc::tmem_wait_st();
         tc::fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(p_full);
-        if (i >= 1) {
-          tc::mbar_wait(pv_done, (gb - 1) & 1);
-          tc::fence_after();
-          fold(alpha_prev, (gb - 1) & 1);
-          tc::fence_before();
-        }
-        alpha_prev = alpha;
         AT_T(3);   // P store + fold
       }
       tc::mbar_wait(pv_done, (gb - 1) & 1);
       AT_T(4);   // wait last PV
       tc::fence_after();
-      fold(alpha_prev, (gb - 1) & 1);
+      fold(alpha_prev);
       // row sum: the two halves' partial sums (same order in both), then this half's dims
       xmax[128 * x + r] = l;
       named_bar(3, 256);
