@@ -13,6 +13,10 @@ struct AttnTcArgs {
   int ring, n_chunks, n_layers, layer;
   float *o_hi, *o_lo; int ldo;               // output tf32 planes [rows, H*64]
   int H, KV, window, slide;                  // window = L_max of the w(j) formula (D10)
+  // decode steps (every tile one row of one chunk): the tile's rows are the H/KV q heads of one
+  // KV group at that single position (q / o planes viewed as [rows * H, 64]); one item per
+  // (tile, KV group) instead of per (tile, q head) -- each row's arithmetic is unchanged (D15)
+  int heads_as_rows;
   int debug;                                 // unused
   int *item_ctr;                             // set by the launcher (persistent item scheduler)
 };

@@ -411,8 +411,10 @@ struct Forward {
   // embed -> n_layers x {QKV, attention, O, gate-up, down} -> head into `logits`.
   // valid = rows that are real tokens (algorithmic work), attn_flops = sum over
   // valid rows of 4*H*dh*n_ctx(j) for one layer.
+  // decode_rows: every tile is one row of one chunk (decode steps): the attention packs the
+  // q heads of a KV group into one tile's rows
   void run(int M, double valid, double attn_flops, const RowMeta &rows, const AttnTile *tiles, int n_tiles,
-           const Params &p, cudaEvent_t ev_head, bool head = true) {
+           const Params &p, cudaEvent_t ev_head, bool head = true, bool decode_rows = false) {
     const Shape &S = m->s;
     Stats &st = stats();
     const int qd = S.H * S.dh, kvd = S.KV * S.dh;
@@ -437,6 +439,7 @@ struct Forward {
         at.ring = ring.ring; at.n_chunks = n_chunks_; at.n_layers = (int)S.n_layers; at.layer = (int)l;
         at.o_hi = o_hi; at.o_lo = o_lo; at.ldo = qd;
         at.H = S.H; at.KV = S.KV; at.window = (int)p.lmax; at.slide = (int)p.slide;
+        at.heads_as_rows = decode_rows ? 1 : 0;
         PROF(K_ATTN, attn_flops, launch_attention_tc(at, s));
       }
       {
@@ -1038,7 +1041,7 @@ void decompress_device(nc_model *m, const uint8_t *blob, const Nc05View &view, c
     const double ctx = (double)j - window_start_h(j, p.lmax, p.slide) + 1;
     PROF(K_MISC, 0, (step_rows_dev_kernel<<<1, 256, 0, s>>>(ntok_d, n_chunks, jctr, rchunk, rpos, tiles, wc, wr, wn)));
     RowMeta rows{x_cur, rchunk, rpos};
-    fw.run(n_chunks, valid, 4.0 * S.H * S.dh * ctx * valid, rows, tiles, n_chunks, p, nullptr);
+    fw.run(n_chunks, valid, 4.0 * S.H * S.dh * ctx * valid, rows, tiles, n_chunks, p, nullptr, true, true);
     PROF(K_WALK, 4.0 * S.V * valid, launch_walk(wa, s));
     st.launches += 2;
   };
@@ -1164,7 +1167,7 @@ void debug_forward(nc_model *m, const uint32_t *x, uint32_t rows, const Params &
       if (p.refresh) rf.before_step(j, p);
       step_rows_kernel<<<1, 32, 0, s>>>(nt_d, 1, (int)j, rc, rp, tiles, wc, wr, wn);
       RowMeta rm{x_d + j, rc, rp};
-      fw.run(1, 0, 0, rm, tiles, 1, p, nullptr);
+      fw.run(1, 0, 0, rm, tiles, 1, p, nullptr, true, true);
       NC_CUDA(cudaMemcpyAsync(out + (size_t)j * S.V, fw.logits, (size_t)S.V * 4, cudaMemcpyDeviceToHost, s));
     }
   }

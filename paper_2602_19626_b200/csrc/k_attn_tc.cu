@@ -132,7 +132,7 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
   float *xmax = reinterpret_cast<float *>(tmem_slot + 4);   // [2 halves][128 rows] row-max / row-sum exchange
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_items = a.n_tiles * a.H;
+  const int n_items = a.n_tiles * (a.heads_as_rows ? a.KV : a.H);
 
   if (threadIdx.x == 0) {
     tc::tma_prefetch(&tmQh); tc::tma_prefetch(&tmKh); tc::tma_prefetch(&tmVh);
@@ -154,15 +154,25 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
   tc::pdl_wait();   // q planes and the KV ring come from the QKV GEMM
 
   // item -> (tile, head, geometry); every role derives the same numbers
+  // item -> (tile, head, geometry); heads_as_rows: (tile, KV group), rows = the group's q heads
+  const int ipt = a.heads_as_rows ? a.KV : a.H;   // items per tile
   struct Item { AttnTile t; int h, g, kb0, nkb, zc; };
   auto item_of = [&](int it) {
     Item x;
-    x.t = a.tiles[it / a.H];
-    x.h = it % a.H;
-    x.g = x.h / (a.H / a.KV);
+    x.t = a.tiles[it / ipt];
+    if (a.heads_as_rows) {
+      x.g = it % ipt;
+      x.h = x.g * (a.H / a.KV);               // first q head of the group (its q row offset)
+      if (x.t.nrows > 0) x.t.nrows = a.H / a.KV;
+      x.t.qrow0 = x.t.qrow0 * a.H + x.h;      // row of [rows * H, 64]
+    } else {
+      x.h = it % a.H;
+      x.g = x.h / (a.H / a.KV);
+    }
     const int w = x.t.w0 >= 0 ? x.t.w0 : wstart(x.t.p0, a.window, a.slide);   // a.window = L_max
     x.kb0 = w / AK;
-    x.nkb = x.t.nrows > 0 ? (x.t.p0 + x.t.nrows - 1) / AK - x.kb0 + 1 : 0;   // 0: inactive decode chunk
+    const int last = a.heads_as_rows ? x.t.p0 : x.t.p0 + x.t.nrows - 1;       // the tile's last position
+    x.nkb = x.t.nrows > 0 ? last / AK - x.kb0 + 1 : 0;   // 0: inactive decode chunk
     x.zc = x.t.chunk * a.n_layers + a.layer;
     return x;
   };
@@ -192,10 +202,11 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
         if (x.nkb == 0) continue;
         tc::mbar_wait(q_empty, (qi & 1) ^ 1);           // all S MMAs of the previous item done
         tc::mbar_expect_tx(q_full, Q_BYTES);
-        tc::tma_load_2d(sQ, &tmQh, x.h * 64, x.t.qrow0, q_full);
-        tc::tma_load_2d(sQ + Q_SUB, &tmQh, x.h * 64 + 32, x.t.qrow0, q_full);
-        tc::tma_load_2d(sQ + 2 * Q_SUB, &tmQl, x.h * 64, x.t.qrow0, q_full);
-        tc::tma_load_2d(sQ + 3 * Q_SUB, &tmQl, x.h * 64 + 32, x.t.qrow0, q_full);
+        const int qc = a.heads_as_rows ? 0 : x.h * 64;   // [rows * H, 64] view: the head is the row
+        tc::tma_load_2d(sQ, &tmQh, qc, x.t.qrow0, q_full);
+        tc::tma_load_2d(sQ + Q_SUB, &tmQh, qc + 32, x.t.qrow0, q_full);
+        tc::tma_load_2d(sQ + 2 * Q_SUB, &tmQl, qc, x.t.qrow0, q_full);
+        tc::tma_load_2d(sQ + 3 * Q_SUB, &tmQl, qc + 32, x.t.qrow0, q_full);
         ++qi;
         for (int i = 0; i < x.nkb; ++i, ++gb) {
           tc::mbar_wait(k_empty, (gb & 1) ^ 1);
@@ -349,7 +360,7 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
       const Item xi = item_of(it);
       if (xi.nkb == 0) continue;
       AT_T(6);   // item gap
-      const int j = xi.t.p0 + r;
+      const int j = a.heads_as_rows ? xi.t.p0 : xi.t.p0 + r;   // this row's position
       float O[32];                                 // output dims [32 x, 32 x + 32) of row r
 #pragma unroll
       for (int d = 0; d < 32; ++d) O[d] = 0.f;
@@ -454,7 +465,8 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
       named_bar(3, 256);
       const float rl = __frcp_rn(lt);              // o = O * (1 / l): one reciprocal per row
       const bool row_ok = r < xi.t.nrows;
-      const size_t ob = (size_t)(xi.t.qrow0 + r) * a.ldo + xi.h * 64 + 32 * x;
+      const size_t ob = a.heads_as_rows ? (size_t)(xi.t.qrow0 + r) * 64 + 32 * x
+                                        : (size_t)(xi.t.qrow0 + r) * a.ldo + xi.h * 64 + 32 * x;
       if (row_ok) {
 #pragma unroll
         for (int d = 0; d < 32; d += 4) {
@@ -570,8 +582,10 @@ void launch_attention_tc(const AttnTcArgs &a, cudaStream_t s) {
   if (first_on_device(attr))
     check_launch(cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ATT_SMEM),
                  "attention smem attribute");
-  const uint64_t qd[2] = {(uint64_t)a.ldq, (uint64_t)a.q_rows};
+  const uint64_t qd[2] = {a.heads_as_rows ? 64ull : (uint64_t)a.ldq,
+                          a.heads_as_rows ? (uint64_t)a.q_rows * a.H : (uint64_t)a.q_rows};
   const uint32_t qb[2] = {32, AQ};
+  if (a.heads_as_rows && a.ldq != a.H * 64) throw std::runtime_error("heads_as_rows needs ldq == H * 64");
   const uint64_t kd[4] = {64, (uint64_t)a.KV, (uint64_t)a.ring, (uint64_t)a.n_chunks * a.n_layers};
   const uint32_t kbx[4] = {32, 1, AH, 1};   // 64-key granules (a 128-key K block is two)
   const CUtensorMap *qh = tmap_nd(a.q_hi, 2, qd, qb), *ql = tmap_nd(a.q_lo, 2, qd, qb);
@@ -596,7 +610,7 @@ void launch_attention_tc(const AttnTcArgs &a, cudaStream_t s) {
   }
   AttnTcArgs aa = a;
   aa.item_ctr = ctr;
-  const int grid = std::min(a.n_tiles * a.H, n_sms);   // persistent: one CTA per SM claims (tile, head) items
+  const int grid = std::min(a.n_tiles * (a.heads_as_rows ? a.KV : a.H), n_sms);   // persistent: one CTA per SM claims items
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(ATT_THREADS);

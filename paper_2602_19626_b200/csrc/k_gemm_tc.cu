@@ -62,6 +62,11 @@
 namespace nc {
 
 constexpr int TBM = 128;              // rows per CTA (pair tile: 256)
+// tile width of the few-row GEMMs of decode steps (M <= 128): their k loop is bound by the
+// N-proportional MMA cost (12 pair MMAs per 32-wide k block), not by rows
+#ifndef NC_DECODE_BN
+#define NC_DECODE_BN 64
+#endif
 // BN = pair tile columns (MMA N; each CTA stages BN / 2 rows of B): 256, or 192 for
 // the N = 576 residual GEMMs (576 = 3 x 192: no padded MMA work, smaller output bursts)
 constexpr int TBK = 32, NPART = 2, NSCHED = 4;
@@ -74,7 +79,7 @@ constexpr int TBK = 32, NPART = 2, NSCHED = 4;
 #endif
 constexpr int KPP = NC_KPP;
 // split-K fixup: rows folded at once (all spans in flight) and the largest span count
-constexpr int SK_ROWS = 2, SK_MIN_SPANS = 16, SK_MAX_SPANS = 24;
+constexpr int SK_ROWS = 2, SK_MIN_SPANS = 16, SK_MAX_SPANS = 24, SK_MAX_ROWS = 16;
 constexpr int TILE_A_BYTES = TBM * TBK * 4;          // 16 KB
 constexpr int TMEM_COLS = 512;                              // NPART x BN <= 512, power of two
 template <int BN>
@@ -82,7 +87,7 @@ struct TileCfg {
   // epilogue warps: 4 TMEM lane quarters x column groups; 192-wide tiles take three groups
   // of 64 (one attention head / two 32-column residual slices per warp) so their output
   // phase -- which the MMA of the next tile can only run two partials ahead of -- is short
-  static constexpr int EPI_COLS = BN == 192 ? 64 : BN / 2;               // columns per epilogue warp
+  static constexpr int EPI_COLS = (BN == 192 || BN == 64) ? 64 : BN / 2;  // columns per epilogue warp
   static constexpr int EPI_WARPS = 4 * (BN / EPI_COLS);                  // 8, or 12 at BN = 192
   static constexpr int THREADS = 32 * (EPI_WARPS + 2);                   // + TMA/allocator + MMA warps
   static constexpr int W_TMA = EPI_WARPS, W_MMA = EPI_WARPS + 1;
@@ -93,7 +98,7 @@ struct TileCfg {
   static constexpr int STAGE_BYTES = 2 * TILE_A_BYTES + 2 * TILE_B_BYTES;   // 64 / 56 KB per CTA
   // pipeline depth: 3 stages of 64 / 56 KB; the 128-wide tiles (decode steps, whose k loop
   // is bound by TMA round trips rather than MMAs) fit a fourth 48 KB stage
-  static constexpr int STAGES = BN == 128 ? 4 : 3;
+  static constexpr int STAGES = BN == 64 ? 5 : (BN == 128 ? 4 : 3);
   static constexpr int SMEM = STAGES * STAGE_BYTES + OUT_STAGE_BYTES + 1024 /*align*/ + 512 /*barriers*/;
   static_assert(NPART * BN <= TMEM_COLS && BN % 32 == 0 && EPI_COLS % 32 == 0, "tile");
 };
@@ -858,8 +863,10 @@ static void launch_tc(const TcGemmArgs &a, const TcOperands &op, cudaStream_t s)
   // k block ~0.9 us on one pair; the fixup's fold is a few dependent L2 round trips per 32
   // columns, so splitting wins only for long k loops (down: K = 1536, 47 -> 37 us) and
   // loses at K = 576 (25 -> 33-40 us).
+  // (At M = 64 -- decode of 64 chunks -- the fixup's fold, 2 rows per round trip over 32 rows
+  // per warp, made the split down projection 76 us against ~37 unsplit: split only few rows.)
   if (g_splitk_mode != 0 && nspan >= SK_MIN_SPANS && nspan <= SK_MAX_SPANS && 2 * tiles <= pairs_avail &&
-      !a.no_store && a.N % 32 == 0) {
+      a.M <= SK_MAX_ROWS && !a.no_store && a.N % 32 == 0) {
     nsplit = std::min(nspan, pairs_avail / tiles);
     aa.sps = (nspan + nsplit - 1) / nsplit;
     nsplit = (nspan + aa.sps - 1) / aa.sps;
@@ -928,15 +935,15 @@ void launch_gemm_tc(GemmEpi epi, const TcGemmArgs &a, const TcOperands &op, cuda
     // it and double the tiles in flight.  Each output element is the same MMA sequence
     // whatever the tile width (D15; test_splitk_bit_identity compares prefill and decode).
     case EPI_QKV:
-      if (a.M <= TBM) launch_tc<EPI_QKV, 128>(a, op, s);
+      if (a.M <= TBM) launch_tc<EPI_QKV, NC_DECODE_BN>(a, op, s);
       else launch_tc<EPI_QKV, 192>(a, op, s);   // N = 960 = 5 x 192: three heads per tile, no padding
       break;
     case EPI_RESID:
-      if (a.M <= TBM) launch_tc<EPI_RESID, 128>(a, op, s);
+      if (a.M <= TBM) launch_tc<EPI_RESID, NC_DECODE_BN>(a, op, s);
       else launch_tc<EPI_RESID, 192>(a, op, s);   // N = 576 = 3 x 192
       break;
     case EPI_SWIGLU:
-      if (a.M <= TBM) launch_tc<EPI_SWIGLU, 128>(a, op, s);
+      if (a.M <= TBM) launch_tc<EPI_SWIGLU, NC_DECODE_BN>(a, op, s);
       else launch_tc<EPI_SWIGLU, 256>(a, op, s);
       break;
     case EPI_HEAD: launch_tc<EPI_HEAD, 256>(a, op, s); break;
