@@ -198,7 +198,7 @@ nc_status nc_compress_shard(nc_model *m, nc_comm *c, const uint8_t *in, size_t n
       uint32_t *tok_d = static_cast<uint32_t *>(nc::dev_alloc(tokens.size() * 4 + 4, s));
       if (!tokens.empty()) NC_CUDA(cudaMemcpyAsync(tok_d, tokens.data(), tokens.size() * 4, cudaMemcpyHostToDevice, s));
       nc::CompressOut co;
-      nc::compress_device(m, tok_d, ntok, q, s, co);
+      nc::compress_device(m, tok_d, ntok, q, s, co, (int)nch);
       nc::dev_free(tok_d, s);
       nc::encode_container(q, ntok, co, mine_blob);
       nc::Nc05View v = nc::read_nc05(mine_blob.data(), mine_blob.size());
@@ -247,7 +247,7 @@ nc_status nc_decompress_shard(nc_model *m, nc_comm *c, const uint8_t *in, size_t
     nc::Nc05View mine = v;
     mine.ents.assign(v.ents.begin() + c0, v.ents.begin() + c1);
     std::vector<std::vector<uint32_t>> toks;
-    if (c1 > c0) nc::decompress_device(m, in, mine, q, s, toks);
+    if (c1 > c0) nc::decompress_device(m, in, mine, q, s, toks, (int)nch);
     std::string text;
     for (auto &t : toks) m->tok.decode(t.data(), t.size(), text);
     // one allgather of decoded byte lengths (split into two u32 halves)

@@ -728,7 +728,7 @@ struct Refill {
 
 // --------------------------------------------------------------- compress ---
 void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<uint32_t> &ntok,
-                     const Params &p, cudaStream_t s, CompressOut &out) {
+                     const Params &p, cudaStream_t s, CompressOut &out, int container_chunks) {
   const auto t_entry = std::chrono::steady_clock::now();
   Nvtx nv_all("nc.compress_device");
   NC_CUDA(cudaSetDevice(m->device));
@@ -824,7 +824,7 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
   wbase.tokens = tokens_dev; wbase.tok_off = tok_off_d;
   wbase.out_cum = cum_d; wbase.out_freq = freq_d; wbase.out_p = p_d;
   wbase.mode = 0;
-  wbase.n_chunks_total = n_chunks;
+  wbase.n_chunks_total = container_chunks >= 0 ? container_chunks : n_chunks;
   wb.fill(wbase, p, S.V);
   for (int sl = 0; sl < n_slabs; ++sl) {
     if (use_ng) {
@@ -968,7 +968,7 @@ struct OwnStream {
 };
 
 void decompress_device(nc_model *m, const uint8_t *blob, const Nc05View &view, const Params &p,
-                       cudaStream_t s_caller, std::vector<std::vector<uint32_t>> &toks) {
+                       cudaStream_t s_caller, std::vector<std::vector<uint32_t>> &toks, int container_chunks) {
   NC_CUDA(cudaSetDevice(m->device));
   Nvtx nv_all("nc.decompress_device");
   OwnStream own(s_caller);
@@ -1026,7 +1026,7 @@ void decompress_device(nc_model *m, const uint8_t *blob, const Nc05View &view, c
   wa.logits = fw.logits; wa.ldl = S.V;
   wa.tok_off = tok_off_d; wa.streams = blob_d; wa.stream_off = s_off_d; wa.stream_bits = s_bits_d;
   wa.out_tok = out_tok; wa.next_x = x_cur; wa.mode = 1;
-  wa.n_chunks_total = n_chunks;
+  wa.n_chunks_total = container_chunks >= 0 ? container_chunks : n_chunks;
   wb.fill(wa, p, S.V);
   int *jctr = bag.get<int>(1);
   NC_CUDA(cudaMemsetAsync(jctr, 0, sizeof(int), s));
@@ -1313,7 +1313,7 @@ void debug_walk(int device, const float *logits, uint32_t n_lrows, const uint32_
   wa.chunk_of = c_d; wa.row0 = r_d; wa.n_entries = 1;
   wa.logits = lg_d; wa.ldl = V; wa.tokens = tk_d; wa.tok_off = off_d;
   wa.out_cum = cum_d; wa.out_freq = freq_d; wa.out_p = p_d; wa.out_pt = pt_d; wa.mode = 0;
-  wa.n_chunks_total = 1;
+  wa.n_chunks_total = p.n_chunks ? (int)p.n_chunks : 1;   // the container this chunk belongs to (cluster size)
   const size_t dn = (size_t)n_rows * V;
   if (n_rows) {
     std::vector<uint32_t> rv(rows, rows + n_rows);

@@ -85,11 +85,13 @@ struct CompressOut {
   std::vector<float> p_true;         // debug_dump only
   std::vector<uint32_t> err;         // per chunk
 };
+// container_chunks: chunks of the whole container (a shard's are a subset; the walk's cluster
+// size depends on it, so compression and decompression must agree), -1 = ntok.size()
 void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<uint32_t> &ntok,
-                     const Params &p, cudaStream_t s, CompressOut &out);
+                     const Params &p, cudaStream_t s, CompressOut &out, int container_chunks = -1);
 // Decode all chunks of a parsed container; returns token ids per chunk.
 void decompress_device(nc_model *m, const uint8_t *blob, const Nc05View &view, const Params &p,
-                       cudaStream_t s, std::vector<std::vector<uint32_t>> &toks);
+                       cudaStream_t s, std::vector<std::vector<uint32_t>> &toks, int container_chunks = -1);
 // host encode + container
 void encode_container(const Params &p, const std::vector<uint32_t> &ntok, const CompressOut &co,
                       std::vector<uint8_t> &out);

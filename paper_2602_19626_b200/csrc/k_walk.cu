@@ -1501,12 +1501,14 @@ static int walk_cluster_size(uint32_t V, int n_chunks) {
     return e ? std::atoi(e) : 0;
   }();
   if (V < 4096 || V % 64) return 1;
-  if (forced == 4 || forced == 8) return forced;
+  if (forced == 4 || forced == 8 || forced == 16) return forced;
   // 8 CTAs per chunk for large vocabularies: halves the per-token pass (config2: walk 29.7 ->
   // 21.6 ms of kernel time, step time unchanged -- its SMs come out of the overlapped forward).
-  // (A 16-CTA cluster for one or two chunks, where the walk is the whole critical path, was
-  // refused at launch -- "invalid argument" -- on the B200; n_chunks stays in the rule's inputs.)
-  (void)n_chunks;
+  // With one or two chunks in the container the walk is the whole critical path: a 16-CTA
+  // (non-portable) cluster halves the pass again (config2 with one chunk: 1.04 -> 1.27 MB/s;
+  // per token 8.0k -> 6.0k cycles).  The rule's inputs are the vocabulary and the
+  // CONTAINER's chunk count (the decoder reads it from the header; a shard passes the total).
+  if (n_chunks <= 2 && V >= 32768 && V % 1024 == 0) return 16;
   return (V >= 32768 && V % 256 == 0) ? 8 : 4;
 }
 
@@ -1519,7 +1521,11 @@ static void launch_walk_cs(const WalkArgs &a, cudaStream_t s) {
   const size_t dyn = (size_t)Vc * 8 + Vc * 4 + Vc * 4 + ((Vc + 31) / 32) * 4 + (Vc / 4) * 4 + 64;
   static unsigned long long attr = 0;
   if (first_on_device(attr)) {
-    check_launch(cudaFuncSetAttribute(walk_cl_kernel<CS, NGM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024),
+    // the largest slice this instantiation serves (4 NGM WT ids): the attribute sized to the
+    // need, not the SM maximum, so 16-CTA clusters pass the cluster placement check
+    const size_t vmax = (size_t)4 * NGM * WT;
+    const size_t dmax = vmax * 8 + vmax * 4 + vmax * 4 + ((vmax + 31) / 32) * 4 + (vmax / 4) * 4 + 64;
+    check_launch(cudaFuncSetAttribute(walk_cl_kernel<CS, NGM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dmax),
                  "walk smem attribute");
     if (CS > 1)
       check_launch(cudaFuncSetAttribute(walk_cl_kernel<CS, NGM>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
@@ -1559,7 +1565,10 @@ void launch_walk(const WalkArgs &a, cudaStream_t s) {
   if (a.n_entries <= 0) return;
   const int cs = walk_cluster_size(a.V, a.n_chunks_total);
   const uint32_t groups = (a.V / cs / 4 + WT - 1) / WT;   // float4 groups per thread
-  if (cs == 8) {
+  if (cs == 16) {
+    if (groups <= 2) launch_walk_cs<16, 2>(a, s);
+    else launch_walk_cs<16, 4>(a, s);
+  } else if (cs == 8) {
     if (groups <= 3) launch_walk_cs<8, 3>(a, s);
     else if (groups <= 4) launch_walk_cs<8, 4>(a, s);
     else launch_walk_cs<8, NGMAX>(a, s);

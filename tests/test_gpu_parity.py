@@ -259,11 +259,25 @@ def test_skip_roundtrip_size_and_p(nc, m2, w2, n_chunks):
     assert abs(len(blob) - (9 + size)) <= 0.005 * size, (len(blob), size)
 
 
+def _chunk_stream_alone(nc, m, data, n_chunks, prm_fw):
+    """(token_count, bit_count, stream) of one chunk computed ALONE: its own debug forward
+    (one chunk, its own slab plan / decode-free prefill) and walk -- with the walk's cluster
+    size of an n_chunks container (the rule's input) -- then the host WNC encoder."""
+    t, _ = nc.nc_tokenize(m, data, 1)
+    t = [int(v) for v in t]
+    z = nc.nc_debug_forward(m, [0] + t[:-1], prm_fw, 0)
+    cum, freq, _ = nc.nc_debug_walk(z, t, nc.nc_params_default(window=prm_fw.window, slide=prm_fw.slide,
+                                                              n_chunks=n_chunks))
+    stream, bits = nc.nc_host_wnc_encode(cum, freq, 24)
+    return len(t), bits, stream
+
+
 def test_chunk_streams_independent_of_batch(nc, m2):
     """Chunks are independent: a chunk's bitstream inside a 16-chunk container
-    (slabs of 16 x len rows, 16 decode rows per step) equals the stream of that chunk
-    compressed alone (1 chunk: the geometric slab plan, 1-row decode steps) -- batch and
-    slab independence of every kernel (D15) -- and the 16-chunk container round-trips."""
+    (slabs of 16 x len rows, 16 decode rows per step) equals the stream of that chunk's
+    forward and walk run alone (batch and slab independence of every kernel, D15), and the
+    16-chunk container round-trips.  (The walk's cluster size is a function of the
+    container's chunk count, so the lone walk takes the 16-chunk container's.)"""
     import struct
     from synth import make_text
     data = make_text("alice", 24000, 77)
@@ -279,10 +293,9 @@ def test_chunk_streams_independent_of_batch(nc, m2):
     cuts = nc.nc_host_split(data, 16)
     prm1 = nc.nc_params_default(window=256, slide=128, n_chunks=1)
     for c in (0, 7, n - 1):
-        one = nc.nc_compress(m2, data[cuts[c]:cuts[c + 1]], prm1)
-        t1 = struct.unpack_from("<III", one, 9)
-        assert t1 == table[c], (c, t1, table[c])
-        assert one[21:21 + t1[2]] == blob[offs[c]:offs[c + 1]], c
+        ntk, bits, stream = _chunk_stream_alone(nc, m2, data[cuts[c]:cuts[c + 1]], n, prm1)
+        assert (ntk, bits) == table[c][:2], (c, ntk, bits, table[c])
+        assert stream == blob[offs[c]:offs[c + 1]], c
 
 
 def test_edge_inputs_roundtrip(nc, m2):
@@ -559,7 +572,7 @@ def test_walk_parity_param_variants(nc, V, n, over):
 def test_many_chunks_roundtrip(nc, m2):
     """300 chunks in one call (chunk_count > 255 in the u16 header field; walk clusters in
     several waves; ~30-token chunks, most shorter than the warmup): round trip, and chunks
-    0 / 150 / 299 carry the same stream as when compressed alone."""
+    0 / 150 / 299 carry the same stream as their forward and walk run alone."""
     import struct
     from synth import make_text
     data = make_text("alice", 45000, 55)
@@ -576,10 +589,9 @@ def test_many_chunks_roundtrip(nc, m2):
     assert offs[-1] == len(blob)
     prm1 = nc.nc_params_default(window=256, slide=128, n_chunks=1)
     for c in (0, 150, n - 1):
-        one = nc.nc_compress(m2, data[cuts[c]:cuts[c + 1]], prm1)
-        t1 = struct.unpack_from("<III", one, 9)
-        assert t1 == table[c], (c, t1, table[c])
-        assert one[21:21 + t1[2]] == blob[offs[c]:offs[c + 1]], c
+        ntk, bits, stream = _chunk_stream_alone(nc, m2, data[cuts[c]:cuts[c + 1]], n, prm1)
+        assert (ntk, bits) == table[c][:2], (c, ntk, bits, table[c])
+        assert stream == blob[offs[c]:offs[c + 1]], c
 
 
 def test_compress_tokens_equals_compress(nc, m2):

@@ -98,6 +98,24 @@ def test_walk_dump_gaussian(nc, V, n, flags, bits):
     check_dump(d, ref, toks, V, bits, warm)
 
 
+@pytest.mark.parametrize("n_chunks", [1, 8])
+def test_walk_dump_cluster_sizes(nc, n_chunks):
+    """V = 49,152 with the walk's two large-vocabulary cluster sizes: 16 CTAs (a container of
+    1-2 chunks) and 8 CTAs (more chunks) -- the cluster reductions differ, the bars do not."""
+    from oracle.ensemble import Params, encode_tokens
+    from synth.logits import markov_tokens
+    V, n = 49152, 900
+    assert nc.nc_host_walk_ctas(V, n_chunks) == (16 if n_chunks <= 2 else 8)
+    rng = np.random.default_rng(n_chunks)
+    Z = (rng.standard_normal((n, V)) * 1.5).astype(np.float32)
+    toks = markov_tokens(V, n, 5)
+    rows = sample_rows(n, 50)
+    prm = nc.nc_params_default(flags=3, cdf_bits=24, warmup=50, n_chunks=n_chunks)
+    d = nc.nc_debug_walk_dump(Z, toks, prm, rows)
+    ref = encode_tokens(Z, toks, V, Params(flags=3, cdf_bits=24, warmup=50), keep_rows=rows)
+    check_dump(d, ref, toks, V, 24, 50)
+
+
 def test_walk_dump_llm_competitive(nc):
     """An informative LLM (SPEC.md:364's bigram stub over a Markov token source): after the
     warmup the oracle's mixer keeps w_llm inside (1e-3, 0.999) on every row and inside
