@@ -26,6 +26,7 @@
 // arithmetic; every float op is an explicit round-to-nearest intrinsic and
 // every reduction has a fixed tree, so the decoder reproduces the encoder's
 // counts bit for bit (D15).
+#include <algorithm>
 #include <cstddef>
 #include <cstdio>
 #include <cstdlib>
@@ -1245,8 +1246,8 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
       const uint32_t i = s_i;
       const int par = it & 1;
       // (1) N-gram prediction by rank 0, shared through DSMEM; decoder target.
-      //     gsum (>= V/32 words, idle here) is the predictor's full-vocab bitmap scratch.
-      for (int w = tid; w < Gc; w += WT) gsum[w] = 0u;
+      //     gsum (max(V/CS/4, V/32) words, idle here) is the predictor's full-vocab bitmap scratch.
+      for (int w = tid; w < (int)((V + 31) / 32); w += WT) gsum[w] = 0u;
       __syncthreads();
       if (rank == 0 && wid == 0 && use_ng && i >= a.warmup) {
         uint32_t hist[4];
@@ -1518,13 +1519,17 @@ static void launch_walk_cs(const WalkArgs &a, cudaStream_t s) {
   if (Vc % 4 || Vc / 4 > (uint32_t)NGM * WT)   // float4 groups, at most NGM per thread (register-resident rows)
     throw std::runtime_error("walk: vocabulary slice of " + std::to_string(Vc) +
                              " ids per CTA unsupported (needs a multiple of 4, at most 16384)");
-  const size_t dyn = (size_t)Vc * 8 + Vc * 4 + Vc * 4 + ((Vc + 31) / 32) * 4 + (Vc / 4) * 4 + 64;
+  // b f64, cu, spadd, the slice bitmap, then gsum: the decoder's per-group counts (Vc / 4 words)
+  // AND the N-gram predictor's full-vocabulary bitmap (V / 32 words; larger at 16 CTAs)
+  const size_t gsum_words = std::max<size_t>(Vc / 4, (a.V + 31) / 32);
+  const size_t dyn = (size_t)Vc * 8 + Vc * 4 + Vc * 4 + ((Vc + 31) / 32) * 4 + gsum_words * 4 + 64;
   static unsigned long long attr = 0;
   if (first_on_device(attr)) {
     // the largest slice this instantiation serves (4 NGM WT ids): the attribute sized to the
     // need, not the SM maximum, so 16-CTA clusters pass the cluster placement check
     const size_t vmax = (size_t)4 * NGM * WT;
-    const size_t dmax = vmax * 8 + vmax * 4 + vmax * 4 + ((vmax + 31) / 32) * 4 + (vmax / 4) * 4 + 64;
+    const size_t gmax = std::max<size_t>(vmax / 4, (size_t)CS * vmax / 32);   // V <= CS vmax
+    const size_t dmax = vmax * 8 + vmax * 4 + vmax * 4 + ((vmax + 31) / 32) * 4 + gmax * 4 + 64;
     check_launch(cudaFuncSetAttribute(walk_cl_kernel<CS, NGM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dmax),
                  "walk smem attribute");
     if (CS > 1)
