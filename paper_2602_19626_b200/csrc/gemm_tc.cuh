@@ -25,7 +25,6 @@ struct TcGemmArgs {
   float *ws;
   int *fix_ctr;
   int no_store;                // diagnostics only (debug_gemm timing): skip the epilogue's global writes
-  int desync;                  // set by the launcher: cycles the odd CTA pairs wait before their first claim
 };
 
 struct TcOperands {

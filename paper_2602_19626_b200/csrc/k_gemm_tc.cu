@@ -379,12 +379,6 @@ __global__ __launch_bounds__(TileCfg<BN>::THREADS, 1) void gemm_tc_kernel(const 
       for (int jt = 0;; ++jt) {
         const int slot = jt % NSCHED;
         int t;
-        if (rank == 0 && jt == 0 && a.desync > 0 && ((blockIdx.x >> 1) & 1)) {
-          // odd pairs start half a tile late: the epilogues' output bursts (HBM-write bound when
-          // every SM stores at once) then alternate between the two halves of the grid
-          const long long t0 = clock64();
-          while (clock64() - t0 < a.desync) __nanosleep(256);
-        }
         if (rank == 0) {
           tc::mbar_wait(&sch_empty[slot], ((jt / NSCHED) & 1) ^ 1);
           const int claimed = atomicAdd(a.tile_ctr, 1);
@@ -863,11 +857,6 @@ static void launch_tc(const TcGemmArgs &a, const TcOperands &op, cudaStream_t s)
   // split-K when the tile grid would leave most SMs idle (decode steps); bit-identical
   // to the unsplit sum (see the kernel header); nc_debug_set_splitk(0) disables it.
   const int nspan = (a.K / TBK + KPP - 1) / KPP;
-  {   // desync (NC_GEMM_DESYNC=1, experiment): half the tile's MMA time, if there are >= 2 waves
-    static const int on = [] { const char *e = std::getenv("NC_GEMM_DESYNC"); return e ? std::atoi(e) : 0; }();
-    const long long mma_cycles = (long long)nspan * KPP * 12 * (BN / 2);   // ~2 cycles per pair-MMA column
-    aa.desync = (on && tiles >= 2 * pairs_avail) ? (int)(mma_cycles / 2) : 0;
-  }
   int nsplit = 1;
   aa.sps = 0;
   // Measured at M = 8 (tools/splitk_time.py): every launch costs ~8 us fixed and each 32-wide
