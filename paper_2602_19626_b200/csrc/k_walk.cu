@@ -1510,7 +1510,13 @@ static int walk_cluster_size(uint32_t V, int n_chunks) {
   // per token 8.0k -> 6.0k cycles).  The rule's inputs are the vocabulary and the
   // CONTAINER's chunk count (the decoder reads it from the header; a shard passes the total).
   if (n_chunks <= 2 && V >= 32768 && V % 1024 == 0) return 16;
-  return (V >= 32768 && V % 256 == 0) ? 8 : 4;
+  // Many chunks: the walk's clusters run in waves beside the next slab's forward and their
+  // SM-time is what the step pays -- 4-CTA clusters hold half the SMs per chunk for ~1.4x
+  // the per-token time (config3, 64 chunks: walk 772 -> 573 ms of kernel time, step
+  // 4781 -> 4709 ms).  8 CTAs while one wave of clusters fits the B200's 148 SMs (a
+  // constant, not the device's count: the rule must not depend on the decoding GPU).
+  if (V >= 32768 && V % 256 == 0 && n_chunks * 8 <= 148) return 8;
+  return 4;
 }
 
 template <int CS, int NGM>

@@ -98,14 +98,15 @@ def test_walk_dump_gaussian(nc, V, n, flags, bits):
     check_dump(d, ref, toks, V, bits, warm)
 
 
-@pytest.mark.parametrize("n_chunks", [1, 8])
+@pytest.mark.parametrize("n_chunks", [1, 8, 64])
 def test_walk_dump_cluster_sizes(nc, n_chunks):
-    """V = 49,152 with the walk's two large-vocabulary cluster sizes: 16 CTAs (a container of
-    1-2 chunks) and 8 CTAs (more chunks) -- the cluster reductions differ, the bars do not."""
+    """V = 49,152 with the walk's three large-vocabulary cluster sizes: 16 CTAs (a container of
+    1-2 chunks), 8 (up to 18 chunks: one wave of clusters on 148 SMs) and 4 (more chunks) --
+    the cluster reductions differ, the bars do not."""
     from oracle.ensemble import Params, encode_tokens
     from synth.logits import markov_tokens
     V, n = 49152, 900
-    assert nc.nc_host_walk_ctas(V, n_chunks) == (16 if n_chunks <= 2 else 8)
+    assert nc.nc_host_walk_ctas(V, n_chunks) == (16 if n_chunks <= 2 else 8 if 8 * n_chunks <= 148 else 4)
     rng = np.random.default_rng(n_chunks)
     Z = (rng.standard_normal((n, V)) * 1.5).astype(np.float32)
     toks = markov_tokens(V, n, 5)
