@@ -372,58 +372,70 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
 #pragma unroll
         for (int d = 0; d < 32; ++d) O[d] = __fmaf_rn(O[d], al, __uint_as_float(x0[d]));
       };
+      // a warp whose 32 rows are all past the tile's rows (decode tiles hold 1-3 rows; ragged
+      // tails) skips its TMEM loads, exponentials, P stores and folds -- the MMAs compute its
+      // rows from whatever P holds, and those rows are never stored (rows are independent) --
+      // but keeps every barrier arrival
+      const bool idle = q * 32 >= xi.t.nrows;
       for (int i = 0; i < xi.nkb; ++i, ++gb) {
         tc::mbar_wait(s_full, gb & 1);
         AT_T(0);   // wait S
         tc::fence_after();
-        uint32_t sr[2][32];
-        tc::tmem_ld32(tmem + T_S + 64 * x + lane_off, sr[0]);
-        tc::tmem_ld32(tmem + T_S + 64 * x + lane_off + 32, sr[1]);
-        tc::tmem_wait_ld();
+        const int key0 = (xi.kb0 + i) * AK + AH * x;
+        float xs[2][32];
+        float mloc = -CUDART_INF_F;
+        if (!idle) {
+          uint32_t sr[2][32];
+          tc::tmem_ld32(tmem + T_S + 64 * x + lane_off, sr[0]);
+          tc::tmem_ld32(tmem + T_S + 64 * x + lane_off + 32, sr[1]);
+          tc::tmem_wait_ld();
+          if (key0 + AH - 1 <= j) {              // whole half inside the window: no masking
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+              for (int k = 0; k < 32; ++k) xs[hh][k] = __uint_as_float(sr[hh][k]);
+          } else {
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+              for (int k = 0; k < 32; ++k)
+                xs[hh][k] = key0 + 32 * hh + k <= j ? __uint_as_float(sr[hh][k]) : -CUDART_INF_F;
+          }
+          // max on the raw scores (kScale > 0, RN monotone: exact), as a tree
+          float tt[32];
+#pragma unroll
+          for (int k = 0; k < 32; ++k) tt[k] = fmaxf(xs[0][k], xs[1][k]);
+#pragma unroll
+          for (int w2 = 16; w2 >= 1; w2 >>= 1)
+#pragma unroll
+            for (int k = 0; k < w2; ++k) tt[k] = fmaxf(tt[k], tt[k + w2]);
+          mloc = __fmul_rn(tt[0], kScale);
+        }
         tc::fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(s_empty);
-        const int key0 = (xi.kb0 + i) * AK + AH * x;
-        float xs[2][32];
-        if (key0 + AH - 1 <= j) {              // whole half inside the window: no masking
-#pragma unroll
-          for (int hh = 0; hh < 2; ++hh)
-#pragma unroll
-            for (int k = 0; k < 32; ++k) xs[hh][k] = __uint_as_float(sr[hh][k]);
-        } else {
-#pragma unroll
-          for (int hh = 0; hh < 2; ++hh)
-#pragma unroll
-            for (int k = 0; k < 32; ++k)
-              xs[hh][k] = key0 + 32 * hh + k <= j ? __uint_as_float(sr[hh][k]) : -CUDART_INF_F;
-        }
-        // max on the raw scores (kScale > 0, RN monotone: exact), as a tree
-        float tt[32];
-#pragma unroll
-        for (int k = 0; k < 32; ++k) tt[k] = fmaxf(xs[0][k], xs[1][k]);
-#pragma unroll
-        for (int w2 = 16; w2 >= 1; w2 >>= 1)
-#pragma unroll
-          for (int k = 0; k < w2; ++k) tt[k] = fmaxf(tt[k], tt[k + w2]);
         // the row's two halves exchange their maxima
-        xmax[128 * x + r] = __fmul_rn(tt[0], kScale);
+        xmax[128 * x + r] = mloc;
         named_bar(3, 256);
         const float mb = fmaxf(xmax[r], xmax[128 + r]);   // same operand order in both halves
         named_bar(3, 256);                         // both read before the next exchange writes
-        const float mn = fmaxf(m, mb);
-        const float alpha = (mn == -CUDART_INF_F) ? 1.f : tc::ex2(__fsub_rn(m, mn));
-        const float nmn = mn == -CUDART_INF_F ? 0.f : -mn;
-        float ps4[4] = {0.f, 0.f, 0.f, 0.f};   // 4 independent partial sums (latency), fixed order
+        float alpha = 1.f;
+        if (!idle) {
+          const float mn = fmaxf(m, mb);
+          alpha = (mn == -CUDART_INF_F) ? 1.f : tc::ex2(__fsub_rn(m, mn));
+          const float nmn = mn == -CUDART_INF_F ? 0.f : -mn;
+          float ps4[4] = {0.f, 0.f, 0.f, 0.f};   // 4 independent partial sums (latency), fixed order
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh)
+          for (int hh = 0; hh < 2; ++hh)
 #pragma unroll
-          for (int k = 0; k < 32; ++k) {
-            xs[hh][k] = tc::ex2(__fmaf_rn(xs[hh][k], kScale, nmn));   // masked: ex2(-inf) = 0
-            ps4[k & 3] = __fadd_rn(ps4[k & 3], xs[hh][k]);
-          }
-        const float ps = __fadd_rn(__fadd_rn(ps4[0], ps4[1]), __fadd_rn(ps4[2], ps4[3]));
-        l = __fmaf_rn(l, alpha, ps);
-        m = mn;
+            for (int k = 0; k < 32; ++k) {
+              xs[hh][k] = tc::ex2(__fmaf_rn(xs[hh][k], kScale, nmn));   // masked: ex2(-inf) = 0
+              ps4[k & 3] = __fadd_rn(ps4[k & 3], xs[hh][k]);
+            }
+          const float ps = __fadd_rn(__fadd_rn(ps4[0], ps4[1]), __fadd_rn(ps4[2], ps4[3]));
+          l = __fmaf_rn(l, alpha, ps);
+          m = mn;
+        }
         AT_T(1);   // S load + max/exp/sum
         // the P buffers and the O partial were last used by PV(gb-1): wait for it (within the
         // item; the previous item's last PV was waited for at its end), store P, fold
@@ -432,23 +444,25 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
           tc::fence_after();
         }
         AT_T(2);   // wait PV(i-1)
-        const uint32_t ph_t = tmem + T_P + 128 * x + lane_off;
+        if (!idle) {
+          const uint32_t ph_t = tmem + T_P + 128 * x + lane_off;
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          uint32_t hi[32], lo[32];
+          for (int hh = 0; hh < 2; ++hh) {
+            uint32_t hi[32], lo[32];
 #pragma unroll
-          for (int k = 0; k < 32; ++k) {
-            float fh, fl;
-            tc::split_tf32(xs[hh][k], fh, fl);
-            hi[k] = __float_as_uint(fh);
-            lo[k] = __float_as_uint(fl);
+            for (int k = 0; k < 32; ++k) {
+              float fh, fl;
+              tc::split_tf32(xs[hh][k], fh, fl);
+              hi[k] = __float_as_uint(fh);
+              lo[k] = __float_as_uint(fl);
+            }
+            tc::tmem_st32(ph_t + 32 * hh, hi);
+            tc::tmem_st32(ph_t + 64 + 32 * hh, lo);
           }
-          tc::tmem_st32(ph_t + 32 * hh, hi);
-          tc::tmem_st32(ph_t + 64 + 32 * hh, lo);
+          if (i >= 1) fold(alpha_prev);
+          tc::tmem_wait_st();
         }
-        if (i >= 1) fold(alpha_prev);
         alpha_prev = alpha;
-        tc::tmem_wait_st();
         tc::fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(p_full);
@@ -457,7 +471,7 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
       tc::mbar_wait(pv_done, (gb - 1) & 1);
       AT_T(4);   // wait last PV
       tc::fence_after();
-      fold(alpha_prev);
+      if (!idle) fold(alpha_prev);
       // row sum: the two halves' partial sums (same order in both), then this half's dims
       xmax[128 * x + r] = l;
       named_bar(3, 256);
