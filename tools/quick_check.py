@@ -23,7 +23,8 @@ model = nc.Model(path, 0)
 data = open(ensure_text(wl.name), "rb").read()
 tokens, ntok = nc.nc_tokenize(model, data, wl.n_chunks)
 tok = torch.from_numpy(tokens.view(np.int32).copy()).cuda()
-prm = nc.nc_params_default(window=wl.window, slide=wl.slide, n_chunks=wl.n_chunks, cdf_bits=wl.cdf_bits)
+prm = nc.nc_params_default(window=wl.window, slide=wl.slide, n_chunks=wl.n_chunks, cdf_bits=wl.cdf_bits,
+                           flags=int(os.environ.get("QC_FLAGS", "3")))
 s = torch.cuda.current_stream()
 for _ in range(2):
     nc.nc_compress_tokens(model, tok.data_ptr(), ntok, prm, s.cuda_stream)
