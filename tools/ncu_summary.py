@@ -81,6 +81,8 @@ def full(tag, name, rep):
         wr = float(r[idx["dram__bytes_write.sum"]].replace(",", "")) * (1e6 if units[idx["dram__bytes_write.sum"]] == "Mbyte" else 1e3 if units[idx["dram__bytes_write.sum"]] == "Kbyte" else 1e9 if units[idx["dram__bytes_write.sum"]] == "Gbyte" else 1)
         base = kn.split("(")[0].replace("void ", "").strip()
         base = re.sub(r"gemm_tc_kernel<\(?\w*\)?(\d+), \(?\w*\)?\d+(, \(?\w*\)?\w+)?>", r"gemm_tc_kernel<\1>", base)
+        if base.startswith("walk_cl_kernel") or base.startswith("nc::walk_cl_kernel"):
+            base = "walk_cl_kernel<8>"
         alts = CLASS.get(base, base).split("|")   # several classes share a kernel: capture order
         k_ = seen.get(base, 0)
         seen[base] = k_ + 1
