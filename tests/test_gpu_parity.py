@@ -768,3 +768,80 @@ def test_hf_checkpoint_forward_tokenizer_roundtrip(nc):
         _, _, p_gpu = nc.nc_debug_walk(zz, t, prm)
         assert (np.abs(p_gpu - p_ref) / p_ref).max() < P_TOL
     m.close()
+
+
+@pytest.mark.slow
+def test_config3_full_size_chunk_stream_and_p(nc):
+    """config3 at full size in bench.py's launch configuration (10 MB, 64 chunks, 30 layers,
+    L = 2048 / C = 512, 512-position slabs, 4-CTA walk clusters): the container's structure;
+    chunk 17's stream (~39K tokens) equals the host WNC encoding of its forward + walk run
+    alone (batch / slab independence at full size); the §8(c) coder bound on its bit count;
+    and the fp64 oracle (blocked LM + walk) on the chunk's first 2,600 rows (one slide):
+    logits within 1e-5 of max|z| on sampled rows, p(t) within 1e-4 at every one of them."""
+    import struct
+    from oracle.chunking import split_chunks
+    from oracle.ensemble import Params, encode_tokens
+    from oracle.lm import LM
+    from oracle.ncw import Weights
+    from oracle.tokenizer import Tokenizer
+    from synth import WORKLOADS, ensure_model, ensure_text
+    wl = WORKLOADS["config3"]
+    path = ensure_model(wl.shape)
+    data = open(ensure_text("config3"), "rb").read()
+    m = nc.Model(path, 0)
+    prm = nc.nc_params_default(window=wl.window, slide=wl.slide, n_chunks=wl.n_chunks)
+    toks, ntok = nc.nc_tokenize(m, data, wl.n_chunks)
+    td = torch.from_numpy(toks.view(np.int32).copy()).cuda()
+    blob = nc.nc_compress_tokens(m, td.data_ptr(), ntok, prm, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    n = struct.unpack_from("<BHH", blob, 4)[2]
+    assert n == wl.n_chunks == len(ntok)
+    table = [struct.unpack_from("<III", blob, 9 + 12 * c) for c in range(n)]
+    assert [t[0] for t in table] == list(ntok)
+    assert len(blob) == 9 + 12 * n + sum(t[2] for t in table)
+    c = 17
+    off = 9 + 12 * n + sum(t[2] for t in table[:c])
+    t = [int(v) for v in toks[int(sum(ntok[:c])):int(sum(ntok[:c + 1]))]]
+    assert len(t) > 30000
+    x = [0] + t[:-1]
+    z = nc.nc_debug_forward(m, x, nc.nc_params_default(window=wl.window, slide=wl.slide), 0)
+    cum, freq, p_gpu = nc.nc_debug_walk(z, t, prm)            # prm.n_chunks = 64: the container's walk
+    stream, bits = nc.nc_host_wnc_encode(cum, freq, 24)
+    assert bits == table[c][1] and stream == blob[off:off + table[c][2]]
+    T = 1 << 24
+    f = freq.astype(np.float64)
+    assert bits <= (-np.log2(f / T) - np.log2(1.0 - 2.0 ** (24 - 30) / f)).sum() + 64
+    w = Weights(path)
+    nr = 2600
+    Z = LM(w).forward_blocked(x[:nr], wl.window, wl.slide)
+    rows = sorted(set([0, 99, 100, 2047, 2048, nr - 1] + list(range(0, nr, 131))))
+    assert np.abs(z[rows] - Z[rows]).max() / np.abs(Z[rows]).max() < Z_TOL
+    ref = encode_tokens(Z, t[:nr], w.V, Params(window=wl.window, slide=wl.slide))
+    p_ref = np.array(ref["p_true"])
+    assert (np.abs(p_gpu[:nr] - p_ref) / p_ref).max() < P_TOL
+    m.close()
+
+
+@pytest.mark.slow
+def test_full_model_head_only_end_to_end(nc):
+    """The LLM visible end to end: with the N-gram off (flags = 2) the coded distribution is
+    the head's p~ = softmax(z + b) on every row, so the 30-layer forward drives every code.
+    GPU compress -> decompress round trip; size within 0.5 % of the oracle pipeline (fp64
+    blocked LM + walk) and p(t) within 1e-4 at every row (3 window slides)."""
+    from oracle.ensemble import Params
+    from oracle.ncw import Weights
+    from synth import ensure_model, make_text
+    path = ensure_model("smollm2-135m")
+    m = nc.Model(path, 0)
+    w = Weights(path)
+    data = make_text("alice", 16000, 2024)
+    prm = nc.nc_params_default(window=1024, slide=256, n_chunks=1, flags=2)
+    blob = nc.nc_compress(m, data, prm)
+    assert nc.nc_decompress(m, blob, prm) == data
+    size, ps, xs, ts = _oracle_size_and_p(w, data, Params(window=1024, slide=256, n_chunks=1, flags=2))
+    assert len(ts[0]) > 1024 + 2 * 256
+    assert abs(len(blob) - size) <= 0.005 * size, (len(blob), size)
+    z = nc.nc_debug_forward(m, xs[0], prm, 0)
+    _, _, p_gpu = nc.nc_debug_walk(z, ts[0], prm)
+    assert (np.abs(p_gpu - ps[0]) / ps[0]).max() < P_TOL
+    m.close()
