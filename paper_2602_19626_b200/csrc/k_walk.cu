@@ -1536,8 +1536,14 @@ static void launch_walk_cs(const WalkArgs &a, cudaStream_t s) {
     const size_t vmax = (size_t)4 * NGM * WT;
     const size_t gmax = std::max<size_t>(vmax / 4, (size_t)CS * vmax / 32);   // V <= CS vmax
     const size_t dmax = vmax * 8 + vmax * 4 + vmax * 4 + ((vmax + 31) / 32) * 4 + gmax * 4 + 64;
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, walk_cl_kernel<CS, NGM>);
+    const size_t cap = (size_t)std::max(0, optin - (int)fa.sharedSizeBytes);   // what static smem leaves
     check_launch(cudaFuncSetAttribute(walk_cl_kernel<CS, NGM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)std::min<size_t>(dmax, 200 * 1024)),
+                                      (int)std::min(dmax, cap)),
                  "walk smem attribute");
     if (CS > 1)
       check_launch(cudaFuncSetAttribute(walk_cl_kernel<CS, NGM>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
