@@ -24,6 +24,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from .ans import AnsDecoder, AnsEncoder
 from .cdf import quantize
 from .coder import Decoder, Encoder
 from .ngram import NGram
@@ -62,6 +63,7 @@ class Params:
     w_llm0: float = 0.85
     lmax_minus_one: bool = False    # NEXT-4 / D10: L_max = L - 1 instead of L
     refresh: bool = False           # NEXT-4: refresh window semantics (naive re-evaluation)
+    coder: str = "wnc"              # "wnc": 32-bit arithmetic coder; "ans": rANS
 
     @property
     def lmax(self):
@@ -140,7 +142,7 @@ def encode_tokens(Z, toks, V, prm: Params, keep_rows=()):
     Returns dict(stream, bits, cum, freq, p_true, pt_true, rows={j: (p, pt)}, w_llm) -- w_llm[j] is
     the mixer's LLM weight used for row j (None where no mix happens)."""
     cm = ChunkModel(V, prm)
-    enc = Encoder()
+    enc = AnsEncoder() if prm.coder == "ans" else Encoder()
     cum, freq, p_true, pt_true, rows, skipped, h_ng, w_llm = [], [], [], [], {}, [], [], []
     keep = set(keep_rows)
     for j, t in enumerate(toks):
@@ -160,14 +162,14 @@ def encode_tokens(Z, toks, V, prm: Params, keep_rows=()):
         cm.update(t, pt, png)
     stream, bits = enc.finish()
     return dict(stream=stream, bits=bits, cum=cum, freq=freq, p_true=p_true,
-                pt_true=pt_true, rows=rows, min_range=enc.min_range, skipped=skipped, h_ng=h_ng,
-                w_llm=w_llm)
+                pt_true=pt_true, rows=rows, min_range=getattr(enc, "min_range", None), skipped=skipped,
+                h_ng=h_ng, w_llm=w_llm)
 
 
 def decode_tokens(step, n, stream, V, prm: Params):
     """step(x) -> logits row for LM input token x (BOS first).  Returns tokens."""
     cm = ChunkModel(V, prm)
-    dec = Decoder(stream)
+    dec = AnsDecoder(stream) if prm.coder == "ans" else Decoder(stream)
     out = []
     x = None
     for j in range(n):
@@ -179,4 +181,6 @@ def decode_tokens(step, n, stream, V, prm: Params):
         out.append(t)
         cm.update(t, pt, png)
         x = t
+    if prm.coder == "ans" and not dec.finished_ok():
+        raise ValueError("rANS stream does not end in the start state (corrupt stream or wrong params)")
     return out

@@ -105,6 +105,24 @@ def test_pipeline_window_variants_roundtrip(tiny_weights, refresh, lm1):
     assert blob != compress(data, tiny_weights, Params(window=16, slide=4, n_chunks=2))
 
 
+@pytest.mark.parametrize("flags,bits,chunks", [(3, 24, 2), (0, 16, 1), (7, 24, 1)])
+def test_pipeline_ans_roundtrip(tiny_weights, flags, bits, chunks):
+    """the rANS coder through the whole oracle pipeline: round trip, and the
+    same per-token counts as the arithmetic coder (only the entropy coder differs), so the
+    two container sizes differ by the coders' few bytes of overhead per chunk"""
+    from synth import make_text
+    data = make_text("alice", 900, 31)
+    pa = Params(window=16, slide=4, n_chunks=chunks, flags=flags, cdf_bits=bits, coder="ans")
+    pw = Params(window=16, slide=4, n_chunks=chunks, flags=flags, cdf_bits=bits)
+    blob = compress(data, tiny_weights, pa)
+    assert decompress(blob, tiny_weights, pa) == data
+    ra, rw = [], []
+    compress(data, tiny_weights, pa, collect=ra)
+    compress(data, tiny_weights, pw, collect=rw)
+    assert [r["freq"] for r in ra] == [r["freq"] for r in rw]
+    assert abs(len(blob) - len(compress(data, tiny_weights, pw))) <= 12 * chunks
+
+
 def test_pipeline_empty_and_binary(tiny_weights):
     prm = Params(window=16, slide=4, warmup=5, n_chunks=2)
     for data in (b"", b"\x00\x01\xff" * 10, b"\n\n\n"):
