@@ -80,7 +80,17 @@ typedef struct {
   uint32_t debug_dump;   /* test only: nonzero -> keep per-token p(t) values  */
   uint32_t window_variant; /* NC_WINDOW_* bits, default 0 = retained KV with
                               L_max = L (D9-D10, what the paper ran) */
+  uint32_t coder;        /* NC_CODER_WNC (default) or NC_CODER_ANS; like L and C it is not
+                            stored in the container: the decoder must pass the same value */
 } nc_params;
+
+/* Entropy coder of the chunk streams.  NC_CODER_WNC: the paper's 32-bit arithmetic coder
+ * (D7-D8).  NC_CODER_ANS: rANS, the paper's future-work replacement (
+ * reading D39): 64-bit state in [2^31, 2^64), 32-bit renormalisation words, symbols coded in
+ * reverse on the host, decoded forward on the device; bit_count = 32 x words; a stream whose
+ * decoder does not end in the start state 2^31 with every word consumed is NC_ERR_INTEGRITY. */
+#define NC_CODER_WNC 0u
+#define NC_CODER_ANS 1u
 
 /* Window variants, nc_params.window_variant.  Not stored in the
  * container: the decoder must pass the same value (a mismatch fails the integrity checks). */
@@ -267,6 +277,9 @@ nc_status nc_debug_attention(int device, const float *q, const float *k, const f
 nc_status nc_host_split(const uint8_t *in, size_t n, uint32_t n_chunks, uint64_t *cuts,
                         uint32_t *n_cuts); /* cuts: n_chunks+1 capacity, chunk i = [cuts[i], cuts[i+1]) */
 nc_status nc_host_wnc_encode(const uint32_t *cum, const uint32_t *freq, size_t n, uint32_t cdf_bits,
+                             uint8_t **stream, size_t *stream_n, uint64_t *bit_count);
+/* rANS encoding of (cum, freq) pairs in coding order (NC_CODER_ANS's stream of one chunk). */
+nc_status nc_host_ans_encode(const uint32_t *cum, const uint32_t *freq, size_t n, uint32_t cdf_bits,
                              uint8_t **stream, size_t *stream_n, uint64_t *bit_count);
 nc_status nc_host_tokenize_vocab(const uint8_t *vocab_blob, const uint32_t *vocab_len, uint32_t V,
                                  uint32_t n_special, const uint8_t *in, size_t n,

@@ -14,6 +14,7 @@ STATUS_NAMES = {0: "NC_OK", 1: "NC_ERR_FORMAT", 2: "NC_ERR_BACKEND", 3: "NC_ERR_
                 5: "NC_ERR_TRUNCATED", 6: "NC_ERR_INTEGRITY"}
 FLAG_NGRAM, FLAG_HEAD, FLAG_SKIP = 1, 2, 4
 WINDOW_REFRESH, WINDOW_LMAX_M1 = 1, 2          # nc_params.window_variant (NEXT-4)
+CODER_WNC, CODER_ANS = 0, 1                    # nc_params.coder (NEXT-4, D39)
 
 # every symbol declared in include/nc.h (checked by tests/test_abi.py)
 EXPORTS = [
@@ -23,7 +24,7 @@ EXPORTS = [
     "nc_host_segment", "nc_host_blob_encode", "nc_host_blob_decode", "nc_compress_tokens", "nc_comm_unique_id",
     "nc_comm_init", "nc_comm_free", "nc_compress_shard", "nc_decompress_shard", "nc_free",
     "nc_last_error", "nc_last_stats", "nc_debug_quantize", "nc_debug_walk", "nc_debug_walk_dump", "nc_debug_forward",
-    "nc_host_split", "nc_host_wnc_encode", "nc_host_tokenize_vocab", "nc_host_shard_range", "nc_host_walk_ctas",
+    "nc_host_split", "nc_host_wnc_encode", "nc_host_ans_encode", "nc_host_tokenize_vocab", "nc_host_shard_range", "nc_host_walk_ctas",
     "nc_host_shard_part", "nc_set_profiling", "nc_profile", "nc_debug_set_splitk", "nc_debug_gemm", "nc_debug_attention",
 ]
 
@@ -40,7 +41,7 @@ class nc_params(C.Structure):
                 ("eta", C.c_double), ("alpha", C.c_double), ("ngram_orders", C.c_uint32),
                 ("ngram_cap", C.c_uint32), ("n_chunks", C.c_uint32), ("chunks_per_gpu", C.c_uint32),
                 ("max_slab_rows", C.c_uint32), ("debug_dump", C.c_uint32),
-                ("window_variant", C.c_uint32)]
+                ("window_variant", C.c_uint32), ("coder", C.c_uint32)]
 
 
 _lib = None
@@ -94,6 +95,7 @@ def lib():
             "nc_debug_gemm": (C.c_int, [C.c_int, f32p, f32p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int, f32p]),
             "nc_host_split": (C.c_int, [P, C.c_size_t, C.c_uint32, u64p, u32p]),
             "nc_host_wnc_encode": (C.c_int, [u32p, u32p, C.c_size_t, C.c_uint32, pp, szp, u64p]),
+            "nc_host_ans_encode": (C.c_int, [u32p, u32p, C.c_size_t, C.c_uint32, pp, szp, u64p]),
             "nc_host_tokenize_vocab": (C.c_int, [P, u32p, C.c_uint32, C.c_uint32, P, C.c_size_t, pp, szp]),
             "nc_host_shard_range": (C.c_int, [C.c_uint32, C.c_int, C.c_int, u32p, u32p]),
             "nc_host_walk_ctas": (C.c_int, [C.c_uint32, C.c_uint32, u32p]),
@@ -349,6 +351,15 @@ def nc_host_wnc_encode(cum, freq, cdf_bits: int):
     f, fp = _u32(freq)
     s, sn, bits = C.c_void_p(), C.c_size_t(), C.c_uint64()
     _check(lib().nc_host_wnc_encode(cp, fp, len(c), cdf_bits, C.byref(s), C.byref(sn), C.byref(bits)))
+    return _take_bytes(s.value, sn.value), bits.value
+
+
+def nc_host_ans_encode(cum, freq, cdf_bits: int):
+    """rANS stream of (cum, freq) pairs in coding order (NC_CODER_ANS, D39)."""
+    c, cp = _u32(cum)
+    f, fp = _u32(freq)
+    s, sn, bits = C.c_void_p(), C.c_size_t(), C.c_uint64()
+    _check(lib().nc_host_ans_encode(cp, fp, len(c), cdf_bits, C.byref(s), C.byref(sn), C.byref(bits)))
     return _take_bytes(s.value, sn.value), bits.value
 
 

@@ -79,6 +79,7 @@ void nc_params_default(nc_params *p) {
   p->max_slab_rows = 32768;
   p->debug_dump = 0;
   p->window_variant = 0;
+  p->coder = NC_CODER_WNC;
 }
 
 nc_status nc_set_allocator(void *(*alloc)(size_t, void *), void (*free_fn)(void *, void *), void *ctx) {
@@ -561,6 +562,22 @@ nc_status nc_host_wnc_encode(const uint32_t *cum, const uint32_t *freq, size_t n
     }
     std::vector<uint8_t> s;
     enc.finish(s, *bit_count);
+    *stream = dup_out(s);
+    *stream_n = s.size();
+  });
+}
+
+nc_status nc_host_ans_encode(const uint32_t *cum, const uint32_t *freq, size_t n, uint32_t cdf_bits, uint8_t **stream,
+                             size_t *stream_n, uint64_t *bit_count) {
+  if ((!cum || !freq) && n) return set_err(NC_ERR_INVALID, "null argument");
+  if (!stream || !stream_n || !bit_count) return set_err(NC_ERR_INVALID, "null argument");
+  *stream = nullptr; *stream_n = 0;
+  return guard([&] {
+    if (cdf_bits < 1 || cdf_bits > 31) nc::fail(NC_ERR_INVALID, "cdf_bits");
+    for (size_t i = 0; i < n; ++i)
+      if ((uint64_t)cum[i] + freq[i] > (1ull << cdf_bits)) nc::fail(NC_ERR_INVALID, "interval beyond T");
+    std::vector<uint8_t> s;
+    nc::ans_encode(cum, freq, n, cdf_bits, s, *bit_count);
     *stream = dup_out(s);
     *stream_n = s.size();
   });

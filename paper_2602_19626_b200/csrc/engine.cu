@@ -667,7 +667,7 @@ struct WalkBufs {
     a.st = st; a.b = b; a.cu = cu; a.spadd = spadd; a.ng_keys = keys; a.ng_vals = vals; a.ng_recs = recs;
     a.hcap = hcap; a.rcap = rcap; a.ng_pre = ng_pre; a.ng_ring = ng_ring; a.ng_spadd = ng_spadd;
     a.V = V; a.cdf_bits = p.cdf_bits; a.warmup = p.warmup; a.flags = p.flags; a.orders = p.orders; a.cap = p.cap;
-    a.inv_tau = (float)p.inv_tau; a.alpha = p.alpha; a.eta = p.eta;
+    a.inv_tau = (float)p.inv_tau; a.alpha = p.alpha; a.eta = p.eta; a.coder = p.coder;
   }
 };
 
@@ -921,10 +921,15 @@ void encode_container(const Params &p, const std::vector<uint32_t> &ntok, const 
   for (size_t c = 0; c < n; ++c)
     if (co.err[c]) fail(NC_ERR_INTEGRITY, "quantizer residual would drop a count below 1 (D6)");
   auto work = [&](size_t c) {
-    WncEncoder enc;
-    for (size_t i = off[c]; i < off[c + 1]; ++i) enc.encode(co.cum[i], co.freq[i], p.cdf_bits);
     uint64_t bits;
-    enc.finish(chunks[c].stream, bits);
+    if (p.coder == NC_CODER_ANS) {
+      ans_encode(co.cum.data() + off[c], co.freq.data() + off[c], off[c + 1] - off[c], p.cdf_bits,
+                 chunks[c].stream, bits);
+    } else {
+      WncEncoder enc;
+      for (size_t i = off[c]; i < off[c + 1]; ++i) enc.encode(co.cum[i], co.freq[i], p.cdf_bits);
+      enc.finish(chunks[c].stream, bits);
+    }
     if (bits > 0xFFFFFFFFull) fail(NC_ERR_INVALID, "chunk bitstream exceeds the u32 bit_count field");
     chunks[c].bits = (uint32_t)bits;
     chunks[c].tokens = ntok[c];
@@ -1096,6 +1101,15 @@ void decompress_device(nc_model *m, const uint8_t *blob, const Nc05View &view, c
   cudaEventDestroy(e1);
   for (int c = 0; c < n_chunks; ++c) {
     if (hs[c].err) fail(NC_ERR_INTEGRITY, "decoder integrity failure in chunk " + std::to_string(c));
+    if (p.coder == NC_CODER_ANS) {
+      // rANS (D39): the decoder ends in the encoder's start state L = 2^31 having read every
+      // word, and the stream is whole words with nothing after them
+      if (ntok[c] && (hs[c].value != (1ull << 31) || hs[c].bitpos != s_bits[c] ||
+                      (uint64_t)view.ents[c].len * 8 != s_bits[c]))
+        fail(NC_ERR_INTEGRITY, "rANS end state of chunk " + std::to_string(c) + " is not the encoder's start state (wrong params or corrupt stream)");
+      toks[c].assign(all.begin() + tok_off[c], all.begin() + tok_off[c] + ntok[c]);
+      continue;
+    }
     // every renormalisation shift of the decoder matches one encoder step;
     // bit_count = steps + 2 (finish emits 1 + (pending+1) bits)  (D8)
     if (ntok[c] && hs[c].bitpos - 32 + 2 != s_bits[c])

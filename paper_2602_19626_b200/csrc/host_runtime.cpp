@@ -185,6 +185,31 @@ void WncEncoder::finish(std::vector<uint8_t> &out, uint64_t &bit_count) {
   out.swap(bytes_);
 }
 
+// ------------------------------------------------------------------ rANS ---
+void ans_encode(const uint32_t *cum, const uint32_t *freq, size_t n, uint32_t cdf_bits,
+                std::vector<uint8_t> &out, uint64_t &bit_count) {
+  constexpr uint64_t L = 1ull << 31;
+  uint64_t x = L;
+  std::vector<uint32_t> words;                       // in emission order (reversed below)
+  for (size_t k = n; k-- > 0;) {                     // rANS codes the symbols in reverse
+    const uint64_t f = freq[k];
+    if (f == 0) fail(NC_ERR_INTEGRITY, "zero-width symbol interval");
+    const uint64_t x_max = ((L >> cdf_bits) << 32) * f;
+    if (x >= x_max) {
+      words.push_back((uint32_t)x);
+      x >>= 32;
+    }
+    x = ((x / f) << cdf_bits) + x % f + cum[k];
+  }
+  words.push_back((uint32_t)x);                      // flush: low, then high (reversed: high first)
+  words.push_back((uint32_t)(x >> 32));
+  out.clear();
+  out.reserve(4 * words.size());
+  for (size_t k = words.size(); k-- > 0;)
+    for (int by = 3; by >= 0; --by) out.push_back((uint8_t)(words[k] >> (8 * by)));
+  bit_count = 32ull * words.size();
+}
+
 // ------------------------------------------------------------------ NC05 ---
 static void put_u16(std::vector<uint8_t> &o, uint16_t v) { o.push_back(v & 255); o.push_back(v >> 8); }
 static void put_u32(std::vector<uint8_t> &o, uint32_t v) {
@@ -268,6 +293,8 @@ Params validate(const nc_params *p) {
   q.debug_dump = p->debug_dump;
   if (p->window_variant & ~3u) fail(NC_ERR_INVALID, "window_variant: only bits 0-1 are defined");
   q.refresh = (p->window_variant & NC_WINDOW_REFRESH) != 0;
+  if (p->coder > NC_CODER_ANS) fail(NC_ERR_INVALID, "coder must be NC_CODER_WNC or NC_CODER_ANS");
+  q.coder = p->coder;
   q.lmax = (p->window_variant & NC_WINDOW_LMAX_M1) ? q.window - 1 : q.window;
   return q;
 }

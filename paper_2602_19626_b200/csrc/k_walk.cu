@@ -75,6 +75,13 @@ __device__ __forceinline__ double b_step(double b, float pt, bool is_t, double a
 // floor() and the integer conversion run on the FMA/ALU pipes, no SFU-class
 // FRND/F2I: for 0 <= x < 2^23, x + 2^23 rounded down holds floor(x) in its low
 // mantissa bits (exact); every float >= 2^23 is an integer, read from its bits.
+// rANS stream word at bit position bp (a multiple of 32; big-endian; 0 past the end, D39)
+__device__ __forceinline__ unsigned long long ans_word(const uint8_t *s, unsigned long long bp,
+                                                       unsigned long long nb) {
+  if (bp + 32 > nb) return 0ull;
+  const uint8_t *q = s + (bp >> 3);
+  return ((unsigned long long)q[0] << 24) | ((unsigned long long)q[1] << 16) | ((unsigned long long)q[2] << 8) | q[3];
+}
 __device__ __forceinline__ uint32_t quant(float p, float TmV) {
   const float x = __fmul_rn(p, TmV);
   const float t = __fadd_rd(x, 8388608.f);
@@ -786,12 +793,17 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
     s_lw[0] = st->lw[0]; s_lw[1] = st->lw[1];
     s_w[0] = st->wl; s_w[1] = st->wn;
     s_i = st->i;
-    if (!enc && st->i == 0 && rank == 0) {   // prime the decoder with 32 bits
+    if (!enc && st->i == 0 && rank == 0) {
       const uint8_t *s = a.streams + a.stream_off[c];
       const unsigned long long nb = a.stream_bits[c];
-      unsigned long long v = 0;
-      for (int k = 0; k < 32; ++k) v = 2 * v + ((unsigned long long)k < nb ? (s[k >> 3] >> (7 - (k & 7))) & 1u : 0u);
-      st->low = 0; st->high = 0xFFFFFFFFull; st->value = v; st->bitpos = 32; st->pend = 0;
+      if (a.coder == 1) {   // rANS (D39): x = the first two words (the encoder's flush)
+        st->value = (ans_word(s, 0, nb) << 32) | ans_word(s, 32, nb);
+        st->bitpos = 64; st->low = 0; st->high = 0; st->pend = 0;
+      } else {              // WNC: prime the decoder with 32 bits
+        unsigned long long v = 0;
+        for (int k = 0; k < 32; ++k) v = 2 * v + ((unsigned long long)k < nb ? (s[k >> 3] >> (7 - (k & 7))) & 1u : 0u);
+        st->low = 0; st->high = 0xFFFFFFFFull; st->value = v; st->bitpos = 32; st->pend = 0;
+      }
     }
   }
   __syncthreads();
@@ -1271,8 +1283,12 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
         }
         scatter_list(i);
         if (lane == 0) {
-          const unsigned long long R = st->high - st->low + 1;
-          sm.target = ((st->value - st->low + 1) * T - 1) / R;
+          if (a.coder == 1) {   // rANS: the slot x mod T (D39)
+            sm.target = st->value & (T - 1);
+          } else {
+            const unsigned long long R = st->high - st->low + 1;
+            sm.target = ((st->value - st->low + 1) * T - 1) / R;
+          }
         }
       }
       __syncthreads();
@@ -1440,24 +1456,36 @@ __global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
             if (a.next_x) a.next_x[c] = tt;
             if (a.out_p) a.out_p[oi] = sm.p_t;
             if (a.out_pt) a.out_pt[oi] = sm.pt_t;
-            const unsigned long long Rg = st->high - st->low + 1;
-            unsigned long long lo = st->low, hi = st->low + ((Rg * (sm.cum_t + sm.freq_t)) >> a.cdf_bits) - 1;
-            lo = lo + ((Rg * sm.cum_t) >> a.cdf_bits);
-            unsigned long long val = st->value, bp = st->bitpos;
-            uint32_t pend = st->pend;
-            const uint8_t *s = a.streams + a.stream_off[c];
-            const unsigned long long nb = a.stream_bits[c];
-            for (;;) {
-              if (hi < HALF) { pend = 0; }
-              else if (lo >= HALF) { lo -= HALF; hi -= HALF; val -= HALF; pend = 0; }
-              else if (lo >= QTR && hi < 3 * QTR) { lo -= QTR; hi -= QTR; val -= QTR; ++pend; }
-              else break;
-              lo = 2 * lo; hi = 2 * hi + 1;
-              const unsigned long long bit = bp < nb ? (s[bp >> 3] >> (7 - (bp & 7))) & 1u : 0u;
-              val = 2 * val + bit;
-              ++bp;
+            if (a.coder == 1) {   // rANS: x = freq (x >> b) + slot - cum, then refill 32-bit words (D39)
+              const uint8_t *s = a.streams + a.stream_off[c];
+              const unsigned long long nb = a.stream_bits[c];
+              unsigned long long x = st->value, bp = st->bitpos;
+              x = sm.freq_t * (x >> a.cdf_bits) + (x & (T - 1)) - sm.cum_t;
+              // a valid stream refills at most once (x >= freq (L >> b) >= 1 before it); x = 0
+              // only comes from a corrupt stream and must not spin on zero words
+              for (int r = 0; r < 2 && x < (1ull << 31); ++r) { x = (x << 32) | ans_word(s, bp, nb); bp += 32; }
+              if (x < (1ull << 31)) st->err = 3;
+              st->value = x; st->bitpos = bp;
+            } else {
+              const unsigned long long Rg = st->high - st->low + 1;
+              unsigned long long lo = st->low, hi = st->low + ((Rg * (sm.cum_t + sm.freq_t)) >> a.cdf_bits) - 1;
+              lo = lo + ((Rg * sm.cum_t) >> a.cdf_bits);
+              unsigned long long val = st->value, bp = st->bitpos;
+              uint32_t pend = st->pend;
+              const uint8_t *s = a.streams + a.stream_off[c];
+              const unsigned long long nb = a.stream_bits[c];
+              for (;;) {
+                if (hi < HALF) { pend = 0; }
+                else if (lo >= HALF) { lo -= HALF; hi -= HALF; val -= HALF; pend = 0; }
+                else if (lo >= QTR && hi < 3 * QTR) { lo -= QTR; hi -= QTR; val -= QTR; ++pend; }
+                else break;
+                lo = 2 * lo; hi = 2 * hi + 1;
+                const unsigned long long bit = bp < nb ? (s[bp >> 3] >> (7 - (bp & 7))) & 1u : 0u;
+                val = 2 * val + bit;
+                ++bp;
+              }
+              st->low = lo; st->high = hi; st->value = val; st->bitpos = bp; st->pend = pend;
             }
-            st->low = lo; st->high = hi; st->value = val; st->bitpos = bp; st->pend = pend;
           }
           if (mix) mixer_update(sm.pt_t, sm.png_t);
           if (use_ng && lt >= 0 && lt < (int)Vc) cu_s[lt] = __fadd_rn(cu_s[lt], 1.f);

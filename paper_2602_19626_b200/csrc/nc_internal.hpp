@@ -77,6 +77,12 @@ class WncEncoder {
   uint64_t nbits_ = 0;
 };
 
+// rANS coder (the paper's future-work ANS; reading D39): 64-bit state, L = 2^31,
+// 32-bit renormalisation words, symbols encoded in reverse; the stream holds the words in the
+// decoder's order, big-endian; bit_count = 32 x words.
+void ans_encode(const uint32_t *cum, const uint32_t *freq, size_t n, uint32_t cdf_bits,
+                std::vector<uint8_t> &out, uint64_t &bit_count);
+
 // NC05 container.
 struct Nc05Chunk {
   uint32_t tokens, bits;
@@ -102,6 +108,7 @@ struct Params {
   double eta, alpha, inv_tau;
   bool refresh;     // NEXT-4: refresh window semantics (NC_WINDOW_REFRESH)
   uint32_t lmax;    // D10: L_max = window, or window - 1 (NC_WINDOW_LMAX_M1)
+  uint32_t coder;   // NC_CODER_WNC (0) or NC_CODER_ANS (1)
 };
 Params validate(const nc_params *p);
 

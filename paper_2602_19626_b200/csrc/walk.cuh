@@ -36,7 +36,8 @@ struct WalkState {                    // per chunk, device resident
   uint32_t err;                       // nonzero = integrity failure
   float wl, wn;                       // current mixer weights (softmax of lw) as f32
   uint32_t pend;                      // decoder: pending E3 (underflow) steps, as the encoder counts them
-  // device WNC decoder (D27)
+  // device decoder: WNC (D27) uses low, high, value, bitpos; rANS (D39) keeps its state x in
+  // value and its read position (bits, a multiple of 32) in bitpos
   unsigned long long low, high, value, bitpos;
 };
 
@@ -69,6 +70,7 @@ struct WalkArgs {
   uint32_t V, cdf_bits, warmup, flags, orders, cap;
   float inv_tau; double alpha, eta;
   int mode;                           // 0 encode, 1 decode
+  uint32_t coder;                     // decode: NC_CODER_WNC (0) or NC_CODER_ANS (1)
   int n_chunks_total;                 // chunks of the container (or shard): with V, fixes the cluster size
 };
 

@@ -69,6 +69,33 @@ def test_host_wnc_encoder_matches_oracle():
             assert (s, b) == (ref, ref_bits)
 
 
+def test_host_ans_encoder_matches_oracle():
+    """NC_CODER_ANS's host encoder (D39) writes the oracle rANS encoder's bytes, and the
+    oracle rANS decoder recovers the symbols from them (every renormalisation branch: tiny
+    and near-T frequencies, 16 and 24 bits)."""
+    from oracle.ans import AnsDecoder, AnsEncoder
+    rng = np.random.default_rng(11)
+    for bits in (16, 24):
+        T = 1 << bits
+        for trial in range(20):
+            n = int(rng.integers(0, 400))
+            cum = rng.integers(0, T - 1, n)
+            freq = np.array([int(rng.integers(1, T - c + 1)) if rng.random() < 0.3 else
+                             int(rng.integers(1, min(64, T - c) + 1)) for c in cum], dtype=np.int64)
+            enc = AnsEncoder()
+            for c, f in zip(cum, freq):
+                enc.encode(int(c), int(f), T)
+            ref, ref_bits = enc.finish()
+            s, b = nc.nc_host_ans_encode(cum, freq, bits)
+            assert (s, b) == (ref, ref_bits)
+            dec = AnsDecoder(s)
+            for c, f in zip(cum, freq):   # a two-symbol-per-step CDF around each pair
+                cdf = np.array([0, int(c), int(c) + int(f), T]) if c else np.array([0, int(f), T])
+                sym = dec.decode(cdf, T)
+                assert int(cdf[sym]) == int(c) and int(cdf[sym + 1] - cdf[sym]) == int(f)
+            assert dec.finished_ok()
+
+
 def test_host_tokenizer_matches_oracle():
     from synth import make_text, make_vocab
     vocab = make_vocab(49152)

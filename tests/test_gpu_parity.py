@@ -845,3 +845,71 @@ def test_full_model_head_only_end_to_end(nc):
     _, _, p_gpu = nc.nc_debug_walk(z, ts[0], prm)
     assert (np.abs(p_gpu - ps[0]) / ps[0]).max() < P_TOL
     m.close()
+
+
+# ------------------------------------------------------------------ rANS ---
+@pytest.mark.parametrize("n_chunks,flags", [(1, 3), (3, 3), (2, 1)])
+def test_ans_coder_roundtrip_size_and_streams(nc, m2, w2, n_chunks, flags):
+    """NEXT-4 rANS (D39): NC_CODER_ANS containers round-trip through the device rANS decoder;
+    the size is within 0.5 % of the oracle pipeline with coder="ans"; every chunk stream is
+    the oracle rANS encoder's bytes of the walk's own (cum, freq) pairs (the coder is the
+    same function on both sides, the pairs come from the GPU walk); and the coder costs at
+    most 12 bytes per chunk over the WNC container of the same input (the 64-bit flush plus
+    a partial word)."""
+    import struct
+    from oracle.ans import AnsEncoder
+    from oracle.ensemble import Params
+    from synth import make_text
+    data = make_text("alice", 4096, 1001)
+    prm = nc.nc_params_default(window=512, slide=128, n_chunks=n_chunks, flags=flags, coder=nc._lib.CODER_ANS)
+    blob = nc.nc_compress(m2, data, prm)
+    assert nc.nc_decompress(m2, blob, prm) == data
+    size, _, xs, ts = _oracle_size_and_p(w2, data, Params(window=512, slide=128, n_chunks=n_chunks,
+                                                           flags=flags, coder="ans"))
+    assert abs(len(blob) - size) <= 0.005 * size, (len(blob), size)
+    wnc = nc.nc_compress(m2, data, nc.nc_params_default(window=512, slide=128, n_chunks=n_chunks, flags=flags))
+    assert len(wnc) - 2 * n_chunks <= len(blob) <= len(wnc) + 12 * n_chunks, (len(blob), len(wnc))
+    n = struct.unpack_from("<BHH", blob, 4)[2]
+    table = [struct.unpack_from("<III", blob, 9 + 12 * c) for c in range(n)]
+    off = 9 + 12 * n
+    for c in range(n):
+        z = nc.nc_debug_forward(m2, xs[c], prm, 0)
+        cum, freq, _ = nc.nc_debug_walk(z, ts[c], nc.nc_params_default(window=512, slide=128, n_chunks=n,
+                                                                       flags=flags))
+        enc = AnsEncoder()
+        for a, f in zip(cum, freq):
+            enc.encode(int(a), int(f), 1 << 24)
+        ref, ref_bits = enc.finish()
+        assert table[c][:2] == (len(ts[c]), ref_bits), c
+        assert blob[off:off + table[c][2]] == ref, c
+        off += table[c][2]
+
+
+def test_ans_coder_detects_wrong_coder_and_corruption(nc, m2):
+    """rANS integrity (D39): a container decoded with the other coder, and any single bit flip
+    in an rANS stream (its flush words, the middle, its last word) end in NC_ERR_INTEGRITY --
+    the decoder must finish in the encoder's start state 2^31 with every word read."""
+    import struct
+    from synth import make_text
+    data = make_text("alice", 1500, 5)
+    ans = nc.nc_params_default(window=256, slide=128, n_chunks=1, coder=nc._lib.CODER_ANS)
+    wnc = nc.nc_params_default(window=256, slide=128, n_chunks=1)
+    blob = nc.nc_compress(m2, data, ans)
+    assert nc.nc_decompress(m2, blob, ans) == data
+    for p_enc, p_dec in ((ans, wnc), (wnc, ans)):
+        b = nc.nc_compress(m2, data, p_enc)
+        with pytest.raises(nc.NcError) as ei:
+            nc.nc_decompress(m2, b, p_dec)
+        assert ei.value.status == nc._lib.NC_ERR_INTEGRITY
+    bits = struct.unpack_from("<I", blob, 13)[0]
+    assert bits % 32 == 0
+    s0 = 21
+    for bit in [0, 5, 31, 40, 63, bits // 3, bits // 2, bits - 33, bits - 9, bits - 1]:
+        corrupt = bytearray(blob)
+        corrupt[s0 + bit // 8] ^= 0x80 >> (bit % 8)
+        with pytest.raises(nc.NcError) as ei:
+            nc.nc_decompress(m2, bytes(corrupt), ans)
+        assert ei.value.status == nc._lib.NC_ERR_INTEGRITY, bit
+    with pytest.raises(nc.NcError):   # a trailing byte after the last word
+        nc.nc_decompress(m2, blob[:17] + struct.pack("<I", struct.unpack_from("<I", blob, 17)[0] + 1) + blob[21:] + b"\0",
+                         ans)

@@ -79,3 +79,31 @@ def test_ans_empty_and_corruption():
     out = [dec.decode(cdfs[i % 8], T) for i in range(2000)]
     assert out != syms or not dec.finished_ok()
     assert not dec.finished_ok()
+
+
+def test_ans_one_and_two_symbol_closed_forms():
+    """hand-derived streams: one symbol from the start state L (no renormalisation, since
+    L < ((L >> b) << 32) freq) is the 8-byte big-endian x = floor(L / f) T + (L mod f) + c;
+    a second symbol first in coding order (encoded last) applies the same map to that x,
+    renormalising once when x >= ((L >> b) << 32) f (its low word goes to the stream END)."""
+    T, b = 1 << 16, 16
+    c, f = 1234, 777
+    x1 = (L // f) * T + L % f + c
+    assert AnsEncoder().finish() == (L.to_bytes(8, "big"), 64)
+    e = AnsEncoder()
+    e.encode(c, f, T)
+    assert e.finish() == (x1.to_bytes(8, "big"), 64)
+    c, f = 1234, 1                         # x1 = 2^47 + c
+    x1 = (L // f) * T + L % f + c
+    c2, f2 = 5, 1                          # x1 >= ((L >> 16) << 32) * 1 = 2^47 -> one word out
+    assert x1 >= ((L >> b) << 32) * f2
+    y = x1 >> 32
+    x2 = (y // f2) * T + y % f2 + c2
+    e = AnsEncoder()
+    e.encode(c2, f2, T)                    # decoded first
+    e.encode(c, f, T)
+    data, nbits = e.finish()
+    assert data == x2.to_bytes(8, "big") + (x1 & 0xFFFFFFFF).to_bytes(4, "big") and nbits == 96
+    d = AnsDecoder(data)
+    assert d.decode(np.array([0, c2, c2 + f2, T]), T) == 1
+    assert d.decode(np.array([0, c, c + f, T]), T) == 1 and d.finished_ok()
