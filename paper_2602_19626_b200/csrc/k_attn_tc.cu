@@ -6,9 +6,10 @@
 //     S_b = Q K_b^T                     tcgen05 kind::tf32, 3 products x 8 k-steps, N = 128 -> TMEM
 //     m  <- max(m, rowmax(S_b / 8))     (the row's two key halves exchange their maxima)
 //     P_b = exp(S_b / 8 - m) (masked), l_X <- l_X alpha + rowsum(P_bX) per key half X
-//     O_b = P_b V_b                     tcgen05 kind::tf32 (P from TMEM, V MN-major), K = 128 keys
-//                                       -> one fresh TMEM partial per block
-//     O  <- O * alpha + O_b             in fp32 RN registers (promotion, see k_gemm_tc.cu)
+//     O_b = P_b V_b                     tcgen05 kind::tf32 (P from TMEM, V MN-major), K = 128 keys:
+//                                       P_hi [V_hi | V_lo] as one N = 128 MMA + P_lo V_hi (N = 64)
+//                                       -> one fresh TMEM partial [main | corrections] per block
+//     O  <- O * alpha + (main + corr)   in fp32 RN registers (promotion, see k_gemm_tc.cu)
 //   o = O / (l_A + l_B)
 //
 // Every row's arithmetic is the same whatever tile it is in, so decode (tiles of one row)
@@ -19,7 +20,7 @@
 //   warp 0  TMA: Q once (hi/lo, 64 KB), then K of each 128-key block (64 KB, one buffer)
 //   warp 3  TMA: V in 64-key granules (32 KB) through a ring of 3
 //   warp 1  MMA issue (whole warp, one elected lane per instruction): S(i), then PV(i-1)
-//   warp 2  TMEM allocator: S (128 cols) | P_A hi,lo | P_B hi,lo (64 each) | O partial (64)
+//   warp 2  TMEM allocator: S (128 cols) | P_A hi,lo | P_B hi,lo (64 each) | O partial (128)
 //   warps 4-7 / 8-11  softmax of key half A / B and the promotion of output dims 0-31 / 32-63,
 //                     thread = query row (TMEM lane); the halves share the row max (smem)
 // Measured (tools/micro): an N = 128 tf32 MMA costs 64 cycles, N = 64 costs 48-57.  Per
@@ -59,7 +60,8 @@ constexpr int V_GRAN = 4 * KV_SUB;               // V hi/lo x two 32-dim halves,
 constexpr int ATT_SMEM = Q_BYTES + K_BYTES + VG * V_GRAN + 1024 + 256 + 2 * 128 * 4;
 constexpr int ATT_THREADS = 384;
 // TMEM columns
-constexpr uint32_t T_S = 0, T_P = 128, T_O = 384;   // P half X at T_P + 128 X (hi, lo +64); O partial at T_O
+// P half X at T_P + 128 X (hi, lo +64); the block's O partial at T_O: [P_hi V_hi | corrections]
+constexpr uint32_t T_S = 0, T_P = 128, T_O = 384;
 
 #ifdef NC_ATT_TIMING
 // diagnostics build only: per-thread phase cycles accumulated in registers, flushed once per CTA
@@ -71,6 +73,12 @@ __device__ unsigned long long g_att_clk[32];
 #define AT_DECL do {} while (0)
 #define AT_T(k) do {} while (0)
 #define AT_FLUSH(base, cond) do {} while (0)
+#endif
+
+// diagnostics builds only (-DNC_ATT_ABL=k, results wrong): 1 no exponentials, 2 no O-partial
+// loads in the fold, 3 no S loads, 4 no P stores, 5 no PV MMAs, 6 no S MMAs
+#ifndef NC_ATT_ABL
+#define NC_ATT_ABL 0
 #endif
 
 __device__ __forceinline__ int wstart(int j, int L, int C) {
@@ -250,7 +258,13 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
     // MMA issuer: the whole warp runs the loop on warp-uniform values; one elected
     // lane issues each tcgen05 instruction (see tc::elect_one)
     constexpr uint32_t idS = tc::idesc_tf32(AQ, AK);                  // S: K-major A and B, N = 128
-    constexpr uint32_t idO = tc::idesc_tf32(AQ, 64) | (1u << 16);     // O: B (V) MN-major, N = 64
+    // O: B (V) MN-major.  P_hi multiplies [V_hi | V_lo] in ONE N = 128 MMA (the granule's four
+    // 32-dim blocks are consecutive: an N = 128 operand), writing P_hi V_hi to T_O and P_hi V_lo
+    // to T_O + 64; P_lo V_hi (N = 64) accumulates onto the latter.  An N = 64 tf32 MMA costs
+    // ~55 cycles and N = 128 64 (tools/micro/mma_bench4.cu), so this is 119 cycles per k-step
+    // instead of three N = 64 MMAs (165); the fold sums the two halves.
+    constexpr uint32_t idO = tc::idesc_tf32(AQ, 128) | (1u << 16);
+    constexpr uint32_t idC = tc::idesc_tf32(AQ, 64) | (1u << 16);
     const uint64_t q_desc = tc::desc_k_sw128(tc::smem_u32(sQ));
     const uint64_t k_desc = tc::desc_k_sw128(tc::smem_u32(sK));
     const uint64_t v_desc0 = desc_mn_sw128_32b(tc::smem_u32(sV), KV_SUB);
@@ -268,22 +282,17 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
       tc::fence_after();
       const uint32_t dO = tmem + T_O;
       const uint64_t vd[2] = {v_desc0 + off(vs0 * V_GRAN), v_desc0 + off(vs1 * V_GRAN)};
+#if NC_ATT_ABL != 5
 #pragma unroll
-      for (int x = 0; x < 2; ++x) {                // corrections first, hi*hi last (see k_gemm_tc.cu)
+      for (int x = 0; x < 2; ++x) {
         const uint32_t ph_t = tmem + T_P + 128 * x, pl_t = ph_t + 64;
 #pragma unroll
         for (int j = 0; j < AH / 8; ++j) {
-          if (tc::elect_one()) tc::mma_tf32_ts(dO, ph_t + j * 8, vd[x] + off(2 * KV_SUB + j * 1024), idO, (x | j) != 0);
-          if (tc::elect_one()) tc::mma_tf32_ts(dO, pl_t + j * 8, vd[x] + off(j * 1024), idO, 1);
+          if (tc::elect_one()) tc::mma_tf32_ts(dO, ph_t + j * 8, vd[x] + off(j * 1024), idO, (x | j) != 0);
+          if (tc::elect_one()) tc::mma_tf32_ts(dO + 64, pl_t + j * 8, vd[x] + off(j * 1024), idC, 1);
         }
       }
-#pragma unroll
-      for (int x = 0; x < 2; ++x) {
-        const uint32_t ph_t = tmem + T_P + 128 * x;
-#pragma unroll
-        for (int j = 0; j < AH / 8; ++j)
-          if (tc::elect_one()) tc::mma_tf32_ts(dO, ph_t + j * 8, vd[x] + off(j * 1024), idO, 1);
-      }
+#endif
       if (tc::elect_one()) {
         tc::mma_commit(pv_done);                   // P buffers free + O partial ready
         tc::mma_commit(&v_empty[vs0]);
@@ -307,6 +316,7 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
         if (gb > 0) tc::mbar_wait(s_empty, (gb - 1) & 1);   // both softmax groups read S(gb-1)
         AT_T(2);   // wait s_empty
         tc::fence_after();
+#if NC_ATT_ABL != 6
 #pragma unroll
         for (int dsub = 0; dsub < 2; ++dsub)     // corrections first, hi*hi last (see k_gemm_tc.cu)
 #pragma unroll
@@ -327,6 +337,7 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
             if (tc::elect_one())
               tc::mma_tf32(tmem + T_S, q_desc + off(dsub * Q_SUB + adv), k_desc + off(dsub * K_SUB + adv), idS, 1);
           }
+#endif
         if (tc::elect_one()) {
           tc::mma_commit(s_full);
           tc::mma_commit(k_empty);
@@ -366,11 +377,17 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
       for (int d = 0; d < 32; ++d) O[d] = 0.f;
       float m = -CUDART_INF_F, l = 0.f, alpha_prev = 1.f;
       auto fold = [&](float al) {                  // O <- O * alpha + O_partial  (fp32 RN promotion)
-        uint32_t x0[32];
+        uint32_t x0[32], x1[32];
+#if NC_ATT_ABL == 2
+        for (int d = 0; d < 32; ++d) { x0[d] = __float_as_uint(al); x1[d] = 0u; }
+#else
         tc::tmem_ld32(tmem + T_O + 32 * x + lane_off, x0);
+        tc::tmem_ld32(tmem + T_O + 64 + 32 * x + lane_off, x1);
         tc::tmem_wait_ld();
+#endif
 #pragma unroll
-        for (int d = 0; d < 32; ++d) O[d] = __fmaf_rn(O[d], al, __uint_as_float(x0[d]));
+        for (int d = 0; d < 32; ++d)
+          O[d] = __fmaf_rn(O[d], al, __fadd_rn(__uint_as_float(x0[d]), __uint_as_float(x1[d])));
       };
       // a warp whose 32 rows are all past the tile's rows (decode tiles hold 1-3 rows; ragged
       // tails) skips its TMEM loads, exponentials, P stores and folds -- the MMAs compute its
@@ -386,9 +403,13 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
         float mloc = -CUDART_INF_F;
         if (!idle) {
           uint32_t sr[2][32];
+#if NC_ATT_ABL == 3
+          for (int k = 0; k < 32; ++k) { sr[0][k] = __float_as_uint(0.01f * (k ^ lane)); sr[1][k] = __float_as_uint(0.02f * (k ^ lane)); }
+#else
           tc::tmem_ld32(tmem + T_S + 64 * x + lane_off, sr[0]);
           tc::tmem_ld32(tmem + T_S + 64 * x + lane_off + 32, sr[1]);
           tc::tmem_wait_ld();
+#endif
           if (key0 + AH - 1 <= j) {              // whole half inside the window: no masking
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh)
@@ -429,7 +450,11 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
           for (int hh = 0; hh < 2; ++hh)
 #pragma unroll
             for (int k = 0; k < 32; ++k) {
+#if NC_ATT_ABL == 1
+              xs[hh][k] = __fmaf_rn(xs[hh][k], kScale, nmn);
+#else
               xs[hh][k] = tc::ex2(__fmaf_rn(xs[hh][k], kScale, nmn));   // masked: ex2(-inf) = 0
+#endif
               ps4[k & 3] = __fadd_rn(ps4[k & 3], xs[hh][k]);
             }
           const float ps = __fadd_rn(__fadd_rn(ps4[0], ps4[1]), __fadd_rn(ps4[2], ps4[3]));
@@ -456,8 +481,12 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
               hi[k] = __float_as_uint(fh);
               lo[k] = __float_as_uint(fl);
             }
+#if NC_ATT_ABL == 4
+            if (hi[0] == 0x7fffffffu && lo[1] == 0x7fffffffu) tc::tmem_st32(ph_t + 32 * hh, hi);
+#else
             tc::tmem_st32(ph_t + 32 * hh, hi);
             tc::tmem_st32(ph_t + 64 + 32 * hh, lo);
+#endif
           }
           if (i >= 1) fold(alpha_prev);
           tc::tmem_wait_st();
