@@ -369,6 +369,7 @@ struct Forward {
   cudaStream_t s;
   int Mmax = 0;
   float *h, *rinv, *logits, *lbuf[2];
+  float *ssq; int *rms_ctr;            // RMSNorm statistics of h: slice sums of squares, per-32-row counters
   float *h_hi, *h_lo, *o_hi, *o_lo, *act_hi, *act_lo;   // tf32 planes (tensor-core GEMM operands)
   float *q_hi = nullptr, *q_lo = nullptr;               // tf32 planes of q (tensor-core attention)
   int n_chunks_ = 0;
@@ -381,6 +382,9 @@ struct Forward {
     const Shape &S = m->s;
     h = bag.get<float>((size_t)Mmax * S.d);
     rinv = bag.get<float>((size_t)Mmax);
+    ssq = bag.get<float>((size_t)(S.d / 32) * ((Mmax + 31) / 32 * 32));   // [slice][row]
+    rms_ctr = bag.get<int>((size_t)(Mmax + 31) / 32);
+    NC_CUDA(cudaMemsetAsync(rms_ctr, 0, (size_t)(Mmax + 31) / 32 * sizeof(int), s));   // self-resetting
     h_hi = bag.get<float>((size_t)Mmax * S.d);
     h_lo = bag.get<float>((size_t)Mmax * S.d);
     o_hi = bag.get<float>((size_t)Mmax * S.H * S.dh);
@@ -419,13 +423,19 @@ struct Forward {
     Stats &st = stats();
     const int qd = S.H * S.dh, kvd = S.KV * S.dh;
     const double d = S.d;
-    PROF(K_EMBED, 4.0 * d * valid, launch_embed(rows.x, M, m->E, S.d, h, h_hi, h_lo, s));
+    PROF(K_EMBED, 4.0 * d * valid, launch_embed(rows.x, M, m->E, S.d, h, h_hi, h_lo, ssq, rinv, (float)S.eps, s));
     st.launches++;
+    // RMSNorm (D16): rinv = 1/sqrt(mean(h^2) + eps) comes with h (the embedding, the residual
+    // epilogues); the consuming projection scales its rows by it in its epilogue
+    auto norm = [&](TcGemmArgs &g) { g.rinv = rinv; };
+    auto stats_out = [&](TcGemmArgs &g) {
+      g.ssq_out = ssq; g.ssq_ld = (Mmax + 31) / 32 * 32;
+      g.rinv_out = rinv; g.rms_ctr = rms_ctr; g.rms_d = (float)S.d; g.rms_eps = (float)S.eps;
+    };
     for (uint32_t l = 0; l < S.n_layers; ++l) {
-      PROF(K_RMS, 4.0 * d * valid, launch_rms(h, M, S.d, (float)S.eps, rinv, s));
       {  // RMSNorm scale + QKV + RoPE + KV-ring scatter (q and K/V as tf32 planes)
         TcGemmArgs g{};
-        g.M = M; g.N = qd + 2 * kvd; g.K = S.d; g.rinv = rinv; g.C = nullptr; g.ldc = qd;
+        g.M = M; g.N = qd + 2 * kvd; g.K = S.d; norm(g); g.C = nullptr; g.ldc = qd;
         g.layer = (int)l; g.n_q_cols = qd; g.n_kv_cols = kvd; g.rows = rows; g.ring = ring;
         g.rope_cos = m->rope_cos; g.rope_sin = m->rope_sin;
         g.C_hi = q_hi; g.C_lo = q_lo;
@@ -444,36 +454,34 @@ struct Forward {
       }
       {
         TcGemmArgs g{};
-        g.M = M; g.N = S.d; g.K = qd; g.C = h; g.ldc = S.d; g.C_hi = h_hi; g.C_lo = h_lo;
+        g.M = M; g.N = S.d; g.K = qd; g.C = h; g.ldc = S.d; g.C_hi = h_hi; g.C_lo = h_lo; stats_out(g);
         TcOperands op{o_hi, o_lo, (uint64_t)Mmax, m->wo_hi[l], m->wo_lo[l]};
         PROF(K_OPROJ, 2.0 * valid * d * qd, launch_gemm_tc(EPI_RESID, g, op, s));
       }
-      PROF(K_RMS, 4.0 * d * valid, launch_rms(h, M, S.d, (float)S.eps, rinv, s));
       {
         TcGemmArgs g{};
-        g.M = M; g.N = 2 * S.d_ff; g.K = S.d; g.rinv = rinv; g.C_hi = act_hi; g.C_lo = act_lo; g.ldc = S.d_ff;
+        g.M = M; g.N = 2 * S.d_ff; g.K = S.d; norm(g); g.C_hi = act_hi; g.C_lo = act_lo; g.ldc = S.d_ff;
         TcOperands op{h_hi, h_lo, (uint64_t)Mmax, m->wgu_hi[l], m->wgu_lo[l]};
         PROF(K_GATEUP, 2.0 * valid * 2 * S.d_ff * d, launch_gemm_tc(EPI_SWIGLU, g, op, s));
         TcGemmArgs g2{};
-        g2.M = M; g2.N = S.d; g2.K = S.d_ff; g2.C = h; g2.ldc = S.d; g2.C_hi = h_hi; g2.C_lo = h_lo;
+        g2.M = M; g2.N = S.d; g2.K = S.d_ff; g2.C = h; g2.ldc = S.d; g2.C_hi = h_hi; g2.C_lo = h_lo; stats_out(g2);
         TcOperands op2{act_hi, act_lo, (uint64_t)Mmax, m->wd_hi[l], m->wd_lo[l]};
         PROF(K_DOWN, 2.0 * valid * d * S.d_ff, launch_gemm_tc(EPI_RESID, g2, op2, s));
       }
-      st.launches += 7;   // 2 RMSNorm scales, QKV, attention, O, gate/up, down
+      st.launches += 5;   // QKV, attention, O, gate/up, down
     }
     if (ev_head) NC_CUDA(cudaEventRecord(ev_head, s));
     if (!head) {
       NC_CUDA(cudaGetLastError());
       return;
     }
-    PROF(K_RMS, 4.0 * d * valid, launch_rms(h, M, S.d, (float)S.eps, rinv, s));
     {
       TcGemmArgs g{};
-      g.M = M; g.N = S.V; g.K = S.d; g.rinv = rinv; g.C = logits; g.ldc = S.V;
+      g.M = M; g.N = S.V; g.K = S.d; norm(g); g.C = logits; g.ldc = S.V;
       TcOperands op{h_hi, h_lo, (uint64_t)Mmax, m->E_head_hi, m->E_head_lo};
       PROF(K_HEAD, 2.0 * valid * S.V * d, launch_gemm_tc(EPI_HEAD, g, op, s));
     }
-    st.launches += 2;
+    st.launches += 1;
     NC_CUDA(cudaGetLastError());
   }
 };

@@ -11,6 +11,12 @@ namespace nc {
 struct TcGemmArgs {
   int M, N, K;
   const float *rinv;          // per-row RMSNorm scale (QKV, SWIGLU, HEAD)
+  // RESID: the RMSNorm statistics of the new h, for the next projection.  Every epilogue warp
+  // writes its rows' sums of squares per 32-column slice (ssq_out [N / 32][ssq_ld >= M rounded
+  // up to 32]) and counts in
+  // rms_ctr (one counter per 32 rows); the last of the N / 64 warps covering those rows forms
+  // rinv_out = 1/sqrt(sum_s ssq[s] / rms_d + rms_eps) (slices in order) and resets the counter
+  float *ssq_out, *rinv_out; int *rms_ctr; float rms_d, rms_eps; int ssq_ld;
   float *C; int ldc;          // fp32 output: logits (HEAD), residual h in/out (RESID), q (QKV)
   float *C_hi, *C_lo;         // tf32 planes written for the next GEMM (RESID: h, SWIGLU: act; QKV: q planes)
   int layer, n_q_cols, n_kv_cols;

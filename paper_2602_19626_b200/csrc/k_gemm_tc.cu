@@ -143,10 +143,15 @@ __device__ __forceinline__ void tma_store32_planes(float *stg, const CUtensorMap
 // destinations (this lane's row); d0 == nullptr skips the row.
 //   ST_PLAIN  d0 = v
 //   ST_SPLIT  d0 = tf32 hi(v), d1 = lo(v)
-//   ST_RESID  h = d0 + v (fp32 RN); d0 = h, d1 = hi(h), d2 = lo(h)
+//   ST_RESID  h = d0 + v (fp32 RN); d0 = h, d1 = hi(h), d2 = lo(h); and, if ssq != nullptr, the
+//             slice's sum of squares of h for each row r of the warp at ssq[r] (one coalesced
+//             128 B store; rows past M hold garbage): per lane ((x^2 + y^2) + z^2) + w^2 (fma)
+//             over its 4 columns, then an xor tree over the row's 8 lanes (1, 2, 4) -- the same
+//             arithmetic as embed_kernel's
 enum { ST_PLAIN = 0, ST_SPLIT = 1, ST_RESID = 2 };
 template <int MODE>
-__device__ __forceinline__ void store_rows32(float *stg, const float *v, float *d0, float *d1, float *d2, int lane) {
+__device__ __forceinline__ void store_rows32(float *stg, const float *v, float *d0, float *d1, float *d2, int lane,
+                                             float *ssq = nullptr) {
 #pragma unroll
   for (int k = 0; k < 8; ++k)
     *reinterpret_cast<float4 *>(stg + lane * 32 + 4 * (k ^ (lane & 7))) =
@@ -163,9 +168,11 @@ __device__ __forceinline__ void store_rows32(float *stg, const float *v, float *
       hin[i] = p0 ? *reinterpret_cast<const float4 *>(p0 + 4 * c4) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
   }
+  float sq[MODE == ST_RESID ? 8 : 1];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const int r = 4 * i + (lane >> 3);
+    if (MODE == ST_RESID) sq[i] = 0.f;
     float *p0 = reinterpret_cast<float *>(__shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(d0), r));
     float *p1 = MODE != ST_PLAIN
                     ? reinterpret_cast<float *>(__shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(d1), r))
@@ -182,6 +189,7 @@ __device__ __forceinline__ void store_rows32(float *stg, const float *v, float *
           y.x = __fadd_rn(hin[i].x, y.x); y.y = __fadd_rn(hin[i].y, y.y);
           y.z = __fadd_rn(hin[i].z, y.z); y.w = __fadd_rn(hin[i].w, y.w);
           *reinterpret_cast<float4 *>(p0 + 4 * c4) = y;
+          sq[i] = __fmaf_rn(y.w, y.w, __fmaf_rn(y.z, y.z, __fmaf_rn(y.y, y.y, __fmul_rn(y.x, y.x))));
         }
         float4 hi, lo;
         tc::split_tf32(y.x, hi.x, lo.x); tc::split_tf32(y.y, hi.y, lo.y);
@@ -191,6 +199,19 @@ __device__ __forceinline__ void store_rows32(float *stg, const float *v, float *
         *reinterpret_cast<float4 *>(pl + 4 * c4) = lo;
       }
     }
+  }
+  if (MODE == ST_RESID && ssq) {
+    float mine = 0.f;   // row `lane`'s sum: row 4 i + j sits in lanes 8 j .. 8 j + 7 at step i
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float t = sq[i];
+      t = __fadd_rn(t, __shfl_xor_sync(0xffffffffu, t, 1));
+      t = __fadd_rn(t, __shfl_xor_sync(0xffffffffu, t, 2));
+      t = __fadd_rn(t, __shfl_xor_sync(0xffffffffu, t, 4));
+      const float u = __shfl_sync(0xffffffffu, t, 8 * (lane & 3));
+      if ((lane >> 2) == i) mine = u;
+    }
+    ssq[lane] = mine;
   }
   __syncwarp();
 }
@@ -505,6 +526,33 @@ __global__ __launch_bounds__(TileCfg<BN>::THREADS, 1) void gemm_tc_kernel(const 
     const uint32_t tempty_leader = tc::mapa(&tempty[0], 0);
     int buf = 0;
     uint32_t buf_phase = 0;
+    // RESID: RMSNorm statistics of the rows this warp stored (first row rms_pend, -1 = none),
+    // counted after the next tile's k loop -- by then the stores have drained and the fence is
+    // cheap (a fence right after them stalled the store-bound epilogue).  The last of the N / EPI_COLS warps
+    // covering these 32 rows sums their slice sums in order into rinv_out.
+    int rms_pend = -1;
+    auto rms_flush = [&]() {
+      if (EPI != EPI_RESID || rms_pend < 0) return;
+      __threadfence();
+      __syncwarp();
+      int last = 0;
+      if (lane == 0) {
+        int *ctr = a.rms_ctr + rms_pend / 32;
+        last = atomicAdd(ctr, 1) == (a.N + EPI_COLS - 1) / EPI_COLS - 1;
+        if (last) *ctr = 0;   // every warp of these rows is in: reset for the next launch
+      }
+      last = __shfl_sync(0xffffffffu, last, 0);
+      const int mr = rms_pend + lane;
+      if (last && mr < a.M) {
+        __threadfence();
+        const int ns = a.N / 32;
+        const float *q = a.ssq_out + mr;
+        float ss = 0.f;
+        for (int k = 0; k < ns; ++k) ss = __fadd_rn(ss, __ldcg(q + (size_t)k * a.ssq_ld));
+        a.rinv_out[mr] = __frsqrt_rn(__fadd_rn(__fdiv_rn(ss, a.rms_d), a.rms_eps));
+      }
+      rms_pend = -1;
+    };
     for (int jt = 0;; ++jt) {
       const int slot = jt % NSCHED;
 #ifdef NC_GEMM_TIMING
@@ -515,7 +563,10 @@ __global__ __launch_bounds__(TileCfg<BN>::THREADS, 1) void gemm_tc_kernel(const 
       const int t = sch_tile[slot];
       __syncwarp();
       if (lane == 0) tc::mbar_arrive_remote(sch_empty_leader + slot * 8);
-      if (t < 0) break;
+      if (t < 0) {
+        rms_flush();
+        break;
+      }
 #ifdef NC_GEMM_TIMING
       if (threadIdx.x == 0) atomicAdd(&g_gemm_clk[EPI * 8 + 7], 1ull);
 #endif
@@ -589,6 +640,7 @@ __global__ __launch_bounds__(TileCfg<BN>::THREADS, 1) void gemm_tc_kernel(const 
         if (++buf == NPART) { buf = 0; buf_phase ^= 1; }
       }
       GEMM_MARK(5);   // partials drained / written
+      rms_flush();    // the previous tile's RMSNorm count: its stores drained under this k loop
       if (split) {
         // the last of the nsplit warps covering this (tile, warp) region sums every span's
         // partial in span order (= the unsplit promotion sum) and runs the epilogue
@@ -647,8 +699,10 @@ __global__ __launch_bounds__(TileCfg<BN>::THREADS, 1) void gemm_tc_kernel(const 
           // (TMA stores measured slower here: three serialized stores per slice)
           const size_t o = (size_t)m * a.ldc + cb;
           if (split) fold32(acc + sl * 32, sl * 32);
-          store_rows32<ST_RESID>(stg, acc + sl * 32, row_ok ? a.C + o : nullptr, a.C_hi + o, a.C_lo + o, lane);
+          store_rows32<ST_RESID>(stg, acc + sl * 32, row_ok ? a.C + o : nullptr, a.C_hi + o, a.C_lo + o, lane,
+                                 a.ssq_out && row0 < a.M ? a.ssq_out + (size_t)(cb / 32) * a.ssq_ld + row0 : nullptr);
         }
+        if (a.ssq_out && col0 < a.N && row0 < a.M) rms_pend = row0;   // counted at the next tile (see rms_flush)
       } else {
         static_assert(EPI == EPI_RESID || EPI_COLS % 64 == 0, "64-column epilogue blocks");
 #pragma unroll

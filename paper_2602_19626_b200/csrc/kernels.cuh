@@ -24,8 +24,8 @@ struct KvRing {
 };
 
 // ---------------------------------------------------------------- launchers
-void launch_embed(const uint32_t *x, int M, const float *E, int d, float *h, float *h_hi, float *h_lo, cudaStream_t s);
-void launch_rms(const float *h, int M, int d, float eps, float *rinv, cudaStream_t s);
+void launch_embed(const uint32_t *x, int M, const float *E, int d, float *h, float *h_hi, float *h_lo, float *ssq,
+                  float *rinv, float eps, cudaStream_t s);
 
 enum GemmEpi { EPI_QKV = 0, EPI_RESID = 1, EPI_SWIGLU = 2, EPI_HEAD = 3 };
 
