@@ -875,7 +875,8 @@ void compress_device(nc_model *m, const uint32_t *tokens_dev, const std::vector<
     wa.n_entries = w_off[sl + 1] - w_off[sl];
     wa.logits = fw.logits;
     prof().begin(K_WALK, 4.0 * S.V * valid, ws);
-    launch_walk(wa, ws);
+    static const bool no_walk = std::getenv("NC_DIAG_NO_WALK") != nullptr;   // diagnostics only (output wrong)
+    if (!no_walk) launch_walk(wa, ws);
     prof().end(ws);
     NC_CUDA(cudaEventRecord(ev[4 * sl + 3], ws));
     st.launches++;
