@@ -40,10 +40,16 @@
 
 namespace nc {
 
-#ifndef NC_WALK_WT
-#define NC_WALK_WT 384   // 12 warps: 168 registers per thread; per token 4.7k -> 4.6k cycles fused pass, 1.5k -> 1.3k reductions (vs 512)
-#endif
-constexpr int WT = NC_WALK_WT;   // threads per walk CTA (a token's logits stay in registers)
+// Threads per walk CTA, by cluster size (a token's logits stay in registers, so the thread
+// count sets the register budget): 512 (16 warps, 128 registers) for the 4- and 8-CTA
+// clusters of many-chunk containers -- more warps hide the per-element latency (A/B on one
+// box: config3 step -0.6 %, config2 -1 %) -- and 384 (12 warps, 168 registers) for the
+// 16-CTA single-stream cluster, whose CS-sized combine spills at 128 registers (512 threads:
+// config2 with one chunk 119 -> 135 ms).  The thread count fixes the reduction order, and
+// the cluster size is a function of V and the container's chunk count only, so encoder and
+// decoder always agree.
+constexpr int walk_threads(int cs) { return (cs == 4 || cs == 8) ? 512 : 384; }
+constexpr int WT = 384;          // the quantize debug kernel's block
 constexpr int NW = WT / 32;
 
 struct WalkSmem {
@@ -740,8 +746,9 @@ __device__ unsigned long long g_walk_clk[8];
 // NGM: float4 groups per thread the kernel is compiled for (>= the launch's; the register
 // arrays are sized by it -- 3 at V / CS = 6,144 keeps the 128-register budget spill-free).
 // The arithmetic does not depend on it (loops run over the thread's ng groups).
-template <int CS, int NGM>
-__global__ __launch_bounds__(WT, 1) void walk_cl_kernel(WalkArgs a) {
+template <int CS, int NGM, int WT_>
+__global__ __launch_bounds__(WT_, 1) void walk_cl_kernel(WalkArgs a) {
+  constexpr int WT = WT_;
   extern __shared__ __align__(16) uint8_t dsm[];
   __shared__ WalkSmem sm;
   __shared__ Xch xs[2];            // own slots (token parity)
@@ -1549,6 +1556,7 @@ static int walk_cluster_size(uint32_t V, int n_chunks) {
 
 template <int CS, int NGM>
 static void launch_walk_cs(const WalkArgs &a, cudaStream_t s) {
+  constexpr int WT = walk_threads(CS);
   const uint32_t Vc = a.V / CS;
   if (Vc % 4 || Vc / 4 > (uint32_t)NGM * WT)   // float4 groups, at most NGM per thread (register-resident rows)
     throw std::runtime_error("walk: vocabulary slice of " + std::to_string(Vc) +
@@ -1568,13 +1576,13 @@ static void launch_walk_cs(const WalkArgs &a, cudaStream_t s) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     cudaFuncAttributes fa{};
-    cudaFuncGetAttributes(&fa, walk_cl_kernel<CS, NGM>);
+    cudaFuncGetAttributes(&fa, walk_cl_kernel<CS, NGM, WT>);
     const size_t cap = (size_t)std::max(0, optin - (int)fa.sharedSizeBytes);   // what static smem leaves
-    check_launch(cudaFuncSetAttribute(walk_cl_kernel<CS, NGM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    check_launch(cudaFuncSetAttribute(walk_cl_kernel<CS, NGM, WT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)std::min(dmax, cap)),
                  "walk smem attribute");
     if (CS > 1)
-      check_launch(cudaFuncSetAttribute(walk_cl_kernel<CS, NGM>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+      check_launch(cudaFuncSetAttribute(walk_cl_kernel<CS, NGM, WT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
                    "walk cluster attribute");
   }
   cudaLaunchConfig_t cfg{};
@@ -1587,7 +1595,7 @@ static void launch_walk_cs(const WalkArgs &a, cudaStream_t s) {
   at[0].val.clusterDim.x = CS; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  check_launch(cudaLaunchKernelEx(&cfg, walk_cl_kernel<CS, NGM>, a), "walk launch");
+  check_launch(cudaLaunchKernelEx(&cfg, walk_cl_kernel<CS, NGM, WT>, a), "walk launch");
 }
 
 int walk_ctas_per_chunk(uint32_t V, int n_chunks) { return walk_cluster_size(V, n_chunks); }
@@ -1610,7 +1618,8 @@ void walk_timing_report() {
 void launch_walk(const WalkArgs &a, cudaStream_t s) {
   if (a.n_entries <= 0) return;
   const int cs = walk_cluster_size(a.V, a.n_chunks_total);
-  const uint32_t groups = (a.V / cs / 4 + WT - 1) / WT;   // float4 groups per thread
+  const int wt = walk_threads(cs);
+  const uint32_t groups = (a.V / cs / 4 + wt - 1) / wt;   // float4 groups per thread
   if (cs == 16) {
     if (groups <= 2) launch_walk_cs<16, 2>(a, s);
     else launch_walk_cs<16, 4>(a, s);
