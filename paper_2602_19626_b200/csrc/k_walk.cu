@@ -35,6 +35,8 @@
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
+#include <type_traits>
+
 #include "tc_common.cuh"
 #include "walk.cuh"
 
@@ -70,10 +72,19 @@ struct WalkSmem {
 
 // ------------------------------------------------------------ elementwise ---
 __device__ __forceinline__ float walk_u(float z, double b, float inv_tau) { return __fmaf_rn(z, inv_tau, (float)b); }
-__device__ __forceinline__ double b_step(double b, float pt, bool is_t, double alpha) {
-  // b - alpha (p~ - 1[t]) in f64 (D17); the subtraction only for the coded token (pt - 0 = pt)
-  const double d = (double)pt;
-  return __fma_rn(-alpha, is_t ? __dsub_rn(d, 1.0) : d, b);
+// b <- b - alpha (p~ - 1[t]) in f64 (D17), as two steps: b - alpha p~ for every id (one DFMA),
+// then + alpha for the coded token only (b_tok_fix, one thread) -- the per-element select of
+// p~ - 1 was ~8 % of the walk's instructions.  Encoder and decoder both use exactly this.
+__device__ __forceinline__ double b_step(double b, float pt, double alpha) {
+  return __fma_rn(-alpha, (double)pt, b);
+}
+// the coded token's correction, applied to component j of its float4 group (b01 = ids 0-1,
+// b23 = ids 2-3)
+__device__ __forceinline__ void b_tok_fix(double2 &b01, double2 &b23, int j, double alpha) {
+  if (j == 0) b01.x = __dadd_rn(b01.x, alpha);
+  else if (j == 1) b01.y = __dadd_rn(b01.y, alpha);
+  else if (j == 2) b23.x = __dadd_rn(b23.x, alpha);
+  else b23.y = __dadd_rn(b23.y, alpha);
 }
 // c = max(1, floor(p * (T - V))) with the EXACT product (D5), in fp32 only:
 // T - V < 2^24 is exact in fp32; q = floor(rn(p * TmV)) is off by at most one,
@@ -1102,14 +1113,12 @@ __global__ __launch_bounds__(WT_, 1) void walk_cl_kernel(WalkArgs a) {
       float tm = -CUDART_INF_F, ts = 0.f;   // next token's softmax statistics (after the group loop)
       const int tg = ltok >= 0 ? (ltok >> 2) : -1;
       const int gcut = ltok < 0 ? 0 : (ltok >= (int)Vc ? Gc : tg);   // local groups entirely below tok
-#pragma unroll
-      for (int k = 0; k < NGM; ++k) {
-        if (k >= ng) break;
-        const int g = tid + k * WT;
-        float pt[4], png[4], p[4];
+      // p~ and the mixed p of group k (MIX: the N-gram is mixed in)
+      auto probs = [&](auto MIXC, int k, int g, float (&pt)[4], float (&png)[4], float (&p)[4]) {
+        constexpr bool MIX = decltype(MIXC)::value;
 #pragma unroll
         for (int j = 0; j < 4; ++j) pt[j] = __fmul_rn(uc[k][j], scale);
-        if (!mix) {
+        if (!MIX) {
 #pragma unroll
           for (int j = 0; j < 4; ++j) { png[j] = 0.f; p[j] = pt[j]; }
         } else {
@@ -1121,46 +1130,80 @@ __global__ __launch_bounds__(WT_, 1) void walk_cl_kernel(WalkArgs a) {
 #pragma unroll
           for (int j = 0; j < 4; ++j) p[j] = mix_p(pt[j], a0f, cc[j], sa[j], wl, wn, png[j], skip);
         }
-        uint32_t cv[4];
-        quant4(p, TmV, cv);
-        if (dump) {
+      };
+      if (dump) {   // test-only full vectors of this token (same values as the pass below)
+#pragma unroll
+        for (int k = 0; k < NGM; ++k) {
+          if (k >= ng) break;
+          const int g = tid + k * WT;
+          float pt[4], png[4], p[4];
+          if (mix) probs(std::true_type{}, k, g, pt, png, p);
+          else probs(std::false_type{}, k, g, pt, png, p);
+          uint32_t cv[4];
+          quant4(p, TmV, cv);
           const size_t o = (size_t)dslot * V + vb + 4 * g;
           *reinterpret_cast<float4 *>(a.dump_pt + o) = make_float4(pt[0], pt[1], pt[2], pt[3]);
           *reinterpret_cast<float4 *>(a.dump_p + o) = make_float4(p[0], p[1], p[2], p[3]);
           *reinterpret_cast<uint4 *>(a.dump_c + o) = make_uint4(cv[0], cv[1], cv[2], cv[3]);
         }
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (p[j] > bb.v) { bb.v = p[j]; bb.i = (int)vb + 4 * g + j; bb.c = cv[j]; }
-        const uint32_t gs = cv[0] + cv[1] + cv[2] + cv[3];
-        my_sum += gs;
-        if (g < gcut) {
-          my_cum += gs;
-        } else if (g == tg && ltok < (int)Vc) {
-          const int jt = ltok & 3;
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            if (j < jt) my_cum += cv[j];
-            else if (j == jt) { xs[par].pt_t = pt[j]; xs[par].png_t = png[j]; xs[par].p_t = p[j]; xs[par].freq_t = cv[j]; }
-        }
-        if (use_head) {
-          double2 *bp = reinterpret_cast<double2 *>(b_s) + 2 * g;
-          double2 b01 = bp[0], b23 = bp[1];
-          const int v = 4 * g;
-          b01.x = b_step(b01.x, pt[0], v == ltok, a.alpha);
-          b01.y = b_step(b01.y, pt[1], v + 1 == ltok, a.alpha);
-          b23.x = b_step(b23.x, pt[2], v + 2 == ltok, a.alpha);
-          b23.y = b_step(b23.y, pt[3], v + 3 == ltok, a.alpha);
-          bp[0] = b01; bp[1] = b23;
-          if (has_next) {   // next token's u with the updated bias (== walk_u(z, b_new)), stats in decoder order
-            uc[k][0] = __fmaf_rn(zn[k].x, inv_tau, (float)b01.x); uc[k][1] = __fmaf_rn(zn[k].y, inv_tau, (float)b01.y);
-            uc[k][2] = __fmaf_rn(zn[k].z, inv_tau, (float)b23.x); uc[k][3] = __fmaf_rn(zn[k].w, inv_tau, (float)b23.y);
-          }
-        } else if (has_next) {
-          uc[k][0] = __fmul_rn(zn[k].x, inv_tau); uc[k][1] = __fmul_rn(zn[k].y, inv_tau);   // b == 0
-          uc[k][2] = __fmul_rn(zn[k].z, inv_tau); uc[k][3] = __fmul_rn(zn[k].w, inv_tau);
-        }
       }
+      // the fused pass, specialised on (mix, head) so the per-group loop carries no branches on them
+      auto pass = [&](auto MIXC, auto HEADC) {
+        constexpr bool HEAD = decltype(HEADC)::value;
+#pragma unroll
+        for (int k = 0; k < NGM; ++k) {
+          if (k >= ng) break;
+          const int g = tid + k * WT;
+          float pt[4], png[4], p[4];
+          probs(MIXC, k, g, pt, png, p);
+          uint32_t cv[4];
+          quant4(p, TmV, cv);
+          // argmax (largest p, lowest id on ties): the group's max, then its first position;
+          // the winner's count is quant(p) after the loop
+          const float gm = fmaxf(fmaxf(p[0], p[1]), fmaxf(p[2], p[3]));
+          if (gm > bb.v) {
+            bb.v = gm;
+            bb.i = (int)vb + 4 * g + (p[0] == gm ? 0 : (p[1] == gm ? 1 : (p[2] == gm ? 2 : 3)));
+          }
+          const uint32_t gs = cv[0] + cv[1] + cv[2] + cv[3];
+          my_sum += gs;
+          const bool tokg = g == tg && ltok < (int)Vc;
+          if (g < gcut) {
+            my_cum += gs;
+          } else if (tokg) {
+            const int jt = ltok & 3;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (j < jt) my_cum += cv[j];
+              else if (j == jt) { xs[par].pt_t = pt[j]; xs[par].png_t = png[j]; xs[par].p_t = p[j]; xs[par].freq_t = cv[j]; }
+          }
+          if (HEAD) {
+            double2 *bp = reinterpret_cast<double2 *>(b_s) + 2 * g;
+            double2 b01 = bp[0], b23 = bp[1];
+            b01.x = b_step(b01.x, pt[0], a.alpha);
+            b01.y = b_step(b01.y, pt[1], a.alpha);
+            b23.x = b_step(b23.x, pt[2], a.alpha);
+            b23.y = b_step(b23.y, pt[3], a.alpha);
+            if (tokg) b_tok_fix(b01, b23, ltok & 3, a.alpha);
+            bp[0] = b01; bp[1] = b23;
+            if (has_next) {   // next token's u with the updated bias (== walk_u(z, b_new)), stats in decoder order
+              uc[k][0] = __fmaf_rn(zn[k].x, inv_tau, (float)b01.x); uc[k][1] = __fmaf_rn(zn[k].y, inv_tau, (float)b01.y);
+              uc[k][2] = __fmaf_rn(zn[k].z, inv_tau, (float)b23.x); uc[k][3] = __fmaf_rn(zn[k].w, inv_tau, (float)b23.y);
+            }
+          } else if (has_next) {
+            uc[k][0] = __fmul_rn(zn[k].x, inv_tau); uc[k][1] = __fmul_rn(zn[k].y, inv_tau);   // b == 0
+            uc[k][2] = __fmul_rn(zn[k].z, inv_tau); uc[k][3] = __fmul_rn(zn[k].w, inv_tau);
+          }
+        }
+      };
+      if (mix) {
+        if (use_head) pass(std::true_type{}, std::true_type{});
+        else pass(std::true_type{}, std::false_type{});
+      } else {
+        if (use_head) pass(std::false_type{}, std::true_type{});
+        else pass(std::false_type{}, std::false_type{});
+      }
+      bb.c = bb.v >= 0.f ? quant(bb.v, TmV) : 0u;   // = the quant4 count of that element
 #if defined(NC_WALK_ABL) && NC_WALK_ABL >= 2   // diagnostics: no statistics
       tm = 0.f; ts = 1.f;
 #else
@@ -1445,11 +1488,11 @@ __global__ __launch_bounds__(WT_, 1) void walk_cl_kernel(WalkArgs a) {
           prob4(z, g, mth, scale, wl, wn, a0f, mix, skip, pt, png, p);
           double2 *bp = reinterpret_cast<double2 *>(b_s) + 2 * g;
           double2 b01 = bp[0], b23 = bp[1];
-          const int v = 4 * g;
-          b01.x = b_step(b01.x, pt[0], v == lt, a.alpha);
-          b01.y = b_step(b01.y, pt[1], v + 1 == lt, a.alpha);
-          b23.x = b_step(b23.x, pt[2], v + 2 == lt, a.alpha);
-          b23.y = b_step(b23.y, pt[3], v + 3 == lt, a.alpha);
+          b01.x = b_step(b01.x, pt[0], a.alpha);
+          b01.y = b_step(b01.y, pt[1], a.alpha);
+          b23.x = b_step(b23.x, pt[2], a.alpha);
+          b23.y = b_step(b23.y, pt[3], a.alpha);
+          if (lt >= 0 && (lt >> 2) == g) b_tok_fix(b01, b23, lt & 3, a.alpha);
           bp[0] = b01; bp[1] = b23;
         }
       __syncthreads();
