@@ -760,6 +760,7 @@ __device__ unsigned long long g_walk_clk[8];
 template <int CS, int NGM, int WT_>
 __global__ __launch_bounds__(WT_, 1) void walk_cl_kernel(WalkArgs a) {
   constexpr int WT = WT_;
+  static_assert(CS <= 32, "the combine reads one cluster slot per lane");
   extern __shared__ __align__(16) uint8_t dsm[];
   __shared__ WalkSmem sm;
   __shared__ Xch xs[2];            // own slots (token parity)
@@ -1247,17 +1248,20 @@ __global__ __launch_bounds__(WT_, 1) void walk_cl_kernel(WalkArgs a) {
         // the combine, split over three warps that run concurrently (same arithmetic as one
         // thread in sequence): warp 0 codes the token, warp 2 runs the mixer, warp 3 the
         // next token's softmax statistics (warp 1 swaps the N-gram fixups meanwhile)
-        if (wid == 0 && lane == 0) {
-          unsigned long long s1 = 0, s2 = 0;
-          Best b2{-1.f, 0x7fffffff, 0};
-          float p_t = 0.f, pt_t = 0.f;
-          uint32_t fq = 0;
-          for (int r = 0; r < CS; ++r) {
-            const Xch &x = xin[par][r];
-            s1 += x.sum; s2 += x.cum;
-            best_merge(b2, x.bv, x.bi, x.bc);
-            if (x.has_tok) { p_t = x.p_t; pt_t = x.pt_t; fq = x.freq_t; }
-          }
+        if (wid == 0) {
+          // the CS slots across the warp's lanes: exact integer sums (order-free; a CTA's
+          // count sum is <= T < 2^31), the order-free argmax, and the one slot holding the token
+          const bool in = lane < CS;
+          const Xch &x = xin[par][in ? lane : 0];
+          const unsigned long long s1 = __reduce_add_sync(0xffffffffu, in ? (uint32_t)x.sum : 0u);
+          const unsigned long long s2 = __reduce_add_sync(0xffffffffu, in ? (uint32_t)x.cum : 0u);
+          const Best b2 = best_warp(in ? Best{x.bv, x.bi, x.bc} : Best{-1.f, 0x7fffffff, 0u});
+          const unsigned tb = __ballot_sync(0xffffffffu, in && x.has_tok);
+          const int src = tb ? __ffs(tb) - 1 : 0;
+          const float p_t = tb ? __shfl_sync(0xffffffffu, x.p_t, src) : 0.f;
+          const float pt_t = tb ? __shfl_sync(0xffffffffu, x.pt_t, src) : 0.f;
+          const uint32_t fq = tb ? __shfl_sync(0xffffffffu, x.freq_t, src) : 0u;
+          if (lane == 0) {
           const long long R = (long long)T - (long long)s1;
           if ((long long)b2.c + R < 1) st->err = 1;     // D6
           if (dump && (uint32_t)b2.i / Vc == rank)       // the argmax's final count (its owner CTA)
@@ -1272,6 +1276,7 @@ __global__ __launch_bounds__(WT_, 1) void walk_cl_kernel(WalkArgs a) {
             if (a.out_pt) a.out_pt[oi] = pt_t;
           }
           if (use_ng && ltok >= 0 && ltok < (int)Vc) cu_s[ltok] = __fadd_rn(cu_s[ltok], 1.f);
+          }
         } else if (wid == 2 && lane == 0) {
           if (mix) {
             float pt_t = 0.f, png_t = 0.f;
