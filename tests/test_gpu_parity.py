@@ -913,3 +913,29 @@ def test_ans_coder_detects_wrong_coder_and_corruption(nc, m2):
     with pytest.raises(nc.NcError):   # a trailing byte after the last word
         nc.nc_decompress(m2, blob[:17] + struct.pack("<I", struct.unpack_from("<I", blob, 17)[0] + 1) + blob[21:] + b"\0",
                          ans)
+
+
+def test_ans_coder_with_other_paths(nc, m2):
+    """NC_CODER_ANS (D39) composes with every other entry point: NC06 files, the refresh
+    window variant (the re-prefill decode), the skip flag, and nc_compress_tokens (device ids)
+    == nc_compress (host bytes); every container round-trips and is no more than 12 bytes
+    per chunk larger than the WNC container of the same input."""
+    from synth import make_text
+    ans = nc._lib.CODER_ANS
+    data = make_text("mixed", 12000, 91)
+    for over in ({}, {"window_variant": 1}, {"flags": 7}):
+        p_ans = nc.nc_params_default(window=256, slide=128, n_chunks=2, coder=ans, **over)
+        p_wnc = nc.nc_params_default(window=256, slide=128, n_chunks=2, **over)
+        b_ans = nc.nc_compress_file(m2, data, p_ans)
+        assert nc.nc_decompress_file(m2, b_ans, p_ans) == data, over
+        assert len(b_ans) <= len(nc.nc_compress_file(m2, data, p_wnc)) + 12 * 4, over
+    text = make_text("alice", 9000, 92)
+    prm = nc.nc_params_default(window=256, slide=128, n_chunks=3, coder=ans)
+    blob = nc.nc_compress(m2, text, prm)
+    cuts = nc.nc_host_split(text, 3)
+    toks = [nc.nc_tokenize(m2, text[cuts[c]:cuts[c + 1]], 1)[0] for c in range(len(cuts) - 1)]
+    td = torch.from_numpy(np.concatenate(toks).view(np.int32).copy()).cuda()
+    s = torch.cuda.current_stream()
+    blob2 = nc.nc_compress_tokens(m2, td.data_ptr(), np.array([len(t) for t in toks], np.uint32), prm, s.cuda_stream)
+    torch.cuda.synchronize()
+    assert blob2 == blob and nc.nc_decompress(m2, blob, prm) == text
