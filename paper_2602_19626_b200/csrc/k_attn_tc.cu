@@ -377,17 +377,20 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
       for (int d = 0; d < 32; ++d) O[d] = 0.f;
       float m = -CUDART_INF_F, l = 0.f, alpha_prev = 1.f;
       auto fold = [&](float al) {                  // O <- O * alpha + O_partial  (fp32 RN promotion)
-        uint32_t x0[32], x1[32];
+#pragma unroll
+        for (int hd = 0; hd < 2; ++hd) {           // 16 dims at a time: 32 live registers, not 64
+          uint32_t x0[16], x1[16];
 #if NC_ATT_ABL == 2
-        for (int d = 0; d < 32; ++d) { x0[d] = __float_as_uint(al); x1[d] = 0u; }
+          for (int d = 0; d < 16; ++d) { x0[d] = __float_as_uint(al); x1[d] = 0u; }
 #else
-        tc::tmem_ld32(tmem + T_O + 32 * x + lane_off, x0);
-        tc::tmem_ld32(tmem + T_O + 64 + 32 * x + lane_off, x1);
-        tc::tmem_wait_ld();
+          tc::tmem_ld16(tmem + T_O + 32 * x + 16 * hd + lane_off, x0);
+          tc::tmem_ld16(tmem + T_O + 64 + 32 * x + 16 * hd + lane_off, x1);
+          tc::tmem_wait_ld();
 #endif
 #pragma unroll
-        for (int d = 0; d < 32; ++d)
-          O[d] = __fmaf_rn(O[d], al, __fadd_rn(__uint_as_float(x0[d]), __uint_as_float(x1[d])));
+          for (int d = 0; d < 16; ++d)
+            O[16 * hd + d] = __fmaf_rn(O[16 * hd + d], al, __fadd_rn(__uint_as_float(x0[d]), __uint_as_float(x1[d])));
+        }
       };
       // a warp whose 32 rows are all past the tile's rows (decode tiles hold 1-3 rows; ragged
       // tails) skips its TMEM loads, exponentials, P stores and folds -- the MMAs compute its
