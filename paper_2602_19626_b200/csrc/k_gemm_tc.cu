@@ -168,11 +168,11 @@ __device__ __forceinline__ void store_rows32(float *stg, const float *v, float *
       hin[i] = p0 ? *reinterpret_cast<const float4 *>(p0 + 4 * c4) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
   }
-  float sq[MODE == ST_RESID ? 8 : 1];
+  float mine = 0.f;   // ST_RESID: row `lane`'s slice sum (row 4 i + j sits in lanes 8 j .. 8 j + 7 at step i)
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const int r = 4 * i + (lane >> 3);
-    if (MODE == ST_RESID) sq[i] = 0.f;
+    float sq = 0.f;
     float *p0 = reinterpret_cast<float *>(__shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(d0), r));
     float *p1 = MODE != ST_PLAIN
                     ? reinterpret_cast<float *>(__shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(d1), r))
@@ -189,7 +189,7 @@ __device__ __forceinline__ void store_rows32(float *stg, const float *v, float *
           y.x = __fadd_rn(hin[i].x, y.x); y.y = __fadd_rn(hin[i].y, y.y);
           y.z = __fadd_rn(hin[i].z, y.z); y.w = __fadd_rn(hin[i].w, y.w);
           *reinterpret_cast<float4 *>(p0 + 4 * c4) = y;
-          sq[i] = __fmaf_rn(y.w, y.w, __fmaf_rn(y.z, y.z, __fmaf_rn(y.y, y.y, __fmul_rn(y.x, y.x))));
+          sq = __fmaf_rn(y.w, y.w, __fmaf_rn(y.z, y.z, __fmaf_rn(y.y, y.y, __fmul_rn(y.x, y.x))));
         }
         float4 hi, lo;
         tc::split_tf32(y.x, hi.x, lo.x); tc::split_tf32(y.y, hi.y, lo.y);
@@ -199,20 +199,16 @@ __device__ __forceinline__ void store_rows32(float *stg, const float *v, float *
         *reinterpret_cast<float4 *>(pl + 4 * c4) = lo;
       }
     }
-  }
-  if (MODE == ST_RESID && ssq) {
-    float mine = 0.f;   // row `lane`'s sum: row 4 i + j sits in lanes 8 j .. 8 j + 7 at step i
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      float t = sq[i];
+    if (MODE == ST_RESID && ssq) {   // the row's 8 lanes reduce (all lanes shuffle)
+      float t = sq;
       t = __fadd_rn(t, __shfl_xor_sync(0xffffffffu, t, 1));
       t = __fadd_rn(t, __shfl_xor_sync(0xffffffffu, t, 2));
       t = __fadd_rn(t, __shfl_xor_sync(0xffffffffu, t, 4));
       const float u = __shfl_sync(0xffffffffu, t, 8 * (lane & 3));
       if ((lane >> 2) == i) mine = u;
     }
-    ssq[lane] = mine;
   }
+  if (MODE == ST_RESID && ssq) ssq[lane] = mine;
   __syncwarp();
 }
 
