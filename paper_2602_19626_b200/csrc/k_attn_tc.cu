@@ -475,22 +475,24 @@ __global__ __launch_bounds__(ATT_THREADS, 1) void attn_tc_kernel(const __grid_co
         if (!idle) {
           const uint32_t ph_t = tmem + T_P + 128 * x + lane_off;
 #pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
-            uint32_t hi[32], lo[32];
+          for (int hh = 0; hh < 2; ++hh)
 #pragma unroll
-            for (int k = 0; k < 32; ++k) {
-              float fh, fl;
-              tc::split_tf32(xs[hh][k], fh, fl);
-              hi[k] = __float_as_uint(fh);
-              lo[k] = __float_as_uint(fl);
-            }
+            for (int qq = 0; qq < 2; ++qq) {   // 16 columns at a time: 32 live plane registers
+              uint32_t hi[16], lo[16];
+#pragma unroll
+              for (int k = 0; k < 16; ++k) {
+                float fh, fl;
+                tc::split_tf32(xs[hh][16 * qq + k], fh, fl);
+                hi[k] = __float_as_uint(fh);
+                lo[k] = __float_as_uint(fl);
+              }
 #if NC_ATT_ABL == 4
-            if (hi[0] == 0x7fffffffu && lo[1] == 0x7fffffffu) tc::tmem_st32(ph_t + 32 * hh, hi);
+              if (hi[0] == 0x7fffffffu && lo[1] == 0x7fffffffu) tc::tmem_st16(ph_t + 32 * hh + 16 * qq, hi);
 #else
-            tc::tmem_st32(ph_t + 32 * hh, hi);
-            tc::tmem_st32(ph_t + 64 + 32 * hh, lo);
+              tc::tmem_st16(ph_t + 32 * hh + 16 * qq, hi);
+              tc::tmem_st16(ph_t + 64 + 32 * hh + 16 * qq, lo);
 #endif
-          }
+            }
           if (i >= 1) fold(alpha_prev);
           tc::tmem_wait_st();
         }
